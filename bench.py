@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""HPCCG CG benchmark on B200 (BASELINE.json metric: CG GFLOP/s and iters/s,
+fraction of the HBM roofline, beside the reference CPU path).
+
+A step is one CG iteration (K1 spmv_pAp + K2 update_xr + K3 update_p) on the
+configuration the metric is quoted on: a 256^3 grid per GPU, weak scaling
+over z-slabs (global 256 x 256 x 256N), b = xorshift seed 7
+(acceptance.cpp:48-58), x0 = 0.  The working set (6.9 GB per iteration) is
+far larger than L2, so no flush is needed between iterations.
+
+  python bench.py [--gpus N --steps K --warmup W]           # our arm
+  python bench.py --impl reference ...                      # reference CPU arm
+  torchrun --nproc-per-node N bench.py --gpus N ...         # N GPUs, one rank each
+
+Prints ONE JSON line (rank 0).  Algorithmic work per iteration:
+FLOPs = 2 nnz + 10 n; bytes = 12 nnz + 88 n; K1 alone: 12 nnz + 16 n.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nx", type=int, default=256)
+    ap.add_argument("--ny", type=int, default=256)
+    ap.add_argument("--nz", type=int, default=256, help="planes per GPU (weak scaling)")
+    ap.add_argument("--strong", action="store_true", help="nz is the GLOBAL plane count")
+    ap.add_argument("--variant", choices=["mono", "tasks"], default="mono")
+    ap.add_argument("--tiles", type=int, default=4)
+    ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--e2e-runs", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-nz", type=int, default=64)
+    ap.add_argument("--cpu-sample-iters", type=int, default=10)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return PEAKS_FALLBACK["hbm_gbs"], "fallback"
+
+
+def work(nx, ny, zb, ze, nz):
+    """(n, nnz) owned by the slab [zb, ze) of an nx*ny*nz grid."""
+    sx = 1 if nx == 1 else 3 * nx - 2
+    sy = 1 if ny == 1 else 3 * ny - 2
+    zspan = sum(1 + (z > 0) + (z + 1 < nz) for z in range(zb, ze))
+    return nx * ny * (ze - zb), sx * sy * zspan
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+        return dist, rank, world, local
+    return None, 0, 1, 0
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def load_traffic():
+    """ncu dram bytes per K1 launch from the committed profile summary, if any."""
+    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ CPU baseline
+
+def cpu_reference_sample(nx, ny, nz_sample, iters, threads):
+    """The reference's own task-based CPU path (oracle/_ref: cg_tasks on the
+    threaded substrate with real_seconds_per_unit = 0, tiles = 8 x threads)
+    on a bounded z-slab sample of the workload.  Returns GFLOP/s etc."""
+    from oracle import Oracle, Reference
+    R = Reference()
+    o = Oracle()
+    M = R.stencil(nx, ny, nz_sample)
+    b = o.rhs_xorshift(M.n, 7)
+    tiles = min(8 * threads, M.n)
+    R.cg_tasks(M, b, 1, tiles=tiles, workers=threads, real_threads=True)  # warm
+    _, _, secs = R.cg_tasks(M, b, iters, tiles=tiles, workers=threads, real_threads=True)
+    flops = (2 * M.nnz + 10 * M.n) * iters
+    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads,
+            "kind": "reference", "iters_per_s": iters / secs,
+            "sample": f"reference cg_tasks (oracle/_ref, real threads, tiles={tiles}) on a "
+                      f"{nx}x{ny}x{nz_sample} slab of the workload, {iters} CG iterations, "
+                      f"{secs:.2f} s wall"}
+
+
+def run_reference_arm(args, dist, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    from oracle import Oracle, Reference
+    R = Reference()
+    o = Oracle()
+    nzs = args.cpu_sample_nz
+    M = R.stencil(args.nx, args.ny, nzs)
+    b = o.rhs_xorshift(M.n, 7)
+    tiles = min(8 * threads, M.n)
+    if args.warmup > 0:
+        R.cg_tasks(M, b, args.warmup, tiles=tiles, workers=threads, real_threads=True)
+    _, _, secs = R.cg_tasks(M, b, args.steps, tiles=tiles, workers=threads, real_threads=True)
+    flops = (2 * M.nnz + 10 * M.n) * args.steps
+    v = flops / secs / 1e9
+    line = {
+        "impl": "reference", "metric": "CG GFLOP/s (HPCCG 27-pt stencil, fp64)", "value": v,
+        "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (xorshift64 seed 7 rhs)",
+        "iters_per_s": args.steps / secs,
+        "config": {"workload": f"HPCCG {args.nx}x{args.ny}x{args.nz} per GPU weak scaling; "
+                               f"reference step = one CG iteration on a {args.nx}x{args.ny}x{nzs} "
+                               f"slab sample", "variant": "cg_tasks (reference, CPU threads)"},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": f"cg_tasks real threads tiles={tiles} on {args.nx}x{args.ny}x{nzs}, "
+                                   f"{args.steps} iterations after {args.warmup} warm-up"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, dist, rank, world, local):
+    import torch
+
+    import paper_2602_21897_b200 as P
+
+    nx, ny = args.nx, args.ny
+    if args.strong:
+        nz = args.nz
+        zb, ze = nz * rank // world, nz * (rank + 1) // world
+    else:
+        nz = args.nz * world
+        zb, ze = args.nz * rank, args.nz * (rank + 1)
+    rt = P.Runtime(local)
+    if world > 1:
+        obj = [P.Runtime.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rt.init_comm(rank, world, obj[0])
+    A = P.gen_stencil_matrix(nx, ny, nz, rt=rt, z_begin=zb, z_end=ze)
+    n, nnz = A.n, A.nnz()
+    assert (n, nnz) == work(nx, ny, zb, ze, nz)
+    flops_it = 2 * nnz + 10 * n
+    bytes_it = 12 * nnz + 88 * n
+    k1_bytes = 12 * nnz + 16 * n
+    b = P.rhs_xorshift(rt, n, 7, first=A.info.row_offset)
+    variant = 0 if args.variant == "mono" else 1
+    K, W = args.steps, args.warmup
+    use_graph = args.graph
+    opt = P.CgOptions(tiles=args.tiles, use_graph=use_graph, iteration_marks=False)
+    S = P.CgSolver(rt, A, W + K, opt, variant=variant)
+    kern_timing = variant == 0 and not use_graph
+    stream = torch.cuda.ExternalStream(rt.compute_stream, device=torch.device("cuda", local))
+
+    def timed_run():
+        S.set_rhs(b)
+        S.iterate(W)
+        S.wait()
+        if kern_timing:
+            S.enable_kernel_timing(True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier(dist)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            S.iterate(K)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier(dist)
+        ms = e0.elapsed_time(e1)
+        kt = S.kernel_times() if kern_timing else None
+        if kern_timing:
+            S.enable_kernel_timing(False)
+        return ms, clk.summary(), kt
+
+    ms, clocks, kt = timed_run()
+    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    if set(clocks["reasons"]) & bad:
+        ms, clocks, kt = timed_run()  # rejected: re-measure once
+    hist = S.history(W + K)
+    assert np.all(np.isfinite(hist)) and np.all(hist[1:] <= hist[:-1] * (1 + 1e-12))
+    ms_max = max_over_ranks(dist, ms)
+    total_flops = sum_over_ranks(dist, float(flops_it))
+    total_bytes = sum_over_ranks(dist, float(bytes_it))
+    gflops = total_flops * K / (ms_max / 1e3) / 1e9
+    its = K / (ms_max / 1e3)
+    peak, peak_kind = peaks()
+    kernels_it, colls_it = S.launches_per_iteration()
+
+    roofline = None
+    if kt is not None:
+        k1_ms, k2_ms, k3_ms, nt = kt
+        k1_avg = k1_ms / nt
+        ach = k1_bytes / (k1_avg / 1e3) / 1e9
+        tr = load_traffic()
+        traffic = None
+        if tr and tr.get("workload") == f"{nx}x{ny}x{args.nz}" and world == 1:
+            traffic = tr.get("dram_bytes_per_launch")
+        roofline = {"bound": "hbm", "kernel": "spmv_kernel<true> (K1: SpMV + p.Ap)",
+                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "traffic": traffic, "algorithmic_bytes": k1_bytes,
+                    "avg_launch_ms": k1_avg, "peak_source": f"{peak_kind} hbm_gbs",
+                    "share_of_step": k1_ms / ms,
+                    "k2_update_xr_gbs": 48 * n / (k2_ms / nt / 1e3) / 1e9,
+                    "k3_update_p_gbs": 24 * n / (k3_ms / nt / 1e3) / 1e9}
+    iter_gbs = total_bytes / (ms_max / 1e3 / K) / 1e9
+    roofline_iter = {"bound": "hbm", "achieved": iter_gbs, "peak": peak * world, "unit": "GB/s",
+                     "frac": iter_gbs / (peak * world), "algorithmic_bytes_per_iter": total_bytes}
+
+    # ---- e2e: through the public API with host buffers (pinned b in, history + x out)
+    b_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    bh = b_host.numpy()
+    torch.cuda.synchronize()
+    import ctypes
+    from paper_2602_21897_b200 import _native as N
+    N.check(N.load().tw_memcpy(rt.h, ctypes.c_void_p(b_host.data_ptr()), ctypes.c_void_p(b.ptr),
+                               8 * n, None))
+    rt.synchronize()
+    x_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_times = []
+    for _ in range(max(args.e2e_runs, 1)):
+        barrier(dist)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        S.set_rhs(bh)                       # H2D of b (pinned)
+        S.iterate(K)
+        h = S.history(K)                    # D2H of the residual history
+        N.check(N.load().tw_cg_solution(S.h, ctypes.cast(x_host.data_ptr(),
+                                                             ctypes.POINTER(ctypes.c_double))))
+        t1 = time.perf_counter()
+        barrier(dist)
+        e2e_times.append(max_over_ranks(dist, t1 - t0))
+        assert np.all(np.isfinite(h))
+    e2e_t = min(e2e_times)
+    e2e = {"value": total_flops * K / e2e_t / 1e9, "unit": "GFLOP/s",
+           "h2d_bytes_per_step": 8 * n / K, "d2h_bytes_per_step": (8 * n + 8 * K) / K,
+           "iters_per_s": K / e2e_t,
+           "api": "CgSolver.set_rhs(host b) + iterate(K) + history + solution (C ABI tw_cg_*)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(nx, ny, min(args.cpu_sample_nz, nz),
+                                       args.cpu_sample_iters, os.cpu_count() or 1)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {type(ex).__name__}: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": "CG GFLOP/s (HPCCG 27-pt stencil, fp64)", "value": gflops, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K,
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: gen_stencil_matrix on device, b = xorshift64 seed 7, x0 = 0",
+            "iters_per_s": its,
+            "config": {"workload": (f"HPCCG {nx}x{ny}x{args.nz} " +
+                                    ("global strong scaling" if args.strong else
+                                     "per GPU weak scaling (z-slab)")),
+                       "global_grid": [nx, ny, nz], "variant": args.variant,
+                       "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
+                       "rows_per_gpu": n, "nnz_per_gpu": nnz,
+                       "l2": "inputs larger than L2 (6.9 GB/iteration vs 126 MB)",
+                       "parallelism": f"z-slab x{world}"},
+            "roofline": roofline, "roofline_iteration": roofline_iter,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,
+            "residual_last": float(hist[-1]),
+        }
+        print(json.dumps(line), flush=True)
+    S.close()
+
+
+def main():
+    args = parse()
+    dist, rank, world, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference_arm(args, dist, rank, world)
+        else:
+            run_ours(args, dist, rank, world, local)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * tw_hpccg.h -- C ABI of the B200-native HPCCG hot path (libtw_hpccg.so).
+ *
+ * Drop-in boundary for the reference's CG path (taskweave, arXiv 2602.21897
+ * artifact).  Every entry point names the reference interface it replaces
+ * (file:line under /root/reference/proj).  Plain pointers and sizes only; no
+ * C++ or torch types cross this boundary and no exception escapes it.
+ *
+ * Errors follow the reference's two exception classes
+ * (include/taskweave/types.hpp:23-33): TW_ERR_CONFIG for malformed input
+ * (ConfigError, CLI exit 1), TW_ERR_CONTRACT for API misuse
+ * (ContractViolation, CLI exit 2), plus TW_ERR_CUDA / TW_ERR_NCCL for device
+ * and communicator failures.  tw_last_error_string() returns the message of
+ * the last failing call on the calling thread.
+ *
+ * Pointers documented "device" are CUDA device pointers on the context's
+ * device; "host" pointers are ordinary (preferably pinned) host memory.
+ * `stream` arguments are cudaStream_t passed as void* (NULL = the context's
+ * compute stream).
+ */
+#ifndef TW_HPCCG_H
+#define TW_HPCCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TW_OK 0
+#define TW_ERR_CONFIG 1
+#define TW_ERR_CONTRACT 2
+#define TW_ERR_CUDA 3
+#define TW_ERR_NCCL 4
+
+#define TW_ABI_VERSION 1
+
+typedef struct tw_ctx tw_ctx; /* replaces tw::Runtime + sim::Device (runtime.hpp:25-55, sim_device.hpp:91-166) */
+typedef struct tw_ell tw_ell; /* replaces tw::bench::CsrMatrix on the device (csr.hpp:9-17) */
+typedef struct tw_cg tw_cg;   /* replaces the CgRun solve state (cg.cpp:24-48) */
+
+const char* tw_last_error_string(void);
+int tw_abi_version(void);
+
+/* ---------------------------------------------------------------- context */
+
+/* Runtime(RuntimeConfig) + Device(...) (runtime.cpp:5-34, sim_device.cpp:77-85):
+ * binds `device`, creates the compute stream and a pool of
+ * `stream_pool_capacity` streams (QueuePool capacity, task_aware.hpp:83-109;
+ * CgOptions::stream_pool_capacity default 4, cg.hpp:42). */
+int tw_ctx_create(int device, unsigned stream_pool_capacity, tw_ctx** out);
+int tw_ctx_destroy(tw_ctx* ctx);
+int tw_ctx_compute_stream(tw_ctx* ctx, void** stream_out);
+int tw_ctx_synchronize(tw_ctx* ctx);
+/* Number of SMs and device ordinal, for launch sizing reports. */
+int tw_ctx_device_info(tw_ctx* ctx, int* device, int* sm_count);
+
+/* Multi-GPU (no reference equivalent: SPEC.md:291 lists multiple devices as a
+ * non-goal).  One rank per GPU; the 128-byte id comes from
+ * rank 0's tw_comm_unique_id and is broadcast by the caller.  NCCL is loaded
+ * at run time (libnccl.so.2). */
+int tw_comm_unique_id(unsigned char id_out[128]);
+int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[128]);
+int tw_ctx_comm_info(tw_ctx* ctx, int* rank, int* nranks);
+
+/* Device buffers for callers without another allocator (tests, bench). */
+int tw_malloc(tw_ctx* ctx, void** ptr, int64_t bytes);
+int tw_free(tw_ctx* ctx, void* ptr);
+int tw_malloc_host(void** ptr, int64_t bytes); /* pinned */
+int tw_free_host(void* ptr);
+int tw_memcpy(tw_ctx* ctx, void* dst, const void* src, int64_t bytes, void* stream); /* any direction, async */
+
+/* ----------------------------------------------------------- matrix (K0) */
+
+typedef struct tw_ell_info_t {
+    int64_t nx, ny, nz;      /* 0 for matrices not generated as a stencil   */
+    int64_t z_begin, z_end;  /* owned z-planes of the slab                  */
+    int64_t n_global;        /* rows of the global operator                 */
+    int64_t n_rows;          /* owned rows (local)                          */
+    int64_t row_offset;      /* global row of local row 0                   */
+    int64_t col_offset;      /* global column of local column 0             */
+    int64_t x_len;           /* local length of a gathered vector (owned + ghost planes) */
+    int64_t nnz;             /* true nonzeros of the owned rows             */
+    int64_t n_slices;        /* 32-row slices                               */
+    int64_t ell_entries;     /* stored entries incl. padding                */
+    int32_t max_width;       /* widest slice                                */
+    int32_t slice_rows;      /* 32                                          */
+} tw_ell_info_t;
+
+/* gen_stencil_matrix(nx,ny,nz) (csr.cpp:29-59), generated on the device into
+ * sliced ELL, for the z-slab [z_begin, z_end) (pass 0, nz for the whole grid).
+ * Per-row entry order, columns and values are the reference's exactly.
+ * TW_ERR_CONFIG on dims < 1 or overflow (csr.cpp:30-34). */
+int tw_gen_stencil_ell(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t z_begin,
+                       int64_t z_end, tw_ell** out);
+/* CsrMatrix -> device ELL (load_csr interop, csr.cpp:76-98).  Host arrays;
+ * validated like CsrMatrix::validate (csr.cpp:13-27). */
+int tw_ell_from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values, tw_ell** out);
+int tw_ell_info(const tw_ell* A, tw_ell_info_t* out);
+/* Device ELL -> host CSR with GLOBAL column indices (row_ptr int64[n_rows+1],
+ * col_idx int64[nnz], values double[nnz]); the structure parity check. */
+int tw_ell_to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values);
+int tw_ell_destroy(tw_ell* A);
+
+/* ------------------------------------------------------- kernels (K1-K4) */
+
+/* spmv_range(A, x, y, r0, r1) (kernels.cpp:5-13): y[i] for local rows
+ * [r0, r1); x is a device vector of length x_len (owned + ghost planes),
+ * y of length n_rows.  Bit-identical to the reference (per-row order kept,
+ * no FMA, padding masked). */
+int tw_spmv_range(const tw_ell* A, const double* x, double* y, int64_t r0, int64_t r1,
+                  void* stream);
+/* spmv_range + dot_range(p, Ap, r0, r1) fused (K1): *dot_dev (device double)
+ * receives sum_{i in [r0,r1)} p[i]*Ap[i] (fixed-order tree reduction). */
+int tw_spmv_dot(const tw_ell* A, const double* p, double* Ap, int64_t r0, int64_t r1,
+                double* dot_dev, void* stream);
+/* dot_range(a, b, i0, i1) (kernels.cpp:15-20) into *out_dev (device double). */
+int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int64_t i1,
+                 double* out_dev, void* stream);
+/* waxpby_range(alpha, x, beta, y, w, i0, i1) (kernels.cpp:22-26): three
+ * roundings per element, w may alias x or y; bit-identical. */
+int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, const double* y,
+                    double* w, int64_t i0, int64_t i1, void* stream);
+
+/* make_tile_plan(A, tiles) (cg.cpp:348-370) over the owned rows; band in
+ * GLOBAL columns like the reference.  TW_ERR_CONFIG if tiles < 1 or > rows. */
+int tw_make_tile_plan(const tw_ell* A, int tiles, int64_t* r0, int64_t* r1, int64_t* band_lo,
+                      int64_t* band_hi);
+
+/* Right-hand sides generated on the device, element offset `first` of the
+ * global sequence: xorshift64 (acceptance.cpp:48-58 / test_bench.cpp:26-36)
+ * and SplitMix64 (scenario.cpp:46-55). */
+int tw_rhs_xorshift(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double* out_dev,
+                    void* stream);
+int tw_rhs_splitmix(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double* out_dev,
+                    void* stream);
+
+/* ------------------------------------------------------------------- CG */
+
+#define TW_CG_MONOLITHIC 0 /* cg_monolithic (cg.cpp:397-436)                    */
+#define TW_CG_TASKS 1      /* cg_tasks block-task DAG (cg.cpp:166-334, 438-447)  */
+
+typedef struct tw_cg_options {
+    int variant;                   /* TW_CG_MONOLITHIC | TW_CG_TASKS                  */
+    int tiles;                     /* CgOptions::tiles (cg.hpp:38); forced 1 for monolithic */
+    unsigned stream_pool_capacity; /* CgOptions::stream_pool_capacity (cg.hpp:42)    */
+    int use_graph;                 /* capture one iteration as a CUDA graph            */
+    int iteration_marks;           /* CgOptions::iteration_marks: host poller stamps cg_iter=i */
+    double tol;                    /* CgOptions::tol: converged = last residual < tol  */
+} tw_cg_options;
+
+/* Fills the defaults of CgOptions (cg.hpp:37-45) with the cuda backend. */
+void tw_cg_options_default(tw_cg_options* opt);
+
+/* setup_state (cg.cpp:75-128): allocates x|r|p|Ap and the scalar block on the
+ * device for up to `max_iterations` history entries. */
+int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max_iterations,
+                 tw_cg** out);
+int tw_cg_destroy(tw_cg* cg);
+/* x = 0, r = p = b, rtrans = dot(r, r) (cg.cpp:124-127); b has n_rows entries
+ * (this rank's rows), on the host or the device. */
+int tw_cg_set_rhs(tw_cg* cg, const double* b, int b_is_device);
+/* Enqueues `iterations` CG iterations (asynchronous; scalars stay on the
+ * device, no host round trip). */
+int tw_cg_iterate(tw_cg* cg, int iterations);
+/* Waits for everything enqueued (host poll of the completion events,
+ * TaskAware::wait_transformed semantics, task_aware.cpp:50-60). */
+int tw_cg_wait(tw_cg* cg);
+int tw_cg_iterations_done(tw_cg* cg, int* done);
+/* residual_history (cg.hpp:13): sqrt(r.r) after each iteration run so far. */
+int tw_cg_history(tw_cg* cg, double* host_out, int count);
+/* x of this rank's rows, to host. */
+int tw_cg_solution(tw_cg* cg, double* host_x);
+/* Device pointers of the state vectors (x, r, p incl. ghosts, Ap). */
+int tw_cg_vectors(tw_cg* cg, double** x, double** r, double** p, double** Ap);
+/* Host wall time (seconds since tw_cg_set_rhs) at which the poller saw each
+ * iteration complete (the cg_iter=i marks, cg.cpp:307-308); 0 if unseen. */
+int tw_cg_iteration_marks(tw_cg* cg, double* host_out, int count);
+/* Logical block-task DAG of the tasks variant for the iterations enqueued so
+ * far: edges as "pred succ\n" label pairs (labels "spmv:i:t", "dot_pAp:i:t",
+ * "alpha:i:0", ... as in cg.cpp:168-170).  Returns needed size in *needed. */
+int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed);
+/* Per-kernel device timing of the monolithic variant (graph capture off):
+ * when enabled, each iteration brackets K1 (spmv_pAp), K2 (update_xr) and
+ * K3 (update_p) with CUDA timing events on the stream they launch on.
+ * tw_cg_kernel_times returns the summed milliseconds per kernel and the
+ * number of timed iterations since the last enable; it synchronises. */
+int tw_cg_enable_kernel_timing(tw_cg* cg, int enable);
+int tw_cg_kernel_times(tw_cg* cg, double* k1_ms, double* k2_ms, double* k3_ms, int* iterations);
+/* Physical launches per iteration (kernels + NCCL calls), for reports. */
+int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
+
+/* cg_monolithic / cg_tasks in one call (cg.cpp:397-447): host b in, host
+ * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17). */
+int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iterations,
+                const tw_cg_options* opt, double* history_out, double* x_out, int* converged);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TW_HPCCG_H */

@@ -1,0 +1,20 @@
+"""B200-native HPCCG conjugate-gradient hot path (arXiv 2602.21897 artifact).
+
+Hand-written sm_100a CUDA kernels and a C++ host runtime in
+``_lib/libtw_hpccg.so`` behind the C ABI ``include/tw_hpccg.h``; this package
+is the Python face that mirrors the reference's operator API
+(``hpccg.py``).  There is no CPU fallback.
+"""
+from . import _native
+from .hpccg import (CgBackend, CgOptions, CgResult, CgSolver, ConfigError, ContractViolation,
+                    CudaError, EllMatrix, NcclError, Runtime, Tile, cg_monolithic, cg_tasks,
+                    default_runtime, dot_range, ell_from_csr, gen_stencil_matrix,
+                    make_tile_plan, rhs_splitmix, rhs_xorshift, spmv_dot, spmv_range,
+                    waxpby_range)
+
+__all__ = [
+    "CgBackend", "CgOptions", "CgResult", "CgSolver", "ConfigError", "ContractViolation",
+    "CudaError", "EllMatrix", "NcclError", "Runtime", "Tile", "cg_monolithic", "cg_tasks",
+    "default_runtime", "dot_range", "ell_from_csr", "gen_stencil_matrix", "make_tile_plan",
+    "rhs_splitmix", "rhs_xorshift", "spmv_dot", "spmv_range", "waxpby_range", "_native",
+]

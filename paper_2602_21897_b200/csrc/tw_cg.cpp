@@ -1,0 +1,883 @@
+// CG drivers of libtw_hpccg: cg_monolithic and the cg_tasks block-task DAG
+// (cg.cpp:166-447) re-expressed as CUDA streams, events and graphs, with all
+// scalars resident on the device and, across GPUs, a z-slab decomposition
+// with NCCL halo exchange and rank-ordered scalar reductions.
+//
+// Per iteration the device work is three HBM-bound kernels:
+//   K1 spmv_pAp   Ap = A p, p.Ap            (spmv:i:t + dot_pAp:i:t)
+//   K2 update_xr  x += a p, r -= a Ap, r.r  (x_up:i:t + r_up:i:t + dot_rr:i:t)
+//   K3 update_p   p = r + b p               (p_up:i:t)
+// with alpha:i / beta_res:i folded into the last block of K1 / K2 (one tile,
+// one rank) or run as one-warp combine kernels over the tile / rank partials.
+//
+// The tasks variant keeps the reference's data-flow semantics: a region
+// ledger infers the per-iteration logical DAG from the same byte-interval
+// accesses spawn_iteration declares (cg.cpp:173-333); fused physical nodes
+// inherit the union of their members' edges and become cudaStreamWaitEvent
+// edges between pooled streams (or edges of a captured CUDA graph).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <optional>
+#include <set>
+#include <sstream>
+
+#include "tw_objects.h"
+
+namespace tw {
+
+// --------------------------------------------------------------- ledger
+//
+// Byte-interval dependency inference with the reference's rules
+// (region_ledger.hpp:11-27): a read conflicts with the last writer; a write
+// or readwrite conflicts with the last writer and every reader since.
+
+enum AccMode { ACC_R = 0, ACC_W = 1, ACC_RW = 2 };
+struct Acc {
+    uint64_t lo, hi; // [lo, hi)
+    int mode;
+};
+
+class Ledger {
+public:
+    void conflicts(const Acc& a, std::vector<int>& out) const {
+        auto it = seg_.upper_bound(a.lo);
+        if (it != seg_.begin()) --it;
+        for (; it != seg_.end() && it->first < a.hi; ++it) {
+            const Seg& s = it->second;
+            if (s.hi <= a.lo) continue;
+            if (s.writer >= 0) out.push_back(s.writer);
+            if (a.mode != ACC_R) out.insert(out.end(), s.readers.begin(), s.readers.end());
+        }
+    }
+    void record(const Acc& a, int task) {
+        split(a.lo);
+        split(a.hi);
+        if (a.mode != ACC_R) {
+            seg_.erase(seg_.lower_bound(a.lo), seg_.lower_bound(a.hi));
+            seg_[a.lo] = Seg{a.hi, task, {}};
+            return;
+        }
+        uint64_t pos = a.lo;
+        auto it = seg_.lower_bound(a.lo);
+        while (pos < a.hi) {
+            if (it == seg_.end() || it->first >= a.hi) {
+                seg_[pos] = Seg{a.hi, -1, {task}};
+                break;
+            }
+            if (it->first > pos) {
+                seg_[pos] = Seg{it->first, -1, {task}};
+                pos = it->first;
+                continue;
+            }
+            auto& rd = it->second.readers;
+            if (std::find(rd.begin(), rd.end(), task) == rd.end()) rd.push_back(task);
+            pos = it->second.hi;
+            ++it;
+        }
+    }
+
+private:
+    struct Seg {
+        uint64_t hi;
+        int writer;
+        std::vector<int> readers;
+    };
+    void split(uint64_t x) {
+        auto it = seg_.upper_bound(x);
+        if (it == seg_.begin()) return;
+        --it;
+        if (it->first == x || it->second.hi <= x) return;
+        Seg right = it->second;
+        it->second.hi = x;
+        seg_[x] = std::move(right);
+    }
+    std::map<uint64_t, Seg> seg_;
+};
+
+enum PhysKind { PK_HALO, PK_SPMV, PK_ALPHA, PK_UPD, PK_BETA, PK_UPDP };
+
+struct LTask {
+    std::string label;
+    std::vector<Acc> acc;
+    int phys; // physical node index within the iteration
+};
+
+struct PNode {
+    PhysKind kind;
+    int tile;
+    std::vector<int> preds_first; // iteration right after a fork point
+    std::vector<int> preds_intra; // same-iteration predecessors (steady state)
+    std::vector<int> preds_cross; // previous-iteration predecessors
+};
+
+} // namespace tw
+
+using namespace tw;
+
+struct tw_cg {
+    tw_ctx* ctx = nullptr;
+    const tw_ell* A = nullptr;
+    tw_cg_options opt{};
+    int max_iters = 0;
+    int T = 1;
+    int P = 1;
+    int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
+    bool glo = false, ghi = false;
+
+    double* x = nullptr;
+    double* r = nullptr;
+    double* p_base = nullptr;
+    double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
+    double* p_owned = nullptr;
+    double* Ap = nullptr;
+    CgScalars* sc = nullptr;
+    double* history = nullptr;
+    double* parts = nullptr;
+    double* block_parts = nullptr;
+    unsigned* tickets = nullptr;
+    int maxg = 0;
+
+    // partial slots (offsets into parts)
+    double *pa = nullptr, *rrp = nullptr, *pm = nullptr, *send_a = nullptr, *send_b = nullptr,
+           *recv_a = nullptr, *recv_b = nullptr, *send_r = nullptr, *recv_r = nullptr;
+
+    std::vector<int64_t> t_r0, t_r1, t_lo, t_hi; // tile plan (local rows / local columns)
+    std::vector<LTask> ltasks;                   // one iteration's logical tasks (template)
+    std::vector<PNode> nodes;                    // one iteration's physical nodes
+    std::vector<cudaEvent_t> ev[2];              // per node, by iteration parity
+    std::vector<cudaEvent_t> tail_ev;            // per pool stream + comm
+    cudaEvent_t fork_ev = nullptr, halo_ev = nullptr, pready_ev = nullptr;
+
+    cudaGraphExec_t graph = nullptr;
+    int enqueued = 0;
+    // per-kernel timing (monolithic, no graph): 4 events per timed iteration
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;
+    int timed = 0;
+    double t0 = 0.0;
+    std::vector<double> marks;
+    std::unique_ptr<TaskAware> ta;
+
+    RedScratch slot(int i) const {
+        return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
+    }
+    EllView view() const { return A->view(); }
+    cudaStream_t node_stream(const PNode& nd) const {
+        if (nd.kind == PK_HALO) return ctx->comm;
+        const unsigned C = ctx->pool.capacity();
+        if (nd.kind == PK_ALPHA || nd.kind == PK_BETA) return ctx->pool.stream(0);
+        return ctx->pool.stream(static_cast<int>(static_cast<unsigned>(nd.tile) % C));
+    }
+};
+
+namespace tw {
+namespace {
+
+// Synthetic byte addresses for the ledger: one 2^40-byte window per array,
+// element i of array k at (k << 40) + 8 i.  Only overlap matters for edges.
+enum Arr : uint64_t { A_X = 1, A_R, A_P, A_AP, A_PA, A_RR, A_RTRANS, A_ALPHA, A_BETA };
+Acc reg(Arr a, int64_t i0, int64_t i1, int mode) {
+    return Acc{(static_cast<uint64_t>(a) << 40) + 8u * static_cast<uint64_t>(i0),
+               (static_cast<uint64_t>(a) << 40) + 8u * static_cast<uint64_t>(i1), mode};
+}
+
+// spawn_iteration (cg.cpp:166-334): same tasks, labels and access regions;
+// plus, across GPUs, a halo task that refreshes p's ghost planes.  p is
+// addressed in local x coordinates (ghost planes included).
+void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNode>* nodes) {
+    const int T = cg->T;
+    const int64_t ds = cg->diag_shift;
+    auto tag = [iter](const char* fam, int t) {
+        return std::string(fam) + ":" + std::to_string(iter) + ":" + std::to_string(t);
+    };
+    out.clear();
+    const bool halo = cg->P > 1;
+    const int off_spmv = halo ? 1 : 0, off_alpha = off_spmv + T, off_upd = off_alpha + 1,
+              off_beta = off_upd + T, off_updp = off_beta + 1;
+    if (nodes) {
+        nodes->clear();
+        if (halo) nodes->push_back(PNode{PK_HALO, 0, {}, {}, {}});
+        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_SPMV, t, {}, {}, {}});
+        nodes->push_back(PNode{PK_ALPHA, 0, {}, {}, {}});
+        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_UPD, t, {}, {}, {}});
+        nodes->push_back(PNode{PK_BETA, 0, {}, {}, {}});
+        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_UPDP, t, {}, {}, {}});
+    }
+    if (halo) {
+        std::vector<Acc> acc;
+        const int64_t n = cg->n, pl = cg->plane;
+        if (cg->glo) {
+            acc.push_back(reg(A_P, ds, ds + pl, ACC_R));
+            acc.push_back(reg(A_P, 0, pl, ACC_W));
+        }
+        if (cg->ghi) {
+            acc.push_back(reg(A_P, ds + n - pl, ds + n, ACC_R));
+            acc.push_back(reg(A_P, ds + n, ds + n + pl, ACC_W));
+        }
+        out.push_back(LTask{tag("halo", 0), acc, 0});
+    }
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("spmv", t),
+                            {reg(A_P, cg->t_lo[t], cg->t_hi[t] + 1, ACC_R),
+                             reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_W)},
+                            off_spmv + t});
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("dot_pAp", t),
+                            {reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_R),
+                             reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_R), reg(A_PA, t, t + 1, ACC_W)},
+                            off_spmv + t});
+    out.push_back(LTask{tag("alpha", 0),
+                        {reg(A_PA, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_R),
+                         reg(A_ALPHA, 0, 1, ACC_W)},
+                        off_alpha});
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("x_up", t),
+                            {reg(A_ALPHA, 0, 1, ACC_R),
+                             reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_R),
+                             reg(A_X, cg->t_r0[t], cg->t_r1[t], ACC_RW)},
+                            off_upd + t});
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("r_up", t),
+                            {reg(A_ALPHA, 0, 1, ACC_R), reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_R),
+                             reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_RW)},
+                            off_upd + t});
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("dot_rr", t),
+                            {reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_R), reg(A_RR, t, t + 1, ACC_W)},
+                            off_upd + t});
+    out.push_back(LTask{tag("beta_res", 0),
+                        {reg(A_RR, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_RW),
+                         reg(A_BETA, 0, 1, ACC_W)},
+                        off_beta});
+    for (int t = 0; t < T; ++t)
+        out.push_back(LTask{tag("p_up", t),
+                            {reg(A_BETA, 0, 1, ACC_R), reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_R),
+                             reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_RW)},
+                            off_updp + t});
+}
+
+// Runs the ledger over `iters` iterations; returns logical edges (global
+// task ids = iter * tasks_per_iter + k) and, optionally, the label list.
+void logical_edges(tw_cg* cg, int iters, std::vector<std::pair<int, int>>& edges,
+                   std::vector<std::string>* labels, std::vector<int>* phys_of) {
+    Ledger led;
+    std::vector<LTask> it_tasks;
+    int base = 0;
+    for (int it = 0; it < iters; ++it) {
+        build_logical(cg, it, it_tasks, nullptr);
+        for (size_t k = 0; k < it_tasks.size(); ++k) {
+            const int id = base + static_cast<int>(k);
+            std::vector<int> pr;
+            for (const Acc& a : it_tasks[k].acc) led.conflicts(a, pr);
+            std::sort(pr.begin(), pr.end());
+            pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+            for (int p : pr)
+                if (p != id) edges.emplace_back(p, id);
+            for (const Acc& a : it_tasks[k].acc) led.record(a, id);
+            if (labels) labels->push_back(it_tasks[k].label);
+            if (phys_of) phys_of->push_back(it_tasks[k].phys);
+        }
+        base += static_cast<int>(it_tasks.size());
+    }
+    std::sort(edges.begin(), edges.end());
+}
+
+// Physical predecessor lists from the logical DAG of iterations 0 and 1.
+void build_schedule(tw_cg* cg) {
+    build_logical(cg, 0, cg->ltasks, &cg->nodes);
+    const int L = static_cast<int>(cg->ltasks.size());
+    std::vector<std::pair<int, int>> edges;
+    std::vector<int> phys;
+    logical_edges(cg, 2, edges, nullptr, &phys);
+    std::vector<std::set<int>> first(cg->nodes.size()), intra(cg->nodes.size()),
+        cross(cg->nodes.size());
+    for (auto [a, b] : edges) {
+        const int pa = phys[static_cast<size_t>(a)], pb = phys[static_cast<size_t>(b)];
+        const int ia = a / L, ib = b / L;
+        if (ib == 0) {
+            if (pa != pb) first[static_cast<size_t>(pb)].insert(pa);
+        } else if (ia == 1) {
+            if (pa != pb) intra[static_cast<size_t>(pb)].insert(pa);
+        } else {
+            cross[static_cast<size_t>(pb)].insert(pa);
+        }
+    }
+    for (size_t j = 0; j < cg->nodes.size(); ++j) {
+        cg->nodes[j].preds_first.assign(first[j].begin(), first[j].end());
+        cg->nodes[j].preds_intra.assign(intra[j].begin(), intra[j].end());
+        cg->nodes[j].preds_cross.assign(cross[j].begin(), cross[j].end());
+        for (int p : cg->nodes[j].preds_first)
+            if (p >= static_cast<int>(j)) contract_error("physical task order is not topological");
+    }
+}
+
+int launch_blocks(const tw_cg* cg, bool spmv) {
+    return spmv ? cg->ctx->cfg.spmv_blocks : cg->ctx->cfg.stream_blocks;
+}
+
+void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s) {
+    TW_NCCL(nccl().AllGather(send, recv, 1, ncclDouble, cg->ctx->nccl_comm, s));
+}
+
+void halo_exchange(tw_cg* cg, cudaStream_t s) {
+    const auto& api = nccl();
+    const size_t pl = static_cast<size_t>(cg->plane);
+    const int rank = cg->ctx->rank;
+    TW_NCCL(api.GroupStart());
+    if (cg->glo) {
+        TW_NCCL(api.Recv(cg->p_owned - pl, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
+        TW_NCCL(api.Send(cg->p_owned, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
+    }
+    if (cg->ghi) {
+        TW_NCCL(api.Recv(cg->p_owned + cg->n, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
+        TW_NCCL(api.Send(cg->p_owned + cg->n - pl, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
+    }
+    TW_NCCL(api.GroupEnd());
+}
+
+// One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
+// stream; across ranks the SpMV is split so the interior rows overlap the
+// halo exchange on the comm stream.
+// Timing event k (0..3) of the current timed iteration, or null.
+cudaEvent_t tmark(tw_cg* cg, int k) {
+    if (!cg->timing) return nullptr;
+    const size_t i = static_cast<size_t>(cg->timed) * 4 + static_cast<size_t>(k);
+    while (cg->tev.size() <= i) {
+        cudaEvent_t e;
+        TW_CUDA(cudaEventCreate(&e));
+        cg->tev.push_back(e);
+    }
+    return cg->tev[i];
+}
+
+void record(cudaEvent_t e, cudaStream_t s) {
+    if (e) TW_CUDA(cudaEventRecord(e, s));
+}
+
+void enqueue_mono(tw_cg* cg) {
+    cudaStream_t s = cg->ctx->compute;
+    const EllView A = cg->view();
+    const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
+    const RedScratch rs = cg->slot(0);
+    if (cg->P == 1) {
+        record(tmark(cg, 0), s);
+        launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs,
+                    Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, bs, s);
+        record(tmark(cg, 1), s);
+        launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
+                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s);
+        record(tmark(cg, 2), s);
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                        cg->history, bv, s);
+        record(tmark(cg, 3), s);
+        if (cg->timing) ++cg->timed;
+        return;
+    }
+    cudaStream_t c = cg->ctx->comm;
+    const int64_t lo = cg->glo ? cg->plane : 0;
+    int64_t hi = cg->ghi ? cg->n - cg->plane : cg->n;
+    if (hi < lo) hi = lo;
+    TW_CUDA(cudaEventRecord(cg->pready_ev, s));
+    TW_CUDA(cudaStreamWaitEvent(c, cg->pready_ev, 0));
+    halo_exchange(cg, c);
+    TW_CUDA(cudaEventRecord(cg->halo_ev, c));
+    record(tmark(cg, 0), s);
+    launch_spmv(A, cg->p_local, cg->Ap, RowRange{lo, hi}, RowRange{0, 0}, true, rs,
+                Fin{FIN_STORE, cg->pm, nullptr, nullptr}, bs, s);
+    TW_CUDA(cudaStreamWaitEvent(s, cg->halo_ev, 0));
+    launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, lo}, RowRange{hi, cg->n}, true, rs,
+                Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, bs, s);
+    launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
+    allgather1(cg, cg->send_a, cg->recv_a, s);
+    record(tmark(cg, 1), s);
+    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+                     ScalarSrc{cg->recv_a, cg->P}, rs, Fin{FIN_STORE, cg->send_b, nullptr, nullptr},
+                     bv, s);
+    allgather1(cg, cg->send_b, cg->recv_b, s);
+    record(tmark(cg, 2), s);
+    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, rs,
+                    cg->history, bv, s);
+    record(tmark(cg, 3), s);
+    if (cg->timing) ++cg->timed;
+}
+
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
+    const EllView A = cg->view();
+    const int t = nd.tile;
+    const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
+    switch (nd.kind) {
+    case PK_HALO:
+        halo_exchange(cg, st);
+        break;
+    case PK_SPMV:
+        launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0}, true,
+                    cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
+        break;
+    case PK_ALPHA:
+        if (cg->P == 1) {
+            launch_combine(cg->pa, cg->T, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
+        } else {
+            launch_combine(cg->pa, cg->T, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, st);
+            allgather1(cg, cg->send_a, cg->recv_a, st);
+            launch_combine(cg->recv_a, cg->P, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
+        }
+        break;
+    case PK_UPD:
+        launch_update_xr(cg->t_r0[t], cg->t_r1[t], cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+                         ScalarSrc{nullptr, 0}, cg->slot(t),
+                         Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}, bv, st);
+        break;
+    case PK_BETA:
+        if (cg->P == 1) {
+            launch_combine(cg->rrp, cg->T, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
+        } else {
+            launch_combine(cg->rrp, cg->T, Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, st);
+            allgather1(cg, cg->send_b, cg->recv_b, st);
+            launch_combine(cg->recv_b, cg->P, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
+        }
+        break;
+    case PK_UPDP:
+        launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0},
+                        cg->slot(t), cg->history, bv, st);
+        break;
+    }
+}
+
+// All pooled streams (and the comm stream) start after everything already
+// on the compute stream.
+void fork_streams(tw_cg* cg) {
+    TW_CUDA(cudaEventRecord(cg->fork_ev, cg->ctx->compute));
+    for (unsigned i = 0; i < cg->ctx->pool.capacity(); ++i)
+        TW_CUDA(cudaStreamWaitEvent(cg->ctx->pool.stream(static_cast<int>(i)), cg->fork_ev, 0));
+    TW_CUDA(cudaStreamWaitEvent(cg->ctx->comm, cg->fork_ev, 0));
+}
+
+void join_streams(tw_cg* cg) {
+    const unsigned C = cg->ctx->pool.capacity();
+    for (unsigned i = 0; i <= C; ++i) {
+        cudaStream_t st = i < C ? cg->ctx->pool.stream(static_cast<int>(i)) : cg->ctx->comm;
+        TW_CUDA(cudaEventRecord(cg->tail_ev[i], st));
+        TW_CUDA(cudaStreamWaitEvent(cg->ctx->compute, cg->tail_ev[i], 0));
+    }
+}
+
+// One block-task iteration: physical nodes in topological order, each on its
+// stream after waiting for predecessors on other streams.
+void enqueue_tasks(tw_cg* cg, int parity, bool first) {
+    for (size_t j = 0; j < cg->nodes.size(); ++j) {
+        const PNode& nd = cg->nodes[j];
+        cudaStream_t st = cg->node_stream(nd);
+        for (int p : first ? nd.preds_first : nd.preds_intra)
+            if (cg->node_stream(cg->nodes[static_cast<size_t>(p)]) != st)
+                TW_CUDA(cudaStreamWaitEvent(st, cg->ev[parity][static_cast<size_t>(p)], 0));
+        if (!first)
+            for (int p : nd.preds_cross)
+                if (cg->node_stream(cg->nodes[static_cast<size_t>(p)]) != st)
+                    TW_CUDA(cudaStreamWaitEvent(st, cg->ev[parity ^ 1][static_cast<size_t>(p)], 0));
+        launch_node(cg, nd, st);
+        TW_CUDA(cudaEventRecord(cg->ev[parity][j], st));
+    }
+}
+
+void enqueue_iteration_body(tw_cg* cg, int parity, bool first) {
+    if (cg->opt.variant == TW_CG_MONOLITHIC)
+        enqueue_mono(cg);
+    else
+        enqueue_tasks(cg, parity, first);
+}
+
+void build_graph(tw_cg* cg) {
+    cudaStream_t s = cg->ctx->compute;
+    cudaGraph_t g = nullptr;
+    TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+        if (cg->opt.variant == TW_CG_TASKS) {
+            fork_streams(cg);
+            enqueue_tasks(cg, 0, true);
+            join_streams(cg);
+        } else {
+            enqueue_mono(cg);
+        }
+    } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    TW_CUDA(cudaStreamEndCapture(s, &g));
+    cudaError_t e = cudaGraphInstantiate(&cg->graph, g, 0);
+    cudaGraphDestroy(g);
+    TW_CUDA(e);
+}
+
+void free_cg(tw_cg* cg) {
+    if (!cg) return;
+    cudaSetDevice(cg->ctx->device);
+    cudaDeviceSynchronize();
+    cg->ta.reset();
+    if (cg->graph) cudaGraphExecDestroy(cg->graph);
+    for (auto& v : cg->ev)
+        for (auto e : v) cudaEventDestroy(e);
+    for (auto e : cg->tail_ev) cudaEventDestroy(e);
+    for (auto e : cg->tev) cudaEventDestroy(e);
+    if (cg->fork_ev) cudaEventDestroy(cg->fork_ev);
+    if (cg->halo_ev) cudaEventDestroy(cg->halo_ev);
+    if (cg->pready_ev) cudaEventDestroy(cg->pready_ev);
+    cudaFree(cg->x);
+    cudaFree(cg->r);
+    cudaFree(cg->p_base);
+    cudaFree(cg->Ap);
+    cudaFree(cg->sc);
+    cudaFree(cg->history);
+    cudaFree(cg->parts);
+    cudaFree(cg->block_parts);
+    cudaFree(cg->tickets);
+    delete cg;
+}
+
+tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_iters) {
+    if (!ctx || !A) contract_error("null context or matrix");
+    if (A->ctx != ctx) contract_error("matrix belongs to another context");
+    if (max_iters < 0) config_error("iterations must be non-negative");
+    auto* cg = new tw_cg;
+    try {
+        cg->ctx = ctx;
+        cg->A = A;
+        if (o)
+            cg->opt = *o;
+        else
+            tw_cg_options_default(&cg->opt);
+        if (cg->opt.variant != TW_CG_MONOLITHIC && cg->opt.variant != TW_CG_TASKS)
+            config_error("unknown CG variant");
+        cg->T = cg->opt.variant == TW_CG_MONOLITHIC ? 1 : cg->opt.tiles; // cg.cpp:400
+        cg->P = ctx->nranks;
+        cg->max_iters = max_iters;
+        const tw_ell_info_t& in = A->info;
+        cg->n = in.n_rows;
+        cg->x_len = in.x_len;
+        cg->diag_shift = A->diag_shift;
+        if (cg->P > 1) {
+            if (in.nx == 0) config_error("multi-GPU CG needs a stencil slab (tw_gen_stencil_ell)");
+            cg->plane = in.nx * in.ny;
+            cg->glo = in.z_begin > 0;
+            cg->ghi = in.z_end < in.nz;
+            if (cg->glo != (ctx->rank > 0) || cg->ghi != (ctx->rank < cg->P - 1))
+                contract_error("slab z-range does not match this rank's position");
+            if (!ctx->nccl_comm) contract_error("multi-rank context without communicator");
+        } else if (in.z_begin > 0 || (in.nx && in.z_end < in.nz)) {
+            contract_error("a partial slab needs a multi-rank context");
+        }
+        tile_plan(A, cg->T, cg->t_r0, cg->t_r1, cg->t_lo, cg->t_hi);
+        TW_CUDA(cudaSetDevice(ctx->device));
+        const size_t n = static_cast<size_t>(cg->n);
+        TW_CUDA(cudaMalloc(&cg->x, sizeof(double) * (n + 2)));
+        TW_CUDA(cudaMalloc(&cg->r, sizeof(double) * (n + 2)));
+        TW_CUDA(cudaMalloc(&cg->Ap, sizeof(double) * (n + 2)));
+        // p_owned 16-byte aligned for the paired loads of K2/K3
+        const int64_t pad = cg->diag_shift & 1;
+        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + pad) + 2)));
+        cg->p_local = cg->p_base + pad;
+        cg->p_owned = cg->p_local + cg->diag_shift;
+        TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
+        TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
+        const int T = cg->T, P = cg->P;
+        const size_t np = static_cast<size_t>(2 * T + 8 + 3 * P + 8);
+        TW_CUDA(cudaMalloc(&cg->parts, sizeof(double) * np));
+        TW_CUDA(cudaMemset(cg->parts, 0, sizeof(double) * np));
+        cg->pa = cg->parts;
+        cg->rrp = cg->pa + T;
+        cg->pm = cg->rrp + T;
+        cg->send_a = cg->pm + 4;
+        cg->send_b = cg->send_a + 1;
+        cg->send_r = cg->send_b + 1;
+        cg->recv_a = cg->send_r + 1;
+        cg->recv_b = cg->recv_a + P;
+        cg->recv_r = cg->recv_b + P;
+        cg->maxg = std::max(ctx->cfg.spmv_blocks, ctx->cfg.stream_blocks);
+        TW_CUDA(cudaMalloc(&cg->block_parts, sizeof(double) * static_cast<size_t>(cg->maxg) * T));
+        TW_CUDA(cudaMalloc(&cg->tickets, sizeof(unsigned) * 4 * T));
+        TW_CUDA(cudaMemset(cg->tickets, 0, sizeof(unsigned) * 4 * T));
+        TW_CUDA(cudaEventCreateWithFlags(&cg->fork_ev, cudaEventDisableTiming));
+        TW_CUDA(cudaEventCreateWithFlags(&cg->halo_ev, cudaEventDisableTiming));
+        TW_CUDA(cudaEventCreateWithFlags(&cg->pready_ev, cudaEventDisableTiming));
+        for (unsigned i = 0; i <= ctx->pool.capacity(); ++i) {
+            cudaEvent_t e;
+            TW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            cg->tail_ev.push_back(e);
+        }
+        if (cg->opt.variant == TW_CG_TASKS) {
+            build_schedule(cg);
+            for (auto& v : cg->ev)
+                for (size_t j = 0; j < cg->nodes.size(); ++j) {
+                    cudaEvent_t e;
+                    TW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    v.push_back(e);
+                }
+        }
+        cg->marks.assign(static_cast<size_t>(std::max(max_iters, 1)), 0.0);
+        cg->ta = std::make_unique<TaskAware>(ctx->device, 20e-6);
+    } catch (...) {
+        free_cg(cg);
+        throw;
+    }
+    return cg;
+}
+
+void set_rhs(tw_cg* cg, const double* b, bool on_device) {
+    tw_ctx* ctx = cg->ctx;
+    cudaStream_t s = ctx->compute;
+    TW_CUDA(cudaSetDevice(ctx->device));
+    TW_CUDA(cudaStreamSynchronize(s));
+    const size_t bytes = sizeof(double) * static_cast<size_t>(cg->n);
+    CgScalars init{};
+    init.history_cap = cg->max_iters;
+    TW_CUDA(cudaMemcpyAsync(cg->sc, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    TW_CUDA(cudaMemsetAsync(cg->x, 0, bytes, s));
+    TW_CUDA(cudaMemsetAsync(cg->Ap, 0, bytes, s));
+    TW_CUDA(cudaMemsetAsync(cg->p_local, 0, sizeof(double) * static_cast<size_t>(cg->x_len), s));
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, k, s));
+    TW_CUDA(cudaMemcpyAsync(cg->p_owned, cg->r, bytes, cudaMemcpyDeviceToDevice, s));
+    const RedScratch rs = cg->slot(0);
+    if (cg->P == 1) {
+        launch_dot(cg->r, cg->r, 0, cg->n, rs, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr},
+                   ctx->cfg.stream_blocks, s);
+    } else {
+        launch_dot(cg->r, cg->r, 0, cg->n, rs, Fin{FIN_STORE, cg->send_r, nullptr, nullptr},
+                   ctx->cfg.stream_blocks, s);
+        allgather1(cg, cg->send_r, cg->recv_r, s);
+        launch_combine(cg->recv_r, cg->P, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr}, s);
+    }
+    TW_CUDA(cudaStreamSynchronize(s));
+    cg->enqueued = 0;
+    std::fill(cg->marks.begin(), cg->marks.end(), 0.0);
+    cg->t0 = host_seconds();
+}
+
+void iterate(tw_cg* cg, int k) {
+    if (k < 0) config_error("negative iteration count");
+    if (cg->enqueued + k > cg->max_iters)
+        contract_error("iterations beyond max_iterations (" + std::to_string(cg->max_iters) + ")");
+    if (k == 0) return;
+    TW_CUDA(cudaSetDevice(cg->ctx->device));
+    cudaStream_t s = cg->ctx->compute;
+    if (cg->opt.use_graph && !cg->graph) build_graph(cg);
+    const bool tasks = cg->opt.variant == TW_CG_TASKS;
+    if (!cg->opt.use_graph && tasks) fork_streams(cg);
+    for (int i = 0; i < k; ++i) {
+        const int it = cg->enqueued + i;
+        if (cg->opt.use_graph) {
+            TW_CUDA(cudaGraphLaunch(cg->graph, s));
+        } else {
+            enqueue_iteration_body(cg, it & 1, i == 0);
+        }
+        if (cg->opt.iteration_marks) {
+            // cg_iter=i mark (cg.cpp:307-308): the poller stamps the host time
+            // at which it first sees this iteration complete.
+            cudaStream_t ms = s;
+            if (tasks && !cg->opt.use_graph) {
+                for (const PNode& nd : cg->nodes)
+                    if (nd.kind == PK_BETA) ms = cg->node_stream(nd);
+            }
+            cudaEvent_t e = cg->ta->take_event();
+            TW_CUDA(cudaEventRecord(e, ms));
+            cg->ta->bind(e, &cg->marks[static_cast<size_t>(it)], cg->t0);
+        }
+    }
+    if (!cg->opt.use_graph && tasks) join_streams(cg);
+    cg->enqueued += k;
+}
+
+void wait_cg(tw_cg* cg) {
+    TW_CUDA(cudaSetDevice(cg->ctx->device));
+    cudaEvent_t e = cg->ta->take_event();
+    TW_CUDA(cudaEventRecord(e, cg->ctx->compute));
+    cg->ta->wait(e); // wait_transformed: poll + yield, never a blocking device wait
+    cudaEventDestroy(e);
+    TW_CUDA(cudaGetLastError());
+}
+
+} // namespace
+} // namespace tw
+
+extern "C" {
+
+void tw_cg_options_default(tw_cg_options* o) {
+    if (!o) return;
+    o->variant = TW_CG_TASKS;
+    o->tiles = 16;
+    o->stream_pool_capacity = 4;
+    o->use_graph = 0;
+    o->iteration_marks = 1;
+    o->tol = 0.0;
+}
+
+int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max_iterations,
+                 tw_cg** out) {
+    return guarded([&] { *out = create_cg(ctx, A, opt, max_iterations); });
+}
+
+int tw_cg_destroy(tw_cg* cg) {
+    return guarded([&] { free_cg(cg); });
+}
+
+int tw_cg_set_rhs(tw_cg* cg, const double* b, int b_is_device) {
+    return guarded([&] {
+        if (!cg || !b) contract_error("null solver or rhs");
+        set_rhs(cg, b, b_is_device != 0);
+    });
+}
+
+int tw_cg_iterate(tw_cg* cg, int iterations) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        iterate(cg, iterations);
+    });
+}
+
+int tw_cg_wait(tw_cg* cg) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        wait_cg(cg);
+    });
+}
+
+int tw_cg_iterations_done(tw_cg* cg, int* done) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        CgScalars sc;
+        TW_CUDA(cudaMemcpy(&sc, cg->sc, sizeof(sc), cudaMemcpyDeviceToHost));
+        *done = sc.iter;
+    });
+}
+
+int tw_cg_history(tw_cg* cg, double* host_out, int count) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        if (count < 0 || count > cg->max_iters) contract_error("history count out of range");
+        wait_cg(cg);
+        if (count)
+            TW_CUDA(cudaMemcpy(host_out, cg->history, sizeof(double) * count, cudaMemcpyDeviceToHost));
+    });
+}
+
+int tw_cg_solution(tw_cg* cg, double* host_x) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        wait_cg(cg);
+        TW_CUDA(cudaMemcpy(host_x, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
+                           cudaMemcpyDeviceToHost));
+    });
+}
+
+int tw_cg_vectors(tw_cg* cg, double** x, double** r, double** p, double** Ap) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        if (x) *x = cg->x;
+        if (r) *r = cg->r;
+        if (p) *p = cg->p_local;
+        if (Ap) *Ap = cg->Ap;
+    });
+}
+
+int tw_cg_iteration_marks(tw_cg* cg, double* host_out, int count) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        if (count < 0 || count > cg->max_iters) contract_error("mark count out of range");
+        wait_cg(cg);
+        while (cg->ta->pending()) std::this_thread::yield();
+        std::copy(cg->marks.begin(), cg->marks.begin() + count, host_out);
+    });
+}
+
+int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        std::vector<std::pair<int, int>> edges;
+        std::vector<std::string> labels;
+        logical_edges(cg, std::max(cg->enqueued, 1), edges, &labels, nullptr);
+        std::ostringstream os;
+        for (auto [a, b] : edges) os << labels[static_cast<size_t>(a)] << ' ' << labels[static_cast<size_t>(b)] << '\n';
+        const std::string s = os.str();
+        if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
+        if (buf && cap > 0) {
+            const int64_t k = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
+            std::memcpy(buf, s.data(), static_cast<size_t>(k));
+            buf[k] = '\0';
+        }
+    });
+}
+
+int tw_cg_enable_kernel_timing(tw_cg* cg, int enable) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        if (enable && (cg->opt.variant != TW_CG_MONOLITHIC || cg->opt.use_graph))
+            config_error("kernel timing needs the monolithic variant without graph capture");
+        cg->timing = enable != 0;
+        cg->timed = 0;
+    });
+}
+
+int tw_cg_kernel_times(tw_cg* cg, double* k1, double* k2, double* k3, int* iterations) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        wait_cg(cg);
+        double acc[3] = {0, 0, 0};
+        for (int i = 0; i < cg->timed; ++i)
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                TW_CUDA(cudaEventElapsedTime(&ms, cg->tev[static_cast<size_t>(4 * i + k)],
+                                             cg->tev[static_cast<size_t>(4 * i + k + 1)]));
+                acc[k] += ms;
+            }
+        if (k1) *k1 = acc[0];
+        if (k2) *k2 = acc[1];
+        if (k3) *k3 = acc[2];
+        if (iterations) *iterations = cg->timed;
+    });
+}
+
+int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        int k = 0, c = 0;
+        if (cg->opt.variant == TW_CG_MONOLITHIC) {
+            k = cg->P == 1 ? 3 : 5;
+            c = cg->P == 1 ? 0 : 3;
+        } else {
+            k = 3 * cg->T + (cg->P == 1 ? 2 : 4);
+            c = cg->P == 1 ? 0 : 3;
+        }
+        if (kernels) *kernels = k;
+        if (collectives) *collectives = c;
+    });
+}
+
+int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iterations,
+                const tw_cg_options* opt, double* history_out, double* x_out, int* converged) {
+    return guarded([&] {
+        tw_cg* cg = create_cg(ctx, A, opt, iterations);
+        try {
+            set_rhs(cg, b_host, false);
+            iterate(cg, iterations);
+            wait_cg(cg);
+            std::vector<double> h(static_cast<size_t>(std::max(iterations, 1)));
+            if (iterations)
+                TW_CUDA(cudaMemcpy(h.data(), cg->history, sizeof(double) * iterations,
+                                   cudaMemcpyDeviceToHost));
+            if (history_out) std::copy(h.begin(), h.begin() + iterations, history_out);
+            if (x_out)
+                TW_CUDA(cudaMemcpy(x_out, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
+                                   cudaMemcpyDeviceToHost));
+            if (converged) // CgResult::converged (cg.cpp:392-393)
+                *converged = cg->opt.tol > 0 && iterations > 0 && h[iterations - 1] < cg->opt.tol;
+        } catch (...) {
+            free_cg(cg);
+            throw;
+        }
+        free_cg(cg);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,164 @@
+// Internal declarations shared by the libtw_hpccg translation units.
+// Public C ABI: include/tw_hpccg.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tw_hpccg.h"
+
+namespace tw {
+
+// Exceptions mapped 1:1 onto the ABI status codes at the extern "C" boundary
+// (mirrors the reference's ConfigError / ContractViolation, types.hpp:23-33).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void config_error(const std::string& m) { throw Error(TW_ERR_CONFIG, m); }
+[[noreturn]] inline void contract_error(const std::string& m) { throw Error(TW_ERR_CONTRACT, m); }
+void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+#define TW_CUDA(x) ::tw::cuda_check((x), #x, __FILE__, __LINE__)
+
+constexpr int kSliceRows = 32; // one warp per slice: lane = row within slice
+
+// ---------------------------------------------------------------- device views
+
+// Sliced ELL, 32-row slices.  Slice s stores its rows' entries in a block of
+// 32*w entries starting at slice_off[s] (w = slice width = longest row).
+// Inside a block entry k of lane l sits at a chunked position chosen so one
+// 128-bit load gives a lane several consecutive entries of ITS row:
+//   values  (f64): pairs  [k/2][l][2], odd tail k=w-1 at [w-1][l]
+//   columns (i32): quads  [k/4][l][4], then a pair, then a single for w%4
+// Rows keep the reference's entry order (csr.cpp:46-53); padding entries
+// (k >= row length) carry col = -1 and are skipped, never accumulated.
+struct EllView {
+    const int64_t* slice_off; // [n_slices + 1], in entries
+    const double* vals;
+    const int32_t* cols;      // local column = global column - col_offset
+    int64_t n_rows;
+    int64_t n_slices;
+    int64_t diag_shift;       // x index of local row i is i + diag_shift
+};
+
+__host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
+    const int full = w & ~1;
+    if (k < full) return 32LL * (k & ~1) + 2 * lane + (k & 1);
+    return 32LL * (w - 1) + lane;
+}
+__host__ __device__ inline int64_t ell_col_pos(int k, int lane, int w) {
+    const int full = w & ~3;
+    if (k < full) return 32LL * (k & ~3) + 4 * lane + (k & 3);
+    const int rem = w - full;
+    if (rem >= 2 && k < full + 2) return 32LL * full + 2 * lane + (k - full);
+    return 32LL * (w - 1) + lane;
+}
+
+// Scalar state of one solve, resident on the device (never round-trips to
+// the host inside the iteration loop).
+struct CgScalars {
+    double rtrans; // r.r of the current residual
+    double alpha;
+    double beta;
+    double pAp;
+    double rr;
+    int iter;      // iterations completed (index into history)
+    int history_cap;
+};
+
+// Scratch for fixed-order grid reductions: one partial per block plus a
+// wrap-around ticket so the last block to finish combines them.
+struct RedScratch {
+    double* block_part;
+    unsigned* ticket;
+};
+
+enum FinMode : int {
+    FIN_NONE = 0,
+    FIN_STORE = 1, // *out = total
+    FIN_ALPHA = 2, // pAp = total; alpha = rtrans / pAp
+    FIN_BETA = 3,  // rr = total; beta = rr / rtrans; rtrans = rr; history[iter++] = sqrt(rr)
+    FIN_RTRANS = 4 // rtrans = total; iter = 0 (setup_state, cg.cpp:126)
+};
+
+struct Fin {
+    int mode;
+    double* out;
+    CgScalars* sc;
+    double* history;
+};
+
+// Where an update kernel takes its scalar from: sc->alpha / sc->beta when
+// count == 0, else recomputed per block from `count` partials summed in
+// order (the cross-rank allgather result).
+struct ScalarSrc {
+    const double* parts;
+    int count;
+};
+
+// ---------------------------------------------------------------- launchers
+
+struct LaunchCfg {
+    int spmv_blocks;   // grid for the SpMV family (SMs x resident blocks)
+    int stream_blocks; // grid for streaming vector kernels
+    int threads;       // 256
+};
+
+struct RowRange {
+    int64_t r0, r1;
+};
+
+// K1: y = A x over up to two local row ranges; optional fused dot(x_diag, y).
+void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s);
+// K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.
+void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
+                      const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
+                      Fin fin, int blocks, cudaStream_t s);
+// K3: p = r + beta p (beta from sc or recomputed from partials; with
+// partials, the last block also commits rtrans/history/iter).
+void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
+                     ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
+                     cudaStream_t s);
+// K4: dot(a, b) over [i0, i1) with finalize.
+void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
+                int blocks, cudaStream_t s);
+void launch_waxpby(double alpha, const double* x, double beta, const double* y, double* w,
+                   int64_t i0, int64_t i1, int blocks, cudaStream_t s);
+// Sum `count` partials in order, then finalize (1 warp).
+void launch_combine(const double* parts, int count, Fin fin, cudaStream_t s);
+void launch_fill(double* p, int64_t n, double v, int blocks, cudaStream_t s);
+void launch_rhs_splitmix(uint64_t seed, int64_t first, int64_t count, double* out, int blocks,
+                         cudaStream_t s);
+void launch_rhs_xorshift(const uint64_t* chunk_states, int64_t chunk, int64_t count,
+                         int64_t skip, double* out, int blocks, cudaStream_t s);
+
+// K0 pieces
+void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                           int64_t n_rows, int64_t n_slices, int64_t* widths_out, int blocks,
+                           cudaStream_t s);
+void launch_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                         int64_t col_offset, int64_t n_rows, int64_t n_slices,
+                         const int64_t* slice_off, double* vals, int32_t* cols, int blocks,
+                         cudaStream_t s);
+void launch_csr_fill(const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                     int64_t n_rows, int64_t n_slices, const int64_t* slice_off, double* vals,
+                     int32_t* cols, int blocks, cudaStream_t s);
+void launch_csr_widths(const int64_t* row_ptr, int64_t n_rows, int64_t n_slices,
+                       int64_t* widths_out, int blocks, cudaStream_t s);
+// In-place exclusive scan of int64 (n + 1 entries written: out[0] = 0).
+void scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp,
+                        cudaStream_t s);
+int64_t scan_tmp_elems(int64_t n);
+void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* minmax,
+                 int blocks, cudaStream_t s);
+
+// Occupancy-derived launch configuration for this device.
+LaunchCfg query_launch_cfg(int sm_count);
+
+} // namespace tw

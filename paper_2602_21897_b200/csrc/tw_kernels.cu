@@ -1,0 +1,730 @@
+// sm_100a kernels of the HPCCG hot path.
+//
+//   K0  stencil generation into sliced ELL          (gen_stencil_matrix, csr.cpp:29-59)
+//   K1  SpMV fused with p.Ap                        (spmv_range + dot_range, kernels.cpp:5-20)
+//   K2  x += a p ; r -= a Ap ; r.r                  (2x waxpby_range + dot_range, kernels.cpp:15-26)
+//   K3  p = r + b p                                 (waxpby_range, kernels.cpp:22-26)
+//   K4  dot / waxpby standalone, scalar combines
+//
+// Everything here is HBM-bound f64 streaming (0.16 flop/byte, far below the
+// FP64 ridge), so the design levers are: 128-bit coalesced loads of the
+// matrix with evict-first (__ldcs) so the gathered vector stays in L1/L2,
+// grids sized to SMs x resident blocks with warps of a block walking
+// neighbouring slices (shared x-lines hit L1), and fused reductions that
+// finish in the last block (no extra launch, no host round trip).
+//
+// Arithmetic parity: this file is compiled with --fmad=false and uses
+// __dmul_rn/__dadd_rn explicitly, so every product and sum rounds exactly as
+// the reference's x86-64 build (no FMA).  Dot products are
+// fixed-order trees: deterministic run to run, within reassociation error of
+// the reference's sequential sums (SURVEY.md 8(c) tolerance rule).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tw_internal.h"
+
+namespace tw {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide fixed-order sum; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) smem[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int w = 0; w < nw; ++w) t = __dadd_rn(t, smem[w]);
+    }
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ void finalize(const Fin& fin, double total) {
+    switch (fin.mode) {
+    case FIN_STORE:
+        *fin.out = total;
+        break;
+    case FIN_ALPHA:
+        fin.sc->pAp = total;
+        fin.sc->alpha = __ddiv_rn(fin.sc->rtrans, total);
+        break;
+    case FIN_BETA: {
+        CgScalars* sc = fin.sc;
+        sc->rr = total;
+        sc->beta = __ddiv_rn(total, sc->rtrans);
+        sc->rtrans = total;
+        if (sc->iter < sc->history_cap) fin.history[sc->iter] = __dsqrt_rn(total);
+        sc->iter = sc->iter + 1;
+        break;
+    }
+    case FIN_RTRANS:
+        fin.sc->rtrans = total;
+        fin.sc->iter = 0;
+        break;
+    default:
+        break;
+    }
+}
+
+// Grid-wide fixed-order reduction finished by the last block to arrive.
+__device__ void grid_reduce_finalize(double v, RedScratch rs, const Fin& fin) {
+    __shared__ double smem[32];
+    __shared__ bool last;
+    double b = block_sum(v, smem);
+    if (threadIdx.x == 0) {
+        rs.block_part[blockIdx.x] = b;
+        __threadfence();
+        unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+        acc = __dadd_rn(acc, __ldcg(rs.block_part + i));
+    double total = block_sum(acc, smem);
+    if (threadIdx.x == 0) finalize(fin, total);
+}
+
+__device__ __forceinline__ double sum_parts(const double* parts, int count) {
+    double t = 0.0;
+    for (int i = 0; i < count; ++i) t = __dadd_rn(t, __ldcg(parts + i));
+    return t;
+}
+
+// ------------------------------------------------------------------ K1 SpMV
+
+// One row of a width-W slice: all matrix loads issued up front as 128-bit
+// evict-first loads, then the gathers, then the reference's left-to-right
+// sum (acc from 0.0, multiply then add).
+template <int W>
+__device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
+                                                  const int32_t* __restrict__ cb,
+                                                  const double* __restrict__ x, int lane) {
+    double v[W];
+    int c[W];
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        double2 t = __ldcs(reinterpret_cast<const double2*>(vb + 64 * j) + lane);
+        v[2 * j] = t.x;
+        v[2 * j + 1] = t.y;
+    }
+    if (W & 1) v[W - 1] = __ldcs(vb + 32 * (W - 1) + lane);
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+        int4 t = __ldcs(reinterpret_cast<const int4*>(cb + 128 * q) + lane);
+        c[4 * q] = t.x;
+        c[4 * q + 1] = t.y;
+        c[4 * q + 2] = t.z;
+        c[4 * q + 3] = t.w;
+    }
+    constexpr int F = W & ~3;
+    if (W - F >= 2) {
+        int2 t = __ldcs(reinterpret_cast<const int2*>(cb + 32 * F) + lane);
+        c[F] = t.x;
+        c[F + 1] = t.y;
+    }
+    if ((W - F) & 1) c[W - 1] = __ldcs(cb + 32 * (W - 1) + lane);
+    double xv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) xv[k] = c[k] >= 0 ? __ldg(x + c[k]) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+        if (c[k] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[k], xv[k]));
+    return acc;
+}
+
+__device__ __forceinline__ double slice_row_generic(const double* __restrict__ vb,
+                                                    const int32_t* __restrict__ cb,
+                                                    const double* __restrict__ x, int lane,
+                                                    int w) {
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+        int c = __ldcs(cb + ell_col_pos(k, lane, w));
+        if (c < 0) break; // padding only ever trails a row
+        double v = __ldcs(vb + ell_val_pos(k, lane, w));
+        acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
+    }
+    return acc;
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
+            RowRange rb, RedScratch rs, Fin fin) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    // The slices covering range a, then those covering range b, as one index space.
+    const int64_t sa0 = ra.r0 >> 5, sa1 = ra.r1 > ra.r0 ? (ra.r1 + 31) >> 5 : sa0;
+    const int64_t sb0 = rb.r0 >> 5, sb1 = rb.r1 > rb.r0 ? (rb.r1 + 31) >> 5 : sb0;
+    const int64_t na = sa1 - sa0, ntot = na + (sb1 - sb0);
+    double part = 0.0;
+    for (int64_t i = warp_g; i < ntot; i += nwarps) {
+        const bool in_a = i < na;
+        const int64_t s = in_a ? sa0 + i : sb0 + (i - na);
+        const int64_t off = __ldg(A.slice_off + s);
+        const int w = static_cast<int>((__ldg(A.slice_off + s + 1) - off) >> 5);
+        const double* vb = A.vals + off;
+        const int32_t* cb = A.cols + off;
+        double acc;
+        switch (w) {
+        case 27: acc = slice_row_fixed<27>(vb, cb, x, lane); break;
+        case 18: acc = slice_row_fixed<18>(vb, cb, x, lane); break;
+        case 12: acc = slice_row_fixed<12>(vb, cb, x, lane); break;
+        case 8: acc = slice_row_fixed<8>(vb, cb, x, lane); break;
+        default: acc = slice_row_generic(vb, cb, x, lane, w); break;
+        }
+        const int64_t row = (s << 5) + lane;
+        const RowRange r = in_a ? ra : rb;
+        if (row >= r.r0 && row < r.r1) {
+            y[row] = acc;
+            if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
+        }
+    }
+    if (DOT) grid_reduce_finalize(part, rs, fin);
+}
+
+// --------------------------------------------------------- K2 / K3 / K4 streams
+
+// Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
+// 128-bit accesses, the (at most two) ragged ends go scalar.
+template <typename F>
+__device__ __forceinline__ void for_pairs(int64_t i0, int64_t i1, F&& f) {
+    const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t j = j0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < j1;
+         j += stride) {
+        const int64_t e = 2 * j;
+        f(e, e >= i0, e + 1 < i1);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
+                 double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
+                 ScalarSrc asrc, RedScratch rs, Fin fin) {
+    double alpha;
+    if (asrc.count > 0)
+        alpha = __ddiv_rn(sc->rtrans, sum_parts(asrc.parts, asrc.count));
+    else
+        alpha = sc->alpha;
+    const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
+    double part = 0.0;
+    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
+        if (lo && hi) {
+            double2 xv = __ldcs(reinterpret_cast<const double2*>(x + e));
+            double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
+            double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
+            double2 av = __ldcs(reinterpret_cast<const double2*>(Ap + e));
+            xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+            xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+            rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+            rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+            __stcs(reinterpret_cast<double2*>(x + e), xv);
+            __stcs(reinterpret_cast<double2*>(r + e), rv);
+            part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+            part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+        } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (!(h == 0 ? lo : hi)) continue;
+                const int64_t i = e + h;
+                x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+                double rv = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
+                r[i] = rv;
+                part = __dadd_rn(part, __dmul_rn(rv, rv));
+            }
+        }
+    });
+    grid_reduce_finalize(part, rs, fin);
+}
+
+__global__ void __launch_bounds__(kThreads)
+update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
+                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history) {
+    double beta, rr = 0.0;
+    if (bsrc.count > 0) {
+        rr = sum_parts(bsrc.parts, bsrc.count);
+        beta = __ddiv_rn(rr, sc->rtrans);
+    } else {
+        beta = sc->beta;
+    }
+    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
+        if (lo && hi) {
+            double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
+            double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
+            pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+            pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+            *reinterpret_cast<double2*>(p + e) = pv;
+        } else {
+            if (lo) p[e] = __dadd_rn(r[e], __dmul_rn(beta, p[e]));
+            if (hi) p[e + 1] = __dadd_rn(r[e + 1], __dmul_rn(beta, p[e + 1]));
+        }
+    });
+    if (bsrc.count > 0) {
+        // Every block read rtrans above; the last one through commits the
+        // iteration (beta_res task, cg.cpp:290-311).
+        __shared__ bool last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
+            last = (t == gridDim.x - 1);
+        }
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence();
+            sc->rr = rr;
+            sc->beta = beta;
+            sc->rtrans = rr;
+            if (sc->iter < sc->history_cap) history[sc->iter] = __dsqrt_rn(rr);
+            sc->iter = sc->iter + 1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+dot_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t i0, int64_t i1,
+           RedScratch rs, Fin fin) {
+    double part = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < i1;
+         i += stride)
+        part = __dadd_rn(part, __dmul_rn(__ldg(a + i), __ldg(b + i)));
+    grid_reduce_finalize(part, rs, fin);
+}
+
+__global__ void __launch_bounds__(kThreads)
+waxpby_kernel(double alpha, const double* x, double beta, const double* y, double* w, int64_t i0,
+              int64_t i1) {
+    // x, y, w may alias (kernels.cpp:22-26): each element is read before it
+    // is written by the same thread, so aliasing is safe.
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = i0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < i1;
+         i += stride)
+        w[i] = __dadd_rn(__dmul_rn(alpha, x[i]), __dmul_rn(beta, y[i]));
+}
+
+__global__ void combine_kernel(const double* parts, int count, Fin fin) {
+    if (threadIdx.x == 0) finalize(fin, sum_parts(parts, count));
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += stride)
+        p[i] = v;
+}
+
+// SplitMix64 (scenario.cpp:46-55) is counter based: element i uses state
+// seed + (i+1)*gamma.
+__global__ void rhs_splitmix_kernel(uint64_t seed, int64_t first, int64_t count, double* out) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += stride) {
+        uint64_t z = seed + static_cast<uint64_t>(first + i + 1) * 0x9e3779b97f4a7c15ull;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        out[i] = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+    }
+}
+
+// xorshift64 (acceptance.cpp:48-58) is sequential; the host jumps the state
+// to every chunk start (GF(2) matrix powers) and each thread walks a chunk.
+__global__ void rhs_xorshift_kernel(const uint64_t* states, int64_t chunk, int64_t count,
+                                    int64_t skip, double* out) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t begin = c * chunk - skip; // output index of this chunk's first value
+    if (begin >= count) return;
+    uint64_t s = states[c];
+    for (int64_t j = 0; j < chunk; ++j) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        const int64_t i = begin + j;
+        if (i >= count) break;
+        if (i >= 0) out[i] = 0.5 + static_cast<double>(s % 1000u) / 1000.0;
+    }
+}
+
+// --------------------------------------------------------------- K0 generator
+
+__device__ __forceinline__ int64_t axis_span(int64_t c, int64_t d) {
+    return 1 + (c > 0) + (c + 1 < d);
+}
+
+// Width of each 32-row slice = longest stencil row in it (closed form).
+__global__ void stencil_widths_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                                      int64_t n_rows, int64_t n_slices, int64_t* widths) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t plane = nx * ny;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t row = s * 32 + lane;
+        int len = 0;
+        if (row < n_rows) {
+            const int64_t g = row + row_offset;
+            const int64_t z = g / plane, rem = g - z * plane, y = rem / nx, x = rem - y * nx;
+            len = static_cast<int>(axis_span(x, nx) * axis_span(y, ny) * axis_span(z, nz));
+        }
+        const int w = __reduce_max_sync(0xffffffffu, len);
+        if (lane == 0) widths[s] = 32LL * w;
+    }
+}
+
+// One warp per slice, lane = row: walk the row's neighbours in the
+// reference's (dz, dy, dx) order (csr.cpp:46-54) and drop them into the
+// chunked slice layout; pad to the slice width with col = -1.
+__global__ void stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                                    int64_t col_offset, int64_t n_rows, int64_t n_slices,
+                                    const int64_t* __restrict__ slice_off, double* vals,
+                                    int32_t* cols) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t plane = nx * ny;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t off = slice_off[s];
+        const int w = static_cast<int>((slice_off[s + 1] - off) >> 5);
+        double* vb = vals + off;
+        int32_t* cb = cols + off;
+        const int64_t row = s * 32 + lane;
+        int k = 0;
+        if (row < n_rows) {
+            const int64_t g = row + row_offset;
+            const int64_t z = g / plane, rem = g - z * plane, y = rem / nx, x = rem - y * nx;
+            for (int64_t cz = z - 1; cz <= z + 1; ++cz) {
+                if (cz < 0 || cz >= nz) continue;
+                for (int64_t cy = y - 1; cy <= y + 1; ++cy) {
+                    if (cy < 0 || cy >= ny) continue;
+                    const int64_t line = (cz * ny + cy) * nx;
+                    for (int64_t cx = x - 1; cx <= x + 1; ++cx) {
+                        if (cx < 0 || cx >= nx) continue;
+                        const bool diag = cx == x && cy == y && cz == z;
+                        vb[ell_val_pos(k, lane, w)] = diag ? 27.0 : -1.0;
+                        cb[ell_col_pos(k, lane, w)] = static_cast<int32_t>(line + cx - col_offset);
+                        ++k;
+                    }
+                }
+            }
+        }
+        for (; k < w; ++k) {
+            vb[ell_val_pos(k, lane, w)] = 0.0;
+            cb[ell_col_pos(k, lane, w)] = -1;
+        }
+    }
+}
+
+__global__ void csr_widths_kernel(const int64_t* __restrict__ row_ptr, int64_t n_rows,
+                                  int64_t n_slices, int64_t* widths) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t row = s * 32 + lane;
+        unsigned len = row < n_rows ? static_cast<unsigned>(row_ptr[row + 1] - row_ptr[row]) : 0u;
+        const unsigned w = __reduce_max_sync(0xffffffffu, len);
+        if (lane == 0) widths[s] = 32LL * w;
+    }
+}
+
+__global__ void csr_fill_kernel(const int64_t* __restrict__ row_ptr,
+                                const int64_t* __restrict__ col_idx,
+                                const double* __restrict__ values, int64_t n_rows,
+                                int64_t n_slices, const int64_t* __restrict__ slice_off,
+                                double* vals, int32_t* cols) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t off = slice_off[s];
+        const int w = static_cast<int>((slice_off[s + 1] - off) >> 5);
+        const int64_t row = s * 32 + lane;
+        int k = 0;
+        if (row < n_rows) {
+            for (int64_t e = row_ptr[row]; e < row_ptr[row + 1]; ++e, ++k) {
+                vals[off + ell_val_pos(k, lane, w)] = values[e];
+                cols[off + ell_col_pos(k, lane, w)] = static_cast<int32_t>(col_idx[e]);
+            }
+        }
+        for (; k < w; ++k) {
+            vals[off + ell_val_pos(k, lane, w)] = 0.0;
+            cols[off + ell_col_pos(k, lane, w)] = -1;
+        }
+    }
+}
+
+// Per-tile column band (make_tile_plan, cg.cpp:358-367): min and max local
+// column over the rows [r0, r1), packed as atomics on 64-bit slots.
+__global__ void band_kernel(EllView A, int64_t r0, int64_t r1, unsigned long long* minmax) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t s0 = r0 >> 5, s1 = (r1 + 31) >> 5;
+    long long lo = 0x7fffffffffffffffLL, hi = -1;
+    for (int64_t s = s0 + warp_g; s < s1; s += nwarps) {
+        const int64_t off = A.slice_off[s];
+        const int w = static_cast<int>((A.slice_off[s + 1] - off) >> 5);
+        const int64_t row = s * 32 + lane;
+        if (row < r0 || row >= r1) continue;
+        for (int k = 0; k < w; ++k) {
+            const int c = A.cols[off + ell_col_pos(k, lane, w)];
+            if (c < 0) break;
+            lo = c < lo ? c : lo;
+            hi = c > hi ? c : hi;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if (lane == 0 && hi >= 0) {
+        atomicMin(minmax, static_cast<unsigned long long>(lo));
+        atomicMax(minmax + 1, static_cast<unsigned long long>(hi));
+    }
+}
+
+// ------------------------------------------------------------------- scan
+// Three-phase exclusive scan of int64 (slice offsets): per-block sums, one
+// block scanning the block sums, per-block rescan with the carried base.
+constexpr int kScanItems = 8; // per thread
+constexpr int kScanTile = kThreads * kScanItems;
+
+__device__ int64_t block_exclusive_scan(int64_t v, int64_t* smem, int64_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) smem[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < (kThreads >> 5) ? smem[lane] : 0;
+        int64_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < (kThreads >> 5)) smem[lane] = wi - w;
+        if (lane == (kThreads >> 5) - 1) smem[32] = wi;
+    }
+    __syncthreads();
+    int64_t excl = smem[warp] + inc - v;
+    *total = smem[32];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void scan_sums_kernel(const int64_t* in, int64_t n, int64_t* sums) {
+    __shared__ int64_t smem[33];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    int64_t v = 0;
+    for (int j = 0; j < kScanItems; ++j)
+        if (base + j < n) v += in[base + j];
+    int64_t total;
+    block_exclusive_scan(v, smem, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void scan_top_kernel(int64_t* sums, int64_t nb) {
+    __shared__ int64_t smem[33];
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += kThreads) {
+        const int64_t i = b0 + threadIdx.x;
+        int64_t v = i < nb ? sums[i] : 0;
+        int64_t total;
+        int64_t e = block_exclusive_scan(v, smem, &total);
+        if (i < nb) sums[i] = e + carry;
+        carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[nb] = carry;
+}
+
+__global__ void scan_apply_kernel(const int64_t* in, int64_t n, const int64_t* sums,
+                                  int64_t* out) {
+    __shared__ int64_t smem[33];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    int64_t loc[kScanItems];
+    int64_t v = 0;
+    for (int j = 0; j < kScanItems; ++j) {
+        loc[j] = base + j < n ? in[base + j] : 0;
+        v += loc[j];
+    }
+    int64_t total;
+    int64_t e = block_exclusive_scan(v, smem, &total) + sums[blockIdx.x];
+    for (int j = 0; j < kScanItems; ++j) {
+        if (base + j < n) out[base + j] = e;
+        e += loc[j];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+}
+
+} // namespace
+
+// ------------------------------------------------------------------ launchers
+
+LaunchCfg query_launch_cfg(int sm_count) {
+    int occ_spmv = 0, occ_stream = 0;
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_spmv, spmv_kernel<true>, kThreads, 0));
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_stream, update_xr_kernel, kThreads, 0));
+    LaunchCfg c;
+    c.spmv_blocks = sm_count * (occ_spmv > 0 ? occ_spmv : 1);
+    c.stream_blocks = sm_count * (occ_stream > 0 ? occ_stream : 1);
+    c.threads = kThreads;
+    return c;
+}
+
+static int clamp_blocks(int64_t work_threads, int blocks) {
+    int64_t need = (work_threads + kThreads - 1) / kThreads;
+    if (need < 1) need = 1;
+    return static_cast<int>(need < blocks ? need : blocks);
+}
+
+void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s) {
+    auto slices = [](RowRange r) { return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : 0; };
+    const int64_t ns = slices(a) + slices(b);
+    const int g = clamp_blocks(ns * 32, blocks);
+    if (with_dot)
+        spmv_kernel<true><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin);
+    else
+        spmv_kernel<false><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
+                      const double* Ap, CgScalars* sc, ScalarSrc asrc, RedScratch rs, Fin fin,
+                      int blocks, cudaStream_t s) {
+    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
+    update_xr_kernel<<<g, kThreads, 0, s>>>(i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
+                     ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
+                     cudaStream_t s) {
+    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
+    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
+                int blocks, cudaStream_t s) {
+    const int g = clamp_blocks(i1 - i0, blocks);
+    dot_kernel<<<g, kThreads, 0, s>>>(a, b, i0, i1, rs, fin);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_waxpby(double alpha, const double* x, double beta, const double* y, double* w,
+                   int64_t i0, int64_t i1, int blocks, cudaStream_t s) {
+    if (i1 <= i0) return;
+    const int g = clamp_blocks(i1 - i0, blocks);
+    waxpby_kernel<<<g, kThreads, 0, s>>>(alpha, x, beta, y, w, i0, i1);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_combine(const double* parts, int count, Fin fin, cudaStream_t s) {
+    combine_kernel<<<1, 32, 0, s>>>(parts, count, fin);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_fill(double* p, int64_t n, double v, int blocks, cudaStream_t s) {
+    if (n <= 0) return;
+    fill_kernel<<<clamp_blocks(n, blocks), kThreads, 0, s>>>(p, n, v);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_rhs_splitmix(uint64_t seed, int64_t first, int64_t count, double* out, int blocks,
+                         cudaStream_t s) {
+    if (count <= 0) return;
+    rhs_splitmix_kernel<<<clamp_blocks(count, blocks), kThreads, 0, s>>>(seed, first, count, out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_rhs_xorshift(const uint64_t* chunk_states, int64_t chunk, int64_t count,
+                         int64_t skip, double* out, int /*blocks*/, cudaStream_t s) {
+    if (count <= 0) return;
+    const int64_t nchunks = (count + skip + chunk - 1) / chunk;
+    const int g = static_cast<int>((nchunks + kThreads - 1) / kThreads);
+    rhs_xorshift_kernel<<<g, kThreads, 0, s>>>(chunk_states, chunk, count, skip, out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                           int64_t n_rows, int64_t n_slices, int64_t* widths_out, int blocks,
+                           cudaStream_t s) {
+    stencil_widths_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        nx, ny, nz, row_offset, n_rows, n_slices, widths_out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                         int64_t col_offset, int64_t n_rows, int64_t n_slices,
+                         const int64_t* slice_off, double* vals, int32_t* cols, int blocks,
+                         cudaStream_t s) {
+    stencil_fill_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        nx, ny, nz, row_offset, col_offset, n_rows, n_slices, slice_off, vals, cols);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_csr_widths(const int64_t* row_ptr, int64_t n_rows, int64_t n_slices,
+                       int64_t* widths_out, int blocks, cudaStream_t s) {
+    csr_widths_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        row_ptr, n_rows, n_slices, widths_out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_csr_fill(const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                     int64_t n_rows, int64_t n_slices, const int64_t* slice_off, double* vals,
+                     int32_t* cols, int blocks, cudaStream_t s) {
+    csr_fill_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        row_ptr, col_idx, values, n_rows, n_slices, slice_off, vals, cols);
+    TW_CUDA(cudaGetLastError());
+}
+
+int64_t scan_tmp_elems(int64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+void scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp,
+                        cudaStream_t s) {
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb == 0) {
+        TW_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+        return;
+    }
+    scan_sums_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(in, n, tmp);
+    scan_top_kernel<<<1, kThreads, 0, s>>>(tmp, nb);
+    scan_apply_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(in, n, tmp, out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* minmax, int blocks,
+                 cudaStream_t s) {
+    const int64_t ns = ((r1 + 31) >> 5) - (r0 >> 5);
+    band_kernel<<<clamp_blocks(ns * 32, blocks), kThreads, 0, s>>>(A, r0, r1, minmax);
+    TW_CUDA(cudaGetLastError());
+}
+
+} // namespace tw

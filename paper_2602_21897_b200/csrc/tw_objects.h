@@ -1,0 +1,133 @@
+// Host-side objects behind the opaque C handles.
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "tw_internal.h"
+#include "tw_nccl.h"
+
+namespace tw {
+
+// Fixed-capacity stream pool with FIFO acquisition: the QueuePool of the
+// reference (task_aware.hpp:80-109) over real cudaStream_t.  A caller that
+// asks while every stream is out waits (host side) for the next release.
+class StreamPool {
+public:
+    void init(int device, unsigned capacity);
+    void destroy();
+    int acquire();               // index into streams()
+    void release(int idx);
+    cudaStream_t stream(int idx) const { return streams_[static_cast<size_t>(idx)]; }
+    unsigned capacity() const { return static_cast<unsigned>(streams_.size()); }
+    size_t outstanding() const;
+
+private:
+    std::vector<cudaStream_t> streams_;
+    mutable std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<int> free_;
+};
+
+// Task-aware completion layer over CUDA events: the TACUDA mechanism of
+// ta::TaskAware (task_aware.cpp:16-100).  bind() ties an event to a
+// completion slot that the polling thread fills with the host time at which
+// it first observed the event complete (bind_event_async semantics);
+// wait() polls until an event completes, yielding the thread between polls
+// (wait_transformed semantics).  Device-to-device ordering never goes
+// through here: it is expressed as cudaStreamWaitEvent edges.
+class TaskAware {
+public:
+    explicit TaskAware(int device, double poll_period_s) : device_(device), period_(poll_period_s) {}
+    ~TaskAware();
+    void bind(cudaEvent_t ev, double* slot, double t0);
+    void wait(cudaEvent_t ev);
+    size_t pending() const;
+    size_t polled() const { return polled_.load(); }
+    cudaEvent_t take_event();
+
+private:
+    void loop();
+    size_t poll_once();
+    struct Bind {
+        cudaEvent_t ev;
+        double* slot;
+        double t0;
+    };
+    int device_;
+    double period_;
+    mutable std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Bind> binds_;
+    std::vector<cudaEvent_t> spare_;
+    std::thread th_;
+    bool stop_ = false;
+    bool started_ = false;
+    std::atomic<size_t> polled_{0};
+};
+
+double host_seconds();
+
+extern thread_local std::string g_last_error;
+
+// Runs f, mapping exceptions onto ABI status codes (never throws).
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return TW_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return TW_ERR_CONFIG;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TW_ERR_CONTRACT;
+    }
+}
+
+} // namespace tw
+
+struct tw_ctx {
+    int device = 0;
+    int sm_count = 0;
+    tw::LaunchCfg cfg{};
+    cudaStream_t compute = nullptr;
+    cudaStream_t comm = nullptr;
+    tw::StreamPool pool;
+    // scratch for standalone reductions (tw_dot_range / tw_spmv_dot)
+    double* red_part = nullptr;
+    unsigned* red_ticket = nullptr;
+    std::mutex red_mu;
+    // multi-GPU
+    ncclComm_t nccl_comm = nullptr;
+    int rank = 0;
+    int nranks = 1;
+};
+
+struct tw_ell {
+    tw_ctx* ctx = nullptr;
+    tw_ell_info_t info{};
+    int64_t diag_shift = 0;
+    int64_t* slice_off = nullptr;
+    double* vals = nullptr;
+    int32_t* cols = nullptr;
+    tw::EllView view() const {
+        return tw::EllView{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift};
+    }
+};
+
+namespace tw {
+// helpers shared across translation units
+void ctx_red_scratch(tw_ctx* ctx, RedScratch* rs);
+void tile_plan(const tw_ell* A, int tiles, std::vector<int64_t>& r0, std::vector<int64_t>& r1,
+               std::vector<int64_t>& band_lo_local, std::vector<int64_t>& band_hi_local);
+} // namespace tw

@@ -1,0 +1,767 @@
+// Host runtime of libtw_hpccg: errors, context (device + streams + pool +
+// NCCL), device sliced-ELL matrices, the kernel entry points and right-hand
+// side generators.  The CG drivers live in tw_cg.cpp.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "tw_objects.h"
+
+namespace tw {
+
+thread_local std::string g_last_error;
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    throw Error(TW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                 ":" + std::to_string(line) + ")");
+}
+
+double host_seconds() {
+    using clk = std::chrono::steady_clock;
+    return std::chrono::duration<double>(clk::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------------- NCCL
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        auto sym = [h](const char* n) { return dlsym(h, n); };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+        api.GetErrorString =
+            reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+        api.loaded = api.GetUniqueId && api.CommInitRank && api.AllGather && api.Send &&
+                     api.Recv && api.GroupStart && api.GroupEnd;
+    });
+    if (!api.loaded) throw Error(TW_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return;
+    const char* s = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+    throw Error(TW_ERR_NCCL, std::string(what) + ": " + s);
+}
+
+// -------------------------------------------------------------- StreamPool
+
+void StreamPool::init(int device, unsigned capacity) {
+    TW_CUDA(cudaSetDevice(device));
+    for (unsigned i = 0; i < capacity; ++i) {
+        cudaStream_t s;
+        TW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        streams_.push_back(s);
+        free_.push_back(static_cast<int>(i));
+    }
+}
+
+void StreamPool::destroy() {
+    for (auto s : streams_) cudaStreamDestroy(s);
+    streams_.clear();
+    free_.clear();
+}
+
+int StreamPool::acquire() {
+    std::unique_lock lk(mu_);
+    cv_.wait(lk, [this] { return !free_.empty(); });
+    int i = free_.front();
+    free_.pop_front();
+    return i;
+}
+
+void StreamPool::release(int idx) {
+    {
+        std::lock_guard lk(mu_);
+        free_.push_back(idx);
+    }
+    cv_.notify_one();
+}
+
+size_t StreamPool::outstanding() const {
+    std::lock_guard lk(mu_);
+    return streams_.size() - free_.size();
+}
+
+// --------------------------------------------------------------- TaskAware
+
+TaskAware::~TaskAware() {
+    {
+        std::lock_guard lk(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    if (th_.joinable()) th_.join();
+    for (auto& b : binds_) cudaEventDestroy(b.ev);
+    for (auto e : spare_) cudaEventDestroy(e);
+}
+
+cudaEvent_t TaskAware::take_event() {
+    std::lock_guard lk(mu_);
+    if (!spare_.empty()) {
+        cudaEvent_t e = spare_.back();
+        spare_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    TW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+}
+
+void TaskAware::bind(cudaEvent_t ev, double* slot, double t0) {
+    {
+        std::lock_guard lk(mu_);
+        binds_.push_back({ev, slot, t0});
+        if (!started_) {
+            started_ = true;
+            th_ = std::thread([this] { loop(); });
+        }
+    }
+    cv_.notify_all();
+}
+
+size_t TaskAware::poll_once() {
+    std::lock_guard lk(mu_);
+    size_t done = 0;
+    const double now = host_seconds();
+    // Events complete in stream order; stop at the first one still pending.
+    while (!binds_.empty()) {
+        Bind& b = binds_.front();
+        cudaError_t q = cudaEventQuery(b.ev);
+        if (q == cudaErrorNotReady) break;
+        if (b.slot) *b.slot = now - b.t0;
+        spare_.push_back(b.ev);
+        binds_.pop_front();
+        ++done;
+    }
+    polled_ += done;
+    return done;
+}
+
+void TaskAware::loop() {
+    cudaSetDevice(device_);
+    std::unique_lock lk(mu_);
+    while (!stop_) {
+        if (binds_.empty()) {
+            cv_.wait(lk, [this] { return stop_ || !binds_.empty(); });
+            continue;
+        }
+        lk.unlock();
+        poll_once();
+        std::this_thread::sleep_for(std::chrono::duration<double>(period_));
+        lk.lock();
+    }
+}
+
+void TaskAware::wait(cudaEvent_t ev) {
+    for (;;) {
+        cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) TW_CUDA(q);
+        std::this_thread::yield();
+    }
+}
+
+size_t TaskAware::pending() const {
+    std::lock_guard lk(mu_);
+    return binds_.size();
+}
+
+// ------------------------------------------------------------------ helpers
+
+void ctx_red_scratch(tw_ctx* ctx, RedScratch* rs) {
+    rs->block_part = ctx->red_part;
+    rs->ticket = ctx->red_ticket;
+}
+
+static void check_ctx(const tw_ctx* c) {
+    if (!c) contract_error("null tw_ctx");
+}
+static void check_ell(const tw_ell* a) {
+    if (!a || !a->ctx) contract_error("null tw_ell");
+}
+static cudaStream_t pick(tw_ctx* c, void* s) {
+    return s ? static_cast<cudaStream_t>(s) : c->compute;
+}
+
+static int64_t span_sum(int64_t d) { return d == 1 ? 1 : 3 * d - 2; }
+static int64_t axis_span_h(int64_t c, int64_t d) { return 1 + (c > 0) + (c + 1 < d); }
+
+static void finish_ell(tw_ell* A, int64_t* widths, int64_t n_slices, cudaStream_t s) {
+    int64_t* tmp = nullptr;
+    TW_CUDA(cudaMalloc(&A->slice_off, sizeof(int64_t) * (n_slices + 1)));
+    TW_CUDA(cudaMalloc(&tmp, sizeof(int64_t) * scan_tmp_elems(n_slices)));
+    scan_exclusive_i64(widths, A->slice_off, n_slices, tmp, s);
+    int64_t entries = 0;
+    TW_CUDA(cudaMemcpyAsync(&entries, A->slice_off + n_slices, sizeof(int64_t),
+                            cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> w(static_cast<size_t>(n_slices));
+    if (n_slices)
+        TW_CUDA(cudaMemcpyAsync(w.data(), widths, sizeof(int64_t) * n_slices,
+                                cudaMemcpyDeviceToHost, s));
+    TW_CUDA(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    int64_t mw = 0;
+    for (int64_t v : w) mw = std::max(mw, v / 32);
+    A->info.max_width = static_cast<int32_t>(mw);
+    A->info.ell_entries = entries;
+    A->info.n_slices = n_slices;
+    A->info.slice_rows = kSliceRows;
+    // +32 entries of slack so 128-bit loads of a final short slice stay in bounds
+    TW_CUDA(cudaMalloc(&A->vals, sizeof(double) * (entries + 64)));
+    TW_CUDA(cudaMalloc(&A->cols, sizeof(int32_t) * (entries + 128)));
+}
+
+static void free_ell(tw_ell* A) {
+    if (!A) return;
+    cudaFree(A->slice_off);
+    cudaFree(A->vals);
+    cudaFree(A->cols);
+    delete A;
+}
+
+// gen_stencil_matrix (csr.cpp:29-59) for the slab [z_begin, z_end).
+static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t zb,
+                           int64_t ze) {
+    if (nx < 1 || ny < 1 || nz < 1) config_error("stencil dims must be at least 1");
+    __int128 cells = static_cast<__int128>(nx) * ny * nz;
+    if (cells * 27 > std::numeric_limits<int64_t>::max() / 8) config_error("stencil dims overflow");
+    if (zb < 0 || ze > nz || zb >= ze) contract_error("slab [z_begin, z_end) outside [0, nz)");
+    const int64_t plane = nx * ny;
+    const bool glo = zb > 0, ghi = ze < nz;
+    const int64_t col_lo_plane = zb - (glo ? 1 : 0), col_hi_plane = ze + (ghi ? 1 : 0);
+    const int64_t x_len = (col_hi_plane - col_lo_plane) * plane;
+    if (x_len > std::numeric_limits<int32_t>::max())
+        config_error("slab too large for 32-bit local column indices (" + std::to_string(x_len) +
+                     " columns); split it over more ranks");
+    auto* A = new tw_ell;
+    A->ctx = ctx;
+    tw_ell_info_t& in = A->info;
+    in.nx = nx;
+    in.ny = ny;
+    in.nz = nz;
+    in.z_begin = zb;
+    in.z_end = ze;
+    in.n_global = nx * ny * nz;
+    in.n_rows = (ze - zb) * plane;
+    in.row_offset = zb * plane;
+    in.col_offset = col_lo_plane * plane;
+    in.x_len = x_len;
+    int64_t zspan = 0;
+    for (int64_t z = zb; z < ze; ++z) zspan += axis_span_h(z, nz);
+    in.nnz = span_sum(nx) * span_sum(ny) * zspan;
+    A->diag_shift = in.row_offset - in.col_offset;
+    const int64_t n_slices = (in.n_rows + 31) / 32;
+    cudaStream_t s = ctx->compute;
+    int64_t* widths = nullptr;
+    try {
+        TW_CUDA(cudaMalloc(&widths, sizeof(int64_t) * std::max<int64_t>(n_slices, 1)));
+        launch_stencil_widths(nx, ny, nz, in.row_offset, in.n_rows, n_slices, widths,
+                              ctx->cfg.stream_blocks, s);
+        finish_ell(A, widths, n_slices, s);
+        launch_stencil_fill(nx, ny, nz, in.row_offset, in.col_offset, in.n_rows, n_slices,
+                            A->slice_off, A->vals, A->cols, ctx->cfg.stream_blocks, s);
+        TW_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaFree(widths);
+        free_ell(A);
+        throw;
+    }
+    cudaFree(widths);
+    return A;
+}
+
+// CsrMatrix::validate (csr.cpp:13-27) then device conversion.
+static tw_ell* from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                        const double* values) {
+    if (n < 0 || !row_ptr) config_error("csr: row_ptr must hold n+1 offsets");
+    if (row_ptr[0] != 0) config_error("csr: row_ptr must start at 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (row_ptr[i] > row_ptr[i + 1])
+            config_error("csr: row_ptr decreases at row " + std::to_string(i));
+    const int64_t nnz = row_ptr[n];
+    for (int64_t k = 0; k < nnz; ++k)
+        if (col_idx[k] < 0 || col_idx[k] >= n)
+            config_error("csr: column index " + std::to_string(col_idx[k]) + " out of range");
+    if (n > std::numeric_limits<int32_t>::max())
+        config_error("csr: more rows than 32-bit column indices address");
+    auto* A = new tw_ell;
+    A->ctx = ctx;
+    tw_ell_info_t& in = A->info;
+    in.n_global = n;
+    in.n_rows = n;
+    in.z_end = 0;
+    in.x_len = n;
+    in.nnz = nnz;
+    const int64_t n_slices = (n + 31) / 32;
+    cudaStream_t s = ctx->compute;
+    int64_t *d_rp = nullptr, *d_ci = nullptr, *widths = nullptr;
+    double* d_v = nullptr;
+    try {
+        TW_CUDA(cudaMalloc(&d_rp, sizeof(int64_t) * (n + 1)));
+        TW_CUDA(cudaMalloc(&d_ci, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+        TW_CUDA(cudaMalloc(&d_v, sizeof(double) * std::max<int64_t>(nnz, 1)));
+        TW_CUDA(cudaMalloc(&widths, sizeof(int64_t) * std::max<int64_t>(n_slices, 1)));
+        TW_CUDA(cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+        if (nnz) {
+            TW_CUDA(cudaMemcpyAsync(d_ci, col_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+            TW_CUDA(cudaMemcpyAsync(d_v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+        }
+        launch_csr_widths(d_rp, n, n_slices, widths, ctx->cfg.stream_blocks, s);
+        finish_ell(A, widths, n_slices, s);
+        launch_csr_fill(d_rp, d_ci, d_v, n, n_slices, A->slice_off, A->vals, A->cols,
+                        ctx->cfg.stream_blocks, s);
+        TW_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaFree(d_rp);
+        cudaFree(d_ci);
+        cudaFree(d_v);
+        cudaFree(widths);
+        free_ell(A);
+        throw;
+    }
+    cudaFree(d_rp);
+    cudaFree(d_ci);
+    cudaFree(d_v);
+    cudaFree(widths);
+    return A;
+}
+
+static void to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values) {
+    const tw_ell_info_t& in = A->info;
+    std::vector<int64_t> off(static_cast<size_t>(in.n_slices + 1));
+    std::vector<double> v(static_cast<size_t>(in.ell_entries));
+    std::vector<int32_t> c(static_cast<size_t>(in.ell_entries));
+    TW_CUDA(cudaMemcpy(off.data(), A->slice_off, sizeof(int64_t) * (in.n_slices + 1),
+                       cudaMemcpyDeviceToHost));
+    if (in.ell_entries) {
+        TW_CUDA(cudaMemcpy(v.data(), A->vals, sizeof(double) * in.ell_entries, cudaMemcpyDeviceToHost));
+        TW_CUDA(cudaMemcpy(c.data(), A->cols, sizeof(int32_t) * in.ell_entries, cudaMemcpyDeviceToHost));
+    }
+    int64_t k = 0;
+    row_ptr[0] = 0;
+    for (int64_t row = 0; row < in.n_rows; ++row) {
+        const int64_t s = row / 32;
+        const int lane = static_cast<int>(row % 32);
+        const int w = static_cast<int>((off[s + 1] - off[s]) / 32);
+        bool padded = false;
+        for (int e = 0; e < w; ++e) {
+            const int32_t col = c[static_cast<size_t>(off[s] + ell_col_pos(e, lane, w))];
+            if (col < 0) {
+                padded = true;
+                continue;
+            }
+            if (padded) contract_error("ELL row " + std::to_string(row) + " has an entry after padding");
+            col_idx[k] = static_cast<int64_t>(col) + in.col_offset;
+            values[k] = v[static_cast<size_t>(off[s] + ell_val_pos(e, lane, w))];
+            ++k;
+        }
+        row_ptr[row + 1] = k;
+    }
+}
+
+void tile_plan(const tw_ell* A, int tiles, std::vector<int64_t>& r0, std::vector<int64_t>& r1,
+               std::vector<int64_t>& lo, std::vector<int64_t>& hi) {
+    const int64_t n = A->info.n_rows;
+    if (tiles < 1) config_error("tile plan needs at least one tile");
+    if (tiles > n) config_error("more tiles than matrix rows");
+    tw_ctx* ctx = A->ctx;
+    cudaStream_t s = ctx->compute;
+    unsigned long long* mm = nullptr;
+    TW_CUDA(cudaMalloc(&mm, sizeof(unsigned long long) * 2 * tiles));
+    std::vector<unsigned long long> init(static_cast<size_t>(2 * tiles));
+    for (int t = 0; t < tiles; ++t) {
+        init[2 * t] = std::numeric_limits<unsigned long long>::max();
+        init[2 * t + 1] = 0;
+    }
+    r0.resize(tiles);
+    r1.resize(tiles);
+    lo.resize(tiles);
+    hi.resize(tiles);
+    try {
+        TW_CUDA(cudaMemcpyAsync(mm, init.data(), sizeof(unsigned long long) * 2 * tiles,
+                                cudaMemcpyHostToDevice, s));
+        for (int t = 0; t < tiles; ++t) {
+            r0[t] = n * t / tiles;
+            r1[t] = n * (t + 1) / tiles;
+            launch_band(A->view(), r0[t], r1[t], mm + 2 * t, ctx->cfg.stream_blocks, s);
+        }
+        TW_CUDA(cudaMemcpyAsync(init.data(), mm, sizeof(unsigned long long) * 2 * tiles,
+                                cudaMemcpyDeviceToHost, s));
+        TW_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaFree(mm);
+        throw;
+    }
+    cudaFree(mm);
+    for (int t = 0; t < tiles; ++t) {
+        if (init[2 * t] == std::numeric_limits<unsigned long long>::max()) {
+            // empty tile: band collapses onto its first row (cg.cpp:364-367)
+            lo[t] = hi[t] = r0[t] + A->diag_shift;
+        } else {
+            lo[t] = static_cast<int64_t>(init[2 * t]);
+            hi[t] = static_cast<int64_t>(init[2 * t + 1]);
+        }
+    }
+}
+
+// xorshift64 jump-ahead: the step is linear over GF(2); columns[j] is the
+// image of bit j.
+struct Gf2 {
+    uint64_t col[64];
+    static Gf2 step() {
+        Gf2 m;
+        for (int j = 0; j < 64; ++j) {
+            uint64_t s = 1ull << j;
+            s ^= s << 13;
+            s ^= s >> 7;
+            s ^= s << 17;
+            m.col[j] = s;
+        }
+        return m;
+    }
+    static Gf2 identity() {
+        Gf2 m;
+        for (int j = 0; j < 64; ++j) m.col[j] = 1ull << j;
+        return m;
+    }
+    uint64_t apply(uint64_t v) const {
+        uint64_t r = 0;
+        for (int j = 0; j < 64; ++j)
+            if (v >> j & 1) r ^= col[j];
+        return r;
+    }
+    Gf2 mul(const Gf2& b) const { // this * b
+        Gf2 m;
+        for (int j = 0; j < 64; ++j) m.col[j] = apply(b.col[j]);
+        return m;
+    }
+    static Gf2 power(uint64_t e) {
+        Gf2 r = identity(), b = step();
+        while (e) {
+            if (e & 1) r = b.mul(r);
+            b = b.mul(b);
+            e >>= 1;
+        }
+        return r;
+    }
+};
+
+static void rhs_xorshift(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double* out,
+                         cudaStream_t s) {
+    if (first < 0 || count < 0) contract_error("rhs: negative range");
+    if (count == 0) return;
+    const int64_t chunk = 1024;
+    const int64_t nchunks = (count + chunk - 1) / chunk;
+    std::vector<uint64_t> st(static_cast<size_t>(nchunks));
+    const Gf2 jump = Gf2::power(static_cast<uint64_t>(chunk));
+    uint64_t cur = Gf2::power(static_cast<uint64_t>(first)).apply(seed);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        st[static_cast<size_t>(c)] = cur;
+        cur = jump.apply(cur);
+    }
+    uint64_t* d = nullptr;
+    TW_CUDA(cudaMalloc(&d, sizeof(uint64_t) * nchunks));
+    try {
+        TW_CUDA(cudaMemcpyAsync(d, st.data(), sizeof(uint64_t) * nchunks, cudaMemcpyHostToDevice, s));
+        launch_rhs_xorshift(d, chunk, count, 0, out, ctx->cfg.stream_blocks, s);
+        TW_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+        cudaFree(d);
+        throw;
+    }
+    cudaFree(d);
+}
+
+} // namespace tw
+
+using namespace tw;
+
+extern "C" {
+
+const char* tw_last_error_string(void) { return g_last_error.c_str(); }
+int tw_abi_version(void) { return TW_ABI_VERSION; }
+
+int tw_ctx_create(int device, unsigned cap, tw_ctx** out) {
+    return guarded([&] {
+        if (!out) contract_error("null out pointer");
+        if (cap < 1) config_error("stream pool capacity must be at least 1");
+        int ndev = 0;
+        TW_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev)
+            config_error("device " + std::to_string(device) + " not present (" + std::to_string(ndev) + ")");
+        TW_CUDA(cudaSetDevice(device));
+        auto c = std::make_unique<tw_ctx>();
+        c->device = device;
+        TW_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        int major = 0, minor = 0;
+        TW_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        TW_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+        if (major != 10 || minor != 0)
+            config_error("libtw_hpccg is built for sm_100a (B200); device is sm_" +
+                         std::to_string(major) + std::to_string(minor));
+        c->cfg = query_launch_cfg(c->sm_count);
+        TW_CUDA(cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking));
+        TW_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
+        c->pool.init(device, cap);
+        const int maxg = std::max(c->cfg.spmv_blocks, c->cfg.stream_blocks);
+        TW_CUDA(cudaMalloc(&c->red_part, sizeof(double) * maxg));
+        TW_CUDA(cudaMalloc(&c->red_ticket, sizeof(unsigned) * 4));
+        TW_CUDA(cudaMemset(c->red_ticket, 0, sizeof(unsigned) * 4));
+        *out = c.release();
+    });
+}
+
+int tw_ctx_destroy(tw_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaDeviceSynchronize();
+        if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->nccl_comm);
+        ctx->pool.destroy();
+        cudaStreamDestroy(ctx->compute);
+        cudaStreamDestroy(ctx->comm);
+        cudaFree(ctx->red_part);
+        cudaFree(ctx->red_ticket);
+        delete ctx;
+    });
+}
+
+int tw_ctx_compute_stream(tw_ctx* ctx, void** s) {
+    return guarded([&] {
+        check_ctx(ctx);
+        *s = ctx->compute;
+    });
+}
+
+int tw_ctx_synchronize(tw_ctx* ctx) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TW_CUDA(cudaSetDevice(ctx->device));
+        TW_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+int tw_ctx_device_info(tw_ctx* ctx, int* device, int* sm_count) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (device) *device = ctx->device;
+        if (sm_count) *sm_count = ctx->sm_count;
+    });
+}
+
+int tw_comm_unique_id(unsigned char id_out[128]) {
+    return guarded([&] {
+        ncclUniqueId id;
+        TW_NCCL(nccl().GetUniqueId(&id));
+        static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id_out, &id, 128);
+    });
+}
+
+int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[128]) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (nranks < 1 || rank < 0 || rank >= nranks) config_error("bad rank / world size");
+        if (ctx->nccl_comm) contract_error("communicator already initialised");
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        if (nranks == 1) return;
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        TW_CUDA(cudaSetDevice(ctx->device));
+        TW_NCCL(nccl().CommInitRank(&ctx->nccl_comm, nranks, uid, rank));
+    });
+}
+
+int tw_ctx_comm_info(tw_ctx* ctx, int* rank, int* nranks) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (rank) *rank = ctx->rank;
+        if (nranks) *nranks = ctx->nranks;
+    });
+}
+
+int tw_malloc(tw_ctx* ctx, void** ptr, int64_t bytes) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (bytes < 0) contract_error("negative allocation");
+        TW_CUDA(cudaSetDevice(ctx->device));
+        TW_CUDA(cudaMalloc(ptr, static_cast<size_t>(std::max<int64_t>(bytes, 16))));
+    });
+}
+
+int tw_free(tw_ctx* ctx, void* ptr) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TW_CUDA(cudaFree(ptr));
+    });
+}
+
+int tw_malloc_host(void** ptr, int64_t bytes) {
+    return guarded([&] { TW_CUDA(cudaMallocHost(ptr, static_cast<size_t>(std::max<int64_t>(bytes, 16)))); });
+}
+
+int tw_free_host(void* ptr) {
+    return guarded([&] { TW_CUDA(cudaFreeHost(ptr)); });
+}
+
+int tw_memcpy(tw_ctx* ctx, void* dst, const void* src, int64_t bytes, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (bytes <= 0) return;
+        TW_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                                pick(ctx, stream)));
+    });
+}
+
+int tw_gen_stencil_ell(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t z_begin,
+                       int64_t z_end, tw_ell** out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TW_CUDA(cudaSetDevice(ctx->device));
+        *out = gen_stencil(ctx, nx, ny, nz, z_begin, z_end);
+    });
+}
+
+int tw_ell_from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values, tw_ell** out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        TW_CUDA(cudaSetDevice(ctx->device));
+        *out = from_csr(ctx, n, row_ptr, col_idx, values);
+    });
+}
+
+int tw_ell_info(const tw_ell* A, tw_ell_info_t* out) {
+    return guarded([&] {
+        check_ell(A);
+        *out = A->info;
+    });
+}
+
+int tw_ell_to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values) {
+    return guarded([&] {
+        check_ell(A);
+        TW_CUDA(cudaSetDevice(A->ctx->device));
+        to_csr(A, row_ptr, col_idx, values);
+    });
+}
+
+int tw_ell_destroy(tw_ell* A) {
+    return guarded([&] {
+        if (!A) return;
+        cudaSetDevice(A->ctx->device);
+        free_ell(A);
+    });
+}
+
+int tw_spmv_range(const tw_ell* A, const double* x, double* y, int64_t r0, int64_t r1,
+                  void* stream) {
+    return guarded([&] {
+        check_ell(A);
+        if (r0 < 0 || r1 > A->info.n_rows || r0 > r1) contract_error("spmv row range out of bounds");
+        if (r0 == r1) return;
+        RedScratch rs{};
+        launch_spmv(A->view(), x, y, RowRange{r0, r1}, RowRange{0, 0}, false, rs,
+                    Fin{FIN_NONE, nullptr, nullptr, nullptr}, A->ctx->cfg.spmv_blocks,
+                    pick(A->ctx, stream));
+    });
+}
+
+int tw_spmv_dot(const tw_ell* A, const double* p, double* Ap, int64_t r0, int64_t r1,
+                double* dot_dev, void* stream) {
+    return guarded([&] {
+        check_ell(A);
+        if (r0 < 0 || r1 > A->info.n_rows || r0 > r1) contract_error("spmv row range out of bounds");
+        tw_ctx* c = A->ctx;
+        cudaStream_t s = pick(c, stream);
+        if (r0 == r1) {
+            TW_CUDA(cudaMemsetAsync(dot_dev, 0, sizeof(double), s));
+            return;
+        }
+        std::lock_guard lk(c->red_mu);
+        RedScratch rs;
+        ctx_red_scratch(c, &rs);
+        launch_spmv(A->view(), p, Ap, RowRange{r0, r1}, RowRange{0, 0}, true, rs,
+                    Fin{FIN_STORE, dot_dev, nullptr, nullptr}, c->cfg.spmv_blocks, s);
+    });
+}
+
+int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int64_t i1,
+                 double* out_dev, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (i0 > i1) contract_error("dot range reversed");
+        cudaStream_t s = pick(ctx, stream);
+        if (i0 == i1) {
+            TW_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
+            return;
+        }
+        std::lock_guard lk(ctx->red_mu);
+        RedScratch rs;
+        ctx_red_scratch(ctx, &rs);
+        launch_dot(a, b, i0, i1, rs, Fin{FIN_STORE, out_dev, nullptr, nullptr},
+                   ctx->cfg.stream_blocks, s);
+    });
+}
+
+int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, const double* y,
+                    double* w, int64_t i0, int64_t i1, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (i0 > i1) contract_error("waxpby range reversed");
+        launch_waxpby(alpha, x, beta, y, w, i0, i1, ctx->cfg.stream_blocks, pick(ctx, stream));
+    });
+}
+
+int tw_make_tile_plan(const tw_ell* A, int tiles, int64_t* r0, int64_t* r1, int64_t* band_lo,
+                      int64_t* band_hi) {
+    return guarded([&] {
+        check_ell(A);
+        TW_CUDA(cudaSetDevice(A->ctx->device));
+        std::vector<int64_t> a, b, lo, hi;
+        tile_plan(A, tiles, a, b, lo, hi);
+        for (int t = 0; t < tiles; ++t) {
+            r0[t] = a[t];
+            r1[t] = b[t];
+            band_lo[t] = lo[t] + A->info.col_offset;
+            band_hi[t] = hi[t] + A->info.col_offset;
+        }
+    });
+}
+
+int tw_rhs_xorshift(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double* out_dev,
+                    void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        rhs_xorshift(ctx, seed, first, count, out_dev, pick(ctx, stream));
+    });
+}
+
+int tw_rhs_splitmix(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, double* out_dev,
+                    void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (first < 0 || count < 0) contract_error("rhs: negative range");
+        launch_rhs_splitmix(seed, first, count, out_dev, ctx->cfg.stream_blocks, pick(ctx, stream));
+    });
+}
+
+} // extern "C"

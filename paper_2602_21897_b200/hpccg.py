@@ -1,0 +1,460 @@
+"""Reference-facing host API of the B200 HPCCG path.
+
+Mirrors the reference's operator interface (proj/include/taskweave/
+{csr,kernels,cg}.hpp) with the same names, argument meaning and error
+behaviour, over the C ABI of ``include/tw_hpccg.h``:
+
+==========================  =====================================================
+reference                   here
+==========================  =====================================================
+``Runtime`` (runtime.hpp)   ``Runtime`` -- device context, compute stream, stream
+                            pool (QueuePool capacity), optional NCCL communicator
+``CsrMatrix`` (csr.hpp)     ``EllMatrix`` -- sliced ELL resident in HBM
+``gen_stencil_matrix``      ``gen_stencil_matrix(nx, ny, nz, rt=None, ...)``
+``spmv_range``              ``spmv_range(A, x, y, r0, r1)``
+``dot_range``               ``dot_range(a, b, i0, i1)``
+``waxpby_range``            ``waxpby_range(alpha, x, beta, y, w, i0, i1)``
+``make_tile_plan``          ``make_tile_plan(A, tiles)``
+``cg_monolithic``           ``cg_monolithic(rt, A, b, iterations, opt)``
+``cg_tasks``                ``cg_tasks(rt, A, b, iterations, opt)``
+``CgOptions`` / ``CgResult``  same fields (``backend`` is always the CUDA device)
+==========================  =====================================================
+
+Vectors handed to the kernel functions are device buffers: torch CUDA float64
+tensors, or ``DeviceBuffer`` objects from ``Runtime.alloc``.  Errors raise
+``ConfigError`` (bad input) or ``ContractViolation`` (API misuse), as the
+reference's exceptions do.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _native as N
+from ._native import ConfigError, ContractViolation, CudaError, NcclError  # noqa: F401
+
+
+def _lib():
+    return N.load()
+
+
+def _ptr(v: Any) -> int:
+    """Device pointer of a torch tensor / DeviceBuffer / int."""
+    if v is None:
+        return 0
+    if isinstance(v, int):
+        return v
+    if hasattr(v, "data_ptr"):
+        if getattr(v, "dtype", None) is not None and "float64" not in str(v.dtype) and \
+                "int" not in str(v.dtype):
+            raise ContractViolation(f"expected a float64 device tensor, got {v.dtype}")
+        if hasattr(v, "is_cuda") and not v.is_cuda:
+            raise ContractViolation("expected a CUDA tensor")
+        return int(v.data_ptr())
+    if isinstance(v, DeviceBuffer):
+        return v.ptr
+    raise ContractViolation(f"not a device buffer: {type(v)!r}")
+
+
+class DeviceBuffer:
+    """Raw device allocation owned by a Runtime (for callers without torch)."""
+
+    def __init__(self, rt: "Runtime", nbytes: int):
+        self.rt, self.nbytes = rt, nbytes
+        p = C.c_void_p()
+        N.check(_lib().tw_malloc(rt.h, C.byref(p), nbytes))
+        self.ptr = int(p.value or 0)
+
+    def __del__(self):
+        if getattr(self, "ptr", 0) and self.rt.h:
+            _lib().tw_free(self.rt.h, C.c_void_p(self.ptr))
+            self.ptr = 0
+
+    def upload(self, arr: np.ndarray) -> "DeviceBuffer":
+        arr = np.ascontiguousarray(arr)
+        if arr.nbytes > self.nbytes:
+            raise ContractViolation("upload larger than the buffer")
+        N.check(_lib().tw_memcpy(self.rt.h, C.c_void_p(self.ptr), arr.ctypes.data_as(C.c_void_p),
+                                 arr.nbytes, None))
+        self.rt.synchronize()
+        return self
+
+    def download(self, dtype=np.float64, count: int | None = None) -> np.ndarray:
+        count = self.nbytes // np.dtype(dtype).itemsize if count is None else count
+        out = np.empty(count, dtype)
+        self.rt.synchronize()
+        N.check(_lib().tw_memcpy(self.rt.h, out.ctypes.data_as(C.c_void_p), C.c_void_p(self.ptr),
+                                 out.nbytes, None))
+        self.rt.synchronize()
+        return out
+
+
+class Runtime:
+    """Device context: the tw::Runtime + sim::Device pair of the reference
+    (runtime.hpp:25-55, sim_device.hpp:91-166) on a real B200."""
+
+    def __init__(self, device: int = 0, stream_pool_capacity: int = 4):
+        h = C.c_void_p()
+        N.check(_lib().tw_ctx_create(device, stream_pool_capacity, C.byref(h)))
+        self.h = h
+        self.device = device
+        s = C.c_void_p()
+        N.check(_lib().tw_ctx_compute_stream(self.h, C.byref(s)))
+        self.compute_stream = int(s.value or 0)
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.check(_lib().tw_ctx_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def synchronize(self):
+        N.check(_lib().tw_ctx_synchronize(self.h))
+
+    @property
+    def sm_count(self) -> int:
+        d, s = C.c_int(), C.c_int()
+        N.check(_lib().tw_ctx_device_info(self.h, C.byref(d), C.byref(s)))
+        return s.value
+
+    def alloc(self, count: int, dtype=np.float64) -> DeviceBuffer:
+        return DeviceBuffer(self, int(count) * np.dtype(dtype).itemsize)
+
+    # multi-GPU
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        N.check(_lib().tw_comm_unique_id(buf))
+        return buf.raw
+
+    def init_comm(self, rank: int, nranks: int, uid: bytes | None):
+        uid = uid if uid is not None else bytes(128)
+        N.check(_lib().tw_ctx_init_comm(self.h, rank, nranks, C.c_char_p(uid)))
+
+    @property
+    def rank(self) -> int:
+        r, n = C.c_int(), C.c_int()
+        N.check(_lib().tw_ctx_comm_info(self.h, C.byref(r), C.byref(n)))
+        return r.value
+
+    @property
+    def nranks(self) -> int:
+        r, n = C.c_int(), C.c_int()
+        N.check(_lib().tw_ctx_comm_info(self.h, C.byref(r), C.byref(n)))
+        return n.value
+
+
+_default_rt: Runtime | None = None
+
+
+def default_runtime() -> Runtime:
+    global _default_rt
+    if _default_rt is None:
+        _default_rt = Runtime(0)
+    return _default_rt
+
+
+@dataclass
+class Tile:
+    """tw::bench::Tile (cg.hpp:55-62); band in global columns."""
+    r0: int
+    r1: int
+    band_lo: int
+    band_hi: int
+
+
+class EllMatrix:
+    """The device-resident replacement of CsrMatrix (csr.hpp:9-17)."""
+
+    def __init__(self, rt: Runtime, handle: C.c_void_p):
+        self.rt, self.h = rt, handle
+        info = N.EllInfo()
+        N.check(_lib().tw_ell_info(self.h, C.byref(info)))
+        self.info = info
+
+    def __del__(self):
+        if getattr(self, "h", None) and getattr(self.rt, "h", None):
+            _lib().tw_ell_destroy(self.h)
+            self.h = None
+
+    @property
+    def n(self) -> int:
+        """Rows owned by this rank (all rows on one GPU)."""
+        return int(self.info.n_rows)
+
+    @property
+    def n_global(self) -> int:
+        return int(self.info.n_global)
+
+    def nnz(self) -> int:
+        return int(self.info.nnz)
+
+    @property
+    def x_len(self) -> int:
+        return int(self.info.x_len)
+
+    def to_csr(self):
+        """(row_ptr int64[n+1], col_idx int64[nnz], values f64[nnz]), global columns."""
+        n, nnz = self.n, self.nnz()
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(nnz, np.int64)
+        va = np.empty(nnz, np.float64)
+        N.check(_lib().tw_ell_to_csr(self.h, rp.ctypes.data_as(N.lp), ci.ctypes.data_as(N.lp),
+                                     va.ctypes.data_as(N.dp)))
+        return rp, ci, va
+
+    def validate(self):
+        """CsrMatrix::validate (csr.cpp:13-27) on the converted structure."""
+        rp, ci, _ = self.to_csr()
+        if rp[0] != 0 or np.any(np.diff(rp) < 0) or rp[-1] != len(ci):
+            raise ConfigError("ell: row structure inconsistent")
+        if len(ci) and (ci.min() < 0 or ci.max() >= self.n_global):
+            raise ConfigError("ell: column index out of range")
+
+
+def gen_stencil_matrix(nx: int, ny: int, nz: int, rt: Runtime | None = None,
+                       z_begin: int = 0, z_end: int | None = None) -> EllMatrix:
+    """gen_stencil_matrix (csr.cpp:29-59), generated on the device."""
+    rt = rt or default_runtime()
+    h = C.c_void_p()
+    N.check(_lib().tw_gen_stencil_ell(rt.h, nx, ny, nz, z_begin, nz if z_end is None else z_end,
+                                      C.byref(h)))
+    return EllMatrix(rt, h)
+
+
+def ell_from_csr(row_ptr, col_idx, values, rt: Runtime | None = None) -> EllMatrix:
+    """CsrMatrix (host arrays) -> device ELL; validation as csr.cpp:13-27."""
+    rt = rt or default_runtime()
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    va = np.ascontiguousarray(values, np.float64)
+    if len(ci) != len(va):
+        raise ConfigError("csr: row_ptr[n] disagrees with stored entries")
+    if len(rp) < 1:
+        raise ConfigError("csr: row_ptr must hold n+1 offsets")
+    if rp[-1] != len(ci):
+        raise ConfigError("csr: row_ptr[n] disagrees with stored entries")
+    h = C.c_void_p()
+    N.check(_lib().tw_ell_from_csr(rt.h, len(rp) - 1, rp.ctypes.data_as(N.lp),
+                                   ci.ctypes.data_as(N.lp), va.ctypes.data_as(N.dp), C.byref(h)))
+    return EllMatrix(rt, h)
+
+
+def spmv_range(A: EllMatrix, x, y, r0: int, r1: int, stream: int | None = None) -> None:
+    """y[r0:r1] = A x over local rows (kernels.cpp:5-13); bit-identical."""
+    N.check(_lib().tw_spmv_range(A.h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), r0, r1,
+                                 C.c_void_p(stream or 0)))
+
+
+def spmv_dot(A: EllMatrix, p, Ap, r0: int, r1: int, stream: int | None = None) -> float:
+    """Fused K1: Ap = A p on [r0, r1) and returns p.Ap over the same rows."""
+    out = A.rt.alloc(1)
+    N.check(_lib().tw_spmv_dot(A.h, C.c_void_p(_ptr(p)), C.c_void_p(_ptr(Ap)), r0, r1,
+                               C.c_void_p(out.ptr), C.c_void_p(stream or 0)))
+    return float(out.download()[0])
+
+
+def dot_range(a, b, i0: int, i1: int, rt: Runtime | None = None) -> float:
+    """dot_range (kernels.cpp:15-20) as a fixed-order device reduction."""
+    rt = rt or default_runtime()
+    out = rt.alloc(1)
+    N.check(_lib().tw_dot_range(rt.h, C.c_void_p(_ptr(a)), C.c_void_p(_ptr(b)), i0, i1,
+                                C.c_void_p(out.ptr), None))
+    return float(out.download()[0])
+
+
+def waxpby_range(alpha: float, x, beta: float, y, w, i0: int, i1: int,
+                 rt: Runtime | None = None) -> None:
+    """w = alpha x + beta y on [i0, i1) (kernels.cpp:22-26); bit-identical."""
+    rt = rt or default_runtime()
+    N.check(_lib().tw_waxpby_range(rt.h, alpha, C.c_void_p(_ptr(x)), beta, C.c_void_p(_ptr(y)),
+                                   C.c_void_p(_ptr(w)), i0, i1, None))
+
+
+def make_tile_plan(A: EllMatrix, tiles: int) -> list[Tile]:
+    """make_tile_plan (cg.cpp:348-370); ConfigError for tiles < 1 or > rows."""
+    arrs = [np.empty(max(tiles, 1), np.int64) for _ in range(4)]
+    N.check(_lib().tw_make_tile_plan(A.h, tiles, *[a.ctypes.data_as(N.lp) for a in arrs]))
+    return [Tile(int(arrs[0][t]), int(arrs[1][t]), int(arrs[2][t]), int(arrs[3][t]))
+            for t in range(tiles)]
+
+
+def rhs_xorshift(rt: Runtime, n: int, seed: int = 7, first: int = 0, out=None):
+    """b of acceptance.cpp:48-58 (xorshift64), generated on the device."""
+    out = out if out is not None else rt.alloc(n)
+    N.check(_lib().tw_rhs_xorshift(rt.h, seed, first, n, C.c_void_p(_ptr(out)), None))
+    return out
+
+
+def rhs_splitmix(rt: Runtime, n: int, seed: int = 7, first: int = 0, out=None):
+    """b of scenario.cpp:46-55 / 91-95 (SplitMix64), generated on the device."""
+    out = out if out is not None else rt.alloc(n)
+    N.check(_lib().tw_rhs_splitmix(rt.h, seed, first, n, C.c_void_p(_ptr(out)), None))
+    return out
+
+
+# ----------------------------------------------------------------------- CG
+
+class CgBackend:
+    """CgBackend (cg.hpp:24-28) plus the real device: only ``cuda`` runs here."""
+    cuda = "cuda"
+
+
+@dataclass
+class CgOptions:
+    """CgOptions (cg.hpp:37-45) for the CUDA backend."""
+    tiles: int = 16
+    backend: str = CgBackend.cuda
+    stream_pool_capacity: int = 4
+    iteration_marks: bool = True
+    tol: float = 0.0
+    use_graph: bool = False
+
+    def to_c(self, variant: int) -> N.CgOptionsC:
+        if self.backend != CgBackend.cuda:
+            raise ConfigError(f"backend {self.backend!r} is not available on the B200 build")
+        o = N.CgOptionsC()
+        o.variant = variant
+        o.tiles = int(self.tiles)
+        o.stream_pool_capacity = int(self.stream_pool_capacity)
+        o.use_graph = 1 if self.use_graph else 0
+        o.iteration_marks = 1 if self.iteration_marks else 0
+        o.tol = float(self.tol)
+        return o
+
+
+@dataclass
+class CgResult:
+    """CgResult (cg.hpp:12-17)."""
+    residual_history: np.ndarray
+    x: np.ndarray
+    iterations: int = 0
+    converged: bool = False
+    iteration_marks: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+class CgSolver:
+    """Persistent solve state (CgRun, cg.cpp:24-48) for repeated runs."""
+
+    def __init__(self, rt: Runtime, A: EllMatrix, max_iterations: int,
+                 opt: CgOptions | None = None, variant: int = N.TW_CG_TASKS):
+        self.rt, self.A, self.opt = rt, A, opt or CgOptions()
+        self.max_iterations = max_iterations
+        h = C.c_void_p()
+        copt = self.opt.to_c(variant)
+        N.check(_lib().tw_cg_create(rt.h, A.h, C.byref(copt), max_iterations, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.check(_lib().tw_cg_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_rhs(self, b) -> None:
+        if isinstance(b, np.ndarray):
+            b = np.ascontiguousarray(b, np.float64)
+            if len(b) != self.A.n:
+                raise ContractViolation("rhs length differs from the owned rows")
+            N.check(_lib().tw_cg_set_rhs(self.h, b.ctypes.data_as(C.c_void_p), 0))
+        else:
+            N.check(_lib().tw_cg_set_rhs(self.h, C.c_void_p(_ptr(b)), 1))
+
+    def iterate(self, k: int) -> None:
+        N.check(_lib().tw_cg_iterate(self.h, k))
+
+    def wait(self) -> None:
+        N.check(_lib().tw_cg_wait(self.h))
+
+    def history(self, count: int) -> np.ndarray:
+        out = np.zeros(count, np.float64)
+        N.check(_lib().tw_cg_history(self.h, out.ctypes.data_as(N.dp), count))
+        return out
+
+    def solution(self) -> np.ndarray:
+        out = np.zeros(self.A.n, np.float64)
+        N.check(_lib().tw_cg_solution(self.h, out.ctypes.data_as(N.dp)))
+        return out
+
+    def marks(self, count: int) -> np.ndarray:
+        out = np.zeros(count, np.float64)
+        N.check(_lib().tw_cg_iteration_marks(self.h, out.ctypes.data_as(N.dp), count))
+        return out
+
+    def iterations_done(self) -> int:
+        d = C.c_int()
+        N.check(_lib().tw_cg_iterations_done(self.h, C.byref(d)))
+        return d.value
+
+    def vectors(self):
+        ps = [C.c_void_p() for _ in range(4)]
+        N.check(_lib().tw_cg_vectors(self.h, *[C.byref(p) for p in ps]))
+        return [int(p.value or 0) for p in ps]
+
+    def task_edges(self) -> list[tuple[str, str]]:
+        need = C.c_int64()
+        N.check(_lib().tw_cg_task_edges(self.h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(int(need.value))
+        N.check(_lib().tw_cg_task_edges(self.h, buf, need.value, C.byref(need)))
+        return [tuple(l.split()) for l in buf.value.decode().splitlines() if l]
+
+    def enable_kernel_timing(self, on: bool = True) -> None:
+        N.check(_lib().tw_cg_enable_kernel_timing(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> tuple[float, float, float, int]:
+        """(K1 ms, K2 ms, K3 ms, timed iterations) summed since enable."""
+        a, b, c, k = C.c_double(), C.c_double(), C.c_double(), C.c_int()
+        N.check(_lib().tw_cg_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(c), C.byref(k)))
+        return a.value, b.value, c.value, k.value
+
+    def launches_per_iteration(self) -> tuple[int, int]:
+        k, c = C.c_int(), C.c_int()
+        N.check(_lib().tw_cg_launches_per_iteration(self.h, C.byref(k), C.byref(c)))
+        return k.value, c.value
+
+
+def _solve(rt: Runtime, A: EllMatrix, b, iterations: int, opt: CgOptions | None,
+           variant: int) -> CgResult:
+    opt = opt or CgOptions()
+    s = CgSolver(rt, A, iterations, opt, variant)
+    try:
+        s.set_rhs(b)
+        s.iterate(iterations)
+        hist = s.history(iterations)
+        x = s.solution()
+        marks = s.marks(iterations) if opt.iteration_marks else np.zeros(0)
+    finally:
+        s.close()
+    conv = bool(opt.tol > 0 and iterations > 0 and hist[-1] < opt.tol)
+    return CgResult(hist, x, iterations, conv, marks)
+
+
+def cg_monolithic(rt: Runtime, A: EllMatrix, b, iterations: int,
+                  opt: CgOptions | None = None) -> CgResult:
+    """cg_monolithic (cg.cpp:397-436): one stream, tiles forced to 1."""
+    return _solve(rt, A, b, iterations, opt, N.TW_CG_MONOLITHIC)
+
+
+def cg_tasks(rt: Runtime, A: EllMatrix, b, iterations: int,
+             opt: CgOptions | None = None) -> CgResult:
+    """cg_tasks (cg.cpp:438-447): the block-task DAG on pooled streams."""
+    return _solve(rt, A, b, iterations, opt, N.TW_CG_TASKS)

@@ -1,0 +1,70 @@
+"""CPU tests of the C-ABI boundary: the product library loads without a GPU,
+exports every symbol include/tw_hpccg.h declares, and fails loudly (never
+silently falls back) when no B200 is present."""
+import ctypes as C
+import os
+import subprocess
+
+import pytest
+
+import paper_2602_21897_b200 as P
+from paper_2602_21897_b200 import _native as N
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.load()
+    declared = N.declared_symbols()
+    assert len(declared) >= 40
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert missing == []
+    bound = {name for name, _, _ in N.SIGNATURES}
+    assert set(declared) == bound, set(declared) ^ bound
+
+
+def test_abi_version_and_struct_layout():
+    lib = N.load()
+    assert lib.tw_abi_version() == 1
+    assert C.sizeof(N.EllInfo) == 13 * 8 + 2 * 4
+    assert C.sizeof(N.CgOptionsC) == 4 * 5 + 4 + 8  # 5 ints + pad + double
+    o = N.CgOptionsC()
+    lib.tw_cg_options_default(C.byref(o))
+    # CgOptions defaults (cg.hpp:37-45): tiles 16, stream pool 4, marks on, tol 0
+    assert (o.variant, o.tiles, o.stream_pool_capacity, o.iteration_marks, o.tol) == \
+        (N.TW_CG_TASKS, 16, 4, 1, 0.0)
+
+
+def test_exports_are_plain_c():
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    tw = [l.split()[-1] for l in out.splitlines() if " T tw_" in l]
+    assert set(N.declared_symbols()) <= set(tw)
+    assert not any(s.startswith("_Z") and "tw_" in s and " T " in s for s in out.splitlines()
+                   if s.split()[-1].startswith("tw_"))
+
+
+def test_null_handles_are_contract_violations():
+    lib = N.load()
+    assert lib.tw_ctx_compute_stream(None, None) == N.TW_ERR_CONTRACT
+    assert b"null" in lib.tw_last_error_string()
+    assert lib.tw_cg_iterate(None, 1) == N.TW_ERR_CONTRACT
+    assert lib.tw_ell_info(None, None) == N.TW_ERR_CONTRACT
+    with pytest.raises(P.ContractViolation):
+        N.check(lib.tw_cg_wait(None))
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises((P.CudaError, P.ConfigError)):
+        P.Runtime(0)
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.dirname(P.__file__)
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".h")):
+                text = open(os.path.join(root, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "hpccg_oracle" not in text and "libtwref" not in text, f

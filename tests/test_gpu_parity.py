@@ -1,0 +1,321 @@
+"""GPU parity tests: the CUDA path (libtw_hpccg.so through the C ABI) against
+the oracle and the reference's golden vectors.
+
+Bar: matrix structure and values bit-exact; SpMV and waxpby
+bit-exact; dots within reassociation error; CG residual histories within
+1e-10 relative inside the window res_k >= 1e-15 res_0 (|d| <= 1e-10 res_0
+after it); final x within 1e-10 relative elementwise."""
+import numpy as np
+import pytest
+
+from conftest import check_history, rel_gap
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_2602_21897_b200")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0")
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------- K0
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 2, 2), (4, 3, 5), (5, 5, 5), (6, 5, 4)])
+def test_structure_bit_exact_vs_golden(rt, golden, dims):
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    rp, ci, va = A.to_csr()
+    key = "csr_%dx%dx%d" % dims
+    assert np.array_equal(rp, golden[key + "_row_ptr"])
+    assert np.array_equal(ci, golden[key + "_col_idx"])
+    assert np.array_equal(va, golden[key + "_values"])
+    A.validate()
+
+
+@pytest.mark.parametrize("dims", [(3, 1, 7), (1, 9, 2), (33, 17, 5), (32, 32, 32), (64, 48, 40),
+                                  (128, 128, 128)])
+def test_structure_bit_exact_vs_oracle(rt, orc, dims):
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    m = orc.stencil(*dims)
+    rp, ci, va = A.to_csr()
+    assert A.nnz() == m.nnz
+    assert np.array_equal(rp, m.row_ptr)
+    assert np.array_equal(ci, m.col_idx)
+    assert np.array_equal(va, m.values)
+    assert A.info.max_width == (27 if min(dims) >= 3 else A.info.max_width)
+
+
+@pytest.mark.parametrize("dims,zb,ze", [((8, 6, 10), 0, 3), ((8, 6, 10), 3, 7), ((8, 6, 10), 7, 10),
+                                        ((5, 7, 4), 1, 2)])
+def test_slab_structure_is_a_row_block(rt, orc, dims, zb, ze):
+    nx, ny, nz = dims
+    A = P.gen_stencil_matrix(nx, ny, nz, rt=rt, z_begin=zb, z_end=ze)
+    m = orc.stencil(*dims)
+    r0, r1 = zb * nx * ny, ze * nx * ny
+    rp, ci, va = A.to_csr()
+    assert np.array_equal(rp, m.row_ptr[r0:r1 + 1] - m.row_ptr[r0])
+    assert np.array_equal(ci, m.col_idx[m.row_ptr[r0]:m.row_ptr[r1]])
+    assert np.array_equal(va, m.values[m.row_ptr[r0]:m.row_ptr[r1]])
+    assert A.info.row_offset == r0
+    assert A.info.col_offset == max(zb - 1, 0) * nx * ny
+
+
+def test_bad_dims_config_error(rt):
+    with pytest.raises(P.ConfigError):
+        P.gen_stencil_matrix(0, 1, 1, rt=rt)  # csr.cpp:30-31
+    with pytest.raises(P.ConfigError):
+        P.gen_stencil_matrix(1 << 40, 1 << 20, 1, rt=rt)  # csr.cpp:32-34
+    with pytest.raises(P.ContractViolation):
+        P.gen_stencil_matrix(4, 4, 4, rt=rt, z_begin=3, z_end=2)
+
+
+def test_from_csr_roundtrip_and_validation(rt, orc):
+    m = orc.stencil(7, 5, 3)
+    vals = m.values.copy()
+    vals[5] = 0.1 + 1.0 / 3.0  # full-precision-hostile value (test_bench.cpp:117-130)
+    A = P.ell_from_csr(m.row_ptr, m.col_idx, vals, rt=rt)
+    rp, ci, va = A.to_csr()
+    assert np.array_equal(rp, m.row_ptr) and np.array_equal(ci, m.col_idx)
+    assert np.array_equal(va, vals)
+    bad = m.col_idx.copy()
+    bad[0] = 99999
+    with pytest.raises(P.ConfigError):
+        P.ell_from_csr(m.row_ptr, bad, m.values, rt=rt)  # test_bench.cpp:132-135
+    rpb = m.row_ptr.copy()
+    rpb[1] = rpb[2] + 1
+    with pytest.raises(P.ConfigError):
+        P.ell_from_csr(rpb, m.col_idx, m.values, rt=rt)
+
+
+# ------------------------------------------------------------------- K1
+
+@pytest.mark.parametrize("dims", [(6, 5, 4), (32, 32, 32), (37, 29, 23), (128, 128, 128)])
+def test_spmv_bit_exact(rt, orc, golden, dims):
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    m = orc.stencil(*dims)
+    x = orc.rhs_xorshift(m.n, 3) if dims == (6, 5, 4) else orc.rhs_splitmix(m.n, 11) - 0.5
+    xd, yd = dev(x), torch.zeros(m.n, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(A, xd, yd, 0, m.n)
+    y = host(yd)
+    want = golden["spmv_6x5x4_y"] if dims == (6, 5, 4) else orc.spmv(m, x)
+    assert np.array_equal(y, want)
+    # fused K1: same Ap bits, p.Ap within reassociation error
+    y2 = torch.zeros_like(yd)
+    d = P.spmv_dot(A, xd, y2, 0, m.n)
+    assert np.array_equal(host(y2), want)
+    assert rel_gap(d, orc.dot(x, want)) < 1e-12
+
+
+def test_spmv_tiled_equals_full(rt, orc):
+    m = orc.stencil(6, 5, 4)  # test_bench.cpp:177-186
+    A = P.gen_stencil_matrix(6, 5, 4, rt=rt)
+    x = dev(orc.rhs_xorshift(m.n, 3))
+    full = torch.zeros(m.n, dtype=torch.float64, device="cuda:0")
+    tiled = torch.zeros_like(full)
+    P.spmv_range(A, x, full, 0, m.n)
+    for t in P.make_tile_plan(A, 7):
+        P.spmv_range(A, x, tiled, t.r0, t.r1)
+    assert torch.equal(full, tiled)
+
+
+def test_spmv_identity_hand_matrix_and_padding(rt, orc):
+    ident = P.ell_from_csr(np.arange(6), np.arange(5), np.ones(5), rt=rt)
+    x = orc.rhs_xorshift(5, 11)
+    y = torch.zeros(5, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(ident, dev(x), y, 0, 5)
+    assert np.array_equal(host(y), x)
+    H = P.ell_from_csr([0, 2, 3, 6], [0, 2, 1, 0, 1, 2], [2, 1, 3, 4, 5, 6], rt=rt)
+    y = torch.zeros(3, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(H, dev(np.array([1.0, -2.0, 3.0])), y, 0, 3)
+    assert np.array_equal(host(y), [5.0, -6.0, 12.0])
+    # ragged rows of a general matrix (padding masked, -0.0 preserved)
+    rng = np.random.default_rng(5)
+    n = 300
+    lens = rng.integers(0, 40, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int64)
+    va = rng.standard_normal(len(ci))
+    from oracle import Csr
+    G = P.ell_from_csr(rp, ci, va, rt=rt)
+    xv = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(G, dev(xv), y, 0, n)
+    assert np.array_equal(host(y), orc.spmv(Csr(n, rp, ci, va), xv))
+
+
+# ------------------------------------------------------------------- K2-K4
+
+def test_waxpby_bit_exact_and_aliasing(rt, orc):
+    n = 257  # test_bench.cpp:207-222
+    x, y = orc.rhs_xorshift(n, 21), orc.rhs_xorshift(n, 22)
+    xd, yd, wd = dev(x), dev(y), torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    P.waxpby_range(1.0, xd, 0.0, yd, wd, 0, n, rt=rt)
+    assert np.array_equal(host(wd), x)
+    P.waxpby_range(0.0, xd, 1.0, yd, wd, 0, n, rt=rt)
+    assert np.array_equal(host(wd), y)
+    P.waxpby_range(2.0, xd, 3.0, yd, wd, 0, n, rt=rt)
+    assert np.array_equal(host(wd), orc.waxpby(2.0, x, 3.0, y))
+    P.waxpby_range(1.0, xd, -0.37, yd, xd, 3, 200, rt=rt)  # w aliases x
+    want = x.copy()
+    want[3:200] = orc.waxpby(1.0, x, -0.37, y)[3:200]
+    assert np.array_equal(host(xd), want)
+
+
+def test_dot_identities(rt, orc):
+    n = 1000  # test_bench.cpp:188-205
+    ones = dev(np.ones(n))
+    assert P.dot_range(ones, ones, 0, n, rt=rt) == float(n)
+    a, b = orc.rhs_xorshift(n, 5), orc.rhs_xorshift(n, 9)
+    assert rel_gap(P.dot_range(dev(a), dev(b), 0, n, rt=rt), orc.dot(a, b)) < 1e-12
+    big = orc.rhs_splitmix(3_000_001, 2)
+    bd = dev(big)
+    assert rel_gap(P.dot_range(bd, bd, 17, 3_000_001, rt=rt), orc.dot(big, big, 17)) < 1e-12
+    assert P.dot_range(bd, bd, 5, 5, rt=rt) == 0.0
+
+
+def test_rhs_generators_bit_exact(rt, orc):
+    for first, count in [(0, 1000), (12345, 70000)]:
+        b = host(torch.zeros(count, dtype=torch.float64, device="cuda:0"))
+        xs = torch.zeros(count, dtype=torch.float64, device="cuda:0")
+        P.rhs_xorshift(rt, count, 7, first, out=xs)
+        assert np.array_equal(host(xs), orc.rhs_xorshift(first + count, 7)[first:])
+        sm = torch.zeros(count, dtype=torch.float64, device="cuda:0")
+        P.rhs_splitmix(rt, count, 7, first, out=sm)
+        assert np.array_equal(host(sm), orc.rhs_splitmix(first + count, 7)[first:])
+        del b
+
+
+@pytest.mark.parametrize("T", [1, 3, 7])
+def test_tile_plan_vs_golden(rt, golden, T):
+    A = P.gen_stencil_matrix(5, 4, 3, rt=rt)
+    got = np.array([[t.r0, t.r1, t.band_lo, t.band_hi] for t in P.make_tile_plan(A, T)]).T
+    assert np.array_equal(got, golden["tiles_5x4x3_T%d" % T])
+    with pytest.raises(P.ConfigError):
+        P.make_tile_plan(A, 0)
+    with pytest.raises(P.ConfigError):
+        P.make_tile_plan(A, A.n + 1)
+
+
+# ------------------------------------------------------------------- CG
+
+@pytest.mark.parametrize("variant,T,graph", [("mono", 1, False), ("mono", 1, True),
+                                             ("tasks", 4, False), ("tasks", 16, True),
+                                             ("tasks", 64, False)])
+def test_cg_32cubed_vs_reference(rt, orc, golden, variant, T, graph):
+    """Acceptance criterion 5 input (acceptance.cpp:298-349) at 150 iterations."""
+    A = P.gen_stencil_matrix(32, 32, 32, rt=rt)
+    b = orc.rhs_xorshift(A.n, 7)
+    opt = P.CgOptions(tiles=T, use_graph=graph)
+    run = P.cg_monolithic if variant == "mono" else P.cg_tasks
+    res = run(rt, A, b, 150, opt)
+    check_history(res.residual_history, golden["cg_32_xorshift7_history"])
+    assert np.all(rel_gap(res.x, golden["cg_32_xorshift7_x"]) <= 1e-10)
+    h = res.residual_history[:50]
+    assert np.all(h[1:] <= h[:-1] * (1 + 1e-12))
+    if variant == "tasks":
+        check_history(res.residual_history[:50], golden["cgtasks_32_T%d_history" % T]
+                      if "cgtasks_32_T%d_history" % T in golden else h)
+
+
+def test_cg_splitmix_and_small_cases(rt, orc, golden):
+    A = P.gen_stencil_matrix(32, 32, 32, rt=rt)
+    res = P.cg_monolithic(rt, A, orc.rhs_splitmix(A.n, 7), 150)
+    check_history(res.residual_history, golden["cg_32_splitmix7_history"])
+    A8 = P.gen_stencil_matrix(8, 8, 8, rt=rt)  # test_bench.cpp:275-295
+    b8 = golden["cg_8_xorshift7_b"]
+    for T in (1, 4, 16):
+        r = P.cg_tasks(rt, A8, b8, 10, P.CgOptions(tiles=T))
+        check_history(r.residual_history, golden["cg_8_xorshift7_history"])
+    A6 = P.gen_stencil_matrix(6, 6, 6, rt=rt)  # test_bench.cpp:307-334
+    r = P.cg_tasks(rt, A6, golden["cg_6_xorshift17_b"], 8, P.CgOptions(tiles=8))
+    check_history(r.residual_history, golden["cg_6_device_ta_T8_history"])
+
+
+def test_cg_identity_converges(rt, golden):
+    ident = P.ell_from_csr(np.arange(7), np.arange(6), np.ones(6), rt=rt)
+    r = P.cg_monolithic(rt, ident, golden["cg_identity_b"], 1, P.CgOptions(tol=1e-12))
+    assert r.converged and abs(r.residual_history[0]) < 1e-14
+    assert np.allclose(r.x, golden["cg_identity_b"], rtol=1e-14)
+
+
+def test_cg_deterministic_and_marks(rt, orc):
+    A = P.gen_stencil_matrix(48, 40, 36, rt=rt)
+    b = orc.rhs_xorshift(A.n, 7)
+    r1 = P.cg_tasks(rt, A, b, 30, P.CgOptions(tiles=8))
+    r2 = P.cg_tasks(rt, A, b, 30, P.CgOptions(tiles=8, use_graph=True))
+    assert np.array_equal(r1.residual_history, r2.residual_history)
+    assert np.array_equal(r1.x, r2.x)
+    assert np.all(r1.iteration_marks > 0) and np.all(np.diff(r1.iteration_marks) >= 0)
+    m = orc.stencil(48, 40, 36)
+    h, x, _ = orc.cg(m, b, 30, tiles=8)
+    check_history(r1.residual_history, h)
+    assert np.all(rel_gap(r1.x, x) <= 1e-10)
+
+
+def test_cg_task_dag_edges_match_reference(rt, orc, golden):
+    A = P.gen_stencil_matrix(4, 4, 4, rt=rt)
+    s = P.CgSolver(rt, A, 2, P.CgOptions(tiles=4))
+    s.set_rhs(orc.rhs_xorshift(64, 7))
+    s.iterate(2)
+    s.wait()
+    got = sorted(" ".join(e) for e in s.task_edges())
+    want = sorted(str(e) for e in golden["dag_4x4x4_T4_it2_edges"])
+    assert got == want
+    s.close()
+
+
+def test_cg_iterate_in_pieces_equals_one_shot(rt, orc):
+    A = P.gen_stencil_matrix(20, 20, 20, rt=rt)
+    b = orc.rhs_splitmix(A.n, 3)
+    for variant in (0, 1):
+        s = P.CgSolver(rt, A, 40, P.CgOptions(tiles=5), variant=variant)
+        s.set_rhs(b)
+        s.iterate(13)
+        s.iterate(27)
+        h = s.history(40)
+        x = s.solution()
+        s.set_rhs(dev(b))
+        s.iterate(40)
+        assert np.array_equal(h, s.history(40)) and np.array_equal(x, s.solution())
+        with pytest.raises(P.ContractViolation):
+            s.iterate(1)
+        s.close()
+
+
+def test_cg_256_properties(rt):
+    """Full-size (256^3) properties the domain offers: residual non-increasing,
+    deterministic replay, and r = b - A x consistency of the recurrence."""
+    A = P.gen_stencil_matrix(256, 256, 256, rt=rt)
+    assert A.nnz() == 449455096 and A.info.max_width == 27
+    n = A.n
+    b = P.rhs_xorshift(rt, n, 7)
+    s = P.CgSolver(rt, A, 20, P.CgOptions(iteration_marks=False), variant=0)
+    s.set_rhs(b)
+    s.iterate(20)
+    h = s.history(20)
+    assert np.all(h[1:] <= h[:-1] * (1 + 1e-12))
+    x, r, p, Ap = s.vectors()
+    # true residual ||b - A x|| tracks the recurrence residual (CG, 20 its)
+    xt = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    bt = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    import ctypes
+    ctypes.memmove  # noqa
+    from paper_2602_21897_b200 import _native as N
+    N.check(N.load().tw_memcpy(rt.h, ctypes.c_void_p(xt.data_ptr()), ctypes.c_void_p(x), 8 * n, None))
+    N.check(N.load().tw_memcpy(rt.h, ctypes.c_void_p(bt.data_ptr()), ctypes.c_void_p(b.ptr), 8 * n, None))
+    rt.synchronize()
+    ax = torch.zeros_like(xt)
+    P.spmv_range(A, xt, ax, 0, n)
+    rt.synchronize()
+    true_res = torch.linalg.norm(bt - ax).item()
+    assert abs(true_res - h[-1]) / h[-1] < 1e-6
+    s.set_rhs(b)
+    s.iterate(20)
+    assert np.array_equal(h, s.history(20))
+    s.close()
