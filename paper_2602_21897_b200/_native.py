@@ -119,6 +119,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("TW_HPCCG_LIB", path)  # tuning variants built by scripts/
     if not os.path.exists(path):
         raise NativeLibraryMissing(
             f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "

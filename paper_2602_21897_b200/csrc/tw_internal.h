@@ -44,6 +44,8 @@ struct EllView {
     int64_t n_rows;
     int64_t n_slices;
     int64_t diag_shift;       // x index of local row i is i + diag_shift
+    int max_width;            // widest slice (sizes the TMA stages)
+    int tma_blocks;           // persistent grid of the TMA SpMV (0 = plain kernel)
 };
 
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
@@ -107,6 +109,7 @@ struct LaunchCfg {
     int spmv_blocks;   // grid for the SpMV family (SMs x resident blocks)
     int stream_blocks; // grid for streaming vector kernels
     int threads;       // 256
+    int tma_blocks;    // one CTA per SM for the TMA-staged SpMV
 };
 
 struct RowRange {
@@ -157,6 +160,8 @@ void scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp
 int64_t scan_tmp_elems(int64_t n);
 void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* minmax,
                  int blocks, cudaStream_t s);
+
+int spmv_tma_smem_bytes(int max_width);
 
 // Occupancy-derived launch configuration for this device.
 LaunchCfg query_launch_cfg(int sm_count);

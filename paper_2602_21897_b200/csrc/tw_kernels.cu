@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "tw_internal.h"
 
@@ -29,6 +30,14 @@ namespace tw {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef TW_TMA_WARPS
+#define TW_TMA_WARPS 16
+#endif
+#ifndef TW_TMA_STAGES
+#define TW_TMA_STAGES 1
+#endif
+constexpr int kTmaWarps = TW_TMA_WARPS;   // consumer warps per CTA (one CTA per SM)
+constexpr int kTmaStages = TW_TMA_STAGES; // shared-memory stages per warp
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -141,7 +150,7 @@ __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
     if ((W - F) & 1) c[W - 1] = __ldcs(cb + 32 * (W - 1) + lane);
     double xv[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) xv[k] = c[k] >= 0 ? __ldg(x + c[k]) : 0.0;
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(x + max(c[k], 0)); // branch-free: padding loads x[0], masked below
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < W; ++k)
@@ -196,6 +205,175 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
             y[row] = acc;
             if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
         }
+    }
+    if (DOT) grid_reduce_finalize(part, rs, fin);
+}
+
+// ----------------------------------------------- K1 with TMA-staged matrix
+
+// The matrix stream (12 B per nonzero, 95% of K1's bytes) is moved by the
+// Tensor Memory Accelerator: every warp owns a ring of S shared-memory
+// stages and keeps S slice blocks (values + columns, contiguous in HBM) in
+// flight with cp.async.bulk, completing on a per-stage mbarrier.  The warp
+// computes slice k from shared memory while slices k+1..k+S-1 stream in, so
+// DRAM sees deep memory-level parallelism regardless of the gather latency
+// of x (which stays on the L1/L2 path with __ldg).  The matrix copies carry
+// an L2 evict-first policy so the p planes being gathered stay L2-resident.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// One row of a width-W slice block resident in shared memory: columns first,
+// then every gather issued before any use, then the reference's ordered sum.
+template <int W>
+__device__ __forceinline__ double smem_row_fixed(const double* vb, const int32_t* cb,
+                                                 const double* __restrict__ x, int lane) {
+    int c[W];
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+        int4 t = reinterpret_cast<const int4*>(cb + 128 * q)[lane];
+        c[4 * q] = t.x;
+        c[4 * q + 1] = t.y;
+        c[4 * q + 2] = t.z;
+        c[4 * q + 3] = t.w;
+    }
+    constexpr int F = W & ~3;
+    if (W - F >= 2) {
+        int2 t = reinterpret_cast<const int2*>(cb + 32 * F)[lane];
+        c[F] = t.x;
+        c[F + 1] = t.y;
+    }
+    if ((W - F) & 1) c[W - 1] = cb[32 * (W - 1) + lane];
+    double xv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) xv[k] = __ldg(x + max(c[k], 0)); // branch-free: padding loads x[0], masked below
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
+        if (c[2 * j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v.x, xv[2 * j]));
+        if (c[2 * j + 1] >= 0) acc = __dadd_rn(acc, __dmul_rn(v.y, xv[2 * j + 1]));
+    }
+    if (W & 1)
+        if (c[W - 1] >= 0) acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane], xv[W - 1]));
+    return acc;
+}
+
+__device__ __forceinline__ double smem_row_generic(const double* vb, const int32_t* cb,
+                                                   const double* __restrict__ x, int lane, int w) {
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+        const int c = cb[ell_col_pos(k, lane, w)];
+        if (c < 0) break;
+        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], __ldg(x + c)));
+    }
+    return acc;
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
+                RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kTmaWarps][kTmaStages];
+    __shared__ int stage_w[kTmaWarps][kTmaStages];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* ring = smem + static_cast<size_t>(warp) * kTmaStages * stage_bytes;
+    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    const int64_t sa0 = ra.r0 >> 5, sa1 = ra.r1 > ra.r0 ? (ra.r1 + 31) >> 5 : sa0;
+    const int64_t sb0 = rb.r0 >> 5, sb1 = rb.r1 > rb.r0 ? (rb.r1 + 31) >> 5 : sb0;
+    const int64_t na = sa1 - sa0, ntot = na + (sb1 - sb0);
+    const int64_t mine = warp_g < ntot ? (ntot - warp_g + nwarps - 1) / nwarps : 0;
+    auto slice_of = [&](int64_t k) {
+        const int64_t i = warp_g + k * nwarps;
+        return i < na ? sa0 + i : sb0 + (i - na);
+    };
+    if (lane == 0)
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    auto issue = [&](int64_t k, int st) {
+        const int64_t s = slice_of(k);
+        const int64_t off = A.slice_off[s], end = A.slice_off[s + 1];
+        const uint32_t ents = static_cast<uint32_t>(end - off);
+        stage_w[warp][st] = static_cast<int>(ents >> 5);
+        unsigned char* dst = ring + static_cast<size_t>(st) * stage_bytes;
+        mbar_expect_tx(&bars[warp][st], ents * 12u);
+        bulk_g2s(dst, A.vals + off, ents * 8u, &bars[warp][st], pol);
+        bulk_g2s(dst + val_bytes, A.cols + off, ents * 4u, &bars[warp][st], pol);
+    };
+    if (lane == 0)
+        for (int st = 0; st < kTmaStages && st < mine; ++st) issue(st, st);
+    __syncwarp();
+    double part = 0.0;
+    for (int64_t k = 0; k < mine; ++k) {
+        const int st = static_cast<int>(k % kTmaStages);
+        mbar_wait(&bars[warp][st], static_cast<uint32_t>((k / kTmaStages) & 1));
+        const int w = stage_w[warp][st];
+        const double* vb = reinterpret_cast<const double*>(ring + static_cast<size_t>(st) * stage_bytes);
+        const int32_t* cb = reinterpret_cast<const int32_t*>(ring + static_cast<size_t>(st) * stage_bytes + val_bytes);
+        double acc;
+        switch (w) {
+        case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
+        case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
+        case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
+        case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
+        default: acc = smem_row_generic(vb, cb, x, lane, w); break;
+        }
+        const int64_t s = slice_of(k);
+        const int64_t row = (s << 5) + lane;
+        const RowRange r = (warp_g + k * nwarps) < na ? ra : rb;
+        if (row >= r.r0 && row < r.r1) {
+            y[row] = acc;
+            if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
+        }
+        __syncwarp();
+        if (lane == 0 && k + kTmaStages < mine) {
+            // generic-proxy reads of this stage are done; hand it back to TMA
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + kTmaStages, st);
+        }
+        __syncwarp();
     }
     if (DOT) grid_reduce_finalize(part, rs, fin);
 }
@@ -594,6 +772,9 @@ LaunchCfg query_launch_cfg(int sm_count) {
     c.spmv_blocks = sm_count * (occ_spmv > 0 ? occ_spmv : 1);
     c.stream_blocks = sm_count * (occ_stream > 0 ? occ_stream : 1);
     c.threads = kThreads;
+    // TW_SPMV_PLAIN=1 selects the register-path SpMV (A/B comparisons only)
+    const char* plain = std::getenv("TW_SPMV_PLAIN");
+    c.tma_blocks = (plain && plain[0] == '1') ? 0 : sm_count;
     return c;
 }
 
@@ -603,10 +784,46 @@ static int clamp_blocks(int64_t work_threads, int blocks) {
     return static_cast<int>(need < blocks ? need : blocks);
 }
 
+static int tma_stage_bytes(int max_width, int* val_bytes) {
+    const int vb = ((32 * max_width * 8) + 127) / 128 * 128;
+    const int cb = ((32 * max_width * 4) + 127) / 128 * 128;
+    *val_bytes = vb;
+    return vb + cb;
+}
+
+int spmv_tma_smem_bytes(int max_width) {
+    int vb;
+    return kTmaWarps * kTmaStages * tma_stage_bytes(max_width, &vb);
+}
+
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s) {
     auto slices = [](RowRange r) { return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : 0; };
     const int64_t ns = slices(a) + slices(b);
+    if (A.max_width > 0 && A.tma_blocks > 0) {
+        int vb;
+        const int stage = tma_stage_bytes(A.max_width, &vb);
+        const int smem = kTmaWarps * kTmaStages * stage;
+        auto kern = with_dot ? spmv_tma_kernel<true> : spmv_tma_kernel<false>;
+        static int attr_bytes[2] = {0, 0};
+        static int static_bytes[2] = {-1, -1};
+        if (static_bytes[with_dot] < 0) {
+            cudaFuncAttributes fa;
+            TW_CUDA(cudaFuncGetAttributes(&fa, kern));
+            static_bytes[with_dot] = static_cast<int>(fa.sharedSizeBytes);
+        }
+        if (smem + static_bytes[with_dot] <= 227 * 1024) {
+            if (attr_bytes[with_dot] < smem) {
+                TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                attr_bytes[with_dot] = smem;
+            }
+            int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
+            const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
+            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin);
+            TW_CUDA(cudaGetLastError());
+            return;
+        }
+    }
     const int g = clamp_blocks(ns * 32, blocks);
     if (with_dot)
         spmv_kernel<true><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin);

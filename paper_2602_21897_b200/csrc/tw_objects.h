@@ -121,7 +121,8 @@ struct tw_ell {
     double* vals = nullptr;
     int32_t* cols = nullptr;
     tw::EllView view() const {
-        return tw::EllView{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift};
+        return tw::EllView{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
+                           info.max_width, ctx->cfg.tma_blocks};
     }
 };
 

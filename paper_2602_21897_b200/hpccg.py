@@ -69,9 +69,12 @@ class DeviceBuffer:
         self.ptr = int(p.value or 0)
 
     def __del__(self):
-        if getattr(self, "ptr", 0) and self.rt.h:
-            _lib().tw_free(self.rt.h, C.c_void_p(self.ptr))
-            self.ptr = 0
+        try:
+            if getattr(self, "ptr", 0) and self.rt.h:
+                _lib().tw_free(self.rt.h, C.c_void_p(self.ptr))
+                self.ptr = 0
+        except Exception:
+            pass
 
     def upload(self, arr: np.ndarray) -> "DeviceBuffer":
         arr = np.ascontiguousarray(arr)
@@ -187,9 +190,12 @@ class EllMatrix:
         self.info = info
 
     def __del__(self):
-        if getattr(self, "h", None) and getattr(self.rt, "h", None):
-            _lib().tw_ell_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None) and getattr(self.rt, "h", None):
+                _lib().tw_ell_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
 
     @property
     def n(self) -> int:
