@@ -316,7 +316,7 @@ def run_ours(args, dist, rank, world, local):
         traffic = None
         if tr and tr.get("workload") == f"{nx}x{ny}x{args.nz}" and world == 1:
             traffic = tr.get("dram_bytes_per_launch")
-        roofline = {"bound": "hbm", "kernel": "spmv_kernel<true> (K1: SpMV + p.Ap)",
+        roofline = {"bound": "hbm", "kernel": "spmv_tma_kernel<true> (K1: TMA-staged SpMV + p.Ap)",
                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": traffic, "algorithmic_bytes": k1_bytes,
                     "avg_launch_ms": k1_avg, "peak_source": f"{peak_kind} hbm_gbs",

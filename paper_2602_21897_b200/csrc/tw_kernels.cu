@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kThreads = 256;
 #ifndef TW_TMA_WARPS
-#define TW_TMA_WARPS 16
+#define TW_TMA_WARPS 18
 #endif
 #ifndef TW_TMA_STAGES
 #define TW_TMA_STAGES 1
