@@ -188,6 +188,15 @@ int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed);
  * number of timed iterations since the last enable; it synchronises. */
 int tw_cg_enable_kernel_timing(tw_cg* cg, int enable);
 int tw_cg_kernel_times(tw_cg* cg, double* k1_ms, double* k2_ms, double* k3_ms, int* iterations);
+/* The same logical DAG without a device: dependency inference over the
+ * access regions of spawn_iteration (cg.cpp:173-333) for the given tile plan
+ * (rows local, band in local x coordinates, inclusive), `iterations`
+ * iterations, optional ghost planes (a rank's halo task).  Runs on the host
+ * only; the edge list is what tw_cg_task_edges reports for a real solve. */
+int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_t* r1,
+                      const int64_t* band_lo, const int64_t* band_hi, int64_t diag_shift,
+                      int64_t plane, int ghost_lo, int ghost_hi, int iterations, char* buf,
+                      int64_t cap, int64_t* needed);
 /* Physical launches per iteration (kernels + NCCL calls), for reports. */
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
 

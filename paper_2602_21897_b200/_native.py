@@ -106,6 +106,8 @@ SIGNATURES = [
     ("tw_cg_task_edges", C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
     ("tw_cg_enable_kernel_timing", C.c_int, [vp, C.c_int]),
     ("tw_cg_kernel_times", C.c_int, [vp, dp, dp, dp, C.POINTER(C.c_int)]),
+    ("tw_task_dag_edges", C.c_int, [i64, C.c_int, lp, lp, lp, lp, i64, i64, C.c_int, C.c_int,
+                                    C.c_int, C.c_char_p, i64, C.POINTER(i64)]),
     ("tw_cg_launches_per_iteration", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("tw_cg_solve", C.c_int, [vp, vp, vp, C.c_int, C.POINTER(CgOptionsC), dp, dp,
                               C.POINTER(C.c_int)]),

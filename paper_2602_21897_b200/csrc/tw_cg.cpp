@@ -104,6 +104,16 @@ struct LTask {
     int phys; // physical node index within the iteration
 };
 
+// Everything the logical DAG depends on: tile rows, the p band each tile's
+// SpMV reads (local x coordinates, inclusive, as make_tile_plan's band), and
+// across ranks the ghost-plane geometry.
+struct DagSpec {
+    int T = 1;
+    bool halo = false, glo = false, ghi = false;
+    int64_t n = 0, ds = 0, plane = 0;
+    std::vector<int64_t> r0, r1, lo, hi;
+};
+
 struct PNode {
     PhysKind kind;
     int tile;
@@ -144,6 +154,7 @@ struct tw_cg {
            *recv_a = nullptr, *recv_b = nullptr, *send_r = nullptr, *recv_r = nullptr;
 
     std::vector<int64_t> t_r0, t_r1, t_lo, t_hi; // tile plan (local rows / local columns)
+    DagSpec dag;                                 // inputs of the logical DAG
     std::vector<LTask> ltasks;                   // one iteration's logical tasks (template)
     std::vector<PNode> nodes;                    // one iteration's physical nodes
     std::vector<cudaEvent_t> ev[2];              // per node, by iteration parity
@@ -186,14 +197,15 @@ Acc reg(Arr a, int64_t i0, int64_t i1, int mode) {
 // spawn_iteration (cg.cpp:166-334): same tasks, labels and access regions;
 // plus, across GPUs, a halo task that refreshes p's ghost planes.  p is
 // addressed in local x coordinates (ghost planes included).
-void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNode>* nodes) {
-    const int T = cg->T;
-    const int64_t ds = cg->diag_shift;
+void build_logical(const DagSpec& d, int iter, std::vector<LTask>& out,
+                   std::vector<PNode>* nodes) {
+    const int T = d.T;
+    const int64_t ds = d.ds;
     auto tag = [iter](const char* fam, int t) {
         return std::string(fam) + ":" + std::to_string(iter) + ":" + std::to_string(t);
     };
     out.clear();
-    const bool halo = cg->P > 1;
+    const bool halo = d.halo;
     const int off_spmv = halo ? 1 : 0, off_alpha = off_spmv + T, off_upd = off_alpha + 1,
               off_beta = off_upd + T, off_updp = off_beta + 1;
     if (nodes) {
@@ -207,12 +219,12 @@ void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNo
     }
     if (halo) {
         std::vector<Acc> acc;
-        const int64_t n = cg->n, pl = cg->plane;
-        if (cg->glo) {
+        const int64_t n = d.n, pl = d.plane;
+        if (d.glo) {
             acc.push_back(reg(A_P, ds, ds + pl, ACC_R));
             acc.push_back(reg(A_P, 0, pl, ACC_W));
         }
-        if (cg->ghi) {
+        if (d.ghi) {
             acc.push_back(reg(A_P, ds + n - pl, ds + n, ACC_R));
             acc.push_back(reg(A_P, ds + n, ds + n + pl, ACC_W));
         }
@@ -220,13 +232,13 @@ void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNo
     }
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("spmv", t),
-                            {reg(A_P, cg->t_lo[t], cg->t_hi[t] + 1, ACC_R),
-                             reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_W)},
+                            {reg(A_P, d.lo[t], d.hi[t] + 1, ACC_R),
+                             reg(A_AP, d.r0[t], d.r1[t], ACC_W)},
                             off_spmv + t});
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("dot_pAp", t),
-                            {reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_R),
-                             reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_R), reg(A_PA, t, t + 1, ACC_W)},
+                            {reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_R),
+                             reg(A_AP, d.r0[t], d.r1[t], ACC_R), reg(A_PA, t, t + 1, ACC_W)},
                             off_spmv + t});
     out.push_back(LTask{tag("alpha", 0),
                         {reg(A_PA, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_R),
@@ -235,17 +247,17 @@ void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNo
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("x_up", t),
                             {reg(A_ALPHA, 0, 1, ACC_R),
-                             reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_R),
-                             reg(A_X, cg->t_r0[t], cg->t_r1[t], ACC_RW)},
+                             reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_R),
+                             reg(A_X, d.r0[t], d.r1[t], ACC_RW)},
                             off_upd + t});
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("r_up", t),
-                            {reg(A_ALPHA, 0, 1, ACC_R), reg(A_AP, cg->t_r0[t], cg->t_r1[t], ACC_R),
-                             reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_RW)},
+                            {reg(A_ALPHA, 0, 1, ACC_R), reg(A_AP, d.r0[t], d.r1[t], ACC_R),
+                             reg(A_R, d.r0[t], d.r1[t], ACC_RW)},
                             off_upd + t});
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("dot_rr", t),
-                            {reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_R), reg(A_RR, t, t + 1, ACC_W)},
+                            {reg(A_R, d.r0[t], d.r1[t], ACC_R), reg(A_RR, t, t + 1, ACC_W)},
                             off_upd + t});
     out.push_back(LTask{tag("beta_res", 0),
                         {reg(A_RR, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_RW),
@@ -253,20 +265,20 @@ void build_logical(tw_cg* cg, int iter, std::vector<LTask>& out, std::vector<PNo
                         off_beta});
     for (int t = 0; t < T; ++t)
         out.push_back(LTask{tag("p_up", t),
-                            {reg(A_BETA, 0, 1, ACC_R), reg(A_R, cg->t_r0[t], cg->t_r1[t], ACC_R),
-                             reg(A_P, ds + cg->t_r0[t], ds + cg->t_r1[t], ACC_RW)},
+                            {reg(A_BETA, 0, 1, ACC_R), reg(A_R, d.r0[t], d.r1[t], ACC_R),
+                             reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_RW)},
                             off_updp + t});
 }
 
 // Runs the ledger over `iters` iterations; returns logical edges (global
 // task ids = iter * tasks_per_iter + k) and, optionally, the label list.
-void logical_edges(tw_cg* cg, int iters, std::vector<std::pair<int, int>>& edges,
+void logical_edges(const DagSpec& d, int iters, std::vector<std::pair<int, int>>& edges,
                    std::vector<std::string>* labels, std::vector<int>* phys_of) {
     Ledger led;
     std::vector<LTask> it_tasks;
     int base = 0;
     for (int it = 0; it < iters; ++it) {
-        build_logical(cg, it, it_tasks, nullptr);
+        build_logical(d, it, it_tasks, nullptr);
         for (size_t k = 0; k < it_tasks.size(); ++k) {
             const int id = base + static_cast<int>(k);
             std::vector<int> pr;
@@ -286,11 +298,11 @@ void logical_edges(tw_cg* cg, int iters, std::vector<std::pair<int, int>>& edges
 
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
 void build_schedule(tw_cg* cg) {
-    build_logical(cg, 0, cg->ltasks, &cg->nodes);
+    build_logical(cg->dag, 0, cg->ltasks, &cg->nodes);
     const int L = static_cast<int>(cg->ltasks.size());
     std::vector<std::pair<int, int>> edges;
     std::vector<int> phys;
-    logical_edges(cg, 2, edges, nullptr, &phys);
+    logical_edges(cg->dag, 2, edges, nullptr, &phys);
     std::vector<std::set<int>> first(cg->nodes.size()), intra(cg->nodes.size()),
         cross(cg->nodes.size());
     for (auto [a, b] : edges) {
@@ -569,6 +581,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             contract_error("a partial slab needs a multi-rank context");
         }
         tile_plan(A, cg->T, cg->t_r0, cg->t_r1, cg->t_lo, cg->t_hi);
+        cg->dag = DagSpec{cg->T, cg->P > 1, cg->glo, cg->ghi, cg->n, cg->diag_shift, cg->plane,
+                          cg->t_r0, cg->t_r1, cg->t_lo, cg->t_hi};
         TW_CUDA(cudaSetDevice(ctx->device));
         const size_t n = static_cast<size_t>(cg->n);
         TW_CUDA(cudaMalloc(&cg->x, sizeof(double) * (n + 2)));
@@ -796,7 +810,7 @@ int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed) {
         if (!cg) contract_error("null solver");
         std::vector<std::pair<int, int>> edges;
         std::vector<std::string> labels;
-        logical_edges(cg, std::max(cg->enqueued, 1), edges, &labels, nullptr);
+        logical_edges(cg->dag, std::max(cg->enqueued, 1), edges, &labels, nullptr);
         std::ostringstream os;
         for (auto [a, b] : edges) os << labels[static_cast<size_t>(a)] << ' ' << labels[static_cast<size_t>(b)] << '\n';
         const std::string s = os.str();
@@ -835,6 +849,40 @@ int tw_cg_kernel_times(tw_cg* cg, double* k1, double* k2, double* k3, int* itera
         if (k2) *k2 = acc[1];
         if (k3) *k3 = acc[2];
         if (iterations) *iterations = cg->timed;
+    });
+}
+
+int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_t* r1,
+                      const int64_t* band_lo, const int64_t* band_hi, int64_t diag_shift,
+                      int64_t plane, int ghost_lo, int ghost_hi, int iterations, char* buf,
+                      int64_t cap, int64_t* needed) {
+    return guarded([&] {
+        if (tiles < 1 || n_rows < tiles) config_error("tile plan needs 1 <= tiles <= rows");
+        if (iterations < 1) config_error("iterations must be positive");
+        DagSpec d;
+        d.T = tiles;
+        d.n = n_rows;
+        d.ds = diag_shift;
+        d.plane = plane;
+        d.glo = ghost_lo != 0;
+        d.ghi = ghost_hi != 0;
+        d.halo = d.glo || d.ghi;
+        d.r0.assign(r0, r0 + tiles);
+        d.r1.assign(r1, r1 + tiles);
+        d.lo.assign(band_lo, band_lo + tiles);
+        d.hi.assign(band_hi, band_hi + tiles);
+        std::vector<std::pair<int, int>> edges;
+        std::vector<std::string> labels;
+        logical_edges(d, iterations, edges, &labels, nullptr);
+        std::ostringstream os;
+        for (auto [a, b] : edges) os << labels[static_cast<size_t>(a)] << ' ' << labels[static_cast<size_t>(b)] << '\n';
+        const std::string s = os.str();
+        if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
+        if (buf && cap > 0) {
+            const int64_t k = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
+            std::memcpy(buf, s.data(), static_cast<size_t>(k));
+            buf[k] = '\0';
+        }
     });
 }
 

@@ -299,6 +299,25 @@ def make_tile_plan(A: EllMatrix, tiles: int) -> list[Tile]:
             for t in range(tiles)]
 
 
+def task_dag_edges(n_rows: int, tiles: list[Tile] | tuple, iterations: int,
+                   diag_shift: int = 0, plane: int = 0, ghost_lo: bool = False,
+                   ghost_hi: bool = False) -> list[tuple[str, str]]:
+    """Logical block-task DAG of cg_tasks (cg.cpp:166-334) inferred on the
+    host from the tasks' access regions -- the edges the reference's depsys
+    records (dep_system.cpp:22-65).  ``tiles``: Tile list with bands in local
+    x coordinates (== global columns on one rank)."""
+    T = len(tiles)
+    arrs = [np.array([getattr(t, f) for t in tiles], np.int64)
+            for f in ("r0", "r1", "band_lo", "band_hi")]
+    need = C.c_int64()
+    args = [n_rows, T, *[a.ctypes.data_as(N.lp) for a in arrs], diag_shift, plane,
+            int(ghost_lo), int(ghost_hi), iterations]
+    N.check(_lib().tw_task_dag_edges(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(_lib().tw_task_dag_edges(*args, buf, need.value, C.byref(need)))
+    return [tuple(l.split()) for l in buf.value.decode().splitlines() if l]
+
+
 def rhs_xorshift(rt: Runtime, n: int, seed: int = 7, first: int = 0, out=None):
     """b of acceptance.cpp:48-58 (xorshift64), generated on the device."""
     out = out if out is not None else rt.alloc(n)
