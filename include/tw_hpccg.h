@@ -87,6 +87,21 @@ typedef struct tw_ell_info_t {
     int32_t slice_rows;      /* 32                                          */
 } tw_ell_info_t;
 
+/* z-slab decomposition (no reference equivalent; the reference's row tiles,
+ * cg.cpp:348-370, are the single-address-space analogue): the geometry of
+ * the owned planes [z_begin, z_end) of an nx*ny*nz grid.  Host only. */
+typedef struct tw_slab_t {
+    int64_t nx, ny, nz, z_begin, z_end, plane;
+    int64_t n_rows, row_offset, col_offset, x_len, diag_shift, nnz;
+    int64_t interior_r0, interior_r1;           /* local rows that read no ghost plane */
+    int64_t send_lo, recv_lo, send_hi, recv_hi; /* halo planes, local x coordinates    */
+    int32_t ghost_lo, ghost_hi;
+} tw_slab_t;
+int tw_slab_plan(int64_t nx, int64_t ny, int64_t nz, int64_t z_begin, int64_t z_end,
+                 tw_slab_t* out);
+/* Strong-scaling split of nz planes over ranks: [nz*r/R, nz*(r+1)/R). */
+int tw_slab_partition(int64_t nz, int rank, int nranks, int64_t* z_begin, int64_t* z_end);
+
 /* gen_stencil_matrix(nx,ny,nz) (csr.cpp:29-59), generated on the device into
  * sliced ELL, for the z-slab [z_begin, z_end) (pass 0, nz for the whole grid).
  * Per-row entry order, columns and values are the reference's exactly.

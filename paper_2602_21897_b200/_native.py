@@ -58,6 +58,14 @@ class EllInfo(C.Structure):
                 ("max_width", C.c_int32), ("slice_rows", C.c_int32)]
 
 
+class SlabPlan(C.Structure):
+    _fields_ = [(k, i64) for k in ("nx", "ny", "nz", "z_begin", "z_end", "plane", "n_rows",
+                                   "row_offset", "col_offset", "x_len", "diag_shift", "nnz",
+                                   "interior_r0", "interior_r1", "send_lo", "recv_lo",
+                                   "send_hi", "recv_hi")] + [("ghost_lo", C.c_int32),
+                                                             ("ghost_hi", C.c_int32)]
+
+
 class CgOptionsC(C.Structure):
     _fields_ = [("variant", C.c_int), ("tiles", C.c_int), ("stream_pool_capacity", C.c_uint),
                 ("use_graph", C.c_int), ("iteration_marks", C.c_int), ("tol", C.c_double)]
@@ -80,6 +88,8 @@ SIGNATURES = [
     ("tw_malloc_host", C.c_int, [C.POINTER(vp), i64]),
     ("tw_free_host", C.c_int, [vp]),
     ("tw_memcpy", C.c_int, [vp, vp, vp, i64, vp]),
+    ("tw_slab_plan", C.c_int, [i64, i64, i64, i64, i64, C.POINTER(SlabPlan)]),
+    ("tw_slab_partition", C.c_int, [i64, C.c_int, C.c_int, lp, lp]),
     ("tw_gen_stencil_ell", C.c_int, [vp, i64, i64, i64, i64, i64, C.POINTER(vp)]),
     ("tw_ell_from_csr", C.c_int, [vp, i64, lp, lp, dp, C.POINTER(vp)]),
     ("tw_ell_info", C.c_int, [vp, C.POINTER(EllInfo)]),

@@ -135,6 +135,7 @@ struct tw_cg {
     int P = 1;
     int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
     bool glo = false, ghi = false;
+    tw_slab_t slab{}; // z-slab geometry (multi-rank)
 
     double* x = nullptr;
     double* r = nullptr;
@@ -337,14 +338,16 @@ void halo_exchange(tw_cg* cg, cudaStream_t s) {
     const auto& api = nccl();
     const size_t pl = static_cast<size_t>(cg->plane);
     const int rank = cg->ctx->rank;
+    const tw_slab_t& sp = cg->slab;
+    double* p = cg->p_local;
     TW_NCCL(api.GroupStart());
-    if (cg->glo) {
-        TW_NCCL(api.Recv(cg->p_owned - pl, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
-        TW_NCCL(api.Send(cg->p_owned, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
+    if (sp.ghost_lo) {
+        TW_NCCL(api.Recv(p + sp.recv_lo, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
+        TW_NCCL(api.Send(p + sp.send_lo, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
     }
-    if (cg->ghi) {
-        TW_NCCL(api.Recv(cg->p_owned + cg->n, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
-        TW_NCCL(api.Send(cg->p_owned + cg->n - pl, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
+    if (sp.ghost_hi) {
+        TW_NCCL(api.Recv(p + sp.recv_hi, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
+        TW_NCCL(api.Send(p + sp.send_hi, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
     }
     TW_NCCL(api.GroupEnd());
 }
@@ -388,9 +391,7 @@ void enqueue_mono(tw_cg* cg) {
         return;
     }
     cudaStream_t c = cg->ctx->comm;
-    const int64_t lo = cg->glo ? cg->plane : 0;
-    int64_t hi = cg->ghi ? cg->n - cg->plane : cg->n;
-    if (hi < lo) hi = lo;
+    const int64_t lo = cg->slab.interior_r0, hi = cg->slab.interior_r1;
     TW_CUDA(cudaEventRecord(cg->pready_ev, s));
     TW_CUDA(cudaStreamWaitEvent(c, cg->pready_ev, 0));
     halo_exchange(cg, c);
@@ -576,6 +577,10 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             cg->ghi = in.z_end < in.nz;
             if (cg->glo != (ctx->rank > 0) || cg->ghi != (ctx->rank < cg->P - 1))
                 contract_error("slab z-range does not match this rank's position");
+            if (int rc = tw_slab_plan(in.nx, in.ny, in.nz, in.z_begin, in.z_end, &cg->slab); rc)
+                throw Error(rc, g_last_error);
+            if (cg->slab.diag_shift != cg->diag_shift || cg->slab.x_len != cg->x_len)
+                contract_error("matrix and slab plan disagree");
             if (!ctx->nccl_comm) contract_error("multi-rank context without communicator");
         } else if (in.z_begin > 0 || (in.nx && in.z_end < in.nz)) {
             contract_error("a partial slab needs a multi-rank context");

@@ -200,8 +200,6 @@ static cudaStream_t pick(tw_ctx* c, void* s) {
     return s ? static_cast<cudaStream_t>(s) : c->compute;
 }
 
-static int64_t span_sum(int64_t d) { return d == 1 ? 1 : 3 * d - 2; }
-static int64_t axis_span_h(int64_t c, int64_t d) { return 1 + (c > 0) + (c + 1 < d); }
 
 static void finish_ell(tw_ell* A, int64_t* widths, int64_t n_slices, cudaStream_t s) {
     int64_t* tmp = nullptr;
@@ -237,18 +235,69 @@ static void free_ell(tw_ell* A) {
 }
 
 // gen_stencil_matrix (csr.cpp:29-59) for the slab [z_begin, z_end).
+} // namespace tw
+
+// z-slab geometry shared by the generator, the solver and the host tests:
+// owned planes [z_begin, z_end), one ghost plane on each side that has a
+// neighbour, local x coordinates starting at the lower ghost plane.
+extern "C" int tw_slab_plan(int64_t nx, int64_t ny, int64_t nz, int64_t zb, int64_t ze,
+                            tw_slab_t* out) {
+    return tw::guarded([&] {
+        using namespace tw;
+        if (nx < 1 || ny < 1 || nz < 1) config_error("stencil dims must be at least 1");
+        __int128 cells = static_cast<__int128>(nx) * ny * nz;
+        if (cells * 27 > std::numeric_limits<int64_t>::max() / 8) config_error("stencil dims overflow");
+        if (zb < 0 || ze > nz || zb >= ze) contract_error("slab [z_begin, z_end) outside [0, nz)");
+        tw_slab_t p{};
+        p.nx = nx;
+        p.ny = ny;
+        p.nz = nz;
+        p.z_begin = zb;
+        p.z_end = ze;
+        p.plane = nx * ny;
+        p.ghost_lo = zb > 0;
+        p.ghost_hi = ze < nz;
+        p.n_rows = (ze - zb) * p.plane;
+        p.row_offset = zb * p.plane;
+        p.col_offset = (zb - p.ghost_lo) * p.plane;
+        p.x_len = (ze + p.ghost_hi - (zb - p.ghost_lo)) * p.plane;
+        p.diag_shift = p.row_offset - p.col_offset;
+        // rows whose stencil never touches a ghost plane (overlap the halo)
+        p.interior_r0 = p.ghost_lo ? p.plane : 0;
+        p.interior_r1 = p.ghost_hi ? p.n_rows - p.plane : p.n_rows;
+        if (p.interior_r1 < p.interior_r0) p.interior_r1 = p.interior_r0;
+        // halo in local x coordinates: send the first/last owned plane, receive the ghosts
+        p.send_lo = p.diag_shift;
+        p.recv_lo = 0;
+        p.send_hi = p.diag_shift + p.n_rows - p.plane;
+        p.recv_hi = p.diag_shift + p.n_rows;
+        int64_t zspan = 0;
+        for (int64_t z = zb; z < ze; ++z) zspan += 1 + (z > 0) + (z + 1 < nz);
+        auto ss = [](int64_t d) { return d == 1 ? int64_t{1} : 3 * d - 2; };
+        p.nnz = ss(nx) * ss(ny) * zspan;
+        *out = p;
+    });
+}
+
+extern "C" int tw_slab_partition(int64_t nz, int rank, int nranks, int64_t* z_begin,
+                                 int64_t* z_end) {
+    return tw::guarded([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) tw::config_error("bad rank / world size");
+        if (nz < nranks) tw::config_error("fewer planes than ranks");
+        *z_begin = nz * rank / nranks;
+        *z_end = nz * (rank + 1) / nranks;
+    });
+}
+
+namespace tw {
+
+// gen_stencil_matrix (csr.cpp:29-59) for the slab [z_begin, z_end).
 static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t zb,
                            int64_t ze) {
-    if (nx < 1 || ny < 1 || nz < 1) config_error("stencil dims must be at least 1");
-    __int128 cells = static_cast<__int128>(nx) * ny * nz;
-    if (cells * 27 > std::numeric_limits<int64_t>::max() / 8) config_error("stencil dims overflow");
-    if (zb < 0 || ze > nz || zb >= ze) contract_error("slab [z_begin, z_end) outside [0, nz)");
-    const int64_t plane = nx * ny;
-    const bool glo = zb > 0, ghi = ze < nz;
-    const int64_t col_lo_plane = zb - (glo ? 1 : 0), col_hi_plane = ze + (ghi ? 1 : 0);
-    const int64_t x_len = (col_hi_plane - col_lo_plane) * plane;
-    if (x_len > std::numeric_limits<int32_t>::max())
-        config_error("slab too large for 32-bit local column indices (" + std::to_string(x_len) +
+    tw_slab_t sp;
+    if (int rc = tw_slab_plan(nx, ny, nz, zb, ze, &sp); rc != TW_OK) throw Error(rc, g_last_error);
+    if (sp.x_len > std::numeric_limits<int32_t>::max())
+        config_error("slab too large for 32-bit local column indices (" + std::to_string(sp.x_len) +
                      " columns); split it over more ranks");
     auto* A = new tw_ell;
     A->ctx = ctx;
@@ -259,14 +308,12 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
     in.z_begin = zb;
     in.z_end = ze;
     in.n_global = nx * ny * nz;
-    in.n_rows = (ze - zb) * plane;
-    in.row_offset = zb * plane;
-    in.col_offset = col_lo_plane * plane;
-    in.x_len = x_len;
-    int64_t zspan = 0;
-    for (int64_t z = zb; z < ze; ++z) zspan += axis_span_h(z, nz);
-    in.nnz = span_sum(nx) * span_sum(ny) * zspan;
-    A->diag_shift = in.row_offset - in.col_offset;
+    in.n_rows = sp.n_rows;
+    in.row_offset = sp.row_offset;
+    in.col_offset = sp.col_offset;
+    in.x_len = sp.x_len;
+    in.nnz = sp.nnz;
+    A->diag_shift = sp.diag_shift;
     const int64_t n_slices = (in.n_rows + 31) / 32;
     cudaStream_t s = ctx->compute;
     int64_t* widths = nullptr;

@@ -299,6 +299,20 @@ def make_tile_plan(A: EllMatrix, tiles: int) -> list[Tile]:
             for t in range(tiles)]
 
 
+def slab_plan(nx: int, ny: int, nz: int, z_begin: int, z_end: int) -> N.SlabPlan:
+    """z-slab geometry of the owned planes [z_begin, z_end) (host only)."""
+    out = N.SlabPlan()
+    N.check(_lib().tw_slab_plan(nx, ny, nz, z_begin, z_end, C.byref(out)))
+    return out
+
+
+def slab_partition(nz: int, rank: int, nranks: int) -> tuple[int, int]:
+    """Strong-scaling split: planes [nz r / R, nz (r+1) / R)."""
+    a, b = C.c_int64(), C.c_int64()
+    N.check(_lib().tw_slab_partition(nz, rank, nranks, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
 def task_dag_edges(n_rows: int, tiles: list[Tile] | tuple, iterations: int,
                    diag_shift: int = 0, plane: int = 0, ghost_lo: bool = False,
                    ghost_hi: bool = False) -> list[tuple[str, str]]:
