@@ -192,6 +192,11 @@ int tw_cg_vectors(tw_cg* cg, double** x, double** r, double** p, double** Ap);
 /* Host wall time (seconds since tw_cg_set_rhs) at which the poller saw each
  * iteration complete (the cg_iter=i marks, cg.cpp:307-308); 0 if unseen. */
 int tw_cg_iteration_marks(tw_cg* cg, double* host_out, int count);
+/* Device-timed duration (seconds) of each iteration since tw_cg_set_rhs:
+ * the difference of consecutive iteration-end events (the scenario CSV's
+ * iter_time, scenario.cpp:115-124, in seconds instead of virtual units).
+ * Needs iteration_marks. */
+int tw_cg_iteration_times(tw_cg* cg, double* seconds, int count);
 /* Logical block-task DAG of the tasks variant for the iterations enqueued so
  * far: edges as "pred succ\n" label pairs (labels "spmv:i:t", "dot_pAp:i:t",
  * "alpha:i:0", ... as in cg.cpp:168-170).  Returns needed size in *needed. */

@@ -113,6 +113,7 @@ SIGNATURES = [
     ("tw_cg_solution", C.c_int, [vp, dp]),
     ("tw_cg_vectors", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     ("tw_cg_iteration_marks", C.c_int, [vp, dp, C.c_int]),
+    ("tw_cg_iteration_times", C.c_int, [vp, dp, C.c_int]),
     ("tw_cg_task_edges", C.c_int, [vp, C.c_char_p, i64, C.POINTER(i64)]),
     ("tw_cg_enable_kernel_timing", C.c_int, [vp, C.c_int]),
     ("tw_cg_kernel_times", C.c_int, [vp, dp, dp, dp, C.POINTER(C.c_int)]),

@@ -168,6 +168,7 @@ struct tw_cg {
     bool timing = false;
     std::vector<cudaEvent_t> tev;
     int timed = 0;
+    std::vector<cudaEvent_t> iter_ev; // iteration-end timing events (marks on)
     double t0 = 0.0;
     std::vector<double> marks;
     std::unique_ptr<TaskAware> ta;
@@ -534,6 +535,7 @@ void free_cg(tw_cg* cg) {
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
     for (auto e : cg->tev) cudaEventDestroy(e);
+    for (auto e : cg->iter_ev) cudaEventDestroy(e);
     if (cg->fork_ev) cudaEventDestroy(cg->fork_ev);
     if (cg->halo_ev) cudaEventDestroy(cg->halo_ev);
     if (cg->pready_ev) cudaEventDestroy(cg->pready_ev);
@@ -674,6 +676,16 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device) {
     cg->t0 = host_seconds();
 }
 
+// Timing event at the end of iteration i-1 (i = 0: the start of the solve).
+cudaEvent_t iter_event(tw_cg* cg, int i) {
+    while (static_cast<int>(cg->iter_ev.size()) <= i) {
+        cudaEvent_t e;
+        TW_CUDA(cudaEventCreate(&e));
+        cg->iter_ev.push_back(e);
+    }
+    return cg->iter_ev[static_cast<size_t>(i)];
+}
+
 void iterate(tw_cg* cg, int k) {
     if (k < 0) config_error("negative iteration count");
     if (cg->enqueued + k > cg->max_iters)
@@ -684,6 +696,7 @@ void iterate(tw_cg* cg, int k) {
     if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     const bool tasks = cg->opt.variant == TW_CG_TASKS;
     if (!cg->opt.use_graph && tasks) fork_streams(cg);
+    if (cg->opt.iteration_marks && cg->enqueued == 0) TW_CUDA(cudaEventRecord(iter_event(cg, 0), s));
     for (int i = 0; i < k; ++i) {
         const int it = cg->enqueued + i;
         if (cg->opt.use_graph) {
@@ -702,6 +715,8 @@ void iterate(tw_cg* cg, int k) {
             cudaEvent_t e = cg->ta->take_event();
             TW_CUDA(cudaEventRecord(e, ms));
             cg->ta->bind(e, &cg->marks[static_cast<size_t>(it)], cg->t0);
+            // device-timed iteration end (iter_time of the scenario CSV)
+            TW_CUDA(cudaEventRecord(iter_event(cg, it + 1), ms));
         }
     }
     if (!cg->opt.use_graph && tasks) join_streams(cg);
@@ -807,6 +822,21 @@ int tw_cg_iteration_marks(tw_cg* cg, double* host_out, int count) {
         wait_cg(cg);
         while (cg->ta->pending()) std::this_thread::yield();
         std::copy(cg->marks.begin(), cg->marks.begin() + count, host_out);
+    });
+}
+
+int tw_cg_iteration_times(tw_cg* cg, double* seconds, int count) {
+    return guarded([&] {
+        if (!cg) contract_error("null solver");
+        if (!cg->opt.iteration_marks) config_error("iteration times need iteration_marks");
+        if (count < 0 || count > cg->enqueued) contract_error("count beyond iterations run");
+        wait_cg(cg);
+        for (int i = 0; i < count; ++i) {
+            float ms = 0.f;
+            TW_CUDA(cudaEventElapsedTime(&ms, cg->iter_ev[static_cast<size_t>(i)],
+                                         cg->iter_ev[static_cast<size_t>(i + 1)]));
+            seconds[i] = ms * 1e-3;
+        }
     });
 }
 

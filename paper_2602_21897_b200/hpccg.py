@@ -260,6 +260,71 @@ def ell_from_csr(row_ptr, col_idx, values, rt: Runtime | None = None) -> EllMatr
     return EllMatrix(rt, h)
 
 
+CSR_HEADER = "# taskweave csr v1"
+
+
+def dump_csr(A: "EllMatrix | tuple", out=None) -> str:
+    """dump_csr (csr.cpp:61-74): header, "n nnz", then row_ptr, col_idx and
+    values lines, doubles at 17 significant digits (round-trips exactly).
+    ``A`` is a device EllMatrix or a (row_ptr, col_idx, values) tuple."""
+    rp, ci, va = A.to_csr() if isinstance(A, EllMatrix) else A
+    lines = [CSR_HEADER, f"{len(rp) - 1} {int(rp[-1])}",
+             " ".join(str(int(v)) for v in rp), " ".join(str(int(v)) for v in ci),
+             " ".join("%.17g" % v for v in va)]
+    text = "\n".join(lines) + "\n"
+    if out is not None:
+        out.write(text)
+    return text
+
+
+def parse_csr(text: str):
+    """load_csr's parser + CsrMatrix::validate (csr.cpp:13-27, 76-98) on the
+    host: returns (row_ptr, col_idx, values); ConfigError on bad input."""
+    head, _, rest = text.partition("\n")
+    if head.rstrip("\r") != CSR_HEADER:
+        raise ConfigError("csr load: missing 'taskweave csr v1' header")
+    tok = rest.split()
+    try:
+        n, nnz = int(tok[0]), int(tok[1])
+    except (IndexError, ValueError):
+        raise ConfigError("csr load: bad size line") from None
+    if n < 0 or nnz < 0:
+        raise ConfigError("csr: row_ptr must hold n+1 offsets")
+    pos = 2
+
+    def take(count, conv, what):
+        nonlocal pos
+        if pos + count > len(tok):
+            raise ConfigError(f"csr load: truncated {what}")
+        try:
+            vals = [conv(t) for t in tok[pos:pos + count]]
+        except ValueError:
+            raise ConfigError(f"csr load: truncated {what}") from None
+        pos += count
+        return vals
+    rp = np.array(take(n + 1, int, "row_ptr"), np.int64)
+    ci = np.array(take(nnz, int, "col_idx"), np.int64)
+    va = np.array(take(nnz, float, "values"), np.float64)
+    if rp[0] != 0:
+        raise ConfigError("csr: row_ptr must start at 0")
+    bad = np.nonzero(np.diff(rp) < 0)[0]
+    if len(bad):
+        raise ConfigError(f"csr: row_ptr decreases at row {int(bad[0])}")
+    if rp[-1] != nnz:
+        raise ConfigError("csr: row_ptr[n] disagrees with stored entries")
+    if nnz and (ci.min() < 0 or ci.max() >= n):
+        c = int(ci[(ci < 0) | (ci >= n)][0])
+        raise ConfigError(f"csr: column index {c} out of range")
+    return rp, ci, va
+
+
+def load_csr(src, rt: "Runtime | None" = None) -> "EllMatrix":
+    """load_csr (csr.cpp:76-98) straight into a device EllMatrix."""
+    text = src if isinstance(src, str) else src.read()
+    rp, ci, va = parse_csr(text)
+    return ell_from_csr(rp, ci, va, rt=rt)
+
+
 def spmv_range(A: EllMatrix, x, y, r0: int, r1: int, stream: int | None = None) -> None:
     """y[r0:r1] = A x over local rows (kernels.cpp:5-13); bit-identical."""
     N.check(_lib().tw_spmv_range(A.h, C.c_void_p(_ptr(x)), C.c_void_p(_ptr(y)), r0, r1,
@@ -437,6 +502,12 @@ class CgSolver:
     def marks(self, count: int) -> np.ndarray:
         out = np.zeros(count, np.float64)
         N.check(_lib().tw_cg_iteration_marks(self.h, out.ctypes.data_as(N.dp), count))
+        return out
+
+    def iteration_times(self, count: int) -> np.ndarray:
+        """Device-timed seconds per iteration (needs iteration_marks)."""
+        out = np.zeros(count, np.float64)
+        N.check(_lib().tw_cg_iteration_times(self.h, out.ctypes.data_as(N.dp), count))
         return out
 
     def iterations_done(self) -> int:

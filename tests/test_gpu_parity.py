@@ -319,3 +319,29 @@ def test_cg_256_properties(rt):
     s.iterate(20)
     assert np.array_equal(h, s.history(20))
     s.close()
+
+
+# ------------------------------------------------------------ interop (f)
+
+def test_load_csr_to_device_round_trip(rt, golden):
+    text = str(golden["csr_text_3x3x3"][0])
+    A = P.load_csr(text, rt=rt)
+    assert P.dump_csr(A) == text
+    with pytest.raises(P.ConfigError):
+        P.load_csr("# taskweave csr v1\n2 2\n0 1 2\n0 1\n26\n", rt=rt)
+
+
+def test_scenario_run_point_csv(rt, orc, golden):
+    from paper_2602_21897_b200 import scenario as S
+    c = S.ScenarioConfig(nx=32, ny=32, nz=32, iterations=20, warmup=5, repetitions=2,
+                         tiles=[1, 4], variant="tasks")
+    pts = S.run_sweep(c, rt=rt)
+    assert [p.tile for p in pts] == [1, 4]
+    for p in pts:
+        assert len(p.rows) == 40
+        assert all(r.warmup for r in p.rows[:20])            # repetition 0 is warm-up
+        assert [r.warmup for r in p.rows[20:]] == [True] * 5 + [False] * 15
+        assert all(r.iter_time > 0 for r in p.rows) and p.steady_iter_time > 0
+        check_history(p.residual_history, golden["cg_32_splitmix7_history"][:20])
+    text = S.metrics_to_csv(pts)
+    assert S.parse_metrics_csv(text) == [r for p in pts for r in p.rows]
