@@ -33,7 +33,7 @@ extern "C" {
 #define TW_ERR_CUDA 3
 #define TW_ERR_NCCL 4
 
-#define TW_ABI_VERSION 1
+#define TW_ABI_VERSION 2
 
 typedef struct tw_ctx tw_ctx; /* replaces tw::Runtime + sim::Device (runtime.hpp:25-55, sim_device.hpp:91-166) */
 typedef struct tw_ell tw_ell; /* replaces tw::bench::CsrMatrix on the device (csr.hpp:9-17) */
@@ -163,7 +163,12 @@ typedef struct tw_cg_options {
     int use_graph;                 /* capture one iteration as a CUDA graph            */
     int iteration_marks;           /* CgOptions::iteration_marks: host poller stamps cg_iter=i */
     double tol;                    /* CgOptions::tol: converged = last residual < tol  */
+    int dispatch;                  /* TW_DISPATCH_STREAMS | TW_DISPATCH_PERSISTENT (tasks) */
 } tw_cg_options;
+
+#define TW_DISPATCH_STREAMS 0    /* one launch per task, cudaStreamWaitEvent edges (or graph) */
+#define TW_DISPATCH_PERSISTENT 1 /* one persistent kernel runs the whole DAG: chunked tasks,
+                                    device-side dependency counters (tasks variant, 1 rank) */
 
 /* Fills the defaults of CgOptions (cg.hpp:37-45) with the cuda backend. */
 void tw_cg_options_default(tw_cg_options* opt);

@@ -15,6 +15,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "tw_hpccg.h")
 
 TW_OK, TW_ERR_CONFIG, TW_ERR_CONTRACT, TW_ERR_CUDA, TW_ERR_NCCL = 0, 1, 2, 3, 4
 TW_CG_MONOLITHIC, TW_CG_TASKS = 0, 1
+TW_DISPATCH_STREAMS, TW_DISPATCH_PERSISTENT = 0, 1
 
 
 class NativeLibraryMissing(ImportError):
@@ -68,7 +69,8 @@ class SlabPlan(C.Structure):
 
 class CgOptionsC(C.Structure):
     _fields_ = [("variant", C.c_int), ("tiles", C.c_int), ("stream_pool_capacity", C.c_uint),
-                ("use_graph", C.c_int), ("iteration_marks", C.c_int), ("tol", C.c_double)]
+                ("use_graph", C.c_int), ("iteration_marks", C.c_int), ("tol", C.c_double),
+                ("dispatch", C.c_int)]
 
 
 # (name, restype, argtypes) for every symbol include/tw_hpccg.h declares.

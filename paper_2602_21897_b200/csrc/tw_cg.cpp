@@ -169,6 +169,17 @@ struct tw_cg {
     std::vector<cudaEvent_t> tev;
     int timed = 0;
     std::vector<cudaEvent_t> iter_ev; // iteration-end timing events (marks on)
+    // persistent dispatcher (TW_DISPATCH_PERSISTENT): flattened K-iteration DAG
+    int dag_k = -1, dag_ntasks = 0, dag_nchunks = 0;
+    DagTask* d_tasks = nullptr;
+    int* d_chunk_task = nullptr;
+    int* d_succ = nullptr;
+    int* d_npred = nullptr;
+    int* d_remaining = nullptr;
+    unsigned* d_chunk_done = nullptr;
+    double* d_chunk_part = nullptr;
+    unsigned* d_ticket = nullptr;
+    unsigned long long* d_stamps = nullptr;
     double t0 = 0.0;
     std::vector<double> marks;
     std::unique_ptr<TaskAware> ta;
@@ -548,6 +559,15 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->parts);
     cudaFree(cg->block_parts);
     cudaFree(cg->tickets);
+    cudaFree(cg->d_tasks);
+    cudaFree(cg->d_chunk_task);
+    cudaFree(cg->d_succ);
+    cudaFree(cg->d_npred);
+    cudaFree(cg->d_remaining);
+    cudaFree(cg->d_chunk_done);
+    cudaFree(cg->d_chunk_part);
+    cudaFree(cg->d_ticket);
+    cudaFree(cg->d_stamps);
     delete cg;
 }
 
@@ -563,6 +583,18 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             cg->opt = *o;
         else
             tw_cg_options_default(&cg->opt);
+        if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
+            if (cg->opt.variant != TW_CG_TASKS)
+                config_error("the persistent dispatcher runs the tasks variant");
+            if (ctx->nranks > 1)
+                config_error("the persistent dispatcher runs on one rank (halo needs NCCL launches)");
+            int sb, vb;
+            if (dag_smem_bytes(A->info.max_width, &sb, &vb) > 200 * 1024)
+                config_error("matrix rows too wide for the dispatcher's shared-memory stages");
+            if (cg->opt.use_graph) config_error("the persistent dispatcher is one launch; no graph");
+        } else if (cg->opt.dispatch != TW_DISPATCH_STREAMS) {
+            config_error("unknown dispatch mode");
+        }
         if (cg->opt.variant != TW_CG_MONOLITHIC && cg->opt.variant != TW_CG_TASKS)
             config_error("unknown CG variant");
         cg->T = cg->opt.variant == TW_CG_MONOLITHIC ? 1 : cg->opt.tiles; // cg.cpp:400
@@ -638,6 +670,11 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         }
         cg->marks.assign(static_cast<size_t>(std::max(max_iters, 1)), 0.0);
         cg->ta = std::make_unique<TaskAware>(ctx->device, 20e-6);
+        if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
+            TW_CUDA(cudaMalloc(&cg->d_stamps, sizeof(unsigned long long) * (max_iters + 2)));
+            TW_CUDA(cudaMemset(cg->d_stamps, 0, sizeof(unsigned long long) * (max_iters + 2)));
+            TW_CUDA(cudaMalloc(&cg->d_ticket, sizeof(unsigned) * 4));
+        }
     } catch (...) {
         free_cg(cg);
         throw;
@@ -686,6 +723,121 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
     return cg->iter_ev[static_cast<size_t>(i)];
 }
 
+// Flattens k iterations of the physical DAG into the dispatcher's task table
+// (topological order, chunk list, successor lists, predecessor counts).
+void build_dag_table(tw_cg* cg, int k) {
+    const int L = static_cast<int>(cg->nodes.size());
+    const int64_t spmv_cs = 8 * dag_threads() / 32; // slices per SpMV chunk (8 per warp)
+    const int64_t vec_cr = 32768;                  // rows per update chunk
+    std::vector<DagTask> tasks(static_cast<size_t>(k) * L);
+    std::vector<std::vector<int>> succ(tasks.size());
+    std::vector<int> npred(tasks.size(), 0), chunk_task;
+    for (int it = 0; it < k; ++it)
+        for (int j = 0; j < L; ++j) {
+            const PNode& nd = cg->nodes[static_cast<size_t>(j)];
+            const int id = it * L + j;
+            DagTask& t = tasks[static_cast<size_t>(id)];
+            t.tile = nd.tile;
+            t.r0 = cg->t_r0[static_cast<size_t>(nd.tile)];
+            t.r1 = cg->t_r1[static_cast<size_t>(nd.tile)];
+            int nch = 1;
+            switch (nd.kind) {
+            case PK_SPMV: {
+                t.kind = DK_SPMV;
+                const int64_t ns = ((t.r1 + 31) >> 5) - (t.r0 >> 5);
+                nch = static_cast<int>((ns + spmv_cs - 1) / spmv_cs);
+                break;
+            }
+            case PK_ALPHA: t.kind = DK_ALPHA; break;
+            case PK_UPD: t.kind = DK_UPD; nch = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr); break;
+            case PK_BETA: t.kind = DK_BETA; break;
+            case PK_UPDP: t.kind = DK_UPDP; nch = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr); break;
+            default: contract_error("halo task in the single-rank dispatcher");
+            }
+            t.chunk0 = static_cast<int>(chunk_task.size());
+            t.nchunks = nch;
+            chunk_task.insert(chunk_task.end(), static_cast<size_t>(nch), id);
+            auto add = [&](int pred) {
+                succ[static_cast<size_t>(pred)].push_back(id);
+                ++npred[static_cast<size_t>(id)];
+            };
+            if (it == 0) {
+                for (int p : nd.preds_first) add(p);
+            } else {
+                for (int p : nd.preds_intra) add(it * L + p);
+                for (int p : nd.preds_cross) add((it - 1) * L + p);
+            }
+        }
+    std::vector<int> flat;
+    for (size_t i = 0; i < tasks.size(); ++i) {
+        tasks[i].succ0 = static_cast<int>(flat.size());
+        tasks[i].nsucc = static_cast<int>(succ[i].size());
+        flat.insert(flat.end(), succ[i].begin(), succ[i].end());
+    }
+    if (flat.empty()) flat.push_back(0);
+    auto realloc = [](auto*& p, size_t n) {
+        cudaFree(p);
+        p = nullptr;
+        TW_CUDA(cudaMalloc(&p, sizeof(*p) * std::max<size_t>(n, 1)));
+    };
+    realloc(cg->d_tasks, tasks.size());
+    realloc(cg->d_chunk_task, chunk_task.size());
+    realloc(cg->d_succ, flat.size());
+    realloc(cg->d_npred, npred.size());
+    realloc(cg->d_remaining, npred.size());
+    realloc(cg->d_chunk_done, tasks.size());
+    realloc(cg->d_chunk_part, chunk_task.size());
+    TW_CUDA(cudaMemcpy(cg->d_tasks, tasks.data(), sizeof(DagTask) * tasks.size(), cudaMemcpyHostToDevice));
+    TW_CUDA(cudaMemcpy(cg->d_chunk_task, chunk_task.data(), sizeof(int) * chunk_task.size(),
+                       cudaMemcpyHostToDevice));
+    TW_CUDA(cudaMemcpy(cg->d_succ, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+    TW_CUDA(cudaMemcpy(cg->d_npred, npred.data(), sizeof(int) * npred.size(), cudaMemcpyHostToDevice));
+    cg->dag_k = k;
+    cg->dag_ntasks = static_cast<int>(tasks.size());
+    cg->dag_nchunks = static_cast<int>(chunk_task.size());
+}
+
+// k iterations of cg_tasks as ONE persistent kernel (tw_dag.cu).
+void enqueue_persistent(tw_cg* cg, int k) {
+    cudaStream_t s = cg->ctx->compute;
+    if (cg->dag_k != k) {
+        TW_CUDA(cudaStreamSynchronize(s));
+        build_dag_table(cg, k);
+    }
+    TW_CUDA(cudaMemcpyAsync(cg->d_remaining, cg->d_npred, sizeof(int) * cg->dag_ntasks,
+                            cudaMemcpyDeviceToDevice, s));
+    TW_CUDA(cudaMemsetAsync(cg->d_chunk_done, 0, sizeof(unsigned) * cg->dag_ntasks, s));
+    TW_CUDA(cudaMemsetAsync(cg->d_ticket, 0, sizeof(unsigned), s));
+    DagParams P{};
+    P.tasks = cg->d_tasks;
+    P.chunk_task = cg->d_chunk_task;
+    P.succ = cg->d_succ;
+    P.remaining = cg->d_remaining;
+    P.chunk_done = cg->d_chunk_done;
+    P.chunk_part = cg->d_chunk_part;
+    P.ticket = cg->d_ticket;
+    P.nchunks = cg->dag_nchunks;
+    P.T = cg->T;
+    P.A = cg->view();
+    P.p_local = cg->p_local;
+    P.p_owned = cg->p_owned;
+    P.x = cg->x;
+    P.r = cg->r;
+    P.Ap = cg->Ap;
+    P.sc = cg->sc;
+    P.history = cg->history;
+    P.stamps = cg->d_stamps;
+    P.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
+    P.pa = cg->pa;
+    P.rr = cg->rrp;
+    P.spmv_chunk_slices = 8 * dag_threads() / 32;
+    P.vec_chunk_rows = 32768;
+    dag_smem_bytes(cg->A->info.max_width, &P.stage_bytes, &P.val_bytes);
+    // stamps[0] is the start of the first launch after set_rhs; later launches
+    // write their start into a spare slot so iteration ends stay in place
+    launch_dag(P, cg->ctx->sm_count, s);
+}
+
 void iterate(tw_cg* cg, int k) {
     if (k < 0) config_error("negative iteration count");
     if (cg->enqueued + k > cg->max_iters)
@@ -693,6 +845,16 @@ void iterate(tw_cg* cg, int k) {
     if (k == 0) return;
     TW_CUDA(cudaSetDevice(cg->ctx->device));
     cudaStream_t s = cg->ctx->compute;
+    if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
+        enqueue_persistent(cg, k);
+        if (cg->opt.iteration_marks) {
+            cudaEvent_t e = cg->ta->take_event();
+            TW_CUDA(cudaEventRecord(e, s));
+            cg->ta->bind(e, &cg->marks[static_cast<size_t>(cg->enqueued + k - 1)], cg->t0);
+        }
+        cg->enqueued += k;
+        return;
+    }
     if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     const bool tasks = cg->opt.variant == TW_CG_TASKS;
     if (!cg->opt.use_graph && tasks) fork_streams(cg);
@@ -745,6 +907,7 @@ void tw_cg_options_default(tw_cg_options* o) {
     o->use_graph = 0;
     o->iteration_marks = 1;
     o->tol = 0.0;
+    o->dispatch = TW_DISPATCH_STREAMS;
 }
 
 int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max_iterations,
@@ -831,6 +994,13 @@ int tw_cg_iteration_times(tw_cg* cg, double* seconds, int count) {
         if (!cg->opt.iteration_marks) config_error("iteration times need iteration_marks");
         if (count < 0 || count > cg->enqueued) contract_error("count beyond iterations run");
         wait_cg(cg);
+        if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
+            std::vector<unsigned long long> st(static_cast<size_t>(count) + 1);
+            TW_CUDA(cudaMemcpy(st.data(), cg->d_stamps, sizeof(unsigned long long) * (count + 1),
+                               cudaMemcpyDeviceToHost));
+            for (int i = 0; i < count; ++i) seconds[i] = static_cast<double>(st[i + 1] - st[i]) * 1e-9;
+            return;
+        }
         for (int i = 0; i < count; ++i) {
             float ms = 0.f;
             TW_CUDA(cudaEventElapsedTime(&ms, cg->iter_ev[static_cast<size_t>(i)],

@@ -1,0 +1,213 @@
+// Device helpers shared by the kernel translation units (tw_kernels.cu,
+// tw_dag.cu): fixed-order reductions, the finalize step of the scalar
+// state, mbarrier / TMA bulk-copy wrappers and the per-row SpMV bodies.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tw_internal.h"
+
+namespace tw {
+namespace dev {
+
+constexpr int kThreads = 256;
+#ifndef TW_TMA_WARPS
+#define TW_TMA_WARPS 18
+#endif
+#ifndef TW_TMA_STAGES
+#define TW_TMA_STAGES 1
+#endif
+constexpr int kTmaWarps = TW_TMA_WARPS;   // consumer warps per CTA (one CTA per SM)
+constexpr int kTmaStages = TW_TMA_STAGES; // shared-memory stages per warp
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide fixed-order sum; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* smem) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) smem[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int w = 0; w < nw; ++w) t = __dadd_rn(t, smem[w]);
+    }
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ void finalize(const Fin& fin, double total) {
+    switch (fin.mode) {
+    case FIN_STORE:
+        *fin.out = total;
+        break;
+    case FIN_ALPHA:
+        fin.sc->pAp = total;
+        fin.sc->alpha = __ddiv_rn(fin.sc->rtrans, total);
+        break;
+    case FIN_BETA: {
+        CgScalars* sc = fin.sc;
+        sc->rr = total;
+        sc->beta = __ddiv_rn(total, sc->rtrans);
+        sc->rtrans = total;
+        if (sc->iter < sc->history_cap) fin.history[sc->iter] = __dsqrt_rn(total);
+        sc->iter = sc->iter + 1;
+        break;
+    }
+    case FIN_RTRANS:
+        fin.sc->rtrans = total;
+        fin.sc->iter = 0;
+        break;
+    default:
+        break;
+    }
+}
+
+// Grid-wide fixed-order reduction finished by the last block to arrive.
+__device__ __forceinline__ void grid_reduce_finalize(double v, RedScratch rs, const Fin& fin) {
+    __shared__ double smem[32];
+    __shared__ bool last;
+    double b = block_sum(v, smem);
+    if (threadIdx.x == 0) {
+        rs.block_part[blockIdx.x] = b;
+        __threadfence();
+        unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+        acc = __dadd_rn(acc, __ldcg(rs.block_part + i));
+    double total = block_sum(acc, smem);
+    if (threadIdx.x == 0) finalize(fin, total);
+}
+
+__device__ __forceinline__ double sum_parts(const double* parts, int count) {
+    double t = 0.0;
+    for (int i = 0; i < count; ++i) t = __dadd_rn(t, __ldcg(parts + i));
+    return t;
+}
+
+// ----------------------------------------------- K1 with TMA-staged matrix
+
+// The matrix stream (12 B per nonzero, 95% of K1's bytes) is moved by the
+// Tensor Memory Accelerator: every warp owns a ring of S shared-memory
+// stages and keeps S slice blocks (values + columns, contiguous in HBM) in
+// flight with cp.async.bulk, completing on a per-stage mbarrier.  The warp
+// computes slice k from shared memory while slices k+1..k+S-1 stream in, so
+// DRAM sees deep memory-level parallelism regardless of the gather latency
+// of x (which stays on the L1/L2 path with __ldg).  The matrix copies carry
+// an L2 evict-first policy so the p planes being gathered stay L2-resident.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+// One row of a width-W slice block resident in shared memory: columns first,
+// then every gather issued before any use, then the reference's ordered sum.
+// Gather of x: the read-only path when x is constant for the whole kernel
+// (NC), else a plain coherent L1-cached load (the DAG dispatcher, where p is
+// rewritten inside the same kernel between dependent tasks).
+template <bool NC>
+__device__ __forceinline__ double gather(const double* x, int c) {
+    if (NC) return __ldg(x + c);
+    double v;
+    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(x + c) : "memory");
+    return v;
+}
+
+template <int W, bool NC = true>
+__device__ __forceinline__ double smem_row_fixed(const double* vb, const int32_t* cb,
+                                                 const double* x, int lane) {
+    int c[W];
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+        int4 t = reinterpret_cast<const int4*>(cb + 128 * q)[lane];
+        c[4 * q] = t.x;
+        c[4 * q + 1] = t.y;
+        c[4 * q + 2] = t.z;
+        c[4 * q + 3] = t.w;
+    }
+    constexpr int F = W & ~3;
+    if (W - F >= 2) {
+        int2 t = reinterpret_cast<const int2*>(cb + 32 * F)[lane];
+        c[F] = t.x;
+        c[F + 1] = t.y;
+    }
+    if ((W - F) & 1) c[W - 1] = cb[32 * (W - 1) + lane];
+    double xv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) xv[k] = gather<NC>(x, max(c[k], 0)); // branch-free: padding loads x[0], masked below
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
+        if (c[2 * j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v.x, xv[2 * j]));
+        if (c[2 * j + 1] >= 0) acc = __dadd_rn(acc, __dmul_rn(v.y, xv[2 * j + 1]));
+    }
+    if (W & 1)
+        if (c[W - 1] >= 0) acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane], xv[W - 1]));
+    return acc;
+}
+
+template <bool NC = true>
+__device__ __forceinline__ double smem_row_generic(const double* vb, const int32_t* cb,
+                                                   const double* x, int lane, int w) {
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+        const int c = cb[ell_col_pos(k, lane, w)];
+        if (c < 0) break;
+        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], gather<NC>(x, c)));
+    }
+    return acc;
+}
+
+} // namespace dev
+} // namespace tw

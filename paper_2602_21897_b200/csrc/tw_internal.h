@@ -163,6 +163,51 @@ void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* m
 
 int spmv_tma_smem_bytes(int max_width);
 
+// ------------------------------------------------- persistent DAG dispatcher
+
+enum DagKind : int { DK_SPMV = 0, DK_ALPHA = 1, DK_UPD = 2, DK_BETA = 3, DK_UPDP = 4 };
+
+// One physical task of the flattened K-iteration DAG (tw_dag.cu).
+struct DagTask {
+    int kind;
+    int tile;
+    int64_t r0, r1;   // local rows of the tile
+    int chunk0;       // first index in the global chunk list
+    int nchunks;
+    int succ0, nsucc; // successor task ids in DagParams::succ
+};
+
+struct DagParams {
+    const DagTask* tasks;
+    const int* chunk_task;   // chunk -> task
+    const int* succ;
+    int* remaining;          // unfinished predecessors per task
+    unsigned* chunk_done;    // finished chunks per task
+    double* chunk_part;      // per-chunk dot partial
+    unsigned* ticket;        // next chunk to hand out
+    int nchunks;
+    int T;                   // tiles per iteration
+    EllView A;
+    const double* p_local;   // gathered (owned + ghost planes)
+    double* p_owned;
+    double* x;
+    double* r;
+    double* Ap;
+    CgScalars* sc;
+    double* history;
+    unsigned long long* stamps; // globaltimer at each iteration end (index iter + 1)
+    unsigned long long* start_stamp; // globaltimer when chunk 0 is taken
+    double* pa;              // tile partials of p.Ap
+    double* rr;              // tile partials of r.r
+    int64_t spmv_chunk_slices;
+    int64_t vec_chunk_rows;
+    int stage_bytes, val_bytes;
+};
+
+int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes);
+int dag_threads();
+void launch_dag(const DagParams& P, int blocks, cudaStream_t s);
+
 // Occupancy-derived launch configuration for this device.
 LaunchCfg query_launch_cfg(int sm_count);
 

@@ -427,6 +427,7 @@ class CgOptions:
     iteration_marks: bool = True
     tol: float = 0.0
     use_graph: bool = False
+    persistent: bool = False  # tasks variant: one persistent kernel runs the whole DAG
 
     def to_c(self, variant: int) -> N.CgOptionsC:
         if self.backend != CgBackend.cuda:
@@ -438,6 +439,7 @@ class CgOptions:
         o.use_graph = 1 if self.use_graph else 0
         o.iteration_marks = 1 if self.iteration_marks else 0
         o.tol = float(self.tol)
+        o.dispatch = N.TW_DISPATCH_PERSISTENT if self.persistent else N.TW_DISPATCH_STREAMS
         return o
 
 

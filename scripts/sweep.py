@@ -22,10 +22,10 @@ import torch  # noqa: E402
 import paper_2602_21897_b200 as P  # noqa: E402
 
 
-def measure(rt, A, variant, tiles, graph, K, W):
+def measure(rt, A, variant, tiles, graph, K, W, persistent=False):
     s = torch.cuda.ExternalStream(rt.compute_stream)
-    S = P.CgSolver(rt, A, W + K, P.CgOptions(tiles=tiles, use_graph=graph, iteration_marks=False),
-                   variant=variant)
+    S = P.CgSolver(rt, A, W + K, P.CgOptions(tiles=tiles, use_graph=graph, iteration_marks=False,
+                                             persistent=persistent), variant=variant)
     S.set_rhs(P.rhs_xorshift(rt, A.n, 7))
     t_enq0 = time.perf_counter()
     S.iterate(W)
@@ -66,6 +66,10 @@ def main():
                 print(json.dumps({"config": "C2 HPCCG 128^3 1xB200",
                                   "variant": "monolithic" if variant == 0 else "tasks",
                                   "tiles": tiles, "cuda_graph": graph, **r}), flush=True)
+            if variant == 1:
+                r = measure(rt, A, 1, tiles, False, 100, 10, persistent=True)
+                print(json.dumps({"config": "C2 HPCCG 128^3 1xB200", "variant": "tasks",
+                                  "tiles": tiles, "dispatch": "persistent", **r}), flush=True)
         del A
     if "c5" in cfgs:
         A = P.gen_stencil_matrix(256, 256, 256, rt=rt)
@@ -75,6 +79,10 @@ def main():
                 print(json.dumps({"config": "C5 HPCCG 256^3 granularity, per-GPU tiles",
                                   "blocks_total_8gpu_equiv": tiles * 8, "tiles": tiles,
                                   "cuda_graph": graph, **r}), flush=True)
+            r = measure(rt, A, 1, tiles, False, a.K, a.W, persistent=True)
+            print(json.dumps({"config": "C5 HPCCG 256^3 granularity, per-GPU tiles",
+                              "blocks_total_8gpu_equiv": tiles * 8, "tiles": tiles,
+                              "dispatch": "persistent", **r}), flush=True)
         r = measure(rt, A, 0, 1, True, a.K, a.W)
         print(json.dumps({"config": "C5 HPCCG 256^3 monolithic reference point", "tiles": 1,
                           "cuda_graph": True, **r}), flush=True)

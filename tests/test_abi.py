@@ -23,14 +23,14 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_struct_layout():
     lib = N.load()
-    assert lib.tw_abi_version() == 1
+    assert lib.tw_abi_version() == 2
     assert C.sizeof(N.EllInfo) == 13 * 8 + 2 * 4
-    assert C.sizeof(N.CgOptionsC) == 4 * 5 + 4 + 8  # 5 ints + pad + double
+    assert C.sizeof(N.CgOptionsC) == 4 * 5 + 4 + 8 + 8  # 5 ints + pad + double + int + pad
     o = N.CgOptionsC()
     lib.tw_cg_options_default(C.byref(o))
     # CgOptions defaults (cg.hpp:37-45): tiles 16, stream pool 4, marks on, tol 0
-    assert (o.variant, o.tiles, o.stream_pool_capacity, o.iteration_marks, o.tol) == \
-        (N.TW_CG_TASKS, 16, 4, 1, 0.0)
+    assert (o.variant, o.tiles, o.stream_pool_capacity, o.iteration_marks, o.tol, o.dispatch) == \
+        (N.TW_CG_TASKS, 16, 4, 1, 0.0, N.TW_DISPATCH_STREAMS)
 
 
 def test_exports_are_plain_c():

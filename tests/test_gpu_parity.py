@@ -345,3 +345,42 @@ def test_scenario_run_point_csv(rt, orc, golden):
         check_history(p.residual_history, golden["cg_32_splitmix7_history"][:20])
     text = S.metrics_to_csv(pts)
     assert S.parse_metrics_csv(text) == [r for p in pts for r in p.rows]
+
+
+# ------------------------------------------------ persistent DAG dispatcher
+
+@pytest.mark.parametrize("T", [1, 4, 16, 64])
+def test_persistent_dispatcher_vs_reference(rt, orc, golden, T):
+    A = P.gen_stencil_matrix(32, 32, 32, rt=rt)
+    b = orc.rhs_xorshift(A.n, 7)
+    r1 = P.cg_tasks(rt, A, b, 150, P.CgOptions(tiles=T, persistent=True))
+    check_history(r1.residual_history, golden["cg_32_xorshift7_history"])
+    assert np.all(rel_gap(r1.x, golden["cg_32_xorshift7_x"]) <= 1e-10)
+    if "cgtasks_32_T%d_history" % T in golden:
+        check_history(r1.residual_history[:50], golden["cgtasks_32_T%d_history" % T])
+    r2 = P.cg_tasks(rt, A, b, 150, P.CgOptions(tiles=T, persistent=True))
+    assert np.array_equal(r1.residual_history, r2.residual_history)  # deterministic
+    assert np.array_equal(r1.x, r2.x)
+
+
+def test_persistent_dispatcher_pieces_times_and_rejects(rt, orc):
+    A = P.gen_stencil_matrix(40, 36, 30, rt=rt)
+    b = orc.rhs_splitmix(A.n, 5)
+    s = P.CgSolver(rt, A, 30, P.CgOptions(tiles=6, persistent=True))
+    s.set_rhs(b)
+    s.iterate(7)
+    s.iterate(23)
+    h, x = s.history(30), s.solution()
+    t = s.iteration_times(30)
+    assert np.all(t > 0) and np.all(t < 1.0)
+    s.set_rhs(b)
+    s.iterate(30)
+    assert np.array_equal(h, s.history(30)) and np.array_equal(x, s.solution())
+    s.close()
+    m = orc.stencil(40, 36, 30)
+    want, _, _ = orc.cg(m, b, 30, tiles=6)
+    check_history(h, want)
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 5, P.CgOptions(tiles=1, persistent=True), variant=0)
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 5, P.CgOptions(tiles=4, persistent=True, use_graph=True))
