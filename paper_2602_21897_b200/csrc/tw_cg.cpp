@@ -169,15 +169,20 @@ struct tw_cg {
     std::vector<cudaEvent_t> tev;
     int timed = 0;
     std::vector<cudaEvent_t> iter_ev; // iteration-end timing events (marks on)
-    // persistent dispatcher (TW_DISPATCH_PERSISTENT): flattened K-iteration DAG
-    int dag_k = -1, dag_ntasks = 0, dag_nchunks = 0;
-    DagTask* d_tasks = nullptr;
-    int* d_chunk_task = nullptr;
-    int* d_succ = nullptr;
-    int* d_npred = nullptr;
-    int* d_remaining = nullptr;
-    unsigned* d_chunk_done = nullptr;
-    double* d_chunk_part = nullptr;
+    // persistent dispatcher (TW_DISPATCH_PERSISTENT): flattened K-iteration
+    // DAG tables, cached per K
+    struct DagTable {
+        int ntasks = 0, nchunks = 0;
+        DagTask* d_tasks = nullptr;
+        int* d_chunk_task = nullptr;
+        int* d_succ = nullptr;
+        int* d_npred = nullptr;
+        int* d_remaining = nullptr;
+        unsigned* d_chunk_done = nullptr;
+        double* d_chunk_part = nullptr;
+    };
+    std::map<int, DagTable> dag_tables;
+    int dag_grid = 0;
     unsigned* d_ticket = nullptr;
     unsigned long long* d_stamps = nullptr;
     double t0 = 0.0;
@@ -559,13 +564,16 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->parts);
     cudaFree(cg->block_parts);
     cudaFree(cg->tickets);
-    cudaFree(cg->d_tasks);
-    cudaFree(cg->d_chunk_task);
-    cudaFree(cg->d_succ);
-    cudaFree(cg->d_npred);
-    cudaFree(cg->d_remaining);
-    cudaFree(cg->d_chunk_done);
-    cudaFree(cg->d_chunk_part);
+    for (auto& kv : cg->dag_tables) {
+        auto& t = kv.second;
+        cudaFree(t.d_tasks);
+        cudaFree(t.d_chunk_task);
+        cudaFree(t.d_succ);
+        cudaFree(t.d_npred);
+        cudaFree(t.d_remaining);
+        cudaFree(t.d_chunk_done);
+        cudaFree(t.d_chunk_part);
+    }
     cudaFree(cg->d_ticket);
     cudaFree(cg->d_stamps);
     delete cg;
@@ -674,6 +682,7 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             TW_CUDA(cudaMalloc(&cg->d_stamps, sizeof(unsigned long long) * (max_iters + 2)));
             TW_CUDA(cudaMemset(cg->d_stamps, 0, sizeof(unsigned long long) * (max_iters + 2)));
             TW_CUDA(cudaMalloc(&cg->d_ticket, sizeof(unsigned) * 4));
+            cg->dag_grid = dag_blocks(A->info.max_width, ctx->sm_count);
         }
     } catch (...) {
         free_cg(cg);
@@ -725,10 +734,13 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
 
 // Flattens k iterations of the physical DAG into the dispatcher's task table
 // (topological order, chunk list, successor lists, predecessor counts).
+constexpr int64_t kDagVecChunkRows = 16384; // rows per update chunk
+int64_t dag_spmv_chunk_slices() { return 8 * dag_threads() / 32; } // 8 slices per warp
+
 void build_dag_table(tw_cg* cg, int k) {
     const int L = static_cast<int>(cg->nodes.size());
-    const int64_t spmv_cs = 8 * dag_threads() / 32; // slices per SpMV chunk (8 per warp)
-    const int64_t vec_cr = 32768;                  // rows per update chunk
+    const int64_t spmv_cs = dag_spmv_chunk_slices();
+    const int64_t vec_cr = kDagVecChunkRows;
     std::vector<DagTask> tasks(static_cast<size_t>(k) * L);
     std::vector<std::vector<int>> succ(tasks.size());
     std::vector<int> npred(tasks.size(), 0), chunk_task;
@@ -780,43 +792,44 @@ void build_dag_table(tw_cg* cg, int k) {
         p = nullptr;
         TW_CUDA(cudaMalloc(&p, sizeof(*p) * std::max<size_t>(n, 1)));
     };
-    realloc(cg->d_tasks, tasks.size());
-    realloc(cg->d_chunk_task, chunk_task.size());
-    realloc(cg->d_succ, flat.size());
-    realloc(cg->d_npred, npred.size());
-    realloc(cg->d_remaining, npred.size());
-    realloc(cg->d_chunk_done, tasks.size());
-    realloc(cg->d_chunk_part, chunk_task.size());
-    TW_CUDA(cudaMemcpy(cg->d_tasks, tasks.data(), sizeof(DagTask) * tasks.size(), cudaMemcpyHostToDevice));
-    TW_CUDA(cudaMemcpy(cg->d_chunk_task, chunk_task.data(), sizeof(int) * chunk_task.size(),
+    tw_cg::DagTable& tb = cg->dag_tables[k];
+    realloc(tb.d_tasks, tasks.size());
+    realloc(tb.d_chunk_task, chunk_task.size());
+    realloc(tb.d_succ, flat.size());
+    realloc(tb.d_npred, npred.size());
+    realloc(tb.d_remaining, npred.size());
+    realloc(tb.d_chunk_done, tasks.size());
+    realloc(tb.d_chunk_part, chunk_task.size());
+    TW_CUDA(cudaMemcpy(tb.d_tasks, tasks.data(), sizeof(DagTask) * tasks.size(), cudaMemcpyHostToDevice));
+    TW_CUDA(cudaMemcpy(tb.d_chunk_task, chunk_task.data(), sizeof(int) * chunk_task.size(),
                        cudaMemcpyHostToDevice));
-    TW_CUDA(cudaMemcpy(cg->d_succ, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
-    TW_CUDA(cudaMemcpy(cg->d_npred, npred.data(), sizeof(int) * npred.size(), cudaMemcpyHostToDevice));
-    cg->dag_k = k;
-    cg->dag_ntasks = static_cast<int>(tasks.size());
-    cg->dag_nchunks = static_cast<int>(chunk_task.size());
+    TW_CUDA(cudaMemcpy(tb.d_succ, flat.data(), sizeof(int) * flat.size(), cudaMemcpyHostToDevice));
+    TW_CUDA(cudaMemcpy(tb.d_npred, npred.data(), sizeof(int) * npred.size(), cudaMemcpyHostToDevice));
+    tb.ntasks = static_cast<int>(tasks.size());
+    tb.nchunks = static_cast<int>(chunk_task.size());
 }
 
 // k iterations of cg_tasks as ONE persistent kernel (tw_dag.cu).
 void enqueue_persistent(tw_cg* cg, int k) {
     cudaStream_t s = cg->ctx->compute;
-    if (cg->dag_k != k) {
+    if (!cg->dag_tables.count(k)) {
         TW_CUDA(cudaStreamSynchronize(s));
         build_dag_table(cg, k);
     }
-    TW_CUDA(cudaMemcpyAsync(cg->d_remaining, cg->d_npred, sizeof(int) * cg->dag_ntasks,
+    const tw_cg::DagTable& tb = cg->dag_tables[k];
+    TW_CUDA(cudaMemcpyAsync(tb.d_remaining, tb.d_npred, sizeof(int) * tb.ntasks,
                             cudaMemcpyDeviceToDevice, s));
-    TW_CUDA(cudaMemsetAsync(cg->d_chunk_done, 0, sizeof(unsigned) * cg->dag_ntasks, s));
+    TW_CUDA(cudaMemsetAsync(tb.d_chunk_done, 0, sizeof(unsigned) * tb.ntasks, s));
     TW_CUDA(cudaMemsetAsync(cg->d_ticket, 0, sizeof(unsigned), s));
     DagParams P{};
-    P.tasks = cg->d_tasks;
-    P.chunk_task = cg->d_chunk_task;
-    P.succ = cg->d_succ;
-    P.remaining = cg->d_remaining;
-    P.chunk_done = cg->d_chunk_done;
-    P.chunk_part = cg->d_chunk_part;
+    P.tasks = tb.d_tasks;
+    P.chunk_task = tb.d_chunk_task;
+    P.succ = tb.d_succ;
+    P.remaining = tb.d_remaining;
+    P.chunk_done = tb.d_chunk_done;
+    P.chunk_part = tb.d_chunk_part;
     P.ticket = cg->d_ticket;
-    P.nchunks = cg->dag_nchunks;
+    P.nchunks = tb.nchunks;
     P.T = cg->T;
     P.A = cg->view();
     P.p_local = cg->p_local;
@@ -830,12 +843,12 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
     P.pa = cg->pa;
     P.rr = cg->rrp;
-    P.spmv_chunk_slices = 8 * dag_threads() / 32;
-    P.vec_chunk_rows = 32768;
+    P.spmv_chunk_slices = dag_spmv_chunk_slices();
+    P.vec_chunk_rows = kDagVecChunkRows;
     dag_smem_bytes(cg->A->info.max_width, &P.stage_bytes, &P.val_bytes);
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
-    launch_dag(P, cg->ctx->sm_count, s);
+    launch_dag(P, cg->dag_grid, s);
 }
 
 void iterate(tw_cg* cg, int k) {
@@ -1095,7 +1108,9 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
         int k = 0, c = 0;
-        if (cg->opt.variant == TW_CG_MONOLITHIC) {
+        if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
+            k = 0; // one launch per tw_cg_iterate call, whatever its iteration count
+        } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
             k = cg->P == 1 ? 3 : 5;
             c = cg->P == 1 ? 0 : 3;
         } else {

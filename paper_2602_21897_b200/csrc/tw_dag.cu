@@ -40,6 +40,14 @@ namespace {
 
 using namespace dev;
 
+#ifndef TW_DAG_WARPS
+#define TW_DAG_WARPS 9
+#endif
+// Warps per dispatcher CTA.  Several CTAs share an SM so the chunk-boundary
+// bookkeeping of one (ticket, dependency acquire, completion atomics) runs
+// while the others stream.
+constexpr int kDagWarps = TW_DAG_WARPS;
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -52,10 +60,10 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__global__ void __launch_bounds__(kTmaWarps * 32, 1) dag_kernel(DagParams P) {
+__global__ void __launch_bounds__(kDagWarps * 32, 2) dag_kernel(DagParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[kTmaWarps];
-    __shared__ int stage_w[kTmaWarps];
+    __shared__ uint64_t bars[kDagWarps];
+    __shared__ int stage_w[kDagWarps];
     __shared__ int s_chunk;
     __shared__ int s_last;
     __shared__ double red[32];
@@ -89,7 +97,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) dag_kernel(DagParams P) {
             const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
             int64_t s_hi = s_lo + P.spmv_chunk_slices;
             if (s_hi > s_end) s_hi = s_end;
-            for (int64_t s = s_lo + warp; s < s_hi; s += kTmaWarps) {
+            for (int64_t s = s_lo + warp; s < s_hi; s += kDagWarps) {
                 if (lane == 0) {
                     const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
                     const uint32_t ents = static_cast<uint32_t>(end - off);
@@ -127,12 +135,33 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) dag_kernel(DagParams P) {
             const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
             int64_t b = a + P.vec_chunk_rows;
             if (b > T.r1) b = T.r1;
-            for (int64_t i = a + tid; i < b; i += blockDim.x) {
-                const double xv = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
-                const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
-                P.x[i] = xv;
-                P.r[i] = rv;
-                part = __dadd_rn(part, __dmul_rn(rv, rv));
+            // pairs (2i, 2i+1) fully inside [a, b) use 128-bit accesses
+            const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
+            for (int64_t q = q0 + tid; q < q1; q += blockDim.x) {
+                const int64_t e = 2 * q;
+                double2 xv = *reinterpret_cast<const double2*>(P.x + e);
+                const double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
+                double2 rv = *reinterpret_cast<const double2*>(P.r + e);
+                const double2 av = *reinterpret_cast<const double2*>(P.Ap + e);
+                xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+                xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+                rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+                rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+                *reinterpret_cast<double2*>(P.x + e) = xv;
+                *reinterpret_cast<double2*>(P.r + e) = rv;
+                part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+                part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+            }
+            if (tid < 2) { // ragged ends
+                const int64_t i = tid == 0 ? a : b - 1;
+                const bool mine = tid == 0 ? (a & 1) != 0 : ((b & 1) != 0 && b - 1 >= a && !((a & 1) && b - 1 == a));
+                if (mine && i < b) {
+                    const double xv = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
+                    const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
+                    P.x[i] = xv;
+                    P.r[i] = rv;
+                    part = __dadd_rn(part, __dmul_rn(rv, rv));
+                }
             }
             break;
         }
@@ -141,8 +170,20 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1) dag_kernel(DagParams P) {
             const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
             int64_t b = a + P.vec_chunk_rows;
             if (b > T.r1) b = T.r1;
-            for (int64_t i = a + tid; i < b; i += blockDim.x)
-                P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
+            const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
+            for (int64_t q = q0 + tid; q < q1; q += blockDim.x) {
+                const int64_t e = 2 * q;
+                const double2 rv = *reinterpret_cast<const double2*>(P.r + e);
+                double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
+                pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+                pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+                *reinterpret_cast<double2*>(P.p_owned + e) = pv;
+            }
+            if (tid < 2) {
+                const int64_t i = tid == 0 ? a : b - 1;
+                const bool mine = tid == 0 ? (a & 1) != 0 : ((b & 1) != 0 && b - 1 >= a && !((a & 1) && b - 1 == a));
+                if (mine && i < b) P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
+            }
             break;
         }
         case DK_ALPHA:
@@ -210,20 +251,27 @@ int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes) {
     const int cb = ((32 * max_width * 4) + 127) / 128 * 128;
     *val_bytes = vb;
     *stage_bytes = vb + cb;
-    return kTmaWarps * (vb + cb);
+    return kDagWarps * (vb + cb);
 }
 
-int dag_threads() { return kTmaWarps * 32; }
+int dag_threads() { return kDagWarps * 32; }
+
+// Grid = every dispatcher CTA the device can hold at once (all CTAs must be
+// co-resident: a CTA may wait on chunks other CTAs hold).
+int dag_blocks(int max_width, int sm_count) {
+    int stage, vb;
+    const int smem = dag_smem_bytes(max_width, &stage, &vb);
+    TW_CUDA(cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0;
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, kDagWarps * 32, smem));
+    if (per_sm < 1) config_error("dispatcher CTA does not fit on an SM");
+    return per_sm * sm_count;
+}
 
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s) {
     int stage, vb;
     const int smem = dag_smem_bytes(P.A.max_width, &stage, &vb);
-    static int attr = 0;
-    if (attr < smem) {
-        TW_CUDA(cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = smem;
-    }
-    dag_kernel<<<blocks, kTmaWarps * 32, smem, s>>>(P);
+    dag_kernel<<<blocks, kDagWarps * 32, smem, s>>>(P);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -158,9 +158,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 template <bool NC>
 __device__ __forceinline__ double gather(const double* x, int c) {
     if (NC) return __ldg(x + c);
-    double v;
-    asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(x + c) : "memory");
-    return v;
+    return __ldca(x + c); // ld.global.ca: L1-cached, coherent after the acquire + L1 invalidate
 }
 
 template <int W, bool NC = true>
