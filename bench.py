@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--e2e-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", action="store_true",
+                    help="attach an NCCL communicator even at N=1 (exercises the multi-GPU path)")
     ap.add_argument("--cpu-sample-nz", type=int, default=64)
     ap.add_argument("--cpu-sample-iters", type=int, default=10)
     return ap.parse_args()
@@ -256,6 +258,8 @@ def run_ours(args, dist, rank, world, local):
         obj = [P.Runtime.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         rt.init_comm(rank, world, obj[0])
+    elif args.comm:
+        rt.init_comm(0, 1, P.Runtime.comm_unique_id())
     A = P.gen_stencil_matrix(nx, ny, nz, rt=rt, z_begin=zb, z_end=ze)
     n, nnz = A.n, A.nnz()
     assert (n, nnz) == work(nx, ny, zb, ze, nz)
@@ -381,7 +385,8 @@ def run_ours(args, dist, rank, world, local):
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
                        "l2": "inputs larger than L2 (6.9 GB/iteration vs 126 MB)",
-                       "parallelism": f"z-slab x{world}"},
+                       "parallelism": f"z-slab x{world}",
+                       "nccl_comm": world > 1 or args.comm},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,

@@ -133,6 +133,7 @@ struct tw_cg {
     int max_iters = 0;
     int T = 1;
     int P = 1;
+    bool dist = false; // communicator attached: halo + rank-ordered allgathers
     int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
     bool glo = false, ghi = false;
     tw_slab_t slab{}; // z-slab geometry (multi-rank)
@@ -161,6 +162,7 @@ struct tw_cg {
     std::vector<cudaEvent_t> ev[2];              // per node, by iteration parity
     std::vector<cudaEvent_t> tail_ev;            // per pool stream + comm
     cudaEvent_t fork_ev = nullptr, halo_ev = nullptr, pready_ev = nullptr;
+    cudaEvent_t ag_in_ev = nullptr, ag_out_ev = nullptr;
 
     cudaGraphExec_t graph = nullptr;
     int enqueued = 0;
@@ -347,8 +349,16 @@ int launch_blocks(const tw_cg* cg, bool spmv) {
     return spmv ? cg->ctx->cfg.spmv_blocks : cg->ctx->cfg.stream_blocks;
 }
 
+// Every NCCL call of the communicator is issued on the one comm stream, so
+// the halo and the scalar allgathers are strictly ordered there; the caller's
+// stream is joined in and out with events.
 void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s) {
-    TW_NCCL(nccl().AllGather(send, recv, 1, ncclDouble, cg->ctx->nccl_comm, s));
+    cudaStream_t c = cg->ctx->comm;
+    TW_CUDA(cudaEventRecord(cg->ag_in_ev, s));
+    TW_CUDA(cudaStreamWaitEvent(c, cg->ag_in_ev, 0));
+    TW_NCCL(nccl().AllGather(send, recv, 1, ncclDouble, cg->ctx->nccl_comm, c));
+    TW_CUDA(cudaEventRecord(cg->ag_out_ev, c));
+    TW_CUDA(cudaStreamWaitEvent(s, cg->ag_out_ev, 0));
 }
 
 void halo_exchange(tw_cg* cg, cudaStream_t s) {
@@ -393,7 +403,7 @@ void enqueue_mono(tw_cg* cg) {
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
-    if (cg->P == 1) {
+    if (!cg->dist) {
         record(tmark(cg, 0), s);
         launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs,
                     Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, bs, s);
@@ -446,7 +456,7 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
                     cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
         break;
     case PK_ALPHA:
-        if (cg->P == 1) {
+        if (!cg->dist) {
             launch_combine(cg->pa, cg->T, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
         } else {
             launch_combine(cg->pa, cg->T, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, st);
@@ -460,7 +470,7 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
                          Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}, bv, st);
         break;
     case PK_BETA:
-        if (cg->P == 1) {
+        if (!cg->dist) {
             launch_combine(cg->rrp, cg->T, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
         } else {
             launch_combine(cg->rrp, cg->T, Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, st);
@@ -555,6 +565,8 @@ void free_cg(tw_cg* cg) {
     if (cg->fork_ev) cudaEventDestroy(cg->fork_ev);
     if (cg->halo_ev) cudaEventDestroy(cg->halo_ev);
     if (cg->pready_ev) cudaEventDestroy(cg->pready_ev);
+    if (cg->ag_in_ev) cudaEventDestroy(cg->ag_in_ev);
+    if (cg->ag_out_ev) cudaEventDestroy(cg->ag_out_ev);
     cudaFree(cg->x);
     cudaFree(cg->r);
     cudaFree(cg->p_base);
@@ -594,8 +606,9 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             if (cg->opt.variant != TW_CG_TASKS)
                 config_error("the persistent dispatcher runs the tasks variant");
-            if (ctx->nranks > 1)
-                config_error("the persistent dispatcher runs on one rank (halo needs NCCL launches)");
+            if (ctx->nccl_comm)
+                config_error("the persistent dispatcher runs without a communicator (halo and "
+                             "allgathers are NCCL launches)");
             int sb, vb;
             if (dag_smem_bytes(A->info.max_width, &sb, &vb) > 200 * 1024)
                 config_error("matrix rows too wide for the dispatcher's shared-memory stages");
@@ -607,12 +620,13 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             config_error("unknown CG variant");
         cg->T = cg->opt.variant == TW_CG_MONOLITHIC ? 1 : cg->opt.tiles; // cg.cpp:400
         cg->P = ctx->nranks;
+        cg->dist = ctx->nccl_comm != nullptr; // rank-partial path (also for a 1-rank comm)
         cg->max_iters = max_iters;
         const tw_ell_info_t& in = A->info;
         cg->n = in.n_rows;
         cg->x_len = in.x_len;
         cg->diag_shift = A->diag_shift;
-        if (cg->P > 1) {
+        if (cg->dist) {
             if (in.nx == 0) config_error("multi-GPU CG needs a stencil slab (tw_gen_stencil_ell)");
             cg->plane = in.nx * in.ny;
             cg->glo = in.z_begin > 0;
@@ -623,12 +637,13 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
                 throw Error(rc, g_last_error);
             if (cg->slab.diag_shift != cg->diag_shift || cg->slab.x_len != cg->x_len)
                 contract_error("matrix and slab plan disagree");
-            if (!ctx->nccl_comm) contract_error("multi-rank context without communicator");
+        } else if (cg->P > 1) {
+            contract_error("multi-rank context without communicator");
         } else if (in.z_begin > 0 || (in.nx && in.z_end < in.nz)) {
             contract_error("a partial slab needs a multi-rank context");
         }
         tile_plan(A, cg->T, cg->t_r0, cg->t_r1, cg->t_lo, cg->t_hi);
-        cg->dag = DagSpec{cg->T, cg->P > 1, cg->glo, cg->ghi, cg->n, cg->diag_shift, cg->plane,
+        cg->dag = DagSpec{cg->T, cg->dist, cg->glo, cg->ghi, cg->n, cg->diag_shift, cg->plane,
                           cg->t_r0, cg->t_r1, cg->t_lo, cg->t_hi};
         TW_CUDA(cudaSetDevice(ctx->device));
         const size_t n = static_cast<size_t>(cg->n);
@@ -662,6 +677,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaEventCreateWithFlags(&cg->fork_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->halo_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->pready_ev, cudaEventDisableTiming));
+        TW_CUDA(cudaEventCreateWithFlags(&cg->ag_in_ev, cudaEventDisableTiming));
+        TW_CUDA(cudaEventCreateWithFlags(&cg->ag_out_ev, cudaEventDisableTiming));
         for (unsigned i = 0; i <= ctx->pool.capacity(); ++i) {
             cudaEvent_t e;
             TW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -707,7 +724,7 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device) {
     TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, k, s));
     TW_CUDA(cudaMemcpyAsync(cg->p_owned, cg->r, bytes, cudaMemcpyDeviceToDevice, s));
     const RedScratch rs = cg->slot(0);
-    if (cg->P == 1) {
+    if (!cg->dist) {
         launch_dot(cg->r, cg->r, 0, cg->n, rs, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr},
                    ctx->cfg.stream_blocks, s);
     } else {
@@ -1111,11 +1128,11 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             k = 0; // one launch per tw_cg_iterate call, whatever its iteration count
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
-            k = cg->P == 1 ? 3 : 5;
-            c = cg->P == 1 ? 0 : 3;
+            k = cg->dist ? 5 : 3;
+            c = cg->dist ? 3 : 0;
         } else {
-            k = 3 * cg->T + (cg->P == 1 ? 2 : 4);
-            c = cg->P == 1 ? 0 : 3;
+            k = 3 * cg->T + (cg->dist ? 4 : 2);
+            c = cg->dist ? 3 : 0;
         }
         if (kernels) *kernels = k;
         if (collectives) *collectives = c;

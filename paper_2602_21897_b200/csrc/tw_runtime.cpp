@@ -629,7 +629,7 @@ int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[1
         if (ctx->nccl_comm) contract_error("communicator already initialised");
         ctx->rank = rank;
         ctx->nranks = nranks;
-        if (nranks == 1) return;
+        // a 1-rank communicator is allowed: it runs the distributed code path
         ncclUniqueId uid;
         std::memcpy(&uid, id, 128);
         TW_CUDA(cudaSetDevice(ctx->device));

@@ -384,3 +384,29 @@ def test_persistent_dispatcher_pieces_times_and_rejects(rt, orc):
         P.CgSolver(rt, A, 5, P.CgOptions(tiles=1, persistent=True), variant=0)
     with pytest.raises(P.ConfigError):
         P.CgSolver(rt, A, 5, P.CgOptions(tiles=4, persistent=True, use_graph=True))
+
+
+# ------------------------------------------------ distributed code path (1 rank)
+
+def test_distributed_code_path_on_one_rank(orc, golden):
+    """A real 1-rank NCCL communicator drives the multi-GPU code path on the
+    one available B200: NCCL loading and comm init, the halo group on the comm
+    stream, the interior/boundary SpMV split, allgathers of the rank partials
+    (joined through the comm stream), rank-ordered scalar sums inside K2/K3 and
+    K3's last-block commit of rtrans/history."""
+    rt2 = P.Runtime(0)
+    rt2.init_comm(0, 1, P.Runtime.comm_unique_id())
+    assert (rt2.rank, rt2.nranks) == (0, 1)
+    A = P.gen_stencil_matrix(32, 32, 32, rt=rt2)
+    b = orc.rhs_xorshift(A.n, 7)
+    for run, T, graph in [(P.cg_monolithic, 1, False), (P.cg_tasks, 4, False),
+                          (P.cg_monolithic, 1, True)]:
+        res = run(rt2, A, b, 150, P.CgOptions(tiles=T, use_graph=graph))
+        check_history(res.residual_history, golden["cg_32_xorshift7_history"])
+        assert np.all(rel_gap(res.x, golden["cg_32_xorshift7_x"]) <= 1e-10)
+    s = P.CgSolver(rt2, A, 4, P.CgOptions(), variant=0)
+    assert s.launches_per_iteration() == (5, 3)
+    s.close()
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt2, A, 4, P.CgOptions(tiles=4, persistent=True))
+    rt2.close()
