@@ -17,6 +17,7 @@
 // edges between pooled streams (or edges of a captured CUDA graph).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <optional>
@@ -751,13 +752,26 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
 
 // Flattens k iterations of the physical DAG into the dispatcher's task table
 // (topological order, chunk list, successor lists, predecessor counts).
-constexpr int64_t kDagVecChunkRows = 16384; // rows per update chunk
-int64_t dag_spmv_chunk_slices() { return 8 * dag_threads() / 32; } // 8 slices per warp
+// Chunk sizes: small, because the scheduler warp hides the per-chunk
+// bookkeeping and small chunks keep the tail at each alpha / beta barrier
+// short.  TW_DAG_SPMV_SLICES / TW_DAG_VEC_ROWS override (tuning only).
+int64_t env_or(const char* name, int64_t dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoll(v) : dflt;
+}
+int64_t dag_spmv_chunk_slices() {
+    static const int64_t v = env_or("TW_DAG_SPMV_SLICES", 2 * dag_compute_warps());
+    return v;
+}
+int64_t dag_vec_chunk_rows() {
+    static const int64_t v = env_or("TW_DAG_VEC_ROWS", 4096);
+    return v;
+}
 
 void build_dag_table(tw_cg* cg, int k) {
     const int L = static_cast<int>(cg->nodes.size());
     const int64_t spmv_cs = dag_spmv_chunk_slices();
-    const int64_t vec_cr = kDagVecChunkRows;
+    const int64_t vec_cr = dag_vec_chunk_rows();
     std::vector<DagTask> tasks(static_cast<size_t>(k) * L);
     std::vector<std::vector<int>> succ(tasks.size());
     std::vector<int> npred(tasks.size(), 0), chunk_task;
@@ -861,7 +875,7 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.pa = cg->pa;
     P.rr = cg->rrp;
     P.spmv_chunk_slices = dag_spmv_chunk_slices();
-    P.vec_chunk_rows = kDagVecChunkRows;
+    P.vec_chunk_rows = dag_vec_chunk_rows();
     dag_smem_bytes(cg->A->info.max_width, &P.stage_bytes, &P.val_bytes);
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place

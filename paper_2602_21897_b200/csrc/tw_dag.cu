@@ -60,85 +60,82 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__global__ void __launch_bounds__(kDagWarps * 32, 2) dag_kernel(DagParams P) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[kDagWarps];
-    __shared__ int stage_w[kDagWarps];
-    __shared__ int s_chunk;
-    __shared__ int s_last;
-    __shared__ double red[32];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    unsigned char* stage = smem + static_cast<size_t>(warp) * P.stage_bytes;
-    if (lane == 0) mbar_init(&bars[warp], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    const uint64_t pol = l2_evict_first_policy();
-    uint32_t phase = 0; // completed TMA phases of this warp's stage
+// Named barriers of the slot ring (ids 1..4; 0 is __syncthreads).
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
-    for (;;) {
-        if (tid == 0) s_chunk = static_cast<int>(atomicAdd(P.ticket, 1u));
-        __syncthreads();
-        const int c = s_chunk;
-        if (c >= P.nchunks) break;
-        const int tk = P.chunk_task[c];
-        const DagTask T = P.tasks[tk];
-        const int j = c - T.chunk0;
-        if (tid == 0) {
-            if (c == 0) *P.start_stamp = globaltimer();
-            while (ld_acquire(P.remaining + tk) > 0) __nanosleep(64);
-            __threadfence(); // gpu-scope: orders the acquire, drops stale L1 lines
-        }
-        __syncthreads();
+constexpr int kComputeWarps = kDagWarps - 1; // warp kDagWarps-1 schedules
+constexpr int kSlots = 2;
 
-        double part = 0.0;
-        switch (T.kind) {
-        case DK_SPMV: {
-            const int64_t s_first = T.r0 >> 5, s_end = (T.r1 + 31) >> 5;
-            const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
-            int64_t s_hi = s_lo + P.spmv_chunk_slices;
-            if (s_hi > s_end) s_hi = s_end;
-            for (int64_t s = s_lo + warp; s < s_hi; s += kDagWarps) {
-                if (lane == 0) {
-                    const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
-                    const uint32_t ents = static_cast<uint32_t>(end - off);
-                    stage_w[warp] = static_cast<int>(ents >> 5);
-                    mbar_expect_tx(&bars[warp], ents * 12u);
-                    bulk_g2s(stage, P.A.vals + off, ents * 8u, &bars[warp], pol);
-                    bulk_g2s(stage + P.val_bytes, P.A.cols + off, ents * 4u, &bars[warp], pol);
-                }
-                __syncwarp();
-                mbar_wait(&bars[warp], phase & 1u);
-                ++phase;
-                const int w = stage_w[warp];
-                const double* vb = reinterpret_cast<const double*>(stage);
-                const int32_t* cb = reinterpret_cast<const int32_t*>(stage + P.val_bytes);
-                double acc;
-                switch (w) {
-                case 27: acc = smem_row_fixed<27, false>(vb, cb, P.p_local, lane); break;
-                case 18: acc = smem_row_fixed<18, false>(vb, cb, P.p_local, lane); break;
-                case 12: acc = smem_row_fixed<12, false>(vb, cb, P.p_local, lane); break;
-                case 8: acc = smem_row_fixed<8, false>(vb, cb, P.p_local, lane); break;
-                default: acc = smem_row_generic<false>(vb, cb, P.p_local, lane, w); break;
-                }
-                const int64_t row = (s << 5) + lane;
-                if (row >= T.r0 && row < T.r1) {
-                    P.Ap[row] = acc;
-                    part = __dadd_rn(part, __dmul_rn(P.p_owned[row], acc));
-                }
-                __syncwarp();
-                if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+struct Slot {
+    int c;     // chunk index, -1 = no more work
+    int task;
+    int ready; // the scheduler already observed (acquired) zero predecessors
+    DagTask t;
+};
+
+// One chunk on the compute warps; returns this thread's dot partial.
+__device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T, int j, int warp,
+                                            int lane, unsigned char* stage, uint64_t* bar,
+                                            int* stage_w, uint32_t& phase, uint64_t pol) {
+    const int ctid = warp * 32 + lane, cthreads = kComputeWarps * 32;
+    double part = 0.0;
+    switch (T.kind) {
+    case DK_SPMV: {
+        const int64_t s_first = T.r0 >> 5, s_end = (T.r1 + 31) >> 5;
+        const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
+        int64_t s_hi = s_lo + P.spmv_chunk_slices;
+        if (s_hi > s_end) s_hi = s_end;
+        for (int64_t s = s_lo + warp; s < s_hi; s += kComputeWarps) {
+            if (lane == 0) {
+                const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
+                const uint32_t ents = static_cast<uint32_t>(end - off);
+                *stage_w = static_cast<int>(ents >> 5);
+                mbar_expect_tx(bar, ents * 12u);
+                bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
+                bulk_g2s(stage + P.val_bytes, P.A.cols + off, ents * 4u, bar, pol);
             }
-            break;
+            __syncwarp();
+            mbar_wait(bar, phase & 1u);
+            ++phase;
+            const int w = *stage_w;
+            const double* vb = reinterpret_cast<const double*>(stage);
+            const int32_t* cb = reinterpret_cast<const int32_t*>(stage + P.val_bytes);
+            double acc;
+            switch (w) {
+            case 27: acc = smem_row_fixed<27, false>(vb, cb, P.p_local, lane); break;
+            case 18: acc = smem_row_fixed<18, false>(vb, cb, P.p_local, lane); break;
+            case 12: acc = smem_row_fixed<12, false>(vb, cb, P.p_local, lane); break;
+            case 8: acc = smem_row_fixed<8, false>(vb, cb, P.p_local, lane); break;
+            default: acc = smem_row_generic<false>(vb, cb, P.p_local, lane, w); break;
+            }
+            const int64_t row = (s << 5) + lane;
+            if (row >= T.r0 && row < T.r1) {
+                P.Ap[row] = acc;
+                part = __dadd_rn(part, __dmul_rn(P.p_owned[row], acc));
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        case DK_UPD: {
-            const double alpha = P.sc->alpha, nalpha = -alpha;
-            const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
-            int64_t b = a + P.vec_chunk_rows;
-            if (b > T.r1) b = T.r1;
-            // pairs (2i, 2i+1) fully inside [a, b) use 128-bit accesses
-            const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
-            for (int64_t q = q0 + tid; q < q1; q += blockDim.x) {
-                const int64_t e = 2 * q;
+        break;
+    }
+    case DK_UPD:
+    case DK_UPDP: {
+        const bool upd = T.kind == DK_UPD;
+        const double alpha = upd ? P.sc->alpha : 0.0, nalpha = -alpha;
+        const double beta = upd ? 0.0 : P.sc->beta;
+        const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
+        int64_t b = a + P.vec_chunk_rows;
+        if (b > T.r1) b = T.r1;
+        // pairs (2q, 2q+1) inside [a, b) with 128-bit accesses, ragged ends scalar
+        const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
+        for (int64_t q = q0 + ctid; q < q1; q += cthreads) {
+            const int64_t e = 2 * q;
+            if (upd) {
                 double2 xv = *reinterpret_cast<const double2*>(P.x + e);
                 const double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
                 double2 rv = *reinterpret_cast<const double2*>(P.r + e);
@@ -151,96 +148,166 @@ __global__ void __launch_bounds__(kDagWarps * 32, 2) dag_kernel(DagParams P) {
                 *reinterpret_cast<double2*>(P.r + e) = rv;
                 part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
                 part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
-            }
-            if (tid < 2) { // ragged ends
-                const int64_t i = tid == 0 ? a : b - 1;
-                const bool mine = tid == 0 ? (a & 1) != 0 : ((b & 1) != 0 && b - 1 >= a && !((a & 1) && b - 1 == a));
-                if (mine && i < b) {
-                    const double xv = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
-                    const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
-                    P.x[i] = xv;
-                    P.r[i] = rv;
-                    part = __dadd_rn(part, __dmul_rn(rv, rv));
-                }
-            }
-            break;
-        }
-        case DK_UPDP: {
-            const double beta = P.sc->beta;
-            const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
-            int64_t b = a + P.vec_chunk_rows;
-            if (b > T.r1) b = T.r1;
-            const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
-            for (int64_t q = q0 + tid; q < q1; q += blockDim.x) {
-                const int64_t e = 2 * q;
+            } else {
                 const double2 rv = *reinterpret_cast<const double2*>(P.r + e);
                 double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
                 pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
                 pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
                 *reinterpret_cast<double2*>(P.p_owned + e) = pv;
             }
-            if (tid < 2) {
-                const int64_t i = tid == 0 ? a : b - 1;
-                const bool mine = tid == 0 ? (a & 1) != 0 : ((b & 1) != 0 && b - 1 >= a && !((a & 1) && b - 1 == a));
-                if (mine && i < b) P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
-            }
-            break;
         }
-        case DK_ALPHA:
-            if (tid == 0) { // alpha task: tile partials in tile order (cg.cpp:217-222)
-                double pAp = 0.0;
-                for (int t = 0; t < P.T; ++t) pAp = __dadd_rn(pAp, P.pa[t]);
-                P.sc->pAp = pAp;
-                P.sc->alpha = __ddiv_rn(P.sc->rtrans, pAp);
+        const int64_t lo = (a & 1) ? a : -1;                               // odd start
+        const int64_t hi = ((b & 1) && b - 1 >= a && b - 1 != lo) ? b - 1 : -1; // odd end
+        const int64_t i = ctid == 0 ? lo : (ctid == 1 ? hi : -1);
+        if (i >= 0) {
+            if (upd) {
+                const double xv = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
+                const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
+                P.x[i] = xv;
+                P.r[i] = rv;
+                part = __dadd_rn(part, __dmul_rn(rv, rv));
+            } else {
+                P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
             }
-            break;
-        case DK_BETA:
-            if (tid == 0) { // beta_res task (cg.cpp:299-309)
-                double rr = 0.0;
-                for (int t = 0; t < P.T; ++t) rr = __dadd_rn(rr, P.rr[t]);
-                CgScalars* sc = P.sc;
-                sc->rr = rr;
-                sc->beta = __ddiv_rn(rr, sc->rtrans);
-                sc->rtrans = rr;
-                if (sc->iter < sc->history_cap) {
-                    P.history[sc->iter] = __dsqrt_rn(rr);
-                    P.stamps[sc->iter + 1] = globaltimer();
-                }
-                sc->iter = sc->iter + 1;
-            }
-            break;
-        default:
-            break;
         }
+        break;
+    }
+    default:
+        break;
+    }
+    return part;
+}
 
-        const bool has_part = T.kind == DK_SPMV || T.kind == DK_UPD;
+// The scheduler warp's side of a chunk: alpha / beta_res bodies (one thread),
+// then the chunk partial, completion count and, for a task's last chunk, the
+// tile partial in chunk order and the release of the successors.
+__device__ __forceinline__ void complete_chunk(const DagParams& P, const Slot& S,
+                                               const double* wpart, int lane) {
+    const DagTask& T = S.t;
+    if (lane == 0) {
+        if (T.kind == DK_ALPHA) { // alpha task: tile partials in tile order (cg.cpp:217-222)
+            double pAp = 0.0;
+            for (int t = 0; t < P.T; ++t) pAp = __dadd_rn(pAp, P.pa[t]);
+            P.sc->pAp = pAp;
+            P.sc->alpha = __ddiv_rn(P.sc->rtrans, pAp);
+        } else if (T.kind == DK_BETA) { // beta_res task (cg.cpp:299-309)
+            double rr = 0.0;
+            for (int t = 0; t < P.T; ++t) rr = __dadd_rn(rr, P.rr[t]);
+            CgScalars* sc = P.sc;
+            sc->rr = rr;
+            sc->beta = __ddiv_rn(rr, sc->rtrans);
+            sc->rtrans = rr;
+            if (sc->iter < sc->history_cap) {
+                P.history[sc->iter] = __dsqrt_rn(rr);
+                P.stamps[sc->iter + 1] = globaltimer();
+            }
+            sc->iter = sc->iter + 1;
+        }
+    }
+    const bool has_part = T.kind == DK_SPMV || T.kind == DK_UPD;
+    unsigned last = 0;
+    if (lane == 0) {
         if (has_part) {
-            const double bsum = block_sum(part, red);
-            if (tid == 0) P.chunk_part[c] = bsum;
+            double s = 0.0;
+            for (int w = 0; w < kComputeWarps; ++w) s = __dadd_rn(s, wpart[w]);
+            P.chunk_part[S.c] = s;
         }
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            const unsigned d = atomicAdd(P.chunk_done + tk, 1u);
-            s_last = d + 1 == static_cast<unsigned>(T.nchunks);
+        __threadfence();
+        const unsigned d = atomicAdd(P.chunk_done + S.task, 1u);
+        last = d + 1 == static_cast<unsigned>(T.nchunks);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    if (has_part) { // tile partial = chunk partials summed in chunk order
+        double acc = 0.0;
+        for (int i = lane; i < T.nchunks; i += 32) acc = __dadd_rn(acc, __ldcg(P.chunk_part + T.chunk0 + i));
+        acc = warp_sum(acc);
+        if (lane == 0) (T.kind == DK_SPMV ? P.pa : P.rr)[T.tile] = acc;
+    }
+    __syncwarp();
+    if (lane == 0) __threadfence();
+    __syncwarp();
+    for (int k = lane; k < T.nsucc; k += 32) atomicSub(P.remaining + P.succ[T.succ0 + k], 1);
+}
+
+// Takes the next chunk (scheduler warp).  Never blocks on dependencies: the
+// scheduler must stay free to complete the chunk the compute warps are
+// running, which the new chunk may depend on.  If the task is already
+// runnable the acquire and the L1 invalidation happen here, off the critical
+// path; otherwise the compute warps wait for it.
+__device__ __forceinline__ void fill_slot(const DagParams& P, Slot* S, int lane) {
+    if (lane == 0) {
+        const int c = static_cast<int>(atomicAdd(P.ticket, 1u));
+        if (c >= P.nchunks) {
+            S->c = -1;
+        } else {
+            const int tk = P.chunk_task[c];
+            S->c = c;
+            S->task = tk;
+            S->t = P.tasks[tk];
+            if (c == 0) *P.start_stamp = globaltimer();
+            S->ready = ld_acquire(P.remaining + tk) <= 0;
+            if (S->ready) __threadfence(); // gpu scope: drop stale L1 lines
         }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (has_part) {
-                // tile partial = chunk partials summed in chunk order
-                double acc = 0.0;
-                for (int i = tid; i < T.nchunks; i += blockDim.x)
-                    acc = __dadd_rn(acc, __ldcg(P.chunk_part + T.chunk0 + i));
-                const double tot = block_sum(acc, red);
-                if (tid == 0) (T.kind == DK_SPMV ? P.pa : P.rr)[T.tile] = tot;
-            }
-            __syncthreads();
+    }
+    __syncwarp();
+}
+
+// Persistent dispatcher CTA: kComputeWarps compute warps + 1 scheduler warp
+// over a 2-slot ring.  The scheduler fills slot b+1 (ticket, task record,
+// dependency acquire) while the compute warps run slot b, and completes slot
+// b (partials, counters, successor release) while they run slot b+1, so the
+// per-chunk bookkeeping is off the critical path and chunks can be small.
+__global__ void __launch_bounds__(kDagWarps * 32, 2) dag_kernel(DagParams P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kComputeWarps];
+    __shared__ int stage_w[kComputeWarps];
+    __shared__ Slot slots[kSlots];
+    __shared__ double wpart[kSlots][kComputeWarps];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int kAll = kDagWarps * 32;
+    if (warp < kComputeWarps && lane == 0) mbar_init(&bars[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    if (warp == kComputeWarps) { // ---------------------------------- scheduler
+        for (int b = 0; b < kSlots; ++b) {
+            fill_slot(P, &slots[b], lane);
+            bar_arrive(1 + b, kAll); // FULL[b]
+        }
+        for (int k = 0;; ++k) {
+            const int b = k & 1;
+            if (slots[b].c < 0) break; // compute warps saw the end marker too
+            bar_sync(3 + b, kAll);     // EMPTY[b]: compute warps done with slot b
+            complete_chunk(P, slots[b], wpart[b], lane);
+            fill_slot(P, &slots[b], lane);
+            bar_arrive(1 + b, kAll);
+        }
+        return;
+    }
+    // -------------------------------------------------------------- compute
+    unsigned char* stage = smem + static_cast<size_t>(warp) * P.stage_bytes;
+    const uint64_t pol = l2_evict_first_policy();
+    uint32_t phase = 0;
+    for (int k = 0;; ++k) {
+        const int b = k & 1;
+        bar_sync(1 + b, kAll); // FULL[b]
+        const int c = slots[b].c;
+        if (c < 0) break;
+        if (!slots[b].ready) { // wait for the task's predecessors (compute warps only)
             if (tid == 0) {
+                while (ld_acquire(P.remaining + slots[b].task) > 0) __nanosleep(32);
                 __threadfence();
-                for (int k = 0; k < T.nsucc; ++k) atomicSub(P.remaining + P.succ[T.succ0 + k], 1);
             }
+            bar_sync(5, kComputeWarps * 32);
         }
+        const DagTask T = slots[b].t;
+        const double part = run_chunk(P, T, c - T.chunk0, warp, lane, stage, &bars[warp],
+                                      &stage_w[warp], phase, pol);
+        const double ws = warp_sum(part);
+        if (lane == 0) wpart[b][warp] = ws;
+        bar_arrive(3 + b, kAll); // EMPTY[b]
     }
 }
 
@@ -255,6 +322,8 @@ int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes) {
 }
 
 int dag_threads() { return kDagWarps * 32; }
+
+int dag_compute_warps() { return kComputeWarps; }
 
 // Grid = every dispatcher CTA the device can hold at once (all CTAs must be
 // co-resident: a CTA may wait on chunks other CTAs hold).

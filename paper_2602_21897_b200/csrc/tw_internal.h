@@ -206,6 +206,7 @@ struct DagParams {
 
 int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes);
 int dag_threads();
+int dag_compute_warps();
 int dag_blocks(int max_width, int sm_count);
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s);
 

@@ -1,8 +1,8 @@
 set -x
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 300 -k "persistent" > gpurun_out/pytest_dag.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_dag.log
 rm -f gpurun_out/sweep_dag.log
-for f in default paper_2602_21897_b200/_lib/dagvariants/*.so; do
-  echo "== $f" >> gpurun_out/sweep_dag.log
-  if [ $f = default ]; then L=""; else L="TW_HPCCG_LIB=$f"; fi
-  env $L timeout 600 python scripts/sweep.py --configs c5 --only-persistent --tiles 1,8,64,512 >> gpurun_out/sweep_dag.log 2>&1
+for cfg in "16 4096" "32 4096" "16 8192" "8 2048" "48 16384"; do
+  set -- $cfg
+  echo "== spmv_slices=$1 vec_rows=$2" >> gpurun_out/sweep_dag.log
+  TW_DAG_SPMV_SLICES=$1 TW_DAG_VEC_ROWS=$2 timeout 600 python scripts/sweep.py --configs c5 --only-persistent --tiles 1,8,64,512 >> gpurun_out/sweep_dag.log 2>&1
 done
