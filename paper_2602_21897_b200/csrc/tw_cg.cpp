@@ -760,11 +760,11 @@ int64_t env_or(const char* name, int64_t dflt) {
     return v && *v ? std::atoll(v) : dflt;
 }
 int64_t dag_spmv_chunk_slices() {
-    static const int64_t v = env_or("TW_DAG_SPMV_SLICES", 2 * dag_compute_warps());
+    static const int64_t v = env_or("TW_DAG_SPMV_SLICES", 6 * dag_compute_warps());
     return v;
 }
 int64_t dag_vec_chunk_rows() {
-    static const int64_t v = env_or("TW_DAG_VEC_ROWS", 4096);
+    static const int64_t v = env_or("TW_DAG_VEC_ROWS", 16384);
     return v;
 }
 
