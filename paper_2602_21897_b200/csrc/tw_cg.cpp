@@ -166,6 +166,7 @@ struct tw_cg {
     cudaEvent_t ag_in_ev = nullptr, ag_out_ev = nullptr;
 
     cudaGraphExec_t graph = nullptr;
+    std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;
@@ -395,8 +396,16 @@ cudaEvent_t tmark(tw_cg* cg, int k) {
     return cg->tev[i];
 }
 
+// Timing marks: inside a stream capture a plain cudaEventRecord only forms
+// graph edges, so the marks are captured as external event-record nodes.
 void record(cudaEvent_t e, cudaStream_t s) {
-    if (e) TW_CUDA(cudaEventRecord(e, s));
+    if (!e) return;
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    TW_CUDA(cudaStreamIsCapturing(s, &st));
+    if (st == cudaStreamCaptureStatusActive)
+        TW_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else
+        TW_CUDA(cudaEventRecord(e, s));
 }
 
 void enqueue_mono(tw_cg* cg) {
@@ -558,6 +567,7 @@ void free_cg(tw_cg* cg) {
     cudaDeviceSynchronize();
     cg->ta.reset();
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
+    for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
@@ -899,6 +909,33 @@ void iterate(tw_cg* cg, int k) {
         cg->enqueued += k;
         return;
     }
+    if (cg->opt.use_graph && cg->timing && cg->opt.variant == TW_CG_MONOLITHIC) {
+        // k iterations as ONE graph with the K1/K2/K3 timing events inside:
+        // graph-launch efficiency and per-kernel durations of the same run
+        auto it = cg->timed_graphs.find(k);
+        if (it == cg->timed_graphs.end()) {
+            cudaGraph_t g = nullptr;
+            cg->timed = 0;
+            TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (int i = 0; i < k; ++i) enqueue_mono(cg);
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            TW_CUDA(cudaStreamEndCapture(s, &g));
+            cudaGraphExec_t ge = nullptr;
+            cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            TW_CUDA(e);
+            it = cg->timed_graphs.emplace(k, ge).first;
+        }
+        TW_CUDA(cudaGraphLaunch(it->second, s));
+        cg->timed = k; // the graph records timing slots 0..k-1
+        cg->enqueued += k;
+        return;
+    }
     if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     const bool tasks = cg->opt.variant == TW_CG_TASKS;
     if (!cg->opt.use_graph && tasks) fork_streams(cg);
@@ -1075,8 +1112,8 @@ int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed) {
 int tw_cg_enable_kernel_timing(tw_cg* cg, int enable) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
-        if (enable && (cg->opt.variant != TW_CG_MONOLITHIC || cg->opt.use_graph))
-            config_error("kernel timing needs the monolithic variant without graph capture");
+        if (enable && cg->opt.variant != TW_CG_MONOLITHIC)
+            config_error("kernel timing needs the monolithic variant");
         cg->timing = enable != 0;
         cg->timed = 0;
     });

@@ -410,3 +410,20 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     with pytest.raises(P.ConfigError):
         P.CgSolver(rt2, A, 4, P.CgOptions(tiles=4, persistent=True))
     rt2.close()
+
+
+def test_timed_graph_kernel_times(rt, orc):
+    A = P.gen_stencil_matrix(48, 48, 48, rt=rt)
+    b = orc.rhs_xorshift(A.n, 7)
+    S = P.CgSolver(rt, A, 30, P.CgOptions(use_graph=True, iteration_marks=False), variant=0)
+    S.set_rhs(b)
+    S.enable_kernel_timing(True)
+    S.iterate(20)
+    k1, k2, k3, n = S.kernel_times()
+    assert n == 20 and k1 > 0 and k2 > 0 and k3 > 0
+    h = S.history(20)
+    S.set_rhs(b)
+    S.enable_kernel_timing(False)
+    S.iterate(20)
+    assert np.array_equal(h, S.history(20))
+    S.close()
