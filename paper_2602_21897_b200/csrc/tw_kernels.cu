@@ -625,17 +625,23 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
         const int stage = tma_stage_bytes(A.max_width, &vb);
         const int smem = kTmaWarps * kTmaStages * stage;
         auto kern = with_dot ? spmv_tma_kernel<true> : spmv_tma_kernel<false>;
-        static int attr_bytes[2] = {0, 0};
-        static int static_bytes[2] = {-1, -1};
-        if (static_bytes[with_dot] < 0) {
+        // the opt-in shared-memory size is a per-device function attribute
+        constexpr int kMaxDev = 64;
+        static std::mutex mu;
+        static int attr_bytes[kMaxDev][2] = {};
+        static int static_bytes = -1;
+        int dev = 0;
+        TW_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_bytes < 0) {
             cudaFuncAttributes fa;
-            TW_CUDA(cudaFuncGetAttributes(&fa, kern));
-            static_bytes[with_dot] = static_cast<int>(fa.sharedSizeBytes);
+            TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_kernel<true>));
+            static_bytes = static_cast<int>(fa.sharedSizeBytes);
         }
-        if (smem + static_bytes[with_dot] <= 227 * 1024) {
-            if (attr_bytes[with_dot] < smem) {
+        if (dev < kMaxDev && smem + static_bytes <= 227 * 1024) {
+            if (attr_bytes[dev][with_dot] < smem) {
                 TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr_bytes[with_dot] = smem;
+                attr_bytes[dev][with_dot] = smem;
             }
             int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
             const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);

@@ -725,6 +725,7 @@ int tw_spmv_range(const tw_ell* A, const double* x, double* y, int64_t r0, int64
         check_ell(A);
         if (r0 < 0 || r1 > A->info.n_rows || r0 > r1) contract_error("spmv row range out of bounds");
         if (r0 == r1) return;
+        TW_CUDA(cudaSetDevice(A->ctx->device));
         RedScratch rs{};
         launch_spmv(A->view(), x, y, RowRange{r0, r1}, RowRange{0, 0}, false, rs,
                     Fin{FIN_NONE, nullptr, nullptr, nullptr}, A->ctx->cfg.spmv_blocks,
@@ -738,6 +739,7 @@ int tw_spmv_dot(const tw_ell* A, const double* p, double* Ap, int64_t r0, int64_
         check_ell(A);
         if (r0 < 0 || r1 > A->info.n_rows || r0 > r1) contract_error("spmv row range out of bounds");
         tw_ctx* c = A->ctx;
+        TW_CUDA(cudaSetDevice(c->device));
         cudaStream_t s = pick(c, stream);
         if (r0 == r1) {
             TW_CUDA(cudaMemsetAsync(dot_dev, 0, sizeof(double), s));
@@ -756,6 +758,7 @@ int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int6
     return guarded([&] {
         check_ctx(ctx);
         if (i0 > i1) contract_error("dot range reversed");
+        TW_CUDA(cudaSetDevice(ctx->device));
         cudaStream_t s = pick(ctx, stream);
         if (i0 == i1) {
             TW_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
@@ -774,6 +777,7 @@ int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, con
     return guarded([&] {
         check_ctx(ctx);
         if (i0 > i1) contract_error("waxpby range reversed");
+        TW_CUDA(cudaSetDevice(ctx->device));
         launch_waxpby(alpha, x, beta, y, w, i0, i1, ctx->cfg.stream_blocks, pick(ctx, stream));
     });
 }
@@ -798,6 +802,7 @@ int tw_rhs_xorshift(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, do
                     void* stream) {
     return guarded([&] {
         check_ctx(ctx);
+        TW_CUDA(cudaSetDevice(ctx->device));
         rhs_xorshift(ctx, seed, first, count, out_dev, pick(ctx, stream));
     });
 }
@@ -807,6 +812,7 @@ int tw_rhs_splitmix(tw_ctx* ctx, uint64_t seed, int64_t first, int64_t count, do
     return guarded([&] {
         check_ctx(ctx);
         if (first < 0 || count < 0) contract_error("rhs: negative range");
+        TW_CUDA(cudaSetDevice(ctx->device));
         launch_rhs_splitmix(seed, first, count, out_dev, ctx->cfg.stream_blocks, pick(ctx, stream));
     });
 }
