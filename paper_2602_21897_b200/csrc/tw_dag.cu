@@ -95,9 +95,11 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
                 const uint32_t ents = static_cast<uint32_t>(end - off);
                 *stage_w = static_cast<int>(ents >> 5);
-                mbar_expect_tx(bar, ents * 12u);
-                bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
-                bulk_g2s(stage + P.val_bytes, P.A.cols + off, ents * 4u, bar, pol);
+                mbar_expect_tx(bar, ents * 12u); // ents == 0 (all rows empty): completes at once
+                if (ents) {
+                    bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
+                    bulk_g2s(stage + P.val_bytes, P.A.cols + off, ents * 4u, bar, pol);
+                }
             }
             __syncwarp();
             mbar_wait(bar, phase & 1u);

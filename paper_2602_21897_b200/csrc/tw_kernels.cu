@@ -158,9 +158,11 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         const uint32_t ents = static_cast<uint32_t>(end - off);
         stage_w[warp][st] = static_cast<int>(ents >> 5);
         unsigned char* dst = ring + static_cast<size_t>(st) * stage_bytes;
-        mbar_expect_tx(&bars[warp][st], ents * 12u);
-        bulk_g2s(dst, A.vals + off, ents * 8u, &bars[warp][st], pol);
-        bulk_g2s(dst + val_bytes, A.cols + off, ents * 4u, &bars[warp][st], pol);
+        mbar_expect_tx(&bars[warp][st], ents * 12u); // ents == 0 (all rows empty): completes at once
+        if (ents) {
+            bulk_g2s(dst, A.vals + off, ents * 8u, &bars[warp][st], pol);
+            bulk_g2s(dst + val_bytes, A.cols + off, ents * 4u, &bars[warp][st], pol);
+        }
     };
     if (lane == 0)
         for (int st = 0; st < kTmaStages && st < mine; ++st) issue(st, st);

@@ -427,3 +427,38 @@ def test_timed_graph_kernel_times(rt, orc):
     S.iterate(20)
     assert np.array_equal(h, S.history(20))
     S.close()
+
+
+def test_general_matrix_with_empty_slices(rt, orc):
+    """Rows 32..95 empty (two whole slices of width 0), long rows elsewhere:
+    SpMV bit-exact, empty rows give +0.0, CG on an SPD general matrix."""
+    from oracle import Csr
+    rng = np.random.default_rng(9)
+    n = 200
+    lens = rng.integers(1, 60, n)
+    lens[32:96] = 0
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int64)
+    va = rng.standard_normal(len(ci))
+    G = P.ell_from_csr(rp, ci, va, rt=rt)
+    assert G.info.max_width == lens.max()
+    x = rng.standard_normal(n)
+    y = torch.full((n,), 7.0, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(G, dev(x), y, 0, n)
+    want = orc.spmv(Csr(n, rp, ci, va), x)
+    got = host(y)
+    assert np.array_equal(got, want) and np.all(got[32:96] == 0.0)
+    # SPD: diagonally dominant symmetric tridiagonal + identity rows
+    m = 150
+    rows = [[(i, 4.0)] + ([(i - 1, -1.0)] if i else []) + ([(i + 1, -1.0)] if i + 1 < m else [])
+            for i in range(m)]
+    rows = [sorted(r) for r in rows]
+    rp2 = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    ci2 = np.array([c for r in rows for c, _ in r], np.int64)
+    va2 = np.array([v for r in rows for _, v in r])
+    T = P.ell_from_csr(rp2, ci2, va2, rt=rt)
+    b = orc.rhs_xorshift(m, 3)
+    for run in (P.cg_monolithic, P.cg_tasks):
+        res = run(rt, T, b, 12, P.CgOptions(tiles=3))
+        want_h, want_x, _ = orc.cg(Csr(m, rp2, ci2, va2), b, 12, tiles=1 if run is P.cg_monolithic else 3)
+        check_history(res.residual_history, want_h)
