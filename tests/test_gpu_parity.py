@@ -462,3 +462,18 @@ def test_general_matrix_with_empty_slices(rt, orc):
         res = run(rt, T, b, 12, P.CgOptions(tiles=3))
         want_h, want_x, _ = orc.cg(Csr(m, rp2, ci2, va2), b, 12, tiles=1 if run is P.cg_monolithic else 3)
         check_history(res.residual_history, want_h)
+
+
+def test_cg_128cubed_vs_oracle(rt, orc):
+    """Mid-size parity (C2 grid): monolithic, 8-tile DAG and the dispatcher
+    against the oracle's cg_reference / tile-order cg on 128^3, 25 iterations."""
+    m = orc.stencil(128, 128, 128)
+    b = orc.rhs_splitmix(m.n, 7)
+    want_h, want_x, _ = orc.cg(m, b, 25)
+    A = P.gen_stencil_matrix(128, 128, 128, rt=rt)
+    for run, opt in [(P.cg_monolithic, P.CgOptions()),
+                     (P.cg_tasks, P.CgOptions(tiles=8, use_graph=True)),
+                     (P.cg_tasks, P.CgOptions(tiles=8, persistent=True))]:
+        res = run(rt, A, b, 25, opt)
+        check_history(res.residual_history, want_h)
+        assert np.all(rel_gap(res.x, want_x) <= 1e-10)
