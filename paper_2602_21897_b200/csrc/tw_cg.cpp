@@ -165,7 +165,7 @@ struct tw_cg {
     cudaEvent_t fork_ev = nullptr, halo_ev = nullptr, pready_ev = nullptr;
     cudaEvent_t ag_in_ev = nullptr, ag_out_ev = nullptr;
 
-    cudaGraphExec_t graph[2] = {nullptr, nullptr}; // by iteration parity
+    cudaGraphExec_t graph = nullptr;
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
@@ -408,36 +408,21 @@ void record(cudaEvent_t e, cudaStream_t s) {
         TW_CUDA(cudaEventRecord(e, s));
 }
 
-// Alternating sweep directions: each kernel walks the rows in the opposite
-// direction of the kernel before it (K1 fwd, K2 rev, K3 fwd, next K1 rev ...),
-// so it starts on the rows whose vectors the previous sweep touched last and
-// that are still L2-resident (the matrix stream is L2 evict-first).  Per-row
-// results are unchanged; only the fixed order of the dot partials differs.
-bool sweep_alternates() {
-    static const bool on = [] {
-        const char* v = std::getenv("TW_NO_ALTERNATE");
-        return !(v && v[0] == '1');
-    }();
-    return on;
-}
-
-void enqueue_mono(tw_cg* cg, int it) {
+void enqueue_mono(tw_cg* cg) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
-    const bool odd = sweep_alternates() && (it & 1);
     if (!cg->dist) {
         record(tmark(cg, 0), s);
         launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs,
-                    Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, bs, s, odd);
+                    Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, bs, s);
         record(tmark(cg, 1), s);
         launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
-                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s,
-                         sweep_alternates() && !odd);
+                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s);
         record(tmark(cg, 2), s);
         launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                        cg->history, bv, s, odd);
+                        cg->history, bv, s);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
@@ -450,7 +435,7 @@ void enqueue_mono(tw_cg* cg, int it) {
     TW_CUDA(cudaEventRecord(cg->halo_ev, c));
     record(tmark(cg, 0), s);
     launch_spmv(A, cg->p_local, cg->Ap, RowRange{lo, hi}, RowRange{0, 0}, true, rs,
-                Fin{FIN_STORE, cg->pm, nullptr, nullptr}, bs, s, odd);
+                Fin{FIN_STORE, cg->pm, nullptr, nullptr}, bs, s);
     TW_CUDA(cudaStreamWaitEvent(s, cg->halo_ev, 0));
     launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, lo}, RowRange{hi, cg->n}, true, rs,
                 Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, bs, s);
@@ -459,11 +444,11 @@ void enqueue_mono(tw_cg* cg, int it) {
     record(tmark(cg, 1), s);
     launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                      ScalarSrc{cg->recv_a, cg->P}, rs, Fin{FIN_STORE, cg->send_b, nullptr, nullptr},
-                     bv, s, sweep_alternates() && !odd);
+                     bv, s);
     allgather1(cg, cg->send_b, cg->recv_b, s);
     record(tmark(cg, 2), s);
     launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, rs,
-                    cg->history, bv, s, odd);
+                    cg->history, bv, s);
     record(tmark(cg, 3), s);
     if (cg->timing) ++cg->timed;
 }
@@ -546,16 +531,14 @@ void enqueue_tasks(tw_cg* cg, int parity, bool first) {
     }
 }
 
-void enqueue_iteration_body(tw_cg* cg, int it, bool first) {
+void enqueue_iteration_body(tw_cg* cg, int parity, bool first) {
     if (cg->opt.variant == TW_CG_MONOLITHIC)
-        enqueue_mono(cg, it);
+        enqueue_mono(cg);
     else
-        enqueue_tasks(cg, it & 1, first);
+        enqueue_tasks(cg, parity, first);
 }
 
-// One-iteration graph for iterations of the given parity (the sweep
-// directions of the monolithic loop alternate with it).
-void build_graph(tw_cg* cg, int parity) {
+void build_graph(tw_cg* cg) {
     cudaStream_t s = cg->ctx->compute;
     cudaGraph_t g = nullptr;
     TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
@@ -565,7 +548,7 @@ void build_graph(tw_cg* cg, int parity) {
             enqueue_tasks(cg, 0, true);
             join_streams(cg);
         } else {
-            enqueue_mono(cg, parity);
+            enqueue_mono(cg);
         }
     } catch (...) {
         cudaStreamEndCapture(s, &g);
@@ -573,7 +556,7 @@ void build_graph(tw_cg* cg, int parity) {
         throw;
     }
     TW_CUDA(cudaStreamEndCapture(s, &g));
-    cudaError_t e = cudaGraphInstantiate(&cg->graph[parity], g, 0);
+    cudaError_t e = cudaGraphInstantiate(&cg->graph, g, 0);
     cudaGraphDestroy(g);
     TW_CUDA(e);
 }
@@ -583,8 +566,7 @@ void free_cg(tw_cg* cg) {
     cudaSetDevice(cg->ctx->device);
     cudaDeviceSynchronize();
     cg->ta.reset();
-    for (auto g : cg->graph)
-        if (g) cudaGraphExecDestroy(g);
+    if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
@@ -930,14 +912,13 @@ void iterate(tw_cg* cg, int k) {
     if (cg->opt.use_graph && cg->timing && cg->opt.variant == TW_CG_MONOLITHIC) {
         // k iterations as ONE graph with the K1/K2/K3 timing events inside:
         // graph-launch efficiency and per-kernel durations of the same run
-        const int key = 2 * k + (cg->enqueued & 1);
-        auto it = cg->timed_graphs.find(key);
+        auto it = cg->timed_graphs.find(k);
         if (it == cg->timed_graphs.end()) {
             cudaGraph_t g = nullptr;
             cg->timed = 0;
             TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
-                for (int i = 0; i < k; ++i) enqueue_mono(cg, cg->enqueued + i);
+                for (int i = 0; i < k; ++i) enqueue_mono(cg);
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);
@@ -948,27 +929,23 @@ void iterate(tw_cg* cg, int k) {
             cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
             cudaGraphDestroy(g);
             TW_CUDA(e);
-            it = cg->timed_graphs.emplace(key, ge).first;
+            it = cg->timed_graphs.emplace(k, ge).first;
         }
         TW_CUDA(cudaGraphLaunch(it->second, s));
         cg->timed = k; // the graph records timing slots 0..k-1
         cg->enqueued += k;
         return;
     }
-    if (cg->opt.use_graph) {
-        const int p0 = cg->enqueued & 1;
-        if (!cg->graph[p0]) build_graph(cg, p0);
-        if (k > 1 && !cg->graph[p0 ^ 1]) build_graph(cg, p0 ^ 1);
-    }
+    if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     const bool tasks = cg->opt.variant == TW_CG_TASKS;
     if (!cg->opt.use_graph && tasks) fork_streams(cg);
     if (cg->opt.iteration_marks && cg->enqueued == 0) TW_CUDA(cudaEventRecord(iter_event(cg, 0), s));
     for (int i = 0; i < k; ++i) {
         const int it = cg->enqueued + i;
         if (cg->opt.use_graph) {
-            TW_CUDA(cudaGraphLaunch(cg->graph[it & 1], s));
+            TW_CUDA(cudaGraphLaunch(cg->graph, s));
         } else {
-            enqueue_iteration_body(cg, it, i == 0);
+            enqueue_iteration_body(cg, it & 1, i == 0);
         }
         if (cg->opt.iteration_marks) {
             // cg_iter=i mark (cg.cpp:307-308): the poller stamps the host time

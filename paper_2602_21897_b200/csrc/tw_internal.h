@@ -117,20 +117,17 @@ struct RowRange {
 };
 
 // K1: y = A x over up to two local row ranges; optional fused dot(x_diag, y).
-// `reverse` sweeps the rows last-to-first (the alternating-direction
-// schedule of the monolithic CG loop, tw_cg.cpp).
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
-                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
-                 bool reverse = false);
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s);
 // K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
-                      Fin fin, int blocks, cudaStream_t s, bool reverse = false);
+                      Fin fin, int blocks, cudaStream_t s);
 // K3: p = r + beta p (beta from sc or recomputed from partials; with
 // partials, the last block also commits rtrans/history/iter).
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, bool reverse = false);
+                     cudaStream_t s);
 // K4: dot(a, b) over [i0, i1) with finalize.
 void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
                 int blocks, cudaStream_t s);

@@ -131,7 +131,7 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
 template <bool DOT>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
-                RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin, int reverse) {
+                RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps][kTmaStages];
     __shared__ int stage_w[kTmaWarps][kTmaStages];
@@ -143,14 +143,8 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     const int64_t sb0 = rb.r0 >> 5, sb1 = rb.r1 > rb.r0 ? (rb.r1 + 31) >> 5 : sb0;
     const int64_t na = sa1 - sa0, ntot = na + (sb1 - sb0);
     const int64_t mine = warp_g < ntot ? (ntot - warp_g + nwarps - 1) / nwarps : 0;
-    // sweep order: forward, or reversed so this sweep starts where the
-    // previous kernel's sweep ended (its vectors are still L2-resident)
-    auto index_of = [&](int64_t k) {
-        const int64_t i = warp_g + k * nwarps;
-        return reverse ? ntot - 1 - i : i;
-    };
     auto slice_of = [&](int64_t k) {
-        const int64_t i = index_of(k);
+        const int64_t i = warp_g + k * nwarps;
         return i < na ? sa0 + i : sb0 + (i - na);
     };
     if (lane == 0)
@@ -190,7 +184,7 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         }
         const int64_t s = slice_of(k);
         const int64_t row = (s << 5) + lane;
-        const RowRange r = index_of(k) < na ? ra : rb;
+        const RowRange r = (warp_g + k * nwarps) < na ? ra : rb;
         if (row >= r.r0 && row < r.r1) {
             y[row] = acc;
             if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
@@ -211,12 +205,12 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
 // 128-bit accesses, the (at most two) ragged ends go scalar.
 template <typename F>
-__device__ __forceinline__ void for_pairs(int64_t i0, int64_t i1, bool reverse, F&& f) {
+__device__ __forceinline__ void for_pairs(int64_t i0, int64_t i1, F&& f) {
     const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t j = j0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < j1;
          j += stride) {
-        const int64_t e = 2 * (reverse ? j1 - 1 - (j - j0) : j);
+        const int64_t e = 2 * j;
         f(e, e >= i0, e + 1 < i1);
     }
 }
@@ -224,7 +218,7 @@ __device__ __forceinline__ void for_pairs(int64_t i0, int64_t i1, bool reverse, 
 __global__ void __launch_bounds__(kThreads)
 update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
                  double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
-                 ScalarSrc asrc, RedScratch rs, Fin fin, int reverse) {
+                 ScalarSrc asrc, RedScratch rs, Fin fin) {
     double alpha;
     if (asrc.count > 0)
         alpha = __ddiv_rn(sc->rtrans, sum_parts(asrc.parts, asrc.count));
@@ -232,7 +226,7 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
         alpha = sc->alpha;
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
     double part = 0.0;
-    for_pairs(i0, i1, reverse != 0, [&](int64_t e, bool lo, bool hi) {
+    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
         if (lo && hi) {
             double2 xv = __ldcs(reinterpret_cast<const double2*>(x + e));
             double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
@@ -263,7 +257,7 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 
 __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
-                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history, int reverse) {
+                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history) {
     double beta, rr = 0.0;
     if (bsrc.count > 0) {
         rr = sum_parts(bsrc.parts, bsrc.count);
@@ -271,7 +265,7 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
     } else {
         beta = sc->beta;
     }
-    for_pairs(i0, i1, reverse != 0, [&](int64_t e, bool lo, bool hi) {
+    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
         if (lo && hi) {
             double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
             double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
@@ -625,7 +619,7 @@ int spmv_tma_smem_bytes(int max_width) {
 }
 
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
-                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s, bool reverse) {
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s) {
     auto slices = [](RowRange r) { return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : 0; };
     const int64_t ns = slices(a) + slices(b);
     if (A.max_width > 0 && A.tma_blocks > 0) {
@@ -653,7 +647,7 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
             }
             int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
             const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin, reverse ? 1 : 0);
+            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin);
             TW_CUDA(cudaGetLastError());
             return;
         }
@@ -668,17 +662,17 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
 
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc asrc, RedScratch rs, Fin fin,
-                      int blocks, cudaStream_t s, bool reverse) {
+                      int blocks, cudaStream_t s) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    update_xr_kernel<<<g, kThreads, 0, s>>>(i0, i1, x, p, r, Ap, sc, asrc, rs, fin, reverse ? 1 : 0);
+    update_xr_kernel<<<g, kThreads, 0, s>>>(i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
     TW_CUDA(cudaGetLastError());
 }
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, bool reverse) {
+                     cudaStream_t s) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, reverse ? 1 : 0);
+    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history);
     TW_CUDA(cudaGetLastError());
 }
 
