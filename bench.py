@@ -316,7 +316,9 @@ def run_ours(args, dist, rank, world, local):
         if kern_timing:
             S.enable_kernel_timing(False)
         hist = S.history(W + kr)
-        assert np.all(np.isfinite(hist)) and np.all(hist[1:] <= hist[:-1] * (1 + 1e-12))
+        # finite and decaying (CG minimises the A-norm of the error, so the
+        # residual 2-norm need not fall at every single iteration)
+        assert np.all(np.isfinite(hist)) and hist[-1] < hist[0]
         return e0.elapsed_time(e1), kt, hist
 
     def timed_run():
