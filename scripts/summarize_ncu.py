@@ -1,0 +1,51 @@
+"""Summarise a gpurun ncu capture into profiles/ (launch list + K1 full-set metrics).
+usage: python scripts/summarize_ncu.py <launches.csv> <prof_k1.ncu-rep> <round tag>"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+
+launches, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+rows = list(csv.reader(open(launches)))
+hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+h = rows[hi]
+per, names = collections.defaultdict(dict), {}
+for r in rows[hi + 1:]:
+    per[r[0]][r[h.index("Metric Name")]] = float(r[h.index("Metric Value")].replace(",", ""))
+    names[r[0]] = r[h.index("Kernel Name")]
+agg = collections.OrderedDict()
+for k, m in per.items():
+    nm = names[k].split("(")[0].replace("void ", "").split("::")[-1]
+    a = agg.setdefault(nm, [0, 0.0, 0.0])
+    a[0] += 1
+    a[1] += m.get("gpu__time_duration.sum", 0)
+    a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+it = [k for k in agg if k.startswith(("spmv", "update"))]
+tot = sum(agg[k][1] / agg[k][0] for k in it)
+out = [f"# ncu launch list ({tag}): bench.py --steps 6 --warmup 3 at 256^3, 1 B200, --clock-control none",
+       "# kernel, launches, avg us, avg dram bytes/launch, share of the iteration's kernels"]
+for k, (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    sh = f"share_of_iteration={t / c / tot:.3f}" if k in it else "setup (once per solve)"
+    out.append(f"{k:28s} {c:4d} {t / c / 1e3:10.1f} us {b / c / 1e9:8.3f} GB  {sh}")
+open(f"profiles/{tag}_ncu_launches_summary.txt", "w").write("\n".join(out) + "\n")
+print("\n".join(out))
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(raw.splitlines()))
+H, U, V = r[0], r[1], r[2]
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__t_sector_hit_rate.pct",
+        "lts__t_sector_hit_rate.pct",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+summ = {k: [V[H.index(k)], U[H.index(k)]] for k in keys if k in H}
+scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+traffic = sum(float(summ[k][0]) * scale[summ[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+d = {"kernel": "spmv_tma_kernel<true> (K1)", "workload": "256x256x256", "round": tag,
+     "source": "ncu --set full --clock-control none, bench.py --steps 6 --warmup 3",
+     "dram_bytes_per_launch": traffic, "algorithmic_bytes": 12 * 449455096 + 16 * 16777216,
+     "metrics": summ}
+json.dump(d, open("profiles/k1_traffic.json", "w"), indent=1)
+print(json.dumps(d, indent=1))
