@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", action="store_true",
                     help="attach an NCCL communicator even at N=1 (exercises the multi-GPU path)")
-    ap.add_argument("--cpu-sample-nz", type=int, default=64)
-    ap.add_argument("--cpu-sample-iters", type=int, default=10)
+    ap.add_argument("--cpu-sample-nz", type=int, default=0,
+                    help="planes of the CPU sample (0 = the full per-GPU workload)")
+    ap.add_argument("--cpu-sample-iters", type=int, default=40)
     return ap.parse_args()
 
 
@@ -203,7 +204,8 @@ def cpu_reference_sample(nx, ny, nz_sample, iters, threads):
     return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads,
             "kind": "reference", "iters_per_s": iters / secs,
             "sample": f"reference cg_tasks (oracle/_ref, real threads, tiles={tiles}) on a "
-                      f"{nx}x{ny}x{nz_sample} slab of the workload, {iters} CG iterations, "
+                      f"{nx}x{ny}x{nz_sample} grid (the per-GPU workload when nz matches), "
+                      f"{iters} CG iterations after 1 warm-up, "
                       f"{secs:.2f} s wall"}
 
 
@@ -214,7 +216,7 @@ def run_reference_arm(args, dist, rank, world):
     from oracle import Oracle, Reference
     R = Reference()
     o = Oracle()
-    nzs = args.cpu_sample_nz
+    nzs = args.cpu_sample_nz or args.nz
     M = R.stencil(args.nx, args.ny, nzs)
     b = o.rhs_xorshift(M.n, 7)
     tiles = min(8 * threads, M.n)
@@ -230,8 +232,8 @@ def run_reference_arm(args, dist, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (xorshift64 seed 7 rhs)",
         "iters_per_s": args.steps / secs,
         "config": {"workload": f"HPCCG {args.nx}x{args.ny}x{args.nz} per GPU weak scaling; "
-                               f"reference step = one CG iteration on a {args.nx}x{args.ny}x{nzs} "
-                               f"slab sample", "variant": "cg_tasks (reference, CPU threads)"},
+                               f"reference step = one CG iteration on the {args.nx}x{args.ny}x{nzs} "
+                               f"grid", "variant": "cg_tasks (reference, CPU threads)"},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
                          "sample": f"cg_tasks real threads tiles={tiles} on {args.nx}x{args.ny}x{nzs}, "
                                    f"{args.steps} iterations after {args.warmup} warm-up"},
@@ -399,7 +401,7 @@ def run_ours(args, dist, rank, world, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_sample(nx, ny, min(args.cpu_sample_nz, nz),
+            cpu = cpu_reference_sample(nx, ny, min(args.cpu_sample_nz or args.nz, nz),
                                        args.cpu_sample_iters, os.cpu_count() or 1)
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "reference",

@@ -62,6 +62,12 @@ int tw_ctx_device_info(tw_ctx* ctx, int* device, int* sm_count);
 int tw_comm_unique_id(unsigned char id_out[128]);
 int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[128]);
 int tw_ctx_comm_info(tw_ctx* ctx, int* rank, int* nranks);
+/* Emulated rank r of an nranks group on ONE device (no NCCL): for testing the
+ * multi-rank algorithm on a single GPU.  Solvers on such contexts are driven
+ * together by tw_cg_group_set_rhs / tw_cg_group_iterate, which run every
+ * rank's phases on one stream with loopback device copies in place of the
+ * NCCL halo and allgathers (no kernel waits on another). */
+int tw_ctx_init_emulated_rank(tw_ctx* ctx, int rank, int nranks);
 
 /* Device buffers for callers without another allocator (tests, bench). */
 int tw_malloc(tw_ctx* ctx, void** ptr, int64_t bytes);
@@ -224,6 +230,11 @@ int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_
                       int64_t cap, int64_t* needed);
 /* Physical launches per iteration (kernels + NCCL calls), for reports. */
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
+
+/* Emulated rank group (see tw_ctx_init_emulated_rank): cgs[r] is rank r's
+ * monolithic solver, b[r] its rows of b. */
+int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_is_device);
+int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations);
 
 /* cg_monolithic / cg_tasks in one call (cg.cpp:397-447): host b in, host
  * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17). */

@@ -85,6 +85,7 @@ SIGNATURES = [
     ("tw_comm_unique_id", C.c_int, [C.c_char_p]),
     ("tw_ctx_init_comm", C.c_int, [vp, C.c_int, C.c_int, C.c_char_p]),
     ("tw_ctx_comm_info", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("tw_ctx_init_emulated_rank", C.c_int, [vp, C.c_int, C.c_int]),
     ("tw_malloc", C.c_int, [vp, C.POINTER(vp), i64]),
     ("tw_free", C.c_int, [vp, vp]),
     ("tw_malloc_host", C.c_int, [C.POINTER(vp), i64]),
@@ -122,6 +123,8 @@ SIGNATURES = [
     ("tw_task_dag_edges", C.c_int, [i64, C.c_int, lp, lp, lp, lp, i64, i64, C.c_int, C.c_int,
                                     C.c_int, C.c_char_p, i64, C.POINTER(i64)]),
     ("tw_cg_launches_per_iteration", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("tw_cg_group_set_rhs", C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.c_int]),
+    ("tw_cg_group_iterate", C.c_int, [C.POINTER(vp), C.c_int, C.c_int]),
     ("tw_cg_solve", C.c_int, [vp, vp, vp, C.c_int, C.POINTER(CgOptionsC), dp, dp,
                               C.POINTER(C.c_int)]),
 ]

@@ -381,6 +381,34 @@ void halo_exchange(tw_cg* cg, cudaStream_t s) {
     TW_NCCL(api.GroupEnd());
 }
 
+// Phases of one rank's distributed monolithic iteration.  The NCCL path
+// interleaves them with the halo and the allgathers (enqueue_mono); the
+// emulated rank group (tw_cg_group_iterate) runs them rank by rank with
+// loopback copies in place of NCCL.
+void dist_spmv_interior(tw_cg* cg, cudaStream_t s) { // rows that read no ghost plane
+    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
+                RowRange{0, 0}, true, cg->slot(0), Fin{FIN_STORE, cg->pm, nullptr, nullptr},
+                launch_blocks(cg, true), s);
+}
+
+void dist_spmv_boundary(tw_cg* cg, cudaStream_t s) { // the ghost-reading planes, then p.Ap
+    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+                RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
+                Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, launch_blocks(cg, true), s);
+    launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
+}
+
+void dist_update_xr(tw_cg* cg, cudaStream_t s) { // alpha from the rank partials, local r.r
+    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+                     ScalarSrc{cg->recv_a, cg->P}, cg->slot(0),
+                     Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, launch_blocks(cg, false), s);
+}
+
+void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; commit
+    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, cg->slot(0),
+                    cg->history, launch_blocks(cg, false), s);
+}
+
 // One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
 // stream; across ranks the SpMV is split so the interior rows overlap the
 // halo exchange on the comm stream.
@@ -428,27 +456,20 @@ void enqueue_mono(tw_cg* cg) {
         return;
     }
     cudaStream_t c = cg->ctx->comm;
-    const int64_t lo = cg->slab.interior_r0, hi = cg->slab.interior_r1;
     TW_CUDA(cudaEventRecord(cg->pready_ev, s));
     TW_CUDA(cudaStreamWaitEvent(c, cg->pready_ev, 0));
     halo_exchange(cg, c);
     TW_CUDA(cudaEventRecord(cg->halo_ev, c));
     record(tmark(cg, 0), s);
-    launch_spmv(A, cg->p_local, cg->Ap, RowRange{lo, hi}, RowRange{0, 0}, true, rs,
-                Fin{FIN_STORE, cg->pm, nullptr, nullptr}, bs, s);
+    dist_spmv_interior(cg, s);
     TW_CUDA(cudaStreamWaitEvent(s, cg->halo_ev, 0));
-    launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, lo}, RowRange{hi, cg->n}, true, rs,
-                Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, bs, s);
-    launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
+    dist_spmv_boundary(cg, s);
     allgather1(cg, cg->send_a, cg->recv_a, s);
     record(tmark(cg, 1), s);
-    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
-                     ScalarSrc{cg->recv_a, cg->P}, rs, Fin{FIN_STORE, cg->send_b, nullptr, nullptr},
-                     bv, s);
+    dist_update_xr(cg, s);
     allgather1(cg, cg->send_b, cg->recv_b, s);
     record(tmark(cg, 2), s);
-    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, rs,
-                    cg->history, bv, s);
+    dist_update_p(cg, s);
     record(tmark(cg, 3), s);
     if (cg->timing) ++cg->timed;
 }
@@ -631,7 +652,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             config_error("unknown CG variant");
         cg->T = cg->opt.variant == TW_CG_MONOLITHIC ? 1 : cg->opt.tiles; // cg.cpp:400
         cg->P = ctx->nranks;
-        cg->dist = ctx->nccl_comm != nullptr; // rank-partial path (also for a 1-rank comm)
+        // rank-partial path: an NCCL communicator (also 1 rank) or an emulated rank
+        cg->dist = ctx->nccl_comm != nullptr || ctx->emulated;
         cg->max_iters = max_iters;
         const tw_ell_info_t& in = A->info;
         cg->n = in.n_rows;
@@ -719,11 +741,9 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
     return cg;
 }
 
-void set_rhs(tw_cg* cg, const double* b, bool on_device) {
+// x = 0, r = p = b, and the local r.r into send_r (dist) or rtrans (single).
+void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s) {
     tw_ctx* ctx = cg->ctx;
-    cudaStream_t s = ctx->compute;
-    TW_CUDA(cudaSetDevice(ctx->device));
-    TW_CUDA(cudaStreamSynchronize(s));
     const size_t bytes = sizeof(double) * static_cast<size_t>(cg->n);
     CgScalars init{};
     init.history_cap = cg->max_iters;
@@ -735,19 +755,123 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device) {
     TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, k, s));
     TW_CUDA(cudaMemcpyAsync(cg->p_owned, cg->r, bytes, cudaMemcpyDeviceToDevice, s));
     const RedScratch rs = cg->slot(0);
-    if (!cg->dist) {
+    if (!cg->dist)
         launch_dot(cg->r, cg->r, 0, cg->n, rs, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr},
                    ctx->cfg.stream_blocks, s);
-    } else {
+    else
         launch_dot(cg->r, cg->r, 0, cg->n, rs, Fin{FIN_STORE, cg->send_r, nullptr, nullptr},
                    ctx->cfg.stream_blocks, s);
+}
+
+void reset_solve_state(tw_cg* cg) {
+    cg->enqueued = 0;
+    std::fill(cg->marks.begin(), cg->marks.end(), 0.0);
+    cg->t0 = host_seconds();
+}
+
+void set_rhs(tw_cg* cg, const double* b, bool on_device) {
+    tw_ctx* ctx = cg->ctx;
+    if (ctx->emulated) contract_error("emulated ranks are driven as a group (tw_cg_group_set_rhs)");
+    cudaStream_t s = ctx->compute;
+    TW_CUDA(cudaSetDevice(ctx->device));
+    TW_CUDA(cudaStreamSynchronize(s));
+    set_rhs_prefix(cg, b, on_device, s);
+    if (cg->dist) {
         allgather1(cg, cg->send_r, cg->recv_r, s);
         launch_combine(cg->recv_r, cg->P, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr}, s);
     }
     TW_CUDA(cudaStreamSynchronize(s));
-    cg->enqueued = 0;
-    std::fill(cg->marks.begin(), cg->marks.end(), 0.0);
-    cg->t0 = host_seconds();
+    reset_solve_state(cg);
+}
+
+// ------------------------------------------------ emulated rank group
+//
+// P contexts on ONE device, each owning a z-slab, driven phase by phase on a
+// single stream.  The NCCL transport is replaced by loopback device copies
+// (halo planes into the neighbours' ghost planes, every rank's partial into
+// every rank's receive slots); everything else -- slab geometry, ghost
+// layout, interior/boundary split, rank-ordered scalar sums -- is the code
+// the NCCL path runs.  No kernel ever waits on another: the host sequences
+// the phases, so this is safe on one GPU (B200_PROFILING.md).
+
+void group_check(tw_cg** g, int P) {
+    if (!g || P < 1) contract_error("empty rank group");
+    for (int r = 0; r < P; ++r) {
+        if (!g[r]) contract_error("null solver in rank group");
+        const tw_ctx* c = g[r]->ctx;
+        if (!c->emulated || c->rank != r || c->nranks != P)
+            contract_error("rank group entry " + std::to_string(r) +
+                           " is not emulated rank r of P (tw_ctx_init_emulated_rank)");
+        if (c->device != g[0]->ctx->device) contract_error("emulated ranks share one device");
+        if (g[r]->opt.variant != TW_CG_MONOLITHIC)
+            config_error("the emulated rank group runs the monolithic variant");
+    }
+}
+
+void loopback_allgather(tw_cg** g, int P, double* tw_cg::*send, double* tw_cg::*recv,
+                        cudaStream_t s) {
+    for (int r = 0; r < P; ++r)
+        for (int q = 0; q < P; ++q)
+            TW_CUDA(cudaMemcpyAsync(g[r]->*recv + q, g[q]->*send, sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+}
+
+void loopback_halo(tw_cg** g, int P, cudaStream_t s) {
+    for (int r = 0; r < P; ++r) {
+        const tw_slab_t& sp = g[r]->slab;
+        const size_t bytes = sizeof(double) * static_cast<size_t>(sp.plane);
+        if (sp.ghost_lo) // my lower ghost <- rank r-1's last owned plane
+            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_lo, g[r - 1]->p_local + g[r - 1]->slab.send_hi,
+                                    bytes, cudaMemcpyDeviceToDevice, s));
+        if (sp.ghost_hi) // my upper ghost <- rank r+1's first owned plane
+            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_hi, g[r + 1]->p_local + g[r + 1]->slab.send_lo,
+                                    bytes, cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// Every rank's compute stream continues after the group's work on s.
+void group_join(tw_cg** g, int P, cudaStream_t s) {
+    TW_CUDA(cudaEventRecord(g[0]->fork_ev, s));
+    for (int r = 1; r < P; ++r) TW_CUDA(cudaStreamWaitEvent(g[r]->ctx->compute, g[0]->fork_ev, 0));
+}
+
+void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
+    group_check(g, P);
+    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
+    for (int r = 0; r < P; ++r) TW_CUDA(cudaStreamSynchronize(g[r]->ctx->compute));
+    cudaStream_t s = g[0]->ctx->compute;
+    for (int r = 0; r < P; ++r) set_rhs_prefix(g[r], b[r], on_device, s);
+    loopback_allgather(g, P, &tw_cg::send_r, &tw_cg::recv_r, s);
+    for (int r = 0; r < P; ++r)
+        launch_combine(g[r]->recv_r, P, Fin{FIN_RTRANS, nullptr, g[r]->sc, nullptr}, s);
+    TW_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < P; ++r) reset_solve_state(g[r]);
+}
+
+void group_iterate(tw_cg** g, int P, int k) {
+    group_check(g, P);
+    if (k < 0) config_error("negative iteration count");
+    for (int r = 0; r < P; ++r)
+        if (g[r]->enqueued + k > g[r]->max_iters) contract_error("iterations beyond max_iterations");
+    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
+    cudaStream_t s = g[0]->ctx->compute;
+    for (int r = 1; r < P; ++r) { // order after anything queued on the other ranks' streams
+        TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
+        TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
+    }
+    for (int it = 0; it < k; ++it) {
+        loopback_halo(g, P, s);
+        for (int r = 0; r < P; ++r) {
+            dist_spmv_interior(g[r], s);
+            dist_spmv_boundary(g[r], s);
+        }
+        loopback_allgather(g, P, &tw_cg::send_a, &tw_cg::recv_a, s);
+        for (int r = 0; r < P; ++r) dist_update_xr(g[r], s);
+        loopback_allgather(g, P, &tw_cg::send_b, &tw_cg::recv_b, s);
+        for (int r = 0; r < P; ++r) dist_update_p(g[r], s);
+    }
+    group_join(g, P, s);
+    for (int r = 0; r < P; ++r) g[r]->enqueued += k;
 }
 
 // Timing event at the end of iteration i-1 (i = 0: the start of the solve).
@@ -893,6 +1017,7 @@ void enqueue_persistent(tw_cg* cg, int k) {
 }
 
 void iterate(tw_cg* cg, int k) {
+    if (cg->ctx->emulated) contract_error("emulated ranks iterate as a group (tw_cg_group_iterate)");
     if (k < 0) config_error("negative iteration count");
     if (cg->enqueued + k > cg->max_iters)
         contract_error("iterations beyond max_iterations (" + std::to_string(cg->max_iters) + ")");
@@ -1136,6 +1261,17 @@ int tw_cg_kernel_times(tw_cg* cg, double* k1, double* k2, double* k3, int* itera
         if (k3) *k3 = acc[2];
         if (iterations) *iterations = cg->timed;
     });
+}
+
+int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_is_device) {
+    return guarded([&] {
+        if (!b) contract_error("null rhs list");
+        group_set_rhs(cgs, nranks, b, b_is_device != 0);
+    });
+}
+
+int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations) {
+    return guarded([&] { group_iterate(cgs, nranks, iterations); });
 }
 
 int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_t* r1,

@@ -111,6 +111,7 @@ struct tw_ctx {
     ncclComm_t nccl_comm = nullptr;
     int rank = 0;
     int nranks = 1;
+    bool emulated = false; // rank of an emulated group on one device (no NCCL)
 };
 
 struct tw_ell {

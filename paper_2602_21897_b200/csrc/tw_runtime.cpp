@@ -627,6 +627,7 @@ int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[1
         check_ctx(ctx);
         if (nranks < 1 || rank < 0 || rank >= nranks) config_error("bad rank / world size");
         if (ctx->nccl_comm) contract_error("communicator already initialised");
+        if (ctx->emulated) contract_error("context is an emulated rank");
         ctx->rank = rank;
         ctx->nranks = nranks;
         // a 1-rank communicator is allowed: it runs the distributed code path
@@ -634,6 +635,17 @@ int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[1
         std::memcpy(&uid, id, 128);
         TW_CUDA(cudaSetDevice(ctx->device));
         TW_NCCL(nccl().CommInitRank(&ctx->nccl_comm, nranks, uid, rank));
+    });
+}
+
+int tw_ctx_init_emulated_rank(tw_ctx* ctx, int rank, int nranks) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (nranks < 1 || rank < 0 || rank >= nranks) config_error("bad rank / world size");
+        if (ctx->nccl_comm) contract_error("context already has an NCCL communicator");
+        ctx->rank = rank;
+        ctx->nranks = nranks;
+        ctx->emulated = true;
     });
 }
 

@@ -148,6 +148,11 @@ class Runtime:
         uid = uid if uid is not None else bytes(128)
         N.check(_lib().tw_ctx_init_comm(self.h, rank, nranks, C.c_char_p(uid)))
 
+    def init_emulated_rank(self, rank: int, nranks: int):
+        """Make this context emulated rank `rank` of an `nranks` group on one
+        device (tw_ctx_init_emulated_rank); see EmulatedRankGroup."""
+        N.check(_lib().tw_ctx_init_emulated_rank(self.h, rank, nranks))
+
     @property
     def rank(self) -> int:
         r, n = C.c_int(), C.c_int()
@@ -542,6 +547,54 @@ class CgSolver:
         k, c = C.c_int(), C.c_int()
         N.check(_lib().tw_cg_launches_per_iteration(self.h, C.byref(k), C.byref(c)))
         return k.value, c.value
+
+
+class EmulatedRankGroup:
+    """P z-slab ranks on ONE device, driven together (tw_cg_group_*): the
+    multi-GPU algorithm with loopback copies in place of the NCCL transport.
+    Test infrastructure for the multi-rank path on a single B200."""
+
+    def __init__(self, nx: int, ny: int, nz: int, nranks: int, max_iterations: int,
+                 device: int = 0):
+        self.P = nranks
+        self.rts, self.mats, self.solvers = [], [], []
+        for r in range(nranks):
+            rt = Runtime(device)
+            rt.init_emulated_rank(r, nranks)
+            zb, ze = slab_partition(nz, r, nranks)
+            A = gen_stencil_matrix(nx, ny, nz, rt=rt, z_begin=zb, z_end=ze)
+            self.rts.append(rt)
+            self.mats.append(A)
+            self.solvers.append(CgSolver(rt, A, max_iterations,
+                                         CgOptions(iteration_marks=False),
+                                         variant=N.TW_CG_MONOLITHIC))
+        self._arr = (C.c_void_p * nranks)(*[s.h.value for s in self.solvers])
+
+    def set_rhs(self, b: np.ndarray) -> None:
+        """b: the GLOBAL right-hand side; each rank takes its rows."""
+        b = np.ascontiguousarray(b, np.float64)
+        parts, keep = [], []
+        for A in self.mats:
+            off = int(A.info.row_offset)
+            piece = np.ascontiguousarray(b[off:off + A.n])
+            keep.append(piece)
+            parts.append(piece.ctypes.data)
+        ptrs = (C.c_void_p * self.P)(*parts)
+        N.check(_lib().tw_cg_group_set_rhs(self._arr, self.P, ptrs, 0))
+
+    def iterate(self, k: int) -> None:
+        N.check(_lib().tw_cg_group_iterate(self._arr, self.P, k))
+
+    def history(self, count: int) -> list:
+        return [s.history(count) for s in self.solvers]
+
+    def solution(self) -> np.ndarray:
+        return np.concatenate([s.solution() for s in self.solvers])
+
+    def close(self):
+        for s in self.solvers:
+            s.close()
+        self.solvers = []
 
 
 def _solve(rt: Runtime, A: EllMatrix, b, iterations: int, opt: CgOptions | None,

@@ -477,3 +477,29 @@ def test_cg_128cubed_vs_oracle(rt, orc):
         res = run(rt, A, b, 25, opt)
         check_history(res.residual_history, want_h)
         assert np.all(rel_gap(res.x, want_x) <= 1e-10)
+
+
+# ------------------------------------------- emulated multi-rank group (1 GPU)
+
+@pytest.mark.parametrize("dims,P_", [((32, 32, 32), 2), ((40, 24, 30), 3), ((32, 32, 32), 4),
+                                     ((24, 20, 16), 8), ((16, 16, 2), 2)])
+def test_emulated_rank_group_matches_single_domain(orc, golden, dims, P_):
+    """P z-slab ranks on the one B200 (tw_cg_group_*): slab matrices, ghost
+    planes, interior/boundary SpMV split, rank-ordered scalar sums -- the
+    multi-GPU code with loopback copies for the NCCL transport -- must
+    reproduce the single-domain reference CG."""
+    m = orc.stencil(*dims)
+    b = orc.rhs_xorshift(m.n, 7)
+    want_h, want_x, _ = orc.cg(m, b, 40)
+    G = P.EmulatedRankGroup(*dims, P_, 40)
+    G.set_rhs(b)
+    G.iterate(15)
+    G.iterate(25)
+    hs = G.history(40)
+    for h in hs:
+        assert np.array_equal(h, hs[0])  # every rank holds the same scalars
+    check_history(hs[0], want_h)
+    assert np.all(rel_gap(G.solution(), want_x) <= 1e-10)
+    G.close()
+    if dims == (32, 32, 32):
+        check_history(hs[0], golden["cg_32_xorshift7_history"][:40])
