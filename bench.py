@@ -430,7 +430,11 @@ def run_ours(args, dist, rank, world, local):
             "residual_last": float(hist[-1]),
         }
         print(json.dumps(line), flush=True)
+    # release the solver, the matrix and the NCCL communicator while the
+    # process group is still up (not in interpreter-exit destructors)
     S.close()
+    del A
+    rt.close()
 
 
 def main():
