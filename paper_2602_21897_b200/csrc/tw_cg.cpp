@@ -24,106 +24,8 @@
 #include <set>
 #include <sstream>
 
+#include "tw_dag_host.h"
 #include "tw_objects.h"
-
-namespace tw {
-
-// --------------------------------------------------------------- ledger
-//
-// Byte-interval dependency inference with the reference's rules
-// (region_ledger.hpp:11-27): a read conflicts with the last writer; a write
-// or readwrite conflicts with the last writer and every reader since.
-
-enum AccMode { ACC_R = 0, ACC_W = 1, ACC_RW = 2 };
-struct Acc {
-    uint64_t lo, hi; // [lo, hi)
-    int mode;
-};
-
-class Ledger {
-public:
-    void conflicts(const Acc& a, std::vector<int>& out) const {
-        auto it = seg_.upper_bound(a.lo);
-        if (it != seg_.begin()) --it;
-        for (; it != seg_.end() && it->first < a.hi; ++it) {
-            const Seg& s = it->second;
-            if (s.hi <= a.lo) continue;
-            if (s.writer >= 0) out.push_back(s.writer);
-            if (a.mode != ACC_R) out.insert(out.end(), s.readers.begin(), s.readers.end());
-        }
-    }
-    void record(const Acc& a, int task) {
-        split(a.lo);
-        split(a.hi);
-        if (a.mode != ACC_R) {
-            seg_.erase(seg_.lower_bound(a.lo), seg_.lower_bound(a.hi));
-            seg_[a.lo] = Seg{a.hi, task, {}};
-            return;
-        }
-        uint64_t pos = a.lo;
-        auto it = seg_.lower_bound(a.lo);
-        while (pos < a.hi) {
-            if (it == seg_.end() || it->first >= a.hi) {
-                seg_[pos] = Seg{a.hi, -1, {task}};
-                break;
-            }
-            if (it->first > pos) {
-                seg_[pos] = Seg{it->first, -1, {task}};
-                pos = it->first;
-                continue;
-            }
-            auto& rd = it->second.readers;
-            if (std::find(rd.begin(), rd.end(), task) == rd.end()) rd.push_back(task);
-            pos = it->second.hi;
-            ++it;
-        }
-    }
-
-private:
-    struct Seg {
-        uint64_t hi;
-        int writer;
-        std::vector<int> readers;
-    };
-    void split(uint64_t x) {
-        auto it = seg_.upper_bound(x);
-        if (it == seg_.begin()) return;
-        --it;
-        if (it->first == x || it->second.hi <= x) return;
-        Seg right = it->second;
-        it->second.hi = x;
-        seg_[x] = std::move(right);
-    }
-    std::map<uint64_t, Seg> seg_;
-};
-
-enum PhysKind { PK_HALO, PK_SPMV, PK_ALPHA, PK_UPD, PK_BETA, PK_UPDP };
-
-struct LTask {
-    std::string label;
-    std::vector<Acc> acc;
-    int phys; // physical node index within the iteration
-};
-
-// Everything the logical DAG depends on: tile rows, the p band each tile's
-// SpMV reads (local x coordinates, inclusive, as make_tile_plan's band), and
-// across ranks the ghost-plane geometry.
-struct DagSpec {
-    int T = 1;
-    bool halo = false, glo = false, ghi = false;
-    int64_t n = 0, ds = 0, plane = 0;
-    std::vector<int64_t> r0, r1, lo, hi;
-};
-
-struct PNode {
-    PhysKind kind;
-    int tile;
-    std::vector<int> preds_first; // iteration right after a fork point
-    std::vector<int> preds_intra; // same-iteration predecessors (steady state)
-    std::vector<int> preds_cross; // previous-iteration predecessors
-};
-
-} // namespace tw
 
 using namespace tw;
 
@@ -207,116 +109,6 @@ struct tw_cg {
 
 namespace tw {
 namespace {
-
-// Synthetic byte addresses for the ledger: one 2^40-byte window per array,
-// element i of array k at (k << 40) + 8 i.  Only overlap matters for edges.
-enum Arr : uint64_t { A_X = 1, A_R, A_P, A_AP, A_PA, A_RR, A_RTRANS, A_ALPHA, A_BETA };
-Acc reg(Arr a, int64_t i0, int64_t i1, int mode) {
-    return Acc{(static_cast<uint64_t>(a) << 40) + 8u * static_cast<uint64_t>(i0),
-               (static_cast<uint64_t>(a) << 40) + 8u * static_cast<uint64_t>(i1), mode};
-}
-
-// spawn_iteration (cg.cpp:166-334): same tasks, labels and access regions;
-// plus, across GPUs, a halo task that refreshes p's ghost planes.  p is
-// addressed in local x coordinates (ghost planes included).
-void build_logical(const DagSpec& d, int iter, std::vector<LTask>& out,
-                   std::vector<PNode>* nodes) {
-    const int T = d.T;
-    const int64_t ds = d.ds;
-    auto tag = [iter](const char* fam, int t) {
-        return std::string(fam) + ":" + std::to_string(iter) + ":" + std::to_string(t);
-    };
-    out.clear();
-    const bool halo = d.halo;
-    const int off_spmv = halo ? 1 : 0, off_alpha = off_spmv + T, off_upd = off_alpha + 1,
-              off_beta = off_upd + T, off_updp = off_beta + 1;
-    if (nodes) {
-        nodes->clear();
-        if (halo) nodes->push_back(PNode{PK_HALO, 0, {}, {}, {}});
-        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_SPMV, t, {}, {}, {}});
-        nodes->push_back(PNode{PK_ALPHA, 0, {}, {}, {}});
-        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_UPD, t, {}, {}, {}});
-        nodes->push_back(PNode{PK_BETA, 0, {}, {}, {}});
-        for (int t = 0; t < T; ++t) nodes->push_back(PNode{PK_UPDP, t, {}, {}, {}});
-    }
-    if (halo) {
-        std::vector<Acc> acc;
-        const int64_t n = d.n, pl = d.plane;
-        if (d.glo) {
-            acc.push_back(reg(A_P, ds, ds + pl, ACC_R));
-            acc.push_back(reg(A_P, 0, pl, ACC_W));
-        }
-        if (d.ghi) {
-            acc.push_back(reg(A_P, ds + n - pl, ds + n, ACC_R));
-            acc.push_back(reg(A_P, ds + n, ds + n + pl, ACC_W));
-        }
-        out.push_back(LTask{tag("halo", 0), acc, 0});
-    }
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("spmv", t),
-                            {reg(A_P, d.lo[t], d.hi[t] + 1, ACC_R),
-                             reg(A_AP, d.r0[t], d.r1[t], ACC_W)},
-                            off_spmv + t});
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("dot_pAp", t),
-                            {reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_R),
-                             reg(A_AP, d.r0[t], d.r1[t], ACC_R), reg(A_PA, t, t + 1, ACC_W)},
-                            off_spmv + t});
-    out.push_back(LTask{tag("alpha", 0),
-                        {reg(A_PA, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_R),
-                         reg(A_ALPHA, 0, 1, ACC_W)},
-                        off_alpha});
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("x_up", t),
-                            {reg(A_ALPHA, 0, 1, ACC_R),
-                             reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_R),
-                             reg(A_X, d.r0[t], d.r1[t], ACC_RW)},
-                            off_upd + t});
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("r_up", t),
-                            {reg(A_ALPHA, 0, 1, ACC_R), reg(A_AP, d.r0[t], d.r1[t], ACC_R),
-                             reg(A_R, d.r0[t], d.r1[t], ACC_RW)},
-                            off_upd + t});
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("dot_rr", t),
-                            {reg(A_R, d.r0[t], d.r1[t], ACC_R), reg(A_RR, t, t + 1, ACC_W)},
-                            off_upd + t});
-    out.push_back(LTask{tag("beta_res", 0),
-                        {reg(A_RR, 0, T, ACC_R), reg(A_RTRANS, 0, 1, ACC_RW),
-                         reg(A_BETA, 0, 1, ACC_W)},
-                        off_beta});
-    for (int t = 0; t < T; ++t)
-        out.push_back(LTask{tag("p_up", t),
-                            {reg(A_BETA, 0, 1, ACC_R), reg(A_R, d.r0[t], d.r1[t], ACC_R),
-                             reg(A_P, ds + d.r0[t], ds + d.r1[t], ACC_RW)},
-                            off_updp + t});
-}
-
-// Runs the ledger over `iters` iterations; returns logical edges (global
-// task ids = iter * tasks_per_iter + k) and, optionally, the label list.
-void logical_edges(const DagSpec& d, int iters, std::vector<std::pair<int, int>>& edges,
-                   std::vector<std::string>* labels, std::vector<int>* phys_of) {
-    Ledger led;
-    std::vector<LTask> it_tasks;
-    int base = 0;
-    for (int it = 0; it < iters; ++it) {
-        build_logical(d, it, it_tasks, nullptr);
-        for (size_t k = 0; k < it_tasks.size(); ++k) {
-            const int id = base + static_cast<int>(k);
-            std::vector<int> pr;
-            for (const Acc& a : it_tasks[k].acc) led.conflicts(a, pr);
-            std::sort(pr.begin(), pr.end());
-            pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
-            for (int p : pr)
-                if (p != id) edges.emplace_back(p, id);
-            for (const Acc& a : it_tasks[k].acc) led.record(a, id);
-            if (labels) labels->push_back(it_tasks[k].label);
-            if (phys_of) phys_of->push_back(it_tasks[k].phys);
-        }
-        base += static_cast<int>(it_tasks.size());
-    }
-    std::sort(edges.begin(), edges.end());
-}
 
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
 void build_schedule(tw_cg* cg) {
@@ -409,9 +201,6 @@ void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; 
                     cg->history, launch_blocks(cg, false), s);
 }
 
-// One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
-// stream; across ranks the SpMV is split so the interior rows overlap the
-// halo exchange on the comm stream.
 // Timing event k (0..3) of the current timed iteration, or null.
 cudaEvent_t tmark(tw_cg* cg, int k) {
     if (!cg->timing) return nullptr;
@@ -436,6 +225,9 @@ void record(cudaEvent_t e, cudaStream_t s) {
         TW_CUDA(cudaEventRecord(e, s));
 }
 
+// One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
+// stream; across ranks the SpMV is split so the interior rows overlap the
+// halo exchange on the comm stream.
 void enqueue_mono(tw_cg* cg) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
@@ -1219,12 +1011,7 @@ int tw_cg_iteration_times(tw_cg* cg, double* seconds, int count) {
 int tw_cg_task_edges(tw_cg* cg, char* buf, int64_t cap, int64_t* needed) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
-        std::vector<std::pair<int, int>> edges;
-        std::vector<std::string> labels;
-        logical_edges(cg->dag, std::max(cg->enqueued, 1), edges, &labels, nullptr);
-        std::ostringstream os;
-        for (auto [a, b] : edges) os << labels[static_cast<size_t>(a)] << ' ' << labels[static_cast<size_t>(b)] << '\n';
-        const std::string s = os.str();
+        const std::string s = edges_text(cg->dag, std::max(cg->enqueued, 1));
         if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
         if (buf && cap > 0) {
             const int64_t k = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
@@ -1272,40 +1059,6 @@ int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_i
 
 int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations) {
     return guarded([&] { group_iterate(cgs, nranks, iterations); });
-}
-
-int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_t* r1,
-                      const int64_t* band_lo, const int64_t* band_hi, int64_t diag_shift,
-                      int64_t plane, int ghost_lo, int ghost_hi, int iterations, char* buf,
-                      int64_t cap, int64_t* needed) {
-    return guarded([&] {
-        if (tiles < 1 || n_rows < tiles) config_error("tile plan needs 1 <= tiles <= rows");
-        if (iterations < 1) config_error("iterations must be positive");
-        DagSpec d;
-        d.T = tiles;
-        d.n = n_rows;
-        d.ds = diag_shift;
-        d.plane = plane;
-        d.glo = ghost_lo != 0;
-        d.ghi = ghost_hi != 0;
-        d.halo = d.glo || d.ghi;
-        d.r0.assign(r0, r0 + tiles);
-        d.r1.assign(r1, r1 + tiles);
-        d.lo.assign(band_lo, band_lo + tiles);
-        d.hi.assign(band_hi, band_hi + tiles);
-        std::vector<std::pair<int, int>> edges;
-        std::vector<std::string> labels;
-        logical_edges(d, iterations, edges, &labels, nullptr);
-        std::ostringstream os;
-        for (auto [a, b] : edges) os << labels[static_cast<size_t>(a)] << ' ' << labels[static_cast<size_t>(b)] << '\n';
-        const std::string s = os.str();
-        if (needed) *needed = static_cast<int64_t>(s.size()) + 1;
-        if (buf && cap > 0) {
-            const int64_t k = std::min<int64_t>(cap - 1, static_cast<int64_t>(s.size()));
-            std::memcpy(buf, s.data(), static_cast<size_t>(k));
-            buf[k] = '\0';
-        }
-    });
 }
 
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
