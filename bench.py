@@ -59,6 +59,26 @@ def parse():
     return ap.parse_args()
 
 
+def baseline_metric() -> str:
+    """BASELINE.json's metric, verbatim (the line reports that metric)."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "CG GFLOP/s and iters/s at 1/2/4/8 B200; % of HBM roofline; vs host-CPU ref"
+
+
+def workload_config(args, world: int) -> dict:
+    """The `config` both arms report (BASELINE.json configs[2]/[3])."""
+    nz = args.nz if args.strong else args.nz * world
+    return {"workload": (f"HPCCG {args.nx}x{args.ny}x{args.nz} " +
+                         ("global strong scaling" if args.strong else
+                          "per GPU weak scaling (z-slab)")),
+            "global_grid": [args.nx, args.ny, nz],
+            "l2": "inputs larger than L2 (6.9 GB/iteration vs 126 MB)",
+            "parallelism": f"z-slab x{world}"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -226,14 +246,14 @@ def run_reference_arm(args, dist, rank, world):
     flops = (2 * M.nnz + 10 * M.n) * args.steps
     v = flops / secs / 1e9
     line = {
-        "impl": "reference", "metric": "CG GFLOP/s (HPCCG 27-pt stencil, fp64)", "value": v,
+        "impl": "reference", "metric": baseline_metric(), "value": v,
         "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (xorshift64 seed 7 rhs)",
         "iters_per_s": args.steps / secs,
-        "config": {"workload": f"HPCCG {args.nx}x{args.ny}x{args.nz} per GPU weak scaling; "
-                               f"reference step = one CG iteration on the {args.nx}x{args.ny}x{nzs} "
-                               f"grid", "variant": "cg_tasks (reference, CPU threads)"},
+        "config": {**workload_config(args, world),
+                   "variant": "cg_tasks (the reference, on the host cores)",
+                   "reference_step": f"one CG iteration on the {args.nx}x{args.ny}x{nzs} grid"},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
                          "sample": f"cg_tasks real threads tiles={tiles} on {args.nx}x{args.ny}x{nzs}, "
                                    f"{args.steps} iterations after {args.warmup} warm-up"},
@@ -409,20 +429,15 @@ def run_ours(args, dist, rank, world, local):
 
     if rank == 0:
         line = {
-            "metric": "CG GFLOP/s (HPCCG 27-pt stencil, fp64)", "value": gflops, "unit": "GFLOP/s",
+            "metric": baseline_metric(), "value": gflops, "unit": "GFLOP/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K,
             "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: gen_stencil_matrix on device, b = xorshift64 seed 7, x0 = 0",
             "iters_per_s": its,
-            "config": {"workload": (f"HPCCG {nx}x{ny}x{args.nz} " +
-                                    ("global strong scaling" if args.strong else
-                                     "per GPU weak scaling (z-slab)")),
-                       "global_grid": [nx, ny, nz], "variant": args.variant,
+            "config": {**workload_config(args, world), "variant": args.variant,
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
-                       "l2": "inputs larger than L2 (6.9 GB/iteration vs 126 MB)",
-                       "parallelism": f"z-slab x{world}",
                        "nccl_comm": world > 1 or args.comm},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
