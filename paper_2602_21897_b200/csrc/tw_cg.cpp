@@ -52,7 +52,6 @@ struct tw_cg {
     double* parts = nullptr;
     double* block_parts = nullptr;
     unsigned* tickets = nullptr;
-    unsigned* tile_ctr = nullptr; // finished tiles of the alpha / beta_res joins (wrap to 0)
     int maxg = 0;
 
     // partial slots (offsets into parts)
@@ -275,35 +274,28 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
     case PK_HALO:
         halo_exchange(cg, st);
         break;
-    case PK_SPMV: {
-        // one rank: the last tile kernel to finish runs the alpha task itself
-        const Fin fin = cg->dist ? Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}
-                                 : Fin{FIN_TILE_ALPHA, cg->pa + t, cg->sc, nullptr, cg->pa, cg->T,
-                                       cg->tile_ctr};
+    case PK_SPMV:
         launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0}, true,
-                    cg->slot(t), fin, bs, st);
+                    cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
         break;
-    }
     case PK_ALPHA:
-        // one rank: a pure join (event edges only); alpha was computed by the
-        // last SpMV tile.  Across ranks: tile-order sum, allgather, rank order.
-        if (cg->dist) {
+        if (!cg->dist) {
+            launch_combine(cg->pa, cg->T, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
+        } else {
             launch_combine(cg->pa, cg->T, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, st);
             allgather1(cg, cg->send_a, cg->recv_a, st);
             launch_combine(cg->recv_a, cg->P, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
         }
         break;
-    case PK_UPD: {
-        const Fin fin = cg->dist ? Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}
-                                 : Fin{FIN_TILE_BETA, cg->rrp + t, cg->sc, cg->history, cg->rrp,
-                                       cg->T, cg->tile_ctr + 1};
+    case PK_UPD:
         launch_update_xr(cg->t_r0[t], cg->t_r1[t], cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
-                         ScalarSrc{nullptr, 0}, cg->slot(t), fin, bv, st);
+                         ScalarSrc{nullptr, 0}, cg->slot(t),
+                         Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}, bv, st);
         break;
-    }
     case PK_BETA:
-        // one rank: a pure join; the last update tile ran beta_res
-        if (cg->dist) {
+        if (!cg->dist) {
+            launch_combine(cg->rrp, cg->T, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
+        } else {
             launch_combine(cg->rrp, cg->T, Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, st);
             allgather1(cg, cg->send_b, cg->recv_b, st);
             launch_combine(cg->recv_b, cg->P, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
@@ -408,7 +400,6 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->parts);
     cudaFree(cg->block_parts);
     cudaFree(cg->tickets);
-    cudaFree(cg->tile_ctr);
     for (auto& kv : cg->dag_tables) {
         auto& t = kv.second;
         cudaFree(t.d_tasks);
@@ -508,8 +499,6 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaMalloc(&cg->block_parts, sizeof(double) * static_cast<size_t>(cg->maxg) * T));
         TW_CUDA(cudaMalloc(&cg->tickets, sizeof(unsigned) * 4 * T));
         TW_CUDA(cudaMemset(cg->tickets, 0, sizeof(unsigned) * 4 * T));
-        TW_CUDA(cudaMalloc(&cg->tile_ctr, sizeof(unsigned) * 2));
-        TW_CUDA(cudaMemset(cg->tile_ctr, 0, sizeof(unsigned) * 2));
         TW_CUDA(cudaEventCreateWithFlags(&cg->fork_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->halo_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->pready_ev, cudaEventDisableTiming));
@@ -554,7 +543,6 @@ void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s) 
     TW_CUDA(cudaMemsetAsync(cg->x, 0, bytes, s));
     TW_CUDA(cudaMemsetAsync(cg->Ap, 0, bytes, s));
     TW_CUDA(cudaMemsetAsync(cg->p_local, 0, sizeof(double) * static_cast<size_t>(cg->x_len), s));
-    TW_CUDA(cudaMemsetAsync(cg->tile_ctr, 0, sizeof(unsigned) * 2, s));
     const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, k, s));
     TW_CUDA(cudaMemcpyAsync(cg->p_owned, cg->r, bytes, cudaMemcpyDeviceToDevice, s));
@@ -1083,7 +1071,7 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;
         } else {
-            k = 3 * cg->T + (cg->dist ? 4 : 0); // one rank: alpha / beta_res fold into the tiles
+            k = 3 * cg->T + (cg->dist ? 4 : 2);
             c = cg->dist ? 3 : 0;
         }
         if (kernels) *kernels = k;

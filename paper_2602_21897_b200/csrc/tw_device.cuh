@@ -44,51 +44,28 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
     return t;
 }
 
-// alpha task (cg.cpp:217-222): alpha = rtrans / pAp
-__device__ __forceinline__ void fin_alpha(CgScalars* sc, double pAp) {
-    sc->pAp = pAp;
-    sc->alpha = __ddiv_rn(sc->rtrans, pAp);
-}
-
-// beta_res task (cg.cpp:299-309): beta, rtrans, history[iter++]
-__device__ __forceinline__ void fin_beta(CgScalars* sc, double* history, double rr) {
-    sc->rr = rr;
-    sc->beta = __ddiv_rn(rr, sc->rtrans);
-    sc->rtrans = rr;
-    if (sc->iter < sc->history_cap) history[sc->iter] = __dsqrt_rn(rr);
-    sc->iter = sc->iter + 1;
-}
-
 __device__ __forceinline__ void finalize(const Fin& fin, double total) {
     switch (fin.mode) {
     case FIN_STORE:
         *fin.out = total;
         break;
     case FIN_ALPHA:
-        fin_alpha(fin.sc, total);
+        fin.sc->pAp = total;
+        fin.sc->alpha = __ddiv_rn(fin.sc->rtrans, total);
         break;
-    case FIN_BETA:
-        fin_beta(fin.sc, fin.history, total);
+    case FIN_BETA: {
+        CgScalars* sc = fin.sc;
+        sc->rr = total;
+        sc->beta = __ddiv_rn(total, sc->rtrans);
+        sc->rtrans = total;
+        if (sc->iter < sc->history_cap) fin.history[sc->iter] = __dsqrt_rn(total);
+        sc->iter = sc->iter + 1;
         break;
+    }
     case FIN_RTRANS:
         fin.sc->rtrans = total;
         fin.sc->iter = 0;
         break;
-    case FIN_TILE_ALPHA:
-    case FIN_TILE_BETA: {
-        *fin.out = total;
-        __threadfence();
-        const unsigned done = atomicInc(fin.counter, static_cast<unsigned>(fin.nparts - 1));
-        if (done + 1 != static_cast<unsigned>(fin.nparts)) break;
-        __threadfence(); // every tile partial is visible: tile-order sum
-        double t = 0.0;
-        for (int i = 0; i < fin.nparts; ++i) t = __dadd_rn(t, __ldcg(fin.parts + i));
-        if (fin.mode == FIN_TILE_ALPHA)
-            fin_alpha(fin.sc, t);
-        else
-            fin_beta(fin.sc, fin.history, t);
-        break;
-    }
     default:
         break;
     }

@@ -85,12 +85,7 @@ enum FinMode : int {
     FIN_STORE = 1, // *out = total
     FIN_ALPHA = 2, // pAp = total; alpha = rtrans / pAp
     FIN_BETA = 3,  // rr = total; beta = rr / rtrans; rtrans = rr; history[iter++] = sqrt(rr)
-    FIN_RTRANS = 4, // rtrans = total; iter = 0 (setup_state, cg.cpp:126)
-    // block-task tiles: *out = tile partial; the LAST of the `nparts` tile
-    // kernels to finish sums parts[0..nparts) in tile order and runs the
-    // alpha task (cg.cpp:209-225) / the beta_res task (cg.cpp:290-311)
-    FIN_TILE_ALPHA = 5,
-    FIN_TILE_BETA = 6
+    FIN_RTRANS = 4 // rtrans = total; iter = 0 (setup_state, cg.cpp:126)
 };
 
 struct Fin {
@@ -98,9 +93,6 @@ struct Fin {
     double* out;
     CgScalars* sc;
     double* history;
-    const double* parts = nullptr; // FIN_TILE_*: the tile partials
-    int nparts = 0;
-    unsigned* counter = nullptr;   // FIN_TILE_*: finished tiles (wraps to 0)
 };
 
 // Where an update kernel takes its scalar from: sc->alpha / sc->beta when
