@@ -51,6 +51,9 @@ def parse():
                     help="launch kernels one by one instead of replaying a captured CUDA graph")
     ap.add_argument("--e2e-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
+                    help="multi-rank data path: NCCL halo + allgathers, or NVLink peer stores "
+                         "fused into the kernels (CUDA IPC)")
     ap.add_argument("--comm", action="store_true",
                     help="attach an NCCL communicator even at N=1 (exercises the multi-GPU path)")
     ap.add_argument("--cpu-sample-nz", type=int, default=0,
@@ -302,6 +305,14 @@ def run_ours(args, dist, rank, world, local):
     use_graph = not args.no_graph
     opt = P.CgOptions(tiles=args.tiles, use_graph=use_graph, iteration_marks=False)
     S = P.CgSolver(rt, A, W + KR, opt, variant=variant)
+    peer = args.transport == "peer" and (world > 1 or args.comm)
+    if peer:
+        if variant != 0:
+            raise SystemExit("--transport peer runs the monolithic variant")
+        if world > 1:
+            S.enable_peer_transport()
+        else:
+            S.peer_connect([S.peer_export()])
     kern_timing = variant == 0
     stream = torch.cuda.ExternalStream(rt.compute_stream, device=torch.device("cuda", local))
     if use_graph:
@@ -438,7 +449,8 @@ def run_ours(args, dist, rank, world, local):
             "config": {**workload_config(args, world), "variant": args.variant,
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
-                       "nccl_comm": world > 1 or args.comm},
+                       "nccl_comm": world > 1 or args.comm,
+                       "transport": ("peer" if peer else "nccl") if (world > 1 or args.comm) else None},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,

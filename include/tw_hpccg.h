@@ -235,6 +235,20 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
  * monolithic solver, b[r] its rows of b. */
 int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_is_device);
 int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations);
+/* The emulated group over the NVLink peer transport (below) instead of the
+ * loopback copies: the "peers" are the other ranks' buffers on the device. */
+int tw_cg_group_enable_peer(tw_cg** cgs, int nranks);
+
+/* NVLink peer transport for the monolithic multi-rank iteration: the halo is
+ * stored by K3 straight into the neighbours' ghost planes and the rank
+ * partials of p.Ap / r.r into every rank's receive window, each followed by
+ * a release flag the consumer acquires (no NCCL inside the iteration; NCCL
+ * stays for set_rhs).  Setup: every rank exports a blob (CUDA IPC handles
+ * of its window and p buffer), the blobs are all-gathered in rank order by
+ * the caller, then every rank connects. */
+#define TW_PEER_BLOB_BYTES 256
+int tw_cg_peer_export(tw_cg* cg, unsigned char* blob);
+int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs);
 
 /* cg_monolithic / cg_tasks in one call (cg.cpp:397-447): host b in, host
  * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17). */

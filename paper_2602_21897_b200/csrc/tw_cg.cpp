@@ -17,6 +17,7 @@
 // edges between pooled streams (or edges of a captured CUDA graph).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -40,6 +41,14 @@ struct tw_cg {
     int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
     bool glo = false, ghi = false;
     tw_slab_t slab{}; // z-slab geometry (multi-rank)
+    // NVLink peer transport (tw_peer.cu): own receive window, links to the
+    // other ranks, device copy of the links, IPC mappings to release
+    bool peer = false;
+    PeerWindow* win = nullptr;
+    PeerLinks links{};
+    PeerLinks* d_links = nullptr;
+    std::vector<void*> ipc_mapped;
+    unsigned epoch = 0; // set_rhs count
 
     double* x = nullptr;
     double* r = nullptr;
@@ -201,6 +210,57 @@ void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; 
                     cg->history, launch_blocks(cg, false), s);
 }
 
+// Phases of the peer transport (NVLink stores + flags, fused into the
+// kernels): 4 launches per iteration and no collective call.
+void peer_spmv(tw_cg* cg, cudaStream_t s) {
+    dist_spmv_interior(cg, s); // reads no ghost: overlaps the neighbours' K3 tails
+    const int ng = cg->slab.ghost_lo + cg->slab.ghost_hi;
+    const unsigned long long* gf = cg->slab.ghost_lo ? &cg->win->flag_ghost_lo : &cg->win->flag_ghost_hi;
+    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+                RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
+                Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
+                launch_blocks(cg, true), s, ng ? gf : nullptr, ng);
+}
+
+void peer_update_xr(tw_cg* cg, cudaStream_t s) {
+    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+                     ScalarSrc{cg->win->recv_a, cg->P, cg->win->flag_a}, cg->slot(0),
+                     Fin{FIN_PUBLISH_B, cg->send_b, cg->sc, nullptr, cg->d_links, nullptr},
+                     launch_blocks(cg, false), s);
+}
+
+void peer_update_p(tw_cg* cg, cudaStream_t s) {
+    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
+                    ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
+                    launch_blocks(cg, false), s, cg->d_links);
+}
+
+void alloc_window(tw_cg* cg) {
+    if (!cg->dist) contract_error("the peer transport needs a multi-rank context");
+    if (cg->opt.variant != TW_CG_MONOLITHIC)
+        config_error("the peer transport runs the monolithic variant");
+    if (cg->P > kMaxRanks) config_error("more ranks than the peer window holds");
+    if (!cg->win) {
+        TW_CUDA(cudaMalloc(&cg->win, sizeof(PeerWindow)));
+        TW_CUDA(cudaMemset(cg->win, 0, sizeof(PeerWindow)));
+    }
+}
+
+void finish_links(tw_cg* cg) {
+    cg->links.rank = cg->ctx->rank;
+    cg->links.nranks = cg->P;
+    cg->links.plane = cg->plane;
+    if (!cg->d_links) TW_CUDA(cudaMalloc(&cg->d_links, sizeof(PeerLinks)));
+    TW_CUDA(cudaMemcpy(cg->d_links, &cg->links, sizeof(PeerLinks), cudaMemcpyHostToDevice));
+    cg->peer = true;
+    if (cg->graph) { // graphs captured before the switch used the NCCL path
+        cudaGraphExecDestroy(cg->graph);
+        cg->graph = nullptr;
+    }
+    for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
+    cg->timed_graphs.clear();
+}
+
 // Timing event k (0..3) of the current timed iteration, or null.
 cudaEvent_t tmark(tw_cg* cg, int k) {
     if (!cg->timing) return nullptr;
@@ -243,6 +303,17 @@ void enqueue_mono(tw_cg* cg) {
         record(tmark(cg, 2), s);
         launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
                         cg->history, bv, s);
+        record(tmark(cg, 3), s);
+        if (cg->timing) ++cg->timed;
+        return;
+    }
+    if (cg->peer) {
+        record(tmark(cg, 0), s);
+        peer_spmv(cg, s);
+        record(tmark(cg, 1), s);
+        peer_update_xr(cg, s);
+        record(tmark(cg, 2), s);
+        peer_update_p(cg, s);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
@@ -400,6 +471,9 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->parts);
     cudaFree(cg->block_parts);
     cudaFree(cg->tickets);
+    for (void* m : cg->ipc_mapped) cudaIpcCloseMemHandle(m);
+    cudaFree(cg->win);
+    cudaFree(cg->d_links);
     for (auto& kv : cg->dag_tables) {
         auto& t = kv.second;
         cudaFree(t.d_tasks);
@@ -539,6 +613,7 @@ void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s) 
     const size_t bytes = sizeof(double) * static_cast<size_t>(cg->n);
     CgScalars init{};
     init.history_cap = cg->max_iters;
+    init.epoch = ++cg->epoch;
     TW_CUDA(cudaMemcpyAsync(cg->sc, &init, sizeof(init), cudaMemcpyHostToDevice, s));
     TW_CUDA(cudaMemsetAsync(cg->x, 0, bytes, s));
     TW_CUDA(cudaMemsetAsync(cg->Ap, 0, bytes, s));
@@ -569,8 +644,12 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device) {
     TW_CUDA(cudaStreamSynchronize(s));
     set_rhs_prefix(cg, b, on_device, s);
     if (cg->dist) {
+        // the allgather is also the barrier that orders every rank's memset of
+        // its ghost planes before any neighbour's push into them
         allgather1(cg, cg->send_r, cg->recv_r, s);
         launch_combine(cg->recv_r, cg->P, Fin{FIN_RTRANS, nullptr, cg->sc, nullptr}, s);
+        if (cg->peer)
+            launch_peer_push(cg->p_owned, cg->n, cg->plane, cg->links, cg->sc, cg->tickets, s);
     }
     TW_CUDA(cudaStreamSynchronize(s));
     reset_solve_state(cg);
@@ -627,6 +706,28 @@ void group_join(tw_cg** g, int P, cudaStream_t s) {
     for (int r = 1; r < P; ++r) TW_CUDA(cudaStreamWaitEvent(g[r]->ctx->compute, g[0]->fork_ev, 0));
 }
 
+// Peer transport inside the emulated group: the "peer" pointers are the
+// other ranks' buffers on the same device.
+void group_enable_peer(tw_cg** g, int P) {
+    group_check(g, P);
+    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
+    for (int r = 0; r < P; ++r) alloc_window(g[r]);
+    for (int r = 0; r < P; ++r) {
+        PeerLinks& L = g[r]->links;
+        L = PeerLinks{};
+        for (int q = 0; q < P; ++q) L.win[q] = g[q]->win;
+        if (r > 0) {
+            L.ghost_lo_dst = g[r - 1]->p_local + g[r - 1]->slab.recv_hi;
+            L.ghost_lo_flag = &g[r - 1]->win->flag_ghost_hi;
+        }
+        if (r + 1 < P) {
+            L.ghost_hi_dst = g[r + 1]->p_local + g[r + 1]->slab.recv_lo;
+            L.ghost_hi_flag = &g[r + 1]->win->flag_ghost_lo;
+        }
+        finish_links(g[r]);
+    }
+}
+
 void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
     group_check(g, P);
     TW_CUDA(cudaSetDevice(g[0]->ctx->device));
@@ -636,6 +737,10 @@ void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
     loopback_allgather(g, P, &tw_cg::send_r, &tw_cg::recv_r, s);
     for (int r = 0; r < P; ++r)
         launch_combine(g[r]->recv_r, P, Fin{FIN_RTRANS, nullptr, g[r]->sc, nullptr}, s);
+    if (g[0]->peer)
+        for (int r = 0; r < P; ++r)
+            launch_peer_push(g[r]->p_owned, g[r]->n, g[r]->plane, g[r]->links, g[r]->sc,
+                             g[r]->tickets, s);
     TW_CUDA(cudaStreamSynchronize(s));
     for (int r = 0; r < P; ++r) reset_solve_state(g[r]);
 }
@@ -651,7 +756,12 @@ void group_iterate(tw_cg** g, int P, int k) {
         TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
         TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
     }
-    for (int it = 0; it < k; ++it) {
+    for (int it = 0; it < k && g[0]->peer; ++it) { // peer transport: stores + flags
+        for (int r = 0; r < P; ++r) peer_spmv(g[r], s);
+        for (int r = 0; r < P; ++r) peer_update_xr(g[r], s);
+        for (int r = 0; r < P; ++r) peer_update_p(g[r], s);
+    }
+    for (int it = 0; it < k && !g[0]->peer; ++it) {
         loopback_halo(g, P, s);
         for (int r = 0; r < P; ++r) {
             dist_spmv_interior(g[r], s);
@@ -1061,12 +1171,86 @@ int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations) {
     return guarded([&] { group_iterate(cgs, nranks, iterations); });
 }
 
+int tw_cg_group_enable_peer(tw_cg** cgs, int nranks) {
+    return guarded([&] { group_enable_peer(cgs, nranks); });
+}
+
+// blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
+// byte offset of the lower ghost plane in p_base, [136,144) of the upper,
+// [144,148) rank.
+int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
+    return guarded([&] {
+        if (!cg || !blob) contract_error("null solver or blob");
+        TW_CUDA(cudaSetDevice(cg->ctx->device));
+        alloc_window(cg);
+        std::memset(blob, 0, TW_PEER_BLOB_BYTES);
+        cudaIpcMemHandle_t hw, hp;
+        TW_CUDA(cudaIpcGetMemHandle(&hw, cg->win));
+        TW_CUDA(cudaIpcGetMemHandle(&hp, cg->p_base));
+        std::memcpy(blob, &hw, sizeof(hw));
+        std::memcpy(blob + 64, &hp, sizeof(hp));
+        const int64_t lo = (cg->p_local + cg->slab.recv_lo - cg->p_base) * static_cast<int64_t>(sizeof(double));
+        const int64_t hi = (cg->p_local + cg->slab.recv_hi - cg->p_base) * static_cast<int64_t>(sizeof(double));
+        std::memcpy(blob + 128, &lo, 8);
+        std::memcpy(blob + 136, &hi, 8);
+        const int rank = cg->ctx->rank;
+        std::memcpy(blob + 144, &rank, 4);
+    });
+}
+
+int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
+    return guarded([&] {
+        if (!cg || !blobs) contract_error("null solver or blobs");
+        TW_CUDA(cudaSetDevice(cg->ctx->device));
+        alloc_window(cg);
+        const int P = cg->P, me = cg->ctx->rank;
+        PeerLinks& L = cg->links;
+        L = PeerLinks{};
+        auto open = [&](const unsigned char* h) {
+            cudaIpcMemHandle_t mh;
+            std::memcpy(&mh, h, sizeof(mh));
+            void* p = nullptr;
+            TW_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+            cg->ipc_mapped.push_back(p);
+            return static_cast<unsigned char*>(p);
+        };
+        for (int q = 0; q < P; ++q) {
+            const unsigned char* b = blobs + static_cast<size_t>(q) * TW_PEER_BLOB_BYTES;
+            int rq = -1;
+            std::memcpy(&rq, b + 144, 4);
+            if (rq != q) contract_error("peer blobs must be in rank order");
+            if (q == me) {
+                L.win[q] = cg->win;
+                continue;
+            }
+            auto* w = reinterpret_cast<PeerWindow*>(open(b));
+            L.win[q] = w;
+            if (q == me - 1 || q == me + 1) {
+                unsigned char* pb = open(b + 64);
+                int64_t lo = 0, hi = 0;
+                std::memcpy(&lo, b + 128, 8);
+                std::memcpy(&hi, b + 136, 8);
+                if (q == me - 1) { // my first plane -> its upper ghost
+                    L.ghost_lo_dst = reinterpret_cast<double*>(pb + hi);
+                    L.ghost_lo_flag = &w->flag_ghost_hi;
+                } else {           // my last plane -> its lower ghost
+                    L.ghost_hi_dst = reinterpret_cast<double*>(pb + lo);
+                    L.ghost_hi_flag = &w->flag_ghost_lo;
+                }
+            }
+        }
+        finish_links(cg);
+    });
+}
+
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
         int k = 0, c = 0;
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             k = 0; // one launch per tw_cg_iterate call, whatever its iteration count
+        } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->peer) {
+            k = 4; // K1 interior, K1 boundary (+wait, publish), K2 (+wait, publish), K3 (+wait, halo)
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;

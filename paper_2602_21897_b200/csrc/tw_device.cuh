@@ -44,6 +44,34 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
     return t;
 }
 
+// ------------------------------------------------ peer transport primitives
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Flag stamp of the current iteration (+ahead): solve epoch << 32 | iter + 1.
+__device__ __forceinline__ unsigned long long stamp_of(const CgScalars* sc, int ahead) {
+    return (static_cast<unsigned long long>(sc->epoch) << 32) |
+           static_cast<unsigned long long>(sc->iter + 1 + ahead);
+}
+
+// Block-wide: thread 0 acquire-spins until every flag carries `want`; the
+// barrier extends the acquire to the block.  Call from uniform control flow.
+__device__ __forceinline__ void block_wait_flags(const unsigned long long* flags, int count,
+                                                 unsigned long long want) {
+    if (threadIdx.x == 0)
+        for (int i = 0; i < count; ++i)
+            while (ld_acquire_sys(flags + i) < want) __nanosleep(32);
+    __syncthreads();
+}
+
 __device__ __forceinline__ void finalize(const Fin& fin, double total) {
     switch (fin.mode) {
     case FIN_STORE:
@@ -66,6 +94,19 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         fin.sc->rtrans = total;
         fin.sc->iter = 0;
         break;
+    case FIN_PUBLISH_A:
+    case FIN_PUBLISH_B: {
+        if (fin.out) *fin.out = total;
+        const double v = fin.pre ? __dadd_rn(__dadd_rn(0.0, *fin.pre), total) : total;
+        const PeerLinks* L = fin.links;
+        const bool a = fin.mode == FIN_PUBLISH_A;
+        const int me = L->rank, P = L->nranks;
+        for (int q = 0; q < P; ++q) (a ? L->win[q]->recv_a : L->win[q]->recv_b)[me] = v;
+        __threadfence_system();
+        const unsigned long long st = stamp_of(fin.sc, 0);
+        for (int q = 0; q < P; ++q) st_release_sys((a ? L->win[q]->flag_a : L->win[q]->flag_b) + me, st);
+        break;
+    }
     default:
         break;
     }

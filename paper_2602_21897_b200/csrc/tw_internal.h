@@ -71,6 +71,34 @@ struct CgScalars {
     double rr;
     int iter;      // iterations completed (index into history)
     int history_cap;
+    unsigned epoch; // solve number (set_rhs count): high half of the peer flag stamps
+    unsigned pad_;
+};
+
+// ------------------------------------------------- NVLink peer transport
+
+constexpr int kMaxRanks = 64;
+
+// Per-rank receive window in device memory; peers store into it over NVLink.
+struct PeerWindow {
+    double recv_a[kMaxRanks];               // p.Ap partial of rank q
+    double recv_b[kMaxRanks];               // r.r partial of rank q
+    unsigned long long flag_a[kMaxRanks];   // stamp of recv_a[q]
+    unsigned long long flag_b[kMaxRanks];   // stamp of recv_b[q]
+    unsigned long long flag_ghost_lo;       // my lower ghost plane holds rank-1's data
+    unsigned long long flag_ghost_hi;       // my upper ghost plane holds rank+1's data
+};
+
+// Where this rank's data goes (device pointers: own, IPC-mapped or, for the
+// emulated group, other ranks' buffers on the same device).
+struct PeerLinks {
+    int rank, nranks;
+    PeerWindow* win[kMaxRanks];         // every rank's window (own included)
+    double* ghost_lo_dst;               // rank-1's upper ghost plane <- my first plane
+    double* ghost_hi_dst;               // rank+1's lower ghost plane <- my last plane
+    unsigned long long* ghost_lo_flag;  // rank-1's flag_ghost_hi
+    unsigned long long* ghost_hi_flag;  // rank+1's flag_ghost_lo
+    int64_t plane;
 };
 
 // Scratch for fixed-order grid reductions: one partial per block plus a
@@ -85,22 +113,34 @@ enum FinMode : int {
     FIN_STORE = 1, // *out = total
     FIN_ALPHA = 2, // pAp = total; alpha = rtrans / pAp
     FIN_BETA = 3,  // rr = total; beta = rr / rtrans; rtrans = rr; history[iter++] = sqrt(rr)
-    FIN_RTRANS = 4 // rtrans = total; iter = 0 (setup_state, cg.cpp:126)
+    FIN_RTRANS = 4, // rtrans = total; iter = 0 (setup_state, cg.cpp:126)
+    // peer transport: *out = total (if out); v = pre ? (0 + *pre) + total :
+    // total; v -> recv_a / recv_b [rank] of every rank's window over NVLink,
+    // then the matching flags get this iteration's stamp (release, .sys)
+    FIN_PUBLISH_A = 5,
+    FIN_PUBLISH_B = 6
 };
+
+struct PeerLinks;
 
 struct Fin {
     int mode;
     double* out;
     CgScalars* sc;
     double* history;
+    const PeerLinks* links; // FIN_PUBLISH_*: device copy of the links
+    const double* pre;      // FIN_PUBLISH_A: the interior rows' partial
 };
 
 // Where an update kernel takes its scalar from: sc->alpha / sc->beta when
 // count == 0, else recomputed per block from `count` partials summed in
 // order (the cross-rank allgather result).
+// With `flags` (peer transport) every block first acquire-waits until the
+// `count` flags carry this iteration's stamp, then reads the partials.
 struct ScalarSrc {
     const double* parts;
     int count;
+    const unsigned long long* flags;
 };
 
 // ---------------------------------------------------------------- launchers
@@ -117,17 +157,24 @@ struct RowRange {
 };
 
 // K1: y = A x over up to two local row ranges; optional fused dot(x_diag, y).
+// With `wait_flags` (peer transport: the ghost-plane flags) every block
+// first acquire-waits for this iteration's stamp (fin.sc) before gathering.
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
-                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s);
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
+                 const unsigned long long* wait_flags = nullptr, int nwait = 0);
 // K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
                       Fin fin, int blocks, cudaStream_t s);
 // K3: p = r + beta p (beta from sc or recomputed from partials; with
 // partials, the last block also commits rtrans/history/iter).
+// With `links` (device copy), K3 also stores the first / last owned plane
+// into the neighbours' ghost planes and its last block raises their flags.
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s);
+                     cudaStream_t s, const PeerLinks* links = nullptr);
+void launch_peer_push(const double* p_owned, int64_t n, int64_t plane, const PeerLinks& L,
+                      const CgScalars* sc, unsigned* ticket, cudaStream_t s);
 // K4: dot(a, b) over [i0, i1) with finalize.
 void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
                 int blocks, cudaStream_t s);

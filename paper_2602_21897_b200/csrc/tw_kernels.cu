@@ -93,7 +93,8 @@ __device__ __forceinline__ double slice_row_generic(const double* __restrict__ v
 template <bool DOT>
 __global__ void __launch_bounds__(kThreads)
 spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
-            RowRange rb, RedScratch rs, Fin fin) {
+            RowRange rb, RedScratch rs, Fin fin, const unsigned long long* wait_flags, int nwait) {
+    if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
     const int lane = threadIdx.x & 31;
     const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -131,7 +132,8 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
 template <bool DOT>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
-                RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin) {
+                RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin,
+                const unsigned long long* wait_flags, int nwait) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps][kTmaStages];
     __shared__ int stage_w[kTmaWarps][kTmaStages];
@@ -167,6 +169,9 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     if (lane == 0)
         for (int st = 0; st < kTmaStages && st < mine; ++st) issue(st, st);
     __syncwarp();
+    // peer transport: the matrix is already streaming in; the gathers of p
+    // wait until the neighbours' ghost planes have landed
+    if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
     double part = 0.0;
     for (int64_t k = 0; k < mine; ++k) {
         const int st = static_cast<int>(k % kTmaStages);
@@ -220,6 +225,7 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
                  double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
                  ScalarSrc asrc, RedScratch rs, Fin fin) {
     double alpha;
+    if (asrc.flags) block_wait_flags(asrc.flags, asrc.count, stamp_of(sc, 0));
     if (asrc.count > 0)
         alpha = __ddiv_rn(sc->rtrans, sum_parts(asrc.parts, asrc.count));
     else
@@ -257,8 +263,20 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 
 __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
-                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history) {
+                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
+                const PeerLinks* links) {
     double beta, rr = 0.0;
+    // fused halo (peer transport): the first / last owned plane also goes
+    // straight into the neighbours' ghost planes over NVLink
+    double* lo_dst = links ? links->ghost_lo_dst : nullptr;
+    double* hi_dst = links ? links->ghost_hi_dst : nullptr;
+    const int64_t plane = links ? links->plane : 0, hi_first = i1 - plane;
+    bool remote = false; // this thread stored into a neighbour's ghost plane
+    auto halo = [&](int64_t i, double v) {
+        if (lo_dst && i < plane) { lo_dst[i] = v; remote = true; }
+        if (hi_dst && i >= hi_first) { hi_dst[i - hi_first] = v; remote = true; }
+    };
+    if (bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
         rr = sum_parts(bsrc.parts, bsrc.count);
         beta = __ddiv_rn(rr, sc->rtrans);
@@ -272,29 +290,53 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
             pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
             pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
             *reinterpret_cast<double2*>(p + e) = pv;
+            if (links) {
+                halo(e, pv.x);
+                halo(e + 1, pv.y);
+            }
         } else {
-            if (lo) p[e] = __dadd_rn(r[e], __dmul_rn(beta, p[e]));
-            if (hi) p[e + 1] = __dadd_rn(r[e + 1], __dmul_rn(beta, p[e + 1]));
+            if (lo) {
+                p[e] = __dadd_rn(r[e], __dmul_rn(beta, p[e]));
+                if (links) halo(e, p[e]);
+            }
+            if (hi) {
+                p[e + 1] = __dadd_rn(r[e + 1], __dmul_rn(beta, p[e + 1]));
+                if (links) halo(e + 1, p[e + 1]);
+            }
         }
     });
     if (bsrc.count > 0) {
         // Every block read rtrans above; the last one through commits the
-        // iteration (beta_res task, cg.cpp:290-311).
+        // iteration (beta_res task, cg.cpp:290-311) and, with the peer
+        // transport, raises the neighbours' ghost flags for the next one.
         __shared__ bool last;
-        __syncthreads();
+        // only the few blocks that stored ghost planes pay the system-scope
+        // fence (their NVLink stores land before the ticket); the rest order
+        // at GPU scope and the last block's system fence + release follows
+        const bool sys = __syncthreads_or(remote);
         if (threadIdx.x == 0) {
-            __threadfence();
+            if (sys)
+                __threadfence_system();
+            else
+                __threadfence();
             unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
             last = (t == gridDim.x - 1);
         }
         __syncthreads();
         if (last && threadIdx.x == 0) {
-            __threadfence();
+            __threadfence_system();
+            const unsigned long long next =
+                (static_cast<unsigned long long>(sc->epoch) << 32) |
+                static_cast<unsigned long long>(sc->iter + 2); // stamp of iteration iter + 1
             sc->rr = rr;
             sc->beta = beta;
             sc->rtrans = rr;
             if (sc->iter < sc->history_cap) history[sc->iter] = __dsqrt_rn(rr);
             sc->iter = sc->iter + 1;
+            if (links) {
+                if (links->ghost_lo_flag) st_release_sys(links->ghost_lo_flag, next);
+                if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
+            }
         }
     }
 }
@@ -619,7 +661,8 @@ int spmv_tma_smem_bytes(int max_width) {
 }
 
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
-                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s) {
+                 bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
+                 const unsigned long long* wait_flags, int nwait) {
     auto slices = [](RowRange r) { return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : 0; };
     const int64_t ns = slices(a) + slices(b);
     if (A.max_width > 0 && A.tma_blocks > 0) {
@@ -647,16 +690,16 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
             }
             int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
             const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin);
+            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin, wait_flags, nwait);
             TW_CUDA(cudaGetLastError());
             return;
         }
     }
     const int g = clamp_blocks(ns * 32, blocks);
     if (with_dot)
-        spmv_kernel<true><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin);
+        spmv_kernel<true><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin, wait_flags, nwait);
     else
-        spmv_kernel<false><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin);
+        spmv_kernel<false><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin, wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
 }
 
@@ -670,9 +713,9 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s) {
+                     cudaStream_t s, const PeerLinks* links) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history);
+    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, links);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -543,6 +543,28 @@ class CgSolver:
         N.check(_lib().tw_cg_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(c), C.byref(k)))
         return a.value, b.value, c.value, k.value
 
+    PEER_BLOB_BYTES = 256
+
+    def peer_export(self) -> bytes:
+        """This rank's CUDA-IPC blob for the NVLink peer transport."""
+        buf = C.create_string_buffer(self.PEER_BLOB_BYTES)
+        N.check(_lib().tw_cg_peer_export(self.h, buf))
+        return buf.raw
+
+    def peer_connect(self, blobs: list) -> None:
+        """blobs: every rank's peer_export() in rank order (allgathered by
+        the caller); switches the iteration to the peer transport."""
+        if any(len(b) != self.PEER_BLOB_BYTES for b in blobs):
+            raise ContractViolation("peer blobs must be PEER_BLOB_BYTES long")
+        N.check(_lib().tw_cg_peer_connect(self.h, b"".join(blobs)))
+
+    def enable_peer_transport(self) -> None:
+        """Collective over torch.distributed: export, allgather, connect."""
+        import torch.distributed as dist
+        blobs = [None] * dist.get_world_size()
+        dist.all_gather_object(blobs, self.peer_export())
+        self.peer_connect(blobs)
+
     def launches_per_iteration(self) -> tuple[int, int]:
         k, c = C.c_int(), C.c_int()
         N.check(_lib().tw_cg_launches_per_iteration(self.h, C.byref(k), C.byref(c)))
@@ -555,8 +577,11 @@ class EmulatedRankGroup:
     Test infrastructure for the multi-rank path on a single B200."""
 
     def __init__(self, nx: int, ny: int, nz: int, nranks: int, max_iterations: int,
-                 device: int = 0):
+                 device: int = 0, transport: str = "loopback"):
+        if transport not in ("loopback", "peer"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.P = nranks
+        self.transport = transport
         self.rts, self.mats, self.solvers = [], [], []
         for r in range(nranks):
             rt = Runtime(device)
@@ -569,6 +594,8 @@ class EmulatedRankGroup:
                                          CgOptions(iteration_marks=False),
                                          variant=N.TW_CG_MONOLITHIC))
         self._arr = (C.c_void_p * nranks)(*[s.h.value for s in self.solvers])
+        if transport == "peer":
+            N.check(_lib().tw_cg_group_enable_peer(self._arr, nranks))
 
     def set_rhs(self, b: np.ndarray) -> None:
         """b: the GLOBAL right-hand side; each rank takes its rows."""

@@ -409,6 +409,18 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     s.close()
     with pytest.raises(P.ConfigError):
         P.CgSolver(rt2, A, 4, P.CgOptions(tiles=4, persistent=True))
+    # the NVLink peer transport on the same 1-rank communicator: export /
+    # connect (own window, no IPC mapping), fused publish / wait kernels
+    for graph in (False, True):
+        s = P.CgSolver(rt2, A, 150, P.CgOptions(use_graph=graph), variant=0)
+        s.peer_connect([s.peer_export()])
+        assert s.launches_per_iteration() == (4, 0)
+        s.set_rhs(b)
+        s.iterate(70)
+        s.iterate(80)
+        check_history(s.history(150), golden["cg_32_xorshift7_history"])
+        assert np.all(rel_gap(s.solution(), golden["cg_32_xorshift7_x"]) <= 1e-10)
+        s.close()
     rt2.close()
 
 
@@ -481,9 +493,10 @@ def test_cg_128cubed_vs_oracle(rt, orc):
 
 # ------------------------------------------- emulated multi-rank group (1 GPU)
 
+@pytest.mark.parametrize("transport", ["loopback", "peer"])
 @pytest.mark.parametrize("dims,P_", [((32, 32, 32), 2), ((40, 24, 30), 3), ((32, 32, 32), 4),
                                      ((24, 20, 16), 8), ((16, 16, 2), 2)])
-def test_emulated_rank_group_matches_single_domain(orc, golden, dims, P_):
+def test_emulated_rank_group_matches_single_domain(orc, golden, dims, P_, transport):
     """P z-slab ranks on the one B200 (tw_cg_group_*): slab matrices, ghost
     planes, interior/boundary SpMV split, rank-ordered scalar sums -- the
     multi-GPU code with loopback copies for the NCCL transport -- must
@@ -491,7 +504,7 @@ def test_emulated_rank_group_matches_single_domain(orc, golden, dims, P_):
     m = orc.stencil(*dims)
     b = orc.rhs_xorshift(m.n, 7)
     want_h, want_x, _ = orc.cg(m, b, 40)
-    G = P.EmulatedRankGroup(*dims, P_, 40)
+    G = P.EmulatedRankGroup(*dims, P_, 40, transport=transport)
     G.set_rhs(b)
     G.iterate(15)
     G.iterate(25)
@@ -503,3 +516,28 @@ def test_emulated_rank_group_matches_single_domain(orc, golden, dims, P_):
     G.close()
     if dims == (32, 32, 32):
         check_history(hs[0], golden["cg_32_xorshift7_history"][:40])
+
+
+def test_peer_transport_resolve_new_epoch(orc):
+    """A second solve on the peer transport: the flag stamps carry the solve
+    epoch, so flags left by the first solve must not release the second."""
+    dims = (24, 24, 24)
+    m = orc.stencil(*dims)
+    G = P.EmulatedRankGroup(*dims, 4, 30, transport="peer")
+    for seed in (3, 11, 3):
+        b = orc.rhs_xorshift(m.n, seed)
+        want_h, want_x, _ = orc.cg(m, b, 30)
+        G.set_rhs(b)
+        G.iterate(30)
+        check_history(G.history(30)[0], want_h)
+        assert np.all(rel_gap(G.solution(), want_x) <= 1e-10)
+    G.close()
+
+
+def test_peer_transport_contract_errors(rt):
+    from paper_2602_21897_b200 import _native as N
+    A = P.gen_stencil_matrix(8, 8, 8, rt=rt)
+    s = P.CgSolver(rt, A, 5, variant=N.TW_CG_MONOLITHIC)
+    with pytest.raises(P.ContractViolation):
+        s.peer_export()  # single-rank context
+    s.close()
