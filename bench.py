@@ -51,9 +51,10 @@ def parse():
                     help="launch kernels one by one instead of replaying a captured CUDA graph")
     ap.add_argument("--e2e-runs", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--transport", choices=["nccl", "peer"], default="nccl",
-                    help="multi-rank data path: NCCL halo + allgathers, or NVLink peer stores "
-                         "fused into the kernels (CUDA IPC)")
+    ap.add_argument("--transport", choices=["auto", "nccl", "peer"], default="auto",
+                    help="multi-rank data path: NVLink peer stores fused into the kernels "
+                         "(CUDA IPC; auto = peer for the monolithic variant, validated "
+                         "against the NCCL path before timing) or NCCL halo + allgathers")
     ap.add_argument("--comm", action="store_true",
                     help="attach an NCCL communicator even at N=1 (exercises the multi-GPU path)")
     ap.add_argument("--cpu-sample-nz", type=int, default=0,
@@ -188,6 +189,16 @@ def max_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
+def min_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return float(t.item())
+
+
 def sum_over_ranks(dist, v: float) -> float:
     if dist is None:
         return v
@@ -305,14 +316,33 @@ def run_ours(args, dist, rank, world, local):
     use_graph = not args.no_graph
     opt = P.CgOptions(tiles=args.tiles, use_graph=use_graph, iteration_marks=False)
     S = P.CgSolver(rt, A, W + KR, opt, variant=variant)
-    peer = args.transport == "peer" and (world > 1 or args.comm)
-    if peer:
-        if variant != 0:
-            raise SystemExit("--transport peer runs the monolithic variant")
+    multi = world > 1 or args.comm
+    want_peer = multi and (args.transport == "peer" or (args.transport == "auto" and variant == 0))
+    if want_peer and variant != 0:
+        raise SystemExit("--transport peer runs the monolithic variant")
+    transport = ("peer" if want_peer else "nccl") if multi else None
+    if want_peer:
         if world > 1:
             S.enable_peer_transport()
         else:
             S.peer_connect([S.peer_export()])
+        # validation before timing: the peer path sums the same partials in
+        # the same order as the NCCL path, so the histories must be identical
+        kv = min(20, W + KR)
+        S0 = P.CgSolver(rt, A, kv, P.CgOptions(use_graph=False, iteration_marks=False), variant=0)
+        S0.set_rhs(b)
+        S0.iterate(kv)
+        h0 = S0.history(kv)
+        S0.close()
+        S.set_rhs(b)
+        S.iterate(kv)
+        ok = float(np.array_equal(S.history(kv), h0))
+        if min_over_ranks(dist, ok) < 1.0:
+            if args.transport == "peer":
+                raise SystemExit("peer transport disagrees with the NCCL path")
+            S.close()  # auto: fall back to the NCCL transport, and say so
+            S = P.CgSolver(rt, A, W + KR, opt, variant=variant)
+            transport = "nccl (peer validation failed)"
     kern_timing = variant == 0
     stream = torch.cuda.ExternalStream(rt.compute_stream, device=torch.device("cuda", local))
     if use_graph:
@@ -450,7 +480,7 @@ def run_ours(args, dist, rank, world, local):
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
                        "nccl_comm": world > 1 or args.comm,
-                       "transport": ("peer" if peer else "nccl") if (world > 1 or args.comm) else None},
+                       "transport": transport},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,

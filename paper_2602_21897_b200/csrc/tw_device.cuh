@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "tw_internal.h"
 
@@ -62,13 +63,40 @@ __device__ __forceinline__ unsigned long long stamp_of(const CgScalars* sc, int 
            static_cast<unsigned long long>(sc->iter + 1 + ahead);
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+#ifndef TW_PEER_TIMEOUT_NS
+#define TW_PEER_TIMEOUT_NS 20000000000ull // 20 s: a peer that never publishes
+#endif
+
 // Block-wide: thread 0 acquire-spins until every flag carries `want`; the
 // barrier extends the acquire to the block.  Call from uniform control flow.
+// A flag that stays stale for TW_PEER_TIMEOUT_NS traps (the context reports
+// an error to every later call) instead of hanging the GPU.
 __device__ __forceinline__ void block_wait_flags(const unsigned long long* flags, int count,
                                                  unsigned long long want) {
-    if (threadIdx.x == 0)
-        for (int i = 0; i < count; ++i)
-            while (ld_acquire_sys(flags + i) < want) __nanosleep(32);
+    if (threadIdx.x == 0) {
+        unsigned long long t0 = 0;
+        for (int i = 0; i < count; ++i) {
+            unsigned spins = 0;
+            while (ld_acquire_sys(flags + i) < want) {
+                __nanosleep(32);
+                if ((++spins & 4095u) == 0) {
+                    const unsigned long long t = global_ns();
+                    if (!t0) t0 = t;
+                    else if (t - t0 > TW_PEER_TIMEOUT_NS) {
+                        printf("tw_hpccg: peer flag %d never reached stamp %llx (has %llx)\n", i,
+                               want, ld_acquire_sys(flags + i));
+                        __trap();
+                    }
+                }
+            }
+        }
+    }
     __syncthreads();
 }
 
