@@ -228,7 +228,9 @@ int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_
                       const int64_t* band_lo, const int64_t* band_hi, int64_t diag_shift,
                       int64_t plane, int ghost_lo, int ghost_hi, int iterations, char* buf,
                       int64_t cap, int64_t* needed);
-/* Physical launches per iteration (kernels + NCCL calls), for reports. */
+/* Physical launches per iteration (kernels + NCCL calls), for reports.
+ * Single-domain monolithic solves fuse K3 into the next iteration's K1:
+ * 2 kernels per iteration plus one K3 per tw_cg_iterate call. */
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
 
 /* Emulated rank group (see tw_ctx_init_emulated_rank): cgs[r] is rank r's

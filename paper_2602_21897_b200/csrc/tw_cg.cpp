@@ -78,6 +78,13 @@ struct tw_cg {
 
     cudaGraphExec_t graph = nullptr;
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
+    std::map<int, cudaGraphExec_t> k_graphs;     // K fused iterations, untimed
+    // single-domain monolithic: K3 fused into the next iteration's K1
+    // (launch_spmv_fusep) with p ping-ponging between p_owned and p_alt;
+    // every tw_cg_iterate call starts and ends with p in p_owned
+    bool fusep = false;
+    double* p_alt = nullptr;
+    double* p_cur = nullptr;
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;
@@ -259,6 +266,8 @@ void finish_links(tw_cg* cg) {
     }
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     cg->timed_graphs.clear();
+    for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
+    cg->k_graphs.clear();
 }
 
 // Timing event k (0..3) of the current timed iteration, or null.
@@ -288,21 +297,37 @@ void record(cudaEvent_t e, cudaStream_t s) {
 // One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
 // stream; across ranks the SpMV is split so the interior rows overlap the
 // halo exchange on the comm stream.
-void enqueue_mono(tw_cg* cg) {
+//
+// Single domain, `fuse` (iteration i of a k-iteration call): iteration 0 runs
+// K1 on p; every later one runs K1 with the previous iteration's K3 fused in
+// (p_new = r + beta p_old formed on the fly, stored to the other buffer);
+// the last one ends with K3 proper, back into p_owned.  The arithmetic is
+// K3's, so the results are those of the three-kernel sequence.
+void enqueue_mono(tw_cg* cg, int i = 0, int k = 1, bool fuse = false) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
     if (!cg->dist) {
+        const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
-        launch_spmv(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs,
-                    Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, bs, s);
+        if (fuse && i > 0) {
+            double* next = cg->p_cur == cg->p_owned ? cg->p_alt : cg->p_owned;
+            if (!launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n, rs, fa, s))
+                throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
+            cg->p_cur = next;
+        } else {
+            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s);
+        }
         record(tmark(cg, 1), s);
-        launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
+        launch_update_xr(0, cg->n, cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
                          rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s);
         record(tmark(cg, 2), s);
-        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                        cg->history, bv, s);
+        if (!fuse || i == k - 1) {
+            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                            cg->history, bv, s, nullptr, cg->p_cur);
+            cg->p_cur = cg->p_owned;
+        }
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
@@ -452,6 +477,8 @@ void free_cg(tw_cg* cg) {
     cg->ta.reset();
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
+    cudaFree(cg->p_alt);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
@@ -554,6 +581,16 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + pad) + 2)));
         cg->p_local = cg->p_base + pad;
         cg->p_owned = cg->p_local + cg->diag_shift;
+        cg->p_cur = cg->p_owned;
+        {
+            const char* f = std::getenv("TW_FUSE_P");
+            cg->fusep = cg->opt.variant == TW_CG_MONOLITHIC && !cg->dist &&
+                        cg->opt.dispatch != TW_DISPATCH_PERSISTENT && A->info.max_width > 0 &&
+                        ctx->cfg.tma_blocks > 0 &&
+                        spmv_tma_smem_bytes(A->info.max_width) + 4096 <= 227 * 1024 &&
+                        f && f[0] == '1'; // opt-in: measured slower
+            if (cg->fusep) TW_CUDA(cudaMalloc(&cg->p_alt, sizeof(double) * (n + 2)));
+        }
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
         TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
         const int T = cg->T, P = cg->P;
@@ -936,19 +973,24 @@ void iterate(tw_cg* cg, int k) {
         cg->enqueued += k;
         return;
     }
-    if (cg->opt.use_graph && cg->timing && cg->opt.variant == TW_CG_MONOLITHIC) {
-        // k iterations as ONE graph with the K1/K2/K3 timing events inside:
-        // graph-launch efficiency and per-kernel durations of the same run
-        auto it = cg->timed_graphs.find(k);
-        if (it == cg->timed_graphs.end()) {
+    // the K3 fusion needs the whole call in one piece: streams, or a
+    // k-iteration graph (per-iteration host marks need the 1-iteration graph)
+    const bool fuse = cg->fusep && (!cg->opt.use_graph || cg->timing || !cg->opt.iteration_marks);
+    if (cg->opt.use_graph && cg->opt.variant == TW_CG_MONOLITHIC && (cg->timing || fuse)) {
+        // k iterations as ONE graph; timed: with the K1/K2/K3 timing events
+        // inside (graph-launch efficiency and per-kernel durations of one run)
+        auto& cache = cg->timing ? cg->timed_graphs : cg->k_graphs;
+        auto it = cache.find(k);
+        if (it == cache.end()) {
             cudaGraph_t g = nullptr;
             cg->timed = 0;
             TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
-                for (int i = 0; i < k; ++i) enqueue_mono(cg);
+                for (int i = 0; i < k; ++i) enqueue_mono(cg, i, k, fuse);
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);
+                cg->p_cur = cg->p_owned;
                 throw;
             }
             TW_CUDA(cudaStreamEndCapture(s, &g));
@@ -956,10 +998,10 @@ void iterate(tw_cg* cg, int k) {
             cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
             cudaGraphDestroy(g);
             TW_CUDA(e);
-            it = cg->timed_graphs.emplace(k, ge).first;
+            it = cache.emplace(k, ge).first;
         }
         TW_CUDA(cudaGraphLaunch(it->second, s));
-        cg->timed = k; // the graph records timing slots 0..k-1
+        if (cg->timing) cg->timed = k; // the graph records timing slots 0..k-1
         cg->enqueued += k;
         return;
     }
@@ -971,6 +1013,8 @@ void iterate(tw_cg* cg, int k) {
         const int it = cg->enqueued + i;
         if (cg->opt.use_graph) {
             TW_CUDA(cudaGraphLaunch(cg->graph, s));
+        } else if (!tasks) {
+            enqueue_mono(cg, i, k, fuse);
         } else {
             enqueue_iteration_body(cg, it & 1, i == 0);
         }
@@ -1251,6 +1295,8 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
             k = 0; // one launch per tw_cg_iterate call, whatever its iteration count
         } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->peer) {
             k = 4; // K1 interior, K1 boundary (+wait, publish), K2 (+wait, publish), K3 (+wait, halo)
+        } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fusep) {
+            k = 2; // K1 (with the previous K3 fused in) + K2; one K3 per tw_cg_iterate call
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;

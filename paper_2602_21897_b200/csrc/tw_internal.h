@@ -172,7 +172,14 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 // into the neighbours' ghost planes and its last block raises their flags.
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, const PeerLinks* links = nullptr);
+                     cudaStream_t s, const PeerLinks* links = nullptr,
+                     const double* psrc = nullptr);
+// K1 with the previous iteration's K3 fused in (single-domain monolithic):
+// Ap = A p_new and p_new . Ap where p_new = r + beta p_old (beta = sc->beta)
+// is formed on the fly from gathers of r and p_old and stored into p_new
+// (a different buffer).  False when the TMA-staged path is unavailable.
+bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
+                       double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
 void launch_peer_push(const double* p_owned, int64_t n, int64_t plane, const PeerLinks& L,
                       const CgScalars* sc, unsigned* ticket, cudaStream_t s);
 // K4: dot(a, b) over [i0, i1) with finalize.

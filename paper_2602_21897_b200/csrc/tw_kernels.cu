@@ -129,11 +129,76 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
 }
 
 
-template <bool DOT>
+// One row with the previous iteration's p update fused in (FUSEP): every
+// operand is p_new[c] = r[c] + beta * p_old[c] (waxpby, cg.cpp:389),
+// rounded exactly as K3 rounds it, gathered from r and p_old.
+template <int W>
+__device__ __forceinline__ double smem_row_fixed_fusep(const double* vb, const int32_t* cb,
+                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ p, double beta,
+                                                       int lane) {
+    int c[W];
+#pragma unroll
+    for (int q = 0; q < W / 4; ++q) {
+        int4 t = reinterpret_cast<const int4*>(cb + 128 * q)[lane];
+        c[4 * q] = t.x;
+        c[4 * q + 1] = t.y;
+        c[4 * q + 2] = t.z;
+        c[4 * q + 3] = t.w;
+    }
+    constexpr int F = W & ~3;
+    if (W - F >= 2) {
+        int2 t = reinterpret_cast<const int2*>(cb + 32 * F)[lane];
+        c[F] = t.x;
+        c[F + 1] = t.y;
+    }
+    if ((W - F) & 1) c[W - 1] = cb[32 * (W - 1) + lane];
+    double rv[W], pv[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        rv[k] = __ldg(r + max(c[k], 0));
+        pv[k] = __ldg(p + max(c[k], 0));
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
+        if (c[2 * j] >= 0)
+            acc = __dadd_rn(acc, __dmul_rn(v.x, __dadd_rn(rv[2 * j], __dmul_rn(beta, pv[2 * j]))));
+        if (c[2 * j + 1] >= 0)
+            acc = __dadd_rn(acc, __dmul_rn(v.y, __dadd_rn(rv[2 * j + 1], __dmul_rn(beta, pv[2 * j + 1]))));
+    }
+    if (W & 1)
+        if (c[W - 1] >= 0)
+            acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane],
+                                           __dadd_rn(rv[W - 1], __dmul_rn(beta, pv[W - 1]))));
+    return acc;
+}
+
+__device__ __forceinline__ double smem_row_generic_fusep(const double* vb, const int32_t* cb,
+                                                         const double* __restrict__ r,
+                                                         const double* __restrict__ p, double beta,
+                                                         int lane, int w) {
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+        const int c = cb[ell_col_pos(k, lane, w)];
+        if (c < 0) break;
+        const double pn = __dadd_rn(__ldg(r + c), __dmul_rn(beta, __ldg(p + c)));
+        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], pn));
+    }
+    return acc;
+}
+
+// FUSEP (single-domain monolithic CG): x is p_old, and the kernel also
+// applies the previous iteration's K3 -- gathers p_new from r and p_old,
+// writes p_new for its own rows into pnew (the other buffer of a ping-pong
+// pair, so no block ever reads a p it overwrites) and dots with p_new.
+template <bool DOT, bool FUSEP = false>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
                 RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin,
-                const unsigned long long* wait_flags, int nwait) {
+                const unsigned long long* wait_flags, int nwait, const double* __restrict__ r,
+                double* __restrict__ pnew) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps][kTmaStages];
     __shared__ int stage_w[kTmaWarps][kTmaStages];
@@ -172,6 +237,7 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     // peer transport: the matrix is already streaming in; the gathers of p
     // wait until the neighbours' ghost planes have landed
     if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
+    const double beta = FUSEP ? fin.sc->beta : 0.0;
     double part = 0.0;
     for (int64_t k = 0; k < mine; ++k) {
         const int st = static_cast<int>(k % kTmaStages);
@@ -180,19 +246,35 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         const double* vb = reinterpret_cast<const double*>(ring + static_cast<size_t>(st) * stage_bytes);
         const int32_t* cb = reinterpret_cast<const int32_t*>(ring + static_cast<size_t>(st) * stage_bytes + val_bytes);
         double acc;
-        switch (w) {
-        case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
-        case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
-        case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
-        case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
-        default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
+        if (FUSEP) {
+            switch (w) {
+            case 27: acc = smem_row_fixed_fusep<27>(vb, cb, r, x, beta, lane); break;
+            case 18: acc = smem_row_fixed_fusep<18>(vb, cb, r, x, beta, lane); break;
+            case 12: acc = smem_row_fixed_fusep<12>(vb, cb, r, x, beta, lane); break;
+            case 8: acc = smem_row_fixed_fusep<8>(vb, cb, r, x, beta, lane); break;
+            default: acc = smem_row_generic_fusep(vb, cb, r, x, beta, lane, w); break;
+            }
+        } else {
+            switch (w) {
+            case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
+            case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
+            case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
+            case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
+            default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
+            }
         }
         const int64_t s = slice_of(k);
         const int64_t row = (s << 5) + lane;
-        const RowRange r = (warp_g + k * nwarps) < na ? ra : rb;
-        if (row >= r.r0 && row < r.r1) {
+        const RowRange rr = (warp_g + k * nwarps) < na ? ra : rb;
+        if (row >= rr.r0 && row < rr.r1) {
             y[row] = acc;
-            if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
+            if (FUSEP) {
+                const double pn = __dadd_rn(__ldg(r + row), __dmul_rn(beta, __ldg(x + row)));
+                pnew[row] = pn;
+                if (DOT) part = __dadd_rn(part, __dmul_rn(pn, acc));
+            } else if (DOT) {
+                part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
+            }
         }
         __syncwarp();
         if (lane == 0 && k + kTmaStages < mine) {
@@ -261,10 +343,16 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
     grid_reduce_finalize(part, rs, fin);
 }
 
+// PEER: the peer-transport instantiation (flag wait, fused halo stores);
+// the plain one stays lean so the grid keeps its full occupancy.
+template <bool PEER>
 __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
-                const PeerLinks* links) {
+                const PeerLinks* links_, const double* __restrict__ psrc) {
+    // psrc: p_old, == p in place (each element is read, then written, by the
+    // same thread, so the restrict-qualified aliasing is never observable)
+    const PeerLinks* links = PEER ? links_ : nullptr;
     double beta, rr = 0.0;
     // fused halo (peer transport): the first / last owned plane also goes
     // straight into the neighbours' ghost planes over NVLink
@@ -276,35 +364,52 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
         if (lo_dst && i < plane) { lo_dst[i] = v; remote = true; }
         if (hi_dst && i >= hi_first) { hi_dst[i - hi_first] = v; remote = true; }
     };
-    if (bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
+    if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
         rr = sum_parts(bsrc.parts, bsrc.count);
         beta = __ddiv_rn(rr, sc->rtrans);
     } else {
         beta = sc->beta;
     }
-    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
-        if (lo && hi) {
-            double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
-            double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
-            pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
-            pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-            *reinterpret_cast<double2*>(p + e) = pv;
-            if (links) {
-                halo(e, pv.x);
-                halo(e + 1, pv.y);
-            }
-        } else {
-            if (lo) {
-                p[e] = __dadd_rn(r[e], __dmul_rn(beta, p[e]));
-                if (links) halo(e, p[e]);
-            }
-            if (hi) {
-                p[e + 1] = __dadd_rn(r[e + 1], __dmul_rn(beta, p[e + 1]));
-                if (links) halo(e + 1, p[e + 1]);
-            }
+    // Full pairs [a, b) with 128-bit accesses, two pairs per thread and
+    // step (both pairs' loads issued before either store: twice the bytes
+    // in flight of a one-pair loop); the at most two ragged ends go scalar.
+    auto one = [&](int64_t i) {
+        const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
+        p[i] = v;
+        if (links) halo(i, v);
+    };
+    auto pair = [&](int64_t e, double2 rv, double2 pv) {
+        pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+        pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+        *reinterpret_cast<double2*>(p + e) = pv;
+        if (links) {
+            halo(e, pv.x);
+            halo(e + 1, pv.y);
         }
-    });
+    };
+    {
+        const int64_t a = (i0 + 1) & ~int64_t(1), b = i1 & ~int64_t(1);
+        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        for (int64_t j = (a >> 1) + tid; j < (b >> 1); j += 2 * stride) {
+            const int64_t e0 = 2 * j, e1 = 2 * (j + stride);
+            const bool two = e1 < b;
+            const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
+            const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
+            double2 r1 = make_double2(0.0, 0.0), p1 = r1;
+            if (two) {
+                r1 = __ldcs(reinterpret_cast<const double2*>(r + e1));
+                p1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
+            }
+            pair(e0, r0, p0);
+            if (two) pair(e1, r1, p1);
+        }
+        if (tid == 0) {
+            if ((i0 & 1) && i0 < i1) one(i0);
+            if (b < i1 && b >= i0 && b >= a) one(b);
+        }
+    }
     if (bsrc.count > 0) {
         // Every block read rtrans above; the last one through commits the
         // iteration (beta_res task, cg.cpp:290-311) and, with the peer
@@ -660,47 +765,63 @@ int spmv_tma_smem_bytes(int max_width) {
     return kTmaWarps * kTmaStages * tma_stage_bytes(max_width, &vb);
 }
 
+// The TMA-staged SpMV needs one slice block of the widest slice per warp in
+// shared memory; returns false when that does not fit (then the register
+// path runs).  The opt-in shared-memory size is a per-device attribute.
+template <bool DOT, bool FUSEP>
+static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
+                            RedScratch rs, Fin fin, cudaStream_t s, const unsigned long long* wait_flags,
+                            int nwait, const double* r, double* pnew) {
+    if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
+    const int64_t ns = slices(a) + slices(b);
+    int vb;
+    const int stage = tma_stage_bytes(A.max_width, &vb);
+    const int smem = kTmaWarps * kTmaStages * stage;
+    auto kern = spmv_tma_kernel<DOT, FUSEP>;
+    constexpr int kMaxDev = 64;
+    static std::mutex mu;
+    static int attr_bytes[kMaxDev] = {};
+    static int static_bytes = -1;
+    int dev = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_bytes < 0) {
+        cudaFuncAttributes fa;
+        TW_CUDA(cudaFuncGetAttributes(&fa, kern));
+        static_bytes = static_cast<int>(fa.sharedSizeBytes);
+    }
+    if (dev >= kMaxDev || smem + static_bytes > 227 * 1024) return false;
+    if (attr_bytes[dev] < smem) {
+        TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_bytes[dev] = smem;
+    }
+    const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
+    const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
+    kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin, wait_flags, nwait, r, pnew);
+    TW_CUDA(cudaGetLastError());
+    return true;
+}
+
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
                  const unsigned long long* wait_flags, int nwait) {
-    auto slices = [](RowRange r) { return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : 0; };
-    const int64_t ns = slices(a) + slices(b);
-    if (A.max_width > 0 && A.tma_blocks > 0) {
-        int vb;
-        const int stage = tma_stage_bytes(A.max_width, &vb);
-        const int smem = kTmaWarps * kTmaStages * stage;
-        auto kern = with_dot ? spmv_tma_kernel<true> : spmv_tma_kernel<false>;
-        // the opt-in shared-memory size is a per-device function attribute
-        constexpr int kMaxDev = 64;
-        static std::mutex mu;
-        static int attr_bytes[kMaxDev][2] = {};
-        static int static_bytes = -1;
-        int dev = 0;
-        TW_CUDA(cudaGetDevice(&dev));
-        std::lock_guard<std::mutex> lk(mu);
-        if (static_bytes < 0) {
-            cudaFuncAttributes fa;
-            TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_kernel<true>));
-            static_bytes = static_cast<int>(fa.sharedSizeBytes);
-        }
-        if (dev < kMaxDev && smem + static_bytes <= 227 * 1024) {
-            if (attr_bytes[dev][with_dot] < smem) {
-                TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr_bytes[dev][with_dot] = smem;
-            }
-            int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
-            const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-            kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin, wait_flags, nwait);
-            TW_CUDA(cudaGetLastError());
-            return;
-        }
-    }
-    const int g = clamp_blocks(ns * 32, blocks);
+    if (with_dot ? launch_spmv_tma<true, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr, nullptr)
+                 : launch_spmv_tma<false, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr, nullptr))
+        return;
+    auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
+    const int g = clamp_blocks((slices(a) + slices(b)) * 32, blocks);
     if (with_dot)
         spmv_kernel<true><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin, wait_flags, nwait);
     else
         spmv_kernel<false><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin, wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
+}
+
+bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
+                       double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s) {
+    return launch_spmv_tma<true, true>(A, p_old, Ap, RowRange{0, n}, RowRange{0, 0}, rs, fin, s,
+                                       nullptr, 0, r, p_new);
 }
 
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
@@ -713,9 +834,21 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, const PeerLinks* links) {
-    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    update_p_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, links);
+                     cudaStream_t s, const PeerLinks* links, const double* psrc) {
+    // grid: at most one resident wave of this instantiation (a partial
+    // second wave of a grid-stride loop would double the tail)
+    static int occ[2] = {0, 0};
+    const bool peer = links != nullptr || bsrc.flags != nullptr;
+    auto kern = peer ? update_p_kernel<true> : update_p_kernel<false>;
+    if (!occ[peer]) {
+        int o = 0, dev = 0, sms = 0;
+        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0));
+        TW_CUDA(cudaGetDevice(&dev));
+        TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        occ[peer] = (o > 0 ? o : 1) * sms;
+    }
+    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < occ[peer] ? blocks : occ[peer]);
+    kern<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, links, psrc ? psrc : p);
     TW_CUDA(cudaGetLastError());
 }
 

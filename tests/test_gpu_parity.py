@@ -541,3 +541,48 @@ def test_peer_transport_contract_errors(rt):
     with pytest.raises(P.ContractViolation):
         s.peer_export()  # single-rank context
     s.close()
+
+
+def _read_dev(rt, ptr, n):
+    import ctypes
+    from paper_2602_21897_b200 import _native as N
+    out = np.zeros(n, np.float64)
+    N.check(N.load().tw_memcpy(rt.h, out.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(ptr),
+                               8 * n, None))
+    rt.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, monkeypatch):
+    """Single-domain monolithic CG fuses K3 (p = r + beta p) into the next
+    iteration's K1 with p ping-ponging between two buffers (opt-in,
+    TW_FUSE_P=1).  Against the unfused K1/K2/K3 sequence every residual, x and the p
+    left behind by each tw_cg_iterate call must be bit-identical, whatever
+    the split of the iterations into calls (odd splits end in the other
+    buffer and are copied back by the final K3)."""
+    from paper_2602_21897_b200 import _native as N
+    A = P.gen_stencil_matrix(30, 20, 18, rt=rt)
+    b = orc.rhs_xorshift(A.n, 5)
+    splits = [1, 1, 3, 2, 7, 6]
+    total = sum(splits)
+    runs = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("TW_FUSE_P", fuse)
+        s = P.CgSolver(rt, A, total, P.CgOptions(use_graph=graph, iteration_marks=False),
+                       variant=N.TW_CG_MONOLITHIC)
+        assert s.launches_per_iteration()[0] == (2 if fuse == "1" else 3)
+        s.set_rhs(b)
+        ps = []
+        for k in splits:
+            s.iterate(k)
+            ps.append(_read_dev(rt, s.vectors()[2], A.n))
+        runs.append((s.history(total), s.solution(), ps))
+        s.close()
+    (h1, x1, p1), (h0, x0, p0) = runs
+    assert np.array_equal(h1, h0)
+    assert np.array_equal(x1, x0)
+    for a, c in zip(p1, p0):
+        assert np.array_equal(a, c)
+    want_h, want_x, _ = orc.cg(orc.stencil(30, 20, 18), b, total)
+    check_history(h1, want_h)
