@@ -69,6 +69,10 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 
 constexpr int kComputeWarps = kDagWarps - 1; // warp kDagWarps-1 schedules
+#ifndef TW_DAG_VEC_UNROLL
+#define TW_DAG_VEC_UNROLL 2
+#endif
+constexpr int kVecUnroll = TW_DAG_VEC_UNROLL; // pairs in flight per thread in update chunks
 constexpr int kSlots = 2;
 
 struct Slot {
@@ -135,27 +139,57 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         if (b > T.r1) b = T.r1;
         // pairs (2q, 2q+1) inside [a, b) with 128-bit accesses, ragged ends scalar
         const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
-        for (int64_t q = q0 + ctid; q < q1; q += cthreads) {
-            const int64_t e = 2 * q;
+        // kVecUnroll pairs per thread and step, every load issued before the
+        // first store: the few compute warps of a dispatcher CTA need that
+        // many bytes in flight to stream at HBM rate.  The per-thread sum
+        // still runs q, q + cthreads, q + 2 cthreads, ... as a one-pair loop.
+        constexpr int U = kVecUnroll;
+        for (int64_t q = q0 + ctid; q < q1; q += U * cthreads) {
             if (upd) {
-                double2 xv = *reinterpret_cast<const double2*>(P.x + e);
-                const double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
-                double2 rv = *reinterpret_cast<const double2*>(P.r + e);
-                const double2 av = *reinterpret_cast<const double2*>(P.Ap + e);
-                xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
-                xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-                rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
-                rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                *reinterpret_cast<double2*>(P.x + e) = xv;
-                *reinterpret_cast<double2*>(P.r + e) = rv;
-                part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
-                part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+                double2 xv[U], pv[U], rv[U], av[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
+                    if (e < 2 * q1) {
+                        xv[u] = *reinterpret_cast<const double2*>(P.x + e);
+                        pv[u] = *reinterpret_cast<const double2*>(P.p_owned + e);
+                        rv[u] = *reinterpret_cast<const double2*>(P.r + e);
+                        av[u] = *reinterpret_cast<const double2*>(P.Ap + e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
+                    if (e < 2 * q1) {
+                        xv[u].x = __dadd_rn(xv[u].x, __dmul_rn(alpha, pv[u].x));
+                        xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, pv[u].y));
+                        rv[u].x = __dadd_rn(rv[u].x, __dmul_rn(nalpha, av[u].x));
+                        rv[u].y = __dadd_rn(rv[u].y, __dmul_rn(nalpha, av[u].y));
+                        *reinterpret_cast<double2*>(P.x + e) = xv[u];
+                        *reinterpret_cast<double2*>(P.r + e) = rv[u];
+                        part = __dadd_rn(part, __dmul_rn(rv[u].x, rv[u].x));
+                        part = __dadd_rn(part, __dmul_rn(rv[u].y, rv[u].y));
+                    }
+                }
             } else {
-                const double2 rv = *reinterpret_cast<const double2*>(P.r + e);
-                double2 pv = *reinterpret_cast<const double2*>(P.p_owned + e);
-                pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
-                pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-                *reinterpret_cast<double2*>(P.p_owned + e) = pv;
+                double2 rv[U], pv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
+                    if (e < 2 * q1) {
+                        rv[u] = *reinterpret_cast<const double2*>(P.r + e);
+                        pv[u] = *reinterpret_cast<const double2*>(P.p_owned + e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
+                    if (e < 2 * q1) {
+                        pv[u].x = __dadd_rn(rv[u].x, __dmul_rn(beta, pv[u].x));
+                        pv[u].y = __dadd_rn(rv[u].y, __dmul_rn(beta, pv[u].y));
+                        *reinterpret_cast<double2*>(P.p_owned + e) = pv[u];
+                    }
+                }
             }
         }
         const int64_t lo = (a & 1) ? a : -1;                               // odd start
