@@ -72,6 +72,13 @@ def baseline_metric() -> str:
         return "CG GFLOP/s and iters/s at 1/2/4/8 B200; % of HBM roofline; vs host-CPU ref"
 
 
+def l2_note(args) -> str:
+    n, nnz = work(args.nx, args.ny, 0, args.nz, args.nz)
+    gb = (12 * nnz + 88 * n) / 1e9
+    where = "larger than" if gb > 0.126 else "SMALLER than"
+    return f"inputs {where} L2 ({gb:.3g} GB/iteration per GPU vs 126 MB); no flush"
+
+
 def workload_config(args, world: int) -> dict:
     """The `config` both arms report (BASELINE.json configs[2]/[3])."""
     nz = args.nz if args.strong else args.nz * world
@@ -79,7 +86,7 @@ def workload_config(args, world: int) -> dict:
                          ("global strong scaling" if args.strong else
                           "per GPU weak scaling (z-slab)")),
             "global_grid": [args.nx, args.ny, nz],
-            "l2": "inputs larger than L2 (6.9 GB/iteration vs 126 MB)",
+            "l2": l2_note(args),
             "parallelism": f"z-slab x{world}"}
 
 
@@ -209,9 +216,10 @@ def sum_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
-def load_traffic():
-    """ncu dram bytes per K1 launch from the committed profile summary, if any."""
-    p = os.path.join(ROOT, "profiles", "k1_traffic.json")
+def load_traffic(kernel: str = "k1"):
+    """ncu dram bytes per launch of K1 / K2 / K3 from the committed profile
+    summaries (profiles/k?_traffic.json, one ncu --set full capture), if any."""
+    p = os.path.join(ROOT, "profiles", f"{kernel}_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -232,8 +240,12 @@ def cpu_reference_sample(nx, ny, nz_sample, iters, threads):
     M = R.stencil(nx, ny, nz_sample)
     b = o.rhs_xorshift(M.n, 7)
     tiles = min(8 * threads, M.n)
-    R.cg_tasks(M, b, 1, tiles=tiles, workers=threads, real_threads=True)  # warm
-    _, _, secs = R.cg_tasks(M, b, iters, tiles=tiles, workers=threads, real_threads=True)
+    # one run of 1 + iters iterations; the timed span is the reference's own
+    # cg_iter marks after the warm-up iteration (scenario.cpp:116-124), so
+    # runtime start-up and the first touch of the solver state are excluded
+    _, _, _, marks = R.cg_tasks_marks(M, b, 1 + iters, tiles=tiles, workers=threads,
+                                      real_threads=True)
+    secs = float(marks[iters] - marks[0])
     flops = (2 * M.nnz + 10 * M.n) * iters
     return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads,
             "kind": "reference", "iters_per_s": iters / secs,
@@ -254,9 +266,13 @@ def run_reference_arm(args, dist, rank, world):
     M = R.stencil(args.nx, args.ny, nzs)
     b = o.rhs_xorshift(M.n, 7)
     tiles = min(8 * threads, M.n)
-    if args.warmup > 0:
-        R.cg_tasks(M, b, args.warmup, tiles=tiles, workers=threads, real_threads=True)
-    _, _, secs = R.cg_tasks(M, b, args.steps, tiles=tiles, workers=threads, real_threads=True)
+    # W warm-up + K timed iterations in one cg_tasks run; the K steps are
+    # timed by the reference's own cg_iter marks (scenario.cpp:116-124):
+    # mark[W+K-1] - mark[W-1] (from the runtime start when W = 0)
+    W, K = args.warmup, args.steps
+    _, _, _, marks = R.cg_tasks_marks(M, b, W + K, tiles=tiles, workers=threads,
+                                      real_threads=True)
+    secs = float(marks[W + K - 1] - (marks[W - 1] if W > 0 else 0.0))
     flops = (2 * M.nnz + 10 * M.n) * args.steps
     v = flops / secs / 1e9
     line = {
@@ -270,7 +286,8 @@ def run_reference_arm(args, dist, rank, world):
                    "reference_step": f"one CG iteration on the {args.nx}x{args.ny}x{nzs} grid"},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
                          "sample": f"cg_tasks real threads tiles={tiles} on {args.nx}x{args.ny}x{nzs}, "
-                                   f"{args.steps} iterations after {args.warmup} warm-up"},
+                                   f"{args.steps} iterations after {args.warmup} warm-up, "
+                                   f"timed by the reference's cg_iter marks"},
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -421,10 +438,14 @@ def run_ours(args, dist, rank, world, local):
         k1_avg = k1_ms / nt
         ach = k1_bytes / (k1_avg / 1e3) / 1e9
         k3_launches = nrep if fused else nt
-        tr = load_traffic()
-        traffic = None
-        if tr and tr.get("workload") == f"{nx}x{ny}x{args.nz}" and world == 1:
-            traffic = tr.get("dram_bytes_per_launch")
+        wl = f"{nx}x{ny}x{args.nz}"
+
+        def traffic_of(k):
+            tr = load_traffic(k)
+            ok = tr and tr.get("workload") == wl and world == 1 and not fused
+            return tr.get("dram_bytes_per_launch") if ok else None
+
+        traffic = traffic_of("k1")
         kname = ("spmv_tma_kernel<true,true> (K1: TMA-staged SpMV + p.Ap, previous K3 fused)"
                  if fused else "spmv_tma_kernel<true> (K1: TMA-staged SpMV + p.Ap)")
         roofline = {"bound": "hbm", "kernel": kname,
@@ -434,7 +455,9 @@ def run_ours(args, dist, rank, world, local):
                     "share_of_step": k1_ms / ms,
                     "k2_update_xr_gbs": 48 * n / (k2_ms / nt / 1e3) / 1e9,
                     "k3_update_p_gbs": 24 * n / (k3_ms / k3_launches / 1e3) / 1e9,
-                    "k3_launches": k3_launches}
+                    "k3_launches": k3_launches,
+                    "k2_traffic": traffic_of("k2"), "k2_algorithmic_bytes": 48 * n,
+                    "k3_traffic": traffic_of("k3"), "k3_algorithmic_bytes": 24 * n}
     iter_gbs = total_bytes / (ms_max / 1e3 / K) / 1e9
     roofline_iter = {"bound": "hbm", "achieved": iter_gbs, "peak": peak * world, "unit": "GB/s",
                      "frac": iter_gbs / (peak * world), "algorithmic_bytes_per_iter": total_bytes}

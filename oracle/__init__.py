@@ -200,7 +200,7 @@ class Reference:
         L.twref_cg_reference.argtypes = [C.c_void_p, _dp, C.c_int, C.c_double, _dp, _dp,
                                          C.POINTER(C.c_int)]
         L.twref_cg_tasks.argtypes = [C.c_void_p, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
-                                     C.c_int, C.c_int, _dp, _dp, _dp]
+                                     C.c_int, C.c_int, _dp, _dp, _dp, _dp]
         L.twref_cg_task_edges.restype = _i64
         L.twref_cg_task_edges.argtypes = [C.c_void_p, _dp, C.c_int, C.c_int, C.c_char_p, _i64]
 
@@ -287,13 +287,23 @@ class Reference:
     def cg_tasks(self, M, b, iterations, tiles=16, workers=4, real_threads=False,
                  monolithic=False, backend=0):
         """Returns (history, x, wall_seconds)."""
+        h, x, secs, _ = self.cg_tasks_marks(M, b, iterations, tiles, workers, real_threads,
+                                            monolithic, backend)
+        return h, x, secs
+
+    def cg_tasks_marks(self, M, b, iterations, tiles=16, workers=4, real_threads=False,
+                       monolithic=False, backend=0):
+        """Returns (history, x, wall_seconds, marks): marks[i] = time of the
+        reference's cg_iter=i mark (substrate seconds since runtime start;
+        real seconds with real_threads), as scenario.cpp:116-124 reads them."""
         hist = np.zeros(max(iterations, 1), np.float64)
         x = np.zeros(M.n, np.float64)
+        marks = np.zeros(max(iterations, 1), np.float64)
         secs = C.c_double(0.0)
         self._check(self.lib.twref_cg_tasks(M.h, _d(b), iterations, 0 if monolithic else 1,
                                             tiles, workers, 1 if real_threads else 0, backend,
-                                            _d(hist), _d(x), C.byref(secs)))
-        return hist[:iterations], x, secs.value
+                                            _d(hist), _d(x), C.byref(secs), _d(marks)))
+        return hist[:iterations], x, secs.value, marks[:iterations]
 
     def cg_task_edges(self, M, b, iterations, tiles):
         need = self.lib.twref_cg_task_edges(M.h, _d(b), iterations, tiles, None, 0)

@@ -168,9 +168,12 @@ int twref_cg_reference(void* h, const double* b, int iterations, double tol, dou
 // which wall-clock is a CPU performance number.
 // backend 0 = host, 1 = device_ta, 2 = device_blocking (simulated device).
 // Returns wall seconds spent inside the solver call in *seconds.
+// marks (nullable, `iterations` entries): the time of each cg_iter=i mark
+// (cg.cpp:307-308, :427) in substrate seconds since the runtime started --
+// the reference's own per-iteration timing (scenario.cpp:116-124).
 int twref_cg_tasks(void* h, const double* b, int iterations, int variant, int tiles,
                    int workers, int real_threads, int backend, double* history, double* x,
-                   double* seconds) {
+                   double* seconds, double* marks) {
     return guarded([&] {
         auto* m = as_mat(h);
         std::vector<double> bv(b, b + m->n);
@@ -198,6 +201,14 @@ int twref_cg_tasks(void* h, const double* b, int iterations, int variant, int ti
         auto t1 = std::chrono::steady_clock::now();
         if (seconds)
             *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (marks) {
+            std::fill(marks, marks + iterations, 0.0);
+            for (const tw::LogRecord& rec : rt.log().sorted())
+                if (rec.transition == tw::Transition::mark && rec.note.rfind("cg_iter=", 0) == 0) {
+                    const int i = std::stoi(rec.note.substr(sizeof("cg_iter=") - 1));
+                    if (i >= 0 && i < iterations) marks[i] = rec.time;
+                }
+        }
         write_result(r, history, x);
     });
 }

@@ -10,5 +10,9 @@ $CMD > gpurun_out/prof_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 4 -c 1 \
-    -o gpurun_out/prof_k1 -f $CMD > gpurun_out/ncu_full.log 2>&1
+    -o gpurun_out/prof_k1 -f $CMD > gpurun_out/ncu_full.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:update_xr -s 4 -c 1 \
+    -o gpurun_out/prof_k2 -f $CMD > gpurun_out/ncu_full_k2.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:update_p -s 4 -c 1 \
+    -o gpurun_out/prof_k3 -f $CMD > gpurun_out/ncu_full_k3.log 2>&1
 echo "ncu exit $?"

@@ -1,5 +1,7 @@
-"""Summarise a gpurun ncu capture into profiles/ (launch list + K1 full-set metrics).
+"""Summarise a gpurun ncu capture into profiles/ (launch list + full-set metrics
+of K1, and of K2 / K3 when their reports exist next to K1's).
 usage: python scripts/summarize_ncu.py <launches.csv> <prof_k1.ncu-rep> <round tag>"""
+import os
 import collections
 import csv
 import json
@@ -30,22 +32,36 @@ for k, (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     out.append(f"{k:28s} {c:4d} {t / c / 1e3:10.1f} us {b / c / 1e9:8.3f} GB  {sh}")
 open(f"profiles/{tag}_ncu_launches_summary.txt", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-r = list(csv.reader(raw.splitlines()))
-H, U, V = r[0], r[1], r[2]
-keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "l1tex__t_sector_hit_rate.pct",
         "lts__t_sector_hit_rate.pct",
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
-summ = {k: [V[H.index(k)], U[H.index(k)]] for k in keys if k in H}
-scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
-traffic = sum(float(summ[k][0]) * scale[summ[k][1]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-d = {"kernel": "spmv_tma_kernel<true> (K1)", "workload": "256x256x256", "round": tag,
-     "source": "ncu --set full --clock-control none, bench.py --steps 6 --warmup 3",
-     "dram_bytes_per_launch": traffic, "algorithmic_bytes": 12 * 449455096 + 16 * 16777216,
-     "metrics": summ}
-json.dump(d, open("profiles/k1_traffic.json", "w"), indent=1)
-print(json.dumps(d, indent=1))
+SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+NNZ, N = 449455096, 16777216  # 256^3
+
+
+def summarize(rep_path, kernel, algorithmic, out_json):
+    raw = subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    r = list(csv.reader(raw.splitlines()))
+    H, U, V = r[0], r[1], r[2]
+    summ = {k: [V[H.index(k)], U[H.index(k)]] for k in KEYS if k in H}
+    traffic = sum(float(summ[k][0]) * SCALE[summ[k][1]]
+                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    d = {"kernel": kernel, "workload": "256x256x256", "round": tag,
+         "source": "ncu --set full --clock-control none, bench.py --steps 6 --warmup 3",
+         "dram_bytes_per_launch": traffic, "algorithmic_bytes": algorithmic, "metrics": summ}
+    json.dump(d, open(out_json, "w"), indent=1)
+    print(json.dumps(d, indent=1))
+
+
+summarize(rep, "spmv_tma_kernel<true> (K1)", 12 * NNZ + 16 * N, "profiles/k1_traffic.json")
+base = os.path.dirname(rep)
+for name, kern, alg in (("prof_k2.ncu-rep", "update_xr_kernel (K2)", 48 * N),
+                        ("prof_k3.ncu-rep", "update_p_kernel<false> (K3)", 24 * N)):
+    if os.path.exists(os.path.join(base, name)):
+        summarize(os.path.join(base, name), kern, alg,
+                  f"profiles/{name.split('_')[1].split('.')[0]}_traffic.json")

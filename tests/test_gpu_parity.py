@@ -586,3 +586,35 @@ def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, monkeypatc
         assert np.array_equal(a, c)
     want_h, want_x, _ = orc.cg(orc.stencil(30, 20, 18), b, total)
     check_history(h1, want_h)
+
+
+@pytest.mark.parametrize("maxw", [9, 33, 34, 70])
+def test_spmv_generic_widths_tma_and_register_paths(rt, orc, maxw):
+    """Random general matrices whose slice widths are mostly outside the
+    stencil's fixed set {8, 12, 18, 27}: the TMA-staged kernel's generic row
+    body (max width <= 33 fits 18 warps' stages in shared memory) and the
+    register-path fallback (34, 70) must both be bit-exact, including the
+    fused p.Ap dot's inputs (spmv_dot) and ragged last slices."""
+    from oracle import Csr
+    rng = np.random.default_rng(maxw)
+    n = 32 * 37 + 11
+    lens = rng.integers(0, maxw + 1, n)
+    lens[5] = maxw
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, l, replace=False)) for l in lens]).astype(np.int64)
+    va = rng.standard_normal(len(ci))
+    G = P.ell_from_csr(rp, ci, va, rt=rt)
+    assert G.info.max_width == maxw
+    x = rng.standard_normal(n)
+    want = orc.spmv(Csr(n, rp, ci, va), x)
+    y = torch.zeros(n, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(G, dev(x), y, 0, n)
+    assert np.array_equal(host(y), want)
+    # sub-ranges with ragged ends
+    y2 = torch.full((n,), -3.0, dtype=torch.float64, device="cuda:0")
+    P.spmv_range(G, dev(x), y2, 45, n - 7)
+    got = host(y2)
+    assert np.array_equal(got[45:n - 7], want[45:n - 7])
+    assert np.all(got[:45] == -3.0) and np.all(got[n - 7:] == -3.0)
+    d = P.spmv_dot(G, dev(x), y, 0, n)
+    assert abs(d - float(np.dot(x, want))) <= 1e-12 * np.abs(x * want).sum()
