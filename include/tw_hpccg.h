@@ -144,6 +144,15 @@ int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int6
 int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, const double* y,
                     double* w, int64_t i0, int64_t i1, void* stream);
 
+/* exchange_externals (HPCCG's halo step; in the reference, the column band
+ * of make_tile_plan, cg.cpp:356-367, declared as the read region of p,
+ * cg.cpp:177-180): on a z-slab matrix A (tw_gen_stencil_ell with z_begin /
+ * z_end) of a communicator rank, send the first / last owned plane of the
+ * local vector x (x_len entries: [ghost lo] owned [ghost hi]) to the
+ * neighbours and receive theirs into the ghost planes -- one NCCL send/recv
+ * group on `stream`, collective over the ranks.  A no-op for one rank. */
+int tw_halo_exchange(const tw_ell* A, double* x, void* stream);
+
 /* make_tile_plan(A, tiles) (cg.cpp:348-370) over the owned rows; band in
  * GLOBAL columns like the reference.  TW_ERR_CONFIG if tiles < 1 or > rows. */
 int tw_make_tile_plan(const tw_ell* A, int tiles, int64_t* r0, int64_t* r1, int64_t* band_lo,

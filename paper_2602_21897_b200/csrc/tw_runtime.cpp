@@ -745,6 +745,39 @@ int tw_spmv_range(const tw_ell* A, const double* x, double* y, int64_t r0, int64
     });
 }
 
+// exchange_externals for a z-slab: the first / last owned plane of x to the
+// neighbours' ghost planes and theirs into ours, one NCCL send/recv group on
+// `stream` (every rank of the communicator calls it).  Offsets from the slab
+// plan, i.e. the same ones the solver's halo uses.
+int tw_halo_exchange(const tw_ell* A, double* x, void* stream) {
+    return guarded([&] {
+        check_ell(A);
+        tw_ctx* ctx = A->ctx;
+        if (!ctx->nccl_comm) contract_error("halo exchange needs a communicator (tw_ctx_init_comm)");
+        const tw_ell_info_t& in = A->info;
+        if (in.nx == 0) contract_error("halo exchange needs a stencil slab (tw_gen_stencil_ell)");
+        tw_slab_t sp{};
+        if (int rc = tw_slab_plan(in.nx, in.ny, in.nz, in.z_begin, in.z_end, &sp); rc)
+            throw Error(rc, g_last_error);
+        if (sp.ghost_lo != (ctx->rank > 0) || sp.ghost_hi != (ctx->rank < ctx->nranks - 1))
+            contract_error("slab z-range does not match this rank's position");
+        TW_CUDA(cudaSetDevice(ctx->device));
+        const auto& api = nccl();
+        const size_t pl = static_cast<size_t>(in.nx * in.ny);
+        cudaStream_t s = pick(ctx, stream);
+        TW_NCCL(api.GroupStart());
+        if (sp.ghost_lo) {
+            TW_NCCL(api.Recv(x + sp.recv_lo, pl, ncclDouble, ctx->rank - 1, ctx->nccl_comm, s));
+            TW_NCCL(api.Send(x + sp.send_lo, pl, ncclDouble, ctx->rank - 1, ctx->nccl_comm, s));
+        }
+        if (sp.ghost_hi) {
+            TW_NCCL(api.Recv(x + sp.recv_hi, pl, ncclDouble, ctx->rank + 1, ctx->nccl_comm, s));
+            TW_NCCL(api.Send(x + sp.send_hi, pl, ncclDouble, ctx->rank + 1, ctx->nccl_comm, s));
+        }
+        TW_NCCL(api.GroupEnd());
+    });
+}
+
 int tw_spmv_dot(const tw_ell* A, const double* p, double* Ap, int64_t r0, int64_t r1,
                 double* dot_dev, void* stream) {
     return guarded([&] {

@@ -344,6 +344,12 @@ def spmv_dot(A: EllMatrix, p, Ap, r0: int, r1: int, stream: int | None = None) -
     return float(out.download()[0])
 
 
+def halo_exchange(A: EllMatrix, x, stream: int | None = None) -> None:
+    """exchange_externals: ghost planes of the slab vector x (x_len
+    entries) from the neighbouring ranks (NCCL, collective)."""
+    N.check(_lib().tw_halo_exchange(A.h, C.c_void_p(_ptr(x)), C.c_void_p(stream or 0)))
+
+
 def dot_range(a, b, i0: int, i1: int, rt: Runtime | None = None) -> float:
     """dot_range (kernels.cpp:15-20) as a fixed-order device reduction."""
     rt = rt or default_runtime()

@@ -407,6 +407,10 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     s = P.CgSolver(rt2, A, 4, P.CgOptions(), variant=0)
     assert s.launches_per_iteration() == (5, 3)
     s.close()
+    # exchange_externals on the 1-rank communicator: no neighbour, a no-op
+    xv = dev(b)
+    P.halo_exchange(A, xv)
+    assert np.array_equal(host(xv), b)
     with pytest.raises(P.ConfigError):
         P.CgSolver(rt2, A, 4, P.CgOptions(tiles=4, persistent=True))
     # the NVLink peer transport on the same 1-rank communicator: export /
@@ -537,6 +541,8 @@ def test_peer_transport_resolve_new_epoch(orc):
 def test_peer_transport_contract_errors(rt):
     from paper_2602_21897_b200 import _native as N
     A = P.gen_stencil_matrix(8, 8, 8, rt=rt)
+    with pytest.raises(P.ContractViolation):
+        P.halo_exchange(A, dev(np.zeros(A.n)))  # no communicator
     s = P.CgSolver(rt, A, 5, variant=N.TW_CG_MONOLITHIC)
     with pytest.raises(P.ContractViolation):
         s.peer_export()  # single-rank context
