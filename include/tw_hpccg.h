@@ -249,6 +249,12 @@ int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations);
 /* The emulated group over the NVLink peer transport (below) instead of the
  * loopback copies: the "peers" are the other ranks' buffers on the device. */
 int tw_cg_group_enable_peer(tw_cg** cgs, int nranks);
+/* The peer-transport group as ONE cooperative kernel: the ranks' blocks run
+ * concurrently and wait on one another's flags (the multi-GPU protocol under
+ * real concurrency on one device; the per-rank launches of a real multi-GPU
+ * run must never share a GPU).  jitter != 0 delays rank-dependent blocks to
+ * vary the interleavings.  Synchronous. */
+int tw_cg_group_iterate_concurrent(tw_cg** cgs, int nranks, int iterations, int jitter);
 
 /* NVLink peer transport for the monolithic multi-rank iteration: the halo is
  * stored by K3 straight into the neighbours' ghost planes and the rank

@@ -813,6 +813,55 @@ void group_iterate(tw_cg** g, int P, int k) {
     for (int r = 0; r < P; ++r) g[r]->enqueued += k;
 }
 
+// The peer-transport group as ONE cooperative kernel (rank_group_kernel):
+// the ranks run concurrently and really wait on one another's flags.
+void group_iterate_concurrent(tw_cg** g, int P, int k, int jitter) {
+    group_check(g, P);
+    if (!g[0]->peer) contract_error("the concurrent group runs the peer transport (tw_cg_group_enable_peer)");
+    if (k < 0) config_error("negative iteration count");
+    for (int r = 0; r < P; ++r)
+        if (g[r]->enqueued + k > g[r]->max_iters) contract_error("iterations beyond max_iterations");
+    if (k == 0) return;
+    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
+    cudaStream_t s = g[0]->ctx->compute;
+    for (int r = 1; r < P; ++r) {
+        TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
+        TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
+    }
+    int B = rank_group_blocks_per_rank(P);
+    for (int r = 0; r < P; ++r) B = std::min(B, g[r]->maxg);
+    if (B < 1) config_error("more ranks than co-resident blocks");
+    std::vector<GroupRank> h(static_cast<size_t>(P));
+    GroupRank* d = nullptr;
+    unsigned* bars = nullptr;
+    TW_CUDA(cudaMalloc(&d, sizeof(GroupRank) * P));
+    TW_CUDA(cudaMalloc(&bars, sizeof(unsigned) * 2 * P));
+    TW_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * P, s));
+    for (int r = 0; r < P; ++r) {
+        tw_cg* c = g[r];
+        GroupRank& R = h[static_cast<size_t>(r)];
+        R.A = c->view();
+        R.x = c->x; R.r = c->r; R.p_local = c->p_local; R.p_owned = c->p_owned; R.Ap = c->Ap;
+        R.pm = c->pm; R.send_b = c->send_b; R.history = c->history;
+        R.sc = c->sc;
+        R.rs = c->slot(0);
+        R.win = c->win;
+        R.links = c->d_links;
+        R.n_ghost = c->slab.ghost_lo + c->slab.ghost_hi;
+        R.ghost_flags = c->slab.ghost_lo ? &c->win->flag_ghost_lo : &c->win->flag_ghost_hi;
+        R.P = P;
+        R.n = c->n; R.int_r0 = c->slab.interior_r0; R.int_r1 = c->slab.interior_r1;
+        R.bar = bars + 2 * r;
+    }
+    TW_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(GroupRank) * P, cudaMemcpyHostToDevice, s));
+    launch_rank_group(d, P, B, k, jitter, s);
+    TW_CUDA(cudaStreamSynchronize(s));
+    cudaFree(d);
+    cudaFree(bars);
+    group_join(g, P, s);
+    for (int r = 0; r < P; ++r) g[r]->enqueued += k;
+}
+
 // Timing event at the end of iteration i-1 (i = 0: the start of the solve).
 cudaEvent_t iter_event(tw_cg* cg, int i) {
     while (static_cast<int>(cg->iter_ev.size()) <= i) {
@@ -1213,6 +1262,10 @@ int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_i
 
 int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations) {
     return guarded([&] { group_iterate(cgs, nranks, iterations); });
+}
+
+int tw_cg_group_iterate_concurrent(tw_cg** cgs, int nranks, int iterations, int jitter) {
+    return guarded([&] { group_iterate_concurrent(cgs, nranks, iterations, jitter); });
 }
 
 int tw_cg_group_enable_peer(tw_cg** cgs, int nranks) {

@@ -53,6 +53,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -140,22 +146,33 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
     }
 }
 
+// The blocks a body runs on: the launch grid, or one rank's share of the
+// grid of the concurrent rank-group kernel (bid in [0, nblk)).
+struct GridPos {
+    int bid, nblk;
+};
+
+__device__ __forceinline__ GridPos launch_grid() {
+    return GridPos{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x)};
+}
+
 // Grid-wide fixed-order reduction finished by the last block to arrive.
-__device__ __forceinline__ void grid_reduce_finalize(double v, RedScratch rs, const Fin& fin) {
+__device__ __forceinline__ void grid_reduce_finalize(double v, RedScratch rs, const Fin& fin,
+                                                     GridPos g = launch_grid()) {
     __shared__ double smem[32];
     __shared__ bool last;
     double b = block_sum(v, smem);
     if (threadIdx.x == 0) {
-        rs.block_part[blockIdx.x] = b;
+        rs.block_part[g.bid] = b;
         __threadfence();
-        unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
-        last = (t == gridDim.x - 1);
+        unsigned t = atomicInc(rs.ticket, static_cast<unsigned>(g.nblk - 1));
+        last = (t == static_cast<unsigned>(g.nblk - 1));
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
     double acc = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    for (int i = threadIdx.x; i < g.nblk; i += blockDim.x)
         acc = __dadd_rn(acc, __ldcg(rs.block_part + i));
     double total = block_sum(acc, smem);
     if (threadIdx.x == 0) finalize(fin, total);

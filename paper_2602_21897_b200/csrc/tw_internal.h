@@ -182,6 +182,22 @@ bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, d
                        double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
 void launch_peer_push(const double* p_owned, int64_t n, int64_t plane, const PeerLinks& L,
                       const CgScalars* sc, unsigned* ticket, cudaStream_t s);
+// One rank of the concurrent rank-group kernel (tw_cg_group_iterate_concurrent).
+struct GroupRank {
+    EllView A;
+    double *x, *r, *p_local, *p_owned, *Ap, *pm, *send_b, *history;
+    CgScalars* sc;
+    RedScratch rs;
+    PeerWindow* win;
+    const PeerLinks* links; // device copy
+    const unsigned long long* ghost_flags;
+    int n_ghost, P;
+    int64_t n, int_r0, int_r1;
+    unsigned* bar; // [count, generation]
+};
+int rank_group_blocks_per_rank(int nranks);
+void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
+                       int iterations, int jitter, cudaStream_t s);
 // K4: dot(a, b) over [i0, i1) with finalize.
 void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
                 int blocks, cudaStream_t s);

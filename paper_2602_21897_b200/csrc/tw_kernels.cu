@@ -38,7 +38,7 @@ using namespace dev;
 // One row of a width-W slice: all matrix loads issued up front as 128-bit
 // evict-first loads, then the gathers, then the reference's left-to-right
 // sum (acc from 0.0, multiply then add).
-template <int W>
+template <int W, bool NC = true>
 __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
                                                   const int32_t* __restrict__ cb,
                                                   const double* __restrict__ x, int lane) {
@@ -68,7 +68,7 @@ __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
     if ((W - F) & 1) c[W - 1] = __ldcs(cb + 32 * (W - 1) + lane);
     double xv[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) xv[k] = __ldg(x + max(c[k], 0)); // branch-free: padding loads x[0], masked below
+    for (int k = 0; k < W; ++k) xv[k] = gather<NC>(x, max(c[k], 0)); // branch-free: padding loads x[0], masked below
     double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < W; ++k)
@@ -76,6 +76,7 @@ __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
     return acc;
 }
 
+template <bool NC = true>
 __device__ __forceinline__ double slice_row_generic(const double* __restrict__ vb,
                                                     const int32_t* __restrict__ cb,
                                                     const double* __restrict__ x, int lane,
@@ -85,19 +86,23 @@ __device__ __forceinline__ double slice_row_generic(const double* __restrict__ v
         int c = __ldcs(cb + ell_col_pos(k, lane, w));
         if (c < 0) break; // padding only ever trails a row
         double v = __ldcs(vb + ell_val_pos(k, lane, w));
-        acc = __dadd_rn(acc, __dmul_rn(v, __ldg(x + c)));
+        acc = __dadd_rn(acc, __dmul_rn(v, gather<NC>(x, c)));
     }
     return acc;
 }
 
-template <bool DOT>
-__global__ void __launch_bounds__(kThreads)
-spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
-            RowRange rb, RedScratch rs, Fin fin, const unsigned long long* wait_flags, int nwait) {
+// Register-path K1 body on the blocks of `g`.  NC: x is constant for the
+// whole kernel (read-only path); the concurrent rank-group kernel, which
+// rewrites p between its phases, gathers through the coherent L1 path.
+template <bool DOT, bool NC = true>
+__device__ __forceinline__ void spmv_rows(GridPos g, const EllView& A, const double* __restrict__ x,
+                                          double* __restrict__ y, RowRange ra, RowRange rb,
+                                          RedScratch rs, const Fin& fin,
+                                          const unsigned long long* wait_flags, int nwait) {
     if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
     const int lane = threadIdx.x & 31;
-    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t warp_g = (static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(g.nblk) * blockDim.x) >> 5;
     // The slices covering range a, then those covering range b, as one index space.
     const int64_t sa0 = ra.r0 >> 5, sa1 = ra.r1 > ra.r0 ? (ra.r1 + 31) >> 5 : sa0;
     const int64_t sb0 = rb.r0 >> 5, sb1 = rb.r1 > rb.r0 ? (rb.r1 + 31) >> 5 : sb0;
@@ -112,20 +117,27 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
         const int32_t* cb = A.cols + off;
         double acc;
         switch (w) {
-        case 27: acc = slice_row_fixed<27>(vb, cb, x, lane); break;
-        case 18: acc = slice_row_fixed<18>(vb, cb, x, lane); break;
-        case 12: acc = slice_row_fixed<12>(vb, cb, x, lane); break;
-        case 8: acc = slice_row_fixed<8>(vb, cb, x, lane); break;
-        default: acc = slice_row_generic(vb, cb, x, lane, w); break;
+        case 27: acc = slice_row_fixed<27, NC>(vb, cb, x, lane); break;
+        case 18: acc = slice_row_fixed<18, NC>(vb, cb, x, lane); break;
+        case 12: acc = slice_row_fixed<12, NC>(vb, cb, x, lane); break;
+        case 8: acc = slice_row_fixed<8, NC>(vb, cb, x, lane); break;
+        default: acc = slice_row_generic<NC>(vb, cb, x, lane, w); break;
         }
         const int64_t row = (s << 5) + lane;
         const RowRange r = in_a ? ra : rb;
         if (row >= r.r0 && row < r.r1) {
             y[row] = acc;
-            if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
+            if (DOT) part = __dadd_rn(part, __dmul_rn(gather<NC>(x, row + A.diag_shift), acc));
         }
     }
-    if (DOT) grid_reduce_finalize(part, rs, fin);
+    if (DOT) grid_reduce_finalize(part, rs, fin, g);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
+            RowRange rb, RedScratch rs, Fin fin, const unsigned long long* wait_flags, int nwait) {
+    spmv_rows<DOT>(launch_grid(), A, x, y, ra, rb, rs, fin, wait_flags, nwait);
 }
 
 
@@ -292,20 +304,21 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
 // 128-bit accesses, the (at most two) ragged ends go scalar.
 template <typename F>
-__device__ __forceinline__ void for_pairs(int64_t i0, int64_t i1, F&& f) {
+__device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&& f) {
     const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t j = j0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < j1;
+    const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
+    for (int64_t j = j0 + static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x; j < j1;
          j += stride) {
         const int64_t e = 2 * j;
         f(e, e >= i0, e + 1 < i1);
     }
 }
 
-__global__ void __launch_bounds__(kThreads)
-update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
-                 double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
-                 ScalarSrc asrc, RedScratch rs, Fin fin) {
+__device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1,
+                                               double* __restrict__ x, const double* __restrict__ p,
+                                               double* __restrict__ r, const double* __restrict__ Ap,
+                                               CgScalars* sc, ScalarSrc asrc, RedScratch rs,
+                                               const Fin& fin) {
     double alpha;
     if (asrc.flags) block_wait_flags(asrc.flags, asrc.count, stamp_of(sc, 0));
     if (asrc.count > 0)
@@ -314,7 +327,7 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
         alpha = sc->alpha;
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
     double part = 0.0;
-    for_pairs(i0, i1, [&](int64_t e, bool lo, bool hi) {
+    for_pairs(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
         if (lo && hi) {
             double2 xv = __ldcs(reinterpret_cast<const double2*>(x + e));
             double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
@@ -340,16 +353,24 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
             }
         }
     });
-    grid_reduce_finalize(part, rs, fin);
+    grid_reduce_finalize(part, rs, fin, g);
+}
+
+__global__ void __launch_bounds__(kThreads)
+update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
+                 double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
+                 ScalarSrc asrc, RedScratch rs, Fin fin) {
+    update_xr_rows(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
 }
 
 // PEER: the peer-transport instantiation (flag wait, fused halo stores);
 // the plain one stays lean so the grid keeps its full occupancy.
 template <bool PEER>
-__global__ void __launch_bounds__(kThreads)
-update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
-                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
-                const PeerLinks* links_, const double* __restrict__ psrc) {
+__device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
+                                              const double* __restrict__ r, double* __restrict__ p,
+                                              CgScalars* sc, ScalarSrc bsrc, RedScratch rs,
+                                              double* history, const PeerLinks* links_,
+                                              const double* __restrict__ psrc) {
     // psrc: p_old, == p in place (each element is read, then written, by the
     // same thread, so the restrict-qualified aliasing is never observable)
     const PeerLinks* links = PEER ? links_ : nullptr;
@@ -390,8 +411,8 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
     };
     {
         const int64_t a = (i0 + 1) & ~int64_t(1), b = i1 & ~int64_t(1);
-        const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-        const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+        const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
+        const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
         for (int64_t j = (a >> 1) + tid; j < (b >> 1); j += 2 * stride) {
             const int64_t e0 = 2 * j, e1 = 2 * (j + stride);
             const bool two = e1 < b;
@@ -424,8 +445,8 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
                 __threadfence_system();
             else
                 __threadfence();
-            unsigned t = atomicInc(rs.ticket, gridDim.x - 1);
-            last = (t == gridDim.x - 1);
+            unsigned t = atomicInc(rs.ticket, static_cast<unsigned>(g.nblk - 1));
+            last = (t == static_cast<unsigned>(g.nblk - 1));
         }
         __syncthreads();
         if (last && threadIdx.x == 0) {
@@ -443,6 +464,87 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
                 if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
             }
         }
+    }
+}
+
+template <bool PEER>
+__global__ void __launch_bounds__(kThreads)
+update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
+                CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
+                const PeerLinks* links, const double* __restrict__ psrc) {
+    update_p_rows<PEER>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc);
+}
+
+// ------------------------------------------- concurrent rank group (1 GPU)
+
+// Barrier of one rank's blocks inside the rank-group kernel: stands in for
+// the kernel boundaries between that rank's launches.  Generation counting;
+// the gpu-scope acquire + fence also drops stale L1 lines before the next
+// phase gathers p.
+__device__ __forceinline__ void group_barrier(unsigned* bar, int nblk) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned gen = ld_acquire_gpu(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == static_cast<unsigned>(nblk - 1)) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            const unsigned long long t0 = global_ns();
+            while (ld_acquire_gpu(bar + 1) == gen) {
+                __nanosleep(32);
+                if (global_ns() - t0 > TW_PEER_TIMEOUT_NS) {
+                    printf("tw_hpccg: rank-group barrier timed out\n");
+                    __trap();
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// P ranks of the peer transport as ONE cooperative kernel: blocks
+// [r B, (r+1) B) run rank r's iterations -- the same phase bodies, flag
+// waits, publishes and fused halo stores as the per-rank launches, with a
+// group barrier where those have a kernel boundary.  The ranks run truly
+// concurrently and wait on one another's flags, which separate launches on
+// one GPU must never do; co-residency of the whole grid (cooperative
+// launch) makes the waits safe.  `jitter` delays rank-dependent blocks to
+// vary the interleavings.
+__global__ void __launch_bounds__(kThreads)
+rank_group_kernel(const GroupRank* ranks, int B, int iterations, int jitter) {
+    const int rk = blockIdx.x / B;
+    const GridPos g{static_cast<int>(blockIdx.x % B), B};
+    const GroupRank& R = ranks[rk];
+    const RowRange all{0, 0};
+    for (int it = 0; it < iterations; ++it) {
+        if (jitter && threadIdx.x == 0 && g.bid == (it * 7 + rk * 3) % B)
+            __nanosleep(static_cast<unsigned>(((it + 1) * (rk + 1) * 977) % 20000));
+        // K1 interior rows (no ghost plane), partial into pm[0]
+        spmv_rows<true, false>(g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, all, R.rs,
+                               Fin{FIN_STORE, R.pm, nullptr, nullptr, nullptr, nullptr}, nullptr, 0);
+        group_barrier(R.bar, B);
+        // K1 boundary rows after the ghost flags; publish (0 + pm[0]) + pm[1]
+        spmv_rows<true, false>(g, R.A, R.p_local, R.Ap, RowRange{0, R.int_r0},
+                               RowRange{R.int_r1, R.n}, R.rs,
+                               Fin{FIN_PUBLISH_A, R.pm + 1, R.sc, nullptr, R.links, R.pm},
+                               R.ghost_flags, R.n_ghost);
+        group_barrier(R.bar, B);
+#ifdef TW_BREAK_PEER_WAIT // negative control of the concurrency test only
+        update_xr_rows(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
+                       ScalarSrc{R.win->recv_a, R.P, nullptr}, R.rs,
+#else
+        update_xr_rows(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
+                       ScalarSrc{R.win->recv_a, R.P, R.win->flag_a}, R.rs,
+#endif
+                       Fin{FIN_PUBLISH_B, R.send_b, R.sc, nullptr, R.links, nullptr});
+        group_barrier(R.bar, B);
+        update_p_rows<true>(g, 0, R.n, R.r, R.p_owned, R.sc,
+                            ScalarSrc{R.win->recv_b, R.P, R.win->flag_b}, R.rs, R.history, R.links,
+                            R.p_owned);
+        group_barrier(R.bar, B);
     }
 }
 
@@ -816,6 +918,23 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
     else
         spmv_kernel<false><<<g, kThreads, 0, s>>>(A, x, y, a, b, rs, fin, wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
+}
+
+int rank_group_blocks_per_rank(int nranks) {
+    int occ = 0, dev = 0, sms = 0;
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rank_group_kernel, kThreads, 0));
+    TW_CUDA(cudaGetDevice(&dev));
+    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return occ * sms / nranks;
+}
+
+void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
+                       int iterations, int jitter, cudaStream_t s) {
+    int B = blocks_per_rank, it = iterations;
+    void* args[] = {&ranks_dev, &B, &it, &jitter};
+    TW_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(rank_group_kernel),
+                                        dim3(static_cast<unsigned>(nranks * B)), dim3(kThreads),
+                                        args, 0, s));
 }
 
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,

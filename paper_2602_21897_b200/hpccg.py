@@ -618,6 +618,11 @@ class EmulatedRankGroup:
     def iterate(self, k: int) -> None:
         N.check(_lib().tw_cg_group_iterate(self._arr, self.P, k))
 
+    def iterate_concurrent(self, k: int, jitter: bool = False) -> None:
+        """Peer transport only: all ranks as one cooperative kernel, really
+        waiting on one another's flags (tw_cg_group_iterate_concurrent)."""
+        N.check(_lib().tw_cg_group_iterate_concurrent(self._arr, self.P, k, 1 if jitter else 0))
+
     def history(self, count: int) -> list:
         return [s.history(count) for s in self.solvers]
 

@@ -624,3 +624,28 @@ def test_spmv_generic_widths_tma_and_register_paths(rt, orc, maxw):
     assert np.all(got[:45] == -3.0) and np.all(got[n - 7:] == -3.0)
     d = P.spmv_dot(G, dev(x), y, 0, n)
     assert abs(d - float(np.dot(x, want))) <= 1e-12 * np.abs(x * want).sum()
+
+
+@pytest.mark.parametrize("dims,P_", [((32, 32, 32), 2), ((40, 24, 30), 3), ((32, 32, 32), 4),
+                                     ((24, 20, 16), 8)])
+def test_peer_transport_under_concurrency(orc, golden, dims, P_):
+    """The peer protocol with the ranks really running at the same time:
+    tw_cg_group_iterate_concurrent runs all P ranks as one cooperative
+    kernel whose rank groups spin on one another's flags (stamps, rank-order
+    partial sums, fused halo stores), with and without rank-dependent
+    delays, interleaved with host-sequenced iterations and a re-solve."""
+    m = orc.stencil(*dims)
+    G = P.EmulatedRankGroup(*dims, P_, 60, transport="peer")
+    for seed in (7, 2):
+        b = orc.rhs_xorshift(m.n, seed)
+        want_h, want_x, _ = orc.cg(m, b, 60)
+        G.set_rhs(b)
+        G.iterate_concurrent(17)
+        G.iterate(3)
+        G.iterate_concurrent(40, jitter=True)
+        hs = G.history(60)
+        for h in hs:
+            assert np.array_equal(h, hs[0])
+        check_history(hs[0], want_h)
+        assert np.all(rel_gap(G.solution(), want_x) <= 1e-10)
+    G.close()
