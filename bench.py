@@ -339,10 +339,33 @@ def run_ours(args, dist, rank, world, local):
         raise SystemExit("--transport peer runs the monolithic variant")
     transport = ("peer" if want_peer else "nccl") if multi else None
     if want_peer:
+        # CUDA-IPC setup, collective and failure-tolerant: every rank takes
+        # part in the allgather even if its export failed, and all fall back
+        # together if any rank could not connect
+        note = ""
+        try:
+            blob = S.peer_export()
+        except Exception as ex:
+            blob, note = None, f"export: {ex}"
         if world > 1:
-            S.enable_peer_transport()
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
         else:
-            S.peer_connect([S.peer_export()])
+            blobs = [blob]
+        ok = 1.0 if all(x is not None for x in blobs) else 0.0
+        if ok:
+            try:
+                S.peer_connect(blobs)
+            except Exception as ex:
+                ok, note = 0.0, f"connect: {ex}"
+        if min_over_ranks(dist, ok) < 1.0:
+            if args.transport == "peer":
+                raise SystemExit(f"peer transport setup failed ({note or 'on another rank'})")
+            S.close()
+            S = P.CgSolver(rt, A, W + KR, opt, variant=variant)
+            want_peer = False
+            transport = f"nccl (peer setup failed: {note or 'on another rank'})"
+    if want_peer:
         # validation before timing: the peer path sums the same partials in
         # the same order as the NCCL path, so the histories must be identical
         kv = min(20, W + KR)
