@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // barrier extends the acquire to the block.  Call from uniform control flow.
 // A flag that stays stale for TW_PEER_TIMEOUT_NS traps (the context reports
 // an error to every later call) instead of hanging the GPU.
-__device__ __forceinline__ void block_wait_flags(const unsigned long long* flags, int count,
+static __device__ __noinline__ void block_wait_flags(const unsigned long long* flags, int count,
                                                  unsigned long long want) {
     if (threadIdx.x == 0) {
         unsigned long long t0 = 0;

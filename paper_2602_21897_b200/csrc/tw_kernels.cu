@@ -363,6 +363,41 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
     update_xr_rows(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
 }
 
+// K3's streaming loop over [a0, b0): p = r + beta psrc, two pairs per
+// thread and step.  U: compiler unroll of that loop on top (measured: 4 for
+// the lean kernel, 1 where the peer code already holds many registers).
+template <int U>
+__device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, int64_t stride,
+                                         const double* __restrict__ r,
+                                         const double* __restrict__ psrc, double* __restrict__ p,
+                                         double beta) {
+    const int64_t a = (a0 + 1) & ~int64_t(1), b = b0 & ~int64_t(1);
+    auto pair = [&](int64_t e, double2 rv, double2 pv) {
+        pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+        pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+        *reinterpret_cast<double2*>(p + e) = pv;
+    };
+#pragma unroll U
+    for (int64_t j = (a >> 1) + tid; j < (b >> 1); j += 2 * stride) {
+        const int64_t e0 = 2 * j, e1 = 2 * (j + stride);
+        const bool two = e1 < b;
+        const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
+        const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
+        double2 r1 = make_double2(0.0, 0.0), p1 = r1;
+        if (two) {
+            r1 = __ldcs(reinterpret_cast<const double2*>(r + e1));
+            p1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
+        }
+        pair(e0, r0, p0);
+        if (two) pair(e1, r1, p1);
+    }
+    if (tid == 0) {
+        auto one = [&](int64_t i) { p[i] = __dadd_rn(r[i], __dmul_rn(beta, psrc[i])); };
+        if ((a0 & 1) && a0 < b0) one(a0);
+        if (b < b0 && b >= a0 && b >= a) one(b);
+    }
+}
+
 // PEER: the peer-transport instantiation (flag wait, fused halo stores);
 // the plain one stays lean so the grid keeps its full occupancy.
 template <bool PEER>
@@ -375,16 +410,6 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // same thread, so the restrict-qualified aliasing is never observable)
     const PeerLinks* links = PEER ? links_ : nullptr;
     double beta, rr = 0.0;
-    // fused halo (peer transport): the first / last owned plane also goes
-    // straight into the neighbours' ghost planes over NVLink
-    double* lo_dst = links ? links->ghost_lo_dst : nullptr;
-    double* hi_dst = links ? links->ghost_hi_dst : nullptr;
-    const int64_t plane = links ? links->plane : 0, hi_first = i1 - plane;
-    bool remote = false; // this thread stored into a neighbour's ghost plane
-    auto halo = [&](int64_t i, double v) {
-        if (lo_dst && i < plane) { lo_dst[i] = v; remote = true; }
-        if (hi_dst && i >= hi_first) { hi_dst[i - hi_first] = v; remote = true; }
-    };
     if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
         rr = sum_parts(bsrc.parts, bsrc.count);
@@ -392,43 +417,41 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     } else {
         beta = sc->beta;
     }
-    // Full pairs [a, b) with 128-bit accesses, two pairs per thread and
-    // step (both pairs' loads issued before either store: twice the bytes
-    // in flight of a one-pair loop); the at most two ragged ends go scalar.
-    auto one = [&](int64_t i) {
-        const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
-        p[i] = v;
-        if (links) halo(i, v);
+    const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
+    // Full pairs of [a0, b0) with 128-bit accesses, two pairs per thread and
+    // step (both pairs' loads issued before either store: twice the bytes in
+    // flight of a one-pair loop); the at most two ragged ends go scalar.
+    auto stream = [&](int64_t a0, int64_t b0) {
+        p_stream<PEER ? 1 : 4>(a0, b0, tid, stride, r, psrc, p, beta);
     };
-    auto pair = [&](int64_t e, double2 rv, double2 pv) {
-        pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
-        pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-        *reinterpret_cast<double2*>(p + e) = pv;
-        if (links) {
-            halo(e, pv.x);
-            halo(e + 1, pv.y);
-        }
-    };
-    {
-        const int64_t a = (i0 + 1) & ~int64_t(1), b = i1 & ~int64_t(1);
-        const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
-        const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
-        for (int64_t j = (a >> 1) + tid; j < (b >> 1); j += 2 * stride) {
-            const int64_t e0 = 2 * j, e1 = 2 * (j + stride);
-            const bool two = e1 < b;
-            const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
-            const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
-            double2 r1 = make_double2(0.0, 0.0), p1 = r1;
-            if (two) {
-                r1 = __ldcs(reinterpret_cast<const double2*>(r + e1));
-                p1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
+    // Fused halo (peer transport): the first / last owned plane of p also
+    // goes straight into the neighbours' ghost planes over NVLink.  Those two
+    // planes run as a separate scalar pass so the bulk stays the lean loop.
+    bool remote = false; // this thread stored into a neighbour's ghost plane
+    if (!links) {
+        stream(i0, i1);
+    } else {
+        const int64_t plane = links->plane;
+        const int64_t lo_end = i0 + plane < i1 ? i0 + plane : i1;
+        const int64_t hi_beg = i1 - plane > lo_end ? i1 - plane : lo_end;
+        stream(lo_end, hi_beg);
+        double* lo_dst = links->ghost_lo_dst;
+        double* hi_dst = links->ghost_hi_dst;
+        const int64_t nlo = lo_end - i0, nedge = nlo + (i1 - hi_beg);
+#pragma unroll 1
+        for (int64_t k = tid; k < nedge; k += stride) {
+            const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
+            const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
+            p[i] = v;
+            if (lo_dst && i - i0 < plane) {
+                lo_dst[i - i0] = v;
+                remote = true;
             }
-            pair(e0, r0, p0);
-            if (two) pair(e1, r1, p1);
-        }
-        if (tid == 0) {
-            if ((i0 & 1) && i0 < i1) one(i0);
-            if (b < i1 && b >= i0 && b >= a) one(b);
+            if (hi_dst && i >= i1 - plane) {
+                hi_dst[i - (i1 - plane)] = v;
+                remote = true;
+            }
         }
     }
     if (bsrc.count > 0) {
