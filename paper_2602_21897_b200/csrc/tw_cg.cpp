@@ -747,6 +747,8 @@ void group_join(tw_cg** g, int P, cudaStream_t s) {
 // other ranks' buffers on the same device.
 void group_enable_peer(tw_cg** g, int P) {
     group_check(g, P);
+    for (int r = 0; r < P; ++r)
+        if (g[r]->peer) contract_error("the peer transport is already connected");
     TW_CUDA(cudaSetDevice(g[0]->ctx->device));
     for (int r = 0; r < P; ++r) alloc_window(g[r]);
     for (int r = 0; r < P; ++r) {
@@ -1298,6 +1300,7 @@ int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
 int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
     return guarded([&] {
         if (!cg || !blobs) contract_error("null solver or blobs");
+        if (cg->peer) contract_error("the peer transport is already connected");
         TW_CUDA(cudaSetDevice(cg->ctx->device));
         alloc_window(cg);
         const int P = cg->P, me = cg->ctx->rank;

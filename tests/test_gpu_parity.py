@@ -418,6 +418,8 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     for graph in (False, True):
         s = P.CgSolver(rt2, A, 150, P.CgOptions(use_graph=graph), variant=0)
         s.peer_connect([s.peer_export()])
+        with pytest.raises(P.ContractViolation):
+            s.peer_connect([s.peer_export()])  # connected once per solver
         assert s.launches_per_iteration() == (4, 0)
         s.set_rhs(b)
         s.iterate(70)
