@@ -6,6 +6,7 @@
 #include <deque>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <thread>
 #include <vector>
@@ -103,9 +104,12 @@ struct tw_ctx {
     cudaStream_t compute = nullptr;
     cudaStream_t comm = nullptr;
     tw::StreamPool pool;
-    // scratch for standalone reductions (tw_dot_range / tw_spmv_dot)
-    double* red_part = nullptr;
-    unsigned* red_ticket = nullptr;
+    // scratch for standalone reductions (tw_dot_range / tw_spmv_dot), one per
+    // stream: calls on one stream run in order, calls on different streams
+    // may run at the same time (the reference's kernels may be called from
+    // any worker, kernels.hpp:7-9) and must not share a ticket
+    std::unordered_map<cudaStream_t, tw::RedScratch> red;
+    int red_blocks = 0;
     std::mutex red_mu;
     // multi-GPU
     ncclComm_t nccl_comm = nullptr;
@@ -129,7 +133,7 @@ struct tw_ell {
 
 namespace tw {
 // helpers shared across translation units
-void ctx_red_scratch(tw_ctx* ctx, RedScratch* rs);
+RedScratch ctx_red_scratch(tw_ctx* ctx, cudaStream_t s);
 void tile_plan(const tw_ell* A, int tiles, std::vector<int64_t>& r0, std::vector<int64_t>& r1,
                std::vector<int64_t>& band_lo_local, std::vector<int64_t>& band_hi_local);
 } // namespace tw

@@ -185,9 +185,16 @@ size_t TaskAware::pending() const {
 
 // ------------------------------------------------------------------ helpers
 
-void ctx_red_scratch(tw_ctx* ctx, RedScratch* rs) {
-    rs->block_part = ctx->red_part;
-    rs->ticket = ctx->red_ticket;
+RedScratch ctx_red_scratch(tw_ctx* ctx, cudaStream_t s) {
+    std::lock_guard lk(ctx->red_mu);
+    auto it = ctx->red.find(s);
+    if (it != ctx->red.end()) return it->second;
+    RedScratch rs{};
+    TW_CUDA(cudaMalloc(&rs.block_part, sizeof(double) * static_cast<size_t>(ctx->red_blocks)));
+    TW_CUDA(cudaMalloc(&rs.ticket, sizeof(unsigned) * 4));
+    TW_CUDA(cudaMemset(rs.ticket, 0, sizeof(unsigned) * 4));
+    ctx->red.emplace(s, rs);
+    return rs;
 }
 
 static void check_ctx(const tw_ctx* c) {
@@ -567,10 +574,7 @@ int tw_ctx_create(int device, unsigned cap, tw_ctx** out) {
         TW_CUDA(cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking));
         TW_CUDA(cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking));
         c->pool.init(device, cap);
-        const int maxg = std::max(c->cfg.spmv_blocks, c->cfg.stream_blocks);
-        TW_CUDA(cudaMalloc(&c->red_part, sizeof(double) * maxg));
-        TW_CUDA(cudaMalloc(&c->red_ticket, sizeof(unsigned) * 4));
-        TW_CUDA(cudaMemset(c->red_ticket, 0, sizeof(unsigned) * 4));
+        c->red_blocks = std::max({c->cfg.spmv_blocks, c->cfg.stream_blocks, c->cfg.tma_blocks});
         *out = c.release();
     });
 }
@@ -584,8 +588,10 @@ int tw_ctx_destroy(tw_ctx* ctx) {
         ctx->pool.destroy();
         cudaStreamDestroy(ctx->compute);
         cudaStreamDestroy(ctx->comm);
-        cudaFree(ctx->red_part);
-        cudaFree(ctx->red_ticket);
+        for (auto& kv : ctx->red) {
+            cudaFree(kv.second.block_part);
+            cudaFree(kv.second.ticket);
+        }
         delete ctx;
     });
 }
@@ -790,9 +796,7 @@ int tw_spmv_dot(const tw_ell* A, const double* p, double* Ap, int64_t r0, int64_
             TW_CUDA(cudaMemsetAsync(dot_dev, 0, sizeof(double), s));
             return;
         }
-        std::lock_guard lk(c->red_mu);
-        RedScratch rs;
-        ctx_red_scratch(c, &rs);
+        const RedScratch rs = ctx_red_scratch(c, s);
         launch_spmv(A->view(), p, Ap, RowRange{r0, r1}, RowRange{0, 0}, true, rs,
                     Fin{FIN_STORE, dot_dev, nullptr, nullptr}, c->cfg.spmv_blocks, s);
     });
@@ -809,9 +813,7 @@ int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int6
             TW_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double), s));
             return;
         }
-        std::lock_guard lk(ctx->red_mu);
-        RedScratch rs;
-        ctx_red_scratch(ctx, &rs);
+        const RedScratch rs = ctx_red_scratch(ctx, s);
         launch_dot(a, b, i0, i1, rs, Fin{FIN_STORE, out_dev, nullptr, nullptr},
                    ctx->cfg.stream_blocks, s);
     });

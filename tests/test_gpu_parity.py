@@ -179,6 +179,39 @@ def test_dot_identities(rt, orc):
     assert P.dot_range(bd, bd, 5, 5, rt=rt) == 0.0
 
 
+def test_standalone_reductions_on_concurrent_streams(rt, orc):
+    """tw_dot_range / tw_spmv_dot called on several streams at once (the
+    reference's kernels may run from any worker, kernels.hpp:7-9): each
+    stream has its own reduction scratch, so every result is the one the
+    same call gives alone."""
+    import ctypes
+    from paper_2602_21897_b200 import _native as N
+    lib = N.load()
+    n = 4_000_003
+    vecs = [dev(orc.rhs_splitmix(n, s)) for s in range(4)]
+    want = [P.dot_range(v, v, 0, n, rt=rt) for v in vecs]
+    A = P.gen_stencil_matrix(64, 64, 64, rt=rt)
+    p = dev(orc.rhs_xorshift(A.n, 3))
+    Ap = torch.empty(A.n, dtype=torch.float64, device="cuda:0")
+    want_pap = P.spmv_dot(A, p, Ap, 0, A.n)
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    outs = torch.zeros(8, dtype=torch.float64, device="cuda:0")
+    aps = [torch.empty(A.n, dtype=torch.float64, device="cuda:0") for _ in range(4)]
+    torch.cuda.synchronize()
+    for rep in range(5):
+        for i, st in enumerate(streams):
+            N.check(lib.tw_dot_range(rt.h, ctypes.c_void_p(vecs[i].data_ptr()),
+                                     ctypes.c_void_p(vecs[i].data_ptr()), 0, n,
+                                     ctypes.c_void_p(outs.data_ptr() + 8 * i),
+                                     ctypes.c_void_p(st.cuda_stream)))
+            N.check(lib.tw_spmv_dot(A.h, ctypes.c_void_p(p.data_ptr()),
+                                    ctypes.c_void_p(aps[i].data_ptr()), 0, A.n,
+                                    ctypes.c_void_p(outs.data_ptr() + 8 * (4 + i)),
+                                    ctypes.c_void_p(st.cuda_stream)))
+        got = host(outs)
+        assert list(got[:4]) == want and all(g == want_pap for g in got[4:])
+
+
 def test_rhs_generators_bit_exact(rt, orc):
     for first, count in [(0, 1000), (12345, 70000)]:
         b = host(torch.zeros(count, dtype=torch.float64, device="cuda:0"))
