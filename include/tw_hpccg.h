@@ -124,6 +124,33 @@ int tw_ell_info(const tw_ell* A, tw_ell_info_t* out);
 int tw_ell_to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values);
 int tw_ell_destroy(tw_ell* A);
 
+/* ------------------------------------------------- streams and events
+ * The reference's device / task-aware layer over real CUDA objects, for
+ * callers that keep their own task graph.  Streams and
+ * events are cudaStream_t / cudaEvent_t passed as void*. */
+
+/* QueuePool::acquire / release (task_aware.cpp:122-166): one of the
+ * context's pooled streams (capacity from tw_ctx_create); blocks, FIFO,
+ * while every pooled stream is out.  Releasing a foreign stream is
+ * TW_ERR_CONTRACT. */
+int tw_stream_acquire(tw_ctx* ctx, void** stream);
+int tw_stream_release(tw_ctx* ctx, void* stream);
+/* sim::Device record_event / query / synchronize (sim_device.hpp:101-123). */
+int tw_event_create(void** ev);
+int tw_event_destroy(void* ev);
+int tw_event_record(void* ev, void* stream);
+int tw_event_query(void* ev, int* done); /* non-blocking: *done = 0 / 1 */
+/* TaskAware::wait_transformed (task_aware.cpp:50-60): poll and yield until
+ * ev completes; never a blocking driver wait. */
+int tw_event_wait(tw_ctx* ctx, void* ev);
+/* A device-side edge: later work on `stream` waits for ev. */
+int tw_stream_wait_event(void* stream, void* ev);
+/* TaskAware::bind_event_async (task_aware.cpp:43-48, 92-96): the context's
+ * polling thread calls done(arg) once it observes ev complete (the
+ * release-dependents hook).  The caller keeps ev alive until then;
+ * callbacks still pending at tw_ctx_destroy are dropped. */
+int tw_event_bind_async(tw_ctx* ctx, void* ev, void (*done)(void* arg), void* arg);
+
 /* ------------------------------------------------------- kernels (K1-K4) */
 
 /* spmv_range(A, x, y, r0, r1) (kernels.cpp:5-13): y[i] for local rows

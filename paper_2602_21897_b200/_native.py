@@ -49,6 +49,7 @@ _ERRS = {1: ConfigError, 2: ContractViolation, 3: CudaError, 4: NcclError}
 i64 = C.c_int64
 vp = C.c_void_p
 dp = C.POINTER(C.c_double)
+DONE_CB = C.CFUNCTYPE(None, C.c_void_p)  # tw_event_bind_async callback
 lp = C.POINTER(C.c_int64)
 
 
@@ -126,6 +127,15 @@ SIGNATURES = [
     ("tw_cg_group_set_rhs", C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.c_int]),
     ("tw_cg_group_iterate", C.c_int, [C.POINTER(vp), C.c_int, C.c_int]),
     ("tw_halo_exchange", C.c_int, [vp, vp, vp]),
+    ("tw_stream_acquire", C.c_int, [vp, C.POINTER(vp)]),
+    ("tw_stream_release", C.c_int, [vp, vp]),
+    ("tw_event_create", C.c_int, [C.POINTER(vp)]),
+    ("tw_event_destroy", C.c_int, [vp]),
+    ("tw_event_record", C.c_int, [vp, vp]),
+    ("tw_event_query", C.c_int, [vp, C.POINTER(C.c_int)]),
+    ("tw_event_wait", C.c_int, [vp, vp]),
+    ("tw_stream_wait_event", C.c_int, [vp, vp]),
+    ("tw_event_bind_async", C.c_int, [vp, vp, DONE_CB, vp]),
     ("tw_cg_group_enable_peer", C.c_int, [C.POINTER(vp), C.c_int]),
     ("tw_cg_group_iterate_concurrent", C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int]),
     ("tw_cg_peer_export", C.c_int, [vp, C.c_char_p]),

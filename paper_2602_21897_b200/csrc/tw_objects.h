@@ -26,6 +26,7 @@ public:
     int acquire();               // index into streams()
     void release(int idx);
     cudaStream_t stream(int idx) const { return streams_[static_cast<size_t>(idx)]; }
+    int index_of(cudaStream_t s) const; // -1 if s is not a pool stream
     unsigned capacity() const { return static_cast<unsigned>(streams_.size()); }
     size_t outstanding() const;
 
@@ -47,10 +48,13 @@ class TaskAware {
 public:
     explicit TaskAware(int device, double poll_period_s) : device_(device), period_(poll_period_s) {}
     ~TaskAware();
-    void bind(cudaEvent_t ev, double* slot, double t0);
+    void bind(cudaEvent_t ev, double* slot, double t0);          // event owned, recycled
+    void bind_callback(cudaEvent_t ev, void (*done)(void*), void* arg); // caller's event
     void wait(cudaEvent_t ev);
+    static void wait_static(cudaEvent_t ev); // poll + yield until ev completes
     size_t pending() const;
     size_t polled() const { return polled_.load(); }
+    size_t poll_now() { return poll_once(); }
     cudaEvent_t take_event();
 
 private:
@@ -60,7 +64,11 @@ private:
         cudaEvent_t ev;
         double* slot;
         double t0;
+        void (*done)(void*);
+        void* arg;
+        bool owned;
     };
+    void add(const Bind& b);
     int device_;
     double period_;
     mutable std::mutex mu_;
@@ -116,6 +124,9 @@ struct tw_ctx {
     int rank = 0;
     int nranks = 1;
     bool emulated = false; // rank of an emulated group on one device (no NCCL)
+    // task-aware completion for tw_event_bind_async (lazily started poller)
+    std::unique_ptr<tw::TaskAware> ta;
+    std::mutex ta_mu;
 };
 
 struct tw_ell {

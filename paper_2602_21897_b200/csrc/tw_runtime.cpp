@@ -94,6 +94,12 @@ void StreamPool::release(int idx) {
     cv_.notify_one();
 }
 
+int StreamPool::index_of(cudaStream_t s) const {
+    for (size_t i = 0; i < streams_.size(); ++i)
+        if (streams_[i] == s) return static_cast<int>(i);
+    return -1;
+}
+
 size_t StreamPool::outstanding() const {
     std::lock_guard lk(mu_);
     return streams_.size() - free_.size();
@@ -108,7 +114,8 @@ TaskAware::~TaskAware() {
     }
     cv_.notify_all();
     if (th_.joinable()) th_.join();
-    for (auto& b : binds_) cudaEventDestroy(b.ev);
+    for (auto& b : binds_)
+        if (b.owned) cudaEventDestroy(b.ev);
     for (auto e : spare_) cudaEventDestroy(e);
 }
 
@@ -124,10 +131,10 @@ cudaEvent_t TaskAware::take_event() {
     return e;
 }
 
-void TaskAware::bind(cudaEvent_t ev, double* slot, double t0) {
+void TaskAware::add(const Bind& b) {
     {
         std::lock_guard lk(mu_);
-        binds_.push_back({ev, slot, t0});
+        binds_.push_back(b);
         if (!started_) {
             started_ = true;
             th_ = std::thread([this] { loop(); });
@@ -136,20 +143,37 @@ void TaskAware::bind(cudaEvent_t ev, double* slot, double t0) {
     cv_.notify_all();
 }
 
+void TaskAware::bind(cudaEvent_t ev, double* slot, double t0) {
+    add(Bind{ev, slot, t0, nullptr, nullptr, true});
+}
+
+void TaskAware::bind_callback(cudaEvent_t ev, void (*done)(void*), void* arg) {
+    add(Bind{ev, nullptr, 0.0, done, arg, false});
+}
+
 size_t TaskAware::poll_once() {
-    std::lock_guard lk(mu_);
+    std::vector<std::pair<void (*)(void*), void*>> fire;
     size_t done = 0;
-    const double now = host_seconds();
-    // Events complete in stream order; stop at the first one still pending.
-    while (!binds_.empty()) {
-        Bind& b = binds_.front();
-        cudaError_t q = cudaEventQuery(b.ev);
-        if (q == cudaErrorNotReady) break;
-        if (b.slot) *b.slot = now - b.t0;
-        spare_.push_back(b.ev);
-        binds_.pop_front();
-        ++done;
+    {
+        std::lock_guard lk(mu_);
+        const double now = host_seconds();
+        // One pass over every bound event (they may sit on different streams);
+        // a completed one is stamped / released, the rest stay bound.
+        for (auto it = binds_.begin(); it != binds_.end();) {
+            const cudaError_t q = cudaEventQuery(it->ev);
+            if (q == cudaErrorNotReady) {
+                ++it;
+                continue;
+            }
+            if (it->slot) *it->slot = now - it->t0;
+            if (it->owned) spare_.push_back(it->ev);
+            if (it->done) fire.emplace_back(it->done, it->arg);
+            it = binds_.erase(it);
+            ++done;
+        }
     }
+    // the callbacks run outside the lock: they may bind further events
+    for (auto& f : fire) f.first(f.second);
     polled_ += done;
     return done;
 }
@@ -169,7 +193,9 @@ void TaskAware::loop() {
     }
 }
 
-void TaskAware::wait(cudaEvent_t ev) {
+void TaskAware::wait(cudaEvent_t ev) { wait_static(ev); }
+
+void TaskAware::wait_static(cudaEvent_t ev) {
     for (;;) {
         cudaError_t q = cudaEventQuery(ev);
         if (q == cudaSuccess) return;
@@ -584,6 +610,8 @@ int tw_ctx_destroy(tw_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaDeviceSynchronize();
+        if (ctx->ta) ctx->ta->poll_now(); // fire what completed, then stop the poller
+        ctx->ta.reset();
         if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->nccl_comm);
         ctx->pool.destroy();
         cudaStreamDestroy(ctx->compute);
@@ -660,6 +688,91 @@ int tw_ctx_comm_info(tw_ctx* ctx, int* rank, int* nranks) {
         check_ctx(ctx);
         if (rank) *rank = ctx->rank;
         if (nranks) *nranks = ctx->nranks;
+    });
+}
+
+// ------------------------------------------------ streams and events
+// The reference's QueuePool / sim::Device stream-event calls / TaskAware
+// (task_aware.cpp:43-60, 122-166; sim_device.hpp:101-123) over real CUDA
+// streams and events.
+
+int tw_stream_acquire(tw_ctx* ctx, void** stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!stream) contract_error("null stream out");
+        *stream = ctx->pool.stream(ctx->pool.acquire());
+    });
+}
+
+int tw_stream_release(tw_ctx* ctx, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        const int i = ctx->pool.index_of(static_cast<cudaStream_t>(stream));
+        if (i < 0) contract_error("not a stream of this context's pool");
+        ctx->pool.release(i);
+    });
+}
+
+int tw_event_create(void** ev) {
+    return guarded([&] {
+        if (!ev) contract_error("null event out");
+        cudaEvent_t e;
+        TW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        *ev = e;
+    });
+}
+
+int tw_event_destroy(void* ev) {
+    return guarded([&] {
+        if (!ev) contract_error("null event");
+        TW_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+    });
+}
+
+int tw_event_record(void* ev, void* stream) {
+    return guarded([&] {
+        if (!ev) contract_error("null event");
+        TW_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+    });
+}
+
+int tw_event_query(void* ev, int* done) {
+    return guarded([&] {
+        if (!ev || !done) contract_error("null event or out");
+        const cudaError_t q = cudaEventQuery(static_cast<cudaEvent_t>(ev));
+        if (q == cudaErrorNotReady) {
+            *done = 0;
+            return;
+        }
+        TW_CUDA(q);
+        *done = 1;
+    });
+}
+
+int tw_event_wait(tw_ctx* ctx, void* ev) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!ev) contract_error("null event");
+        TaskAware::wait_static(static_cast<cudaEvent_t>(ev));
+    });
+}
+
+int tw_stream_wait_event(void* stream, void* ev) {
+    return guarded([&] {
+        if (!ev) contract_error("null event");
+        TW_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev), 0));
+    });
+}
+
+int tw_event_bind_async(tw_ctx* ctx, void* ev, void (*done)(void* arg), void* arg) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!ev || !done) contract_error("null event or callback");
+        {
+            std::lock_guard lk(ctx->ta_mu);
+            if (!ctx->ta) ctx->ta = std::make_unique<TaskAware>(ctx->device, 20e-6);
+        }
+        ctx->ta->bind_callback(static_cast<cudaEvent_t>(ev), done, arg);
     });
 }
 

@@ -108,6 +108,15 @@ class Runtime:
         N.check(_lib().tw_ctx_compute_stream(self.h, C.byref(s)))
         self.compute_stream = int(s.value or 0)
 
+    def acquire_stream(self) -> int:
+        """QueuePool::acquire: a pooled stream (blocks while all are out)."""
+        s = C.c_void_p()
+        N.check(_lib().tw_stream_acquire(self.h, C.byref(s)))
+        return int(s.value or 0)
+
+    def release_stream(self, stream: int) -> None:
+        N.check(_lib().tw_stream_release(self.h, C.c_void_p(stream)))
+
     def close(self):
         if getattr(self, "h", None):
             N.check(_lib().tw_ctx_destroy(self.h))
@@ -174,6 +183,45 @@ def default_runtime() -> Runtime:
     if _default_rt is None:
         _default_rt = Runtime(0)
     return _default_rt
+
+
+
+
+class Event:
+    """A device event with the reference's record / query / wait and the
+    task-aware bind_event_async (tw_event_*)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        N.check(_lib().tw_event_create(C.byref(h)))
+        self.h = h
+        self._cbs = []  # keep bound callbacks alive until they fire
+
+    def record(self, stream: int) -> None:
+        N.check(_lib().tw_event_record(self.h, C.c_void_p(stream)))
+
+    def query(self) -> bool:
+        d = C.c_int()
+        N.check(_lib().tw_event_query(self.h, C.byref(d)))
+        return bool(d.value)
+
+    def wait(self, rt: Runtime) -> None:
+        N.check(_lib().tw_event_wait(rt.h, self.h))
+
+    def block_stream(self, stream: int) -> None:
+        """Later work on `stream` waits for this event (device edge)."""
+        N.check(_lib().tw_stream_wait_event(C.c_void_p(stream), self.h))
+
+    def bind_async(self, rt: Runtime, done) -> None:
+        """done() runs on the context's polling thread once the event completes."""
+        cb = N.DONE_CB(lambda _arg: done())
+        self._cbs.append(cb)
+        N.check(_lib().tw_event_bind_async(rt.h, self.h, cb, None))
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.check(_lib().tw_event_destroy(self.h))
+            self.h = None
 
 
 @dataclass

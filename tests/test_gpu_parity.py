@@ -684,3 +684,45 @@ def test_peer_transport_under_concurrency(orc, golden, dims, P_):
         check_history(hs[0], want_h)
         assert np.all(rel_gap(G.solution(), want_x) <= 1e-10)
     G.close()
+
+
+def test_streams_events_and_task_aware_binding():
+    """The reference's QueuePool / Device / TaskAware layer over real CUDA
+    objects (tw_stream_* / tw_event_*): FIFO pool exhaustion, a non-blocking
+    query, a device-side edge and bind_event_async's release hook."""
+    import threading
+    rt = P.Runtime(0, stream_pool_capacity=2)
+    s1, s2 = rt.acquire_stream(), rt.acquire_stream()
+    assert s1 != s2
+    got = []
+    t = threading.Thread(target=lambda: got.append(rt.acquire_stream()))
+    t.start()
+    t.join(0.2)
+    assert t.is_alive()  # pool exhausted: the third acquire waits (FIFO)
+    rt.release_stream(s1)
+    t.join(5)
+    assert got == [s1]
+    with pytest.raises(P.ContractViolation):
+        rt.release_stream(12345)
+    # a long kernel on s2, an event after it, an edge into s1 and a bound callback
+    ts2 = torch.cuda.ExternalStream(s2)
+    ev = P.Event()
+    fired = threading.Event()
+    with torch.cuda.stream(ts2):
+        torch.cuda._sleep(200_000_000)  # ~0.1 s of GPU time
+    ev.record(s2)
+    ev.bind_async(rt, fired.set)
+    assert not ev.query() and not fired.is_set()
+    x = torch.zeros(1, device="cuda:0")
+    ev.block_stream(s1)
+    with torch.cuda.stream(torch.cuda.ExternalStream(s1)):
+        x += 1  # ordered after the sleep through the event edge
+    ev.wait(rt)
+    assert ev.query()
+    assert fired.wait(5)
+    torch.cuda.synchronize()
+    assert x.item() == 1.0
+    rt.release_stream(s1)
+    rt.release_stream(s2)
+    ev.close()
+    rt.close()
