@@ -180,6 +180,18 @@ int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, con
  * group on `stream`, collective over the ranks.  A no-op for one rank. */
 int tw_halo_exchange(const tw_ell* A, double* x, void* stream);
 
+/* The CG's fused update kernels as standalone operators, scalars read on
+ * the device (no host round trip inside a caller's DAG):
+ *   K2 (x_up + r_up + dot_rr, cg.cpp:380-386 / 262-288):
+ *      x += a p; r += (-a) Ap; *rr_dev = sum r[i]^2 over [i0, i1), a = *alpha_dev
+ *   K3 (p_up, cg.cpp:389 / 313-332): p = r + b p, b = *beta_dev
+ * Same roundings as waxpby_range (bit-identical); the dot is a fixed-order
+ * tree. */
+int tw_update_xr_rr(tw_ctx* ctx, const double* alpha_dev, double* x, const double* p, double* r,
+                    const double* Ap, int64_t i0, int64_t i1, double* rr_dev, void* stream);
+int tw_update_p(tw_ctx* ctx, const double* beta_dev, const double* r, double* p, int64_t i0,
+                int64_t i1, void* stream);
+
 /* make_tile_plan(A, tiles) (cg.cpp:348-370) over the owned rows; band in
  * GLOBAL columns like the reference.  TW_ERR_CONFIG if tiles < 1 or > rows. */
 int tw_make_tile_plan(const tw_ell* A, int tiles, int64_t* r0, int64_t* r1, int64_t* band_lo,

@@ -8,14 +8,14 @@ is the Python face that mirrors the reference's operator API
 from . import _native
 from .hpccg import (CgBackend, CgOptions, CgResult, CgSolver, ConfigError, ContractViolation, Event,
                     CudaError, EllMatrix, EmulatedRankGroup, NcclError, Runtime, Tile, cg_monolithic, cg_tasks,
-                    default_runtime, dot_range, dump_csr, halo_exchange, load_csr, parse_csr, ell_from_csr, gen_stencil_matrix,
+                    default_runtime, dot_range, dump_csr, halo_exchange, update_p, update_xr_rr, load_csr, parse_csr, ell_from_csr, gen_stencil_matrix,
                     make_tile_plan, rhs_splitmix, rhs_xorshift, slab_partition, slab_plan, spmv_dot,
                     spmv_range, task_dag_edges, waxpby_range)
 
 __all__ = [
     "CgBackend", "CgOptions", "CgResult", "CgSolver", "ConfigError", "ContractViolation", "Event",
     "CudaError", "EllMatrix", "EmulatedRankGroup", "NcclError", "Runtime", "Tile", "cg_monolithic", "cg_tasks",
-    "default_runtime", "dot_range", "dump_csr", "halo_exchange", "load_csr", "parse_csr", "ell_from_csr", "gen_stencil_matrix", "make_tile_plan",
+    "default_runtime", "dot_range", "dump_csr", "halo_exchange", "update_p", "update_xr_rr", "load_csr", "parse_csr", "ell_from_csr", "gen_stencil_matrix", "make_tile_plan",
     "rhs_splitmix", "rhs_xorshift", "slab_partition", "slab_plan", "spmv_dot", "spmv_range", "task_dag_edges", "waxpby_range",
     "_native",
 ]

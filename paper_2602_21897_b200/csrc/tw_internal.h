@@ -134,7 +134,8 @@ struct Fin {
 
 // Where an update kernel takes its scalar from: sc->alpha / sc->beta when
 // count == 0, else recomputed per block from `count` partials summed in
-// order (the cross-rank allgather result).
+// order (the cross-rank allgather result); with sc == nullptr (the
+// standalone tw_update_* ops) the scalar itself is *parts.
 // With `flags` (peer transport) every block first acquire-waits until the
 // `count` flags carry this iteration's stamp, then reads the partials.
 struct ScalarSrc {

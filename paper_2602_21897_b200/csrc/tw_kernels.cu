@@ -324,7 +324,7 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
     if (asrc.count > 0)
         alpha = __ddiv_rn(sc->rtrans, sum_parts(asrc.parts, asrc.count));
     else
-        alpha = sc->alpha;
+        alpha = sc ? sc->alpha : __ldcg(asrc.parts); // standalone op: alpha from a device scalar
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
     double part = 0.0;
     for_pairs(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
@@ -415,7 +415,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
         rr = sum_parts(bsrc.parts, bsrc.count);
         beta = __ddiv_rn(rr, sc->rtrans);
     } else {
-        beta = sc->beta;
+        beta = sc ? sc->beta : __ldcg(bsrc.parts); // standalone op: beta from a device scalar
     }
     const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;

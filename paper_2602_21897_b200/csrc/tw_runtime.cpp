@@ -932,6 +932,40 @@ int tw_dot_range(tw_ctx* ctx, const double* a, const double* b, int64_t i0, int6
     });
 }
 
+// K2 / K3 as standalone operators (the fused forms of cg.cpp:380-389) with
+// the scalar read on the device, so a caller's DAG never round-trips it.
+int tw_update_xr_rr(tw_ctx* ctx, const double* alpha_dev, double* x, const double* p, double* r,
+                    const double* Ap, int64_t i0, int64_t i1, double* rr_dev, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!alpha_dev || !rr_dev) contract_error("null scalar pointer");
+        if (i0 > i1) contract_error("update range reversed");
+        TW_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = pick(ctx, stream);
+        if (i0 == i1) {
+            TW_CUDA(cudaMemsetAsync(rr_dev, 0, sizeof(double), s));
+            return;
+        }
+        launch_update_xr(i0, i1, x, p, r, Ap, nullptr, ScalarSrc{alpha_dev, 0, nullptr},
+                         ctx_red_scratch(ctx, s), Fin{FIN_STORE, rr_dev, nullptr, nullptr},
+                         ctx->cfg.stream_blocks, s);
+    });
+}
+
+int tw_update_p(tw_ctx* ctx, const double* beta_dev, const double* r, double* p, int64_t i0,
+                int64_t i1, void* stream) {
+    return guarded([&] {
+        check_ctx(ctx);
+        if (!beta_dev) contract_error("null scalar pointer");
+        if (i0 > i1) contract_error("update range reversed");
+        if (i0 == i1) return;
+        TW_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t s = pick(ctx, stream);
+        launch_update_p(i0, i1, r, p, nullptr, ScalarSrc{beta_dev, 0, nullptr},
+                        ctx_red_scratch(ctx, s), nullptr, ctx->cfg.stream_blocks, s);
+    });
+}
+
 int tw_waxpby_range(tw_ctx* ctx, double alpha, const double* x, double beta, const double* y,
                     double* w, int64_t i0, int64_t i1, void* stream) {
     return guarded([&] {

@@ -398,6 +398,28 @@ def halo_exchange(A: EllMatrix, x, stream: int | None = None) -> None:
     N.check(_lib().tw_halo_exchange(A.h, C.c_void_p(_ptr(x)), C.c_void_p(stream or 0)))
 
 
+def update_xr_rr(alpha: float, x, p, r, Ap, i0: int, i1: int, rt: Runtime | None = None) -> float:
+    """Fused K2 standalone: x += alpha p; r -= alpha Ap on [i0, i1); returns
+    r.r over the range (alpha staged in a device scalar)."""
+    rt = rt or default_runtime()
+    sc = rt.alloc(2)
+    sc.upload(np.array([alpha, 0.0]))
+    N.check(_lib().tw_update_xr_rr(rt.h, C.c_void_p(sc.ptr), C.c_void_p(_ptr(x)), C.c_void_p(_ptr(p)),
+                                   C.c_void_p(_ptr(r)), C.c_void_p(_ptr(Ap)), i0, i1,
+                                   C.c_void_p(sc.ptr + 8), None))
+    return float(sc.download()[1])
+
+
+def update_p(beta: float, r, p, i0: int, i1: int, rt: Runtime | None = None) -> None:
+    """Fused K3 standalone: p = r + beta p on [i0, i1)."""
+    rt = rt or default_runtime()
+    sc = rt.alloc(1)
+    sc.upload(np.array([beta]))
+    N.check(_lib().tw_update_p(rt.h, C.c_void_p(sc.ptr), C.c_void_p(_ptr(r)), C.c_void_p(_ptr(p)),
+                               i0, i1, None))
+    rt.synchronize()
+
+
 def dot_range(a, b, i0: int, i1: int, rt: Runtime | None = None) -> float:
     """dot_range (kernels.cpp:15-20) as a fixed-order device reduction."""
     rt = rt or default_runtime()

@@ -167,6 +167,27 @@ def test_waxpby_bit_exact_and_aliasing(rt, orc):
     assert np.array_equal(host(xd), want)
 
 
+def test_standalone_fused_updates_bit_exact(rt, orc):
+    """tw_update_xr_rr / tw_update_p (K2 / K3 as operators) against the
+    reference's waxpby_range and dot_range on ragged ranges."""
+    n = 100_003
+    x, p, r, ap = (orc.rhs_splitmix(n, s) for s in (1, 2, 3, 4))
+    alpha, beta = 0.3712345678901, -1.25e-3
+    for i0, i1 in ((0, n), (1, n - 1), (7, 8), (5, 5)):
+        xd, pd, rd, ad = dev(x), dev(p), dev(r), dev(ap)
+        rr = P.update_xr_rr(alpha, xd, pd, rd, ad, i0, i1, rt=rt)
+        wx, wr = x.copy(), r.copy()
+        wx[i0:i1] = orc.waxpby(1.0, x, alpha, p)[i0:i1]
+        wr[i0:i1] = orc.waxpby(1.0, r, -alpha, ap)[i0:i1]
+        assert np.array_equal(host(xd), wx) and np.array_equal(host(rd), wr)
+        want = orc.dot(wr, wr, i0, i1) if i1 > i0 else 0.0
+        assert (rr == want == 0.0) or rel_gap(rr, want) < 1e-12
+        P.update_p(beta, rd, pd, i0, i1, rt=rt)
+        wp = p.copy()
+        wp[i0:i1] = orc.waxpby(1.0, wr, beta, p)[i0:i1]
+        assert np.array_equal(host(pd), wp)
+
+
 def test_dot_identities(rt, orc):
     n = 1000  # test_bench.cpp:188-205
     ones = dev(np.ones(n))
