@@ -1,7 +1,8 @@
 // CG drivers of libtw_hpccg: cg_monolithic and the cg_tasks block-task DAG
 // (cg.cpp:166-447) re-expressed as CUDA streams, events and graphs, with all
-// scalars resident on the device and, across GPUs, a z-slab decomposition
-// with NCCL halo exchange and rank-ordered scalar reductions.
+// scalars resident on the device; the persistent DAG dispatcher's tables;
+// the solver ABI.  Across ranks the iteration's phases come from
+// tw_cg_dist.cpp (z-slab decomposition, NCCL or NVLink peer transport).
 //
 // Per iteration the device work is three HBM-bound kernels:
 //   K1 spmv_pAp   Ap = A p, p.Ap            (spmv:i:t + dot_pAp:i:t)
@@ -17,114 +18,16 @@
 // edges between pooled streams (or edges of a captured CUDA graph).
 #include <algorithm>
 #include <cmath>
-#include <cstring>
 #include <cstdlib>
 #include <cstring>
-#include <map>
 #include <optional>
 #include <set>
 #include <sstream>
 
-#include "tw_dag_host.h"
-#include "tw_objects.h"
-
-using namespace tw;
-
-struct tw_cg {
-    tw_ctx* ctx = nullptr;
-    const tw_ell* A = nullptr;
-    tw_cg_options opt{};
-    int max_iters = 0;
-    int T = 1;
-    int P = 1;
-    bool dist = false; // communicator attached: halo + rank-ordered allgathers
-    int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
-    bool glo = false, ghi = false;
-    tw_slab_t slab{}; // z-slab geometry (multi-rank)
-    // NVLink peer transport (tw_peer.cu): own receive window, links to the
-    // other ranks, device copy of the links, IPC mappings to release
-    bool peer = false;
-    PeerWindow* win = nullptr;
-    PeerLinks links{};
-    PeerLinks* d_links = nullptr;
-    std::vector<void*> ipc_mapped;
-    unsigned epoch = 0; // set_rhs count
-
-    double* x = nullptr;
-    double* r = nullptr;
-    double* p_base = nullptr;
-    double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
-    double* p_owned = nullptr;
-    double* Ap = nullptr;
-    CgScalars* sc = nullptr;
-    double* history = nullptr;
-    double* parts = nullptr;
-    double* block_parts = nullptr;
-    unsigned* tickets = nullptr;
-    int maxg = 0;
-
-    // partial slots (offsets into parts)
-    double *pa = nullptr, *rrp = nullptr, *pm = nullptr, *send_a = nullptr, *send_b = nullptr,
-           *recv_a = nullptr, *recv_b = nullptr, *send_r = nullptr, *recv_r = nullptr;
-
-    std::vector<int64_t> t_r0, t_r1, t_lo, t_hi; // tile plan (local rows / local columns)
-    DagSpec dag;                                 // inputs of the logical DAG
-    std::vector<LTask> ltasks;                   // one iteration's logical tasks (template)
-    std::vector<PNode> nodes;                    // one iteration's physical nodes
-    std::vector<cudaEvent_t> ev[2];              // per node, by iteration parity
-    std::vector<cudaEvent_t> tail_ev;            // per pool stream + comm
-    cudaEvent_t fork_ev = nullptr, halo_ev = nullptr, pready_ev = nullptr;
-    cudaEvent_t ag_in_ev = nullptr, ag_out_ev = nullptr;
-
-    cudaGraphExec_t graph = nullptr;
-    std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
-    std::map<int, cudaGraphExec_t> k_graphs;     // K fused iterations, untimed
-    // single-domain monolithic: K3 fused into the next iteration's K1
-    // (launch_spmv_fusep) with p ping-ponging between p_owned and p_alt;
-    // every tw_cg_iterate call starts and ends with p in p_owned
-    bool fusep = false;
-    double* p_alt = nullptr;
-    double* p_cur = nullptr;
-    int enqueued = 0;
-    // per-kernel timing (monolithic, no graph): 4 events per timed iteration
-    bool timing = false;
-    std::vector<cudaEvent_t> tev;
-    int timed = 0;
-    std::vector<cudaEvent_t> iter_ev; // iteration-end timing events (marks on)
-    // persistent dispatcher (TW_DISPATCH_PERSISTENT): flattened K-iteration
-    // DAG tables, cached per K
-    struct DagTable {
-        int ntasks = 0, nchunks = 0;
-        DagTask* d_tasks = nullptr;
-        int* d_chunk_task = nullptr;
-        int* d_succ = nullptr;
-        int* d_npred = nullptr;
-        int* d_remaining = nullptr;
-        unsigned* d_chunk_done = nullptr;
-        double* d_chunk_part = nullptr;
-    };
-    std::map<int, DagTable> dag_tables;
-    int dag_grid = 0;
-    unsigned* d_ticket = nullptr;
-    unsigned long long* d_stamps = nullptr;
-    double t0 = 0.0;
-    std::vector<double> marks;
-    std::unique_ptr<TaskAware> ta;
-
-    RedScratch slot(int i) const {
-        return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
-    }
-    EllView view() const { return A->view(); }
-    cudaStream_t node_stream(const PNode& nd) const {
-        if (nd.kind == PK_HALO) return ctx->comm;
-        const unsigned C = ctx->pool.capacity();
-        if (nd.kind == PK_ALPHA || nd.kind == PK_BETA) return ctx->pool.stream(0);
-        return ctx->pool.stream(static_cast<int>(static_cast<unsigned>(nd.tile) % C));
-    }
-};
+#include "tw_cg_state.h"
 
 namespace tw {
-namespace {
+namespace cgi {
 
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
 void build_schedule(tw_cg* cg) {
@@ -157,117 +60,6 @@ void build_schedule(tw_cg* cg) {
 
 int launch_blocks(const tw_cg* cg, bool spmv) {
     return spmv ? cg->ctx->cfg.spmv_blocks : cg->ctx->cfg.stream_blocks;
-}
-
-// Every NCCL call of the communicator is issued on the one comm stream, so
-// the halo and the scalar allgathers are strictly ordered there; the caller's
-// stream is joined in and out with events.
-void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s) {
-    cudaStream_t c = cg->ctx->comm;
-    TW_CUDA(cudaEventRecord(cg->ag_in_ev, s));
-    TW_CUDA(cudaStreamWaitEvent(c, cg->ag_in_ev, 0));
-    TW_NCCL(nccl().AllGather(send, recv, 1, ncclDouble, cg->ctx->nccl_comm, c));
-    TW_CUDA(cudaEventRecord(cg->ag_out_ev, c));
-    TW_CUDA(cudaStreamWaitEvent(s, cg->ag_out_ev, 0));
-}
-
-void halo_exchange(tw_cg* cg, cudaStream_t s) {
-    const auto& api = nccl();
-    const size_t pl = static_cast<size_t>(cg->plane);
-    const int rank = cg->ctx->rank;
-    const tw_slab_t& sp = cg->slab;
-    double* p = cg->p_local;
-    TW_NCCL(api.GroupStart());
-    if (sp.ghost_lo) {
-        TW_NCCL(api.Recv(p + sp.recv_lo, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
-        TW_NCCL(api.Send(p + sp.send_lo, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
-    }
-    if (sp.ghost_hi) {
-        TW_NCCL(api.Recv(p + sp.recv_hi, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
-        TW_NCCL(api.Send(p + sp.send_hi, pl, ncclDouble, rank + 1, cg->ctx->nccl_comm, s));
-    }
-    TW_NCCL(api.GroupEnd());
-}
-
-// Phases of one rank's distributed monolithic iteration.  The NCCL path
-// interleaves them with the halo and the allgathers (enqueue_mono); the
-// emulated rank group (tw_cg_group_iterate) runs them rank by rank with
-// loopback copies in place of NCCL.
-void dist_spmv_interior(tw_cg* cg, cudaStream_t s) { // rows that read no ghost plane
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
-                RowRange{0, 0}, true, cg->slot(0), Fin{FIN_STORE, cg->pm, nullptr, nullptr},
-                launch_blocks(cg, true), s);
-}
-
-void dist_spmv_boundary(tw_cg* cg, cudaStream_t s) { // the ghost-reading planes, then p.Ap
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
-                RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
-                Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, launch_blocks(cg, true), s);
-    launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
-}
-
-void dist_update_xr(tw_cg* cg, cudaStream_t s) { // alpha from the rank partials, local r.r
-    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
-                     ScalarSrc{cg->recv_a, cg->P}, cg->slot(0),
-                     Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, launch_blocks(cg, false), s);
-}
-
-void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; commit
-    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, cg->slot(0),
-                    cg->history, launch_blocks(cg, false), s);
-}
-
-// Phases of the peer transport (NVLink stores + flags, fused into the
-// kernels): 4 launches per iteration and no collective call.
-void peer_spmv(tw_cg* cg, cudaStream_t s) {
-    dist_spmv_interior(cg, s); // reads no ghost: overlaps the neighbours' K3 tails
-    const int ng = cg->slab.ghost_lo + cg->slab.ghost_hi;
-    const unsigned long long* gf = cg->slab.ghost_lo ? &cg->win->flag_ghost_lo : &cg->win->flag_ghost_hi;
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
-                RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
-                Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
-                launch_blocks(cg, true), s, ng ? gf : nullptr, ng);
-}
-
-void peer_update_xr(tw_cg* cg, cudaStream_t s) {
-    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
-                     ScalarSrc{cg->win->recv_a, cg->P, cg->win->flag_a}, cg->slot(0),
-                     Fin{FIN_PUBLISH_B, cg->send_b, cg->sc, nullptr, cg->d_links, nullptr},
-                     launch_blocks(cg, false), s);
-}
-
-void peer_update_p(tw_cg* cg, cudaStream_t s) {
-    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
-                    ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
-                    launch_blocks(cg, false), s, cg->d_links);
-}
-
-void alloc_window(tw_cg* cg) {
-    if (!cg->dist) contract_error("the peer transport needs a multi-rank context");
-    if (cg->opt.variant != TW_CG_MONOLITHIC)
-        config_error("the peer transport runs the monolithic variant");
-    if (cg->P > kMaxRanks) config_error("more ranks than the peer window holds");
-    if (!cg->win) {
-        TW_CUDA(cudaMalloc(&cg->win, sizeof(PeerWindow)));
-        TW_CUDA(cudaMemset(cg->win, 0, sizeof(PeerWindow)));
-    }
-}
-
-void finish_links(tw_cg* cg) {
-    cg->links.rank = cg->ctx->rank;
-    cg->links.nranks = cg->P;
-    cg->links.plane = cg->plane;
-    if (!cg->d_links) TW_CUDA(cudaMalloc(&cg->d_links, sizeof(PeerLinks)));
-    TW_CUDA(cudaMemcpy(cg->d_links, &cg->links, sizeof(PeerLinks), cudaMemcpyHostToDevice));
-    cg->peer = true;
-    if (cg->graph) { // graphs captured before the switch used the NCCL path
-        cudaGraphExecDestroy(cg->graph);
-        cg->graph = nullptr;
-    }
-    for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
-    cg->timed_graphs.clear();
-    for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
-    cg->k_graphs.clear();
 }
 
 // Timing event k (0..3) of the current timed iteration, or null.
@@ -303,7 +95,7 @@ void record(cudaEvent_t e, cudaStream_t s) {
 // (p_new = r + beta p_old formed on the fly, stored to the other buffer);
 // the last one ends with K3 proper, back into p_owned.  The arithmetic is
 // K3's, so the results are those of the three-kernel sequence.
-void enqueue_mono(tw_cg* cg, int i = 0, int k = 1, bool fuse = false) {
+void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
@@ -692,178 +484,6 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device) {
     reset_solve_state(cg);
 }
 
-// ------------------------------------------------ emulated rank group
-//
-// P contexts on ONE device, each owning a z-slab, driven phase by phase on a
-// single stream.  The NCCL transport is replaced by loopback device copies
-// (halo planes into the neighbours' ghost planes, every rank's partial into
-// every rank's receive slots); everything else -- slab geometry, ghost
-// layout, interior/boundary split, rank-ordered scalar sums -- is the code
-// the NCCL path runs.  No kernel ever waits on another: the host sequences
-// the phases, so this is safe on one GPU (B200_PROFILING.md).
-
-void group_check(tw_cg** g, int P) {
-    if (!g || P < 1) contract_error("empty rank group");
-    for (int r = 0; r < P; ++r) {
-        if (!g[r]) contract_error("null solver in rank group");
-        const tw_ctx* c = g[r]->ctx;
-        if (!c->emulated || c->rank != r || c->nranks != P)
-            contract_error("rank group entry " + std::to_string(r) +
-                           " is not emulated rank r of P (tw_ctx_init_emulated_rank)");
-        if (c->device != g[0]->ctx->device) contract_error("emulated ranks share one device");
-        if (g[r]->opt.variant != TW_CG_MONOLITHIC)
-            config_error("the emulated rank group runs the monolithic variant");
-    }
-}
-
-void loopback_allgather(tw_cg** g, int P, double* tw_cg::*send, double* tw_cg::*recv,
-                        cudaStream_t s) {
-    for (int r = 0; r < P; ++r)
-        for (int q = 0; q < P; ++q)
-            TW_CUDA(cudaMemcpyAsync(g[r]->*recv + q, g[q]->*send, sizeof(double),
-                                    cudaMemcpyDeviceToDevice, s));
-}
-
-void loopback_halo(tw_cg** g, int P, cudaStream_t s) {
-    for (int r = 0; r < P; ++r) {
-        const tw_slab_t& sp = g[r]->slab;
-        const size_t bytes = sizeof(double) * static_cast<size_t>(sp.plane);
-        if (sp.ghost_lo) // my lower ghost <- rank r-1's last owned plane
-            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_lo, g[r - 1]->p_local + g[r - 1]->slab.send_hi,
-                                    bytes, cudaMemcpyDeviceToDevice, s));
-        if (sp.ghost_hi) // my upper ghost <- rank r+1's first owned plane
-            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_hi, g[r + 1]->p_local + g[r + 1]->slab.send_lo,
-                                    bytes, cudaMemcpyDeviceToDevice, s));
-    }
-}
-
-// Every rank's compute stream continues after the group's work on s.
-void group_join(tw_cg** g, int P, cudaStream_t s) {
-    TW_CUDA(cudaEventRecord(g[0]->fork_ev, s));
-    for (int r = 1; r < P; ++r) TW_CUDA(cudaStreamWaitEvent(g[r]->ctx->compute, g[0]->fork_ev, 0));
-}
-
-// Peer transport inside the emulated group: the "peer" pointers are the
-// other ranks' buffers on the same device.
-void group_enable_peer(tw_cg** g, int P) {
-    group_check(g, P);
-    for (int r = 0; r < P; ++r)
-        if (g[r]->peer) contract_error("the peer transport is already connected");
-    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
-    for (int r = 0; r < P; ++r) alloc_window(g[r]);
-    for (int r = 0; r < P; ++r) {
-        PeerLinks& L = g[r]->links;
-        L = PeerLinks{};
-        for (int q = 0; q < P; ++q) L.win[q] = g[q]->win;
-        if (r > 0) {
-            L.ghost_lo_dst = g[r - 1]->p_local + g[r - 1]->slab.recv_hi;
-            L.ghost_lo_flag = &g[r - 1]->win->flag_ghost_hi;
-        }
-        if (r + 1 < P) {
-            L.ghost_hi_dst = g[r + 1]->p_local + g[r + 1]->slab.recv_lo;
-            L.ghost_hi_flag = &g[r + 1]->win->flag_ghost_lo;
-        }
-        finish_links(g[r]);
-    }
-}
-
-void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
-    group_check(g, P);
-    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
-    for (int r = 0; r < P; ++r) TW_CUDA(cudaStreamSynchronize(g[r]->ctx->compute));
-    cudaStream_t s = g[0]->ctx->compute;
-    for (int r = 0; r < P; ++r) set_rhs_prefix(g[r], b[r], on_device, s);
-    loopback_allgather(g, P, &tw_cg::send_r, &tw_cg::recv_r, s);
-    for (int r = 0; r < P; ++r)
-        launch_combine(g[r]->recv_r, P, Fin{FIN_RTRANS, nullptr, g[r]->sc, nullptr}, s);
-    if (g[0]->peer)
-        for (int r = 0; r < P; ++r)
-            launch_peer_push(g[r]->p_owned, g[r]->n, g[r]->plane, g[r]->links, g[r]->sc,
-                             g[r]->tickets, s);
-    TW_CUDA(cudaStreamSynchronize(s));
-    for (int r = 0; r < P; ++r) reset_solve_state(g[r]);
-}
-
-void group_iterate(tw_cg** g, int P, int k) {
-    group_check(g, P);
-    if (k < 0) config_error("negative iteration count");
-    for (int r = 0; r < P; ++r)
-        if (g[r]->enqueued + k > g[r]->max_iters) contract_error("iterations beyond max_iterations");
-    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
-    cudaStream_t s = g[0]->ctx->compute;
-    for (int r = 1; r < P; ++r) { // order after anything queued on the other ranks' streams
-        TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
-        TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
-    }
-    for (int it = 0; it < k && g[0]->peer; ++it) { // peer transport: stores + flags
-        for (int r = 0; r < P; ++r) peer_spmv(g[r], s);
-        for (int r = 0; r < P; ++r) peer_update_xr(g[r], s);
-        for (int r = 0; r < P; ++r) peer_update_p(g[r], s);
-    }
-    for (int it = 0; it < k && !g[0]->peer; ++it) {
-        loopback_halo(g, P, s);
-        for (int r = 0; r < P; ++r) {
-            dist_spmv_interior(g[r], s);
-            dist_spmv_boundary(g[r], s);
-        }
-        loopback_allgather(g, P, &tw_cg::send_a, &tw_cg::recv_a, s);
-        for (int r = 0; r < P; ++r) dist_update_xr(g[r], s);
-        loopback_allgather(g, P, &tw_cg::send_b, &tw_cg::recv_b, s);
-        for (int r = 0; r < P; ++r) dist_update_p(g[r], s);
-    }
-    group_join(g, P, s);
-    for (int r = 0; r < P; ++r) g[r]->enqueued += k;
-}
-
-// The peer-transport group as ONE cooperative kernel (rank_group_kernel):
-// the ranks run concurrently and really wait on one another's flags.
-void group_iterate_concurrent(tw_cg** g, int P, int k, int jitter) {
-    group_check(g, P);
-    if (!g[0]->peer) contract_error("the concurrent group runs the peer transport (tw_cg_group_enable_peer)");
-    if (k < 0) config_error("negative iteration count");
-    for (int r = 0; r < P; ++r)
-        if (g[r]->enqueued + k > g[r]->max_iters) contract_error("iterations beyond max_iterations");
-    if (k == 0) return;
-    TW_CUDA(cudaSetDevice(g[0]->ctx->device));
-    cudaStream_t s = g[0]->ctx->compute;
-    for (int r = 1; r < P; ++r) {
-        TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
-        TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
-    }
-    int B = rank_group_blocks_per_rank(P);
-    for (int r = 0; r < P; ++r) B = std::min(B, g[r]->maxg);
-    if (B < 1) config_error("more ranks than co-resident blocks");
-    std::vector<GroupRank> h(static_cast<size_t>(P));
-    GroupRank* d = nullptr;
-    unsigned* bars = nullptr;
-    TW_CUDA(cudaMalloc(&d, sizeof(GroupRank) * P));
-    TW_CUDA(cudaMalloc(&bars, sizeof(unsigned) * 2 * P));
-    TW_CUDA(cudaMemsetAsync(bars, 0, sizeof(unsigned) * 2 * P, s));
-    for (int r = 0; r < P; ++r) {
-        tw_cg* c = g[r];
-        GroupRank& R = h[static_cast<size_t>(r)];
-        R.A = c->view();
-        R.x = c->x; R.r = c->r; R.p_local = c->p_local; R.p_owned = c->p_owned; R.Ap = c->Ap;
-        R.pm = c->pm; R.send_b = c->send_b; R.history = c->history;
-        R.sc = c->sc;
-        R.rs = c->slot(0);
-        R.win = c->win;
-        R.links = c->d_links;
-        R.n_ghost = c->slab.ghost_lo + c->slab.ghost_hi;
-        R.ghost_flags = c->slab.ghost_lo ? &c->win->flag_ghost_lo : &c->win->flag_ghost_hi;
-        R.P = P;
-        R.n = c->n; R.int_r0 = c->slab.interior_r0; R.int_r1 = c->slab.interior_r1;
-        R.bar = bars + 2 * r;
-    }
-    TW_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(GroupRank) * P, cudaMemcpyHostToDevice, s));
-    launch_rank_group(d, P, B, k, jitter, s);
-    TW_CUDA(cudaStreamSynchronize(s));
-    cudaFree(d);
-    cudaFree(bars);
-    group_join(g, P, s);
-    for (int r = 0; r < P; ++r) g[r]->enqueued += k;
-}
-
 // Timing event at the end of iteration i-1 (i = 0: the start of the solve).
 cudaEvent_t iter_event(tw_cg* cg, int i) {
     while (static_cast<int>(cg->iter_ev.size()) <= i) {
@@ -1097,10 +717,13 @@ void wait_cg(tw_cg* cg) {
     TW_CUDA(cudaGetLastError());
 }
 
-} // namespace
+} // namespace cgi
 } // namespace tw
 
+using namespace tw::cgi;
+
 extern "C" {
+
 
 void tw_cg_options_default(tw_cg_options* o) {
     if (!o) return;
@@ -1255,94 +878,6 @@ int tw_cg_kernel_times(tw_cg* cg, double* k1, double* k2, double* k3, int* itera
     });
 }
 
-int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_is_device) {
-    return guarded([&] {
-        if (!b) contract_error("null rhs list");
-        group_set_rhs(cgs, nranks, b, b_is_device != 0);
-    });
-}
-
-int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations) {
-    return guarded([&] { group_iterate(cgs, nranks, iterations); });
-}
-
-int tw_cg_group_iterate_concurrent(tw_cg** cgs, int nranks, int iterations, int jitter) {
-    return guarded([&] { group_iterate_concurrent(cgs, nranks, iterations, jitter); });
-}
-
-int tw_cg_group_enable_peer(tw_cg** cgs, int nranks) {
-    return guarded([&] { group_enable_peer(cgs, nranks); });
-}
-
-// blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
-// byte offset of the lower ghost plane in p_base, [136,144) of the upper,
-// [144,148) rank.
-int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
-    return guarded([&] {
-        if (!cg || !blob) contract_error("null solver or blob");
-        TW_CUDA(cudaSetDevice(cg->ctx->device));
-        alloc_window(cg);
-        std::memset(blob, 0, TW_PEER_BLOB_BYTES);
-        cudaIpcMemHandle_t hw, hp;
-        TW_CUDA(cudaIpcGetMemHandle(&hw, cg->win));
-        TW_CUDA(cudaIpcGetMemHandle(&hp, cg->p_base));
-        std::memcpy(blob, &hw, sizeof(hw));
-        std::memcpy(blob + 64, &hp, sizeof(hp));
-        const int64_t lo = (cg->p_local + cg->slab.recv_lo - cg->p_base) * static_cast<int64_t>(sizeof(double));
-        const int64_t hi = (cg->p_local + cg->slab.recv_hi - cg->p_base) * static_cast<int64_t>(sizeof(double));
-        std::memcpy(blob + 128, &lo, 8);
-        std::memcpy(blob + 136, &hi, 8);
-        const int rank = cg->ctx->rank;
-        std::memcpy(blob + 144, &rank, 4);
-    });
-}
-
-int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
-    return guarded([&] {
-        if (!cg || !blobs) contract_error("null solver or blobs");
-        if (cg->peer) contract_error("the peer transport is already connected");
-        TW_CUDA(cudaSetDevice(cg->ctx->device));
-        alloc_window(cg);
-        const int P = cg->P, me = cg->ctx->rank;
-        PeerLinks& L = cg->links;
-        L = PeerLinks{};
-        auto open = [&](const unsigned char* h) {
-            cudaIpcMemHandle_t mh;
-            std::memcpy(&mh, h, sizeof(mh));
-            void* p = nullptr;
-            TW_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
-            cg->ipc_mapped.push_back(p);
-            return static_cast<unsigned char*>(p);
-        };
-        for (int q = 0; q < P; ++q) {
-            const unsigned char* b = blobs + static_cast<size_t>(q) * TW_PEER_BLOB_BYTES;
-            int rq = -1;
-            std::memcpy(&rq, b + 144, 4);
-            if (rq != q) contract_error("peer blobs must be in rank order");
-            if (q == me) {
-                L.win[q] = cg->win;
-                continue;
-            }
-            auto* w = reinterpret_cast<PeerWindow*>(open(b));
-            L.win[q] = w;
-            if (q == me - 1 || q == me + 1) {
-                unsigned char* pb = open(b + 64);
-                int64_t lo = 0, hi = 0;
-                std::memcpy(&lo, b + 128, 8);
-                std::memcpy(&hi, b + 136, 8);
-                if (q == me - 1) { // my first plane -> its upper ghost
-                    L.ghost_lo_dst = reinterpret_cast<double*>(pb + hi);
-                    L.ghost_lo_flag = &w->flag_ghost_hi;
-                } else {           // my last plane -> its lower ghost
-                    L.ghost_hi_dst = reinterpret_cast<double*>(pb + lo);
-                    L.ghost_hi_flag = &w->flag_ghost_lo;
-                }
-            }
-        }
-        finish_links(cg);
-    });
-}
-
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
@@ -1392,3 +927,4 @@ int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iteratio
 }
 
 } // extern "C"
+

@@ -1,0 +1,161 @@
+// Solver state shared by the CG drivers (tw_cg.cpp: single-GPU monolithic
+// and block-task DAG, graphs, the persistent dispatcher) and the multi-rank
+// transports (tw_cg_dist.cpp: NCCL, NVLink peer, emulated rank groups).
+// Internal header of libtw_hpccg; the C ABI is include/tw_hpccg.h.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "tw_dag_host.h"
+#include "tw_objects.h"
+
+using namespace tw; // internal header: tw_cg sits at global scope (C ABI type)
+
+struct tw_cg {
+    tw_ctx* ctx = nullptr;
+    const tw_ell* A = nullptr;
+    tw_cg_options opt{};
+    int max_iters = 0;
+    int T = 1;
+    int P = 1;
+    bool dist = false; // communicator attached: halo + rank-ordered allgathers
+    int64_t n = 0, plane = 0, x_len = 0, diag_shift = 0;
+    bool glo = false, ghi = false;
+    tw_slab_t slab{}; // z-slab geometry (multi-rank)
+    // NVLink peer transport (tw_peer.cu): own receive window, links to the
+    // other ranks, device copy of the links, IPC mappings to release
+    bool peer = false;
+    PeerWindow* win = nullptr;
+    PeerLinks links{};
+    PeerLinks* d_links = nullptr;
+    std::vector<void*> ipc_mapped;
+    unsigned epoch = 0; // set_rhs count
+
+    double* x = nullptr;
+    double* r = nullptr;
+    double* p_base = nullptr;
+    double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
+    double* p_owned = nullptr;
+    double* Ap = nullptr;
+    CgScalars* sc = nullptr;
+    double* history = nullptr;
+    double* parts = nullptr;
+    double* block_parts = nullptr;
+    unsigned* tickets = nullptr;
+    int maxg = 0;
+
+    // partial slots (offsets into parts)
+    double *pa = nullptr, *rrp = nullptr, *pm = nullptr, *send_a = nullptr, *send_b = nullptr,
+           *recv_a = nullptr, *recv_b = nullptr, *send_r = nullptr, *recv_r = nullptr;
+
+    std::vector<int64_t> t_r0, t_r1, t_lo, t_hi; // tile plan (local rows / local columns)
+    DagSpec dag;                                 // inputs of the logical DAG
+    std::vector<LTask> ltasks;                   // one iteration's logical tasks (template)
+    std::vector<PNode> nodes;                    // one iteration's physical nodes
+    std::vector<cudaEvent_t> ev[2];              // per node, by iteration parity
+    std::vector<cudaEvent_t> tail_ev;            // per pool stream + comm
+    cudaEvent_t fork_ev = nullptr, halo_ev = nullptr, pready_ev = nullptr;
+    cudaEvent_t ag_in_ev = nullptr, ag_out_ev = nullptr;
+
+    cudaGraphExec_t graph = nullptr;
+    std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
+    std::map<int, cudaGraphExec_t> k_graphs;     // K fused iterations, untimed
+    // single-domain monolithic: K3 fused into the next iteration's K1
+    // (launch_spmv_fusep) with p ping-ponging between p_owned and p_alt;
+    // every tw_cg_iterate call starts and ends with p in p_owned
+    bool fusep = false;
+    double* p_alt = nullptr;
+    double* p_cur = nullptr;
+    int enqueued = 0;
+    // per-kernel timing (monolithic, no graph): 4 events per timed iteration
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;
+    int timed = 0;
+    std::vector<cudaEvent_t> iter_ev; // iteration-end timing events (marks on)
+    // persistent dispatcher (TW_DISPATCH_PERSISTENT): flattened K-iteration
+    // DAG tables, cached per K
+    struct DagTable {
+        int ntasks = 0, nchunks = 0;
+        DagTask* d_tasks = nullptr;
+        int* d_chunk_task = nullptr;
+        int* d_succ = nullptr;
+        int* d_npred = nullptr;
+        int* d_remaining = nullptr;
+        unsigned* d_chunk_done = nullptr;
+        double* d_chunk_part = nullptr;
+    };
+    std::map<int, DagTable> dag_tables;
+    int dag_grid = 0;
+    unsigned* d_ticket = nullptr;
+    unsigned long long* d_stamps = nullptr;
+    double t0 = 0.0;
+    std::vector<double> marks;
+    std::unique_ptr<TaskAware> ta;
+
+    RedScratch slot(int i) const {
+        return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
+    }
+    EllView view() const { return A->view(); }
+    cudaStream_t node_stream(const PNode& nd) const {
+        if (nd.kind == PK_HALO) return ctx->comm;
+        const unsigned C = ctx->pool.capacity();
+        if (nd.kind == PK_ALPHA || nd.kind == PK_BETA) return ctx->pool.stream(0);
+        return ctx->pool.stream(static_cast<int>(static_cast<unsigned>(nd.tile) % C));
+    }
+};
+
+namespace tw {
+namespace cgi {
+
+// tw_cg.cpp
+void build_schedule(tw_cg* cg);
+int launch_blocks(const tw_cg* cg, bool spmv);
+cudaEvent_t tmark(tw_cg* cg, int k);
+void record(cudaEvent_t e, cudaStream_t s);
+void enqueue_mono(tw_cg* cg, int i = 0, int k = 1, bool fuse = false);
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st);
+void fork_streams(tw_cg* cg);
+void join_streams(tw_cg* cg);
+void enqueue_tasks(tw_cg* cg, int parity, bool first);
+void enqueue_iteration_body(tw_cg* cg, int parity, bool first);
+void build_graph(tw_cg* cg);
+void free_cg(tw_cg* cg);
+tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_iters);
+void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s);
+void reset_solve_state(tw_cg* cg);
+void set_rhs(tw_cg* cg, const double* b, bool on_device);
+cudaEvent_t iter_event(tw_cg* cg, int i);
+int64_t env_or(const char* name, int64_t dflt);
+int64_t dag_spmv_chunk_slices();
+int64_t dag_vec_chunk_rows();
+void build_dag_table(tw_cg* cg, int k);
+void enqueue_persistent(tw_cg* cg, int k);
+void iterate(tw_cg* cg, int k);
+void wait_cg(tw_cg* cg);
+
+// tw_cg_dist.cpp
+void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s);
+void halo_exchange(tw_cg* cg, cudaStream_t s);
+void dist_spmv_interior(tw_cg* cg, cudaStream_t s);
+void dist_spmv_boundary(tw_cg* cg, cudaStream_t s);
+void dist_update_xr(tw_cg* cg, cudaStream_t s);
+void dist_update_p(tw_cg* cg, cudaStream_t s);
+void peer_spmv(tw_cg* cg, cudaStream_t s);
+void peer_update_xr(tw_cg* cg, cudaStream_t s);
+void peer_update_p(tw_cg* cg, cudaStream_t s);
+void alloc_window(tw_cg* cg);
+void finish_links(tw_cg* cg);
+void group_check(tw_cg** g, int P);
+void loopback_allgather(tw_cg** g, int P, double* tw_cg::*send, double* tw_cg::*recv,
+                        cudaStream_t s);
+void loopback_halo(tw_cg** g, int P, cudaStream_t s);
+void group_join(tw_cg** g, int P, cudaStream_t s);
+void group_enable_peer(tw_cg** g, int P);
+void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device);
+void group_iterate(tw_cg** g, int P, int k);
+void group_iterate_concurrent(tw_cg** g, int P, int k, int jitter);
+
+} // namespace cgi
+} // namespace tw
