@@ -23,6 +23,13 @@ constexpr int kThreads = 256;
 constexpr int kTmaWarps = TW_TMA_WARPS;   // consumer warps per CTA (one CTA per SM)
 constexpr int kTmaStages = TW_TMA_STAGES; // shared-memory stages per warp
 
+// Grid for a grid-stride kernel of `work_threads` threads, at most `blocks`.
+inline int clamp_blocks(int64_t work_threads, int blocks) {
+    int64_t need = (work_threads + kThreads - 1) / kThreads;
+    if (need < 1) need = 1;
+    return static_cast<int>(need < blocks ? need : blocks);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)

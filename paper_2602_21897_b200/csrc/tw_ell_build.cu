@@ -1,0 +1,297 @@
+// sm_100a builders of the sliced-ELL matrix (K0) and their helpers:
+//   stencil_widths / stencil_fill   gen_stencil_matrix (csr.cpp:29-59) on the
+//                                   device, rows in the reference's order
+//   csr_widths / csr_fill           any CSR matrix (tw_ell_from_csr)
+//   band                            min / max column of a row range
+//                                   (make_tile_plan's band, cg.cpp:358-367)
+//   scan_*                          int64 exclusive scan for slice offsets
+// One warp per 32-row slice, lane = row; the chunked entry layout is the
+// one tw_internal.h documents (ell_val_pos / ell_col_pos).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tw_device.cuh"
+#include "tw_internal.h"
+
+namespace tw {
+
+namespace {
+
+using namespace dev;
+
+// --------------------------------------------------------------- K0 generator
+
+__device__ __forceinline__ int64_t axis_span(int64_t c, int64_t d) {
+    return 1 + (c > 0) + (c + 1 < d);
+}
+
+// Width of each 32-row slice = longest stencil row in it (closed form).
+__global__ void stencil_widths_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                                      int64_t n_rows, int64_t n_slices, int64_t* widths) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t plane = nx * ny;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t row = s * 32 + lane;
+        int len = 0;
+        if (row < n_rows) {
+            const int64_t g = row + row_offset;
+            const int64_t z = g / plane, rem = g - z * plane, y = rem / nx, x = rem - y * nx;
+            len = static_cast<int>(axis_span(x, nx) * axis_span(y, ny) * axis_span(z, nz));
+        }
+        const int w = __reduce_max_sync(0xffffffffu, len);
+        if (lane == 0) widths[s] = 32LL * w;
+    }
+}
+
+// One warp per slice, lane = row: walk the row's neighbours in the
+// reference's (dz, dy, dx) order (csr.cpp:46-54) and drop them into the
+// chunked slice layout; pad to the slice width with col = -1.
+__global__ void stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                                    int64_t col_offset, int64_t n_rows, int64_t n_slices,
+                                    const int64_t* __restrict__ slice_off, double* vals,
+                                    int32_t* cols) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t plane = nx * ny;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t off = slice_off[s];
+        const int w = static_cast<int>((slice_off[s + 1] - off) >> 5);
+        double* vb = vals + off;
+        int32_t* cb = cols + off;
+        const int64_t row = s * 32 + lane;
+        int k = 0;
+        if (row < n_rows) {
+            const int64_t g = row + row_offset;
+            const int64_t z = g / plane, rem = g - z * plane, y = rem / nx, x = rem - y * nx;
+            for (int64_t cz = z - 1; cz <= z + 1; ++cz) {
+                if (cz < 0 || cz >= nz) continue;
+                for (int64_t cy = y - 1; cy <= y + 1; ++cy) {
+                    if (cy < 0 || cy >= ny) continue;
+                    const int64_t line = (cz * ny + cy) * nx;
+                    for (int64_t cx = x - 1; cx <= x + 1; ++cx) {
+                        if (cx < 0 || cx >= nx) continue;
+                        const bool diag = cx == x && cy == y && cz == z;
+                        vb[ell_val_pos(k, lane, w)] = diag ? 27.0 : -1.0;
+                        cb[ell_col_pos(k, lane, w)] = static_cast<int32_t>(line + cx - col_offset);
+                        ++k;
+                    }
+                }
+            }
+        }
+        for (; k < w; ++k) {
+            vb[ell_val_pos(k, lane, w)] = 0.0;
+            cb[ell_col_pos(k, lane, w)] = -1;
+        }
+    }
+}
+
+__global__ void csr_widths_kernel(const int64_t* __restrict__ row_ptr, int64_t n_rows,
+                                  int64_t n_slices, int64_t* widths) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t row = s * 32 + lane;
+        unsigned len = row < n_rows ? static_cast<unsigned>(row_ptr[row + 1] - row_ptr[row]) : 0u;
+        const unsigned w = __reduce_max_sync(0xffffffffu, len);
+        if (lane == 0) widths[s] = 32LL * w;
+    }
+}
+
+__global__ void csr_fill_kernel(const int64_t* __restrict__ row_ptr,
+                                const int64_t* __restrict__ col_idx,
+                                const double* __restrict__ values, int64_t n_rows,
+                                int64_t n_slices, const int64_t* __restrict__ slice_off,
+                                double* vals, int32_t* cols) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < n_slices; s += nwarps) {
+        const int64_t off = slice_off[s];
+        const int w = static_cast<int>((slice_off[s + 1] - off) >> 5);
+        const int64_t row = s * 32 + lane;
+        int k = 0;
+        if (row < n_rows) {
+            for (int64_t e = row_ptr[row]; e < row_ptr[row + 1]; ++e, ++k) {
+                vals[off + ell_val_pos(k, lane, w)] = values[e];
+                cols[off + ell_col_pos(k, lane, w)] = static_cast<int32_t>(col_idx[e]);
+            }
+        }
+        for (; k < w; ++k) {
+            vals[off + ell_val_pos(k, lane, w)] = 0.0;
+            cols[off + ell_col_pos(k, lane, w)] = -1;
+        }
+    }
+}
+
+// Per-tile column band (make_tile_plan, cg.cpp:358-367): min and max local
+// column over the rows [r0, r1), packed as atomics on 64-bit slots.
+__global__ void band_kernel(EllView A, int64_t r0, int64_t r1, unsigned long long* minmax) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t s0 = r0 >> 5, s1 = (r1 + 31) >> 5;
+    long long lo = 0x7fffffffffffffffLL, hi = -1;
+    for (int64_t s = s0 + warp_g; s < s1; s += nwarps) {
+        const int64_t off = A.slice_off[s];
+        const int w = static_cast<int>((A.slice_off[s + 1] - off) >> 5);
+        const int64_t row = s * 32 + lane;
+        if (row < r0 || row >= r1) continue;
+        for (int k = 0; k < w; ++k) {
+            const int c = A.cols[off + ell_col_pos(k, lane, w)];
+            if (c < 0) break;
+            lo = c < lo ? c : lo;
+            hi = c > hi ? c : hi;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        long long l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    if (lane == 0 && hi >= 0) {
+        atomicMin(minmax, static_cast<unsigned long long>(lo));
+        atomicMax(minmax + 1, static_cast<unsigned long long>(hi));
+    }
+}
+
+// ------------------------------------------------------------------- scan
+// Three-phase exclusive scan of int64 (slice offsets): per-block sums, one
+// block scanning the block sums, per-block rescan with the carried base.
+constexpr int kScanItems = 8; // per thread
+constexpr int kScanTile = kThreads * kScanItems;
+
+__device__ int64_t block_exclusive_scan(int64_t v, int64_t* smem, int64_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) smem[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < (kThreads >> 5) ? smem[lane] : 0;
+        int64_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < (kThreads >> 5)) smem[lane] = wi - w;
+        if (lane == (kThreads >> 5) - 1) smem[32] = wi;
+    }
+    __syncthreads();
+    int64_t excl = smem[warp] + inc - v;
+    *total = smem[32];
+    __syncthreads();
+    return excl;
+}
+
+__global__ void scan_sums_kernel(const int64_t* in, int64_t n, int64_t* sums) {
+    __shared__ int64_t smem[33];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    int64_t v = 0;
+    for (int j = 0; j < kScanItems; ++j)
+        if (base + j < n) v += in[base + j];
+    int64_t total;
+    block_exclusive_scan(v, smem, &total);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void scan_top_kernel(int64_t* sums, int64_t nb) {
+    __shared__ int64_t smem[33];
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += kThreads) {
+        const int64_t i = b0 + threadIdx.x;
+        int64_t v = i < nb ? sums[i] : 0;
+        int64_t total;
+        int64_t e = block_exclusive_scan(v, smem, &total);
+        if (i < nb) sums[i] = e + carry;
+        carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sums[nb] = carry;
+}
+
+__global__ void scan_apply_kernel(const int64_t* in, int64_t n, const int64_t* sums,
+                                  int64_t* out) {
+    __shared__ int64_t smem[33];
+    const int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+    int64_t loc[kScanItems];
+    int64_t v = 0;
+    for (int j = 0; j < kScanItems; ++j) {
+        loc[j] = base + j < n ? in[base + j] : 0;
+        v += loc[j];
+    }
+    int64_t total;
+    int64_t e = block_exclusive_scan(v, smem, &total) + sums[blockIdx.x];
+    for (int j = 0; j < kScanItems; ++j) {
+        if (base + j < n) out[base + j] = e;
+        e += loc[j];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+}
+
+} // namespace
+
+void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                           int64_t n_rows, int64_t n_slices, int64_t* widths_out, int blocks,
+                           cudaStream_t s) {
+    stencil_widths_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        nx, ny, nz, row_offset, n_rows, n_slices, widths_out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
+                         int64_t col_offset, int64_t n_rows, int64_t n_slices,
+                         const int64_t* slice_off, double* vals, int32_t* cols, int blocks,
+                         cudaStream_t s) {
+    stencil_fill_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        nx, ny, nz, row_offset, col_offset, n_rows, n_slices, slice_off, vals, cols);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_csr_widths(const int64_t* row_ptr, int64_t n_rows, int64_t n_slices,
+                       int64_t* widths_out, int blocks, cudaStream_t s) {
+    csr_widths_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        row_ptr, n_rows, n_slices, widths_out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_csr_fill(const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                     int64_t n_rows, int64_t n_slices, const int64_t* slice_off, double* vals,
+                     int32_t* cols, int blocks, cudaStream_t s) {
+    csr_fill_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
+        row_ptr, col_idx, values, n_rows, n_slices, slice_off, vals, cols);
+    TW_CUDA(cudaGetLastError());
+}
+
+int64_t scan_tmp_elems(int64_t n) { return (n + kScanTile - 1) / kScanTile + 1; }
+
+void scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* tmp,
+                        cudaStream_t s) {
+    const int64_t nb = (n + kScanTile - 1) / kScanTile;
+    if (nb == 0) {
+        TW_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+        return;
+    }
+    scan_sums_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(in, n, tmp);
+    scan_top_kernel<<<1, kThreads, 0, s>>>(tmp, nb);
+    scan_apply_kernel<<<static_cast<unsigned>(nb), kThreads, 0, s>>>(in, n, tmp, out);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* minmax, int blocks,
+                 cudaStream_t s) {
+    const int64_t ns = ((r1 + 31) >> 5) - (r0 >> 5);
+    band_kernel<<<clamp_blocks(ns * 32, blocks), kThreads, 0, s>>>(A, r0, r1, minmax);
+    TW_CUDA(cudaGetLastError());
+}
+
+} // namespace tw
