@@ -605,6 +605,7 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.chunk_part = tb.d_chunk_part;
     P.ticket = cg->d_ticket;
     P.nchunks = tb.nchunks;
+    P.ntasks = tb.ntasks;
     P.T = cg->T;
     P.A = cg->view();
     P.p_local = cg->p_local;

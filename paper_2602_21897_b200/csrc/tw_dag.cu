@@ -279,6 +279,7 @@ __device__ __forceinline__ void fill_slot(const DagParams& P, Slot* S, int lane)
             S->c = -1;
         } else {
             const int tk = P.chunk_task[c];
+            TW_DCHECK(tk >= 0 && tk < P.ntasks);
             S->c = c;
             S->task = tk;
             S->t = P.tasks[tk];

@@ -10,6 +10,22 @@
 
 #include "tw_internal.h"
 
+// Device-side checks of the checked build (make NVFLAGS_EXTRA=-DTW_CHECKS,
+// scripts/gpu_checked.sh): the bounds compute-sanitizer would watch, as traps.
+#ifdef TW_CHECKS
+#define TW_DCHECK(c)                                                                       \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("tw_hpccg check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);        \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define TW_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace tw {
 namespace dev {
 
@@ -142,6 +158,7 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         const PeerLinks* L = fin.links;
         const bool a = fin.mode == FIN_PUBLISH_A;
         const int me = L->rank, P = L->nranks;
+        TW_DCHECK(P >= 1 && P <= kMaxRanks && me >= 0 && me < P);
         for (int q = 0; q < P; ++q) (a ? L->win[q]->recv_a : L->win[q]->recv_b)[me] = v;
         __threadfence_system();
         const unsigned long long st = stamp_of(fin.sc, 0);

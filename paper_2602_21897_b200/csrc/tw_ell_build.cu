@@ -238,7 +238,32 @@ __global__ void scan_apply_kernel(const int64_t* in, int64_t n, const int64_t* s
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
 }
 
+// Checked build: one warp per slice, lane = row.
+__global__ void ell_check_kernel(EllView A) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < A.n_slices; s += nwarps) {
+        const int64_t off = A.slice_off[s], ents = A.slice_off[s + 1] - off;
+        TW_DCHECK(ents >= 0 && ents % 32 == 0 && ents / 32 <= A.max_width);
+        const int w = static_cast<int>(ents / 32);
+        bool pad = false;
+        for (int k = 0; k < w; ++k) {
+            const int c = A.cols[off + ell_col_pos(k, lane, w)];
+            TW_DCHECK(c >= -1 && c < A.x_len);
+            if (c < 0) pad = true;
+            else TW_DCHECK(!pad); // padding only ever trails a row
+        }
+        if ((s << 5) + lane >= A.n_rows) TW_DCHECK(w == 0 || pad || true);
+    }
+}
+
 } // namespace
+
+void launch_ell_check(const EllView& A, cudaStream_t s) {
+    ell_check_kernel<<<clamp_blocks(A.n_slices * 32, 1024), kThreads, 0, s>>>(A);
+    TW_CUDA(cudaGetLastError());
+}
 
 void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
                            int64_t n_rows, int64_t n_slices, int64_t* widths_out, int blocks,

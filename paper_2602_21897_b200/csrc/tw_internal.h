@@ -46,6 +46,7 @@ struct EllView {
     int64_t diag_shift;       // x index of local row i is i + diag_shift
     int max_width;            // widest slice (sizes the TMA stages)
     int tma_blocks;           // persistent grid of the TMA SpMV (0 = plain kernel)
+    int64_t x_len;            // entries of the gathered vector (owned + ghost planes)
 };
 
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
@@ -199,6 +200,9 @@ struct GroupRank {
 int rank_group_blocks_per_rank(int nranks);
 void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
                        int iterations, int jitter, cudaStream_t s);
+// Checked build only: every stored column in [-1, x_len), padding only
+// trailing a row, slice widths within max_width (traps otherwise).
+void launch_ell_check(const EllView& A, cudaStream_t s);
 // K4: dot(a, b) over [i0, i1) with finalize.
 void launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, RedScratch rs, Fin fin,
                 int blocks, cudaStream_t s);
@@ -257,6 +261,7 @@ struct DagParams {
     double* chunk_part;      // per-chunk dot partial
     unsigned* ticket;        // next chunk to hand out
     int nchunks;
+    int ntasks;              // entries of tasks (bounds of the checked build)
     int T;                   // tiles per iteration
     EllView A;
     const double* p_local;   // gathered (owned + ghost planes)

@@ -235,6 +235,7 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         const int64_t s = slice_of(k);
         const int64_t off = A.slice_off[s], end = A.slice_off[s + 1];
         const uint32_t ents = static_cast<uint32_t>(end - off);
+        TW_DCHECK(s >= 0 && s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
         stage_w[warp][st] = static_cast<int>(ents >> 5);
         unsigned char* dst = ring + static_cast<size_t>(st) * stage_bytes;
         mbar_expect_tx(&bars[warp][st], ents * 12u); // ents == 0 (all rows empty): completes at once
@@ -442,6 +443,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
 #pragma unroll 1
         for (int64_t k = tid; k < nedge; k += stride) {
             const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
+            TW_DCHECK(i >= i0 && i < i1);
             const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
             p[i] = v;
             if (lo_dst && i - i0 < plane) {

@@ -138,7 +138,7 @@ struct tw_ell {
     int32_t* cols = nullptr;
     tw::EllView view() const {
         return tw::EllView{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
-                           info.max_width, ctx->cfg.tma_blocks};
+                           info.max_width, ctx->cfg.tma_blocks, info.x_len};
     }
 };
 

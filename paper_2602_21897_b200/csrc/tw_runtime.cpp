@@ -357,6 +357,9 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
         finish_ell(A, widths, n_slices, s);
         launch_stencil_fill(nx, ny, nz, in.row_offset, in.col_offset, in.n_rows, n_slices,
                             A->slice_off, A->vals, A->cols, ctx->cfg.stream_blocks, s);
+#ifdef TW_CHECKS
+        launch_ell_check(A->view(), s);
+#endif
         TW_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaFree(widths);
@@ -407,6 +410,9 @@ static tw_ell* from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
         finish_ell(A, widths, n_slices, s);
         launch_csr_fill(d_rp, d_ci, d_v, n, n_slices, A->slice_off, A->vals, A->cols,
                         ctx->cfg.stream_blocks, s);
+#ifdef TW_CHECKS
+        launch_ell_check(A->view(), s);
+#endif
         TW_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaFree(d_rp);
