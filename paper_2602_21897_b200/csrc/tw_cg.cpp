@@ -496,26 +496,31 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
 
 // Flattens k iterations of the physical DAG into the dispatcher's task table
 // (topological order, chunk list, successor lists, predecessor counts).
-// Chunk sizes: small, because the scheduler warp hides the per-chunk
-// bookkeeping and small chunks keep the tail at each alpha / beta barrier
-// short.  TW_DAG_SPMV_SLICES / TW_DAG_VEC_ROWS override (tuning only).
+// Chunk sizes: up to 216 slices (12 per compute warp) per SpMV chunk and
+// 32768 rows per update chunk (the 256^3 optimum), but about 4 SpMV chunks
+// and 2 update chunks per CTA per pass on smaller problems (the 128^3
+// optimum; profiles/r01_dispatcher_summary.md).
+// TW_DAG_SPMV_SLICES / TW_DAG_VEC_ROWS override (tuning only).
 int64_t env_or(const char* name, int64_t dflt) {
     const char* v = std::getenv(name);
     return v && *v ? std::atoll(v) : dflt;
 }
-int64_t dag_spmv_chunk_slices() {
-    static const int64_t v = env_or("TW_DAG_SPMV_SLICES", 6 * dag_compute_warps());
-    return v;
+int64_t dag_spmv_chunk_slices(const tw_cg* cg) {
+    const int64_t w = dag_compute_warps(), ns = (cg->n + 31) / 32;
+    const int64_t fit = ns / (4 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
+    return env_or("TW_DAG_SPMV_SLICES", std::max(w, std::min(12 * w, fit)));
 }
-int64_t dag_vec_chunk_rows() {
-    static const int64_t v = env_or("TW_DAG_VEC_ROWS", 16384);
-    return v;
+int64_t dag_vec_chunk_rows(const tw_cg* cg) {
+    const int64_t fit = cg->n / (2 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
+    // multiples of 256 rows keep chunk boundaries on 2 KB (cache-line) edges
+    const int64_t rows = fit >= 24576 ? 32768 : std::max<int64_t>(2048, fit & ~int64_t(255));
+    return env_or("TW_DAG_VEC_ROWS", rows);
 }
 
 void build_dag_table(tw_cg* cg, int k) {
     const int L = static_cast<int>(cg->nodes.size());
-    const int64_t spmv_cs = dag_spmv_chunk_slices();
-    const int64_t vec_cr = dag_vec_chunk_rows();
+    const int64_t spmv_cs = dag_spmv_chunk_slices(cg);
+    const int64_t vec_cr = dag_vec_chunk_rows(cg);
     std::vector<DagTask> tasks(static_cast<size_t>(k) * L);
     std::vector<std::vector<int>> succ(tasks.size());
     std::vector<int> npred(tasks.size(), 0), chunk_task;
@@ -619,8 +624,8 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
     P.pa = cg->pa;
     P.rr = cg->rrp;
-    P.spmv_chunk_slices = dag_spmv_chunk_slices();
-    P.vec_chunk_rows = dag_vec_chunk_rows();
+    P.spmv_chunk_slices = dag_spmv_chunk_slices(cg);
+    P.vec_chunk_rows = dag_vec_chunk_rows(cg);
     dag_smem_bytes(cg->A->info.max_width, &P.stage_bytes, &P.val_bytes);
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place

@@ -128,8 +128,8 @@ void reset_solve_state(tw_cg* cg);
 void set_rhs(tw_cg* cg, const double* b, bool on_device);
 cudaEvent_t iter_event(tw_cg* cg, int i);
 int64_t env_or(const char* name, int64_t dflt);
-int64_t dag_spmv_chunk_slices();
-int64_t dag_vec_chunk_rows();
+int64_t dag_spmv_chunk_slices(const tw_cg* cg);
+int64_t dag_vec_chunk_rows(const tw_cg* cg);
 void build_dag_table(tw_cg* cg, int k);
 void enqueue_persistent(tw_cg* cg, int k);
 void iterate(tw_cg* cg, int k);

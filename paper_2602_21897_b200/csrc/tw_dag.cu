@@ -41,12 +41,17 @@ namespace {
 using namespace dev;
 
 #ifndef TW_DAG_WARPS
-#define TW_DAG_WARPS 9
+#define TW_DAG_WARPS 19
 #endif
-// Warps per dispatcher CTA.  Several CTAs share an SM so the chunk-boundary
-// bookkeeping of one (ticket, dependency acquire, completion atomics) runs
-// while the others stream.
+// Warps per dispatcher CTA: one CTA per SM with 18 compute warps (the
+// standalone K1's warp count) and the scheduler warp, which takes the
+// chunk-boundary bookkeeping (ticket, dependency acquire, completion
+// atomics) off the compute warps.  All 18 share each chunk, so neighbouring
+// slices' gathers share the SM's L1 (profiles/r01_dispatcher_summary.md).
 constexpr int kDagWarps = TW_DAG_WARPS;
+#ifndef TW_DAG_CTAS
+#define TW_DAG_CTAS 1 // resident dispatcher CTAs per SM the register budget targets
+#endif
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
@@ -296,7 +301,7 @@ __device__ __forceinline__ void fill_slot(const DagParams& P, Slot* S, int lane)
 // dependency acquire) while the compute warps run slot b, and completes slot
 // b (partials, counters, successor release) while they run slot b+1, so the
 // per-chunk bookkeeping is off the critical path and chunks can be small.
-__global__ void __launch_bounds__(kDagWarps * 32, 2) dag_kernel(DagParams P) {
+__global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(DagParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kComputeWarps];
     __shared__ int stage_w[kComputeWarps];
