@@ -757,17 +757,22 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
                      cudaStream_t s, const PeerLinks* links, const double* psrc) {
     // grid: at most one resident wave of this instantiation (a partial
     // second wave of a grid-stride loop would double the tail)
-    static int occ[2] = {0, 0};
     const bool peer = links != nullptr || bsrc.flags != nullptr;
     auto kern = peer ? update_p_kernel<true> : update_p_kernel<false>;
-    if (!occ[peer]) {
-        int o = 0, dev = 0, sms = 0;
-        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0));
-        TW_CUDA(cudaGetDevice(&dev));
-        TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        occ[peer] = (o > 0 ? o : 1) * sms;
-    }
-    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < occ[peer] ? blocks : occ[peer]);
+    // resident blocks per SM of each instantiation (thread-safe one-time init;
+    // the grid multiplies by this device's SM count)
+    auto occupancy = [](auto k) {
+        int o = 0;
+        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kThreads, 0));
+        return o > 0 ? o : 1;
+    };
+    static const int occ_plain = occupancy(update_p_kernel<false>);
+    static const int occ_peer = occupancy(update_p_kernel<true>);
+    int dev = 0, sms = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int wave = (peer ? occ_peer : occ_plain) * sms;
+    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
     kern<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, links, psrc ? psrc : p);
     TW_CUDA(cudaGetLastError());
 }
