@@ -99,6 +99,24 @@ def peaks():
         return PEAKS_FALLBACK["hbm_gbs"], "fallback"
 
 
+def read_bandwidth(torch, device) -> float:
+    """Context for roofline.frac: a read-only stream (torch's sum over a
+    4.3 GB f64 tensor, best of 5, CUDA events).  The measured copy peak
+    moves as many bytes in as out; K1 is 98 % reads, so it can exceed the
+    copy figure but not this one."""
+    x = torch.ones(1 << 29, dtype=torch.float64, device=device)
+    best = float("inf")
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        x.sum()
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del x
+    return (8 << 29) / (best / 1e3) / 1e9
+
+
 def work(nx, ny, zb, ze, nz):
     """(n, nnz) owned by the slab [zb, ze) of an nx*ny*nz grid."""
     sx = 1 if nx == 1 else 3 * nx - 2
@@ -481,6 +499,10 @@ def run_ours(args, dist, rank, world, local):
                     "k3_launches": k3_launches,
                     "k2_traffic": traffic_of("k2"), "k2_algorithmic_bytes": 48 * n,
                     "k3_traffic": traffic_of("k3"), "k3_algorithmic_bytes": 24 * n}
+        if world == 1:
+            rb = read_bandwidth(torch, torch.device("cuda", local))
+            roofline["read_stream_gbs"] = rb
+            roofline["frac_of_read_stream"] = ach / rb
     iter_gbs = total_bytes / (ms_max / 1e3 / K) / 1e9
     roofline_iter = {"bound": "hbm", "achieved": iter_gbs, "peak": peak * world, "unit": "GB/s",
                      "frac": iter_gbs / (peak * world), "algorithmic_bytes_per_iter": total_bytes}
