@@ -376,6 +376,13 @@ def run_ours(args, dist, rank, world, local):
                 S.peer_connect(blobs)
             except Exception as ex:
                 ok, note = 0.0, f"connect: {ex}"
+        if min_over_ranks(dist, ok) >= 1.0:
+            # transport check: every rank's store must become visible in
+            # every window within 2 s (a bounded wait that reports, never traps)
+            S.peer_ping_send()
+            barrier(dist)
+            if not S.peer_ping_check(2000):
+                ok, note = 0.0, "ping: a peer's store never became visible"
         if min_over_ranks(dist, ok) < 1.0:
             if args.transport == "peer":
                 raise SystemExit(f"peer transport setup failed ({note or 'on another rank'})")

@@ -305,6 +305,12 @@ int tw_cg_group_iterate_concurrent(tw_cg** cgs, int nranks, int iterations, int 
 #define TW_PEER_BLOB_BYTES 256
 int tw_cg_peer_export(tw_cg* cg, unsigned char* blob);
 int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs);
+/* Transport check after connecting: every rank calls ping_send, then (after
+ * a host barrier) ping_check, which waits at most timeout_ms for every
+ * rank's store to be visible in this rank's window and sets *ok = 1 / 0
+ * (never traps).  A caller falls back to NCCL when any rank reports 0. */
+int tw_cg_peer_ping_send(tw_cg* cg);
+int tw_cg_peer_ping_check(tw_cg* cg, int timeout_ms, int* ok);
 
 /* cg_monolithic / cg_tasks in one call (cg.cpp:397-447): host b in, host
  * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17). */

@@ -142,6 +142,8 @@ SIGNATURES = [
     ("tw_cg_group_iterate_concurrent", C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.c_int]),
     ("tw_cg_peer_export", C.c_int, [vp, C.c_char_p]),
     ("tw_cg_peer_connect", C.c_int, [vp, C.c_char_p]),
+    ("tw_cg_peer_ping_send", C.c_int, [vp]),
+    ("tw_cg_peer_ping_check", C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
     ("tw_cg_solve", C.c_int, [vp, vp, vp, C.c_int, C.POINTER(CgOptionsC), dp, dp,
                               C.POINTER(C.c_int)]),
 ]

@@ -326,6 +326,41 @@ int tw_cg_group_enable_peer(tw_cg** cgs, int nranks) {
 // blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
 // byte offset of the lower ghost plane in p_base, [136,144) of the upper,
 // [144,148) rank.
+// Transport check of a connected peer transport (collective in two steps:
+// every rank sends, then every rank checks -- so on one device, too, no
+// kernel ever waits for a kernel that has not been launched).
+int tw_cg_peer_ping_send(tw_cg* cg) {
+    return guarded([&] {
+        if (!cg || !cg->peer) contract_error("the peer transport is not connected");
+        TW_CUDA(cudaSetDevice(cg->ctx->device));
+        ++cg->ping_seq;
+        const unsigned long long token = 0x5057000000000000ull | cg->ping_seq; // 'PW' + round
+        launch_peer_ping_send(cg->links, token, cg->ctx->compute);
+        TW_CUDA(cudaStreamSynchronize(cg->ctx->compute));
+    });
+}
+
+int tw_cg_peer_ping_check(tw_cg* cg, int timeout_ms, int* ok) {
+    return guarded([&] {
+        if (!cg || !cg->peer || !ok) contract_error("the peer transport is not connected");
+        if (timeout_ms < 0) config_error("negative timeout");
+        TW_CUDA(cudaSetDevice(cg->ctx->device));
+        const unsigned long long token = 0x5057000000000000ull | cg->ping_seq;
+        int* d_ok = nullptr;
+        TW_CUDA(cudaMalloc(&d_ok, sizeof(int)));
+        launch_peer_ping_check(cg->win, cg->P, token, static_cast<long long>(timeout_ms) * 1000000LL,
+                               d_ok, cg->ctx->compute);
+        int h = 0;
+        const cudaError_t e = cudaMemcpyAsync(&h, d_ok, sizeof(int), cudaMemcpyDeviceToHost,
+                                              cg->ctx->compute);
+        const cudaError_t e2 = cudaStreamSynchronize(cg->ctx->compute);
+        cudaFree(d_ok);
+        TW_CUDA(e);
+        TW_CUDA(e2);
+        *ok = h;
+    });
+}
+
 int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
     return guarded([&] {
         if (!cg || !blob) contract_error("null solver or blob");

@@ -30,6 +30,7 @@ struct tw_cg {
     PeerWindow* win = nullptr;
     PeerLinks links{};
     PeerLinks* d_links = nullptr;
+    unsigned long long ping_seq = 0; // transport-check round (same on every rank)
     std::vector<void*> ipc_mapped;
     unsigned epoch = 0; // set_rhs count
 

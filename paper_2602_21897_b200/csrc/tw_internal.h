@@ -88,6 +88,7 @@ struct PeerWindow {
     unsigned long long flag_b[kMaxRanks];   // stamp of recv_b[q]
     unsigned long long flag_ghost_lo;       // my lower ghost plane holds rank-1's data
     unsigned long long flag_ghost_hi;       // my upper ghost plane holds rank+1's data
+    unsigned long long ping[kMaxRanks];     // transport check: token from rank q
 };
 
 // Where this rank's data goes (device pointers: own, IPC-mapped or, for the
@@ -182,6 +183,12 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
 // (a different buffer).  False when the TMA-staged path is unavailable.
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
                        double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
+// Transport check: ping_send stores `token` into ping[rank] of every rank's
+// window (release, .sys); ping_check waits (bounded, no trap) until every
+// ping[q] of this rank's window holds it and writes 1 / 0 to *ok.
+void launch_peer_ping_send(const PeerLinks& L, unsigned long long token, cudaStream_t s);
+void launch_peer_ping_check(const PeerWindow* win, int nranks, unsigned long long token,
+                            long long timeout_ns, int* ok, cudaStream_t s);
 void launch_peer_push(const double* p_owned, int64_t n, int64_t plane, const PeerLinks& L,
                       const CgScalars* sc, unsigned* ticket, cudaStream_t s);
 // One rank of the concurrent rank-group kernel (tw_cg_group_iterate_concurrent).

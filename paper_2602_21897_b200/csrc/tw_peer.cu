@@ -10,8 +10,8 @@
 //     slot [rank] and raises flag [rank] there;
 //   * K1b, K2 and K3 start with block_wait_flags: acquire-spin until the
 //     flags they consume carry this iteration's stamp.
-// This file holds the one stand-alone kernel, the initial ghost push of a
-// solve (p = b before iteration 0).
+// This file holds the stand-alone kernels: the initial ghost push of a solve
+// (p = b before iteration 0) and the transport check (ping send / check).
 // Flags hold stamps (solve epoch << 32 | iteration + 1), so they never need
 // resetting.  Peer pointers come from CUDA IPC (one process per GPU) or are
 // plain device pointers (the emulated rank group on one GPU, where the host
@@ -52,7 +52,43 @@ __global__ void peer_push_kernel(const double* p_owned, int64_t n, int64_t plane
     }
 }
 
+__global__ void peer_ping_send_kernel(PeerLinks L, unsigned long long token) {
+    for (int q = threadIdx.x; q < L.nranks; q += blockDim.x) st_release_sys(L.win[q]->ping + L.rank, token);
+}
+
+// Bounded wait that reports instead of trapping: the caller falls back to
+// another transport when a peer's store never becomes visible.
+__global__ void peer_ping_check_kernel(const PeerWindow* win, int nranks, unsigned long long token,
+                                       long long timeout_ns, int* ok) {
+    __shared__ int good;
+    if (threadIdx.x == 0) good = 1;
+    __syncthreads();
+    const unsigned long long t0 = global_ns();
+    for (int q = threadIdx.x; q < nranks; q += blockDim.x) {
+        while (ld_acquire_sys(win->ping + q) != token) {
+            if (static_cast<long long>(global_ns() - t0) > timeout_ns) {
+                atomicAnd(&good, 0);
+                break;
+            }
+            __nanosleep(256);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ok = good;
+}
+
 } // namespace
+
+void launch_peer_ping_send(const PeerLinks& L, unsigned long long token, cudaStream_t s) {
+    peer_ping_send_kernel<<<1, 64, 0, s>>>(L, token);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_peer_ping_check(const PeerWindow* win, int nranks, unsigned long long token,
+                            long long timeout_ns, int* ok, cudaStream_t s) {
+    peer_ping_check_kernel<<<1, 64, 0, s>>>(win, nranks, token, timeout_ns, ok);
+    TW_CUDA(cudaGetLastError());
+}
 
 void launch_peer_push(const double* p_owned, int64_t n, int64_t plane, const PeerLinks& L,
                       const CgScalars* sc, unsigned* ticket, cudaStream_t s) {

@@ -634,6 +634,14 @@ class CgSolver:
             raise ContractViolation("peer blobs must be PEER_BLOB_BYTES long")
         N.check(_lib().tw_cg_peer_connect(self.h, b"".join(blobs)))
 
+    def peer_ping_send(self) -> None:
+        N.check(_lib().tw_cg_peer_ping_send(self.h))
+
+    def peer_ping_check(self, timeout_ms: int = 2000) -> bool:
+        ok = C.c_int()
+        N.check(_lib().tw_cg_peer_ping_check(self.h, timeout_ms, C.byref(ok)))
+        return bool(ok.value)
+
     def enable_peer_transport(self) -> None:
         """Collective over torch.distributed: export, allgather, connect."""
         import torch.distributed as dist
@@ -687,6 +695,13 @@ class EmulatedRankGroup:
 
     def iterate(self, k: int) -> None:
         N.check(_lib().tw_cg_group_iterate(self._arr, self.P, k))
+
+    def peer_check(self, timeout_ms: int = 2000) -> bool:
+        """Transport check of the peer group: every rank pings, then every
+        rank checks (no kernel waits on one not yet launched)."""
+        for s in self.solvers:
+            s.peer_ping_send()
+        return all(s.peer_ping_check(timeout_ms) for s in self.solvers)
 
     def iterate_concurrent(self, k: int, jitter: bool = False) -> None:
         """Peer transport only: all ranks as one cooperative kernel, really

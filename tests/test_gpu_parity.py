@@ -471,7 +471,11 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     # connect (own window, no IPC mapping), fused publish / wait kernels
     for graph in (False, True):
         s = P.CgSolver(rt2, A, 150, P.CgOptions(use_graph=graph), variant=0)
+        with pytest.raises(P.ContractViolation):
+            s.peer_ping_send()  # not connected yet
         s.peer_connect([s.peer_export()])
+        s.peer_ping_send()
+        assert s.peer_ping_check(1000)
         with pytest.raises(P.ContractViolation):
             s.peer_connect([s.peer_export()])  # connected once per solver
         assert s.launches_per_iteration() == (4, 0)
@@ -584,6 +588,11 @@ def test_peer_transport_resolve_new_epoch(orc):
     dims = (24, 24, 24)
     m = orc.stencil(*dims)
     G = P.EmulatedRankGroup(*dims, 4, 30, transport="peer")
+    assert G.peer_check() and G.peer_check()  # two rounds, fresh tokens
+    # a rank that never sends: the others' check reports it (no trap, no hang)
+    for s in G.solvers[1:]:
+        s.peer_ping_send()
+    assert not G.solvers[1].peer_ping_check(50)
     for seed in (3, 11, 3):
         b = orc.rhs_xorshift(m.n, seed)
         want_h, want_x, _ = orc.cg(m, b, 30)
