@@ -159,8 +159,10 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         const bool a = fin.mode == FIN_PUBLISH_A;
         const int me = L->rank, P = L->nranks;
         TW_DCHECK(P >= 1 && P <= kMaxRanks && me >= 0 && me < P);
+        // one thread stores the values, then the flags with release
+        // semantics: each st.release.sys orders this thread's earlier value
+        // stores before the flag (no separate system fence needed)
         for (int q = 0; q < P; ++q) (a ? L->win[q]->recv_a : L->win[q]->recv_b)[me] = v;
-        __threadfence_system();
         const unsigned long long st = stamp_of(fin.sc, 0);
         for (int q = 0; q < P; ++q) st_release_sys((a ? L->win[q]->flag_a : L->win[q]->flag_b) + me, st);
         break;
