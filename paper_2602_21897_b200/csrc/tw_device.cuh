@@ -82,6 +82,14 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     return v;
 }
 
+// Wrap-around ticket with acquire-release semantics at GPU scope.
+__device__ __forceinline__ unsigned atom_inc_acq_rel(unsigned* p, unsigned wrap) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(wrap)
+                 : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

@@ -366,7 +366,7 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 
 // K3's streaming loop over [a0, b0): p = r + beta psrc, two pairs per
 // thread and step.  U: compiler unroll of that loop on top (measured: 4 for
-// the lean kernel, 1 where the peer code already holds many registers).
+// the lean kernel, 2 in the peer instantiation, where 3+ costs registers).
 template <int U>
 __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, int64_t stride,
                                          const double* __restrict__ r,
@@ -411,10 +411,29 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // same thread, so the restrict-qualified aliasing is never observable)
     const PeerLinks* links = PEER ? links_ : nullptr;
     double beta, rr = 0.0;
+    unsigned long long next = 0; // flag stamp of the next iteration (peer ghost flags)
     if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
+        // beta from the rank partials; then the iteration's commit (beta_res,
+        // cg.cpp:290-311) by the LAST block to have read the scalars: every
+        // block takes an acq_rel ticket right after its reads, so the commit
+        // needs no end-of-kernel ticket (which would wait for the p stores)
         rr = sum_parts(bsrc.parts, bsrc.count);
+        const int it = sc->iter;
         beta = __ddiv_rn(rr, sc->rtrans);
+        next = (static_cast<unsigned long long>(sc->epoch) << 32) |
+               static_cast<unsigned long long>(it + 2);
+        __syncthreads(); // the whole block has read sc
+        if (threadIdx.x == 0) {
+            const unsigned t = atom_inc_acq_rel(rs.ticket, static_cast<unsigned>(g.nblk - 1));
+            if (t == static_cast<unsigned>(g.nblk - 1)) {
+                sc->rr = rr;
+                sc->beta = beta;
+                sc->rtrans = rr;
+                if (it < sc->history_cap) history[it] = __dsqrt_rn(rr);
+                sc->iter = it + 1;
+            }
+        }
     } else {
         beta = sc ? sc->beta : __ldcg(bsrc.parts); // standalone op: beta from a device scalar
     }
@@ -424,70 +443,48 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // step (both pairs' loads issued before either store: twice the bytes in
     // flight of a one-pair loop); the at most two ragged ends go scalar.
     auto stream = [&](int64_t a0, int64_t b0) {
-        p_stream<PEER ? 1 : 4>(a0, b0, tid, stride, r, psrc, p, beta);
+        p_stream<PEER ? 2 : 4>(a0, b0, tid, stride, r, psrc, p, beta);
     };
-    // Fused halo (peer transport): the first / last owned plane of p also
-    // goes straight into the neighbours' ghost planes over NVLink.  Those two
-    // planes run as a separate scalar pass so the bulk stays the lean loop.
-    bool remote = false; // this thread stored into a neighbour's ghost plane
     if (!links) {
         stream(i0, i1);
-    } else {
-        const int64_t plane = links->plane;
-        const int64_t lo_end = i0 + plane < i1 ? i0 + plane : i1;
-        const int64_t hi_beg = i1 - plane > lo_end ? i1 - plane : lo_end;
-        stream(lo_end, hi_beg);
-        double* lo_dst = links->ghost_lo_dst;
-        double* hi_dst = links->ghost_hi_dst;
-        const int64_t nlo = lo_end - i0, nedge = nlo + (i1 - hi_beg);
-#pragma unroll 1
-        for (int64_t k = tid; k < nedge; k += stride) {
-            const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
-            TW_DCHECK(i >= i0 && i < i1);
-            const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
-            p[i] = v;
-            if (lo_dst && i - i0 < plane) {
-                lo_dst[i - i0] = v;
-                remote = true;
-            }
-            if (hi_dst && i >= i1 - plane) {
-                hi_dst[i - (i1 - plane)] = v;
-                remote = true;
-            }
-        }
+        return;
     }
-    if (bsrc.count > 0) {
-        // Every block read rtrans above; the last one through commits the
-        // iteration (beta_res task, cg.cpp:290-311) and, with the peer
-        // transport, raises the neighbours' ghost flags for the next one.
-        __shared__ bool last;
-        // only the few blocks that stored ghost planes pay the system-scope
-        // fence (their NVLink stores land before the ticket); the rest order
-        // at GPU scope and the last block's system fence + release follows
-        const bool sys = __syncthreads_or(remote);
-        if (threadIdx.x == 0) {
-            if (sys)
-                __threadfence_system();
-            else
-                __threadfence();
-            unsigned t = atomicInc(rs.ticket, static_cast<unsigned>(g.nblk - 1));
-            last = (t == static_cast<unsigned>(g.nblk - 1));
-        }
-        __syncthreads();
-        if (last && threadIdx.x == 0) {
+    // Fused halo (peer transport): the first / last owned plane of p also
+    // goes straight into the neighbours' ghost planes over NVLink.  The bulk
+    // streams through the lean loop; the two edge planes are a scalar pass
+    // of the first kEdgeBlocks blocks only, which alone fence at system
+    // scope and take a ticket -- the last of them raises the neighbours'
+    // ghost flags for the next iteration.
+    constexpr int kEdgeBlocks = 64;
+    const int64_t plane = links->plane;
+    double* lo_dst = links->ghost_lo_dst;
+    double* hi_dst = links->ghost_hi_dst;
+    // an edge plane without a neighbour streams with the bulk
+    const int64_t lo_end = lo_dst ? (i0 + plane < i1 ? i0 + plane : i1) : i0;
+    const int64_t hi_beg = hi_dst ? (i1 - plane > lo_end ? i1 - plane : lo_end) : i1;
+    stream(lo_end, hi_beg);
+    const int ne = g.nblk < kEdgeBlocks ? g.nblk : kEdgeBlocks;
+    if (g.bid >= ne) return;
+    const int64_t nlo = lo_end - i0, nedge = nlo + (i1 - hi_beg);
+    const int64_t etid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
+    const int64_t estride = static_cast<int64_t>(ne) * blockDim.x;
+#pragma unroll 1
+    for (int64_t k = etid; k < nedge; k += estride) {
+        const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
+        TW_DCHECK(i >= i0 && i < i1);
+        const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
+        p[i] = v;
+        if (lo_dst && i - i0 < plane) lo_dst[i - i0] = v;
+        if (hi_dst && i >= i1 - plane) hi_dst[i - (i1 - plane)] = v;
+    }
+    __syncthreads(); // the block's ghost stores are issued
+    if (threadIdx.x == 0) {
+        __threadfence_system(); // ... and have landed in the neighbours' memory
+        const unsigned t = atomicInc(rs.ticket + 1, static_cast<unsigned>(ne - 1));
+        if (t == static_cast<unsigned>(ne - 1)) {
             __threadfence_system();
-            const unsigned long long next =
-                (static_cast<unsigned long long>(sc->epoch) << 32) |
-                static_cast<unsigned long long>(sc->iter + 2); // stamp of iteration iter + 1
-            sc->rr = rr;
-            sc->beta = beta;
-            sc->rtrans = rr;
-            if (sc->iter < sc->history_cap) history[sc->iter] = __dsqrt_rn(rr);
-            sc->iter = sc->iter + 1;
-            if (links) {
-                if (links->ghost_lo_flag) st_release_sys(links->ghost_lo_flag, next);
-                if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
-            }
+            if (links->ghost_lo_flag) st_release_sys(links->ghost_lo_flag, next);
+            if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
         }
     }
 }

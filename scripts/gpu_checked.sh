@@ -5,8 +5,10 @@
 # on this pool; this is the in-kernel substitute.
 set -e
 cd "$(dirname "$0")/.."
-test -f paper_2602_21897_b200/_lib/variants/libtw_hpccg_checked.so || \
-  { echo "build it first: make -C paper_2602_21897_b200/csrc OUT=... NVFLAGS_EXTRA=-DTW_CHECKS"; exit 1; }
+# always rebuild the checked variant from the current sources
+OUT=$PWD/paper_2602_21897_b200/_lib/variants/checked
+make -s -C paper_2602_21897_b200/csrc -j8 OUT=$OUT NVFLAGS_EXTRA=-DTW_CHECKS >/dev/null
+cp $OUT/libtw_hpccg.so paper_2602_21897_b200/_lib/variants/libtw_hpccg_checked.so
 mkdir -p gpurun_out
 TW_HPCCG_LIB=$PWD/paper_2602_21897_b200/_lib/variants/libtw_hpccg_checked.so \
   timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -5
