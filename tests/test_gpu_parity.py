@@ -756,3 +756,18 @@ def test_streams_events_and_task_aware_binding():
     rt.release_stream(s2)
     ev.close()
     rt.close()
+
+
+def test_reference_binding_drop_in():
+    """The INTEGRATION.md binding end to end: the reference's own CsrMatrix
+    (its gen_stencil_matrix, compiled from its sources into oracle/_ref)
+    through tw_cg_solve on the B200, checked against its own cg_reference."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "oracle", "_ref", "binding_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/binding_demo not built (needs the reference tree at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "binding ok" in r.stdout
