@@ -28,7 +28,10 @@ tot = sum(agg[k][1] / agg[k][0] for k in it)
 out = [f"# ncu launch list ({tag}): bench.py --steps 6 --warmup 3 at 256^3, 1 B200, --clock-control none",
        "# kernel, launches, avg us, avg dram bytes/launch, share of the iteration's kernels"]
 for k, (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-    sh = f"share_of_iteration={t / c / tot:.3f}" if k in it else "setup (once per solve)"
+    ours = k.startswith(("spmv", "update", "stencil", "band", "rhs", "dot", "scan", "combine",
+                         "fill", "csr", "ell", "rank_group", "dag", "peer", "waxpby"))
+    sh = (f"share_of_iteration={t / c / tot:.3f}" if k in it else
+          "setup (once per solve)" if ours else "not this library (torch: bench's read-stream reference)")
     out.append(f"{k:28s} {c:4d} {t / c / 1e3:10.1f} us {b / c / 1e9:8.3f} GB  {sh}")
 open(f"profiles/{tag}_ncu_launches_summary.txt", "w").write("\n".join(out) + "\n")
 print("\n".join(out))
