@@ -130,8 +130,8 @@ struct Fin {
     double* out;
     CgScalars* sc;
     double* history;
-    const PeerLinks* links; // FIN_PUBLISH_*: device copy of the links
-    const double* pre;      // FIN_PUBLISH_A: the interior rows' partial
+    const PeerLinks* links = nullptr; // FIN_PUBLISH_*: device copy of the links
+    const double* pre = nullptr;      // FIN_PUBLISH_A: the interior rows' partial
 };
 
 // Where an update kernel takes its scalar from: sc->alpha / sc->beta when
@@ -143,7 +143,7 @@ struct Fin {
 struct ScalarSrc {
     const double* parts;
     int count;
-    const unsigned long long* flags;
+    const unsigned long long* flags = nullptr;
 };
 
 // ---------------------------------------------------------------- launchers
