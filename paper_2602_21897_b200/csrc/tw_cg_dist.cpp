@@ -323,9 +323,6 @@ int tw_cg_group_enable_peer(tw_cg** cgs, int nranks) {
     return guarded([&] { group_enable_peer(cgs, nranks); });
 }
 
-// blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
-// byte offset of the lower ghost plane in p_base, [136,144) of the upper,
-// [144,148) rank.
 // Transport check of a connected peer transport (collective in two steps:
 // every rank sends, then every rank checks -- so on one device, too, no
 // kernel ever waits for a kernel that has not been launched).
@@ -361,6 +358,10 @@ int tw_cg_peer_ping_check(tw_cg* cg, int timeout_ms, int* ok) {
     });
 }
 
+// blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
+// byte offset of the lower ghost plane in p_base, [136,144) of the upper,
+// [144,148) rank, [148,152) rank count, [152,160) plane size (checked on
+// connect: a neighbour's ghost planes must match this rank's planes).
 int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
     return guarded([&] {
         if (!cg || !blob) contract_error("null solver or blob");
@@ -376,8 +377,11 @@ int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
         const int64_t hi = (cg->p_local + cg->slab.recv_hi - cg->p_base) * static_cast<int64_t>(sizeof(double));
         std::memcpy(blob + 128, &lo, 8);
         std::memcpy(blob + 136, &hi, 8);
-        const int rank = cg->ctx->rank;
+        const int rank = cg->ctx->rank, nranks = cg->P;
         std::memcpy(blob + 144, &rank, 4);
+        std::memcpy(blob + 148, &nranks, 4);
+        const int64_t plane = cg->plane;
+        std::memcpy(blob + 152, &plane, 8); // a neighbour's ghost planes must be this size
     });
 }
 
@@ -398,11 +402,19 @@ int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
             cg->ipc_mapped.push_back(p);
             return static_cast<unsigned char*>(p);
         };
+        for (int q = 0; q < P; ++q) { // validate every blob before mapping any
+            const unsigned char* b = blobs + static_cast<size_t>(q) * TW_PEER_BLOB_BYTES;
+            int rq = -1, pq = -1;
+            int64_t plane_q = -1;
+            std::memcpy(&rq, b + 144, 4);
+            std::memcpy(&pq, b + 148, 4);
+            std::memcpy(&plane_q, b + 152, 8);
+            if (rq != q) contract_error("peer blobs must be in rank order");
+            if (pq != P) contract_error("peer blob of a different rank count");
+            if (plane_q != cg->plane) contract_error("peer blob of a different plane size (nx * ny)");
+        }
         for (int q = 0; q < P; ++q) {
             const unsigned char* b = blobs + static_cast<size_t>(q) * TW_PEER_BLOB_BYTES;
-            int rq = -1;
-            std::memcpy(&rq, b + 144, 4);
-            if (rq != q) contract_error("peer blobs must be in rank order");
             if (q == me) {
                 L.win[q] = cg->win;
                 continue;

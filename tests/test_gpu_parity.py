@@ -473,7 +473,12 @@ def test_distributed_code_path_on_one_rank(orc, golden):
         s = P.CgSolver(rt2, A, 150, P.CgOptions(use_graph=graph), variant=0)
         with pytest.raises(P.ContractViolation):
             s.peer_ping_send()  # not connected yet
-        s.peer_connect([s.peer_export()])
+        blob = s.peer_export()
+        bad = bytearray(blob)
+        bad[152] ^= 1  # a different plane size
+        with pytest.raises(P.ContractViolation):
+            s.peer_connect([bytes(bad)])
+        s.peer_connect([blob])
         s.peer_ping_send()
         assert s.peer_ping_check(1000)
         with pytest.raises(P.ContractViolation):
