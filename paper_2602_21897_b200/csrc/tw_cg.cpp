@@ -891,7 +891,8 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             k = 0; // one launch per tw_cg_iterate call, whatever its iteration count
         } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->peer) {
-            k = 4; // K1 interior, K1 boundary (+wait, publish), K2 (+wait, publish), K3 (+wait, halo)
+            // K1 (one launch, or interior + boundary), K2 (+wait, publish), K3 (+wait, halo)
+            k = peer_k1_fused(cg) ? 3 : 4;
         } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fusep) {
             k = 2; // K1 (with the previous K3 fused in) + K2; one K3 per tw_cg_iterate call
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {

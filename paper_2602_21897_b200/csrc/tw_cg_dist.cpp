@@ -74,10 +74,29 @@ void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; 
 
 // Phases of the peer transport (NVLink stores + flags, fused into the
 // kernels): 4 launches per iteration and no collective call.
+// Whether the peer K1 runs as one launch (launch_spmv_split's conditions).
+bool peer_k1_fused(const tw_cg* cg) {
+    const EllView A = cg->view();
+    if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    if (spmv_tma_smem_bytes(A.max_width) + 2048 > 227 * 1024) return false;
+    auto slices = [](int64_t r0, int64_t r1) { return r1 > r0 ? ((r1 + 31) >> 5) - (r0 >> 5) : 0; };
+    const int64_t full = static_cast<int64_t>(A.tma_blocks) * spmv_tma_warps();
+    return slices(cg->slab.interior_r0, cg->slab.interior_r1) >= full &&
+           slices(0, cg->slab.interior_r0) + slices(cg->slab.interior_r1, cg->n) >= full;
+}
+
 void peer_spmv(tw_cg* cg, cudaStream_t s) {
-    dist_spmv_interior(cg, s); // reads no ghost: overlaps the neighbours' K3 tails
     const int ng = cg->slab.ghost_lo + cg->slab.ghost_hi;
     const unsigned long long* gf = cg->slab.ghost_lo ? &cg->win->flag_ghost_lo : &cg->win->flag_ghost_hi;
+    // one launch: interior rows first (they read no ghost plane, so they
+    // overlap the neighbours' K3 tails), then the boundary rows
+    if (launch_spmv_split(cg->view(), cg->p_local, cg->Ap,
+                          RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
+                          RowRange{0, cg->slab.interior_r0}, RowRange{cg->slab.interior_r1, cg->n},
+                          cg->slot(0), Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
+                          s, ng ? gf : nullptr, ng))
+        return;
+    dist_spmv_interior(cg, s);
     launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
                 RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
                 Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},

@@ -143,6 +143,7 @@ void dist_spmv_interior(tw_cg* cg, cudaStream_t s);
 void dist_spmv_boundary(tw_cg* cg, cudaStream_t s);
 void dist_update_xr(tw_cg* cg, cudaStream_t s);
 void dist_update_p(tw_cg* cg, cudaStream_t s);
+bool peer_k1_fused(const tw_cg* cg);
 void peer_spmv(tw_cg* cg, cudaStream_t s);
 void peer_update_xr(tw_cg* cg, cudaStream_t s);
 void peer_update_p(tw_cg* cg, cudaStream_t s);

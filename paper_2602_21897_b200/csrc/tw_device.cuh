@@ -212,6 +212,39 @@ __device__ __forceinline__ void grid_reduce_finalize(double v, RedScratch rs, co
     if (threadIdx.x == 0) finalize(fin, total);
 }
 
+// Two fixed-order reductions in one pass (K1's interior and boundary p.Ap
+// partials): each is the tree grid_reduce_finalize would build on its own.
+// The last block stores the first total to *fin.pre and finalizes the
+// second with fin (FIN_PUBLISH_A reads *fin.pre back).
+__device__ __forceinline__ void grid_reduce2_finalize(double va, double vb, RedScratch rs,
+                                                      const Fin& fin, GridPos g = launch_grid()) {
+    __shared__ double smem[32];
+    __shared__ bool last;
+    const double ba = block_sum(va, smem);
+    const double bb = block_sum(vb, smem);
+    if (threadIdx.x == 0) {
+        rs.block_part[2 * g.bid] = ba;
+        rs.block_part[2 * g.bid + 1] = bb;
+        __threadfence();
+        const unsigned t = atomicInc(rs.ticket, static_cast<unsigned>(g.nblk - 1));
+        last = (t == static_cast<unsigned>(g.nblk - 1));
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double acc_a = 0.0, acc_b = 0.0;
+    for (int i = threadIdx.x; i < g.nblk; i += blockDim.x) {
+        acc_a = __dadd_rn(acc_a, __ldcg(rs.block_part + 2 * i));
+        acc_b = __dadd_rn(acc_b, __ldcg(rs.block_part + 2 * i + 1));
+    }
+    const double ta = block_sum(acc_a, smem);
+    const double tb = block_sum(acc_b, smem);
+    if (threadIdx.x == 0) {
+        *const_cast<double*>(fin.pre) = ta;
+        finalize(fin, tb);
+    }
+}
+
 __device__ __forceinline__ double sum_parts(const double* parts, int count) {
     double t = 0.0;
     for (int i = 0; i < count; ++i) t = __dadd_rn(t, __ldcg(parts + i));

@@ -181,6 +181,13 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
 // Ap = A p_new and p_new . Ap where p_new = r + beta p_old (beta = sc->beta)
 // is formed on the fly from gathers of r and p_old and stored into p_new
 // (a different buffer).  False when the TMA-staged path is unavailable.
+// K1 of the peer transport as one launch (interior, then the two boundary
+// ranges after a per-warp ghost-flag acquire), partials bit-identical to
+// the two launches; pm[0] = interior p.Ap into *fin.pre, fin (FIN_PUBLISH_A)
+// for the boundary.  False when it does not apply (then two launches).
+bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
+                       RowRange b0, RowRange b1, RedScratch rs, Fin fin, cudaStream_t s,
+                       const unsigned long long* wait_flags, int nwait);
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
                        double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
 // Transport check: ping_send stores `token` into ping[rank] of every rank's
@@ -244,6 +251,7 @@ void launch_band(const EllView& A, int64_t r0, int64_t r1, unsigned long long* m
                  int blocks, cudaStream_t s);
 
 int spmv_tma_smem_bytes(int max_width);
+int spmv_tma_warps(); // consumer warps per CTA of the TMA SpMV
 
 // ------------------------------------------------- persistent DAG dispatcher
 

@@ -300,6 +300,101 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     if (DOT) grid_reduce_finalize(part, rs, fin);
 }
 
+// K1 of the peer transport in ONE launch: the interior rows, then -- after
+// this warp's acquire of the ghost-plane flags -- the two boundary ranges.
+// Each index space is walked exactly as the separate interior / boundary
+// launches walk it (same grid, same slice-to-warp map) and the two p.Ap
+// partials reduce separately, so pm[0] / pm[1] are bit-identical to the
+// two-launch path (and to the NCCL transport).  The last block stores
+// pm[0] and publishes (0 + pm[0]) + pm[1] (FIN_PUBLISH_A).
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
+                      RowRange ri, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
+                      RedScratch rs, Fin fin, const unsigned long long* wait_flags, int nwait) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kTmaWarps];
+    __shared__ int stage_w[kTmaWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
+    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    auto first = [](RowRange q) { return q.r0 >> 5; };
+    auto count = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : int64_t(0); };
+    const int64_t ni = count(ri), nb0 = count(rb0), nb = nb0 + count(rb1);
+    const int64_t mine_i = warp_g < ni ? (ni - warp_g + nwarps - 1) / nwarps : 0;
+    const int64_t mine_b = warp_g < nb ? (nb - warp_g + nwarps - 1) / nwarps : 0;
+    // the k-th slice of this warp: interior ones first, then boundary ones
+    auto slice_of = [&](int64_t k) {
+        if (k < mine_i) return first(ri) + warp_g + k * nwarps;
+        const int64_t i = warp_g + (k - mine_i) * nwarps;
+        return i < nb0 ? first(rb0) + i : first(rb1) + (i - nb0);
+    };
+    auto range_of = [&](int64_t k) {
+        if (k < mine_i) return ri;
+        return warp_g + (k - mine_i) * nwarps < nb0 ? rb0 : rb1;
+    };
+    if (lane == 0) mbar_init(&bars[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    auto issue = [&](int64_t k) {
+        const int64_t s = slice_of(k);
+        const int64_t off = A.slice_off[s];
+        const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
+        TW_DCHECK(s >= 0 && s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
+        stage_w[warp] = static_cast<int>(ents >> 5);
+        mbar_expect_tx(&bars[warp], ents * 12u);
+        if (ents) {
+            bulk_g2s(stage, A.vals + off, ents * 8u, &bars[warp], pol);
+            bulk_g2s(stage + val_bytes, A.cols + off, ents * 4u, &bars[warp], pol);
+        }
+    };
+    const int64_t mine = mine_i + mine_b;
+    if (lane == 0 && mine > 0) issue(0);
+    __syncwarp();
+    const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
+    double part_i = 0.0, part_b = 0.0;
+    const double* vb = reinterpret_cast<const double*>(stage);
+    const int32_t* cb = reinterpret_cast<const int32_t*>(stage + val_bytes);
+    for (int64_t k = 0; k < mine; ++k) {
+        if (k == mine_i && nwait) { // first boundary slice: the ghost planes must have landed
+            if (lane == 0)
+                for (int f = 0; f < nwait; ++f)
+                    while (ld_acquire_sys(wait_flags + f) < want) __nanosleep(32);
+            __syncwarp();
+        }
+        mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
+        const int w = stage_w[warp];
+        double acc;
+        switch (w) {
+        case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
+        case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
+        case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
+        case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
+        default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
+        }
+        const int64_t row = (slice_of(k) << 5) + lane;
+        const RowRange rr = range_of(k);
+        if (row >= rr.r0 && row < rr.r1) {
+            y[row] = acc;
+            const double d = __dmul_rn(__ldg(x + row + A.diag_shift), acc);
+#ifdef TW_BREAK_SPLIT // negative control of the bit-identity test only: one partial
+            part_i = __dadd_rn(part_i, d);
+#else
+            if (k < mine_i) part_i = __dadd_rn(part_i, d);
+            else part_b = __dadd_rn(part_b, d);
+#endif
+        }
+        __syncwarp();
+        if (lane == 0 && k + 1 < mine) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + 1);
+        }
+        __syncwarp();
+    }
+    grid_reduce2_finalize(part_i, part_b, rs, fin);
+}
+
 // --------------------------------------------------------- K2 / K3 / K4 streams
 
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
@@ -660,6 +755,8 @@ static int tma_stage_bytes(int max_width, int* val_bytes) {
     return vb + cb;
 }
 
+int spmv_tma_warps() { return kTmaWarps; }
+
 int spmv_tma_smem_bytes(int max_width) {
     int vb;
     return kTmaWarps * kTmaStages * tma_stage_bytes(max_width, &vb);
@@ -733,6 +830,44 @@ void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_ra
     TW_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(rank_group_kernel),
                                         dim3(static_cast<unsigned>(nranks * B)), dim3(kThreads),
                                         args, 0, s));
+}
+
+bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
+                       RowRange b0, RowRange b1, RedScratch rs, Fin fin, cudaStream_t s,
+                       const unsigned long long* wait_flags, int nwait) {
+    if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    int vb;
+    const int stage = tma_stage_bytes(A.max_width, &vb);
+    const int smem = kTmaWarps * stage;
+    static std::mutex mu;
+    static int attr_bytes[64] = {};
+    static int static_bytes = -1;
+    int dev = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_bytes < 0) {
+            cudaFuncAttributes fa;
+            TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_split_kernel));
+            static_bytes = static_cast<int>(fa.sharedSizeBytes);
+        }
+        if (dev >= 64 || smem + static_bytes > 227 * 1024) return false;
+        if (attr_bytes[dev] < smem) {
+            TW_CUDA(cudaFuncSetAttribute(spmv_tma_split_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_bytes[dev] = smem;
+        }
+    }
+    // the grid the separate interior / boundary launches would use: both are
+    // the full persistent grid whenever each range has >= one slice per warp
+    // of it; smaller ranges would map differently, so they fall back
+    auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
+    const int64_t full = static_cast<int64_t>(A.tma_blocks) * kTmaWarps;
+    if (slices(interior) < full || slices(b0) + slices(b1) < full) return false;
+    spmv_tma_split_kernel<<<A.tma_blocks, kTmaWarps * 32, smem, s>>>(
+        A, x, y, interior, b0, b1, stage, vb, rs, fin, wait_flags, nwait);
+    TW_CUDA(cudaGetLastError());
+    return true;
 }
 
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,

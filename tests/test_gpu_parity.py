@@ -776,3 +776,29 @@ def test_reference_binding_drop_in():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "binding ok" in r.stdout
+
+
+@pytest.mark.parametrize("dims,P_", [((32, 32, 32), 4), ((40, 24, 30), 3), ((24, 20, 16), 8),
+                                     ((320, 288, 9), 3), ((320, 288, 12), 2)])
+def test_peer_transport_bit_identical_to_nccl_path(orc, dims, P_):
+    """The peer transport sums the same partials in the same order as the
+    NCCL path (whose emulation is the loopback group), so histories and x
+    are identical to the bit -- the property bench.py's pre-timing
+    validation relies on.  The 320x288 planes (>= one slice per warp in
+    every range) run the peer path's one-launch K1 (launch_spmv_split)."""
+    b = orc.rhs_xorshift(int(np.prod(dims)), 5)
+    out = []
+    for transport in ("loopback", "peer"):
+        G = P.EmulatedRankGroup(*dims, P_, 40, transport=transport)
+        if transport == "peer":  # one-launch K1 on the big planes
+            assert G.solvers[0].launches_per_iteration() == ((3 if dims[0] == 320 else 4), 0)
+        G.set_rhs(b)
+        G.iterate(40)
+        out.append((G.history(40)[0], G.solution()))
+        G.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    if dims[0] == 320:
+        want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
+        check_history(out[1][0], want_h)
+        assert np.all(rel_gap(out[1][1], want_x) <= 1e-10)
