@@ -118,11 +118,11 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
             const int32_t* cb = reinterpret_cast<const int32_t*>(stage + P.val_bytes);
             double acc;
             switch (w) {
-            case 27: acc = smem_row_fixed<27, false>(vb, cb, P.p_local, lane); break;
-            case 18: acc = smem_row_fixed<18, false>(vb, cb, P.p_local, lane); break;
-            case 12: acc = smem_row_fixed<12, false>(vb, cb, P.p_local, lane); break;
-            case 8: acc = smem_row_fixed<8, false>(vb, cb, P.p_local, lane); break;
-            default: acc = smem_row_generic<false>(vb, cb, P.p_local, lane, w); break;
+            case 27: acc = smem_row_fixed<27, kGatherCA>(vb, cb, P.p_local, lane); break;
+            case 18: acc = smem_row_fixed<18, kGatherCA>(vb, cb, P.p_local, lane); break;
+            case 12: acc = smem_row_fixed<12, kGatherCA>(vb, cb, P.p_local, lane); break;
+            case 8: acc = smem_row_fixed<8, kGatherCA>(vb, cb, P.p_local, lane); break;
+            default: acc = smem_row_generic<kGatherCA>(vb, cb, P.p_local, lane, w); break;
             }
             const int64_t row = (s << 5) + lane;
             if (row >= T.r0 && row < T.r1) {

@@ -305,16 +305,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // One row of a width-W slice block resident in shared memory: columns first,
 // then every gather issued before any use, then the reference's ordered sum.
-// Gather of x: the read-only path when x is constant for the whole kernel
-// (NC), else a plain coherent L1-cached load (the DAG dispatcher, where p is
-// rewritten inside the same kernel between dependent tasks).
-template <bool NC>
+// Gather of x (G):
+//   kGatherNC (1): the read-only path, x constant for the whole kernel;
+//   kGatherCA (0): a coherent L1-cached load (the DAG dispatcher, where p is
+//                  rewritten inside the same kernel between dependent tasks);
+//   kGatherCG (2): L2 only, bypassing L1 -- ghost planes written by another
+//                  GPU while this kernel runs: an L1 line that also holds the
+//                  edge of an owned plane may have been cached before the
+//                  ghost flag was acquired.
+constexpr int kGatherCA = 0, kGatherNC = 1, kGatherCG = 2;
+template <int G>
 __device__ __forceinline__ double gather(const double* x, int c) {
-    if (NC) return __ldg(x + c);
+    if (G == kGatherNC) return __ldg(x + c);
+    if (G == kGatherCG) return __ldcg(x + c);
     return __ldca(x + c); // ld.global.ca: L1-cached, coherent after the acquire + L1 invalidate
 }
 
-template <int W, bool NC = true>
+template <int W, int NC = kGatherNC>
 __device__ __forceinline__ double smem_row_fixed(const double* vb, const int32_t* cb,
                                                  const double* x, int lane) {
     int c[W];
@@ -348,7 +355,7 @@ __device__ __forceinline__ double smem_row_fixed(const double* vb, const int32_t
     return acc;
 }
 
-template <bool NC = true>
+template <int NC = kGatherNC>
 __device__ __forceinline__ double smem_row_generic(const double* vb, const int32_t* cb,
                                                    const double* x, int lane, int w) {
     double acc = 0.0;

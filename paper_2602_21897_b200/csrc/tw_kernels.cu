@@ -38,7 +38,7 @@ using namespace dev;
 // One row of a width-W slice: all matrix loads issued up front as 128-bit
 // evict-first loads, then the gathers, then the reference's left-to-right
 // sum (acc from 0.0, multiply then add).
-template <int W, bool NC = true>
+template <int W, int NC = kGatherNC>
 __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
                                                   const int32_t* __restrict__ cb,
                                                   const double* __restrict__ x, int lane) {
@@ -76,7 +76,7 @@ __device__ __forceinline__ double slice_row_fixed(const double* __restrict__ vb,
     return acc;
 }
 
-template <bool NC = true>
+template <int NC = kGatherNC>
 __device__ __forceinline__ double slice_row_generic(const double* __restrict__ vb,
                                                     const int32_t* __restrict__ cb,
                                                     const double* __restrict__ x, int lane,
@@ -94,7 +94,7 @@ __device__ __forceinline__ double slice_row_generic(const double* __restrict__ v
 // Register-path K1 body on the blocks of `g`.  NC: x is constant for the
 // whole kernel (read-only path); the concurrent rank-group kernel, which
 // rewrites p between its phases, gathers through the coherent L1 path.
-template <bool DOT, bool NC = true>
+template <bool DOT, int NC = kGatherNC>
 __device__ __forceinline__ void spmv_rows(GridPos g, const EllView& A, const double* __restrict__ x,
                                           double* __restrict__ y, RowRange ra, RowRange rb,
                                           RedScratch rs, const Fin& fin,
@@ -366,18 +366,28 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
         mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
         const int w = stage_w[warp];
         double acc;
-        switch (w) {
-        case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
-        case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
-        case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
-        case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
-        default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
+        if (k < mine_i) {
+            switch (w) {
+            case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
+            case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
+            case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
+            case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
+            default: acc = smem_row_generic<kGatherNC>(vb, cb, x, lane, w); break;
+            }
+        } else { // boundary rows gather ghost planes that landed during this kernel
+            switch (w) {
+            case 27: acc = smem_row_fixed<27, kGatherCG>(vb, cb, x, lane); break;
+            case 18: acc = smem_row_fixed<18, kGatherCG>(vb, cb, x, lane); break;
+            case 12: acc = smem_row_fixed<12, kGatherCG>(vb, cb, x, lane); break;
+            case 8: acc = smem_row_fixed<8, kGatherCG>(vb, cb, x, lane); break;
+            default: acc = smem_row_generic<kGatherCG>(vb, cb, x, lane, w); break;
+            }
         }
         const int64_t row = (slice_of(k) << 5) + lane;
         const RowRange rr = range_of(k);
         if (row >= rr.r0 && row < rr.r1) {
             y[row] = acc;
-            const double d = __dmul_rn(__ldg(x + row + A.diag_shift), acc);
+            const double d = __dmul_rn(__ldcg(x + row + A.diag_shift), acc);
 #ifdef TW_BREAK_SPLIT // negative control of the bit-identity test only: one partial
             part_i = __dadd_rn(part_i, d);
 #else
@@ -640,12 +650,12 @@ rank_group_kernel(const GroupRank* ranks, int B, int iterations, int jitter) {
         if (jitter && threadIdx.x == 0 && g.bid == (it * 7 + rk * 3) % B)
             __nanosleep(static_cast<unsigned>(((it + 1) * (rk + 1) * 977) % 20000));
         // K1 interior rows (no ghost plane), partial into pm[0]
-        spmv_rows<true, false>(g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, all, R.rs,
+        spmv_rows<true, kGatherCA>(g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, all, R.rs,
                                Fin{FIN_STORE, R.pm, nullptr, nullptr, nullptr, nullptr}, nullptr, 0);
         group_barrier(R.bar, B);
         // K1 boundary rows after the ghost flags; publish (0 + pm[0]) + pm[1]
-        spmv_rows<true, false>(g, R.A, R.p_local, R.Ap, RowRange{0, R.int_r0},
-                               RowRange{R.int_r1, R.n}, R.rs,
+        spmv_rows<true, kGatherCG>(g, R.A, R.p_local, R.Ap, RowRange{0, R.int_r0},
+                                   RowRange{R.int_r1, R.n}, R.rs,
                                Fin{FIN_PUBLISH_A, R.pm + 1, R.sc, nullptr, R.links, R.pm},
                                R.ghost_flags, R.n_ghost);
         group_barrier(R.bar, B);
