@@ -23,6 +23,7 @@
 #include <optional>
 #include <set>
 #include <sstream>
+#include <string>
 
 #include "tw_cg_state.h"
 
@@ -154,10 +155,31 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
     if (cg->timing) ++cg->timed;
 }
 
+// Tile kernels of one phase run side by side on the pool's streams (at most
+// min(T, capacity) at once), so with few tiles each gets that share of the
+// GPU's resident grid: a full grid per tile would make them queue behind one
+// another, paying a ramp and a tail each (128^3, 4 tiles: 0.149 -> 0.142 ms
+// per iteration with a graph).  TW_TILE_GRID=full keeps full grids (A/B).
+int tile_share(const tw_cg* cg) {
+    static const bool full = [] {
+        const char* e = std::getenv("TW_TILE_GRID");
+        return e && std::string(e) == "full";
+    }();
+    if (full) return 1;
+    const int cap = static_cast<int>(cg->ctx->pool.capacity());
+    // with many tiles each tile's grid is already bounded by its own size
+    // (and measured: sharing then costs up to 15 %, profiles/r01_sweep_summary.md)
+    if (cg->T > 2 * cap) return 1;
+    return std::max(1, std::min(cg->T, cap));
+}
+
 void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
-    const EllView A = cg->view();
+    const int share = tile_share(cg);
+    EllView A = cg->view();
+    A.tma_blocks = (A.tma_blocks + share - 1) / share;
     const int t = nd.tile;
-    const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
+    const int bs = (launch_blocks(cg, true) + share - 1) / share;
+    const int bv = (launch_blocks(cg, false) + share - 1) / share;
     switch (nd.kind) {
     case PK_HALO:
         halo_exchange(cg, st);

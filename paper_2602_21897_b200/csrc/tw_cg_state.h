@@ -116,6 +116,7 @@ int launch_blocks(const tw_cg* cg, bool spmv);
 cudaEvent_t tmark(tw_cg* cg, int k);
 void record(cudaEvent_t e, cudaStream_t s);
 void enqueue_mono(tw_cg* cg, int i = 0, int k = 1, bool fuse = false);
+int tile_share(const tw_cg* cg);
 void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st);
 void fork_streams(tw_cg* cg);
 void join_streams(tw_cg* cg);
