@@ -217,12 +217,14 @@ typedef struct tw_cg_options {
     int use_graph;                 /* capture one iteration as a CUDA graph            */
     int iteration_marks;           /* CgOptions::iteration_marks: host poller stamps cg_iter=i */
     double tol;                    /* CgOptions::tol: converged = last residual < tol  */
-    int dispatch;                  /* TW_DISPATCH_STREAMS | TW_DISPATCH_PERSISTENT (tasks) */
+    int dispatch;                  /* TW_DISPATCH_AUTO (default) | _STREAMS | _PERSISTENT */
 } tw_cg_options;
 
 #define TW_DISPATCH_STREAMS 0    /* one launch per task, cudaStreamWaitEvent edges (or graph) */
 #define TW_DISPATCH_PERSISTENT 1 /* one persistent kernel runs the whole DAG: chunked tasks,
                                     device-side dependency counters (tasks variant, 1 rank) */
+#define TW_DISPATCH_AUTO 2       /* persistent for the tasks variant with > 8 tiles on one
+                                    rank (where it is measured faster), else streams */
 
 /* Fills the defaults of CgOptions (cg.hpp:37-45) with the cuda backend. */
 void tw_cg_options_default(tw_cg_options* opt);

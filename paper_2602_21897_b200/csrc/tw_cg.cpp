@@ -342,6 +342,17 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             cg->opt = *o;
         else
             tw_cg_options_default(&cg->opt);
+        if (cg->opt.dispatch == TW_DISPATCH_AUTO) {
+            // the persistent dispatcher where it wins (many tiles, one rank,
+            // no graph requested; profiles/r01_sweep_summary.md), else streams
+            int sb, vb;
+            const bool fits = dag_smem_bytes(A->info.max_width, &sb, &vb) <= 200 * 1024;
+            cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && cg->opt.tiles > 8 &&
+                                       !ctx->nccl_comm && !ctx->emulated && fits &&
+                                       !cg->opt.use_graph
+                                   ? TW_DISPATCH_PERSISTENT
+                                   : TW_DISPATCH_STREAMS;
+        }
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             if (cg->opt.variant != TW_CG_TASKS)
                 config_error("the persistent dispatcher runs the tasks variant");
@@ -444,6 +455,7 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
                 }
         }
         cg->marks.assign(static_cast<size_t>(std::max(max_iters, 1)), 0.0);
+        cg->mark_real.assign(cg->marks.size(), 0);
         cg->ta = std::make_unique<TaskAware>(ctx->device, 20e-6);
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             TW_CUDA(cudaMalloc(&cg->d_stamps, sizeof(unsigned long long) * (max_iters + 2)));
@@ -484,6 +496,7 @@ void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s) 
 void reset_solve_state(tw_cg* cg) {
     cg->enqueued = 0;
     std::fill(cg->marks.begin(), cg->marks.end(), 0.0);
+    std::fill(cg->mark_real.begin(), cg->mark_real.end(), 0);
     cg->t0 = host_seconds();
 }
 
@@ -668,6 +681,7 @@ void iterate(tw_cg* cg, int k) {
             cudaEvent_t e = cg->ta->take_event();
             TW_CUDA(cudaEventRecord(e, s));
             cg->ta->bind(e, &cg->marks[static_cast<size_t>(cg->enqueued + k - 1)], cg->t0);
+            cg->mark_real[static_cast<size_t>(cg->enqueued + k - 1)] = 1;
         }
         cg->enqueued += k;
         return;
@@ -761,7 +775,7 @@ void tw_cg_options_default(tw_cg_options* o) {
     o->use_graph = 0;
     o->iteration_marks = 1;
     o->tol = 0.0;
-    o->dispatch = TW_DISPATCH_STREAMS;
+    o->dispatch = TW_DISPATCH_AUTO;
 }
 
 int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max_iterations,
@@ -839,6 +853,22 @@ int tw_cg_iteration_marks(tw_cg* cg, double* host_out, int count) {
         wait_cg(cg);
         while (cg->ta->pending()) std::this_thread::yield();
         std::copy(cg->marks.begin(), cg->marks.begin() + count, host_out);
+        if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT && count > 0 && cg->opt.iteration_marks) {
+            // one launch covers a whole tw_cg_iterate call, so the poller marks
+            // only each call's last iteration; earlier ones are placed before
+            // that mark by the device's per-iteration clock (d_stamps)
+            const int done = std::min(count, cg->enqueued);
+            std::vector<unsigned long long> st(static_cast<size_t>(done) + 1);
+            TW_CUDA(cudaMemcpy(st.data(), cg->d_stamps, sizeof(unsigned long long) * (done + 1),
+                               cudaMemcpyDeviceToHost));
+            int real = -1; // the nearest later iteration the poller marked
+            for (int i = done - 1; i >= 0; --i) {
+                if (cg->mark_real[static_cast<size_t>(i)]) real = i;
+                else if (real >= 0)
+                    host_out[i] = cg->marks[static_cast<size_t>(real)] -
+                                  static_cast<double>(st[real + 1] - st[i + 1]) * 1e-9;
+            }
+        }
     });
 }
 

@@ -93,6 +93,7 @@ struct tw_cg {
     unsigned long long* d_stamps = nullptr;
     double t0 = 0.0;
     std::vector<double> marks;
+    std::vector<char> mark_real; // persistent dispatch: the poller marked this iteration
     std::unique_ptr<TaskAware> ta;
 
     RedScratch slot(int i) const {

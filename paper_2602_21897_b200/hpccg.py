@@ -509,6 +509,7 @@ class CgOptions:
     tol: float = 0.0
     use_graph: bool = False
     persistent: bool = False  # tasks variant: one persistent kernel runs the whole DAG
+    auto_dispatch: bool = False  # TW_DISPATCH_AUTO: persistent for > 8 tiles on one rank
 
     def to_c(self, variant: int) -> N.CgOptionsC:
         if self.backend != CgBackend.cuda:
@@ -520,7 +521,8 @@ class CgOptions:
         o.use_graph = 1 if self.use_graph else 0
         o.iteration_marks = 1 if self.iteration_marks else 0
         o.tol = float(self.tol)
-        o.dispatch = N.TW_DISPATCH_PERSISTENT if self.persistent else N.TW_DISPATCH_STREAMS
+        o.dispatch = (N.TW_DISPATCH_PERSISTENT if self.persistent else
+                      N.TW_DISPATCH_AUTO if self.auto_dispatch else N.TW_DISPATCH_STREAMS)
         return o
 
 

@@ -30,7 +30,7 @@ def test_abi_version_and_struct_layout():
     lib.tw_cg_options_default(C.byref(o))
     # CgOptions defaults (cg.hpp:37-45): tiles 16, stream pool 4, marks on, tol 0
     assert (o.variant, o.tiles, o.stream_pool_capacity, o.iteration_marks, o.tol, o.dispatch) == \
-        (N.TW_CG_TASKS, 16, 4, 1, 0.0, N.TW_DISPATCH_STREAMS)
+        (N.TW_CG_TASKS, 16, 4, 1, 0.0, N.TW_DISPATCH_AUTO)
 
 
 def test_exports_are_plain_c():

@@ -802,3 +802,26 @@ def test_peer_transport_bit_identical_to_nccl_path(orc, dims, P_):
         want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
         check_history(out[1][0], want_h)
         assert np.all(rel_gap(out[1][1], want_x) <= 1e-10)
+
+
+def test_auto_dispatch_and_persistent_marks(rt, orc):
+    """TW_DISPATCH_AUTO (the C default): the persistent dispatcher for the
+    tasks variant with > 8 tiles, streams otherwise; the persistent path's
+    per-iteration host marks are placed by the device clock before each
+    call's polled mark (non-decreasing, each call's last one polled)."""
+    A = P.gen_stencil_matrix(48, 40, 36, rt=rt)
+    b = orc.rhs_xorshift(A.n, 3)
+    want_h, want_x, _ = orc.cg(orc.stencil(48, 40, 36), b, 30)
+    for T, want_k in ((16, 0), (4, 3 * 4 + 2)):
+        s = P.CgSolver(rt, A, 30, P.CgOptions(tiles=T, auto_dispatch=True, iteration_marks=True))
+        assert s.launches_per_iteration()[0] == want_k
+        s.set_rhs(b)
+        s.iterate(12)
+        s.iterate(18)
+        check_history(s.history(30), want_h)
+        assert np.all(rel_gap(s.solution(), want_x) <= 1e-10)
+        m = s.marks(30)  # polled marks share a poll's time stamp: non-decreasing
+        assert np.all(m > 0) and np.all(np.diff(m) >= 0)
+        t = s.iteration_times(30)
+        assert np.all(t > 0)
+        s.close()
