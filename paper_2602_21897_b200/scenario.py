@@ -16,7 +16,9 @@ proj/src/{config,scenario}.cpp for the CG workload:
 iteration end, tw_cg_iteration_times) rather than virtual cost units.  The
 per-worker usage columns describe the one device "worker": busy = summed
 iteration time, blocked / suspended / idle = 0.  ``tasks_executed`` counts
-kernel launches, ``events_polled`` the completions the task-aware poller saw.
+kernel launches (one per repetition when the tasks variant's automatic
+dispatch picks the persistent dispatcher, > 8 tiles), ``events_polled`` the
+completions the task-aware poller saw.
 """
 from __future__ import annotations
 
@@ -284,7 +286,7 @@ def run_point(c: ScenarioConfig, tile: int, rt: H.Runtime | None = None) -> Poin
     b = H.rhs_splitmix(rt, A.n, c.seed)  # SplitMix64(seed), scenario.cpp:91-95
     variant = H.N.TW_CG_MONOLITHIC if c.variant == "monolithic" else H.N.TW_CG_TASKS
     opt = H.CgOptions(tiles=tile, stream_pool_capacity=c.stream_pool, iteration_marks=True,
-                      use_graph=c.use_graph)
+                      use_graph=c.use_graph, auto_dispatch=True)
     rows, hist = [], None
     steady, allv = [], []
     for rep in range(c.repetitions):
@@ -295,6 +297,7 @@ def run_point(c: ScenarioConfig, tile: int, rt: H.Runtime | None = None) -> Poin
             times = S.iteration_times(c.iterations)
             hist = S.history(c.iterations)
             kernels, _ = S.launches_per_iteration()
+            launches = kernels * c.iterations if kernels else 1  # persistent: one launch
             polled = c.iterations
         finally:
             S.close()
@@ -302,7 +305,7 @@ def run_point(c: ScenarioConfig, tile: int, rt: H.Runtime | None = None) -> Poin
         for i, t in enumerate(times):
             warm = (c.repetitions > 1 and rep == 0) or i < c.warmup
             rows.append(MetricsRow(c.id_for(tile), rep, i, warm, float(t), [busy], [0.0],
-                                   [0.0], [0.0], kernels * c.iterations, polled))
+                                   [0.0], [0.0], launches, polled))
             allv.append(float(t))
             if not warm:
                 steady.append(float(t))

@@ -388,9 +388,10 @@ def test_load_csr_to_device_round_trip(rt, golden):
 def test_scenario_run_point_csv(rt, orc, golden):
     from paper_2602_21897_b200 import scenario as S
     c = S.ScenarioConfig(nx=32, ny=32, nz=32, iterations=20, warmup=5, repetitions=2,
-                         tiles=[1, 4], variant="tasks")
-    pts = S.run_sweep(c, rt=rt)
-    assert [p.tile for p in pts] == [1, 4]
+                         tiles=[1, 4, 16], variant="tasks")
+    pts = S.run_sweep(c, rt=rt)  # 16 tiles: the persistent dispatcher (automatic dispatch)
+    assert [p.tile for p in pts] == [1, 4, 16]
+    assert pts[2].rows[0].tasks_executed == 1 and pts[1].rows[0].tasks_executed == 14 * 20
     for p in pts:
         assert len(p.rows) == 40
         assert all(r.warmup for r in p.rows[:20])            # repetition 0 is warm-up
