@@ -826,3 +826,51 @@ def test_auto_dispatch_and_persistent_marks(rt, orc):
         t = s.iteration_times(30)
         assert np.all(t > 0)
         s.close()
+
+
+def test_abi_misuse_is_reported_not_crashed(rt):
+    """Misuse through the C ABI comes back as the reference's exception types
+    (ConfigError / ContractViolation, types.hpp:23-33) with the context still
+    usable afterwards: bad ranges, iterations beyond max_iterations, bad
+    options, null scalars, slabs without a rank context."""
+    import ctypes
+    from paper_2602_21897_b200 import _native as N
+    lib = N.load()
+    A = P.gen_stencil_matrix(8, 8, 8, rt=rt)
+    x = dev(np.ones(A.n))
+    y = torch.zeros(A.n, dtype=torch.float64, device="cuda:0")
+    with pytest.raises(P.ContractViolation):
+        P.spmv_range(A, x, y, 0, A.n + 1)
+    with pytest.raises(P.ContractViolation):
+        P.spmv_range(A, x, y, 5, 4)
+    with pytest.raises(P.ContractViolation):
+        P.dot_range(x, x, 9, 3, rt=rt)
+    with pytest.raises(P.ContractViolation):
+        N.check(lib.tw_update_p(rt.h, None, ctypes.c_void_p(x.data_ptr()),
+                                ctypes.c_void_p(y.data_ptr()), 0, 8, None))
+    with pytest.raises(P.ConfigError):
+        P.make_tile_plan(A, 0)
+    with pytest.raises(P.ConfigError):
+        P.make_tile_plan(A, A.n + 1)
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 5, P.CgOptions(tiles=0))
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 5, P.CgOptions(tiles=2), variant=7)
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 5, P.CgOptions(tiles=2, persistent=True, use_graph=True))
+    s = P.CgSolver(rt, A, 5, P.CgOptions(tiles=2))
+    s.set_rhs(np.ones(A.n))
+    with pytest.raises(P.ContractViolation):
+        s.iterate(6)  # beyond max_iterations
+    with pytest.raises(P.ContractViolation):
+        s.set_rhs(np.ones(A.n + 1))
+    s.iterate(5)
+    assert np.all(np.isfinite(s.history(5)))
+    s.close()
+    slab = None
+    with pytest.raises(P.ContractViolation):  # a partial slab needs a rank context
+        slab = P.gen_stencil_matrix(8, 8, 8, rt=rt, z_begin=0, z_end=4)
+        P.CgSolver(rt, slab, 5, P.CgOptions(), variant=N.TW_CG_MONOLITHIC)
+    # the context is still fine
+    P.spmv_range(A, x, y, 0, A.n)
+    torch.cuda.synchronize()
