@@ -411,25 +411,24 @@ def run_ours(args, dist, rank, world, local):
     kern_timing = variant == 0
     stream = torch.cuda.ExternalStream(rt.compute_stream, device=torch.device("cuda", local))
     if use_graph:
-        # untimed: capture (and cache) the graphs the timed region replays --
-        # the one-iteration graph of the warm-up and the K-iteration graph
-        # that carries the per-kernel timing events
+        # untimed: capture (and cache) the graphs the timed passes replay --
+        # the one-iteration graph of the headline pass and the KR-iteration
+        # graph that carries the per-kernel timing events
         S.set_rhs(b)
         S.iterate(1)
-        for kr in sorted(set(reps)):
-            S.set_rhs(b)
-            if kern_timing:
-                S.enable_kernel_timing(True)
-            S.iterate(kr)
-            S.wait()
-            if kern_timing:
-                S.enable_kernel_timing(False)
+        S.set_rhs(b)
+        if kern_timing:
+            S.enable_kernel_timing(True)
+        S.iterate(KR)
+        S.wait()
+        if kern_timing:
+            S.enable_kernel_timing(False)
 
-    def timed_rep(kr):
+    def timed_rep(kr, timing):
         S.set_rhs(b)
         S.iterate(W)
         S.wait()
-        if kern_timing:
+        if timing:
             S.enable_kernel_timing(True)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -440,8 +439,8 @@ def run_ours(args, dist, rank, world, local):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier(dist)
-        kt = S.kernel_times() if kern_timing else None
-        if kern_timing:
+        kt = S.kernel_times() if timing else None
+        if timing:
             S.enable_kernel_timing(False)
         hist = S.history(W + kr)
         # finite and decaying (CG minimises the A-norm of the error, so the
@@ -450,19 +449,24 @@ def run_ours(args, dist, rank, world, local):
         return e0.elapsed_time(e1), kt, hist
 
     def timed_run():
-        ms, kts, hist = 0.0, [0.0, 0.0, 0.0, 0], None
+        # the headline: K iterations with no instrumentation inside (per-kernel
+        # events in the graph cost ~1 % of the step, so they get their own pass)
+        ms, hist = 0.0, None
         with ClockSampler(local) as clk:
             for kr in reps:
-                m, kt, hist = timed_rep(kr)
+                m, _, hist = timed_rep(kr, False)
                 ms += m
-                if kt is not None:
-                    kts = [kts[0] + kt[0], kts[1] + kt[1], kts[2] + kt[2], kts[3] + kt[3]]
-        return ms, clk.summary(), (tuple(kts) if kern_timing else None), hist
+        return ms, clk.summary(), hist
 
-    ms, clocks, kt, hist = timed_run()
+    ms, clocks, hist = timed_run()
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
     if set(clocks["reasons"]) & bad:
-        ms, clocks, kt, hist = timed_run()  # rejected: re-measure once
+        ms, clocks, hist = timed_run()  # rejected: re-measure once
+    # the kernel-timing pass: KR iterations with K1 / K2 / K3 events recorded
+    # around every kernel on its launch stream (roofline.achieved)
+    kt_pass_ms, kt = None, None
+    if kern_timing:
+        kt_pass_ms, kt, _ = timed_rep(KR, True)
     ms_max = max_over_ranks(dist, ms)
     kernels_it, colls_it = S.launches_per_iteration()
     # single-domain monolithic: K3 is fused into the next iteration's K1
@@ -473,7 +477,7 @@ def run_ours(args, dist, rank, world, local):
     nrep = len(reps)
     if fused:
         bytes_it = 12 * nnz + 80 * n + 8 * n * nrep / K
-        k1_bytes = (K * (12 * nnz + 32 * n) - 16 * n * nrep) / K  # average over the K launches
+        k1_bytes = (KR * (12 * nnz + 32 * n) - 16 * n) / KR  # average over the timing pass's launches
     total_flops = sum_over_ranks(dist, float(flops_it))
     total_bytes = sum_over_ranks(dist, float(bytes_it))
     gflops = total_flops * K / (ms_max / 1e3) / 1e9
@@ -485,7 +489,7 @@ def run_ours(args, dist, rank, world, local):
         k1_ms, k2_ms, k3_ms, nt = kt
         k1_avg = k1_ms / nt
         ach = k1_bytes / (k1_avg / 1e3) / 1e9
-        k3_launches = nrep if fused else nt
+        k3_launches = 1 if fused else nt
         wl = f"{nx}x{ny}x{args.nz}"
 
         def traffic_of(k):
@@ -500,7 +504,10 @@ def run_ours(args, dist, rank, world, local):
                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": traffic, "algorithmic_bytes": k1_bytes,
                     "avg_launch_ms": k1_avg, "peak_source": f"{peak_kind} hbm_gbs",
-                    "share_of_step": k1_ms / ms,
+                    "share_of_step": k1_ms / kt_pass_ms,
+                    "kernel_timing": (f"separate timed pass of {nt} iterations with events around "
+                                      f"each kernel: {kt_pass_ms / nt:.4f} ms/iteration there, "
+                                      f"{ms_max / K:.4f} in the event-free headline"),
                     "k2_update_xr_gbs": 48 * n / (k2_ms / nt / 1e3) / 1e9,
                     "k3_update_p_gbs": 24 * n / (k3_ms / k3_launches / 1e3) / 1e9,
                     "k3_launches": k3_launches,

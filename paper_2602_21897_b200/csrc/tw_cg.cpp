@@ -30,6 +30,16 @@
 namespace tw {
 namespace cgi {
 
+// Programmatic dependent launch for the single-domain monolithic chain
+// (TW_PDL=0 turns it off, for A/B).
+bool use_pdl() {
+    static const bool on = [] {
+        const char* e = std::getenv("TW_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
 void build_schedule(tw_cg* cg) {
     build_logical(cg->dag, 0, cg->ltasks, &cg->nodes);
@@ -102,6 +112,10 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
     if (!cg->dist) {
+        // K1 -> K2 -> K3 -> K1 ... as a programmatic-dependent-launch chain:
+        // each kernel queues its successor early and the successor waits in
+        // griddepcontrol.wait, so the launch gaps overlap the tails
+        const bool pdl = use_pdl();
         const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
         if (fuse && i > 0) {
@@ -110,15 +124,16 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
                 throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
             cg->p_cur = next;
         } else {
-            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s);
+            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s,
+                        nullptr, 0, pdl);
         }
         record(tmark(cg, 1), s);
         launch_update_xr(0, cg->n, cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
-                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s);
+                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s, pdl);
         record(tmark(cg, 2), s);
         if (!fuse || i == k - 1) {
             launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p_cur);
+                            cg->history, bv, s, nullptr, cg->p_cur, pdl);
             cg->p_cur = cg->p_owned;
         }
         record(tmark(cg, 3), s);

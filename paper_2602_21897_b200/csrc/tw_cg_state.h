@@ -112,6 +112,7 @@ namespace tw {
 namespace cgi {
 
 // tw_cg.cpp
+bool use_pdl();
 void build_schedule(tw_cg* cg);
 int launch_blocks(const tw_cg* cg, bool spmv);
 cudaEvent_t tmark(tw_cg* cg, int k);

@@ -68,6 +68,13 @@ __device__ __forceinline__ double block_sum(double v, double* smem) {
     return t;
 }
 
+// ------------------------------------ programmatic dependent launch (sm_90+)
+// No-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------ peer transport primitives
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {

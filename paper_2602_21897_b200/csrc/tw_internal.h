@@ -162,13 +162,14 @@ struct RowRange {
 // K1: y = A x over up to two local row ranges; optional fused dot(x_diag, y).
 // With `wait_flags` (peer transport: the ghost-plane flags) every block
 // first acquire-waits for this iteration's stamp (fin.sc) before gathering.
+// pdl: programmatic dependent launch (the single-domain monolithic chain).
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
-                 const unsigned long long* wait_flags = nullptr, int nwait = 0);
+                 const unsigned long long* wait_flags = nullptr, int nwait = 0, bool pdl = false);
 // K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
-                      Fin fin, int blocks, cudaStream_t s);
+                      Fin fin, int blocks, cudaStream_t s, bool pdl = false);
 // K3: p = r + beta p (beta from sc or recomputed from partials; with
 // partials, the last block also commits rtrans/history/iter).
 // With `links` (device copy), K3 also stores the first / last owned plane
@@ -176,7 +177,7 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
-                     const double* psrc = nullptr);
+                     const double* psrc = nullptr, bool pdl = false);
 // K1 with the previous iteration's K3 fused in (single-domain monolithic):
 // Ap = A p_new and p_new . Ap where p_new = r + beta p_old (beta = sc->beta)
 // is formed on the fly from gathers of r and p_old and stored into p_new

@@ -22,6 +22,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
 
 #include "tw_device.cuh"
 #include "tw_internal.h"
@@ -226,6 +227,7 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         const int64_t i = warp_g + k * nwarps;
         return i < na ? sa0 + i : sb0 + (i - na);
     };
+    pdl_launch_dependents(); // programmatic launch: the next kernel may queue up now
     if (lane == 0)
         for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[warp][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -247,6 +249,9 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     if (lane == 0)
         for (int st = 0; st < kTmaStages && st < mine; ++st) issue(st, st);
     __syncwarp();
+    // The matrix does not depend on the previous kernel, so its first slice
+    // streams in before the wait for that kernel's p (and scalars).
+    pdl_wait();
     // peer transport: the matrix is already streaming in; the gathers of p
     // wait until the neighbours' ghost planes have landed
     if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
@@ -425,6 +430,8 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
                                                double* __restrict__ r, const double* __restrict__ Ap,
                                                CgScalars* sc, ScalarSrc asrc, RedScratch rs,
                                                const Fin& fin) {
+    pdl_launch_dependents();
+    pdl_wait(); // Ap and alpha come from K1
     double alpha;
     if (asrc.flags) block_wait_flags(asrc.flags, asrc.count, stamp_of(sc, 0));
     if (asrc.count > 0)
@@ -515,6 +522,8 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // psrc: p_old, == p in place (each element is read, then written, by the
     // same thread, so the restrict-qualified aliasing is never observable)
     const PeerLinks* links = PEER ? links_ : nullptr;
+    pdl_launch_dependents();
+    pdl_wait(); // r and beta come from K2
     double beta, rr = 0.0;
     unsigned long long next = 0; // flag stamp of the next iteration (peer ghost flags)
     if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
@@ -767,6 +776,25 @@ static int tma_stage_bytes(int max_width, int* val_bytes) {
 
 int spmv_tma_warps() { return kTmaWarps; }
 
+// Launch with programmatic dependent launch allowed (pdl): the kernel may
+// start while its stream predecessor drains; its griddepcontrol.wait holds
+// the dependent reads until that predecessor has completed and flushed.
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, bool pdl, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    TW_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 int spmv_tma_smem_bytes(int max_width) {
     int vb;
     return kTmaWarps * kTmaStages * tma_stage_bytes(max_width, &vb);
@@ -778,7 +806,7 @@ int spmv_tma_smem_bytes(int max_width) {
 template <bool DOT, bool FUSEP>
 static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                             RedScratch rs, Fin fin, cudaStream_t s, const unsigned long long* wait_flags,
-                            int nwait, const double* r, double* pnew) {
+                            int nwait, const double* r, double* pnew, bool pdl = false) {
     if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int64_t ns = slices(a) + slices(b);
@@ -805,16 +833,19 @@ static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRan
     }
     const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
     const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-    kern<<<g, kTmaWarps * 32, smem, s>>>(A, x, y, a, b, stage, vb, rs, fin, wait_flags, nwait, r, pnew);
+    launch_k(kern, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, a, b, stage, vb, rs, fin,
+             wait_flags, nwait, r, pnew);
     TW_CUDA(cudaGetLastError());
     return true;
 }
 
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
-                 const unsigned long long* wait_flags, int nwait) {
-    if (with_dot ? launch_spmv_tma<true, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr, nullptr)
-                 : launch_spmv_tma<false, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr, nullptr))
+                 const unsigned long long* wait_flags, int nwait, bool pdl) {
+    if (with_dot ? launch_spmv_tma<true, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr,
+                                                nullptr, pdl)
+                 : launch_spmv_tma<false, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr,
+                                                 nullptr, pdl))
         return;
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int g = clamp_blocks((slices(a) + slices(b)) * 32, blocks);
@@ -888,15 +919,16 @@ bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, d
 
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc asrc, RedScratch rs, Fin fin,
-                      int blocks, cudaStream_t s) {
+                      int blocks, cudaStream_t s, bool pdl) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    update_xr_kernel<<<g, kThreads, 0, s>>>(i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
+    launch_k(update_xr_kernel, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap, sc, asrc, rs,
+             fin);
     TW_CUDA(cudaGetLastError());
 }
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, const PeerLinks* links, const double* psrc) {
+                     cudaStream_t s, const PeerLinks* links, const double* psrc, bool pdl) {
     // grid: at most one resident wave of this instantiation (a partial
     // second wave of a grid-stride loop would double the tail)
     const bool peer = links != nullptr || bsrc.flags != nullptr;
@@ -915,7 +947,8 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
     TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int wave = (peer ? occ_peer : occ_plain) * sms;
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
-    kern<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, bsrc, rs, history, links, psrc ? psrc : p);
+    launch_k(kern, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history, links,
+             psrc ? psrc : p);
     TW_CUDA(cudaGetLastError());
 }
 
