@@ -94,7 +94,7 @@ void peer_spmv(tw_cg* cg, cudaStream_t s) {
                           RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
                           RowRange{0, cg->slab.interior_r0}, RowRange{cg->slab.interior_r1, cg->n},
                           cg->slot(0), Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
-                          s, ng ? gf : nullptr, ng))
+                          s, ng ? gf : nullptr, ng, use_pdl()))
         return;
     dist_spmv_interior(cg, s);
     launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
@@ -107,13 +107,13 @@ void peer_update_xr(tw_cg* cg, cudaStream_t s) {
     launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                      ScalarSrc{cg->win->recv_a, cg->P, cg->win->flag_a}, cg->slot(0),
                      Fin{FIN_PUBLISH_B, cg->send_b, cg->sc, nullptr, cg->d_links, nullptr},
-                     launch_blocks(cg, false), s);
+                     launch_blocks(cg, false), s, use_pdl());
 }
 
 void peer_update_p(tw_cg* cg, cudaStream_t s) {
     launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
                     ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
-                    launch_blocks(cg, false), s, cg->d_links);
+                    launch_blocks(cg, false), s, cg->d_links, nullptr, use_pdl());
 }
 
 void alloc_window(tw_cg* cg) {

@@ -188,7 +188,7 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
 // for the boundary.  False when it does not apply (then two launches).
 bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
                        RowRange b0, RowRange b1, RedScratch rs, Fin fin, cudaStream_t s,
-                       const unsigned long long* wait_flags, int nwait);
+                       const unsigned long long* wait_flags, int nwait, bool pdl = false);
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
                        double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
 // Transport check: ping_send stores `token` into ping[rank] of every rank's

@@ -338,6 +338,7 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
         if (k < mine_i) return ri;
         return warp_g + (k - mine_i) * nwarps < nb0 ? rb0 : rb1;
     };
+    pdl_launch_dependents();
     if (lane == 0) mbar_init(&bars[warp], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
@@ -357,6 +358,7 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
     const int64_t mine = mine_i + mine_b;
     if (lane == 0 && mine > 0) issue(0);
     __syncwarp();
+    pdl_wait(); // p and the scalars come from the previous kernel
     const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
     double part_i = 0.0, part_b = 0.0;
     const double* vb = reinterpret_cast<const double*>(stage);
@@ -875,7 +877,7 @@ void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_ra
 
 bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
                        RowRange b0, RowRange b1, RedScratch rs, Fin fin, cudaStream_t s,
-                       const unsigned long long* wait_flags, int nwait) {
+                       const unsigned long long* wait_flags, int nwait, bool pdl) {
     if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
     int vb;
     const int stage = tma_stage_bytes(A.max_width, &vb);
@@ -905,8 +907,8 @@ bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange in
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int64_t full = static_cast<int64_t>(A.tma_blocks) * kTmaWarps;
     if (slices(interior) < full || slices(b0) + slices(b1) < full) return false;
-    spmv_tma_split_kernel<<<A.tma_blocks, kTmaWarps * 32, smem, s>>>(
-        A, x, y, interior, b0, b1, stage, vb, rs, fin, wait_flags, nwait);
+    launch_k(spmv_tma_split_kernel, dim3(A.tma_blocks), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y,
+             interior, b0, b1, stage, vb, rs, fin, wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
     return true;
 }
