@@ -127,6 +127,7 @@ SIGNATURES = [
     ("tw_cg_group_set_rhs", C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.c_int]),
     ("tw_cg_group_iterate", C.c_int, [C.POINTER(vp), C.c_int, C.c_int]),
     ("tw_halo_exchange", C.c_int, [vp, vp, vp]),
+    ("tw_ell_x_staged", C.c_int, [vp, C.POINTER(C.c_int)]),
     ("tw_update_xr_rr", C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, vp, vp]),
     ("tw_update_p", C.c_int, [vp, vp, vp, vp, i64, i64, vp]),
     ("tw_stream_acquire", C.c_int, [vp, C.POINTER(vp)]),

@@ -123,7 +123,7 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
             if (!launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n, rs, fa, s))
                 throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
             cg->p_cur = next;
-        } else {
+        } else if (!launch_spmv_staged(A, cg->p_local, cg->Ap, cg->n, rs, fa, s, pdl)) {
             launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s,
                         nullptr, 0, pdl);
         }
@@ -416,10 +416,14 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaMalloc(&cg->x, sizeof(double) * (n + 2)));
         TW_CUDA(cudaMalloc(&cg->r, sizeof(double) * (n + 2)));
         TW_CUDA(cudaMalloc(&cg->Ap, sizeof(double) * (n + 2)));
-        // p_owned 16-byte aligned for the paired loads of K2/K3
-        const int64_t pad = cg->diag_shift & 1;
-        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + pad) + 2)));
-        cg->p_local = cg->p_base + pad;
+        // p_owned on a 128-byte line (the streaming kernels' 128-bit accesses
+        // then never straddle lines) with at least 2 doubles of slack before
+        // p_local and after its end: the x-staged K1 copies 36-double runs
+        // that start 2 before a line
+        int64_t front = (16 - cg->diag_shift % 16) % 16;
+        if (front < 2) front += 16;
+        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 8)));
+        cg->p_local = cg->p_base + front;
         cg->p_owned = cg->p_local + cg->diag_shift;
         cg->p_cur = cg->p_owned;
         {

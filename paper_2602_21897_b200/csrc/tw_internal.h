@@ -47,7 +47,47 @@ struct EllView {
     int max_width;            // widest slice (sizes the TMA stages)
     int tma_blocks;           // persistent grid of the TMA SpMV (0 = plain kernel)
     int64_t x_len;            // entries of the gathered vector (owned + ghost planes)
+    // x-staged form (single-domain stencil, nx % 32 == 0; null otherwise):
+    // every stored column as a 16-bit index into the slice's staged window of
+    // x -- 9 runs of 36 doubles, one per (dz, dy) neighbour line -- in the
+    // chunked layout of ell_c16_pos; sx_* is the grid the runs come from
+    const uint16_t* cols16 = nullptr;
+    int64_t sx_nx = 0, sx_ny = 0, sx_nz = 0;
 };
+
+// x-staged windows: run r = (dz + 1) * 3 + (dy + 1) of a slice starts 2
+// doubles before the slice's x0 on line (z + dz, y + dy) and holds 36.
+constexpr int kStageRuns = 9, kStageRunLen = 36;
+constexpr uint16_t kStagePad = 0xFFFF;
+
+// Position of entry k of lane l in a slice block of 16-bit columns: blocks of
+// 8 per lane (one 128-bit load), then 4, then 2, then 1.
+__host__ __device__ inline int64_t ell_c16_pos(int k, int lane, int w) {
+    const int f8 = w & ~7;
+    if (k < f8) return 32LL * (k & ~7) + 8 * lane + (k & 7);
+    int base = f8, rem = w - f8;
+    if (rem >= 4) {
+        if (k < base + 4) return 32LL * base + 4 * lane + (k - base);
+        base += 4;
+        rem -= 4;
+    }
+    if (rem >= 2) {
+        if (k < base + 2) return 32LL * base + 2 * lane + (k - base);
+        base += 2;
+    }
+    return 32LL * base + lane;
+}
+
+// Start (in x indices) of staged run r of slice s of an x-staged matrix; a
+// neighbour line outside the grid stages the slice's own line instead (no
+// stored column refers to it).
+__host__ __device__ inline int64_t stage_run_start(int64_t s, int r, int64_t nx, int64_t ny,
+                                                   int64_t nz) {
+    const int64_t row0 = s * 32, x0 = row0 % nx, t = row0 / nx, y = t % ny, z = t / ny;
+    const int64_t zz = z + r / 3 - 1, yy = y + r % 3 - 1;
+    const bool in = zz >= 0 && zz < nz && yy >= 0 && yy < ny;
+    return (in ? zz * ny + yy : z * ny + y) * nx + x0 - 2;
+}
 
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
     const int full = w & ~1;
@@ -215,6 +255,17 @@ struct GroupRank {
 int rank_group_blocks_per_rank(int nranks);
 void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
                        int iterations, int jitter, cudaStream_t s);
+// Builds the 16-bit staged columns of a single-domain stencil matrix
+// (nx % 32 == 0) from its 32-bit columns; returns false if any stored column
+// falls outside its slice's staged runs (then the matrix stays unstaged).
+void launch_stencil_cols16(const EllView& A, int64_t nx, int64_t ny, int64_t nz, uint16_t* cols16,
+                           unsigned* bad, cudaStream_t s);
+// K1 on an x-staged matrix (single-domain monolithic CG): the slice block
+// and its 9 x runs arrive in one TMA transaction per slice; x must have 2
+// readable doubles of slack before index 0 and after x_len.
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, int64_t n, RedScratch rs,
+                        Fin fin, cudaStream_t s, bool pdl);
+int spmv_staged_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only
 // trailing a row, slice widths within max_width (traps otherwise).
 void launch_ell_check(const EllView& A, cudaStream_t s);

@@ -412,6 +412,146 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
     grid_reduce2_finalize(part_i, part_b, rs, fin);
 }
 
+// ------------------------------------------------------ K1, x staged in smem
+// One row of an x-staged slice: 16-bit columns index the slice's 9 staged
+// runs of x in shared memory, so the 27 operands are shared-memory reads of
+// data that arrived with the slice's own TMA transaction (no global gathers
+// waiting on L1 / L2).  Same per-row order and roundings as smem_row_fixed.
+template <int W>
+__device__ __forceinline__ double staged_row_fixed(const double* vb, const uint16_t* cb,
+                                                   const double* xs, int lane) {
+    uint32_t c[W];
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 t = reinterpret_cast<const uint4*>(cb + 256 * q)[lane];
+        const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            c[8 * q + 2 * h] = w4[h] & 0xFFFFu;
+            c[8 * q + 2 * h + 1] = w4[h] >> 16;
+        }
+    }
+    constexpr int F8 = W & ~7;
+    constexpr int R = W - F8;
+    constexpr int F4 = R >= 4 ? F8 + 4 : F8;
+    if (R >= 4) {
+        const uint2 t = reinterpret_cast<const uint2*>(cb + 32 * F8)[lane];
+        c[F8] = t.x & 0xFFFFu;
+        c[F8 + 1] = t.x >> 16;
+        c[F8 + 2] = t.y & 0xFFFFu;
+        c[F8 + 3] = t.y >> 16;
+    }
+    constexpr int R2 = W - F4;
+    if (R2 >= 2) {
+        const uint32_t t = reinterpret_cast<const uint32_t*>(cb + 32 * F4)[lane];
+        c[F4] = t & 0xFFFFu;
+        c[F4 + 1] = t >> 16;
+    }
+    if (R2 & 1) c[W - 1] = cb[32 * (W - 1) + lane];
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < W / 2; ++j) {
+        const double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
+        if (c[2 * j] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(v.x, xs[c[2 * j]]));
+        if (c[2 * j + 1] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(v.y, xs[c[2 * j + 1]]));
+    }
+    if (W & 1)
+        if (c[W - 1] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane], xs[c[W - 1]]));
+    return acc;
+}
+
+__device__ __forceinline__ double staged_row_generic(const double* vb, const uint16_t* cb,
+                                                     const double* xs, int lane, int w) {
+    double acc = 0.0;
+    for (int k = 0; k < w; ++k) {
+        const uint32_t c = cb[ell_c16_pos(k, lane, w)];
+        if (c == kStagePad) break; // padding only ever trails a row
+        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], xs[c]));
+    }
+    return acc;
+}
+
+// K1 for a single-domain x-staged matrix: per warp one stage holding the
+// slice's values, 16-bit columns and 9 x runs, one mbarrier transaction.
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
+                       int64_t n_slices, int stage_bytes, int val_bytes, int c16_bytes,
+                       RedScratch rs, Fin fin) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kTmaWarps];
+    __shared__ int stage_w[kTmaWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
+    const double* vb = reinterpret_cast<const double*>(stage);
+    const uint16_t* cb = reinterpret_cast<const uint16_t*>(stage + val_bytes);
+    double* xs = reinterpret_cast<double*>(stage + val_bytes + c16_bytes);
+    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    const int64_t mine = warp_g < n_slices ? (n_slices - warp_g + nwarps - 1) / nwarps : 0;
+    pdl_launch_dependents();
+    if (lane == 0) mbar_init(&bars[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    constexpr uint32_t kRunBytes = kStageRunLen * 8;
+    // lane 0: the slice block (values + 16-bit columns) and then its 9 x runs,
+    // all on one mbarrier transaction
+    auto issue_block = [&](int64_t k) {
+        const int64_t s = warp_g + k * nwarps;
+        const int64_t off = A.slice_off[s];
+        const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
+        TW_DCHECK(s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
+        stage_w[warp] = static_cast<int>(ents >> 5);
+        mbar_expect_tx(&bars[warp], ents * 10u + kStageRuns * kRunBytes);
+        if (ents) {
+            bulk_g2s(stage, A.vals + off, ents * 8u, &bars[warp], pol);
+            bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, &bars[warp], pol);
+        }
+    };
+    auto issue_x = [&](int64_t k) { // default L2 policy: neighbouring slices share runs
+        const int64_t s = warp_g + k * nwarps;
+        for (int r = 0; r < kStageRuns; ++r) {
+            const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
+                "l"(x + st), "r"(kRunBytes), "r"(smem_u32(&bars[warp]))
+                : "memory");
+        }
+    };
+    // the matrix does not depend on the previous kernel: the first block
+    // streams in before the wait for it; x (that kernel's p) only after
+    if (lane == 0 && mine > 0) issue_block(0);
+    __syncwarp();
+    pdl_wait();
+    if (lane == 0 && mine > 0) issue_x(0);
+    __syncwarp();
+    double part = 0.0;
+    for (int64_t k = 0; k < mine; ++k) {
+        mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
+        const int w = stage_w[warp];
+        double acc;
+        switch (w) {
+        case 27: acc = staged_row_fixed<27>(vb, cb, xs, lane); break;
+        case 18: acc = staged_row_fixed<18>(vb, cb, xs, lane); break;
+        case 12: acc = staged_row_fixed<12>(vb, cb, xs, lane); break;
+        case 8: acc = staged_row_fixed<8>(vb, cb, xs, lane); break;
+        default: acc = staged_row_generic(vb, cb, xs, lane, w); break;
+        }
+        const int64_t row = ((warp_g + k * nwarps) << 5) + lane;
+        y[row] = acc;
+        part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc)); // p[row]
+        __syncwarp();
+        if (lane == 0 && k + 1 < mine) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_block(k + 1);
+            issue_x(k + 1);
+        }
+        __syncwarp();
+    }
+    grid_reduce_finalize(part, rs, fin);
+}
+
 // --------------------------------------------------------- K2 / K3 / K4 streams
 
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
@@ -911,6 +1051,50 @@ bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange in
              interior, b0, b1, stage, vb, rs, fin, wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
     return true;
+}
+
+static int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
+    *val_bytes = ((32 * max_width * 8) + 127) / 128 * 128;
+    *c16_bytes = ((32 * max_width * 2) + 127) / 128 * 128;
+    return *val_bytes + *c16_bytes + (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
+}
+
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, int64_t n, RedScratch rs,
+                        Fin fin, cudaStream_t s, bool pdl) {
+    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    int vb, cb;
+    const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
+    const int smem = kTmaWarps * stage;
+    static std::mutex mu;
+    static int attr_bytes[64] = {};
+    static int static_bytes = -1;
+    int dev = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (static_bytes < 0) {
+            cudaFuncAttributes fa;
+            TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_staged_kernel));
+            static_bytes = static_cast<int>(fa.sharedSizeBytes);
+        }
+        if (dev >= 64 || smem + static_bytes > 227 * 1024) return false;
+        if (attr_bytes[dev] < smem) {
+            TW_CUDA(cudaFuncSetAttribute(spmv_tma_staged_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_bytes[dev] = smem;
+        }
+    }
+    const int64_t ns = (n + 31) / 32;
+    const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
+    const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
+    launch_k(spmv_tma_staged_kernel, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, ns, stage,
+             vb, cb, rs, fin);
+    return true;
+}
+
+int spmv_staged_smem_bytes(int max_width) {
+    int vb, cb;
+    return kTmaWarps * staged_stage_bytes(max_width, &vb, &cb);
 }
 
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,

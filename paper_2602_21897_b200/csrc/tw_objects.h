@@ -136,9 +136,17 @@ struct tw_ell {
     int64_t* slice_off = nullptr;
     double* vals = nullptr;
     int32_t* cols = nullptr;
+    uint16_t* cols16 = nullptr; // x-staged columns (single-domain stencil, nx % 32 == 0), or null
     tw::EllView view() const {
-        return tw::EllView{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
-                           info.max_width, ctx->cfg.tma_blocks, info.x_len};
+        tw::EllView v{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
+                      info.max_width, ctx->cfg.tma_blocks, info.x_len};
+        if (cols16) {
+            v.cols16 = cols16;
+            v.sx_nx = info.nx;
+            v.sx_ny = info.ny;
+            v.sx_nz = info.nz;
+        }
+        return v;
     }
 };
 

@@ -264,6 +264,7 @@ static void free_ell(tw_ell* A) {
     cudaFree(A->slice_off);
     cudaFree(A->vals);
     cudaFree(A->cols);
+    cudaFree(A->cols16);
     delete A;
 }
 
@@ -360,6 +361,28 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
 #ifdef TW_CHECKS
         launch_ell_check(A->view(), s);
 #endif
+        // The x-staged form for the single-domain CG's K1: slices are whole
+        // x-line segments when nx % 32 == 0 (TW_STAGE_X=0 turns it off, A/B).
+        const char* sx = std::getenv("TW_STAGE_X");
+        if (zb == 0 && ze == nz && nx % 32 == 0 && !(sx && sx[0] == '0') &&
+            spmv_staged_smem_bytes(static_cast<int>(in.max_width)) + 2048 <= 227 * 1024) {
+            const int64_t ents = in.ell_entries;
+            unsigned* bad = nullptr;
+            TW_CUDA(cudaMalloc(&A->cols16, sizeof(uint16_t) * static_cast<size_t>(ents + 64)));
+            TW_CUDA(cudaMalloc(&bad, sizeof(unsigned)));
+            TW_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
+            EllView v = A->view();
+            v.cols16 = nullptr;
+            launch_stencil_cols16(v, nx, ny, nz, A->cols16, bad, s);
+            unsigned hbad = 0;
+            TW_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+            TW_CUDA(cudaStreamSynchronize(s));
+            cudaFree(bad);
+            if (hbad) { // not representable (should not happen for a stencil): stay unstaged
+                cudaFree(A->cols16);
+                A->cols16 = nullptr;
+            }
+        }
         TW_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaFree(widths);
@@ -837,6 +860,14 @@ int tw_ell_info(const tw_ell* A, tw_ell_info_t* out) {
     return guarded([&] {
         check_ell(A);
         *out = A->info;
+    });
+}
+
+int tw_ell_x_staged(const tw_ell* A, int* staged) {
+    return guarded([&] {
+        check_ell(A);
+        if (!staged) contract_error("null out");
+        *staged = A->cols16 ? 1 : 0;
     });
 }
 

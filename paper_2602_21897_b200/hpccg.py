@@ -266,6 +266,13 @@ class EllMatrix:
     def x_len(self) -> int:
         return int(self.info.x_len)
 
+    @property
+    def x_staged(self) -> bool:
+        """The single-domain CG's K1 reads this matrix in its x-staged form."""
+        v = C.c_int()
+        N.check(_lib().tw_ell_x_staged(self.h, C.byref(v)))
+        return bool(v.value)
+
     def to_csr(self):
         """(row_ptr int64[n+1], col_idx int64[nnz], values f64[nnz]), global columns."""
         n, nnz = self.n, self.nnz()

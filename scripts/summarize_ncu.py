@@ -46,7 +46,7 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
 NNZ, N = 449455096, 16777216  # 256^3
 
 
-def summarize(rep_path, kernel, algorithmic, out_json):
+def summarize(rep_path, kernel, algorithmic, out_json, format_bytes=None):
     raw = subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(raw.splitlines()))
@@ -57,11 +57,19 @@ def summarize(rep_path, kernel, algorithmic, out_json):
     d = {"kernel": kernel, "workload": "256x256x256", "round": tag,
          "source": "ncu --set full --clock-control none, bench.py --steps 6 --warmup 3",
          "dram_bytes_per_launch": traffic, "algorithmic_bytes": algorithmic, "metrics": summ}
+    if format_bytes:
+        d["format_bytes"] = format_bytes  # 16-bit staged columns: 10 B per nonzero
     json.dump(d, open(out_json, "w"), indent=1)
     print(json.dumps(d, indent=1))
 
 
-summarize(rep, "spmv_tma_kernel<true> (K1)", 12 * NNZ + 16 * N, "profiles/k1_traffic.json")
+# the K1 capture is whichever TMA SpMV the bench ran (-k regex:spmv_tma)
+_k1 = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+_staged = "staged" in _k1.split("\n", 3)[2] if _k1.count("\n") > 2 else False
+summarize(rep, "spmv_tma_staged_kernel (K1, x-staged)" if _staged else "spmv_tma_kernel<true> (K1)",
+          12 * NNZ + 16 * N, "profiles/k1_traffic.json",
+          format_bytes=(10 * NNZ + 16 * N) if _staged else None)
 base = os.path.dirname(rep)
 for name, kern, alg in (("prof_k2.ncu-rep", "update_xr_kernel (K2)", 48 * N),
                         ("prof_k3.ncu-rep", "update_p_kernel<false> (K3)", 24 * N)):

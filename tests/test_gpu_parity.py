@@ -874,3 +874,26 @@ def test_abi_misuse_is_reported_not_crashed(rt):
     # the context is still fine
     P.spmv_range(A, x, y, 0, A.n)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dims", [(32, 32, 32), (64, 32, 24), (96, 5, 7), (32, 1, 3)])
+def test_x_staged_k1_bit_identical(rt, orc, dims, monkeypatch):
+    """Single-domain stencil matrices with nx % 32 == 0 carry 16-bit columns
+    into per-slice staged runs of x, and the monolithic CG's K1 reads its
+    operands from shared memory.  Same per-row order and roundings, same
+    reductions: histories and x bit-identical to the gather path
+    (TW_STAGE_X=0), and within the rule of the oracle."""
+    from paper_2602_21897_b200 import _native as N
+    b = orc.rhs_xorshift(int(np.prod(dims)), 9)
+    out = []
+    for stage in ("1", "0"):
+        monkeypatch.setenv("TW_STAGE_X", stage)
+        A = P.gen_stencil_matrix(*dims, rt=rt)
+        for graph in (False, True):
+            res = P.cg_monolithic(rt, A, b, 40, P.CgOptions(use_graph=graph))
+            out.append((res.residual_history, res.x))
+    for h, x in out[1:]:
+        assert np.array_equal(h, out[0][0]) and np.array_equal(x, out[0][1])
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
+    check_history(out[0][0], want_h)
+    assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
