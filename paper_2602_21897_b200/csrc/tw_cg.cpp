@@ -30,12 +30,14 @@
 namespace tw {
 namespace cgi {
 
-// Programmatic dependent launch for the single-domain monolithic chain
-// (TW_PDL=0 turns it off, for A/B).
+// Programmatic dependent launch for the monolithic chains: opt-in
+// (TW_PDL=1).  It helped the gather K1 in streams mode (0.138 -> 0.132 ms at
+// 128^3) but costs the x-staged K1 5 % at 256^3 (0.929 vs 0.883 ms): the
+// successor's early blocks share the SMs with K1's CTAs.
 bool use_pdl() {
     static const bool on = [] {
         const char* e = std::getenv("TW_PDL");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on;
 }
@@ -123,7 +125,7 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
             if (!launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n, rs, fa, s))
                 throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
             cg->p_cur = next;
-        } else if (!launch_spmv_staged(A, cg->p_local, cg->Ap, cg->n, rs, fa, s, pdl)) {
+        } else if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, rs, fa, s, pdl)) {
             launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s,
                         nullptr, 0, pdl);
         }
@@ -199,9 +201,11 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
     case PK_HALO:
         halo_exchange(cg, st);
         break;
-    case PK_SPMV:
-        launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0}, true,
-                    cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
+    case PK_SPMV: // the x-staged K1 when the matrix has it (single domain)
+        if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]},
+                                cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, st))
+            launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0},
+                        true, cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
         break;
     case PK_ALPHA:
         if (!cg->dist) {

@@ -263,8 +263,8 @@ void launch_stencil_cols16(const EllView& A, int64_t nx, int64_t ny, int64_t nz,
 // K1 on an x-staged matrix (single-domain monolithic CG): the slice block
 // and its 9 x runs arrive in one TMA transaction per slice; x must have 2
 // readable doubles of slack before index 0 and after x_len.
-bool launch_spmv_staged(const EllView& A, const double* x, double* y, int64_t n, RedScratch rs,
-                        Fin fin, cudaStream_t s, bool pdl);
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows, RedScratch rs,
+                        Fin fin, cudaStream_t s, bool pdl = false);
 int spmv_staged_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only
 // trailing a row, slice widths within max_width (traps otherwise).

@@ -475,7 +475,7 @@ __device__ __forceinline__ double staged_row_generic(const double* vb, const uin
 // slice's values, 16-bit columns and 9 x runs, one mbarrier transaction.
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
-                       int64_t n_slices, int stage_bytes, int val_bytes, int c16_bytes,
+                       RowRange rows, int stage_bytes, int val_bytes, int c16_bytes,
                        RedScratch rs, Fin fin) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps];
@@ -487,6 +487,9 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     double* xs = reinterpret_cast<double*>(stage + val_bytes + c16_bytes);
     const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    // the slices covering the row range (a tile of the tasks variant may
+    // start and end inside a slice: rows outside it are neither written nor dotted)
+    const int64_t s0 = rows.r0 >> 5, n_slices = rows.r1 > rows.r0 ? ((rows.r1 + 31) >> 5) - s0 : 0;
     const int64_t mine = warp_g < n_slices ? (n_slices - warp_g + nwarps - 1) / nwarps : 0;
     pdl_launch_dependents();
     if (lane == 0) mbar_init(&bars[warp], 1);
@@ -497,7 +500,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     // lane 0: the slice block (values + 16-bit columns) and then its 9 x runs,
     // all on one mbarrier transaction
     auto issue_block = [&](int64_t k) {
-        const int64_t s = warp_g + k * nwarps;
+        const int64_t s = s0 + warp_g + k * nwarps;
         const int64_t off = A.slice_off[s];
         const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
         TW_DCHECK(s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
@@ -509,7 +512,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         }
     };
     auto issue_x = [&](int64_t k) { // default L2 policy: neighbouring slices share runs
-        const int64_t s = warp_g + k * nwarps;
+        const int64_t s = s0 + warp_g + k * nwarps;
         for (int r = 0; r < kStageRuns; ++r) {
             const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz);
             asm volatile(
@@ -538,9 +541,11 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         case 8: acc = staged_row_fixed<8>(vb, cb, xs, lane); break;
         default: acc = staged_row_generic(vb, cb, xs, lane, w); break;
         }
-        const int64_t row = ((warp_g + k * nwarps) << 5) + lane;
-        y[row] = acc;
-        part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc)); // p[row]
+        const int64_t row = ((s0 + warp_g + k * nwarps) << 5) + lane;
+        if (row >= rows.r0 && row < rows.r1) {
+            y[row] = acc;
+            part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc)); // p[row]
+        }
         __syncwarp();
         if (lane == 0 && k + 1 < mine) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1059,7 +1064,7 @@ static int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
     return *val_bytes + *c16_bytes + (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
 }
 
-bool launch_spmv_staged(const EllView& A, const double* x, double* y, int64_t n, RedScratch rs,
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows, RedScratch rs,
                         Fin fin, cudaStream_t s, bool pdl) {
     if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
     int vb, cb;
@@ -1084,11 +1089,11 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, int64_t n,
             attr_bytes[dev] = smem;
         }
     }
-    const int64_t ns = (n + 31) / 32;
+    const int64_t ns = rows.r1 > rows.r0 ? ((rows.r1 + 31) >> 5) - (rows.r0 >> 5) : 0;
     const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
     const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-    launch_k(spmv_tma_staged_kernel, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, ns, stage,
-             vb, cb, rs, fin);
+    launch_k(spmv_tma_staged_kernel, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, rows,
+             stage, vb, cb, rs, fin);
     return true;
 }
 

@@ -889,11 +889,18 @@ def test_x_staged_k1_bit_identical(rt, orc, dims, monkeypatch):
     for stage in ("1", "0"):
         monkeypatch.setenv("TW_STAGE_X", stage)
         A = P.gen_stencil_matrix(*dims, rt=rt)
+        assert A.x_staged == (stage == "1")
         for graph in (False, True):
             res = P.cg_monolithic(rt, A, b, 40, P.CgOptions(use_graph=graph))
             out.append((res.residual_history, res.x))
-    for h, x in out[1:]:
-        assert np.array_equal(h, out[0][0]) and np.array_equal(x, out[0][1])
+        for T in (3, 16):  # tiles cut slices: partial slices at the tile edges
+            res = P.cg_tasks(rt, A, b, 40, P.CgOptions(tiles=T))
+            out.append((res.residual_history, res.x))
+    # out: [mono, mono graph, tasks T=3, tasks T=16] staged, then the same gathered
+    def same(i, j):
+        return np.array_equal(out[i][0], out[j][0]) and np.array_equal(out[i][1], out[j][1])
+    assert same(0, 1) and same(0, 4) and same(0, 5)   # monolithic
+    assert same(2, 6) and same(3, 7)                  # tasks, per tile count
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
     check_history(out[0][0], want_h)
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
