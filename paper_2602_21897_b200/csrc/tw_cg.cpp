@@ -364,11 +364,17 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         if (cg->opt.dispatch == TW_DISPATCH_AUTO) {
             // the persistent dispatcher where it wins (many tiles, one rank,
             // no graph requested; profiles/r01_sweep_summary.md), else streams
+            // small tiles: on the x-staged matrix the streams path keeps the
+            // staged K1 (the dispatcher gathers), so it holds out to smaller
+            // tiles -- about 400k rows (256^3: 32 tiles streams, 64 persistent;
+            // 128^3: 16 tiles persistent); on a gather matrix, more than 8 tiles
             int sb, vb;
             const bool fits = dag_smem_bytes(A->info.max_width, &sb, &vb) <= 200 * 1024;
-            cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && cg->opt.tiles > 8 &&
-                                       !ctx->nccl_comm && !ctx->emulated && fits &&
-                                       !cg->opt.use_graph
+            const int64_t rows_per_tile = A->info.n_rows / std::max(cg->opt.tiles, 1);
+            const bool small =
+                cg->opt.tiles > 1 && (A->cols16 ? rows_per_tile < 400000 : cg->opt.tiles > 8);
+            cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && small && !ctx->nccl_comm &&
+                                       !ctx->emulated && fits && !cg->opt.use_graph
                                    ? TW_DISPATCH_PERSISTENT
                                    : TW_DISPATCH_STREAMS;
         }

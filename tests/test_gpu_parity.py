@@ -391,7 +391,10 @@ def test_scenario_run_point_csv(rt, orc, golden):
                          tiles=[1, 4, 16], variant="tasks")
     pts = S.run_sweep(c, rt=rt)  # 16 tiles: the persistent dispatcher (automatic dispatch)
     assert [p.tile for p in pts] == [1, 4, 16]
-    assert pts[2].rows[0].tasks_executed == 1 and pts[1].rows[0].tasks_executed == 14 * 20
+    # automatic dispatch: 1 tile streams (5 launches per iteration); small
+    # tiles of an x-staged matrix the persistent dispatcher (one launch)
+    assert pts[0].rows[0].tasks_executed == 5 * 20
+    assert pts[1].rows[0].tasks_executed == 1 and pts[2].rows[0].tasks_executed == 1
     for p in pts:
         assert len(p.rows) == 40
         assert all(r.warmup for r in p.rows[:20])            # repetition 0 is warm-up
@@ -807,10 +810,12 @@ def test_peer_transport_bit_identical_to_nccl_path(orc, dims, P_):
 
 def test_auto_dispatch_and_persistent_marks(rt, orc):
     """TW_DISPATCH_AUTO (the C default): the persistent dispatcher for the
-    tasks variant with > 8 tiles, streams otherwise; the persistent path's
+    tasks variant with small tiles (> 8 tiles on a gather matrix, < 400k
+    rows per tile on an x-staged one), streams otherwise; the persistent path's
     per-iteration host marks are placed by the device clock before each
     call's polled mark (non-decreasing, each call's last one polled)."""
-    A = P.gen_stencil_matrix(48, 40, 36, rt=rt)
+    A = P.gen_stencil_matrix(48, 40, 36, rt=rt)  # nx % 32 != 0: a gather matrix
+    assert not A.x_staged
     b = orc.rhs_xorshift(A.n, 3)
     want_h, want_x, _ = orc.cg(orc.stencil(48, 40, 36), b, 30)
     for T, want_k in ((16, 0), (4, 3 * 4 + 2)):
