@@ -48,16 +48,25 @@ void halo_exchange(tw_cg* cg, cudaStream_t s) {
 // interleaves them with the halo and the allgathers (enqueue_mono); the
 // emulated rank group (tw_cg_group_iterate) runs them rank by rank with
 // loopback copies in place of NCCL.
+// On an x-staged slab both launches are the staged K1 (the peer transport's
+// one-launch form walks the same two index spaces, so the sums agree to the bit).
 void dist_spmv_interior(tw_cg* cg, cudaStream_t s) { // rows that read no ghost plane
+    const RowRange ri{cg->slab.interior_r0, cg->slab.interior_r1};
+    if (launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, ri, cg->slot(0),
+                           Fin{FIN_STORE, cg->pm, nullptr, nullptr}, s))
+        return;
     launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
                 RowRange{0, 0}, true, cg->slot(0), Fin{FIN_STORE, cg->pm, nullptr, nullptr},
                 launch_blocks(cg, true), s);
 }
 
 void dist_spmv_boundary(tw_cg* cg, cudaStream_t s) { // the ghost-reading planes, then p.Ap
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+    if (!launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+                            RowRange{cg->slab.interior_r1, cg->n}, RowRange{0, 0}, false,
+                            cg->slot(0), Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, s))
+        launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
                 RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
-                Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, launch_blocks(cg, true), s);
+                    Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, launch_blocks(cg, true), s);
     launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
 }
 
@@ -78,7 +87,9 @@ void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; 
 bool peer_k1_fused(const tw_cg* cg) {
     const EllView A = cg->view();
     if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
-    if (spmv_tma_smem_bytes(A.max_width) + 2048 > 227 * 1024) return false;
+    if ((A.cols16 ? spmv_staged_smem_bytes(A.max_width) : spmv_tma_smem_bytes(A.max_width)) + 2048 >
+        227 * 1024)
+        return false;
     auto slices = [](int64_t r0, int64_t r1) { return r1 > r0 ? ((r1 + 31) >> 5) - (r0 >> 5) : 0; };
     const int64_t full = static_cast<int64_t>(A.tma_blocks) * spmv_tma_warps();
     return slices(cg->slab.interior_r0, cg->slab.interior_r1) >= full &&
@@ -88,6 +99,19 @@ bool peer_k1_fused(const tw_cg* cg) {
 void peer_spmv(tw_cg* cg, cudaStream_t s) {
     const int ng = cg->slab.ghost_lo + cg->slab.ghost_hi;
     const unsigned long long* gf = cg->slab.ghost_lo ? &cg->win->flag_ghost_lo : &cg->win->flag_ghost_hi;
+    const Fin fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm};
+    const RowRange ri{cg->slab.interior_r0, cg->slab.interior_r1}, b0{0, cg->slab.interior_r0},
+        b1{cg->slab.interior_r1, cg->n};
+    if (cg->view().cols16) { // x-staged slab: the same two forms with staged x runs
+        if (launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, ri, b0, b1, true, cg->slot(0), fin,
+                               s, ng ? gf : nullptr, ng, use_pdl()))
+            return;
+        dist_spmv_interior(cg, s);
+        if (!launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, b0, b1, RowRange{0, 0}, false,
+                                cg->slot(0), fin, s, ng ? gf : nullptr, ng))
+            throw Error(TW_ERR_CUDA, "staged boundary SpMV did not launch after the interior did");
+        return;
+    }
     // one launch: interior rows first (they read no ghost plane, so they
     // overlap the neighbours' K3 tails), then the boundary rows
     if (launch_spmv_split(cg->view(), cg->p_local, cg->Ap,

@@ -240,25 +240,28 @@ __global__ void scan_apply_kernel(const int64_t* in, int64_t n, const int64_t* s
 
 // 16-bit staged columns (ell_c16_pos layout) from the 32-bit ones: column c
 // of a row in slice s maps to run r (its (dz, dy) line) at c - start(r).
-__global__ void stencil_cols16_kernel(EllView A, int64_t nx, int64_t ny, int64_t nz,
-                                      uint16_t* cols16, unsigned* bad) {
+// Slab matrices work in global coordinates: local row + sx_row_off, local
+// column + sx_col_off.
+__global__ void stencil_cols16_kernel(EllView A, uint16_t* cols16, unsigned* bad) {
     const int lane = threadIdx.x & 31;
     const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    const int64_t plane = nx * ny;
+    const int64_t nx = A.sx_nx, ny = A.sx_ny, nz = A.sx_nz, plane = nx * ny;
     for (int64_t s = warp_g; s < A.n_slices; s += nwarps) {
         const int64_t off = A.slice_off[s];
         const int w = static_cast<int>((A.slice_off[s + 1] - off) >> 5);
-        const int64_t row0 = s * 32, z0 = row0 / plane, y0 = (row0 / nx) % ny;
+        const int64_t row0 = s * 32 + A.sx_row_off, z0 = row0 / plane, y0 = (row0 / nx) % ny;
         for (int k = 0; k < w; ++k) {
             const int c = A.cols[off + ell_col_pos(k, lane, w)];
             uint16_t v = kStagePad;
             if (c >= 0) {
-                const int64_t dz = c / plane - z0, dy = (c / nx) % ny - y0;
+                const int64_t cg = c + A.sx_col_off;
+                const int64_t dz = cg / plane - z0, dy = (cg / nx) % ny - y0;
                 const int r = static_cast<int>((dz + 1) * 3 + (dy + 1));
-                const int64_t o = (dz < -1 || dz > 1 || dy < -1 || dy > 1)
-                                      ? -1
-                                      : c - stage_run_start(s, r, nx, ny, nz);
+                const int64_t o =
+                    (dz < -1 || dz > 1 || dy < -1 || dy > 1)
+                        ? -1
+                        : c - stage_run_start(s, r, nx, ny, nz, A.sx_row_off, A.sx_col_off);
                 if (o < 0 || o >= kStageRunLen) atomicOr(bad, 1u);
                 else v = static_cast<uint16_t>(r * kStageRunLen + o);
             }
@@ -290,10 +293,8 @@ __global__ void ell_check_kernel(EllView A) {
 
 } // namespace
 
-void launch_stencil_cols16(const EllView& A, int64_t nx, int64_t ny, int64_t nz, uint16_t* cols16,
-                           unsigned* bad, cudaStream_t s) {
-    stencil_cols16_kernel<<<clamp_blocks(A.n_slices * 32, 4096), kThreads, 0, s>>>(A, nx, ny, nz,
-                                                                                  cols16, bad);
+void launch_stencil_cols16(const EllView& A, uint16_t* cols16, unsigned* bad, cudaStream_t s) {
+    stencil_cols16_kernel<<<clamp_blocks(A.n_slices * 32, 4096), kThreads, 0, s>>>(A, cols16, bad);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -47,12 +47,14 @@ struct EllView {
     int max_width;            // widest slice (sizes the TMA stages)
     int tma_blocks;           // persistent grid of the TMA SpMV (0 = plain kernel)
     int64_t x_len;            // entries of the gathered vector (owned + ghost planes)
-    // x-staged form (single-domain stencil, nx % 32 == 0; null otherwise):
+    // x-staged form (stencil or z-slab of one, nx % 32 == 0; null otherwise):
     // every stored column as a 16-bit index into the slice's staged window of
     // x -- 9 runs of 36 doubles, one per (dz, dy) neighbour line -- in the
-    // chunked layout of ell_c16_pos; sx_* is the grid the runs come from
+    // chunked layout of ell_c16_pos; sx_* is the global grid the runs come
+    // from and the slab's global row / column offsets
     const uint16_t* cols16 = nullptr;
     int64_t sx_nx = 0, sx_ny = 0, sx_nz = 0;
+    int64_t sx_row_off = 0, sx_col_off = 0;
 };
 
 // x-staged windows: run r = (dz + 1) * 3 + (dy + 1) of a slice starts 2
@@ -78,15 +80,18 @@ __host__ __device__ inline int64_t ell_c16_pos(int k, int lane, int w) {
     return 32LL * base + lane;
 }
 
-// Start (in x indices) of staged run r of slice s of an x-staged matrix; a
-// neighbour line outside the grid stages the slice's own line instead (no
-// stored column refers to it).
+// Start (in local x indices) of staged run r of slice s of an x-staged
+// matrix whose local row 0 is global row row_off and local column 0 global
+// column col_off; a neighbour line outside the global grid stages the
+// slice's own line instead (no stored column refers to it).  A slab's
+// neighbour lines in the planes next to it are its ghost planes.
 __host__ __device__ inline int64_t stage_run_start(int64_t s, int r, int64_t nx, int64_t ny,
-                                                   int64_t nz) {
-    const int64_t row0 = s * 32, x0 = row0 % nx, t = row0 / nx, y = t % ny, z = t / ny;
+                                                   int64_t nz, int64_t row_off = 0,
+                                                   int64_t col_off = 0) {
+    const int64_t row0 = s * 32 + row_off, x0 = row0 % nx, t = row0 / nx, y = t % ny, z = t / ny;
     const int64_t zz = z + r / 3 - 1, yy = y + r % 3 - 1;
     const bool in = zz >= 0 && zz < nz && yy >= 0 && yy < ny;
-    return (in ? zz * ny + yy : z * ny + y) * nx + x0 - 2;
+    return (in ? zz * ny + yy : z * ny + y) * nx + x0 - 2 - col_off;
 }
 
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
@@ -255,16 +260,28 @@ struct GroupRank {
 int rank_group_blocks_per_rank(int nranks);
 void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
                        int iterations, int jitter, cudaStream_t s);
-// Builds the 16-bit staged columns of a single-domain stencil matrix
-// (nx % 32 == 0) from its 32-bit columns; returns false if any stored column
-// falls outside its slice's staged runs (then the matrix stays unstaged).
-void launch_stencil_cols16(const EllView& A, int64_t nx, int64_t ny, int64_t nz, uint16_t* cols16,
-                           unsigned* bad, cudaStream_t s);
-// K1 on an x-staged matrix (single-domain monolithic CG): the slice block
-// and its 9 x runs arrive in one TMA transaction per slice; x must have 2
-// readable doubles of slack before index 0 and after x_len.
-bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows, RedScratch rs,
-                        Fin fin, cudaStream_t s, bool pdl = false);
+// Builds the 16-bit staged columns of a stencil matrix or z-slab
+// (nx % 32 == 0; A carries sx_*) from its 32-bit columns; flags *bad if any
+// stored column falls outside its slice's staged runs (then the matrix
+// stays unstaged).
+void launch_stencil_cols16(const EllView& A, uint16_t* cols16, unsigned* bad, cudaStream_t s);
+// K1 on an x-staged matrix: the slice block and its 9 x runs arrive in one
+// TMA transaction per slice; x must have 2 readable doubles of slack before
+// index 0 and after x_len.  The three ranges form ONE index space (walked
+// like launch_spmv's two), or with split = true two -- ra, then rb0 ++ rb1
+// with its own p.Ap partial (grid_reduce2_finalize), the x runs of its
+// slices staged only after the warp's acquire of wait_flags (the peer
+// transport's ghost planes; launch_spmv_split's contract).  Without split a
+// non-zero nwait holds every slice's x runs until the flags are up.
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange ra, RowRange rb0,
+                        RowRange rb1, bool split, RedScratch rs, Fin fin, cudaStream_t s,
+                        const unsigned long long* wait_flags = nullptr, int nwait = 0,
+                        bool pdl = false);
+inline bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows,
+                               RedScratch rs, Fin fin, cudaStream_t s, bool pdl = false) {
+    return launch_spmv_staged(A, x, y, rows, RowRange{0, 0}, RowRange{0, 0}, false, rs, fin, s,
+                              nullptr, 0, pdl);
+}
 int spmv_staged_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only
 // trailing a row, slice widths within max_width (traps otherwise).

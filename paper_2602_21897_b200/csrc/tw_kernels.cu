@@ -471,12 +471,37 @@ __device__ __forceinline__ double staged_row_generic(const double* vb, const uin
     return acc;
 }
 
-// K1 for a single-domain x-staged matrix: per warp one stage holding the
-// slice's values, 16-bit columns and 9 x runs, one mbarrier transaction.
+// Up to three row ranges walked as one index space of slices (range k's
+// slices follow range k-1's), the order launch_spmv walks its two in.
+struct SliceSpace {
+    RowRange q[3];
+    int64_t c0, c1, n; // slices of q[0], of q[0] ++ q[1], of all three
+    __device__ static int64_t count(RowRange r) {
+        return r.r1 > r.r0 ? ((r.r1 + 31) >> 5) - (r.r0 >> 5) : int64_t(0);
+    }
+    __device__ SliceSpace(RowRange a, RowRange b, RowRange c) : q{a, b, c} {
+        c0 = count(a);
+        c1 = c0 + count(b);
+        n = c1 + count(c);
+    }
+    __device__ int which(int64_t i) const { return i < c0 ? 0 : i < c1 ? 1 : 2; }
+    __device__ int64_t slice(int64_t i, int w) const {
+        return (q[w].r0 >> 5) + i - (w == 0 ? 0 : w == 1 ? c0 : c1);
+    }
+};
+
+// K1 on an x-staged matrix: per warp one stage holding the slice's values,
+// 16-bit columns and 9 x runs, one mbarrier transaction.  The warp's slices
+// are those of space A (split only: the interior rows) and then of space B;
+// B's x runs wait for the warp's acquire of the ghost-plane flags when there
+// are any, and with SPLIT the two spaces keep separate p.Ap partials, so the
+// results are bit-identical to one launch per space (the NCCL transport).
+template <bool SPLIT>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
-                       RowRange rows, int stage_bytes, int val_bytes, int c16_bytes,
-                       RedScratch rs, Fin fin) {
+                       RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
+                       int c16_bytes, RedScratch rs, Fin fin, const unsigned long long* wait_flags,
+                       int nwait) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps];
     __shared__ int stage_w[kTmaWarps];
@@ -487,23 +512,33 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     double* xs = reinterpret_cast<double*>(stage + val_bytes + c16_bytes);
     const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
-    // the slices covering the row range (a tile of the tasks variant may
-    // start and end inside a slice: rows outside it are neither written nor dotted)
-    const int64_t s0 = rows.r0 >> 5, n_slices = rows.r1 > rows.r0 ? ((rows.r1 + 31) >> 5) - s0 : 0;
-    const int64_t mine = warp_g < n_slices ? (n_slices - warp_g + nwarps - 1) / nwarps : 0;
+    // a tile of the tasks variant may start and end inside a slice: rows
+    // outside the ranges are neither written nor dotted
+    const RowRange none{0, 0};
+    const SliceSpace sa(SPLIT ? ra : none, none, none);
+    const SliceSpace sb(SPLIT ? rb0 : ra, SPLIT ? rb1 : rb0, SPLIT ? none : rb1);
+    auto mine_of = [&](int64_t n) { return warp_g < n ? (n - warp_g + nwarps - 1) / nwarps : int64_t(0); };
+    const int64_t mine_a = mine_of(sa.n), mine = mine_a + mine_of(sb.n);
+    auto locate = [&](int64_t k, RowRange& rr) {
+        const SliceSpace& sp = k < mine_a ? sa : sb;
+        const int64_t i = warp_g + (k < mine_a ? k : k - mine_a) * nwarps;
+        const int w = sp.which(i);
+        rr = sp.q[w];
+        return sp.slice(i, w);
+    };
     pdl_launch_dependents();
     if (lane == 0) mbar_init(&bars[warp], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     const uint64_t pol = l2_evict_first_policy();
     constexpr uint32_t kRunBytes = kStageRunLen * 8;
+    const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
     // lane 0: the slice block (values + 16-bit columns) and then its 9 x runs,
     // all on one mbarrier transaction
-    auto issue_block = [&](int64_t k) {
-        const int64_t s = s0 + warp_g + k * nwarps;
+    auto issue_block = [&](int64_t s) {
         const int64_t off = A.slice_off[s];
         const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
-        TW_DCHECK(s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
+        TW_DCHECK(s >= 0 && s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
         stage_w[warp] = static_cast<int>(ents >> 5);
         mbar_expect_tx(&bars[warp], ents * 10u + kStageRuns * kRunBytes);
         if (ents) {
@@ -511,10 +546,17 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
             bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, &bars[warp], pol);
         }
     };
-    auto issue_x = [&](int64_t k) { // default L2 policy: neighbouring slices share runs
-        const int64_t s = s0 + warp_g + k * nwarps;
+    auto issue_x = [&](int64_t k, int64_t s) { // default L2 policy: neighbouring slices share runs
+        if (k == mine_a && nwait) {
+            // first slice of space B: the neighbours' ghost planes must have
+            // landed; then order the async-proxy (TMA) reads after the acquire
+            for (int f = 0; f < nwait; ++f)
+                while (ld_acquire_sys(wait_flags + f) < want) __nanosleep(32);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int r = 0; r < kStageRuns; ++r) {
-            const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz);
+            const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz, A.sx_row_off,
+                                               A.sx_col_off);
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
@@ -524,12 +566,14 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     };
     // the matrix does not depend on the previous kernel: the first block
     // streams in before the wait for it; x (that kernel's p) only after
-    if (lane == 0 && mine > 0) issue_block(0);
+    RowRange rr;
+    int64_t s = mine > 0 ? locate(0, rr) : 0;
+    if (lane == 0 && mine > 0) issue_block(s);
     __syncwarp();
     pdl_wait();
-    if (lane == 0 && mine > 0) issue_x(0);
+    if (lane == 0 && mine > 0) issue_x(0, s);
     __syncwarp();
-    double part = 0.0;
+    double part_a = 0.0, part_b = 0.0;
     for (int64_t k = 0; k < mine; ++k) {
         mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
         const int w = stage_w[warp];
@@ -541,20 +585,26 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         case 8: acc = staged_row_fixed<8>(vb, cb, xs, lane); break;
         default: acc = staged_row_generic(vb, cb, xs, lane, w); break;
         }
-        const int64_t row = ((s0 + warp_g + k * nwarps) << 5) + lane;
-        if (row >= rows.r0 && row < rows.r1) {
+        const int64_t row = (s << 5) + lane;
+        if (row >= rr.r0 && row < rr.r1) {
             y[row] = acc;
-            part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc)); // p[row]
+            const double d = __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc); // p[row] * (Ap)[row]
+            if (SPLIT && k < mine_a) part_a = __dadd_rn(part_a, d);
+            else part_b = __dadd_rn(part_b, d);
         }
         __syncwarp();
-        if (lane == 0 && k + 1 < mine) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_block(k + 1);
-            issue_x(k + 1);
+        if (k + 1 < mine) {
+            s = locate(k + 1, rr);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue_block(s);
+                issue_x(k + 1, s);
+            }
         }
         __syncwarp();
     }
-    grid_reduce_finalize(part, rs, fin);
+    if (SPLIT) grid_reduce2_finalize(part_a, part_b, rs, fin);
+    else grid_reduce_finalize(part_b, rs, fin);
 }
 
 // --------------------------------------------------------- K2 / K3 / K4 streams
@@ -1064,36 +1114,55 @@ static int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
     return *val_bytes + *c16_bytes + (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
 }
 
-bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows, RedScratch rs,
-                        Fin fin, cudaStream_t s, bool pdl) {
-    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
-    int vb, cb;
-    const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
-    const int smem = kTmaWarps * stage;
+template <bool SPLIT>
+static bool staged_attr(int smem) {
     static std::mutex mu;
     static int attr_bytes[64] = {};
     static int static_bytes = -1;
     int dev = 0;
     TW_CUDA(cudaGetDevice(&dev));
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (static_bytes < 0) {
-            cudaFuncAttributes fa;
-            TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_staged_kernel));
-            static_bytes = static_cast<int>(fa.sharedSizeBytes);
-        }
-        if (dev >= 64 || smem + static_bytes > 227 * 1024) return false;
-        if (attr_bytes[dev] < smem) {
-            TW_CUDA(cudaFuncSetAttribute(spmv_tma_staged_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_bytes[dev] = smem;
-        }
+    std::lock_guard<std::mutex> lk(mu);
+    if (static_bytes < 0) {
+        cudaFuncAttributes fa;
+        TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_staged_kernel<SPLIT>));
+        static_bytes = static_cast<int>(fa.sharedSizeBytes);
     }
-    const int64_t ns = rows.r1 > rows.r0 ? ((rows.r1 + 31) >> 5) - (rows.r0 >> 5) : 0;
-    const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
-    const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-    launch_k(spmv_tma_staged_kernel, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, rows,
-             stage, vb, cb, rs, fin);
+    if (dev >= 64 || smem + static_bytes > 227 * 1024) return false;
+    if (attr_bytes[dev] < smem) {
+        TW_CUDA(cudaFuncSetAttribute(spmv_tma_staged_kernel<SPLIT>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_bytes[dev] = smem;
+    }
+    return true;
+}
+
+bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange ra, RowRange rb0,
+                        RowRange rb1, bool split, RedScratch rs, Fin fin, cudaStream_t s,
+                        const unsigned long long* wait_flags, int nwait, bool pdl) {
+    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    int vb, cb;
+    const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
+    const int smem = kTmaWarps * stage;
+    if (!(split ? staged_attr<true>(smem) : staged_attr<false>(smem))) return false;
+    auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
+    const int64_t full = static_cast<int64_t>(A.tma_blocks) * kTmaWarps;
+    int g;
+    if (split) {
+        // the grid the separate launches would use: the full persistent grid
+        // whenever each space has >= one slice per warp of it (else fall back)
+        if (slices(ra) < full || slices(rb0) + slices(rb1) < full) return false;
+        g = A.tma_blocks;
+    } else {
+        const int64_t ns = slices(ra) + slices(rb0) + slices(rb1);
+        const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
+        g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
+    }
+    if (split)
+        launch_k(spmv_tma_staged_kernel<true>, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y,
+                 ra, rb0, rb1, stage, vb, cb, rs, fin, wait_flags, nwait);
+    else
+        launch_k(spmv_tma_staged_kernel<false>, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x,
+                 y, ra, rb0, rb1, stage, vb, cb, rs, fin, wait_flags, nwait);
     return true;
 }
 

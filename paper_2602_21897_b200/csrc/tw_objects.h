@@ -136,7 +136,7 @@ struct tw_ell {
     int64_t* slice_off = nullptr;
     double* vals = nullptr;
     int32_t* cols = nullptr;
-    uint16_t* cols16 = nullptr; // x-staged columns (single-domain stencil, nx % 32 == 0), or null
+    uint16_t* cols16 = nullptr; // x-staged columns (stencil or z-slab, nx % 32 == 0), or null
     tw::EllView view() const {
         tw::EllView v{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
                       info.max_width, ctx->cfg.tma_blocks, info.x_len};
@@ -145,6 +145,8 @@ struct tw_ell {
             v.sx_nx = info.nx;
             v.sx_ny = info.ny;
             v.sx_nz = info.nz;
+            v.sx_row_off = info.row_offset;
+            v.sx_col_off = info.col_offset;
         }
         return v;
     }

@@ -361,19 +361,18 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
 #ifdef TW_CHECKS
         launch_ell_check(A->view(), s);
 #endif
-        // The x-staged form for the single-domain CG's K1: slices are whole
-        // x-line segments when nx % 32 == 0 (TW_STAGE_X=0 turns it off, A/B).
+        // The x-staged form for the CG's K1: slices are whole x-line
+        // segments when nx % 32 == 0 (the slab's first row is a plane
+        // start); TW_STAGE_X=0 turns it off (A/B).
         const char* sx = std::getenv("TW_STAGE_X");
-        if (zb == 0 && ze == nz && nx % 32 == 0 && !(sx && sx[0] == '0') &&
+        if (nx % 32 == 0 && !(sx && sx[0] == '0') &&
             spmv_staged_smem_bytes(static_cast<int>(in.max_width)) + 2048 <= 227 * 1024) {
             const int64_t ents = in.ell_entries;
             unsigned* bad = nullptr;
             TW_CUDA(cudaMalloc(&A->cols16, sizeof(uint16_t) * static_cast<size_t>(ents + 64)));
             TW_CUDA(cudaMalloc(&bad, sizeof(unsigned)));
             TW_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
-            EllView v = A->view();
-            v.cols16 = nullptr;
-            launch_stencil_cols16(v, nx, ny, nz, A->cols16, bad, s);
+            launch_stencil_cols16(A->view(), A->cols16, bad, s); // reads the 32-bit columns
             unsigned hbad = 0;
             TW_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
             TW_CUDA(cudaStreamSynchronize(s));

@@ -909,3 +909,35 @@ def test_x_staged_k1_bit_identical(rt, orc, dims, monkeypatch):
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
     check_history(out[0][0], want_h)
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("dims,P_", [((64, 24, 40), 4), ((32, 8, 32), 8), ((32, 4, 4), 4),
+                                     ((320, 288, 12), 2)])
+def test_x_staged_slabs_multi_rank(orc, dims, P_, monkeypatch):
+    """z-slab matrices with nx % 32 == 0 are x-staged too: their staged runs
+    reach into the ghost planes (global line geometry, local columns).  The
+    NCCL-path phases (loopback) and the peer transport -- whose boundary
+    slices stage x only after the ghost-plane flags are acquired, in one
+    launch on the 320x288 planes -- must agree to the bit, and both within
+    the rule of the oracle; the gather slabs (TW_STAGE_X=0) too."""
+    b = orc.rhs_xorshift(int(np.prod(dims)), 4)
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 30)
+    out = {}
+    for stage in ("1", "0"):
+        monkeypatch.setenv("TW_STAGE_X", stage)
+        for transport in ("loopback", "peer"):
+            G = P.EmulatedRankGroup(*dims, P_, 30, transport=transport)
+            assert all(A.x_staged == (stage == "1") for A in G.mats)
+            G.set_rhs(b)
+            G.iterate(11)
+            G.iterate(19)
+            hs = G.history(30)
+            for h in hs:
+                assert np.array_equal(h, hs[0])
+            out[stage, transport] = (hs[0], G.solution())
+            G.close()
+            check_history(hs[0], want_h)
+            assert np.all(rel_gap(out[stage, transport][1], want_x) <= 1e-10)
+    for stage in ("1", "0"):
+        (h0, x0), (h1, x1) = out[stage, "loopback"], out[stage, "peer"]
+        assert np.array_equal(h0, h1) and np.array_equal(x0, x1)
