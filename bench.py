@@ -492,16 +492,18 @@ def run_ours(args, dist, rank, world, local):
         k3_launches = 1 if fused else nt
         wl = f"{nx}x{ny}x{args.nz}"
 
-        # single-domain stencil matrices carry the x-staged form: K1 then reads
-        # 16-bit column indices (10 B per nonzero instead of SURVEY 8(d)'s 12)
-        # and its operands from per-slice x windows staged by the same TMA
-        # transaction; `achieved` stays on SURVEY's algorithmic bytes, the
-        # format's own bytes are reported beside it
-        staged = variant == 0 and world == 1 and not args.comm and A.x_staged and not fused
+        # stencil matrices and z-slabs with nx % 32 == 0 carry the x-staged
+        # form: K1 then reads 16-bit column indices (10 B per nonzero instead
+        # of SURVEY 8(d)'s 12) and its operands from per-slice x windows staged
+        # by the same TMA transaction; `achieved` stays on SURVEY's
+        # algorithmic bytes, the format's own bytes are reported beside it
+        staged = variant == 0 and A.x_staged and not fused
         k1_format_bytes = (10 * nnz + 16 * n) if staged else k1_bytes
+        slab = world > 1 or args.comm
         kname = ("spmv_tma_kernel<true,true> (K1: TMA-staged SpMV + p.Ap, previous K3 fused)"
                  if fused else
-                 "spmv_tma_staged_kernel (K1: TMA-staged matrix + x windows, 16-bit columns, p.Ap)"
+                 ("spmv_tma_staged_kernel (K1: TMA-staged matrix + x windows, 16-bit columns, p.Ap"
+                  + ("; z-slab: interior rows, then the ghost-reading boundary rows)" if slab else ")"))
                  if staged else "spmv_tma_kernel<true> (K1: TMA-staged SpMV + p.Ap)")
 
         def traffic_of(k):
