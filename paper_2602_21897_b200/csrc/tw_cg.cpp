@@ -364,15 +364,19 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         if (cg->opt.dispatch == TW_DISPATCH_AUTO) {
             // the persistent dispatcher where it wins (many tiles, one rank,
             // no graph requested; profiles/r01_sweep_summary.md), else streams
-            // small tiles: on the x-staged matrix the streams path keeps the
-            // staged K1 (the dispatcher gathers), so it holds out to smaller
-            // tiles -- about 400k rows (256^3: 32 tiles streams, 64 persistent;
-            // 128^3: 16 tiles persistent); on a gather matrix, more than 8 tiles
-            int sb, vb;
-            const bool fits = dag_smem_bytes(A->info.max_width, &sb, &vb) <= 200 * 1024;
+            // small tiles: on an x-staged matrix below ~400k rows per tile,
+            // or from 32 tiles up below 1M rows per tile (measured crossovers:
+            // 128^3 between 4 and 8 tiles, 256^3 between 16 and 32;
+            // profiles/r01_dispatcher_summary.md); on a gather matrix, more
+            // than 8 tiles
+            int sb, vb, cb;
+            const bool fits =
+                dag_smem_bytes(A->info.max_width, A->cols16 != nullptr, &sb, &vb, &cb) <= 225 * 1024;
             const int64_t rows_per_tile = A->info.n_rows / std::max(cg->opt.tiles, 1);
             const bool small =
-                cg->opt.tiles > 1 && (A->cols16 ? rows_per_tile < 400000 : cg->opt.tiles > 8);
+                cg->opt.tiles > 1 &&
+                (A->cols16 ? rows_per_tile < 400000 || (cg->opt.tiles >= 32 && rows_per_tile < 1000000)
+                           : cg->opt.tiles > 8);
             cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && small && !ctx->nccl_comm &&
                                        !ctx->emulated && fits && !cg->opt.use_graph
                                    ? TW_DISPATCH_PERSISTENT
@@ -384,8 +388,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             if (ctx->nccl_comm)
                 config_error("the persistent dispatcher runs without a communicator (halo and "
                              "allgathers are NCCL launches)");
-            int sb, vb;
-            if (dag_smem_bytes(A->info.max_width, &sb, &vb) > 200 * 1024)
+            int sb, vb, cb;
+            if (dag_smem_bytes(A->info.max_width, A->cols16 != nullptr, &sb, &vb, &cb) > 225 * 1024)
                 config_error("matrix rows too wide for the dispatcher's shared-memory stages");
             if (cg->opt.use_graph) config_error("the persistent dispatcher is one launch; no graph");
         } else if (cg->opt.dispatch != TW_DISPATCH_STREAMS) {
@@ -490,7 +494,7 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             TW_CUDA(cudaMalloc(&cg->d_stamps, sizeof(unsigned long long) * (max_iters + 2)));
             TW_CUDA(cudaMemset(cg->d_stamps, 0, sizeof(unsigned long long) * (max_iters + 2)));
             TW_CUDA(cudaMalloc(&cg->d_ticket, sizeof(unsigned) * 4));
-            cg->dag_grid = dag_blocks(A->info.max_width, ctx->sm_count);
+            cg->dag_grid = dag_blocks(A->info.max_width, A->cols16 != nullptr, ctx->sm_count);
         }
     } catch (...) {
         free_cg(cg);
@@ -690,7 +694,8 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.rr = cg->rrp;
     P.spmv_chunk_slices = dag_spmv_chunk_slices(cg);
     P.vec_chunk_rows = dag_vec_chunk_rows(cg);
-    dag_smem_bytes(cg->A->info.max_width, &P.stage_bytes, &P.val_bytes);
+    dag_smem_bytes(cg->A->info.max_width, P.A.cols16 != nullptr, &P.stage_bytes, &P.val_bytes,
+                   &P.c16_bytes);
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
     launch_dag(P, cg->dag_grid, s);

@@ -23,10 +23,12 @@
 // Launch overhead per task disappears (a chunk costs one atomic), and tasks
 // of consecutive iterations overlap wherever the DAG allows it.
 //
-// Coherence: p is rewritten inside the kernel (p_up) and gathered by later
-// SpMV chunks, so gathers use coherent ld.global (not the read-only path);
-// the acquire at chunk start plus a gpu-scope fence invalidates stale L1
-// lines.  The matrix stream stays on TMA (read-only for the kernel).
+// Coherence: p is rewritten inside the kernel (p_up) and read by later SpMV
+// chunks, so gathers use coherent ld.global (not the read-only path); the
+// acquire at chunk start plus a gpu-scope fence invalidates stale L1 lines.
+// On an x-staged matrix the p runs come by TMA with the slice (as in the
+// standalone K1), after a generic -> async proxy fence that orders them
+// behind that acquire.  The matrix itself is read-only for the kernel.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -99,6 +101,57 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
         int64_t s_hi = s_lo + P.spmv_chunk_slices;
         if (s_hi > s_end) s_hi = s_end;
+        if (P.A.cols16) { // x-staged matrix: the slice's x runs ride its TMA transaction
+            // p was written inside this kernel by other CTAs' generic stores
+            // (made visible by the chunk's dependency acquire); order this
+            // warp's async-proxy reads of it after that acquire
+            if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+            const double* vb = reinterpret_cast<const double*>(stage);
+            const uint16_t* cb = reinterpret_cast<const uint16_t*>(stage + P.val_bytes);
+            double* xs = reinterpret_cast<double*>(stage + P.val_bytes + P.c16_bytes);
+            constexpr uint32_t kRunBytes = kStageRunLen * 8;
+            for (int64_t s = s_lo + warp; s < s_hi; s += kComputeWarps) {
+                if (lane == 0) {
+                    const int64_t off = P.A.slice_off[s];
+                    const uint32_t ents = static_cast<uint32_t>(P.A.slice_off[s + 1] - off);
+                    *stage_w = static_cast<int>(ents >> 5);
+                    mbar_expect_tx(bar, ents * 10u + kStageRuns * kRunBytes);
+                    if (ents) {
+                        bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
+                        bulk_g2s(stage + P.val_bytes, P.A.cols16 + off, ents * 2u, bar, pol);
+                    }
+                    for (int r = 0; r < kStageRuns; ++r) {
+                        const int64_t st = stage_run_start(s, r, P.A.sx_nx, P.A.sx_ny, P.A.sx_nz,
+                                                           P.A.sx_row_off, P.A.sx_col_off);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
+                            "l"(P.p_local + st), "r"(kRunBytes), "r"(smem_u32(bar))
+                            : "memory");
+                    }
+                }
+                __syncwarp();
+                mbar_wait(bar, phase & 1u);
+                ++phase;
+                const int w = *stage_w;
+                double acc;
+                switch (w) {
+                case 27: acc = staged_row_fixed<27>(vb, cb, xs, lane); break;
+                case 18: acc = staged_row_fixed<18>(vb, cb, xs, lane); break;
+                case 12: acc = staged_row_fixed<12>(vb, cb, xs, lane); break;
+                case 8: acc = staged_row_fixed<8>(vb, cb, xs, lane); break;
+                default: acc = staged_row_generic(vb, cb, xs, lane, w); break;
+                }
+                const int64_t row = (s << 5) + lane;
+                if (row >= T.r0 && row < T.r1) {
+                    P.Ap[row] = acc;
+                    part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc));
+                }
+                __syncwarp();
+                if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            break;
+        }
         for (int64_t s = s_lo + warp; s < s_hi; s += kComputeWarps) {
             if (lane == 0) {
                 const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
@@ -355,12 +408,15 @@ __global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(DagPar
 
 } // namespace
 
-int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes) {
+int dag_smem_bytes(int max_width, bool staged, int* stage_bytes, int* val_bytes, int* c16_bytes) {
     const int vb = ((32 * max_width * 8) + 127) / 128 * 128;
-    const int cb = ((32 * max_width * 4) + 127) / 128 * 128;
+    // x-staged: 16-bit columns and the 9 x runs; else 32-bit columns
+    const int cb = ((32 * max_width * (staged ? 2 : 4)) + 127) / 128 * 128;
+    const int xb = staged ? (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128 : 0;
     *val_bytes = vb;
-    *stage_bytes = vb + cb;
-    return kDagWarps * (vb + cb);
+    *c16_bytes = cb;
+    *stage_bytes = vb + cb + xb;
+    return kComputeWarps * *stage_bytes; // the scheduler warp has no stage
 }
 
 int dag_threads() { return kDagWarps * 32; }
@@ -369,9 +425,9 @@ int dag_compute_warps() { return kComputeWarps; }
 
 // Grid = every dispatcher CTA the device can hold at once (all CTAs must be
 // co-resident: a CTA may wait on chunks other CTAs hold).
-int dag_blocks(int max_width, int sm_count) {
-    int stage, vb;
-    const int smem = dag_smem_bytes(max_width, &stage, &vb);
+int dag_blocks(int max_width, bool staged, int sm_count) {
+    int stage, vb, cb;
+    const int smem = dag_smem_bytes(max_width, staged, &stage, &vb, &cb);
     TW_CUDA(cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
     TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, kDagWarps * 32, smem));
@@ -380,8 +436,8 @@ int dag_blocks(int max_width, int sm_count) {
 }
 
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s) {
-    int stage, vb;
-    const int smem = dag_smem_bytes(P.A.max_width, &stage, &vb);
+    int stage, vb, cb;
+    const int smem = dag_smem_bytes(P.A.max_width, P.A.cols16 != nullptr, &stage, &vb, &cb);
     dag_kernel<<<blocks, kDagWarps * 32, smem, s>>>(P);
     TW_CUDA(cudaGetLastError());
 }

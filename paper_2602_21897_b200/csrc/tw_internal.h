@@ -361,13 +361,13 @@ struct DagParams {
     double* rr;              // tile partials of r.r
     int64_t spmv_chunk_slices;
     int64_t vec_chunk_rows;
-    int stage_bytes, val_bytes;
+    int stage_bytes, val_bytes, c16_bytes; // c16_bytes: the column block (16- or 32-bit)
 };
 
-int dag_smem_bytes(int max_width, int* stage_bytes, int* val_bytes);
+int dag_smem_bytes(int max_width, bool staged, int* stage_bytes, int* val_bytes, int* c16_bytes);
 int dag_threads();
 int dag_compute_warps();
-int dag_blocks(int max_width, int sm_count);
+int dag_blocks(int max_width, bool staged, int sm_count);
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s);
 
 // Occupancy-derived launch configuration for this device.

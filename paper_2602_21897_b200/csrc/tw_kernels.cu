@@ -413,63 +413,7 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
 }
 
 // ------------------------------------------------------ K1, x staged in smem
-// One row of an x-staged slice: 16-bit columns index the slice's 9 staged
-// runs of x in shared memory, so the 27 operands are shared-memory reads of
-// data that arrived with the slice's own TMA transaction (no global gathers
-// waiting on L1 / L2).  Same per-row order and roundings as smem_row_fixed.
-template <int W>
-__device__ __forceinline__ double staged_row_fixed(const double* vb, const uint16_t* cb,
-                                                   const double* xs, int lane) {
-    uint32_t c[W];
-#pragma unroll
-    for (int q = 0; q < W / 8; ++q) {
-        const uint4 t = reinterpret_cast<const uint4*>(cb + 256 * q)[lane];
-        const uint32_t w4[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            c[8 * q + 2 * h] = w4[h] & 0xFFFFu;
-            c[8 * q + 2 * h + 1] = w4[h] >> 16;
-        }
-    }
-    constexpr int F8 = W & ~7;
-    constexpr int R = W - F8;
-    constexpr int F4 = R >= 4 ? F8 + 4 : F8;
-    if (R >= 4) {
-        const uint2 t = reinterpret_cast<const uint2*>(cb + 32 * F8)[lane];
-        c[F8] = t.x & 0xFFFFu;
-        c[F8 + 1] = t.x >> 16;
-        c[F8 + 2] = t.y & 0xFFFFu;
-        c[F8 + 3] = t.y >> 16;
-    }
-    constexpr int R2 = W - F4;
-    if (R2 >= 2) {
-        const uint32_t t = reinterpret_cast<const uint32_t*>(cb + 32 * F4)[lane];
-        c[F4] = t & 0xFFFFu;
-        c[F4 + 1] = t >> 16;
-    }
-    if (R2 & 1) c[W - 1] = cb[32 * (W - 1) + lane];
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-        const double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
-        if (c[2 * j] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(v.x, xs[c[2 * j]]));
-        if (c[2 * j + 1] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(v.y, xs[c[2 * j + 1]]));
-    }
-    if (W & 1)
-        if (c[W - 1] != kStagePad) acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane], xs[c[W - 1]]));
-    return acc;
-}
-
-__device__ __forceinline__ double staged_row_generic(const double* vb, const uint16_t* cb,
-                                                     const double* xs, int lane, int w) {
-    double acc = 0.0;
-    for (int k = 0; k < w; ++k) {
-        const uint32_t c = cb[ell_c16_pos(k, lane, w)];
-        if (c == kStagePad) break; // padding only ever trails a row
-        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], xs[c]));
-    }
-    return acc;
-}
+// (row bodies staged_row_fixed / staged_row_generic: tw_device.cuh)
 
 // Up to three row ranges walked as one index space of slices (range k's
 // slices follow range k-1's), the order launch_spmv walks its two in.
