@@ -121,26 +121,32 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // barrier extends the acquire to the block.  Call from uniform control flow.
 // A flag that stays stale for TW_PEER_TIMEOUT_NS traps (the context reports
 // an error to every later call) instead of hanging the GPU.
-static __device__ __noinline__ void block_wait_flags(const unsigned long long* flags, int count,
-                                                 unsigned long long want) {
-    if (threadIdx.x == 0) {
-        unsigned long long t0 = 0;
-        for (int i = 0; i < count; ++i) {
-            unsigned spins = 0;
-            while (ld_acquire_sys(flags + i) < want) {
-                __nanosleep(32);
-                if ((++spins & 4095u) == 0) {
-                    const unsigned long long t = global_ns();
-                    if (!t0) t0 = t;
-                    else if (t - t0 > TW_PEER_TIMEOUT_NS) {
-                        printf("tw_hpccg: peer flag %d never reached stamp %llx (has %llx)\n", i,
-                               want, ld_acquire_sys(flags + i));
-                        __trap();
-                    }
+// One thread acquire-waits until every flag reaches `want`; a flag that has
+// not after TW_PEER_TIMEOUT_NS traps (a dead peer ends the kernel with an
+// error instead of hanging the GPU).
+static __device__ __noinline__ void thread_wait_flags(const unsigned long long* flags, int count,
+                                                      unsigned long long want) {
+    unsigned long long t0 = 0;
+    for (int i = 0; i < count; ++i) {
+        unsigned spins = 0;
+        while (ld_acquire_sys(flags + i) < want) {
+            __nanosleep(32);
+            if ((++spins & 4095u) == 0) {
+                const unsigned long long t = global_ns();
+                if (!t0) t0 = t;
+                else if (t - t0 > TW_PEER_TIMEOUT_NS) {
+                    printf("tw_hpccg: peer flag %d never reached stamp %llx (has %llx)\n", i, want,
+                           ld_acquire_sys(flags + i));
+                    __trap();
                 }
             }
         }
     }
+}
+
+static __device__ __forceinline__ void block_wait_flags(const unsigned long long* flags, int count,
+                                                        unsigned long long want) {
+    if (threadIdx.x == 0) thread_wait_flags(flags, count, want);
     __syncthreads();
 }
 

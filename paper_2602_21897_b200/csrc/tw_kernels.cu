@@ -365,9 +365,7 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
     const int32_t* cb = reinterpret_cast<const int32_t*>(stage + val_bytes);
     for (int64_t k = 0; k < mine; ++k) {
         if (k == mine_i && nwait) { // first boundary slice: the ghost planes must have landed
-            if (lane == 0)
-                for (int f = 0; f < nwait; ++f)
-                    while (ld_acquire_sys(wait_flags + f) < want) __nanosleep(32);
+            if (lane == 0) thread_wait_flags(wait_flags, nwait, want);
             __syncwarp();
         }
         mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
@@ -494,8 +492,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         if (k == mine_a && nwait) {
             // first slice of space B: the neighbours' ghost planes must have
             // landed; then order the async-proxy (TMA) reads after the acquire
-            for (int f = 0; f < nwait; ++f)
-                while (ld_acquire_sys(wait_flags + f) < want) __nanosleep(32);
+            thread_wait_flags(wait_flags, nwait, want);
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (int r = 0; r < kStageRuns; ++r) {
