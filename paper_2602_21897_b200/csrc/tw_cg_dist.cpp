@@ -306,8 +306,18 @@ void group_iterate_concurrent(tw_cg** g, int P, int k, int jitter) {
         TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
         TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
     }
-    int B = rank_group_blocks_per_rank(P);
-    for (int r = 0; r < P; ++r) B = std::min(B, g[r]->maxg);
+    // x-staged slabs run the staged K1: kThreads / 32 warp stages per block
+    int wmax = 0;
+    bool staged = false;
+    for (int r = 0; r < P; ++r) {
+        staged = staged || g[r]->view().cols16 != nullptr;
+        wmax = std::max(wmax, static_cast<int>(g[r]->A->info.max_width));
+    }
+    int vb = 0, cb = 0;
+    const int stage = staged ? staged_stage_bytes(wmax, &vb, &cb) : 0;
+    const int smem = staged ? stage * (kGroupThreads / 32) : 0;
+    int B = rank_group_blocks_per_rank(P, smem);
+    for (int r = 0; r < P; ++r) B = std::min(B, staged ? g[r]->maxg / 2 : g[r]->maxg);
     if (B < 1) config_error("more ranks than co-resident blocks");
     std::vector<GroupRank> h(static_cast<size_t>(P));
     GroupRank* d = nullptr;
@@ -330,9 +340,12 @@ void group_iterate_concurrent(tw_cg** g, int P, int k, int jitter) {
         R.P = P;
         R.n = c->n; R.int_r0 = c->slab.interior_r0; R.int_r1 = c->slab.interior_r1;
         R.bar = bars + 2 * r;
+        R.stage_bytes = stage;
+        R.val_bytes = vb;
+        R.c16_bytes = cb;
     }
     TW_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(GroupRank) * P, cudaMemcpyHostToDevice, s));
-    launch_rank_group(d, P, B, k, jitter, s);
+    launch_rank_group(d, P, B, k, jitter, smem, s);
     TW_CUDA(cudaStreamSynchronize(s));
     cudaFree(d);
     cudaFree(bars);

@@ -256,10 +256,15 @@ struct GroupRank {
     int n_ghost, P;
     int64_t n, int_r0, int_r1;
     unsigned* bar; // [count, generation]
+    int stage_bytes, val_bytes, c16_bytes; // x-staged K1 stages (A.cols16 set)
 };
-int rank_group_blocks_per_rank(int nranks);
+constexpr int kGroupThreads = 256; // threads per rank-group block (= kThreads)
+// smem: dynamic shared memory per block (the staged K1's stages, or 0)
+int rank_group_blocks_per_rank(int nranks, int smem);
 void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
-                       int iterations, int jitter, cudaStream_t s);
+                       int iterations, int jitter, int smem, cudaStream_t s);
+// Per-warp stage of the x-staged K1: values, 16-bit columns, 9 x runs.
+int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes);
 // Builds the 16-bit staged columns of a stencil matrix or z-slab
 // (nx % 32 == 0; A carries sx_*) from its 32-bit columns; flags *bad if any
 // stored column falls outside its slice's staged runs (then the matrix

@@ -438,22 +438,25 @@ struct SliceSpace {
 // B's x runs wait for the warp's acquire of the ghost-plane flags when there
 // are any, and with SPLIT the two spaces keep separate p.Ap partials, so the
 // results are bit-identical to one launch per space (the NCCL transport).
-template <bool SPLIT>
-__global__ void __launch_bounds__(kTmaWarps * 32, 1)
-spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
-                       RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
-                       int c16_bytes, RedScratch rs, Fin fin, const unsigned long long* wait_flags,
-                       int nwait) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[kTmaWarps];
-    __shared__ int stage_w[kTmaWarps];
+// NW warps per block over the blocks of g; `phase` counts the waits already
+// done on the warp's barrier (a kernel that calls the body repeatedly keeps
+// it); PDL: the programmatic-launch wait sits between the first slice's
+// matrix block and its x runs.
+template <bool SPLIT, int NW, bool PDL>
+__device__ __forceinline__ void staged_spmv_body(
+    GridPos g, const EllView& A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
+    RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes, int c16_bytes, RedScratch rs,
+    const Fin& fin, const unsigned long long* wait_flags, int nwait, unsigned char* smem,
+    uint64_t* bars, int* stage_ws, uint32_t& phase) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
+    uint64_t* bar = bars + warp;
+    int* stage_w = stage_ws + warp;
     const double* vb = reinterpret_cast<const double*>(stage);
     const uint16_t* cb = reinterpret_cast<const uint16_t*>(stage + val_bytes);
     double* xs = reinterpret_cast<double*>(stage + val_bytes + c16_bytes);
-    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    const int64_t warp_g = static_cast<int64_t>(g.bid) * NW + warp;
+    const int64_t nwarps = static_cast<int64_t>(g.nblk) * NW;
     // a tile of the tasks variant may start and end inside a slice: rows
     // outside the ranges are neither written nor dotted
     const RowRange none{0, 0};
@@ -468,10 +471,6 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         rr = sp.q[w];
         return sp.slice(i, w);
     };
-    pdl_launch_dependents();
-    if (lane == 0) mbar_init(&bars[warp], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
     const uint64_t pol = l2_evict_first_policy();
     constexpr uint32_t kRunBytes = kStageRunLen * 8;
     const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
@@ -481,11 +480,11 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         const int64_t off = A.slice_off[s];
         const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
         TW_DCHECK(s >= 0 && s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
-        stage_w[warp] = static_cast<int>(ents >> 5);
-        mbar_expect_tx(&bars[warp], ents * 10u + kStageRuns * kRunBytes);
+        *stage_w = static_cast<int>(ents >> 5);
+        mbar_expect_tx(bar, ents * 10u + kStageRuns * kRunBytes);
         if (ents) {
-            bulk_g2s(stage, A.vals + off, ents * 8u, &bars[warp], pol);
-            bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, &bars[warp], pol);
+            bulk_g2s(stage, A.vals + off, ents * 8u, bar, pol);
+            bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, bar, pol);
         }
     };
     auto issue_x = [&](int64_t k, int64_t s) { // default L2 policy: neighbouring slices share runs
@@ -501,7 +500,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
-                "l"(x + st), "r"(kRunBytes), "r"(smem_u32(&bars[warp]))
+                "l"(x + st), "r"(kRunBytes), "r"(smem_u32(bar))
                 : "memory");
         }
     };
@@ -511,13 +510,14 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     int64_t s = mine > 0 ? locate(0, rr) : 0;
     if (lane == 0 && mine > 0) issue_block(s);
     __syncwarp();
-    pdl_wait();
+    if (PDL) pdl_wait();
     if (lane == 0 && mine > 0) issue_x(0, s);
     __syncwarp();
     double part_a = 0.0, part_b = 0.0;
     for (int64_t k = 0; k < mine; ++k) {
-        mbar_wait(&bars[warp], static_cast<uint32_t>(k & 1));
-        const int w = stage_w[warp];
+        mbar_wait(bar, phase & 1u);
+        ++phase;
+        const int w = *stage_w;
         double acc;
         switch (w) {
         case 27: acc = staged_row_fixed<27>(vb, cb, xs, lane); break;
@@ -544,8 +544,27 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
         }
         __syncwarp();
     }
-    if (SPLIT) grid_reduce2_finalize(part_a, part_b, rs, fin);
-    else grid_reduce_finalize(part_b, rs, fin);
+    if (SPLIT) grid_reduce2_finalize(part_a, part_b, rs, fin, g);
+    else grid_reduce_finalize(part_b, rs, fin, g);
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
+                       RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
+                       int c16_bytes, RedScratch rs, Fin fin, const unsigned long long* wait_flags,
+                       int nwait) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kTmaWarps];
+    __shared__ int stage_w[kTmaWarps];
+    pdl_launch_dependents();
+    if ((threadIdx.x & 31) == 0) mbar_init(&bars[threadIdx.x >> 5], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t phase = 0;
+    staged_spmv_body<SPLIT, kTmaWarps, true>(launch_grid(), A, x, y, ra, rb0, rb1, stage_bytes,
+                                             val_bytes, c16_bytes, rs, fin, wait_flags, nwait, smem,
+                                             bars, stage_w, phase);
 }
 
 // --------------------------------------------------------- K2 / K3 / K4 streams
@@ -787,25 +806,51 @@ __device__ __forceinline__ void group_barrier(unsigned* bar, int nblk) {
 // one GPU must never do; co-residency of the whole grid (cooperative
 // launch) makes the waits safe.  `jitter` delays rank-dependent blocks to
 // vary the interleavings.
+//
+// On an x-staged slab K1 is the staged one-launch form (interior slices,
+// then per warp: acquire of the ghost flags, proxy fence, TMA of the ghost
+// runs) with kThreads / 32 warps per block and their stages in dynamic
+// shared memory -- the pattern of the peer path's spmv_tma_staged_kernel<true>
+// under real concurrency.
 __global__ void __launch_bounds__(kThreads)
 rank_group_kernel(const GroupRank* ranks, int B, int iterations, int jitter) {
+    static_assert(kThreads == kGroupThreads, "host sizes the group's stages by kGroupThreads");
+    constexpr int kW = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char gsmem[];
+    __shared__ uint64_t gbars[kW];
+    __shared__ int gstage_w[kW];
     const int rk = blockIdx.x / B;
     const GridPos g{static_cast<int>(blockIdx.x % B), B};
     const GroupRank& R = ranks[rk];
     const RowRange all{0, 0};
+    const bool staged = R.A.cols16 != nullptr;
+    if (staged && (threadIdx.x & 31) == 0) mbar_init(&gbars[threadIdx.x >> 5], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    uint32_t phase = 0;
     for (int it = 0; it < iterations; ++it) {
         if (jitter && threadIdx.x == 0 && g.bid == (it * 7 + rk * 3) % B)
             __nanosleep(static_cast<unsigned>(((it + 1) * (rk + 1) * 977) % 20000));
-        // K1 interior rows (no ghost plane), partial into pm[0]
-        spmv_rows<true, kGatherCA>(g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, all, R.rs,
-                               Fin{FIN_STORE, R.pm, nullptr, nullptr, nullptr, nullptr}, nullptr, 0);
-        group_barrier(R.bar, B);
-        // K1 boundary rows after the ghost flags; publish (0 + pm[0]) + pm[1]
-        spmv_rows<true, kGatherCG>(g, R.A, R.p_local, R.Ap, RowRange{0, R.int_r0},
-                                   RowRange{R.int_r1, R.n}, R.rs,
-                               Fin{FIN_PUBLISH_A, R.pm + 1, R.sc, nullptr, R.links, R.pm},
-                               R.ghost_flags, R.n_ghost);
-        group_barrier(R.bar, B);
+        if (staged) {
+            staged_spmv_body<true, kW, false>(
+                g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, RowRange{0, R.int_r0},
+                RowRange{R.int_r1, R.n}, R.stage_bytes, R.val_bytes, R.c16_bytes, R.rs,
+                Fin{FIN_PUBLISH_A, R.pm + 1, R.sc, nullptr, R.links, R.pm}, R.ghost_flags,
+                R.n_ghost, gsmem, gbars, gstage_w, phase);
+            group_barrier(R.bar, B);
+        } else {
+            // K1 interior rows (no ghost plane), partial into pm[0]
+            spmv_rows<true, kGatherCA>(g, R.A, R.p_local, R.Ap, RowRange{R.int_r0, R.int_r1}, all,
+                                       R.rs, Fin{FIN_STORE, R.pm, nullptr, nullptr, nullptr, nullptr},
+                                       nullptr, 0);
+            group_barrier(R.bar, B);
+            // K1 boundary rows after the ghost flags; publish (0 + pm[0]) + pm[1]
+            spmv_rows<true, kGatherCG>(g, R.A, R.p_local, R.Ap, RowRange{0, R.int_r0},
+                                       RowRange{R.int_r1, R.n}, R.rs,
+                                       Fin{FIN_PUBLISH_A, R.pm + 1, R.sc, nullptr, R.links, R.pm},
+                                       R.ghost_flags, R.n_ghost);
+            group_barrier(R.bar, B);
+        }
 #ifdef TW_BREAK_PEER_WAIT // negative control of the concurrency test only
         update_xr_rows(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
                        ScalarSrc{R.win->recv_a, R.P, nullptr}, R.rs,
@@ -994,21 +1039,23 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
     TW_CUDA(cudaGetLastError());
 }
 
-int rank_group_blocks_per_rank(int nranks) {
+int rank_group_blocks_per_rank(int nranks, int smem) {
     int occ = 0, dev = 0, sms = 0;
-    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rank_group_kernel, kThreads, 0));
+    TW_CUDA(cudaFuncSetAttribute(rank_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem));
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rank_group_kernel, kThreads, smem));
     TW_CUDA(cudaGetDevice(&dev));
     TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     return occ * sms / nranks;
 }
 
 void launch_rank_group(const GroupRank* ranks_dev, int nranks, int blocks_per_rank,
-                       int iterations, int jitter, cudaStream_t s) {
+                       int iterations, int jitter, int smem, cudaStream_t s) {
     int B = blocks_per_rank, it = iterations;
     void* args[] = {&ranks_dev, &B, &it, &jitter};
     TW_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(rank_group_kernel),
                                         dim3(static_cast<unsigned>(nranks * B)), dim3(kThreads),
-                                        args, 0, s));
+                                        args, static_cast<size_t>(smem), s));
 }
 
 bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
@@ -1049,7 +1096,7 @@ bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange in
     return true;
 }
 
-static int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
+int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
     *val_bytes = ((32 * max_width * 8) + 127) / 128 * 128;
     *c16_bytes = ((32 * max_width * 2) + 127) / 128 * 128;
     return *val_bytes + *c16_bytes + (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;

@@ -701,15 +701,19 @@ def test_spmv_generic_widths_tma_and_register_paths(rt, orc, maxw):
 
 
 @pytest.mark.parametrize("dims,P_", [((32, 32, 32), 2), ((40, 24, 30), 3), ((32, 32, 32), 4),
-                                     ((24, 20, 16), 8), ((23, 17, 12), 3)])
+                                     ((24, 20, 16), 8), ((23, 17, 12), 3), ((64, 24, 40), 4),
+                                     ((32, 8, 32), 8)])
 def test_peer_transport_under_concurrency(orc, golden, dims, P_):
     """The peer protocol with the ranks really running at the same time:
     tw_cg_group_iterate_concurrent runs all P ranks as one cooperative
     kernel whose rank groups spin on one another's flags (stamps, rank-order
     partial sums, fused halo stores), with and without rank-dependent
-    delays, interleaved with host-sequenced iterations and a re-solve."""
+    delays, interleaved with host-sequenced iterations and a re-solve.
+    Slabs with nx % 32 == 0 are x-staged: their K1 stages the ghost runs by
+    TMA only after each warp's flag acquire and a proxy fence."""
     m = orc.stencil(*dims)
     G = P.EmulatedRankGroup(*dims, P_, 60, transport="peer")
+    assert all(A.x_staged == (dims[0] % 32 == 0) for A in G.mats)
     for seed in (7, 2):
         b = orc.rhs_xorshift(m.n, seed)
         want_h, want_x, _ = orc.cg(m, b, 60)
