@@ -464,7 +464,13 @@ __device__ __forceinline__ void staged_spmv_body(
     const SliceSpace sb(SPLIT ? rb0 : ra, SPLIT ? rb1 : rb0, SPLIT ? none : rb1);
     auto mine_of = [&](int64_t n) { return warp_g < n ? (n - warp_g + nwarps - 1) / nwarps : int64_t(0); };
     const int64_t mine_a = mine_of(sa.n), mine = mine_a + mine_of(sb.n);
+    // one range (the single-domain CG, a tile): slice k of the warp directly
+    const bool one = !SPLIT && rb0.r1 <= rb0.r0 && rb1.r1 <= rb1.r0;
     auto locate = [&](int64_t k, RowRange& rr) {
+        if (one) {
+            rr = ra;
+            return (ra.r0 >> 5) + warp_g + k * nwarps;
+        }
         const SliceSpace& sp = k < mine_a ? sa : sb;
         const int64_t i = warp_g + (k < mine_a ? k : k - mine_a) * nwarps;
         const int w = sp.which(i);
