@@ -365,8 +365,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             // the persistent dispatcher where it wins (many tiles, one rank,
             // no graph requested; profiles/r01_sweep_summary.md), else streams
             // small tiles: on an x-staged matrix below ~400k rows per tile,
-            // or from 32 tiles up below 1M rows per tile (measured crossovers:
-            // 128^3 between 4 and 8 tiles, 256^3 between 16 and 32;
+            // or from 8 tiles up below 3M rows per tile (measured crossovers:
+            // 128^3 between 4 and 8 tiles, 256^3 at 4 tiles (a tie);
             // profiles/r01_dispatcher_summary.md); on a gather matrix, more
             // than 8 tiles
             int sb, vb, cb;
@@ -375,7 +375,7 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             const int64_t rows_per_tile = A->info.n_rows / std::max(cg->opt.tiles, 1);
             const bool small =
                 cg->opt.tiles > 1 &&
-                (A->cols16 ? rows_per_tile < 400000 || (cg->opt.tiles >= 32 && rows_per_tile < 1000000)
+                (A->cols16 ? rows_per_tile < 400000 || (cg->opt.tiles >= 8 && rows_per_tile < 3000000)
                            : cg->opt.tiles > 8);
             cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && small && !ctx->nccl_comm &&
                                        !ctx->emulated && fits && !cg->opt.use_graph
@@ -696,6 +696,12 @@ void enqueue_persistent(tw_cg* cg, int k) {
     P.vec_chunk_rows = dag_vec_chunk_rows(cg);
     dag_smem_bytes(cg->A->info.max_width, P.A.cols16 != nullptr, &P.stage_bytes, &P.val_bytes,
                    &P.c16_bytes);
+    // update chunks by TMA when the stage holds >= 128 rows of each operand
+    // (multiples of 64 rows: one 16-byte pair per lane and step)
+    const bool upd_tma = env_or("TW_DAG_UPD_TMA", 1) != 0;
+    const int ru = (P.stage_bytes / 32) & ~63, rp = (P.stage_bytes / 16) & ~63;
+    P.upd_block_rows = upd_tma && ru >= 128 ? ru : 0;
+    P.updp_block_rows = upd_tma && rp >= 128 ? rp : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
     launch_dag(P, cg->dag_grid, s);

@@ -97,6 +97,9 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
     double part = 0.0;
     switch (T.kind) {
     case DK_SPMV: {
+#ifdef TW_DAG_PROBE_SKIP_SPMV // timing probe only (wrong results): SpMV chunks do nothing
+        break;
+#endif
         const int64_t s_first = T.r0 >> 5, s_end = (T.r1 + 31) >> 5;
         const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
         int64_t s_hi = s_lo + P.spmv_chunk_slices;
@@ -189,12 +192,73 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
     }
     case DK_UPD:
     case DK_UPDP: {
+#ifdef TW_DAG_PROBE_SKIP_UPD // timing probe only (wrong results): update chunks do nothing
+        break;
+#endif
         const bool upd = T.kind == DK_UPD;
         const double alpha = upd ? P.sc->alpha : 0.0, nalpha = -alpha;
         const double beta = upd ? 0.0 : P.sc->beta;
         const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
         int64_t b = a + P.vec_chunk_rows;
         if (b > T.r1) b = T.r1;
+        const int sb = upd ? P.upd_block_rows : P.updp_block_rows;
+        if (sb > 0) {
+            // TMA path: each warp streams blocks of sb rows of its operands
+            // (x, p, r, Ap or r, p) into its stage with bulk copies -- a whole
+            // stage in flight per warp, no registers held -- and writes the
+            // results back with 128-bit stores.  Rows [a2, b2) are the
+            // 16-byte-aligned pairs; the ragged ends go scalar below.
+            if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory"); // see SpMV
+            const int64_t a2 = (a + 1) & ~int64_t(1), b2 = b & ~int64_t(1);
+            double* s0 = reinterpret_cast<double*>(stage);
+            double* s1 = s0 + sb;
+            double* s2 = s1 + sb;
+            double* s3 = s2 + sb;
+            for (int64_t q = a2 + static_cast<int64_t>(warp) * sb; q < b2;
+                 q += static_cast<int64_t>(kComputeWarps) * sb) {
+                const int rows = static_cast<int>((q + sb < b2 ? q + sb : b2) - q);
+                const uint32_t bytes = static_cast<uint32_t>(rows) * 8u;
+                if (lane == 0) {
+                    mbar_expect_tx(bar, (upd ? 4u : 2u) * bytes);
+                    if (upd) {
+                        bulk_g2s_plain(s0, P.x + q, bytes, bar);
+                        bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
+                        bulk_g2s_plain(s2, P.r + q, bytes, bar);
+                        bulk_g2s_plain(s3, P.Ap + q, bytes, bar);
+                    } else {
+                        bulk_g2s_plain(s0, P.r + q, bytes, bar);
+                        bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
+                    }
+                }
+                __syncwarp();
+                mbar_wait(bar, phase & 1u);
+                ++phase;
+                for (int i = 2 * lane; i < rows; i += 64) {
+                    if (upd) {
+                        double2 xv = *reinterpret_cast<const double2*>(s0 + i);
+                        const double2 pv = *reinterpret_cast<const double2*>(s1 + i);
+                        double2 rv = *reinterpret_cast<const double2*>(s2 + i);
+                        const double2 av = *reinterpret_cast<const double2*>(s3 + i);
+                        xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+                        xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+                        rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+                        rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+                        *reinterpret_cast<double2*>(P.x + q + i) = xv;
+                        *reinterpret_cast<double2*>(P.r + q + i) = rv;
+                        part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+                        part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+                    } else {
+                        const double2 rv = *reinterpret_cast<const double2*>(s0 + i);
+                        double2 pv = *reinterpret_cast<const double2*>(s1 + i);
+                        pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+                        pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+                        *reinterpret_cast<double2*>(P.p_owned + q + i) = pv;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+        } else {
         // pairs (2q, 2q+1) inside [a, b) with 128-bit accesses, ragged ends scalar
         const int64_t q0 = (a + 1) >> 1, q1 = b >> 1;
         // kVecUnroll pairs per thread and step, every load issued before the
@@ -250,6 +314,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 }
             }
         }
+        } // register path
         const int64_t lo = (a & 1) ? a : -1;                               // odd start
         const int64_t hi = ((b & 1) && b - 1 >= a && b - 1 != lo) ? b - 1 : -1; // odd end
         const int64_t i = ctid == 0 ? lo : (ctid == 1 ? hi : -1);

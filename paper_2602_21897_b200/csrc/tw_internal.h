@@ -367,6 +367,9 @@ struct DagParams {
     int64_t spmv_chunk_slices;
     int64_t vec_chunk_rows;
     int stage_bytes, val_bytes, c16_bytes; // c16_bytes: the column block (16- or 32-bit)
+    // rows per TMA block of the update chunks (x, p, r, Ap / r, p in the
+    // warp's stage); 0 = register path
+    int upd_block_rows, updp_block_rows;
 };
 
 int dag_smem_bytes(int max_width, bool staged, int* stage_bytes, int* val_bytes, int* c16_bytes);
