@@ -514,6 +514,12 @@ def run_ours(args, dist, rank, world, local):
             return tr.get("dram_bytes_per_launch") if ok else None
 
         traffic = traffic_of("k1")
+        # the library moves the x update (x += alpha p_old) from K2 into K3
+        # from 4M rows per rank (tw_cg.cpp x_in_k3; TW_X_IN_K3 forces it):
+        # K2 then streams 24 n bytes and K3 40 n, 8 n less per iteration
+        xe = os.environ.get("TW_X_IN_K3")
+        xk3 = variant == 0 and not fused and (xe == "1" if xe is not None else n >= (1 << 22))
+        k2_alg, k3_alg = (24 * n, 40 * n) if xk3 else (48 * n, 24 * n)
         roofline = {"bound": "hbm", "kernel": kname,
                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": traffic, "algorithmic_bytes": k1_bytes,
@@ -525,11 +531,12 @@ def run_ours(args, dist, rank, world, local):
                     "kernel_timing": (f"separate timed pass of {nt} iterations with events around "
                                       f"each kernel: {kt_pass_ms / nt:.4f} ms/iteration there, "
                                       f"{ms_max / K:.4f} in the event-free headline"),
-                    "k2_update_xr_gbs": 48 * n / (k2_ms / nt / 1e3) / 1e9,
-                    "k3_update_p_gbs": 24 * n / (k3_ms / k3_launches / 1e3) / 1e9,
+                    "x_update_in": "K3" if xk3 else "K2",
+                    "k2_update_xr_gbs": k2_alg / (k2_ms / nt / 1e3) / 1e9,
+                    "k3_update_p_gbs": k3_alg / (k3_ms / k3_launches / 1e3) / 1e9,
                     "k3_launches": k3_launches,
-                    "k2_traffic": traffic_of("k2"), "k2_algorithmic_bytes": 48 * n,
-                    "k3_traffic": traffic_of("k3"), "k3_algorithmic_bytes": 24 * n}
+                    "k2_traffic": traffic_of("k2"), "k2_algorithmic_bytes": k2_alg,
+                    "k3_traffic": traffic_of("k3"), "k3_algorithmic_bytes": k3_alg}
         if world == 1:
             rb = read_bandwidth(torch, torch.device("cuda", local))
             roofline["read_stream_gbs"] = rb
@@ -538,7 +545,8 @@ def run_ours(args, dist, rank, world, local):
     roofline_iter = {"bound": "hbm", "achieved": iter_gbs, "peak": peak * world, "unit": "GB/s",
                      "frac": iter_gbs / (peak * world), "algorithmic_bytes_per_iter": total_bytes}
     if roofline and roofline.get("format_bytes") != k1_bytes:
-        fb = (bytes_it - k1_bytes + roofline["format_bytes"]) * world
+        fb = (bytes_it - k1_bytes + roofline["format_bytes"]
+              - (8 * n if roofline.get("x_update_in") == "K3" else 0)) * world
         roofline_iter["format_bytes_per_iter"] = fb
         roofline_iter["achieved_format"] = fb / (ms_max / 1e3 / K) / 1e9
         roofline_iter["frac_format"] = roofline_iter["achieved_format"] / (peak * world)

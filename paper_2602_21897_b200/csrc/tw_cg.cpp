@@ -34,6 +34,19 @@ namespace cgi {
 // (TW_PDL=1).  It helped the gather K1 in streams mode (0.138 -> 0.132 ms at
 // 128^3) but costs the x-staged K1 5 % at 256^3 (0.929 vs 0.883 ms): the
 // successor's early blocks share the SMs with K1's CTAs.
+// The x update (x += alpha p_old) in K3 instead of K2: K3 reads p_old
+// anyway, so the iteration moves 8 n bytes less from DRAM once the vectors
+// no longer sit in L2 (measured, event-timed K2 + K3: 256^3 197.5 -> 179.7 us,
+// 128^3 29.0 -> 29.6 us), hence from 4M rows per rank.  TW_X_IN_K3=0 / 1
+// forces it off / on (A/B).
+bool x_in_k3(const tw_cg* cg) {
+    static const int mode = [] {
+        const char* e = std::getenv("TW_X_IN_K3");
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
+    }();
+    return mode < 0 ? cg->n >= (int64_t(1) << 22) : mode == 1;
+}
+
 bool use_pdl() {
     static const bool on = [] {
         const char* e = std::getenv("TW_PDL");
@@ -130,12 +143,14 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
                         nullptr, 0, pdl);
         }
         record(tmark(cg, 1), s);
-        launch_update_xr(0, cg->n, cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc, ScalarSrc{nullptr, 0},
-                         rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv, s, pdl);
+        const bool xk3 = !fuse && x_in_k3(cg); // the fused chain has no K3 to carry x
+        launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc,
+                         ScalarSrc{nullptr, 0}, rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv,
+                         s, pdl);
         record(tmark(cg, 2), s);
         if (!fuse || i == k - 1) {
             launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p_cur, pdl);
+                            cg->history, bv, s, nullptr, cg->p_cur, pdl, xk3 ? cg->x : nullptr);
             cg->p_cur = cg->p_owned;
         }
         record(tmark(cg, 3), s);

@@ -71,14 +71,15 @@ void dist_spmv_boundary(tw_cg* cg, cudaStream_t s) { // the ghost-reading planes
 }
 
 void dist_update_xr(tw_cg* cg, cudaStream_t s) { // alpha from the rank partials, local r.r
-    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+    launch_update_xr(0, cg->n, x_in_k3(cg) ? nullptr : cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                      ScalarSrc{cg->recv_a, cg->P}, cg->slot(0),
                      Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, launch_blocks(cg, false), s);
 }
 
 void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; commit
     launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, cg->slot(0),
-                    cg->history, launch_blocks(cg, false), s);
+                    cg->history, launch_blocks(cg, false), s, nullptr, nullptr, false,
+                    x_in_k3(cg) ? cg->x : nullptr);
 }
 
 // Phases of the peer transport (NVLink stores + flags, fused into the
@@ -128,7 +129,7 @@ void peer_spmv(tw_cg* cg, cudaStream_t s) {
 }
 
 void peer_update_xr(tw_cg* cg, cudaStream_t s) {
-    launch_update_xr(0, cg->n, cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+    launch_update_xr(0, cg->n, x_in_k3(cg) ? nullptr : cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                      ScalarSrc{cg->win->recv_a, cg->P, cg->win->flag_a}, cg->slot(0),
                      Fin{FIN_PUBLISH_B, cg->send_b, cg->sc, nullptr, cg->d_links, nullptr},
                      launch_blocks(cg, false), s, use_pdl());
@@ -137,7 +138,8 @@ void peer_update_xr(tw_cg* cg, cudaStream_t s) {
 void peer_update_p(tw_cg* cg, cudaStream_t s) {
     launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
                     ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
-                    launch_blocks(cg, false), s, cg->d_links, nullptr, use_pdl());
+                    launch_blocks(cg, false), s, cg->d_links, nullptr, use_pdl(),
+                    x_in_k3(cg) ? cg->x : nullptr);
 }
 
 void alloc_window(tw_cg* cg) {

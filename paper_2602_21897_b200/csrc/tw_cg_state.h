@@ -113,6 +113,7 @@ namespace cgi {
 
 // tw_cg.cpp
 bool use_pdl();
+bool x_in_k3(const tw_cg* cg);
 void build_schedule(tw_cg* cg);
 int launch_blocks(const tw_cg* cg, bool spmv);
 cudaEvent_t tmark(tw_cg* cg, int k);

@@ -211,18 +211,20 @@ struct RowRange {
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
                  const unsigned long long* wait_flags = nullptr, int nwait = 0, bool pdl = false);
-// K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.
+// K2: x += alpha p; r -= alpha Ap; r.r partial/finalize.  x == nullptr:
+// r only (K3 applies the x update, launch_update_p's x).
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
                       Fin fin, int blocks, cudaStream_t s, bool pdl = false);
-// K3: p = r + beta p (beta from sc or recomputed from partials; with
+// K3: p = r + beta p (beta from sc or recomputed from partials; with x,
+// also x += alpha p_old, alpha = sc->alpha; with
 // partials, the last block also commits rtrans/history/iter).
 // With `links` (device copy), K3 also stores the first / last owned plane
 // into the neighbours' ghost planes and its last block raises their flags.
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
-                     const double* psrc = nullptr, bool pdl = false);
+                     const double* psrc = nullptr, bool pdl = false, double* x = nullptr);
 // K1 with the previous iteration's K3 fused in (single-domain monolithic):
 // Ap = A p_new and p_new . Ap where p_new = r + beta p_old (beta = sc->beta)
 // is formed on the fly from gathers of r and p_old and stored into p_new

@@ -588,6 +588,11 @@ __device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&&
     }
 }
 
+// WX = false: K2 updates r only and the x update (x += alpha p_old) moves
+// into K3, which reads p_old anyway -- 8 n bytes less per iteration, same
+// roundings (x feeds nothing inside the iteration); with alpha from rank
+// partials block 0 leaves it in sc->alpha for K3.
+template <bool WX>
 __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1,
                                                double* __restrict__ x, const double* __restrict__ p,
                                                double* __restrict__ r, const double* __restrict__ Ap,
@@ -602,9 +607,29 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
     else
         alpha = sc ? sc->alpha : __ldcg(asrc.parts); // standalone op: alpha from a device scalar
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
+    if (!WX && asrc.count > 0 && g.bid == 0 && threadIdx.x == 0) sc->alpha = alpha;
     double part = 0.0;
     for_pairs(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
-        if (lo && hi) {
+        if (!WX) {
+            if (lo && hi) {
+                double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
+                const double2 av = __ldcs(reinterpret_cast<const double2*>(Ap + e));
+                rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+                rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+                __stcs(reinterpret_cast<double2*>(r + e), rv);
+                part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+                part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (!(h == 0 ? lo : hi)) continue;
+                    const int64_t i = e + h;
+                    const double rv = __dadd_rn(r[i], __dmul_rn(nalpha, Ap[i]));
+                    r[i] = rv;
+                    part = __dadd_rn(part, __dmul_rn(rv, rv));
+                }
+            }
+        } else if (lo && hi) {
             double2 xv = __ldcs(reinterpret_cast<const double2*>(x + e));
             double2 pv = __ldcs(reinterpret_cast<const double2*>(p + e));
             double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
@@ -632,23 +657,33 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
     grid_reduce_finalize(part, rs, fin, g);
 }
 
+template <bool WX>
 __global__ void __launch_bounds__(kThreads)
 update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
                  double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
                  ScalarSrc asrc, RedScratch rs, Fin fin) {
-    update_xr_rows(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
+    update_xr_rows<WX>(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
 }
 
 // K3's streaming loop over [a0, b0): p = r + beta psrc, two pairs per
 // thread and step.  U: compiler unroll of that loop on top (measured: 4 for
 // the lean kernel, 2 in the peer instantiation, where 3+ costs registers).
-template <int U>
+#ifndef TW_K3X_UNROLL
+#define TW_K3X_UNROLL 4 // lean K3 with the x update (126 registers; 1.5 % faster than 2)
+#endif
+// WX: also x += alpha p_old (the x update moved out of K2).
+template <int U, bool WX>
 __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, int64_t stride,
                                          const double* __restrict__ r,
                                          const double* __restrict__ psrc, double* __restrict__ p,
-                                         double beta) {
+                                         double beta, double* __restrict__ x, double alpha) {
     const int64_t a = (a0 + 1) & ~int64_t(1), b = b0 & ~int64_t(1);
-    auto pair = [&](int64_t e, double2 rv, double2 pv) {
+    auto pair = [&](int64_t e, double2 rv, double2 pv, double2 xv) {
+        if (WX) {
+            xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+            xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+            __stcs(reinterpret_cast<double2*>(x + e), xv);
+        }
         pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
         *reinterpret_cast<double2*>(p + e) = pv;
@@ -659,16 +694,21 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
         const bool two = e1 < b;
         const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
         const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
-        double2 r1 = make_double2(0.0, 0.0), p1 = r1;
+        double2 r1 = make_double2(0.0, 0.0), p1 = r1, x0 = r1, x1 = r1;
+        if (WX) x0 = __ldcs(reinterpret_cast<const double2*>(x + e0));
         if (two) {
             r1 = __ldcs(reinterpret_cast<const double2*>(r + e1));
             p1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
+            if (WX) x1 = __ldcs(reinterpret_cast<const double2*>(x + e1));
         }
-        pair(e0, r0, p0);
-        if (two) pair(e1, r1, p1);
+        pair(e0, r0, p0, x0);
+        if (two) pair(e1, r1, p1, x1);
     }
     if (tid == 0) {
-        auto one = [&](int64_t i) { p[i] = __dadd_rn(r[i], __dmul_rn(beta, psrc[i])); };
+        auto one = [&](int64_t i) {
+            if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
+            p[i] = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
+        };
         if ((a0 & 1) && a0 < b0) one(a0);
         if (b < b0 && b >= a0 && b >= a) one(b);
     }
@@ -676,18 +716,20 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
 
 // PEER: the peer-transport instantiation (flag wait, fused halo stores);
 // the plain one stays lean so the grid keeps its full occupancy.
-template <bool PEER>
+template <bool PEER, bool WX>
 __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
                                               const double* __restrict__ r, double* __restrict__ p,
                                               CgScalars* sc, ScalarSrc bsrc, RedScratch rs,
                                               double* history, const PeerLinks* links_,
-                                              const double* __restrict__ psrc) {
+                                              const double* __restrict__ psrc,
+                                              double* __restrict__ x) {
     // psrc: p_old, == p in place (each element is read, then written, by the
     // same thread, so the restrict-qualified aliasing is never observable)
     const PeerLinks* links = PEER ? links_ : nullptr;
     pdl_launch_dependents();
     pdl_wait(); // r and beta come from K2
     double beta, rr = 0.0;
+    const double alpha = WX ? sc->alpha : 0.0; // this iteration's (K1 / K2 left it there)
     unsigned long long next = 0; // flag stamp of the next iteration (peer ghost flags)
     if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
@@ -720,7 +762,8 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // step (both pairs' loads issued before either store: twice the bytes in
     // flight of a one-pair loop); the at most two ragged ends go scalar.
     auto stream = [&](int64_t a0, int64_t b0) {
-        p_stream<PEER ? 2 : 4>(a0, b0, tid, stride, r, psrc, p, beta);
+        p_stream<PEER ? 2 : (WX ? TW_K3X_UNROLL : 4), WX>(a0, b0, tid, stride, r, psrc, p, beta, x,
+                                                           alpha);
     };
     if (!links) {
         stream(i0, i1);
@@ -749,6 +792,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     for (int64_t k = etid; k < nedge; k += estride) {
         const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
         TW_DCHECK(i >= i0 && i < i1);
+        if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
         const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
         p[i] = v;
         if (lo_dst && i - i0 < plane) lo_dst[i - i0] = v;
@@ -766,12 +810,12 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     }
 }
 
-template <bool PEER>
+template <bool PEER, bool WX>
 __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
-                const PeerLinks* links, const double* __restrict__ psrc) {
-    update_p_rows<PEER>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc);
+                const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x) {
+    update_p_rows<PEER, WX>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x);
 }
 
 // ------------------------------------------- concurrent rank group (1 GPU)
@@ -858,17 +902,17 @@ rank_group_kernel(const GroupRank* ranks, int B, int iterations, int jitter) {
             group_barrier(R.bar, B);
         }
 #ifdef TW_BREAK_PEER_WAIT // negative control of the concurrency test only
-        update_xr_rows(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
-                       ScalarSrc{R.win->recv_a, R.P, nullptr}, R.rs,
+        update_xr_rows<false>(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
+                              ScalarSrc{R.win->recv_a, R.P, nullptr}, R.rs,
 #else
-        update_xr_rows(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
-                       ScalarSrc{R.win->recv_a, R.P, R.win->flag_a}, R.rs,
+        update_xr_rows<false>(g, 0, R.n, R.x, R.p_owned, R.r, R.Ap, R.sc,
+                              ScalarSrc{R.win->recv_a, R.P, R.win->flag_a}, R.rs,
 #endif
                        Fin{FIN_PUBLISH_B, R.send_b, R.sc, nullptr, R.links, nullptr});
         group_barrier(R.bar, B);
-        update_p_rows<true>(g, 0, R.n, R.r, R.p_owned, R.sc,
-                            ScalarSrc{R.win->recv_b, R.P, R.win->flag_b}, R.rs, R.history, R.links,
-                            R.p_owned);
+        update_p_rows<true, true>(g, 0, R.n, R.r, R.p_owned, R.sc,
+                                  ScalarSrc{R.win->recv_b, R.P, R.win->flag_b}, R.rs, R.history,
+                                  R.links, R.p_owned, R.x);
         group_barrier(R.bar, B);
     }
 }
@@ -945,7 +989,7 @@ __global__ void rhs_xorshift_kernel(const uint64_t* states, int64_t chunk, int64
 LaunchCfg query_launch_cfg(int sm_count) {
     int occ_spmv = 0, occ_stream = 0;
     TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_spmv, spmv_kernel<true>, kThreads, 0));
-    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_stream, update_xr_kernel, kThreads, 0));
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_stream, update_xr_kernel<true>, kThreads, 0));
     LaunchCfg c;
     c.spmv_blocks = sm_count * (occ_spmv > 0 ? occ_spmv : 1);
     c.stream_blocks = sm_count * (occ_stream > 0 ? occ_stream : 1);
@@ -1175,34 +1219,44 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
                       const double* Ap, CgScalars* sc, ScalarSrc asrc, RedScratch rs, Fin fin,
                       int blocks, cudaStream_t s, bool pdl) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
-    launch_k(update_xr_kernel, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap, sc, asrc, rs,
-             fin);
+    if (x)
+        launch_k(update_xr_kernel<true>, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap, sc,
+                 asrc, rs, fin);
+    else
+        launch_k(update_xr_kernel<false>, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap,
+                 sc, asrc, rs, fin);
     TW_CUDA(cudaGetLastError());
 }
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
-                     cudaStream_t s, const PeerLinks* links, const double* psrc, bool pdl) {
+                     cudaStream_t s, const PeerLinks* links, const double* psrc, bool pdl,
+                     double* x) {
     // grid: at most one resident wave of this instantiation (a partial
     // second wave of a grid-stride loop would double the tail)
     const bool peer = links != nullptr || bsrc.flags != nullptr;
-    auto kern = peer ? update_p_kernel<true> : update_p_kernel<false>;
+    const int which = (peer ? 2 : 0) + (x ? 1 : 0);
+    using K = decltype(&update_p_kernel<false, false>);
+    static const K kerns[4] = {update_p_kernel<false, false>, update_p_kernel<false, true>,
+                               update_p_kernel<true, false>, update_p_kernel<true, true>};
     // resident blocks per SM of each instantiation (thread-safe one-time init;
     // the grid multiplies by this device's SM count)
-    auto occupancy = [](auto k) {
+    auto occupancy = [](K k) {
         int o = 0;
-        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, kThreads, 0));
+        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, reinterpret_cast<const void*>(k),
+                                                              kThreads, 0));
         return o > 0 ? o : 1;
     };
-    static const int occ_plain = occupancy(update_p_kernel<false>);
-    static const int occ_peer = occupancy(update_p_kernel<true>);
+    static const int occ[4] = {occupancy(kerns[0]), occupancy(kerns[1]), occupancy(kerns[2]),
+                               occupancy(kerns[3])};
     int dev = 0, sms = 0;
     TW_CUDA(cudaGetDevice(&dev));
     TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int wave = (peer ? occ_peer : occ_plain) * sms;
+    const int wave = occ[which] * sms;
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
-    launch_k(kern, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history, links,
-             psrc ? psrc : p);
+    if (x && !sc) throw Error(TW_ERR_CONTRACT, "the fused x update needs the solver's scalars");
+    launch_k(kerns[which], dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history,
+             links, psrc ? psrc : p, x);
     TW_CUDA(cudaGetLastError());
 }
 

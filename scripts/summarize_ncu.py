@@ -71,8 +71,21 @@ summarize(rep, "spmv_tma_staged_kernel (K1, x-staged)" if _staged else "spmv_tma
           12 * NNZ + 16 * N, "profiles/k1_traffic.json",
           format_bytes=(10 * NNZ + 16 * N) if _staged else None)
 base = os.path.dirname(rep)
-for name, kern, alg in (("prof_k2.ncu-rep", "update_xr_kernel (K2)", 48 * N),
-                        ("prof_k3.ncu-rep", "update_p_kernel<false> (K3)", 24 * N)):
+
+
+def _name_of(path):  # demangled kernel name of a one-kernel capture
+    t = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                       text=True).stdout
+    return t.split("\n", 3)[2] if t.count("\n") > 2 else ""
+
+
+# from 4M rows the x update runs in K3 (update_xr_kernel<false> streams
+# r, Ap -> r: 24 n; update_p_kernel<false, true> r, p, x -> p, x: 40 n)
+_xk3 = "update_xr_kernel<0>" in _name_of(os.path.join(base, "prof_k2.ncu-rep"))
+for name, kern, alg in (("prof_k2.ncu-rep", "update_xr_kernel (K2%s)" % (", r only" if _xk3 else ""),
+                         (24 if _xk3 else 48) * N),
+                        ("prof_k3.ncu-rep", "update_p_kernel<false%s> (K3)" % (", true" if _xk3 else ""),
+                         (40 if _xk3 else 24) * N)):
     if os.path.exists(os.path.join(base, name)):
         summarize(os.path.join(base, name), kern, alg,
                   f"profiles/{name.split('_')[1].split('.')[0]}_traffic.json")
