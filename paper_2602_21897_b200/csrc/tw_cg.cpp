@@ -39,12 +39,11 @@ namespace cgi {
 // no longer sit in L2 (measured, event-timed K2 + K3: 256^3 197.5 -> 179.7 us,
 // 128^3 29.0 -> 29.6 us), hence from 4M rows per rank.  TW_X_IN_K3=0 / 1
 // forces it off / on (A/B).
-bool x_in_k3(const tw_cg* cg) {
-    static const int mode = [] {
-        const char* e = std::getenv("TW_X_IN_K3");
-        return e ? (e[0] == '0' ? 0 : 1) : -1;
-    }();
-    return mode < 0 ? cg->n >= (int64_t(1) << 22) : mode == 1;
+bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
+
+static bool decide_x_in_k3(int64_t n) { // at solver creation
+    const char* e = std::getenv("TW_X_IN_K3");
+    return e ? e[0] != '0' : n >= (int64_t(1) << 22);
 }
 
 bool use_pdl() {
@@ -464,6 +463,7 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
                         f && f[0] == '1'; // opt-in: measured slower
             if (cg->fusep) TW_CUDA(cudaMalloc(&cg->p_alt, sizeof(double) * (n + 2)));
         }
+        cg->x_k3 = decide_x_in_k3(n);
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
         TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
         const int T = cg->T, P = cg->P;

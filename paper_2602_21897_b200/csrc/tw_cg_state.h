@@ -67,6 +67,7 @@ struct tw_cg {
     // (launch_spmv_fusep) with p ping-ponging between p_owned and p_alt;
     // every tw_cg_iterate call starts and ends with p in p_owned
     bool fusep = false;
+    bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
     double* p_alt = nullptr;
     double* p_cur = nullptr;
     int enqueued = 0;

@@ -945,3 +945,32 @@ def test_x_staged_slabs_multi_rank(orc, dims, P_, monkeypatch):
     for stage in ("1", "0"):
         (h0, x0), (h1, x1) = out[stage, "loopback"], out[stage, "peer"]
         assert np.array_equal(h0, h1) and np.array_equal(x0, x1)
+
+
+@pytest.mark.parametrize("where", ["mono", "mono_graph", "loopback", "peer"])
+def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
+    """From 4M rows per rank the x update (x += alpha p_old) runs in K3, which
+    reads p_old anyway, instead of K2.  x feeds nothing inside the iteration
+    and keeps its roundings, so histories and x must be bit-identical to the
+    K2 placement (TW_X_IN_K3 forces either at solver creation), on the
+    single-domain CG and on both multi-rank transports."""
+    dims = (64, 40, 36)
+    b = orc.rhs_xorshift(int(np.prod(dims)), 6)
+    out = []
+    for xk3 in ("1", "0"):
+        monkeypatch.setenv("TW_X_IN_K3", xk3)
+        if where.startswith("mono"):
+            A = P.gen_stencil_matrix(*dims, rt=rt)
+            res = P.cg_monolithic(rt, A, b, 35, P.CgOptions(use_graph=where == "mono_graph"))
+            out.append((res.residual_history, res.x))
+        else:
+            G = P.EmulatedRankGroup(*dims, 3, 35, transport=where)
+            G.set_rhs(b)
+            G.iterate(20)
+            G.iterate(15)
+            out.append((G.history(35)[0], G.solution()))
+            G.close()
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 35)
+    check_history(out[0][0], want_h)
+    assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
