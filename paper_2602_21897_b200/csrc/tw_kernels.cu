@@ -575,12 +575,17 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
 
 // --------------------------------------------------------- K2 / K3 / K4 streams
 
+#ifndef TW_PAIRS_UNROLL
+#define TW_PAIRS_UNROLL 1
+#endif
+constexpr int kPairsUnroll = TW_PAIRS_UNROLL;
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
 // 128-bit accesses, the (at most two) ragged ends go scalar.
 template <typename F>
 __device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&& f) {
     const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
     const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
+#pragma unroll kPairsUnroll
     for (int64_t j = j0 + static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x; j < j1;
          j += stride) {
         const int64_t e = 2 * j;
