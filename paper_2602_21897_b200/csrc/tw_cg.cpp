@@ -230,8 +230,9 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
             launch_combine(cg->recv_a, cg->P, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
         }
         break;
-    case PK_UPD:
-        launch_update_xr(cg->t_r0[t], cg->t_r1[t], cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+    case PK_UPD: // x += alpha p moves into the p update from 4M rows (x_in_k3)
+        launch_update_xr(cg->t_r0[t], cg->t_r1[t], x_in_k3(cg) ? nullptr : cg->x, cg->p_owned,
+                         cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, cg->slot(t),
                          Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}, bv, st);
         break;
@@ -246,7 +247,8 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
         break;
     case PK_UPDP:
         launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0},
-                        cg->slot(t), cg->history, bv, st);
+                        cg->slot(t), cg->history, bv, st, nullptr, nullptr, false,
+                        x_in_k3(cg) ? cg->x : nullptr);
         break;
     }
 }
@@ -714,7 +716,14 @@ void enqueue_persistent(tw_cg* cg, int k) {
     // update chunks by TMA when the stage holds >= 128 rows of each operand
     // (multiples of 64 rows: one 16-byte pair per lane and step)
     const bool upd_tma = env_or("TW_DAG_UPD_TMA", 1) != 0;
-    const int ru = (P.stage_bytes / 32) & ~63, rp = (P.stage_bytes / 16) & ~63;
+    // x update in the p-update chunks (x_in_k3): x/r chunks stream r, Ap and
+    // p chunks r, p, x; else x, p, r, Ap and r, p
+    const int rows2 = (P.stage_bytes / 16) & ~63, rows3 = (P.stage_bytes / 24) & ~63,
+              rows4 = (P.stage_bytes / 32) & ~63;
+    P.x_in_updp = upd_tma && x_in_k3(cg) && rows3 >= 128;
+    // x/r chunks keep the 4-operand block size either way: a lane's rows (and
+    // so its r.r partial) do not depend on where x is updated
+    const int ru = rows4, rp = P.x_in_updp ? rows3 : rows2;
     P.upd_block_rows = upd_tma && ru >= 128 ? ru : 0;
     P.updp_block_rows = upd_tma && rp >= 128 ? rp : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches

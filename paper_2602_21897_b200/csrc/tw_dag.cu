@@ -196,7 +196,11 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         break;
 #endif
         const bool upd = T.kind == DK_UPD;
-        const double alpha = upd ? P.sc->alpha : 0.0, nalpha = -alpha;
+        // x_in_updp: x += alpha p_old rides on the p update's read of p_old
+        // (alpha of this iteration is still in sc: the next alpha task waits
+        // for every p update of this one)
+        const bool xin = P.x_in_updp != 0;
+        const double alpha = upd || xin ? P.sc->alpha : 0.0, nalpha = -alpha;
         const double beta = upd ? 0.0 : P.sc->beta;
         const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
         int64_t b = a + P.vec_chunk_rows;
@@ -219,22 +223,34 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 const int rows = static_cast<int>((q + sb < b2 ? q + sb : b2) - q);
                 const uint32_t bytes = static_cast<uint32_t>(rows) * 8u;
                 if (lane == 0) {
-                    mbar_expect_tx(bar, (upd ? 4u : 2u) * bytes);
-                    if (upd) {
+                    mbar_expect_tx(bar, (upd ? (xin ? 2u : 4u) : (xin ? 3u : 2u)) * bytes);
+                    if (upd && xin) { // r, Ap
+                        bulk_g2s_plain(s0, P.r + q, bytes, bar);
+                        bulk_g2s_plain(s1, P.Ap + q, bytes, bar);
+                    } else if (upd) {
                         bulk_g2s_plain(s0, P.x + q, bytes, bar);
                         bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
                         bulk_g2s_plain(s2, P.r + q, bytes, bar);
                         bulk_g2s_plain(s3, P.Ap + q, bytes, bar);
-                    } else {
+                    } else { // r, p (and x)
                         bulk_g2s_plain(s0, P.r + q, bytes, bar);
                         bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
+                        if (xin) bulk_g2s_plain(s2, P.x + q, bytes, bar);
                     }
                 }
                 __syncwarp();
                 mbar_wait(bar, phase & 1u);
                 ++phase;
                 for (int i = 2 * lane; i < rows; i += 64) {
-                    if (upd) {
+                    if (upd && xin) {
+                        double2 rv = *reinterpret_cast<const double2*>(s0 + i);
+                        const double2 av = *reinterpret_cast<const double2*>(s1 + i);
+                        rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+                        rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+                        *reinterpret_cast<double2*>(P.r + q + i) = rv;
+                        part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+                        part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+                    } else if (upd) {
                         double2 xv = *reinterpret_cast<const double2*>(s0 + i);
                         const double2 pv = *reinterpret_cast<const double2*>(s1 + i);
                         double2 rv = *reinterpret_cast<const double2*>(s2 + i);
@@ -250,6 +266,12 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                     } else {
                         const double2 rv = *reinterpret_cast<const double2*>(s0 + i);
                         double2 pv = *reinterpret_cast<const double2*>(s1 + i);
+                        if (xin) {
+                            double2 xv = *reinterpret_cast<const double2*>(s2 + i);
+                            xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+                            xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+                            *reinterpret_cast<double2*>(P.x + q + i) = xv;
+                        }
                         pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
                         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
                         *reinterpret_cast<double2*>(P.p_owned + q + i) = pv;
@@ -320,12 +342,12 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         const int64_t i = ctid == 0 ? lo : (ctid == 1 ? hi : -1);
         if (i >= 0) {
             if (upd) {
-                const double xv = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
+                if (!xin) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
                 const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
-                P.x[i] = xv;
                 P.r[i] = rv;
                 part = __dadd_rn(part, __dmul_rn(rv, rv));
             } else {
+                if (xin) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
                 P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
             }
         }

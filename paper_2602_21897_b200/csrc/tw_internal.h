@@ -372,6 +372,7 @@ struct DagParams {
     // rows per TMA block of the update chunks (x, p, r, Ap / r, p in the
     // warp's stage); 0 = register path
     int upd_block_rows, updp_block_rows;
+    int x_in_updp; // x += alpha p_old in the p-update chunks (TMA path only)
 };
 
 int dag_smem_bytes(int max_width, bool staged, int* stage_bytes, int* val_bytes, int* c16_bytes);

@@ -947,13 +947,15 @@ def test_x_staged_slabs_multi_rank(orc, dims, P_, monkeypatch):
         assert np.array_equal(h0, h1) and np.array_equal(x0, x1)
 
 
-@pytest.mark.parametrize("where", ["mono", "mono_graph", "loopback", "peer"])
+@pytest.mark.parametrize("where", ["mono", "mono_graph", "loopback", "peer", "tasks",
+                                   "tasks_graph", "persistent"])
 def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
     """From 4M rows per rank the x update (x += alpha p_old) runs in K3, which
-    reads p_old anyway, instead of K2.  x feeds nothing inside the iteration
-    and keeps its roundings, so histories and x must be bit-identical to the
-    K2 placement (TW_X_IN_K3 forces either at solver creation), on the
-    single-domain CG and on both multi-rank transports."""
+    reads p_old anyway, instead of K2 (in the tasks variant: in the p-update
+    tile kernels / dispatcher chunks instead of the x/r ones).  x feeds
+    nothing inside the iteration and keeps its roundings, so histories and x
+    must be bit-identical to the K2 placement (TW_X_IN_K3 forces either at
+    solver creation), on every executor and both multi-rank transports."""
     dims = (64, 40, 36)
     b = orc.rhs_xorshift(int(np.prod(dims)), 6)
     out = []
@@ -962,6 +964,12 @@ def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
         if where.startswith("mono"):
             A = P.gen_stencil_matrix(*dims, rt=rt)
             res = P.cg_monolithic(rt, A, b, 35, P.CgOptions(use_graph=where == "mono_graph"))
+            out.append((res.residual_history, res.x))
+        elif where.startswith("tasks") or where == "persistent":
+            A = P.gen_stencil_matrix(*dims, rt=rt)
+            opt = P.CgOptions(tiles=5, use_graph=where == "tasks_graph",
+                              persistent=where == "persistent")
+            res = P.cg_tasks(rt, A, b, 35, opt)
             out.append((res.residual_history, res.x))
         else:
             G = P.EmulatedRankGroup(*dims, 3, 35, transport=where)
