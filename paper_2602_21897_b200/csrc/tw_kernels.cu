@@ -673,6 +673,9 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 // K3's streaming loop over [a0, b0): p = r + beta psrc, two pairs per
 // thread and step.  U: compiler unroll of that loop on top (measured: 4 for
 // the lean kernel, 2 in the peer instantiation, where 3+ costs registers).
+#ifndef TW_K3PX_UNROLL
+#define TW_K3PX_UNROLL 4 // the peer K3 with the x update (124 registers; 2.3 % faster than 2)
+#endif
 #ifndef TW_K3X_UNROLL
 #define TW_K3X_UNROLL 4 // lean K3 with the x update (126 registers; 1.5 % faster than 2)
 #endif
@@ -767,8 +770,8 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // step (both pairs' loads issued before either store: twice the bytes in
     // flight of a one-pair loop); the at most two ragged ends go scalar.
     auto stream = [&](int64_t a0, int64_t b0) {
-        p_stream<PEER ? 2 : (WX ? TW_K3X_UNROLL : 4), WX>(a0, b0, tid, stride, r, psrc, p, beta, x,
-                                                           alpha);
+        p_stream<PEER ? (WX ? TW_K3PX_UNROLL : 2) : (WX ? TW_K3X_UNROLL : 4), WX>(
+            a0, b0, tid, stride, r, psrc, p, beta, x, alpha);
     };
     if (!links) {
         stream(i0, i1);
