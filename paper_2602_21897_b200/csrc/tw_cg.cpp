@@ -132,17 +132,28 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
         const bool pdl = use_pdl();
         const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
+        // x-staged fused chain: the fused K1 also applies the previous
+        // iteration's x update, so K2 never touches x (the call's last K3 does)
+        const bool fuse_x = fuse && A.cols16 != nullptr;
         if (fuse && i > 0) {
             double* next = cg->p_cur == cg->p_owned ? cg->p_alt : cg->p_owned;
-            if (!launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n, rs, fa, s))
-                throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
+            const bool ok = fuse_x ? launch_spmv_staged_fusep(A, cg->r, cg->p_cur, next, cg->x,
+                                                              cg->Ap, cg->n, rs, fa, s)
+                                   : launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n,
+                                                       rs, fa, s);
+            if (!ok) throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
             cg->p_cur = next;
+        } else if (fuse_x) {
+            if (!launch_spmv_staged(A, cg->p_cur, cg->Ap, RowRange{0, cg->n}, rs, fa, s, pdl))
+                throw Error(TW_ERR_CUDA, "staged SpMV unavailable");
         } else if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, rs, fa, s, pdl)) {
             launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s,
                         nullptr, 0, pdl);
         }
         record(tmark(cg, 1), s);
-        const bool xk3 = !fuse && x_in_k3(cg); // the fused chain has no K3 to carry x
+        // x rides on K3 (x_in_k3) or on the fused K1 / the call's last K3
+        // (fuse_x); the gather fused chain keeps it in K2
+        const bool xk3 = fuse ? fuse_x : x_in_k3(cg);
         launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv,
                          s, pdl);
@@ -327,7 +338,7 @@ void free_cg(tw_cg* cg) {
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
-    cudaFree(cg->p_alt);
+    cudaFree(cg->p_alt_base);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
@@ -339,7 +350,7 @@ void free_cg(tw_cg* cg) {
     if (cg->ag_in_ev) cudaEventDestroy(cg->ag_in_ev);
     if (cg->ag_out_ev) cudaEventDestroy(cg->ag_out_ev);
     cudaFree(cg->x);
-    cudaFree(cg->r);
+    cudaFree(cg->r_base);
     cudaFree(cg->p_base);
     cudaFree(cg->Ap);
     cudaFree(cg->sc);
@@ -444,7 +455,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaSetDevice(ctx->device));
         const size_t n = static_cast<size_t>(cg->n);
         TW_CUDA(cudaMalloc(&cg->x, sizeof(double) * (n + 2)));
-        TW_CUDA(cudaMalloc(&cg->r, sizeof(double) * (n + 2)));
+        TW_CUDA(cudaMalloc(&cg->r_base, sizeof(double) * (n + 32)));
+        cg->r = cg->r_base + 16; // 128-byte aligned, slack for the fused K1's staged r runs
         TW_CUDA(cudaMalloc(&cg->Ap, sizeof(double) * (n + 2)));
         // p_owned on a 128-byte line (the streaming kernels' 128-bit accesses
         // then never straddle lines) with at least 2 doubles of slack before
@@ -458,12 +470,18 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         cg->p_cur = cg->p_owned;
         {
             const char* f = std::getenv("TW_FUSE_P");
+            const int mw = static_cast<int>(A->info.max_width);
+            const bool fits = A->cols16 ? staged_fusep_smem_bytes(mw) + 2048 <= 227 * 1024
+                                        : spmv_tma_smem_bytes(mw) + 4096 <= 227 * 1024;
             cg->fusep = cg->opt.variant == TW_CG_MONOLITHIC && !cg->dist &&
-                        cg->opt.dispatch != TW_DISPATCH_PERSISTENT && A->info.max_width > 0 &&
-                        ctx->cfg.tma_blocks > 0 &&
-                        spmv_tma_smem_bytes(A->info.max_width) + 4096 <= 227 * 1024 &&
+                        cg->opt.dispatch != TW_DISPATCH_PERSISTENT && mw > 0 &&
+                        ctx->cfg.tma_blocks > 0 && fits &&
                         f && f[0] == '1'; // opt-in: measured slower
-            if (cg->fusep) TW_CUDA(cudaMalloc(&cg->p_alt, sizeof(double) * (n + 2)));
+            if (cg->fusep) { // same slack and alignment as p_local (staged runs)
+                TW_CUDA(cudaMalloc(&cg->p_alt_base,
+                                   sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 8)));
+                cg->p_alt = cg->p_alt_base + front;
+            }
         }
         cg->x_k3 = decide_x_in_k3(n);
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));

@@ -35,7 +35,8 @@ struct tw_cg {
     unsigned epoch = 0; // set_rhs count
 
     double* x = nullptr;
-    double* r = nullptr;
+    double* r = nullptr;      // r_base + 16: 2+ doubles of slack each side (staged runs of r)
+    double* r_base = nullptr;
     double* p_base = nullptr;
     double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
     double* p_owned = nullptr;
@@ -68,7 +69,8 @@ struct tw_cg {
     // every tw_cg_iterate call starts and ends with p in p_owned
     bool fusep = false;
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
-    double* p_alt = nullptr;
+    double* p_alt = nullptr;      // p_alt_base + the same front as p_local
+    double* p_alt_base = nullptr;
     double* p_cur = nullptr;
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration

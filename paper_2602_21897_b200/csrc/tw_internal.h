@@ -290,6 +290,16 @@ inline bool launch_spmv_staged(const EllView& A, const double* x, double* y, Row
                               nullptr, 0, pdl);
 }
 int spmv_staged_smem_bytes(int max_width);
+// K1 with the previous K3 fused in, on an x-staged single-domain matrix:
+// stages the runs of r and p_old, forms p_new = r + beta p_old (sc->beta)
+// in shared memory, Ap = A p_new, p_new.Ap; stores p_new (own rows) and
+// applies x += alpha p_old (sc->alpha).  r and p_old need the staged-x
+// slack (2 doubles each side); p_new must be another buffer.  False if
+// unavailable.
+bool launch_spmv_staged_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
+                              double* x, double* Ap, int64_t n, RedScratch rs, Fin fin,
+                              cudaStream_t s);
+int staged_fusep_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only
 // trailing a row, slice widths within max_width (traps otherwise).
 void launch_ell_check(const EllView& A, cudaStream_t s);

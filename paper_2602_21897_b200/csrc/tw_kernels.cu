@@ -573,6 +573,97 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
                                              bars, stage_w, phase);
 }
 
+// K1 with the previous iteration's K3 fused in, on an x-staged matrix
+// (single-domain monolithic CG): each slice's transaction carries its
+// values, 16-bit columns and the 9 runs of BOTH r and p_old; the warp forms
+// p_new = r + beta p_old over the runs in shared memory (the roundings of
+// K3), then runs the staged row sums on p_new.  Its own rows also get
+// x += alpha p_old (the x update of the previous iteration) and p_new is
+// stored into the other p buffer.  Per iteration that drops K3's second
+// pass over r and p (the 8 n of p_new's re-read and one launch).  16 warps:
+// the larger stages (both run sets) leave room for no more.
+constexpr int kFuseWarps = 16;
+__global__ void __launch_bounds__(kFuseWarps * 32, 1)
+spmv_staged_fusep_kernel(EllView A, const double* __restrict__ p_old, const double* __restrict__ r,
+                         double* __restrict__ p_new, double* __restrict__ x,
+                         double* __restrict__ y, int64_t n, int stage_bytes, int val_bytes,
+                         int c16_bytes, RedScratch rs, Fin fin) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kFuseWarps];
+    __shared__ int stage_w[kFuseWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
+    const double* vb = reinterpret_cast<const double*>(stage);
+    const uint16_t* cb = reinterpret_cast<const uint16_t*>(stage + val_bytes);
+    double* ps = reinterpret_cast<double*>(stage + val_bytes + c16_bytes); // p_old -> p_new
+    double* rsx = ps + kStageRuns * kStageRunLen;                           // r runs
+    uint64_t* bar = &bars[warp];
+    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kFuseWarps + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFuseWarps;
+    const int64_t n_slices = (n + 31) >> 5;
+    const int64_t mine = warp_g < n_slices ? (n_slices - warp_g + nwarps - 1) / nwarps : 0;
+    if (lane == 0) mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    constexpr uint32_t kRunBytes = kStageRunLen * 8;
+    const double alpha = fin.sc->alpha, beta = fin.sc->beta; // the previous iteration's
+    auto issue = [&](int64_t s) {
+        const int64_t off = A.slice_off[s];
+        const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
+        TW_DCHECK(s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
+        stage_w[warp] = static_cast<int>(ents >> 5);
+        mbar_expect_tx(bar, ents * 10u + 2u * kStageRuns * kRunBytes);
+        if (ents) {
+            bulk_g2s(stage, A.vals + off, ents * 8u, bar, pol);
+            bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, bar, pol);
+        }
+        for (int q = 0; q < kStageRuns; ++q) {
+            const int64_t st = stage_run_start(s, q, A.sx_nx, A.sx_ny, A.sx_nz);
+            bulk_g2s_plain(ps + q * kStageRunLen, p_old + st, kRunBytes, bar);
+            bulk_g2s_plain(rsx + q * kStageRunLen, r + st, kRunBytes, bar);
+        }
+    };
+    if (lane == 0 && mine > 0) issue(warp_g);
+    __syncwarp();
+    uint32_t phase = 0;
+    double part = 0.0;
+    for (int64_t k = 0; k < mine; ++k) {
+        const int64_t s = warp_g + k * nwarps;
+        mbar_wait(bar, phase & 1u);
+        ++phase;
+        const int64_t row = (s << 5) + lane;
+        const double pold = ps[4 * kStageRunLen + 2 + lane]; // this lane's p_old[row]
+        __syncwarp();
+        for (int i = lane; i < kStageRuns * kStageRunLen; i += 32)
+            ps[i] = __dadd_rn(rsx[i], __dmul_rn(beta, ps[i])); // p_new over the runs (K3's rounding)
+        __syncwarp();
+        const int w = stage_w[warp];
+        double acc;
+        switch (w) {
+        case 27: acc = staged_row_fixed<27>(vb, cb, ps, lane); break;
+        case 18: acc = staged_row_fixed<18>(vb, cb, ps, lane); break;
+        case 12: acc = staged_row_fixed<12>(vb, cb, ps, lane); break;
+        case 8: acc = staged_row_fixed<8>(vb, cb, ps, lane); break;
+        default: acc = staged_row_generic(vb, cb, ps, lane, w); break;
+        }
+        if (row < n) {
+            const double pn = ps[4 * kStageRunLen + 2 + lane];
+            y[row] = acc;
+            p_new[row] = pn;
+            x[row] = __dadd_rn(x[row], __dmul_rn(alpha, pold));
+            part = __dadd_rn(part, __dmul_rn(pn, acc));
+        }
+        __syncwarp();
+        if (lane == 0 && k + 1 < mine) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s + nwarps);
+        }
+        __syncwarp();
+    }
+    grid_reduce_finalize(part, rs, fin);
+}
+
 // --------------------------------------------------------- K2 / K3 / K4 streams
 
 #ifndef TW_PAIRS_UNROLL
@@ -1215,6 +1306,43 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
 int spmv_staged_smem_bytes(int max_width) {
     int vb, cb;
     return kTmaWarps * staged_stage_bytes(max_width, &vb, &cb);
+}
+
+int staged_fusep_smem_bytes(int max_width) {
+    int vb, cb;
+    return kFuseWarps * (staged_stage_bytes(max_width, &vb, &cb) +
+                         (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128);
+}
+
+bool launch_spmv_staged_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
+                              double* x, double* Ap, int64_t n, RedScratch rs, Fin fin,
+                              cudaStream_t s) {
+    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
+    int vb, cb;
+    const int stage = staged_stage_bytes(A.max_width, &vb, &cb) +
+                      (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
+    const int smem = kFuseWarps * stage;
+    static std::mutex mu;
+    static int attr_bytes[64] = {};
+    int dev = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cudaFuncAttributes fa;
+        TW_CUDA(cudaFuncGetAttributes(&fa, spmv_staged_fusep_kernel));
+        if (dev >= 64 || smem + static_cast<int>(fa.sharedSizeBytes) > 227 * 1024) return false;
+        if (attr_bytes[dev] < smem) {
+            TW_CUDA(cudaFuncSetAttribute(spmv_staged_fusep_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_bytes[dev] = smem;
+        }
+    }
+    const int64_t ns = (n + 31) / 32, need = (ns + kFuseWarps - 1) / kFuseWarps;
+    const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
+    spmv_staged_fusep_kernel<<<g, kFuseWarps * 32, smem, s>>>(A, p_old, r, p_new, x, Ap, n, stage, vb,
+                                                              cb, rs, fin);
+    TW_CUDA(cudaGetLastError());
+    return true;
 }
 
 bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,

@@ -633,16 +633,20 @@ def _read_dev(rt, ptr, n):
     return out
 
 
+@pytest.mark.parametrize("dims", [(30, 20, 18), (64, 20, 18)])
 @pytest.mark.parametrize("graph", [False, True])
-def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, monkeypatch):
+def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, dims, monkeypatch):
     """Single-domain monolithic CG fuses K3 (p = r + beta p) into the next
     iteration's K1 with p ping-ponging between two buffers (opt-in,
     TW_FUSE_P=1).  Against the unfused K1/K2/K3 sequence every residual, x and the p
     left behind by each tw_cg_iterate call must be bit-identical, whatever
     the split of the iterations into calls (odd splits end in the other
-    buffer and are copied back by the final K3)."""
+    buffer and are copied back by the final K3).  On an x-staged matrix
+    (64 x 20 x 18) the fused K1 stages the runs of r and p_old, forms p_new
+    in shared memory and also carries the x update."""
     from paper_2602_21897_b200 import _native as N
-    A = P.gen_stencil_matrix(30, 20, 18, rt=rt)
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    assert A.x_staged == (dims[0] % 32 == 0)
     b = orc.rhs_xorshift(A.n, 5)
     splits = [1, 1, 3, 2, 7, 6]
     total = sum(splits)
@@ -660,12 +664,21 @@ def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, monkeypatc
         runs.append((s.history(total), s.solution(), ps))
         s.close()
     (h1, x1, p1), (h0, x0, p0) = runs
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
+    check_history(h1, want_h)
+    if A.x_staged:
+        # the staged fused K1 runs 16-warp CTAs (both run sets fill shared
+        # memory), so its p.Ap tree differs from the 18-warp K1's: same
+        # per-element roundings, results within the rule
+        check_history(h0, want_h)
+        assert np.all(rel_gap(x1, want_x) <= 1e-10) and np.all(rel_gap(x0, want_x) <= 1e-10)
+        for a, c in zip(p1, p0):
+            assert np.max(np.abs(a - c)) <= 1e-9 * np.max(np.abs(c))
+        return
     assert np.array_equal(h1, h0)
     assert np.array_equal(x1, x0)
     for a, c in zip(p1, p0):
         assert np.array_equal(a, c)
-    want_h, want_x, _ = orc.cg(orc.stencil(30, 20, 18), b, total)
-    check_history(h1, want_h)
 
 
 @pytest.mark.parametrize("maxw", [9, 33, 34, 70])
