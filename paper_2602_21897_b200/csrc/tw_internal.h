@@ -55,6 +55,10 @@ struct EllView {
     const uint16_t* cols16 = nullptr;
     int64_t sx_nx = 0, sx_ny = 0, sx_nz = 0;
     int64_t sx_row_off = 0, sx_col_off = 0;
+    // stage the x runs with an L2 evict_last hint (x up to 8M entries: it
+    // then stays in L2 across the iteration; measured 128^3 K1 -2.4 %,
+    // neutral at 256^3, profiles/r01_ab_k1_k2_k3_variants.md)
+    int sx_keep = 0;
 };
 
 // x-staged windows: run r = (dz + 1) * 3 + (dy + 1) of a slice starts 2

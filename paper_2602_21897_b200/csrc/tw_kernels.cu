@@ -442,7 +442,7 @@ struct SliceSpace {
 // done on the warp's barrier (a kernel that calls the body repeatedly keeps
 // it); PDL: the programmatic-launch wait sits between the first slice's
 // matrix block and its x runs.
-template <bool SPLIT, int NW, bool PDL>
+template <bool SPLIT, int NW, bool PDL, bool KEEP = false>
 __device__ __forceinline__ void staged_spmv_body(
     GridPos g, const EllView& A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
     RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes, int c16_bytes, RedScratch rs,
@@ -478,6 +478,7 @@ __device__ __forceinline__ void staged_spmv_body(
         return sp.slice(i, w);
     };
     const uint64_t pol = l2_evict_first_policy();
+    const uint64_t xpol = KEEP ? l2_evict_last_policy() : 0;
     constexpr uint32_t kRunBytes = kStageRunLen * 8;
     const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
     // lane 0: the slice block (values + 16-bit columns) and then its 9 x runs,
@@ -503,11 +504,10 @@ __device__ __forceinline__ void staged_spmv_body(
         for (int r = 0; r < kStageRuns; ++r) {
             const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz, A.sx_row_off,
                                                A.sx_col_off);
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
-                "l"(x + st), "r"(kRunBytes), "r"(smem_u32(bar))
-                : "memory");
+            if (KEEP) // small x: keep its lines in L2 (evict_last) for the other runs
+                bulk_g2s(xs + r * kStageRunLen, x + st, kRunBytes, bar, xpol);
+            else
+                bulk_g2s_plain(xs + r * kStageRunLen, x + st, kRunBytes, bar);
         }
     };
     // the matrix does not depend on the previous kernel: the first block
@@ -554,7 +554,7 @@ __device__ __forceinline__ void staged_spmv_body(
     else grid_reduce_finalize(part_b, rs, fin, g);
 }
 
-template <bool SPLIT>
+template <bool SPLIT, bool KEEP>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
                        RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
@@ -568,7 +568,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     uint32_t phase = 0;
-    staged_spmv_body<SPLIT, kTmaWarps, true>(launch_grid(), A, x, y, ra, rb0, rb1, stage_bytes,
+    staged_spmv_body<SPLIT, kTmaWarps, true, KEEP>(launch_grid(), A, x, y, ra, rb0, rb1, stage_bytes,
                                              val_bytes, c16_bytes, rs, fin, wait_flags, nwait, smem,
                                              bars, stage_w, phase);
 }
@@ -1251,7 +1251,7 @@ int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes) {
     return *val_bytes + *c16_bytes + (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
 }
 
-template <bool SPLIT>
+template <bool SPLIT, bool KEEP>
 static bool staged_attr(int smem) {
     static std::mutex mu;
     static int attr_bytes[64] = {};
@@ -1261,12 +1261,12 @@ static bool staged_attr(int smem) {
     std::lock_guard<std::mutex> lk(mu);
     if (static_bytes < 0) {
         cudaFuncAttributes fa;
-        TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_staged_kernel<SPLIT>));
+        TW_CUDA(cudaFuncGetAttributes(&fa, spmv_tma_staged_kernel<SPLIT, KEEP>));
         static_bytes = static_cast<int>(fa.sharedSizeBytes);
     }
     if (dev >= 64 || smem + static_bytes > 227 * 1024) return false;
     if (attr_bytes[dev] < smem) {
-        TW_CUDA(cudaFuncSetAttribute(spmv_tma_staged_kernel<SPLIT>,
+        TW_CUDA(cudaFuncSetAttribute(spmv_tma_staged_kernel<SPLIT, KEEP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_bytes[dev] = smem;
     }
@@ -1280,7 +1280,10 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
     int vb, cb;
     const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
     const int smem = kTmaWarps * stage;
-    if (!(split ? staged_attr<true>(smem) : staged_attr<false>(smem))) return false;
+    const bool keep = A.sx_keep != 0;
+    const bool attr_ok = split ? (keep ? staged_attr<true, true>(smem) : staged_attr<true, false>(smem))
+                               : (keep ? staged_attr<false, true>(smem) : staged_attr<false, false>(smem));
+    if (!attr_ok) return false;
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int64_t full = static_cast<int64_t>(A.tma_blocks) * kTmaWarps;
     int g;
@@ -1294,12 +1297,12 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
         const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
         g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
     }
-    if (split)
-        launch_k(spmv_tma_staged_kernel<true>, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y,
-                 ra, rb0, rb1, stage, vb, cb, rs, fin, wait_flags, nwait);
-    else
-        launch_k(spmv_tma_staged_kernel<false>, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x,
-                 y, ra, rb0, rb1, stage, vb, cb, rs, fin, wait_flags, nwait);
+    using K = decltype(&spmv_tma_staged_kernel<false, false>);
+    const K kern = split ? (keep ? spmv_tma_staged_kernel<true, true> : spmv_tma_staged_kernel<true, false>)
+                         : (keep ? spmv_tma_staged_kernel<false, true>
+                                 : spmv_tma_staged_kernel<false, false>);
+    launch_k(kern, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, ra, rb0, rb1, stage, vb, cb,
+             rs, fin, wait_flags, nwait);
     return true;
 }
 

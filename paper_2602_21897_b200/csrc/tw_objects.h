@@ -147,6 +147,7 @@ struct tw_ell {
             v.sx_nz = info.nz;
             v.sx_row_off = info.row_offset;
             v.sx_col_off = info.col_offset;
+            v.sx_keep = info.x_len <= (int64_t(1) << 23) ? 1 : 0;
         }
         return v;
     }
