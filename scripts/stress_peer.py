@@ -16,7 +16,10 @@ from oracle import Oracle  # noqa: E402
 
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 o = Oracle()
-cases = [((24, 20, 16), 8), ((32, 32, 32), 4), ((40, 24, 30), 3), ((64, 64, 48), 6), ((16, 16, 8), 8)]
+# nx % 32 == 0 cases run the x-staged one-launch K1 (ghost runs staged after
+# each warp's flag acquire); the others the gather K1
+cases = [((24, 20, 16), 8), ((32, 32, 32), 4), ((40, 24, 30), 3), ((64, 64, 48), 6), ((16, 16, 8), 8),
+         ((64, 24, 40), 4), ((32, 8, 32), 8), ((96, 40, 24), 3)]
 fails = 0
 for dims, ranks in cases:
     m = o.stencil(*dims)
