@@ -20,6 +20,6 @@ for nx, K in ((256, 200), (128, 600)):
     S.iterate(K)
     S.wait()
     k1, k2, k3, nt = S.kernel_times()
-    print(f"x_in_k3={os.environ.get('TW_X_IN_K3', '1')} {nx}^3 K1 {1e3 * k1 / nt:.1f} K2 {1e3 * k2 / nt:.1f} "
+    print(f"x_in_k3={os.environ.get('TW_X_IN_K3', 'auto')} {nx}^3 K1 {1e3 * k1 / nt:.1f} K2 {1e3 * k2 / nt:.1f} "
           f"K3 {1e3 * k3 / nt:.1f} K2+K3 {1e3 * (k2 + k3) / nt:.1f} us", flush=True)
     S.close()
