@@ -135,6 +135,19 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
         // x-staged fused chain: the fused K1 also applies the previous
         // iteration's x update, so K2 never touches x (the call's last K3 does)
         const bool fuse_x = fuse && A.cols16 != nullptr;
+        const bool xk3f = fuse ? fuse_x : x_in_k3(cg);
+        if (cg->fold_k2 && !fuse &&
+            launch_spmv_staged_fold_k2(A, cg->p_local, cg->Ap, cg->r, xk3f ? nullptr : cg->x,
+                                       cg->p_cur, cg->n, cg->sc, cg->history, rs, s)) {
+            record(tmark(cg, 1), s); // K1 and K2 in one launch: K2's share reads 0
+            record(tmark(cg, 2), s);
+            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                            cg->history, bv, s, nullptr, cg->p_cur, pdl, xk3f ? cg->x : nullptr);
+            cg->p_cur = cg->p_owned;
+            record(tmark(cg, 3), s);
+            if (cg->timing) ++cg->timed;
+            return;
+        }
         if (fuse && i > 0) {
             double* next = cg->p_cur == cg->p_owned ? cg->p_alt : cg->p_owned;
             const bool ok = fuse_x ? launch_spmv_staged_fusep(A, cg->r, cg->p_cur, next, cg->x,
@@ -484,6 +497,11 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             }
         }
         cg->x_k3 = decide_x_in_k3(n);
+        {
+            const char* f = std::getenv("TW_FOLD_K2");
+            cg->fold_k2 = f && f[0] == '1' && A->cols16 && !cg->dist &&
+                          cg->opt.variant == TW_CG_MONOLITHIC && !cg->fusep;
+        }
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
         TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
         const int T = cg->T, P = cg->P;
@@ -1029,6 +1047,8 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
             k = peer_k1_fused(cg) ? 3 : 4;
         } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fusep) {
             k = 2; // K1 (with the previous K3 fused in) + K2; one K3 per tw_cg_iterate call
+        } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fold_k2) {
+            k = 2; // K1 + K2 folded into one cooperative launch, K3
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;

@@ -69,6 +69,7 @@ struct tw_cg {
     // every tw_cg_iterate call starts and ends with p in p_owned
     bool fusep = false;
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
+    bool fold_k2 = false; // K1 + K2 as one cooperative launch (opt-in TW_FOLD_K2=1)
     double* p_alt = nullptr;      // p_alt_base + the same front as p_local
     double* p_alt_base = nullptr;
     double* p_cur = nullptr;

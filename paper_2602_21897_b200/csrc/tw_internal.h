@@ -123,6 +123,7 @@ struct CgScalars {
     int history_cap;
     unsigned epoch; // solve number (set_rhs count): high half of the peer flag stamps
     unsigned pad_;
+    unsigned long long alpha_stamp; // folded K1 + K2: alpha of stamp_of(sc, 0) published
 };
 
 // ------------------------------------------------- NVLink peer transport
@@ -169,7 +170,8 @@ enum FinMode : int {
     // total; v -> recv_a / recv_b [rank] of every rank's window over NVLink,
     // then the matching flags get this iteration's stamp (release, .sys)
     FIN_PUBLISH_A = 5,
-    FIN_PUBLISH_B = 6
+    FIN_PUBLISH_B = 6,
+    FIN_ALPHA_GRID = 7 // FIN_ALPHA, then release sc->alpha_stamp (the folded K1 + K2's barrier)
 };
 
 struct PeerLinks;
@@ -294,6 +296,13 @@ inline bool launch_spmv_staged(const EllView& A, const double* x, double* y, Row
                               nullptr, 0, pdl);
 }
 int spmv_staged_smem_bytes(int max_width);
+// K1 and K2 of the single-domain CG in one cooperative launch (opt-in,
+// TW_FOLD_K2=1): the x-staged K1, a grid barrier on alpha, then r -= alpha Ap
+// (and with x, x += alpha p) streamed through the warps' stages, r.r and the
+// beta commit.  False if unavailable.
+bool launch_spmv_staged_fold_k2(const EllView& A, const double* p_local, double* Ap, double* r,
+                                double* x, const double* p, int64_t n, CgScalars* sc,
+                                double* history, RedScratch rs, cudaStream_t s);
 // K1 with the previous K3 fused in, on an x-staged single-domain matrix:
 // stages the runs of r and p_old, forms p_new = r + beta p_old (sc->beta)
 // in shared memory, Ap = A p_new, p_new.Ap; stores p_new (own rows) and

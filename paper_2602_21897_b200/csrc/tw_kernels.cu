@@ -664,6 +664,91 @@ spmv_staged_fusep_kernel(EllView A, const double* __restrict__ p_old, const doub
     grid_reduce_finalize(part, rs, fin);
 }
 
+// K1 + K2 folded (opt-in): the x-staged K1 over all rows, its last block
+// publishes alpha with a release of sc->alpha_stamp, every block acquires it
+// (grid barrier: cooperative launch, one CTA per SM), then the warps stream
+// r -= alpha Ap (WX: also x += alpha p) through their stages in blocks of
+// `rows` rows and the r.r tree commits beta (FIN_BETA).
+template <bool KEEP, bool WX>
+__global__ void __launch_bounds__(kTmaWarps * 32, 1)
+spmv_staged_fold_k2_kernel(EllView A, const double* __restrict__ p_local, double* Ap,
+                           double* __restrict__ r, double* __restrict__ x,
+                           const double* __restrict__ p, int64_t n, int stage_bytes,
+                           int val_bytes, int c16_bytes, int rows, CgScalars* sc,
+                           double* history, RedScratch rs) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t bars[kTmaWarps];
+    __shared__ int stage_w[kTmaWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) mbar_init(&bars[warp], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const unsigned long long want = stamp_of(sc, 0); // iter is stable until this kernel's end
+    uint32_t phase = 0;
+    const RowRange none{0, 0};
+    staged_spmv_body<false, kTmaWarps, false, KEEP>(
+        launch_grid(), A, p_local, Ap, RowRange{0, n}, none, none, stage_bytes, val_bytes, c16_bytes,
+        rs, Fin{FIN_ALPHA_GRID, nullptr, sc, nullptr}, nullptr, 0, smem, bars, stage_w, phase);
+    __syncthreads();
+    if (threadIdx.x == 0) thread_wait_flags(&sc->alpha_stamp, 1, want);
+    __syncthreads();
+    const double alpha = __ldcg(&sc->alpha), nalpha = -alpha;
+    // Ap was stored by other CTAs' generic stores: order the TMA reads after the acquire
+    if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
+    double* s0 = reinterpret_cast<double*>(stage);
+    double* s1 = s0 + rows;
+    double* s2 = s1 + rows;
+    double* s3 = s2 + rows;
+    uint64_t* bar = &bars[warp];
+    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
+    const int64_t n2 = n & ~int64_t(1);
+    double part = 0.0;
+    for (int64_t q = warp_g * rows; q < n2; q += nwarps * rows) {
+        const int cnt = static_cast<int>(q + rows < n2 ? rows : n2 - q);
+        const uint32_t bytes = static_cast<uint32_t>(cnt) * 8u;
+        if (lane == 0) {
+            mbar_expect_tx(bar, (WX ? 4u : 2u) * bytes);
+            bulk_g2s_plain(s0, r + q, bytes, bar);
+            bulk_g2s_plain(s1, Ap + q, bytes, bar);
+            if (WX) {
+                bulk_g2s_plain(s2, x + q, bytes, bar);
+                bulk_g2s_plain(s3, p + q, bytes, bar);
+            }
+        }
+        __syncwarp();
+        mbar_wait(bar, phase & 1u);
+        ++phase;
+        for (int i = 2 * lane; i < cnt; i += 64) {
+            double2 rv = *reinterpret_cast<const double2*>(s0 + i);
+            const double2 av = *reinterpret_cast<const double2*>(s1 + i);
+            rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
+            rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
+            __stcs(reinterpret_cast<double2*>(r + q + i), rv);
+            part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
+            part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
+            if (WX) {
+                double2 xv = *reinterpret_cast<const double2*>(s2 + i);
+                const double2 pv = *reinterpret_cast<const double2*>(s3 + i);
+                xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
+                xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
+                __stcs(reinterpret_cast<double2*>(x + q + i), xv);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (n2 < n && blockIdx.x == 0 && threadIdx.x == 0) { // odd n: the last row
+        const double rv = __dadd_rn(r[n2], __dmul_rn(nalpha, __ldcg(Ap + n2)));
+        r[n2] = rv;
+        part = __dadd_rn(part, __dmul_rn(rv, rv));
+        if (WX) x[n2] = __dadd_rn(x[n2], __dmul_rn(alpha, p[n2]));
+    }
+    grid_reduce_finalize(part, rs, Fin{FIN_BETA, nullptr, sc, history});
+}
+
 // --------------------------------------------------------- K2 / K3 / K4 streams
 
 #ifndef TW_PAIRS_UNROLL
@@ -1303,6 +1388,51 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
                                  : spmv_tma_staged_kernel<false, false>);
     launch_k(kern, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, ra, rb0, rb1, stage, vb, cb,
              rs, fin, wait_flags, nwait);
+    return true;
+}
+
+bool launch_spmv_staged_fold_k2(const EllView& A, const double* p_local, double* Ap, double* r,
+                                double* x, const double* p, int64_t n, CgScalars* sc,
+                                double* history, RedScratch rs, cudaStream_t s) {
+    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0 || n < 2) return false;
+    int vb, cb;
+    const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
+    const int smem = kTmaWarps * stage;
+    const bool keep = A.sx_keep != 0, wx = x != nullptr;
+    using K = decltype(&spmv_staged_fold_k2_kernel<false, false>);
+    const K kern = keep ? (wx ? spmv_staged_fold_k2_kernel<true, true> : spmv_staged_fold_k2_kernel<true, false>)
+                        : (wx ? spmv_staged_fold_k2_kernel<false, true>
+                              : spmv_staged_fold_k2_kernel<false, false>);
+    {
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        cudaFuncAttributes fa;
+        TW_CUDA(cudaFuncGetAttributes(&fa, kern));
+        if (smem + static_cast<int>(fa.sharedSizeBytes) > 227 * 1024) return false;
+        TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    // rows per stage block: 2 (or 4) operands, multiples of 64 rows
+    const int rows = (stage / (wx ? 32 : 16)) & ~63;
+    if (rows < 128) return false;
+    int dev = 0, sms = 0, occ = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaWarps * 32, smem));
+    // the grid barrier needs every CTA resident: the persistent grid, one per SM
+    const int g = A.tma_blocks;
+    if (occ < 1 || g > occ * sms) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kTmaWarps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TW_CUDA(cudaLaunchKernelEx(&cfg, kern, A, p_local, Ap, r, x, p, n, stage, vb, cb, rows, sc,
+                               history, rs));
     return true;
 }
 

@@ -995,3 +995,29 @@ def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 35)
     check_history(out[0][0], want_h)
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("dims", [(64, 40, 36), (96, 48, 33)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_fold_k2_into_k1(rt, orc, dims, graph, monkeypatch):
+    """Opt-in TW_FOLD_K2=1: K1 and K2 of the single-domain CG in one
+    cooperative launch (grid barrier on alpha, then r -= alpha Ap streamed
+    through the K1 warps' stages).  Two launches per iteration; its r.r tree
+    differs from the standalone K2's, so it is checked under the parity rule,
+    with the x update in the fold (TW_X_IN_K3=0) and in K3 (=1)."""
+    from paper_2602_21897_b200 import _native as N
+    b = orc.rhs_xorshift(int(np.prod(dims)), 8)
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
+    monkeypatch.setenv("TW_FOLD_K2", "1")
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    for xk3 in ("0", "1"):
+        monkeypatch.setenv("TW_X_IN_K3", xk3)
+        s = P.CgSolver(rt, A, 40, P.CgOptions(use_graph=graph, iteration_marks=False),
+                       variant=N.TW_CG_MONOLITHIC)
+        assert s.launches_per_iteration()[0] == 2
+        s.set_rhs(b)
+        s.iterate(13)
+        s.iterate(27)
+        check_history(s.history(40), want_h)
+        assert np.all(rel_gap(s.solution(), want_x) <= 1e-10)
+        s.close()
