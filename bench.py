@@ -317,6 +317,7 @@ def run_ours(args, dist, rank, world, local):
     import torch
 
     import paper_2602_21897_b200 as P
+    from paper_2602_21897_b200 import _native as N
 
     nx, ny = args.nx, args.ny
     if args.strong:
@@ -469,15 +470,7 @@ def run_ours(args, dist, rank, world, local):
         kt_pass_ms, kt, _ = timed_rep(KR, True)
     ms_max = max_over_ranks(dist, ms)
     kernels_it, colls_it = S.launches_per_iteration()
-    # single-domain monolithic: K3 is fused into the next iteration's K1
-    # (2 kernels per iteration + one K3 per repetition); the fused K1 also
-    # gathers r and writes p_new: 12 nnz + 32 n bytes, and the iteration
-    # moves 12 nnz + 80 n (+ 8 n per repetition: first K1 plain, K3 flush)
-    fused = variant == 0 and kernels_it == 2
-    nrep = len(reps)
-    if fused:
-        bytes_it = 12 * nnz + 80 * n + 8 * n * nrep / K
-        k1_bytes = (KR * (12 * nnz + 32 * n) - 16 * n) / KR  # average over the timing pass's launches
+    mode = S.mode()  # what the solver executes (tw_cg_mode)
     total_flops = sum_over_ranks(dist, float(flops_it))
     total_bytes = sum_over_ranks(dist, float(bytes_it))
     gflops = total_flops * K / (ms_max / 1e3) / 1e9
@@ -489,7 +482,7 @@ def run_ours(args, dist, rank, world, local):
         k1_ms, k2_ms, k3_ms, nt = kt
         k1_avg = k1_ms / nt
         ach = k1_bytes / (k1_avg / 1e3) / 1e9
-        k3_launches = 1 if fused else nt
+        k3_launches = nt
         wl = f"{nx}x{ny}x{args.nz}"
 
         # stencil matrices and z-slabs with nx % 32 == 0 carry the x-staged
@@ -497,28 +490,26 @@ def run_ours(args, dist, rank, world, local):
         # of SURVEY 8(d)'s 12) and its operands from per-slice x windows staged
         # by the same TMA transaction; `achieved` stays on SURVEY's
         # algorithmic bytes, the format's own bytes are reported beside it
-        staged = variant == 0 and A.x_staged and not fused
+        staged = mode["k1_form"] in (N.TW_K1_STAGED, N.TW_K1_STAGED_TABLE)
         k1_format_bytes = (10 * nnz + 16 * n) if staged else k1_bytes
         slab = world > 1 or args.comm
-        kname = ("spmv_tma_kernel<true,true> (K1: TMA-staged SpMV + p.Ap, previous K3 fused)"
-                 if fused else
-                 ("spmv_tma_staged_kernel (K1: TMA-staged matrix + x windows, 16-bit columns, p.Ap"
-                  + ("; z-slab: interior rows, then the ghost-reading boundary rows)" if slab else ")"))
+        kname = (f"spmv_tma_staged_kernel<SPLIT={int(slab and transport == 'peer')},"
+                 f"KEEP={mode['k1_l2_keep']}> (K1: TMA-staged matrix + x windows, 16-bit columns, p.Ap"
+                 + ("; z-slab: interior rows, then the ghost-reading boundary rows)" if slab else ")")
                  if staged else "spmv_tma_kernel<true> (K1: TMA-staged SpMV + p.Ap)")
 
         def traffic_of(k):
             tr = load_traffic(k)
-            ok = tr and tr.get("workload") == wl and world == 1 and not fused
+            ok = tr and tr.get("workload") == wl and world == 1
             if ok and k == "k1":  # the capture must be of the kernel this run used
                 ok = ("staged" in tr.get("kernel", "")) == staged
             return tr.get("dram_bytes_per_launch") if ok else None
 
         traffic = traffic_of("k1")
         # the library moves the x update (x += alpha p_old) from K2 into K3
-        # from 4M rows per rank (tw_cg.cpp x_in_k3; TW_X_IN_K3 forces it):
-        # K2 then streams 24 n bytes and K3 40 n, 8 n less per iteration
-        xe = os.environ.get("TW_X_IN_K3")
-        xk3 = variant == 0 and not fused and (xe == "1" if xe is not None else n >= (1 << 22))
+        # from 4M rows per rank (CgOptions.x_update): K2 then streams 24 n
+        # bytes and K3 40 n, 8 n less per iteration
+        xk3 = bool(mode["x_in_k3"])
         k2_alg, k3_alg = (24 * n, 40 * n) if xk3 else (48 * n, 24 * n)
         roofline = {"bound": "hbm", "kernel": kname,
                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
@@ -556,7 +547,6 @@ def run_ours(args, dist, rank, world, local):
     bh = b_host.numpy()
     torch.cuda.synchronize()
     import ctypes
-    from paper_2602_21897_b200 import _native as N
     N.check(N.load().tw_memcpy(rt.h, ctypes.c_void_p(b_host.data_ptr()), ctypes.c_void_p(b.ptr),
                                8 * n, None))
     rt.synchronize()
@@ -605,10 +595,11 @@ def run_ours(args, dist, rank, world, local):
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
                        "nccl_comm": world > 1 or args.comm,
-                       "transport": transport},
+                       "transport": transport,
+                       "k1": mode["k1_kernel"], "x_update_in": "K3" if mode["x_in_k3"] else "K2"},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": kernels_it * K + (nrep if fused else 0), "nccl_calls": colls_it * K,
+            "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,
             "residual_last": float(hist[-1]),
         }
         print(json.dumps(line), flush=True)

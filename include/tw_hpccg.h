@@ -33,7 +33,7 @@ extern "C" {
 #define TW_ERR_CUDA 3
 #define TW_ERR_NCCL 4
 
-#define TW_ABI_VERSION 2
+#define TW_ABI_VERSION 3
 
 typedef struct tw_ctx tw_ctx; /* replaces tw::Runtime + sim::Device (runtime.hpp:25-55, sim_device.hpp:91-166) */
 typedef struct tw_ell tw_ell; /* replaces tw::bench::CsrMatrix on the device (csr.hpp:9-17) */
@@ -123,9 +123,25 @@ int tw_ell_info(const tw_ell* A, tw_ell_info_t* out);
  * stencil matrix or z-slab with nx % 32 == 0: 16-bit column indices into
  * per-slice windows of x; TW_STAGE_X=0 at build time disables it), else 0. */
 int tw_ell_x_staged(const tw_ell* A, int* staged);
+/* Builds (enable != 0) or drops the x-staged form; *staged (optional) says
+ * whether the matrix carries it afterwards.  tw_ell_from_csr matrices get it
+ * as a per-slice run table when every 32-row slice's columns fall into at
+ * most 9 windows of 36 entries (the 27-point stencil does for nx % 32 == 0:
+ * the reference's own gen_stencil_matrix output passed as a CsrMatrix runs
+ * the same K1 as a device-generated grid); dropping it frees 2 B per entry
+ * and makes the CG run the gather K1 (the results are bit-identical). */
+int tw_ell_set_x_staged(tw_ell* A, int enable, int* staged);
 /* Device ELL -> host CSR with GLOBAL column indices (row_ptr int64[n_rows+1],
  * col_idx int64[nnz], values double[nnz]); the structure parity check. */
 int tw_ell_to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values);
+/* Rows [row_begin, row_end) only (row_ptr relative: row_end - row_begin + 1
+ * entries; col_idx / values sized max_width per row), so a grid whose CSR
+ * does not fit host memory is checked a z-slab at a time.  staged != 0
+ * decodes the 16-bit x-staged columns (the form the CG's K1 reads) through
+ * the slices' run starts instead of the int32 columns (TW_ERR_CONTRACT when
+ * the matrix has no x-staged form). */
+int tw_ell_to_csr_rows(const tw_ell* A, int64_t row_begin, int64_t row_end, int staged,
+                       int64_t* row_ptr, int64_t* col_idx, double* values);
 int tw_ell_destroy(tw_ell* A);
 
 /* ------------------------------------------------- streams and events
@@ -222,7 +238,21 @@ typedef struct tw_cg_options {
     int iteration_marks;           /* CgOptions::iteration_marks: host poller stamps cg_iter=i */
     double tol;                    /* CgOptions::tol: converged = last residual < tol  */
     int dispatch;                  /* TW_DISPATCH_AUTO (default) | _STREAMS | _PERSISTENT */
+    /* Placement and tuning choices that change no result bit (x_update,
+     * l2_keep) or only the dispatcher's chunk-order reduction tree (chunk
+     * sizes; within the SURVEY 8(c) rule).  0 = the library's choice. */
+    int x_update;                  /* TW_XUPD_AUTO | _K2 | _K3: where x += alpha p runs    */
+    int l2_keep;                   /* TW_L2KEEP_AUTO | _ON | _OFF: staged K1's x-run policy */
+    int64_t dag_spmv_slices;       /* persistent dispatcher: slices per SpMV chunk         */
+    int64_t dag_vec_rows;          /* persistent dispatcher: rows per update chunk         */
 } tw_cg_options;
+
+#define TW_XUPD_AUTO 0   /* K3 from 4M rows per rank (8n bytes less per iteration), else K2 */
+#define TW_XUPD_K2 1     /* in K2 with r -= alpha Ap                                        */
+#define TW_XUPD_K3 2     /* in K3, reading p before it is overwritten                       */
+#define TW_L2KEEP_AUTO 0 /* evict_last on the staged x runs while x has <= 8M entries       */
+#define TW_L2KEEP_ON 1
+#define TW_L2KEEP_OFF 2
 
 #define TW_DISPATCH_STREAMS 0    /* one launch per task, cudaStreamWaitEvent edges (or graph) */
 #define TW_DISPATCH_PERSISTENT 1 /* one persistent kernel runs the whole DAG: chunked tasks,
@@ -286,6 +316,31 @@ int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_
  * Single-domain monolithic solves fuse K3 into the next iteration's K1:
  * 2 kernels per iteration plus one K3 per tw_cg_iterate call. */
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
+
+/* What a solver actually executes (for reports and tests: the bench line
+ * names the kernel instantiation its roofline is measured on). */
+#define TW_K1_REGISTER 0       /* register-path gather SpMV (rows wider than the TMA stages) */
+#define TW_K1_TMA_GATHER 1     /* spmv_tma_kernel: TMA-staged matrix, gathered x              */
+#define TW_K1_STAGED 2         /* spmv_tma_staged_kernel, closed-form x runs (nx % 32 == 0)   */
+#define TW_K1_STAGED_TABLE 3   /* spmv_tma_staged_kernel, per-slice run table                 */
+#define TW_TRANSPORT_NONE 0
+#define TW_TRANSPORT_NCCL 1
+#define TW_TRANSPORT_PEER 2
+#define TW_TRANSPORT_LOOPBACK 3 /* emulated rank group on one device */
+typedef struct tw_cg_mode_t {
+    int32_t variant;   /* TW_CG_MONOLITHIC | TW_CG_TASKS                     */
+    int32_t tiles;
+    int32_t dispatch;  /* TW_DISPATCH_STREAMS | _PERSISTENT (AUTO resolved)  */
+    int32_t use_graph;
+    int32_t k1_form;   /* TW_K1_*                                            */
+    int32_t k1_l2_keep; /* staged K1 stages the x runs with L2 evict_last     */
+    int32_t x_in_k3;   /* x += alpha p runs in K3 (else in K2)               */
+    int32_t transport; /* TW_TRANSPORT_*                                     */
+    int32_t nranks;
+    int32_t kernels_per_iteration;
+    int32_t collectives_per_iteration;
+} tw_cg_mode_t;
+int tw_cg_mode(tw_cg* cg, tw_cg_mode_t* out);
 
 /* Emulated rank group (see tw_ctx_init_emulated_rank): cgs[r] is rank r's
  * monolithic solver, b[r] its rows of b. */

@@ -72,6 +72,9 @@ class Oracle:
         L.orc_stencil_nnz.argtypes = [_i64, _i64, _i64]
         L.orc_stencil_check.argtypes = [_i64, _i64, _i64]
         L.orc_gen_stencil_csr.argtypes = [_i64, _i64, _i64, _lp, _lp, _dp]
+        L.orc_gen_stencil_csr_rows.argtypes = [_i64] * 5 + [_lp, _lp, _dp]
+        L.orc_cg_stencil_mt.argtypes = [_i64, _i64, _i64, _dp, C.c_int, C.c_int, C.c_int, _dp,
+                                        _dp, _dp]
         L.orc_stencil_row_len.restype = _i64
         L.orc_stencil_row_len.argtypes = [_i64] * 6
         L.orc_csr_validate.argtypes = [_i64, _lp, _i64, _lp]
@@ -98,6 +101,18 @@ class Oracle:
         va = np.empty(nnz, np.float64)
         self.lib.orc_gen_stencil_csr(nx, ny, nz, _l(rp), _l(ci), _d(va))
         return Csr(n, rp, ci, va)
+
+    def stencil_rows(self, nx: int, ny: int, nz: int, r0: int, r1: int) -> Csr:
+        """Rows [r0, r1) of the full stencil matrix (row_ptr relative to r0)."""
+        if self.lib.orc_stencil_check(nx, ny, nz) != 0 or not 0 <= r0 <= r1 <= nx * ny * nz:
+            raise OracleError("stencil dims / row range")
+        rp = np.empty(r1 - r0 + 1, np.int64)
+        cap = 27 * (r1 - r0)
+        ci = np.empty(cap, np.int64)
+        va = np.empty(cap, np.float64)
+        self.lib.orc_gen_stencil_csr_rows(nx, ny, nz, r0, r1, _l(rp), _l(ci), _d(va))
+        k = int(rp[-1])
+        return Csr(r1 - r0, rp, ci[:k], va[:k])
 
     def stencil_nnz(self, nx, ny, nz) -> int:
         return int(self.lib.orc_stencil_nnz(nx, ny, nz))
@@ -157,6 +172,18 @@ class Oracle:
         if self.lib.orc_cg_stencil(nx, ny, nz, _d(b), iterations, tiles, _d(hist), _d(x),
                                    _d(work)) != 0:
             raise OracleError("cg_stencil: bad dims / tiles")
+        return hist[:iterations], x
+
+    def cg_stencil_mt(self, nx, ny, nz, b, iterations, tiles=1, threads=None):
+        """cg_stencil with the row-parallel phases threaded (bit-identical)."""
+        n = nx * ny * nz
+        threads = threads or min(os.cpu_count() or 1, 64)
+        hist = np.zeros(max(iterations, 1), np.float64)
+        x = np.empty(n, np.float64)
+        work = np.empty(3 * n, np.float64)
+        if self.lib.orc_cg_stencil_mt(nx, ny, nz, _d(b), iterations, tiles, threads, _d(hist),
+                                      _d(x), _d(work)) != 0:
+            raise OracleError("cg_stencil_mt: bad dims / tiles / threads")
         return hist[:iterations], x
 
     # right-hand sides (acceptance.cpp:48-58, scenario.cpp:46-55)

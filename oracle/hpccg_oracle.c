@@ -16,6 +16,7 @@
  * no FMA: SURVEY.md section 7 "Bitwise SpMV/waxpby need no-FMA arithmetic").
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stddef.h>
 
@@ -55,35 +56,43 @@ int orc_stencil_check(int64_t nx, int64_t ny, int64_t nz) {
 /* Rows z-major, row = (z*ny + y)*nx + x (csr.cpp:43-45); per row the
  * neighbours in (dz,dy,dx) lexicographic order, which is ascending column
  * order (csr.cpp:46-53); 27.0 on the diagonal, -1.0 elsewhere (csr.cpp:54).
- * Caller sizes col_idx/values with orc_stencil_nnz(). */
+ * Rows [r0, r1) of the full matrix; row_ptr is relative (row_ptr[0] = 0,
+ * r1 - r0 + 1 entries), so a grid whose CSR does not fit host memory is
+ * checked a z-slab at a time.  Caller sizes col_idx/values. */
+int orc_gen_stencil_csr_rows(int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1,
+                             int64_t* row_ptr, int64_t* col_idx, double* values) {
+    if (orc_stencil_check(nx, ny, nz) != ORC_OK)
+        return ORC_ERR_CONFIG;
+    if (r0 < 0 || r1 < r0 || r1 > nx * ny * nz)
+        return ORC_ERR_CONFIG;
+    int64_t k = 0;
+    row_ptr[0] = 0;
+    for (int64_t row = r0; row < r1; ++row) {
+        const int64_t x = row % nx, y = (row / nx) % ny, z = row / (nx * ny);
+        for (int64_t cz = z - 1; cz <= z + 1; ++cz) {
+            if (cz < 0 || cz >= nz) continue;
+            for (int64_t cy = y - 1; cy <= y + 1; ++cy) {
+                if (cy < 0 || cy >= ny) continue;
+                int64_t line = (cz * ny + cy) * nx;
+                for (int64_t cx = x - 1; cx <= x + 1; ++cx) {
+                    if (cx < 0 || cx >= nx) continue;
+                    col_idx[k] = line + cx;
+                    values[k] = (cx == x && cy == y && cz == z) ? 27.0 : -1.0;
+                    ++k;
+                }
+            }
+        }
+        row_ptr[row - r0 + 1] = k;
+    }
+    return ORC_OK;
+}
+
+/* The whole matrix (gen_stencil_matrix, csr.cpp:29-59). */
 int orc_gen_stencil_csr(int64_t nx, int64_t ny, int64_t nz, int64_t* row_ptr,
                         int64_t* col_idx, double* values) {
     if (orc_stencil_check(nx, ny, nz) != ORC_OK)
         return ORC_ERR_CONFIG;
-    int64_t k = 0;
-    int64_t row = 0;
-    row_ptr[0] = 0;
-    for (int64_t z = 0; z < nz; ++z) {
-        for (int64_t y = 0; y < ny; ++y) {
-            for (int64_t x = 0; x < nx; ++x, ++row) {
-                for (int64_t cz = z - 1; cz <= z + 1; ++cz) {
-                    if (cz < 0 || cz >= nz) continue;
-                    for (int64_t cy = y - 1; cy <= y + 1; ++cy) {
-                        if (cy < 0 || cy >= ny) continue;
-                        int64_t line = (cz * ny + cy) * nx;
-                        for (int64_t cx = x - 1; cx <= x + 1; ++cx) {
-                            if (cx < 0 || cx >= nx) continue;
-                            col_idx[k] = line + cx;
-                            values[k] = (cx == x && cy == y && cz == z) ? 27.0 : -1.0;
-                            ++k;
-                        }
-                    }
-                }
-                row_ptr[row + 1] = k;
-            }
-        }
-    }
-    return ORC_OK;
+    return orc_gen_stencil_csr_rows(nx, ny, nz, 0, nx * ny * nz, row_ptr, col_idx, values);
 }
 
 /* Row length of the stencil at (x,y,z), used by structure checks. */
@@ -279,6 +288,86 @@ int orc_cg_stencil(int64_t nx, int64_t ny, int64_t nz, const double* b, int iter
         rtrans = rr;
         history[it] = sqrt(rr);
         orc_waxpby_range(1.0, r, beta, p, p, 0, n);
+    }
+    return ORC_OK;
+}
+
+/* The same CG with the row-parallel phases on `threads` host threads, for
+ * the sizes the GPU headline runs (256^3, 512^3).  SpMV rows and waxpby
+ * elements are independent, so splitting them changes no bit; every dot
+ * stays a sequential left-to-right sum per tile, tiles summed in order, so
+ * the result is bit-identical to orc_cg_stencil for any thread count
+ * (pinned by tests/test_oracle.py). */
+typedef struct {
+    int64_t nx, ny, nz, n, i0, i1;
+    int phase; /* 0: Ap = A p; 1: x += alpha p, r -= alpha Ap; 2: p = r + beta p */
+    double alpha, beta;
+    double *x, *r, *p, *Ap;
+} orc_job;
+
+static void* orc_job_run(void* arg) {
+    orc_job* j = (orc_job*)arg;
+    if (j->phase == 0) {
+        orc_stencil_spmv_range(j->nx, j->ny, j->nz, j->p, j->Ap, j->i0, j->i1);
+    } else if (j->phase == 1) {
+        orc_waxpby_range(1.0, j->x, j->alpha, j->p, j->x, j->i0, j->i1);
+        orc_waxpby_range(1.0, j->r, -j->alpha, j->Ap, j->r, j->i0, j->i1);
+    } else {
+        orc_waxpby_range(1.0, j->r, j->beta, j->p, j->p, j->i0, j->i1);
+    }
+    return NULL;
+}
+
+#define ORC_MAX_THREADS 256
+
+static int orc_parallel(orc_job* tmpl, int threads) {
+    pthread_t th[ORC_MAX_THREADS];
+    orc_job jobs[ORC_MAX_THREADS];
+    int started = 0;
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = *tmpl;
+        jobs[t].i0 = tmpl->n * t / threads;
+        jobs[t].i1 = tmpl->n * (t + 1) / threads;
+        if (t == threads - 1 || pthread_create(&th[t], NULL, orc_job_run, &jobs[t]) != 0) {
+            orc_job_run(&jobs[t]);
+        } else {
+            ++started;
+        }
+    }
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    return ORC_OK;
+}
+
+int orc_cg_stencil_mt(int64_t nx, int64_t ny, int64_t nz, const double* b, int iterations,
+                      int tiles, int threads, double* history, double* x_out, double* work) {
+    if (orc_stencil_check(nx, ny, nz) != ORC_OK)
+        return ORC_ERR_CONFIG;
+    const int64_t n = nx * ny * nz;
+    if (tiles < 1 || (int64_t)tiles > n || threads < 1 || threads > ORC_MAX_THREADS)
+        return ORC_ERR_CONFIG;
+    if ((int64_t)threads > n) threads = (int)n;
+    orc_job j = {nx, ny, nz, n, 0, n, 0, 0.0, 0.0, x_out, work, work + n, work + 2 * n};
+    for (int64_t i = 0; i < n; ++i) {
+        j.x[i] = 0.0; j.r[i] = b[i]; j.p[i] = b[i]; j.Ap[i] = 0.0;
+    }
+    double rtrans = orc_dot_range(j.r, j.r, 0, n);
+    for (int it = 0; it < iterations; ++it) {
+        j.phase = 0;
+        orc_parallel(&j, threads);
+        double pAp = 0.0;
+        for (int t = 0; t < tiles; ++t)
+            pAp += orc_dot_range(j.p, j.Ap, n * t / tiles, n * (t + 1) / tiles);
+        j.alpha = rtrans / pAp;
+        j.phase = 1;
+        orc_parallel(&j, threads);
+        double rr = 0.0;
+        for (int t = 0; t < tiles; ++t)
+            rr += orc_dot_range(j.r, j.r, n * t / tiles, n * (t + 1) / tiles);
+        j.beta = rr / rtrans;
+        rtrans = rr;
+        history[it] = sqrt(rr);
+        j.phase = 2;
+        orc_parallel(&j, threads);
     }
     return ORC_OK;
 }

@@ -71,7 +71,19 @@ class SlabPlan(C.Structure):
 class CgOptionsC(C.Structure):
     _fields_ = [("variant", C.c_int), ("tiles", C.c_int), ("stream_pool_capacity", C.c_uint),
                 ("use_graph", C.c_int), ("iteration_marks", C.c_int), ("tol", C.c_double),
-                ("dispatch", C.c_int)]
+                ("dispatch", C.c_int), ("x_update", C.c_int), ("l2_keep", C.c_int),
+                ("dag_spmv_slices", C.c_int64), ("dag_vec_rows", C.c_int64)]
+
+
+class CgMode(C.Structure):
+    _fields_ = [(k, C.c_int32) for k in ("variant", "tiles", "dispatch", "use_graph", "k1_form",
+                                         "k1_l2_keep", "x_in_k3", "transport", "nranks",
+                                         "kernels_per_iteration", "collectives_per_iteration")]
+
+
+TW_K1_NAMES = {0: "spmv_kernel (register path)", 1: "spmv_tma_kernel (TMA matrix, gathered x)",
+               2: "spmv_tma_staged_kernel (closed-form x runs)",
+               3: "spmv_tma_staged_kernel (run-table x runs)"}
 
 
 # (name, restype, argtypes) for every symbol include/tw_hpccg.h declares.
@@ -98,6 +110,7 @@ SIGNATURES = [
     ("tw_ell_from_csr", C.c_int, [vp, i64, lp, lp, dp, C.POINTER(vp)]),
     ("tw_ell_info", C.c_int, [vp, C.POINTER(EllInfo)]),
     ("tw_ell_to_csr", C.c_int, [vp, lp, lp, dp]),
+    ("tw_ell_to_csr_rows", C.c_int, [vp, i64, i64, C.c_int, lp, lp, dp]),
     ("tw_ell_destroy", C.c_int, [vp]),
     ("tw_spmv_range", C.c_int, [vp, vp, vp, i64, i64, vp]),
     ("tw_spmv_dot", C.c_int, [vp, vp, vp, i64, i64, vp, vp]),
@@ -124,10 +137,12 @@ SIGNATURES = [
     ("tw_task_dag_edges", C.c_int, [i64, C.c_int, lp, lp, lp, lp, i64, i64, C.c_int, C.c_int,
                                     C.c_int, C.c_char_p, i64, C.POINTER(i64)]),
     ("tw_cg_launches_per_iteration", C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("tw_cg_mode", C.c_int, [vp, C.POINTER(CgMode)]),
     ("tw_cg_group_set_rhs", C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(vp), C.c_int]),
     ("tw_cg_group_iterate", C.c_int, [C.POINTER(vp), C.c_int, C.c_int]),
     ("tw_halo_exchange", C.c_int, [vp, vp, vp]),
     ("tw_ell_x_staged", C.c_int, [vp, C.POINTER(C.c_int)]),
+    ("tw_ell_set_x_staged", C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
     ("tw_update_xr_rr", C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, vp, vp]),
     ("tw_update_p", C.c_int, [vp, vp, vp, vp, i64, i64, vp]),
     ("tw_stream_acquire", C.c_int, [vp, C.POINTER(vp)]),

@@ -30,28 +30,17 @@
 namespace tw {
 namespace cgi {
 
-// Programmatic dependent launch for the monolithic chains: opt-in
-// (TW_PDL=1).  It helped the gather K1 in streams mode (0.138 -> 0.132 ms at
-// 128^3) but costs the x-staged K1 5 % at 256^3 (0.929 vs 0.883 ms): the
-// successor's early blocks share the SMs with K1's CTAs.
 // The x update (x += alpha p_old) in K3 instead of K2: K3 reads p_old
 // anyway, so the iteration moves 8 n bytes less from DRAM once the vectors
 // no longer sit in L2 (measured, event-timed K2 + K3: 256^3 197.5 -> 179.7 us,
-// 128^3 29.0 -> 29.6 us), hence from 4M rows per rank.  TW_X_IN_K3=0 / 1
-// forces it off / on (A/B).
+// 128^3 29.0 -> 29.6 us), hence from 4M rows per rank by default.  The
+// placement changes no bit (each element's update is the same rounding).
 bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
 
-static bool decide_x_in_k3(int64_t n) { // at solver creation
-    const char* e = std::getenv("TW_X_IN_K3");
-    return e ? e[0] != '0' : n >= (int64_t(1) << 22);
-}
-
-bool use_pdl() {
-    static const bool on = [] {
-        const char* e = std::getenv("TW_PDL");
-        return e && e[0] == '1';
-    }();
-    return on;
+static bool decide_x_in_k3(const tw_cg_options& o, int64_t n) { // at solver creation
+    if (o.x_update == TW_XUPD_K2) return false;
+    if (o.x_update == TW_XUPD_K3) return true;
+    return n >= (int64_t(1) << 22);
 }
 
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
@@ -112,70 +101,28 @@ void record(cudaEvent_t e, cudaStream_t s) {
 }
 
 // One monolithic iteration (cg_monolithic, cg.cpp:408-431) on the compute
-// stream; across ranks the SpMV is split so the interior rows overlap the
-// halo exchange on the comm stream.
-//
-// Single domain, `fuse` (iteration i of a k-iteration call): iteration 0 runs
-// K1 on p; every later one runs K1 with the previous iteration's K3 fused in
-// (p_new = r + beta p_old formed on the fly, stored to the other buffer);
-// the last one ends with K3 proper, back into p_owned.  The arithmetic is
-// K3's, so the results are those of the three-kernel sequence.
-void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
+// stream: K1 -> K2 -> K3 (x rides on K2 or on K3, x_in_k3); across ranks the
+// SpMV is split so the interior rows overlap the halo exchange on the comm
+// stream.
+void enqueue_mono(tw_cg* cg) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
     if (!cg->dist) {
-        // K1 -> K2 -> K3 -> K1 ... as a programmatic-dependent-launch chain:
-        // each kernel queues its successor early and the successor waits in
-        // griddepcontrol.wait, so the launch gaps overlap the tails
-        const bool pdl = use_pdl();
         const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
-        // x-staged fused chain: the fused K1 also applies the previous
-        // iteration's x update, so K2 never touches x (the call's last K3 does)
-        const bool fuse_x = fuse && A.cols16 != nullptr;
-        const bool xk3f = fuse ? fuse_x : x_in_k3(cg);
-        if (cg->fold_k2 && !fuse &&
-            launch_spmv_staged_fold_k2(A, cg->p_local, cg->Ap, cg->r, xk3f ? nullptr : cg->x,
-                                       cg->p_cur, cg->n, cg->sc, cg->history, rs, s)) {
-            record(tmark(cg, 1), s); // K1 and K2 in one launch: K2's share reads 0
-            record(tmark(cg, 2), s);
-            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p_cur, pdl, xk3f ? cg->x : nullptr);
-            cg->p_cur = cg->p_owned;
-            record(tmark(cg, 3), s);
-            if (cg->timing) ++cg->timed;
-            return;
-        }
-        if (fuse && i > 0) {
-            double* next = cg->p_cur == cg->p_owned ? cg->p_alt : cg->p_owned;
-            const bool ok = fuse_x ? launch_spmv_staged_fusep(A, cg->r, cg->p_cur, next, cg->x,
-                                                              cg->Ap, cg->n, rs, fa, s)
-                                   : launch_spmv_fusep(A, cg->r, cg->p_cur, next, cg->Ap, cg->n,
-                                                       rs, fa, s);
-            if (!ok) throw Error(TW_ERR_CUDA, "fused SpMV unavailable");
-            cg->p_cur = next;
-        } else if (fuse_x) {
-            if (!launch_spmv_staged(A, cg->p_cur, cg->Ap, RowRange{0, cg->n}, rs, fa, s, pdl))
-                throw Error(TW_ERR_CUDA, "staged SpMV unavailable");
-        } else if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, rs, fa, s, pdl)) {
-            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s,
-                        nullptr, 0, pdl);
-        }
+        if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, rs, fa, s))
+            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs,
+                        s);
         record(tmark(cg, 1), s);
-        // x rides on K3 (x_in_k3) or on the fused K1 / the call's last K3
-        // (fuse_x); the gather fused chain keeps it in K2
-        const bool xk3 = fuse ? fuse_x : x_in_k3(cg);
-        launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, cg->p_cur, cg->r, cg->Ap, cg->sc,
+        const bool xk3 = x_in_k3(cg);
+        launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv,
-                         s, pdl);
+                         s);
         record(tmark(cg, 2), s);
-        if (!fuse || i == k - 1) {
-            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p_cur, pdl, xk3 ? cg->x : nullptr);
-            cg->p_cur = cg->p_owned;
-        }
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                        cg->history, bv, s, nullptr, nullptr, false, xk3 ? cg->x : nullptr);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
@@ -214,13 +161,8 @@ void enqueue_mono(tw_cg* cg, int i, int k, bool fuse) {
 // min(T, capacity) at once), so with few tiles each gets that share of the
 // GPU's resident grid: a full grid per tile would make them queue behind one
 // another, paying a ramp and a tail each (128^3, 4 tiles: 0.149 -> 0.142 ms
-// per iteration with a graph).  TW_TILE_GRID=full keeps full grids (A/B).
+// per iteration with a graph).
 int tile_share(const tw_cg* cg) {
-    static const bool full = [] {
-        const char* e = std::getenv("TW_TILE_GRID");
-        return e && std::string(e) == "full";
-    }();
-    if (full) return 1;
     const int cap = static_cast<int>(cg->ctx->pool.capacity());
     // with many tiles each tile's grid is already bounded by its own size
     // (and measured: sharing then costs up to 15 %, profiles/r01_sweep_summary.md)
@@ -350,8 +292,6 @@ void free_cg(tw_cg* cg) {
     cg->ta.reset();
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
-    for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
-    cudaFree(cg->p_alt_base);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
@@ -477,31 +417,12 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         // that start 2 before a line
         int64_t front = (16 - cg->diag_shift % 16) % 16;
         if (front < 2) front += 16;
-        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 8)));
+        // (and at least kStageRunLen after: a run-table run may start at the
+        // last column)
+        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
         cg->p_local = cg->p_base + front;
         cg->p_owned = cg->p_local + cg->diag_shift;
-        cg->p_cur = cg->p_owned;
-        {
-            const char* f = std::getenv("TW_FUSE_P");
-            const int mw = static_cast<int>(A->info.max_width);
-            const bool fits = A->cols16 ? staged_fusep_smem_bytes(mw) + 2048 <= 227 * 1024
-                                        : spmv_tma_smem_bytes(mw) + 4096 <= 227 * 1024;
-            cg->fusep = cg->opt.variant == TW_CG_MONOLITHIC && !cg->dist &&
-                        cg->opt.dispatch != TW_DISPATCH_PERSISTENT && mw > 0 &&
-                        ctx->cfg.tma_blocks > 0 && fits &&
-                        f && f[0] == '1'; // opt-in: measured slower
-            if (cg->fusep) { // same slack and alignment as p_local (staged runs)
-                TW_CUDA(cudaMalloc(&cg->p_alt_base,
-                                   sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 8)));
-                cg->p_alt = cg->p_alt_base + front;
-            }
-        }
-        cg->x_k3 = decide_x_in_k3(n);
-        {
-            const char* f = std::getenv("TW_FOLD_K2");
-            cg->fold_k2 = f && f[0] == '1' && A->cols16 && !cg->dist &&
-                          cg->opt.variant == TW_CG_MONOLITHIC && !cg->fusep;
-        }
+        cg->x_k3 = decide_x_in_k3(cg->opt, n);
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
         TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
         const int T = cg->T, P = cg->P;
@@ -621,21 +542,18 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
 // 32768 rows per update chunk (the 256^3 optimum), but about 4 SpMV chunks
 // and 2 update chunks per CTA per pass on smaller problems (the 128^3
 // optimum; profiles/r01_dispatcher_summary.md).
-// TW_DAG_SPMV_SLICES / TW_DAG_VEC_ROWS override (tuning only).
-int64_t env_or(const char* name, int64_t dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::atoll(v) : dflt;
-}
+// tw_cg_options::dag_spmv_slices / dag_vec_rows override (tuning sweeps).
 int64_t dag_spmv_chunk_slices(const tw_cg* cg) {
+    if (cg->opt.dag_spmv_slices > 0) return cg->opt.dag_spmv_slices;
     const int64_t w = dag_compute_warps(), ns = (cg->n + 31) / 32;
     const int64_t fit = ns / (4 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
-    return env_or("TW_DAG_SPMV_SLICES", std::max(w, std::min(12 * w, fit)));
+    return std::max(w, std::min(12 * w, fit));
 }
 int64_t dag_vec_chunk_rows(const tw_cg* cg) {
     const int64_t fit = cg->n / (2 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
     // multiples of 256 rows keep chunk boundaries on 2 KB (cache-line) edges
-    const int64_t rows = fit >= 24576 ? 32768 : std::max<int64_t>(2048, fit & ~int64_t(255));
-    return env_or("TW_DAG_VEC_ROWS", rows);
+    if (cg->opt.dag_vec_rows > 0) return cg->opt.dag_vec_rows;
+    return fit >= 24576 ? 32768 : std::max<int64_t>(2048, fit & ~int64_t(255));
 }
 
 void build_dag_table(tw_cg* cg, int k) {
@@ -751,7 +669,8 @@ void enqueue_persistent(tw_cg* cg, int k) {
                    &P.c16_bytes);
     // update chunks by TMA when the stage holds >= 128 rows of each operand
     // (multiples of 64 rows: one 16-byte pair per lane and step)
-    const bool upd_tma = env_or("TW_DAG_UPD_TMA", 1) != 0;
+    // (the register path remains for stages too small for that)
+    const bool upd_tma = true;
     // x update in the p-update chunks (x_in_k3): x/r chunks stream r, Ap and
     // p chunks r, p, x; else x, p, r, Ap and r, p
     const int rows2 = (P.stage_bytes / 16) & ~63, rows3 = (P.stage_bytes / 24) & ~63,
@@ -786,24 +705,20 @@ void iterate(tw_cg* cg, int k) {
         cg->enqueued += k;
         return;
     }
-    // the K3 fusion needs the whole call in one piece: streams, or a
-    // k-iteration graph (per-iteration host marks need the 1-iteration graph)
-    const bool fuse = cg->fusep && (!cg->opt.use_graph || cg->timing || !cg->opt.iteration_marks);
-    if (cg->opt.use_graph && cg->opt.variant == TW_CG_MONOLITHIC && (cg->timing || fuse)) {
+    if (cg->opt.use_graph && cg->opt.variant == TW_CG_MONOLITHIC && cg->timing) {
         // k iterations as ONE graph; timed: with the K1/K2/K3 timing events
         // inside (graph-launch efficiency and per-kernel durations of one run)
-        auto& cache = cg->timing ? cg->timed_graphs : cg->k_graphs;
+        auto& cache = cg->timed_graphs;
         auto it = cache.find(k);
         if (it == cache.end()) {
             cudaGraph_t g = nullptr;
             cg->timed = 0;
             TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
-                for (int i = 0; i < k; ++i) enqueue_mono(cg, i, k, fuse);
+                for (int i = 0; i < k; ++i) enqueue_mono(cg);
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);
-                cg->p_cur = cg->p_owned;
                 throw;
             }
             TW_CUDA(cudaStreamEndCapture(s, &g));
@@ -827,7 +742,7 @@ void iterate(tw_cg* cg, int k) {
         if (cg->opt.use_graph) {
             TW_CUDA(cudaGraphLaunch(cg->graph, s));
         } else if (!tasks) {
-            enqueue_mono(cg, i, k, fuse);
+            enqueue_mono(cg);
         } else {
             enqueue_iteration_body(cg, it & 1, i == 0);
         }
@@ -876,6 +791,10 @@ void tw_cg_options_default(tw_cg_options* o) {
     o->iteration_marks = 1;
     o->tol = 0.0;
     o->dispatch = TW_DISPATCH_AUTO;
+    o->x_update = TW_XUPD_AUTO;
+    o->l2_keep = TW_L2KEEP_AUTO;
+    o->dag_spmv_slices = 0;
+    o->dag_vec_rows = 0;
 }
 
 int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max_iterations,
@@ -1045,10 +964,6 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
         } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->peer) {
             // K1 (one launch, or interior + boundary), K2 (+wait, publish), K3 (+wait, halo)
             k = peer_k1_fused(cg) ? 3 : 4;
-        } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fusep) {
-            k = 2; // K1 (with the previous K3 fused in) + K2; one K3 per tw_cg_iterate call
-        } else if (cg->opt.variant == TW_CG_MONOLITHIC && cg->fold_k2) {
-            k = 2; // K1 + K2 folded into one cooperative launch, K3
         } else if (cg->opt.variant == TW_CG_MONOLITHIC) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;
@@ -1058,6 +973,38 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
         }
         if (kernels) *kernels = k;
         if (collectives) *collectives = c;
+    });
+}
+
+int tw_cg_mode(tw_cg* cg, tw_cg_mode_t* out) {
+    return guarded([&] {
+        if (!cg || !out) contract_error("null solver / out");
+        const EllView v = cg->view();
+        tw_cg_mode_t m{};
+        m.variant = cg->opt.variant;
+        m.tiles = cg->T;
+        m.dispatch = cg->opt.dispatch;
+        m.use_graph = cg->opt.use_graph;
+        if (v.cols16) {
+            m.k1_form = v.sx_runs ? TW_K1_STAGED_TABLE : TW_K1_STAGED;
+            m.k1_l2_keep = v.sx_keep;
+        } else {
+            m.k1_form = v.tma_blocks > 0 && v.max_width > 0 &&
+                                spmv_tma_smem_bytes(v.max_width) + 4096 <= 227 * 1024
+                            ? TW_K1_TMA_GATHER
+                            : TW_K1_REGISTER;
+        }
+        m.x_in_k3 = x_in_k3(cg);
+        m.transport = cg->ctx->emulated ? TW_TRANSPORT_LOOPBACK
+                      : cg->peer        ? TW_TRANSPORT_PEER
+                      : cg->dist        ? TW_TRANSPORT_NCCL
+                                        : TW_TRANSPORT_NONE;
+        m.nranks = cg->P;
+        int k = 0, c = 0;
+        if (tw_cg_launches_per_iteration(cg, &k, &c) != TW_OK) throw Error(TW_ERR_CONTRACT, g_last_error);
+        m.kernels_per_iteration = k;
+        m.collectives_per_iteration = c;
+        *out = m;
     });
 }
 

@@ -105,7 +105,7 @@ void peer_spmv(tw_cg* cg, cudaStream_t s) {
         b1{cg->slab.interior_r1, cg->n};
     if (cg->view().cols16) { // x-staged slab: the same two forms with staged x runs
         if (launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, ri, b0, b1, true, cg->slot(0), fin,
-                               s, ng ? gf : nullptr, ng, use_pdl()))
+                               s, ng ? gf : nullptr, ng))
             return;
         dist_spmv_interior(cg, s);
         if (!launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, b0, b1, RowRange{0, 0}, false,
@@ -119,7 +119,7 @@ void peer_spmv(tw_cg* cg, cudaStream_t s) {
                           RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
                           RowRange{0, cg->slab.interior_r0}, RowRange{cg->slab.interior_r1, cg->n},
                           cg->slot(0), Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
-                          s, ng ? gf : nullptr, ng, use_pdl()))
+                          s, ng ? gf : nullptr, ng))
         return;
     dist_spmv_interior(cg, s);
     launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
@@ -132,13 +132,13 @@ void peer_update_xr(tw_cg* cg, cudaStream_t s) {
     launch_update_xr(0, cg->n, x_in_k3(cg) ? nullptr : cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
                      ScalarSrc{cg->win->recv_a, cg->P, cg->win->flag_a}, cg->slot(0),
                      Fin{FIN_PUBLISH_B, cg->send_b, cg->sc, nullptr, cg->d_links, nullptr},
-                     launch_blocks(cg, false), s, use_pdl());
+                     launch_blocks(cg, false), s);
 }
 
 void peer_update_p(tw_cg* cg, cudaStream_t s) {
     launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
                     ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
-                    launch_blocks(cg, false), s, cg->d_links, nullptr, use_pdl(),
+                    launch_blocks(cg, false), s, cg->d_links, nullptr, false,
                     x_in_k3(cg) ? cg->x : nullptr);
 }
 
@@ -166,8 +166,6 @@ void finish_links(tw_cg* cg) {
     }
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     cg->timed_graphs.clear();
-    for (auto& kv : cg->k_graphs) cudaGraphExecDestroy(kv.second);
-    cg->k_graphs.clear();
 }
 
 // ------------------------------------------------ emulated rank group

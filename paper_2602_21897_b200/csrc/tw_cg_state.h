@@ -63,16 +63,7 @@ struct tw_cg {
 
     cudaGraphExec_t graph = nullptr;
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
-    std::map<int, cudaGraphExec_t> k_graphs;     // K fused iterations, untimed
-    // single-domain monolithic: K3 fused into the next iteration's K1
-    // (launch_spmv_fusep) with p ping-ponging between p_owned and p_alt;
-    // every tw_cg_iterate call starts and ends with p in p_owned
-    bool fusep = false;
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
-    bool fold_k2 = false; // K1 + K2 as one cooperative launch (opt-in TW_FOLD_K2=1)
-    double* p_alt = nullptr;      // p_alt_base + the same front as p_local
-    double* p_alt_base = nullptr;
-    double* p_cur = nullptr;
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;
@@ -103,7 +94,13 @@ struct tw_cg {
     RedScratch slot(int i) const {
         return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
     }
-    EllView view() const { return A->view(); }
+    // K1's view of A; l2_keep overrides the x-run L2 policy of the staged K1
+    EllView view() const {
+        EllView v = A->view();
+        if (v.cols16 && opt.l2_keep == TW_L2KEEP_ON) v.sx_keep = 1;
+        if (v.cols16 && opt.l2_keep == TW_L2KEEP_OFF) v.sx_keep = 0;
+        return v;
+    }
     cudaStream_t node_stream(const PNode& nd) const {
         if (nd.kind == PK_HALO) return ctx->comm;
         const unsigned C = ctx->pool.capacity();
@@ -116,13 +113,12 @@ namespace tw {
 namespace cgi {
 
 // tw_cg.cpp
-bool use_pdl();
 bool x_in_k3(const tw_cg* cg);
 void build_schedule(tw_cg* cg);
 int launch_blocks(const tw_cg* cg, bool spmv);
 cudaEvent_t tmark(tw_cg* cg, int k);
 void record(cudaEvent_t e, cudaStream_t s);
-void enqueue_mono(tw_cg* cg, int i = 0, int k = 1, bool fuse = false);
+void enqueue_mono(tw_cg* cg);
 int tile_share(const tw_cg* cg);
 void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st);
 void fork_streams(tw_cg* cg);
@@ -136,7 +132,6 @@ void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s);
 void reset_solve_state(tw_cg* cg);
 void set_rhs(tw_cg* cg, const double* b, bool on_device);
 cudaEvent_t iter_event(tw_cg* cg, int i);
-int64_t env_or(const char* name, int64_t dflt);
 int64_t dag_spmv_chunk_slices(const tw_cg* cg);
 int64_t dag_vec_chunk_rows(const tw_cg* cg);
 void build_dag_table(tw_cg* cg, int k);

@@ -124,8 +124,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         bulk_g2s(stage + P.val_bytes, P.A.cols16 + off, ents * 2u, bar, pol);
                     }
                     for (int r = 0; r < kStageRuns; ++r) {
-                        const int64_t st = stage_run_start(s, r, P.A.sx_nx, P.A.sx_ny, P.A.sx_nz,
-                                                           P.A.sx_row_off, P.A.sx_col_off);
+                        const int64_t st = run_start(P.A, s, r);
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),

@@ -156,10 +156,8 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         *fin.out = total;
         break;
     case FIN_ALPHA:
-    case FIN_ALPHA_GRID:
         fin.sc->pAp = total;
         fin.sc->alpha = __ddiv_rn(fin.sc->rtrans, total);
-        if (fin.mode == FIN_ALPHA_GRID) st_release_sys(&fin.sc->alpha_stamp, stamp_of(fin.sc, 0));
         break;
     case FIN_BETA: {
         CgScalars* sc = fin.sc;

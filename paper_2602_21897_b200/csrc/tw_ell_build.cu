@@ -270,6 +270,74 @@ __global__ void stencil_cols16_kernel(EllView A, uint16_t* cols16, unsigned* bad
     }
 }
 
+// Run table + 16-bit columns of a general matrix (tw_ell_from_csr), one warp
+// per slice, lane = row.  Run 4 is the window of the slice's own rows
+// ([row0 - 2, row0 + 34) in x: K1's p.Ap reads p[row] from it); the other 8
+// runs cover the remaining columns greedily: each starts at the smallest
+// column not yet covered (rounded down to the 16-byte grid of x) and takes
+// every column below its end.  A column maps to the first run covering it.
+// Slices whose columns need more than 9 runs flag *bad.
+__global__ void csr_runs_kernel(EllView A, int32_t* runs, uint16_t* cols16, unsigned* bad) {
+    constexpr int64_t kNone = INT64_MAX;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = warp_g; s < A.n_slices; s += nwarps) {
+        const int64_t off = A.slice_off[s];
+        const int w = static_cast<int>((A.slice_off[s + 1] - off) >> 5);
+        const int64_t own = s * 32 + A.diag_shift - 2;
+        auto col = [&](int k) -> int64_t {
+            if (k >= w) return kNone;
+            const int c = A.cols[off + ell_col_pos(k, lane, w)];
+            return c < 0 ? kNone : c;
+        };
+        auto in_own = [&](int64_t c) { return c >= own && c < own + kStageRunLen; };
+        int64_t start[kStageRuns];
+        int k = 0; // this lane's next column not yet covered
+        auto skip = [&](int64_t end) {
+            for (int64_t c = col(k); c != kNone && (c < end || in_own(c)); c = col(++k)) {
+            }
+        };
+        skip(INT64_MIN); // the columns inside run 4 only
+        for (int r = 0; r < kStageRuns; ++r) {
+            if (r == 4) {
+                start[r] = own;
+                continue;
+            }
+            int64_t m = col(k);
+            for (int o = 16; o; o >>= 1) {
+                const int64_t t = __shfl_xor_sync(0xffffffffu, m, o);
+                m = t < m ? t : m;
+            }
+            if (m == kNone) {
+                start[r] = own; // unused: any in-bounds window
+                continue;
+            }
+            start[r] = m - ((m - A.diag_shift) & 1);
+            skip(start[r] + kStageRunLen);
+        }
+        if (col(k) != kNone) atomicOr(bad, 1u);
+        if (lane < kStageRuns) {
+            int64_t v = start[0];
+            for (int r = 1; r < kStageRuns; ++r)
+                if (lane == r) v = start[r];
+            runs[s * kStageRuns + lane] = static_cast<int32_t>(v);
+        }
+        for (int e = 0; e < w; ++e) {
+            const int64_t c = col(e);
+            uint16_t v = kStagePad;
+            if (c != kNone) {
+                int rr = -1;
+                if (in_own(c)) rr = 4;
+                for (int r = 0; r < kStageRuns && rr < 0; ++r)
+                    if (c >= start[r] && c < start[r] + kStageRunLen) rr = r;
+                if (rr >= 0) v = static_cast<uint16_t>(rr * kStageRunLen + (c - start[rr]));
+            }
+            cols16[off + ell_c16_pos(e, lane, w)] = v;
+        }
+    }
+}
+
 #ifdef TW_CHECKS
 // Checked build: one warp per slice, lane = row.
 __global__ void ell_check_kernel(EllView A) {
@@ -292,6 +360,12 @@ __global__ void ell_check_kernel(EllView A) {
 #endif
 
 } // namespace
+
+void launch_csr_runs(const EllView& A, int32_t* runs, uint16_t* cols16, unsigned* bad,
+                     cudaStream_t s) {
+    csr_runs_kernel<<<clamp_blocks(A.n_slices * 32, 4096), kThreads, 0, s>>>(A, runs, cols16, bad);
+    TW_CUDA(cudaGetLastError());
+}
 
 void launch_stencil_cols16(const EllView& A, uint16_t* cols16, unsigned* bad, cudaStream_t s) {
     stencil_cols16_kernel<<<clamp_blocks(A.n_slices * 32, 4096), kThreads, 0, s>>>(A, cols16, bad);

@@ -59,6 +59,11 @@ struct EllView {
     // then stays in L2 across the iteration; measured 128^3 K1 -2.4 %,
     // neutral at 256^3, profiles/r01_ab_k1_k2_k3_variants.md)
     int sx_keep = 0;
+    // run-table form (a CSR matrix whose slices' columns fall into at most 9
+    // windows of 36 doubles, tw_ell_from_csr): the run starts per slice,
+    // int32[n_slices * 9], run 4 = the slice's own rows' window; null for
+    // the closed-form runs of a stencil (sx_* above)
+    const int32_t* sx_runs = nullptr;
 };
 
 // x-staged windows: run r = (dz + 1) * 3 + (dy + 1) of a slice starts 2
@@ -98,6 +103,12 @@ __host__ __device__ inline int64_t stage_run_start(int64_t s, int r, int64_t nx,
     return (in ? zz * ny + yy : z * ny + y) * nx + x0 - 2 - col_off;
 }
 
+// Start of staged run r of slice s, from the run table or the closed form.
+__host__ __device__ inline int64_t run_start(const EllView& A, int64_t s, int r) {
+    return A.sx_runs ? static_cast<int64_t>(A.sx_runs[s * kStageRuns + r])
+                     : stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz, A.sx_row_off, A.sx_col_off);
+}
+
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {
     const int full = w & ~1;
     if (k < full) return 32LL * (k & ~1) + 2 * lane + (k & 1);
@@ -123,7 +134,6 @@ struct CgScalars {
     int history_cap;
     unsigned epoch; // solve number (set_rhs count): high half of the peer flag stamps
     unsigned pad_;
-    unsigned long long alpha_stamp; // folded K1 + K2: alpha of stamp_of(sc, 0) published
 };
 
 // ------------------------------------------------- NVLink peer transport
@@ -170,8 +180,7 @@ enum FinMode : int {
     // total; v -> recv_a / recv_b [rank] of every rank's window over NVLink,
     // then the matching flags get this iteration's stamp (release, .sys)
     FIN_PUBLISH_A = 5,
-    FIN_PUBLISH_B = 6,
-    FIN_ALPHA_GRID = 7 // FIN_ALPHA, then release sc->alpha_stamp (the folded K1 + K2's barrier)
+    FIN_PUBLISH_B = 6
 };
 
 struct PeerLinks;
@@ -231,10 +240,6 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
                      const double* psrc = nullptr, bool pdl = false, double* x = nullptr);
-// K1 with the previous iteration's K3 fused in (single-domain monolithic):
-// Ap = A p_new and p_new . Ap where p_new = r + beta p_old (beta = sc->beta)
-// is formed on the fly from gathers of r and p_old and stored into p_new
-// (a different buffer).  False when the TMA-staged path is unavailable.
 // K1 of the peer transport as one launch (interior, then the two boundary
 // ranges after a per-warp ghost-flag acquire), partials bit-identical to
 // the two launches; pm[0] = interior p.Ap into *fin.pre, fin (FIN_PUBLISH_A)
@@ -242,8 +247,6 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
 bool launch_spmv_split(const EllView& A, const double* x, double* y, RowRange interior,
                        RowRange b0, RowRange b1, RedScratch rs, Fin fin, cudaStream_t s,
                        const unsigned long long* wait_flags, int nwait, bool pdl = false);
-bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
-                       double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s);
 // Transport check: ping_send stores `token` into ping[rank] of every rank's
 // window (release, .sys); ping_check waits (bounded, no trap) until every
 // ping[q] of this rank's window holds it and writes 1 / 0 to *ok.
@@ -278,6 +281,11 @@ int staged_stage_bytes(int max_width, int* val_bytes, int* c16_bytes);
 // stored column falls outside its slice's staged runs (then the matrix
 // stays unstaged).
 void launch_stencil_cols16(const EllView& A, uint16_t* cols16, unsigned* bad, cudaStream_t s);
+// Run table (int32[n_slices * 9]) + 16-bit columns of a general matrix from
+// its 32-bit columns (tw_ell_from_csr); flags *bad if a slice's columns need
+// more than 9 runs of 36 (then the matrix stays unstaged).
+void launch_csr_runs(const EllView& A, int32_t* runs, uint16_t* cols16, unsigned* bad,
+                     cudaStream_t s);
 // K1 on an x-staged matrix: the slice block and its 9 x runs arrive in one
 // TMA transaction per slice; x must have 2 readable doubles of slack before
 // index 0 and after x_len.  The three ranges form ONE index space (walked
@@ -296,23 +304,6 @@ inline bool launch_spmv_staged(const EllView& A, const double* x, double* y, Row
                               nullptr, 0, pdl);
 }
 int spmv_staged_smem_bytes(int max_width);
-// K1 and K2 of the single-domain CG in one cooperative launch (opt-in,
-// TW_FOLD_K2=1): the x-staged K1, a grid barrier on alpha, then r -= alpha Ap
-// (and with x, x += alpha p) streamed through the warps' stages, r.r and the
-// beta commit.  False if unavailable.
-bool launch_spmv_staged_fold_k2(const EllView& A, const double* p_local, double* Ap, double* r,
-                                double* x, const double* p, int64_t n, CgScalars* sc,
-                                double* history, RedScratch rs, cudaStream_t s);
-// K1 with the previous K3 fused in, on an x-staged single-domain matrix:
-// stages the runs of r and p_old, forms p_new = r + beta p_old (sc->beta)
-// in shared memory, Ap = A p_new, p_new.Ap; stores p_new (own rows) and
-// applies x += alpha p_old (sc->alpha).  r and p_old need the staged-x
-// slack (2 doubles each side); p_new must be another buffer.  False if
-// unavailable.
-bool launch_spmv_staged_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
-                              double* x, double* Ap, int64_t n, RedScratch rs, Fin fin,
-                              cudaStream_t s);
-int staged_fusep_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only
 // trailing a row, slice widths within max_width (traps otherwise).
 void launch_ell_check(const EllView& A, cudaStream_t s);

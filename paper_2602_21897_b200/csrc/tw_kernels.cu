@@ -142,76 +142,11 @@ spmv_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, Row
 }
 
 
-// One row with the previous iteration's p update fused in (FUSEP): every
-// operand is p_new[c] = r[c] + beta * p_old[c] (waxpby, cg.cpp:389),
-// rounded exactly as K3 rounds it, gathered from r and p_old.
-template <int W>
-__device__ __forceinline__ double smem_row_fixed_fusep(const double* vb, const int32_t* cb,
-                                                       const double* __restrict__ r,
-                                                       const double* __restrict__ p, double beta,
-                                                       int lane) {
-    int c[W];
-#pragma unroll
-    for (int q = 0; q < W / 4; ++q) {
-        int4 t = reinterpret_cast<const int4*>(cb + 128 * q)[lane];
-        c[4 * q] = t.x;
-        c[4 * q + 1] = t.y;
-        c[4 * q + 2] = t.z;
-        c[4 * q + 3] = t.w;
-    }
-    constexpr int F = W & ~3;
-    if (W - F >= 2) {
-        int2 t = reinterpret_cast<const int2*>(cb + 32 * F)[lane];
-        c[F] = t.x;
-        c[F + 1] = t.y;
-    }
-    if ((W - F) & 1) c[W - 1] = cb[32 * (W - 1) + lane];
-    double rv[W], pv[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        rv[k] = __ldg(r + max(c[k], 0));
-        pv[k] = __ldg(p + max(c[k], 0));
-    }
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < W / 2; ++j) {
-        double2 v = reinterpret_cast<const double2*>(vb + 64 * j)[lane];
-        if (c[2 * j] >= 0)
-            acc = __dadd_rn(acc, __dmul_rn(v.x, __dadd_rn(rv[2 * j], __dmul_rn(beta, pv[2 * j]))));
-        if (c[2 * j + 1] >= 0)
-            acc = __dadd_rn(acc, __dmul_rn(v.y, __dadd_rn(rv[2 * j + 1], __dmul_rn(beta, pv[2 * j + 1]))));
-    }
-    if (W & 1)
-        if (c[W - 1] >= 0)
-            acc = __dadd_rn(acc, __dmul_rn(vb[32 * (W - 1) + lane],
-                                           __dadd_rn(rv[W - 1], __dmul_rn(beta, pv[W - 1]))));
-    return acc;
-}
-
-__device__ __forceinline__ double smem_row_generic_fusep(const double* vb, const int32_t* cb,
-                                                         const double* __restrict__ r,
-                                                         const double* __restrict__ p, double beta,
-                                                         int lane, int w) {
-    double acc = 0.0;
-    for (int k = 0; k < w; ++k) {
-        const int c = cb[ell_col_pos(k, lane, w)];
-        if (c < 0) break;
-        const double pn = __dadd_rn(__ldg(r + c), __dmul_rn(beta, __ldg(p + c)));
-        acc = __dadd_rn(acc, __dmul_rn(vb[ell_val_pos(k, lane, w)], pn));
-    }
-    return acc;
-}
-
-// FUSEP (single-domain monolithic CG): x is p_old, and the kernel also
-// applies the previous iteration's K3 -- gathers p_new from r and p_old,
-// writes p_new for its own rows into pnew (the other buffer of a ping-pong
-// pair, so no block ever reads a p it overwrites) and dots with p_new.
-template <bool DOT, bool FUSEP = false>
+template <bool DOT>
 __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
                 RowRange rb, int stage_bytes, int val_bytes, RedScratch rs, Fin fin,
-                const unsigned long long* wait_flags, int nwait, const double* __restrict__ r,
-                double* __restrict__ pnew) {
+                const unsigned long long* wait_flags, int nwait) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps][kTmaStages];
     __shared__ int stage_w[kTmaWarps][kTmaStages];
@@ -255,7 +190,6 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
     // peer transport: the matrix is already streaming in; the gathers of p
     // wait until the neighbours' ghost planes have landed
     if (nwait) block_wait_flags(wait_flags, nwait, stamp_of(fin.sc, 0));
-    const double beta = FUSEP ? fin.sc->beta : 0.0;
     double part = 0.0;
     for (int64_t k = 0; k < mine; ++k) {
         const int st = static_cast<int>(k % kTmaStages);
@@ -264,35 +198,19 @@ spmv_tma_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
         const double* vb = reinterpret_cast<const double*>(ring + static_cast<size_t>(st) * stage_bytes);
         const int32_t* cb = reinterpret_cast<const int32_t*>(ring + static_cast<size_t>(st) * stage_bytes + val_bytes);
         double acc;
-        if (FUSEP) {
-            switch (w) {
-            case 27: acc = smem_row_fixed_fusep<27>(vb, cb, r, x, beta, lane); break;
-            case 18: acc = smem_row_fixed_fusep<18>(vb, cb, r, x, beta, lane); break;
-            case 12: acc = smem_row_fixed_fusep<12>(vb, cb, r, x, beta, lane); break;
-            case 8: acc = smem_row_fixed_fusep<8>(vb, cb, r, x, beta, lane); break;
-            default: acc = smem_row_generic_fusep(vb, cb, r, x, beta, lane, w); break;
-            }
-        } else {
-            switch (w) {
-            case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
-            case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
-            case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
-            case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
-            default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
-            }
+        switch (w) {
+        case 27: acc = smem_row_fixed<27>(vb, cb, x, lane); break;
+        case 18: acc = smem_row_fixed<18>(vb, cb, x, lane); break;
+        case 12: acc = smem_row_fixed<12>(vb, cb, x, lane); break;
+        case 8: acc = smem_row_fixed<8>(vb, cb, x, lane); break;
+        default: acc = smem_row_generic<true>(vb, cb, x, lane, w); break;
         }
         const int64_t s = slice_of(k);
         const int64_t row = (s << 5) + lane;
         const RowRange rr = (warp_g + k * nwarps) < na ? ra : rb;
         if (row >= rr.r0 && row < rr.r1) {
             y[row] = acc;
-            if (FUSEP) {
-                const double pn = __dadd_rn(__ldg(r + row), __dmul_rn(beta, __ldg(x + row)));
-                pnew[row] = pn;
-                if (DOT) part = __dadd_rn(part, __dmul_rn(pn, acc));
-            } else if (DOT) {
-                part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
-            }
+            if (DOT) part = __dadd_rn(part, __dmul_rn(__ldg(x + row + A.diag_shift), acc));
         }
         __syncwarp();
         if (lane == 0 && k + kTmaStages < mine) {
@@ -502,8 +420,7 @@ __device__ __forceinline__ void staged_spmv_body(
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (int r = 0; r < kStageRuns; ++r) {
-            const int64_t st = stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz, A.sx_row_off,
-                                               A.sx_col_off);
+            const int64_t st = run_start(A, s, r);
             if (KEEP) // small x: keep its lines in L2 (evict_last) for the other runs
                 bulk_g2s(xs + r * kStageRunLen, x + st, kRunBytes, bar, xpol);
             else
@@ -571,182 +488,6 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
     staged_spmv_body<SPLIT, kTmaWarps, true, KEEP>(launch_grid(), A, x, y, ra, rb0, rb1, stage_bytes,
                                              val_bytes, c16_bytes, rs, fin, wait_flags, nwait, smem,
                                              bars, stage_w, phase);
-}
-
-// K1 with the previous iteration's K3 fused in, on an x-staged matrix
-// (single-domain monolithic CG): each slice's transaction carries its
-// values, 16-bit columns and the 9 runs of BOTH r and p_old; the warp forms
-// p_new = r + beta p_old over the runs in shared memory (the roundings of
-// K3), then runs the staged row sums on p_new.  Its own rows also get
-// x += alpha p_old (the x update of the previous iteration) and p_new is
-// stored into the other p buffer.  Per iteration that drops K3's second
-// pass over r and p (the 8 n of p_new's re-read and one launch).  16 warps:
-// the larger stages (both run sets) leave room for no more.
-constexpr int kFuseWarps = 16;
-__global__ void __launch_bounds__(kFuseWarps * 32, 1)
-spmv_staged_fusep_kernel(EllView A, const double* __restrict__ p_old, const double* __restrict__ r,
-                         double* __restrict__ p_new, double* __restrict__ x,
-                         double* __restrict__ y, int64_t n, int stage_bytes, int val_bytes,
-                         int c16_bytes, RedScratch rs, Fin fin) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[kFuseWarps];
-    __shared__ int stage_w[kFuseWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
-    const double* vb = reinterpret_cast<const double*>(stage);
-    const uint16_t* cb = reinterpret_cast<const uint16_t*>(stage + val_bytes);
-    double* ps = reinterpret_cast<double*>(stage + val_bytes + c16_bytes); // p_old -> p_new
-    double* rsx = ps + kStageRuns * kStageRunLen;                           // r runs
-    uint64_t* bar = &bars[warp];
-    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kFuseWarps + warp;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFuseWarps;
-    const int64_t n_slices = (n + 31) >> 5;
-    const int64_t mine = warp_g < n_slices ? (n_slices - warp_g + nwarps - 1) / nwarps : 0;
-    if (lane == 0) mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    const uint64_t pol = l2_evict_first_policy();
-    constexpr uint32_t kRunBytes = kStageRunLen * 8;
-    const double alpha = fin.sc->alpha, beta = fin.sc->beta; // the previous iteration's
-    auto issue = [&](int64_t s) {
-        const int64_t off = A.slice_off[s];
-        const uint32_t ents = static_cast<uint32_t>(A.slice_off[s + 1] - off);
-        TW_DCHECK(s < A.n_slices && ents <= 32u * static_cast<uint32_t>(A.max_width));
-        stage_w[warp] = static_cast<int>(ents >> 5);
-        mbar_expect_tx(bar, ents * 10u + 2u * kStageRuns * kRunBytes);
-        if (ents) {
-            bulk_g2s(stage, A.vals + off, ents * 8u, bar, pol);
-            bulk_g2s(stage + val_bytes, A.cols16 + off, ents * 2u, bar, pol);
-        }
-        for (int q = 0; q < kStageRuns; ++q) {
-            const int64_t st = stage_run_start(s, q, A.sx_nx, A.sx_ny, A.sx_nz);
-            bulk_g2s_plain(ps + q * kStageRunLen, p_old + st, kRunBytes, bar);
-            bulk_g2s_plain(rsx + q * kStageRunLen, r + st, kRunBytes, bar);
-        }
-    };
-    if (lane == 0 && mine > 0) issue(warp_g);
-    __syncwarp();
-    uint32_t phase = 0;
-    double part = 0.0;
-    for (int64_t k = 0; k < mine; ++k) {
-        const int64_t s = warp_g + k * nwarps;
-        mbar_wait(bar, phase & 1u);
-        ++phase;
-        const int64_t row = (s << 5) + lane;
-        const double pold = ps[4 * kStageRunLen + 2 + lane]; // this lane's p_old[row]
-        __syncwarp();
-        for (int i = lane; i < kStageRuns * kStageRunLen; i += 32)
-            ps[i] = __dadd_rn(rsx[i], __dmul_rn(beta, ps[i])); // p_new over the runs (K3's rounding)
-        __syncwarp();
-        const int w = stage_w[warp];
-        double acc;
-        switch (w) {
-        case 27: acc = staged_row_fixed<27>(vb, cb, ps, lane); break;
-        case 18: acc = staged_row_fixed<18>(vb, cb, ps, lane); break;
-        case 12: acc = staged_row_fixed<12>(vb, cb, ps, lane); break;
-        case 8: acc = staged_row_fixed<8>(vb, cb, ps, lane); break;
-        default: acc = staged_row_generic(vb, cb, ps, lane, w); break;
-        }
-        if (row < n) {
-            const double pn = ps[4 * kStageRunLen + 2 + lane];
-            y[row] = acc;
-            p_new[row] = pn;
-            x[row] = __dadd_rn(x[row], __dmul_rn(alpha, pold));
-            part = __dadd_rn(part, __dmul_rn(pn, acc));
-        }
-        __syncwarp();
-        if (lane == 0 && k + 1 < mine) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(s + nwarps);
-        }
-        __syncwarp();
-    }
-    grid_reduce_finalize(part, rs, fin);
-}
-
-// K1 + K2 folded (opt-in): the x-staged K1 over all rows, its last block
-// publishes alpha with a release of sc->alpha_stamp, every block acquires it
-// (grid barrier: cooperative launch, one CTA per SM), then the warps stream
-// r -= alpha Ap (WX: also x += alpha p) through their stages in blocks of
-// `rows` rows and the r.r tree commits beta (FIN_BETA).
-template <bool KEEP, bool WX>
-__global__ void __launch_bounds__(kTmaWarps * 32, 1)
-spmv_staged_fold_k2_kernel(EllView A, const double* __restrict__ p_local, double* Ap,
-                           double* __restrict__ r, double* __restrict__ x,
-                           const double* __restrict__ p, int64_t n, int stage_bytes,
-                           int val_bytes, int c16_bytes, int rows, CgScalars* sc,
-                           double* history, RedScratch rs) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t bars[kTmaWarps];
-    __shared__ int stage_w[kTmaWarps];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) mbar_init(&bars[warp], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    const unsigned long long want = stamp_of(sc, 0); // iter is stable until this kernel's end
-    uint32_t phase = 0;
-    const RowRange none{0, 0};
-    staged_spmv_body<false, kTmaWarps, false, KEEP>(
-        launch_grid(), A, p_local, Ap, RowRange{0, n}, none, none, stage_bytes, val_bytes, c16_bytes,
-        rs, Fin{FIN_ALPHA_GRID, nullptr, sc, nullptr}, nullptr, 0, smem, bars, stage_w, phase);
-    __syncthreads();
-    if (threadIdx.x == 0) thread_wait_flags(&sc->alpha_stamp, 1, want);
-    __syncthreads();
-    const double alpha = __ldcg(&sc->alpha), nalpha = -alpha;
-    // Ap was stored by other CTAs' generic stores: order the TMA reads after the acquire
-    if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-    __syncwarp();
-    unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
-    double* s0 = reinterpret_cast<double*>(stage);
-    double* s1 = s0 + rows;
-    double* s2 = s1 + rows;
-    double* s3 = s2 + rows;
-    uint64_t* bar = &bars[warp];
-    const int64_t warp_g = static_cast<int64_t>(blockIdx.x) * kTmaWarps + warp;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kTmaWarps;
-    const int64_t n2 = n & ~int64_t(1);
-    double part = 0.0;
-    for (int64_t q = warp_g * rows; q < n2; q += nwarps * rows) {
-        const int cnt = static_cast<int>(q + rows < n2 ? rows : n2 - q);
-        const uint32_t bytes = static_cast<uint32_t>(cnt) * 8u;
-        if (lane == 0) {
-            mbar_expect_tx(bar, (WX ? 4u : 2u) * bytes);
-            bulk_g2s_plain(s0, r + q, bytes, bar);
-            bulk_g2s_plain(s1, Ap + q, bytes, bar);
-            if (WX) {
-                bulk_g2s_plain(s2, x + q, bytes, bar);
-                bulk_g2s_plain(s3, p + q, bytes, bar);
-            }
-        }
-        __syncwarp();
-        mbar_wait(bar, phase & 1u);
-        ++phase;
-        for (int i = 2 * lane; i < cnt; i += 64) {
-            double2 rv = *reinterpret_cast<const double2*>(s0 + i);
-            const double2 av = *reinterpret_cast<const double2*>(s1 + i);
-            rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
-            rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-            __stcs(reinterpret_cast<double2*>(r + q + i), rv);
-            part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
-            part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
-            if (WX) {
-                double2 xv = *reinterpret_cast<const double2*>(s2 + i);
-                const double2 pv = *reinterpret_cast<const double2*>(s3 + i);
-                xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
-                xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-                __stcs(reinterpret_cast<double2*>(x + q + i), xv);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (n2 < n && blockIdx.x == 0 && threadIdx.x == 0) { // odd n: the last row
-        const double rv = __dadd_rn(r[n2], __dmul_rn(nalpha, __ldcg(Ap + n2)));
-        r[n2] = rv;
-        part = __dadd_rn(part, __dmul_rn(rv, rv));
-        if (WX) x[n2] = __dadd_rn(x[n2], __dmul_rn(alpha, p[n2]));
-    }
-    grid_reduce_finalize(part, rs, Fin{FIN_BETA, nullptr, sc, history});
 }
 
 // --------------------------------------------------------- K2 / K3 / K4 streams
@@ -1178,9 +919,7 @@ LaunchCfg query_launch_cfg(int sm_count) {
     c.spmv_blocks = sm_count * (occ_spmv > 0 ? occ_spmv : 1);
     c.stream_blocks = sm_count * (occ_stream > 0 ? occ_stream : 1);
     c.threads = kThreads;
-    // TW_SPMV_PLAIN=1 selects the register-path SpMV (A/B comparisons only)
-    const char* plain = std::getenv("TW_SPMV_PLAIN");
-    c.tma_blocks = (plain && plain[0] == '1') ? 0 : sm_count;
+    c.tma_blocks = sm_count;
     return c;
 }
 
@@ -1220,17 +959,17 @@ int spmv_tma_smem_bytes(int max_width) {
 // The TMA-staged SpMV needs one slice block of the widest slice per warp in
 // shared memory; returns false when that does not fit (then the register
 // path runs).  The opt-in shared-memory size is a per-device attribute.
-template <bool DOT, bool FUSEP>
+template <bool DOT>
 static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                             RedScratch rs, Fin fin, cudaStream_t s, const unsigned long long* wait_flags,
-                            int nwait, const double* r, double* pnew, bool pdl = false) {
+                            int nwait, bool pdl = false) {
     if (A.max_width <= 0 || A.tma_blocks <= 0) return false;
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int64_t ns = slices(a) + slices(b);
     int vb;
     const int stage = tma_stage_bytes(A.max_width, &vb);
     const int smem = kTmaWarps * kTmaStages * stage;
-    auto kern = spmv_tma_kernel<DOT, FUSEP>;
+    auto kern = spmv_tma_kernel<DOT>;
     constexpr int kMaxDev = 64;
     static std::mutex mu;
     static int attr_bytes[kMaxDev] = {};
@@ -1251,7 +990,7 @@ static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRan
     const int64_t need = (ns + kTmaWarps - 1) / kTmaWarps;
     const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
     launch_k(kern, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, a, b, stage, vb, rs, fin,
-             wait_flags, nwait, r, pnew);
+             wait_flags, nwait);
     TW_CUDA(cudaGetLastError());
     return true;
 }
@@ -1259,10 +998,8 @@ static bool launch_spmv_tma(const EllView& A, const double* x, double* y, RowRan
 void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRange b,
                  bool with_dot, RedScratch rs, Fin fin, int blocks, cudaStream_t s,
                  const unsigned long long* wait_flags, int nwait, bool pdl) {
-    if (with_dot ? launch_spmv_tma<true, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr,
-                                                nullptr, pdl)
-                 : launch_spmv_tma<false, false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, nullptr,
-                                                 nullptr, pdl))
+    if (with_dot ? launch_spmv_tma<true>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, pdl)
+                 : launch_spmv_tma<false>(A, x, y, a, b, rs, fin, s, wait_flags, nwait, pdl))
         return;
     auto slices = [](RowRange q) { return q.r1 > q.r0 ? ((q.r1 + 31) >> 5) - (q.r0 >> 5) : 0; };
     const int g = clamp_blocks((slices(a) + slices(b)) * 32, blocks);
@@ -1391,97 +1128,9 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
     return true;
 }
 
-bool launch_spmv_staged_fold_k2(const EllView& A, const double* p_local, double* Ap, double* r,
-                                double* x, const double* p, int64_t n, CgScalars* sc,
-                                double* history, RedScratch rs, cudaStream_t s) {
-    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0 || n < 2) return false;
-    int vb, cb;
-    const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
-    const int smem = kTmaWarps * stage;
-    const bool keep = A.sx_keep != 0, wx = x != nullptr;
-    using K = decltype(&spmv_staged_fold_k2_kernel<false, false>);
-    const K kern = keep ? (wx ? spmv_staged_fold_k2_kernel<true, true> : spmv_staged_fold_k2_kernel<true, false>)
-                        : (wx ? spmv_staged_fold_k2_kernel<false, true>
-                              : spmv_staged_fold_k2_kernel<false, false>);
-    {
-        static std::mutex mu;
-        std::lock_guard<std::mutex> lk(mu);
-        cudaFuncAttributes fa;
-        TW_CUDA(cudaFuncGetAttributes(&fa, kern));
-        if (smem + static_cast<int>(fa.sharedSizeBytes) > 227 * 1024) return false;
-        TW_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    }
-    // rows per stage block: 2 (or 4) operands, multiples of 64 rows
-    const int rows = (stage / (wx ? 32 : 16)) & ~63;
-    if (rows < 128) return false;
-    int dev = 0, sms = 0, occ = 0;
-    TW_CUDA(cudaGetDevice(&dev));
-    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaWarps * 32, smem));
-    // the grid barrier needs every CTA resident: the persistent grid, one per SM
-    const int g = A.tma_blocks;
-    if (occ < 1 || g > occ * sms) return false;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g);
-    cfg.blockDim = dim3(kTmaWarps * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    TW_CUDA(cudaLaunchKernelEx(&cfg, kern, A, p_local, Ap, r, x, p, n, stage, vb, cb, rows, sc,
-                               history, rs));
-    return true;
-}
-
 int spmv_staged_smem_bytes(int max_width) {
     int vb, cb;
     return kTmaWarps * staged_stage_bytes(max_width, &vb, &cb);
-}
-
-int staged_fusep_smem_bytes(int max_width) {
-    int vb, cb;
-    return kFuseWarps * (staged_stage_bytes(max_width, &vb, &cb) +
-                         (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128);
-}
-
-bool launch_spmv_staged_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
-                              double* x, double* Ap, int64_t n, RedScratch rs, Fin fin,
-                              cudaStream_t s) {
-    if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
-    int vb, cb;
-    const int stage = staged_stage_bytes(A.max_width, &vb, &cb) +
-                      (kStageRuns * kStageRunLen * 8 + 127) / 128 * 128;
-    const int smem = kFuseWarps * stage;
-    static std::mutex mu;
-    static int attr_bytes[64] = {};
-    int dev = 0;
-    TW_CUDA(cudaGetDevice(&dev));
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        cudaFuncAttributes fa;
-        TW_CUDA(cudaFuncGetAttributes(&fa, spmv_staged_fusep_kernel));
-        if (dev >= 64 || smem + static_cast<int>(fa.sharedSizeBytes) > 227 * 1024) return false;
-        if (attr_bytes[dev] < smem) {
-            TW_CUDA(cudaFuncSetAttribute(spmv_staged_fusep_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_bytes[dev] = smem;
-        }
-    }
-    const int64_t ns = (n + 31) / 32, need = (ns + kFuseWarps - 1) / kFuseWarps;
-    const int g = static_cast<int>(need < A.tma_blocks ? (need < 1 ? 1 : need) : A.tma_blocks);
-    spmv_staged_fusep_kernel<<<g, kFuseWarps * 32, smem, s>>>(A, p_old, r, p_new, x, Ap, n, stage, vb,
-                                                              cb, rs, fin);
-    TW_CUDA(cudaGetLastError());
-    return true;
-}
-
-bool launch_spmv_fusep(const EllView& A, const double* r, const double* p_old, double* p_new,
-                       double* Ap, int64_t n, RedScratch rs, Fin fin, cudaStream_t s) {
-    return launch_spmv_tma<true, true>(A, p_old, Ap, RowRange{0, n}, RowRange{0, 0}, rs, fin, s,
-                                       nullptr, 0, r, p_new);
 }
 
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,

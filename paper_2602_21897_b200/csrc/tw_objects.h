@@ -35,6 +35,7 @@ private:
     mutable std::mutex mu_;
     std::condition_variable cv_;
     std::deque<int> free_;
+    std::vector<char> held_; // held_[i]: stream i is acquired (release checks it)
 };
 
 // Task-aware completion layer over CUDA events: the TACUDA mechanism of
@@ -137,6 +138,7 @@ struct tw_ell {
     double* vals = nullptr;
     int32_t* cols = nullptr;
     uint16_t* cols16 = nullptr; // x-staged columns (stencil or z-slab, nx % 32 == 0), or null
+    int32_t* runs = nullptr;    // run table of a staged CSR matrix (EllView::sx_runs), or null
     tw::EllView view() const {
         tw::EllView v{slice_off, vals, cols, info.n_rows, info.n_slices, diag_shift,
                       info.max_width, ctx->cfg.tma_blocks, info.x_len};
@@ -148,6 +150,7 @@ struct tw_ell {
             v.sx_row_off = info.row_offset;
             v.sx_col_off = info.col_offset;
             v.sx_keep = info.x_len <= (int64_t(1) << 23) ? 1 : 0;
+            v.sx_runs = runs;
         }
         return v;
     }

@@ -69,6 +69,7 @@ void StreamPool::init(int device, unsigned capacity) {
         TW_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         streams_.push_back(s);
         free_.push_back(static_cast<int>(i));
+        held_.push_back(0);
     }
 }
 
@@ -76,6 +77,7 @@ void StreamPool::destroy() {
     for (auto s : streams_) cudaStreamDestroy(s);
     streams_.clear();
     free_.clear();
+    held_.clear();
 }
 
 int StreamPool::acquire() {
@@ -83,12 +85,19 @@ int StreamPool::acquire() {
     cv_.wait(lk, [this] { return !free_.empty(); });
     int i = free_.front();
     free_.pop_front();
+    held_[static_cast<size_t>(i)] = 1;
     return i;
 }
 
+// Releasing a stream that is not held (never acquired, or released twice)
+// is API misuse, as QueuePool::release treats it (task_aware.cpp:150-153):
+// accepting it would hand one stream to two later acquirers.
 void StreamPool::release(int idx) {
     {
         std::lock_guard lk(mu_);
+        if (idx < 0 || static_cast<size_t>(idx) >= held_.size() || !held_[static_cast<size_t>(idx)])
+            contract_error("release of a pool stream that is not held");
+        held_[static_cast<size_t>(idx)] = 0;
         free_.push_back(idx);
     }
     cv_.notify_one();
@@ -171,10 +180,10 @@ size_t TaskAware::poll_once() {
             it = binds_.erase(it);
             ++done;
         }
+        polled_ += done; // under the lock: polled() never runs ahead of binds_
     }
     // the callbacks run outside the lock: they may bind further events
     for (auto& f : fire) f.first(f.second);
-    polled_ += done;
     return done;
 }
 
@@ -265,6 +274,7 @@ static void free_ell(tw_ell* A) {
     cudaFree(A->vals);
     cudaFree(A->cols);
     cudaFree(A->cols16);
+    cudaFree(A->runs);
     delete A;
 }
 
@@ -325,6 +335,54 @@ extern "C" int tw_slab_partition(int64_t nz, int rank, int nranks, int64_t* z_be
 
 namespace tw {
 
+// The x-staged form the CG's K1 reads (EllView::cols16), built from the
+// int32 columns:
+//  * a stencil matrix or z-slab with nx % 32 == 0: every slice is one x-line
+//    segment and its 9 runs follow from the geometry (stage_run_start);
+//  * any other matrix (stencils with nx % 32 != 0, tw_ell_from_csr): a
+//    per-slice run table -- run 4 the window of the slice's own rows, the
+//    other 8 cover the remaining columns greedily -- when every slice's
+//    columns fit in 9 runs (any 27-point stencil does: the rows of a slice
+//    are contiguous, so each (dz, dy) neighbour offset spans 34 columns).
+// A matrix that does not fit stays unstaged (the gather K1 reads it).
+static void build_x_staged(tw_ell* A, cudaStream_t s) {
+    const tw_ell_info_t& in = A->info;
+    if (A->cols16 || in.n_rows == 0 || in.max_width <= 0) return;
+    if (spmv_staged_smem_bytes(static_cast<int>(in.max_width)) + 2048 > 227 * 1024) return;
+    const bool stencil = in.nx > 0 && in.nx % 32 == 0;
+    const int64_t ents = in.ell_entries;
+    unsigned* bad = nullptr;
+    TW_CUDA(cudaMalloc(&A->cols16, sizeof(uint16_t) * static_cast<size_t>(ents + 64)));
+    if (!stencil)
+        TW_CUDA(cudaMalloc(&A->runs, sizeof(int32_t) * kStageRuns * static_cast<size_t>(in.n_slices)));
+    TW_CUDA(cudaMalloc(&bad, sizeof(unsigned)));
+    TW_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
+    if (stencil) {
+        launch_stencil_cols16(A->view(), A->cols16, bad, s); // reads the 32-bit columns
+    } else {
+        EllView v = A->view();
+        v.cols16 = nullptr; // not built yet
+        launch_csr_runs(v, A->runs, A->cols16, bad, s);
+    }
+    unsigned hbad = 0;
+    TW_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    TW_CUDA(cudaStreamSynchronize(s));
+    cudaFree(bad);
+    if (hbad) { // not representable: stay unstaged
+        cudaFree(A->cols16);
+        cudaFree(A->runs);
+        A->cols16 = nullptr;
+        A->runs = nullptr;
+    }
+}
+
+static void drop_x_staged(tw_ell* A) {
+    cudaFree(A->cols16);
+    cudaFree(A->runs);
+    A->cols16 = nullptr;
+    A->runs = nullptr;
+}
+
 // gen_stencil_matrix (csr.cpp:29-59) for the slab [z_begin, z_end).
 static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t zb,
                            int64_t ze) {
@@ -361,27 +419,7 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
 #ifdef TW_CHECKS
         launch_ell_check(A->view(), s);
 #endif
-        // The x-staged form for the CG's K1: slices are whole x-line
-        // segments when nx % 32 == 0 (the slab's first row is a plane
-        // start); TW_STAGE_X=0 turns it off (A/B).
-        const char* sx = std::getenv("TW_STAGE_X");
-        if (nx % 32 == 0 && !(sx && sx[0] == '0') &&
-            spmv_staged_smem_bytes(static_cast<int>(in.max_width)) + 2048 <= 227 * 1024) {
-            const int64_t ents = in.ell_entries;
-            unsigned* bad = nullptr;
-            TW_CUDA(cudaMalloc(&A->cols16, sizeof(uint16_t) * static_cast<size_t>(ents + 64)));
-            TW_CUDA(cudaMalloc(&bad, sizeof(unsigned)));
-            TW_CUDA(cudaMemsetAsync(bad, 0, sizeof(unsigned), s));
-            launch_stencil_cols16(A->view(), A->cols16, bad, s); // reads the 32-bit columns
-            unsigned hbad = 0;
-            TW_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
-            TW_CUDA(cudaStreamSynchronize(s));
-            cudaFree(bad);
-            if (hbad) { // not representable (should not happen for a stencil): stay unstaged
-                cudaFree(A->cols16);
-                A->cols16 = nullptr;
-            }
-        }
+        build_x_staged(A, s);
         TW_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaFree(widths);
@@ -435,6 +473,7 @@ static tw_ell* from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
 #ifdef TW_CHECKS
         launch_ell_check(A->view(), s);
 #endif
+        build_x_staged(A, s);
         TW_CUDA(cudaStreamSynchronize(s));
     } catch (...) {
         cudaFree(d_rp);
@@ -451,37 +490,74 @@ static tw_ell* from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
     return A;
 }
 
-static void to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values) {
+// Rows [r0, r1) of A as CSR with global columns; row_ptr relative to r0
+// (r1 - r0 + 1 entries).  Copies only the slices the range touches, so a
+// matrix whose CSR does not fit host memory is exported a z-slab at a time.
+// staged: decode the 16-bit x-staged columns (the form the CG's K1 reads)
+// through the slices' run starts instead of reading the int32 columns.
+static void to_csr_rows(const tw_ell* A, int64_t r0, int64_t r1, bool staged, int64_t* row_ptr,
+                        int64_t* col_idx, double* values) {
     const tw_ell_info_t& in = A->info;
-    std::vector<int64_t> off(static_cast<size_t>(in.n_slices + 1));
-    std::vector<double> v(static_cast<size_t>(in.ell_entries));
-    std::vector<int32_t> c(static_cast<size_t>(in.ell_entries));
-    TW_CUDA(cudaMemcpy(off.data(), A->slice_off, sizeof(int64_t) * (in.n_slices + 1),
+    if (r0 < 0 || r1 > in.n_rows || r0 > r1) contract_error("csr export row range out of bounds");
+    if (staged && !A->cols16) contract_error("matrix has no x-staged form");
+    row_ptr[0] = 0;
+    if (r0 == r1) return;
+    const int64_t s0 = r0 / 32, s1 = (r1 + 31) / 32;
+    std::vector<int64_t> off(static_cast<size_t>(s1 - s0 + 1));
+    TW_CUDA(cudaMemcpy(off.data(), A->slice_off + s0, sizeof(int64_t) * off.size(),
                        cudaMemcpyDeviceToHost));
-    if (in.ell_entries) {
-        TW_CUDA(cudaMemcpy(v.data(), A->vals, sizeof(double) * in.ell_entries, cudaMemcpyDeviceToHost));
-        TW_CUDA(cudaMemcpy(c.data(), A->cols, sizeof(int32_t) * in.ell_entries, cudaMemcpyDeviceToHost));
+    const int64_t e0 = off.front(), ents = off.back() - e0;
+    std::vector<double> v(static_cast<size_t>(ents));
+    std::vector<int32_t> c(staged ? 0 : static_cast<size_t>(ents));
+    std::vector<uint16_t> c16(staged ? static_cast<size_t>(ents) : 0);
+    std::vector<int32_t> runs(staged && A->runs ? static_cast<size_t>(kStageRuns * (s1 - s0)) : 0);
+    if (!runs.empty())
+        TW_CUDA(cudaMemcpy(runs.data(), A->runs + kStageRuns * s0, sizeof(int32_t) * runs.size(),
+                           cudaMemcpyDeviceToHost));
+    if (ents) {
+        TW_CUDA(cudaMemcpy(v.data(), A->vals + e0, sizeof(double) * ents, cudaMemcpyDeviceToHost));
+        if (staged)
+            TW_CUDA(cudaMemcpy(c16.data(), A->cols16 + e0, sizeof(uint16_t) * ents,
+                               cudaMemcpyDeviceToHost));
+        else
+            TW_CUDA(cudaMemcpy(c.data(), A->cols + e0, sizeof(int32_t) * ents,
+                               cudaMemcpyDeviceToHost));
     }
     int64_t k = 0;
-    row_ptr[0] = 0;
-    for (int64_t row = 0; row < in.n_rows; ++row) {
+    for (int64_t row = r0; row < r1; ++row) {
         const int64_t s = row / 32;
         const int lane = static_cast<int>(row % 32);
-        const int w = static_cast<int>((off[s + 1] - off[s]) / 32);
+        const int64_t base = off[s - s0] - e0;
+        const int w = static_cast<int>((off[s - s0 + 1] - off[s - s0]) / 32);
         bool padded = false;
         for (int e = 0; e < w; ++e) {
-            const int32_t col = c[static_cast<size_t>(off[s] + ell_col_pos(e, lane, w))];
+            int64_t col;
+            if (staged) {
+                const uint16_t j = c16[static_cast<size_t>(base + ell_c16_pos(e, lane, w))];
+                const int r = j / kStageRunLen;
+                const int64_t st =
+                    runs.empty() ? stage_run_start(s, r, in.nx, in.ny, in.nz, in.row_offset,
+                                                   in.col_offset)
+                                 : runs[static_cast<size_t>((s - s0) * kStageRuns + r)];
+                col = j == kStagePad ? -1 : st + j % kStageRunLen;
+            } else {
+                col = c[static_cast<size_t>(base + ell_col_pos(e, lane, w))];
+            }
             if (col < 0) {
                 padded = true;
                 continue;
             }
             if (padded) contract_error("ELL row " + std::to_string(row) + " has an entry after padding");
-            col_idx[k] = static_cast<int64_t>(col) + in.col_offset;
-            values[k] = v[static_cast<size_t>(off[s] + ell_val_pos(e, lane, w))];
+            col_idx[k] = col + in.col_offset;
+            values[k] = v[static_cast<size_t>(base + ell_val_pos(e, lane, w))];
             ++k;
         }
-        row_ptr[row + 1] = k;
+        row_ptr[row - r0 + 1] = k;
     }
+}
+
+static void to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values) {
+    to_csr_rows(A, 0, A->info.n_rows, false, row_ptr, col_idx, values);
 }
 
 void tile_plan(const tw_ell* A, int tiles, std::vector<int64_t>& r0, std::vector<int64_t>& r1,
@@ -870,11 +946,31 @@ int tw_ell_x_staged(const tw_ell* A, int* staged) {
     });
 }
 
+int tw_ell_set_x_staged(tw_ell* A, int enable, int* staged) {
+    return guarded([&] {
+        check_ell(A);
+        TW_CUDA(cudaSetDevice(A->ctx->device));
+        TW_CUDA(cudaStreamSynchronize(A->ctx->compute));
+        if (enable) build_x_staged(A, A->ctx->compute);
+        else drop_x_staged(A);
+        if (staged) *staged = A->cols16 ? 1 : 0;
+    });
+}
+
 int tw_ell_to_csr(const tw_ell* A, int64_t* row_ptr, int64_t* col_idx, double* values) {
     return guarded([&] {
         check_ell(A);
         TW_CUDA(cudaSetDevice(A->ctx->device));
         to_csr(A, row_ptr, col_idx, values);
+    });
+}
+
+int tw_ell_to_csr_rows(const tw_ell* A, int64_t row_begin, int64_t row_end, int staged,
+                       int64_t* row_ptr, int64_t* col_idx, double* values) {
+    return guarded([&] {
+        check_ell(A);
+        TW_CUDA(cudaSetDevice(A->ctx->device));
+        to_csr_rows(A, row_begin, row_end, staged != 0, row_ptr, col_idx, values);
     });
 }
 

@@ -273,6 +273,13 @@ class EllMatrix:
         N.check(_lib().tw_ell_x_staged(self.h, C.byref(v)))
         return bool(v.value)
 
+    def set_x_staged(self, enable: bool) -> bool:
+        """Build or drop the x-staged form (K1's 16-bit columns); returns
+        whether the matrix carries it afterwards."""
+        v = C.c_int()
+        N.check(_lib().tw_ell_set_x_staged(self.h, int(enable), C.byref(v)))
+        return bool(v.value)
+
     def to_csr(self):
         """(row_ptr int64[n+1], col_idx int64[nnz], values f64[nnz]), global columns."""
         n, nnz = self.n, self.nnz()
@@ -282,6 +289,18 @@ class EllMatrix:
         N.check(_lib().tw_ell_to_csr(self.h, rp.ctypes.data_as(N.lp), ci.ctypes.data_as(N.lp),
                                      va.ctypes.data_as(N.dp)))
         return rp, ci, va
+
+    def to_csr_rows(self, r0: int, r1: int, staged: bool = False):
+        """Rows [r0, r1) as (row_ptr relative to r0, col_idx global, values);
+        staged=True decodes the 16-bit x-staged columns the CG's K1 reads."""
+        cap = self.info.max_width * (r1 - r0)
+        rp = np.empty(r1 - r0 + 1, np.int64)
+        ci = np.empty(cap, np.int64)
+        va = np.empty(cap, np.float64)
+        N.check(_lib().tw_ell_to_csr_rows(self.h, r0, r1, int(staged), rp.ctypes.data_as(N.lp),
+                                          ci.ctypes.data_as(N.lp), va.ctypes.data_as(N.dp)))
+        k = int(rp[-1])
+        return rp, ci[:k], va[:k]
 
     def validate(self):
         """CsrMatrix::validate (csr.cpp:13-27) on the converted structure."""
@@ -517,6 +536,12 @@ class CgOptions:
     use_graph: bool = False
     persistent: bool = False  # tasks variant: one persistent kernel runs the whole DAG
     auto_dispatch: bool = False  # TW_DISPATCH_AUTO: persistent for > 8 tiles on one rank
+    # placement / tuning (no result bit changes, except the dispatcher's chunk
+    # sizes, which set its chunk-order reduction tree): None = the library's choice
+    x_update: str | None = None   # "k2" | "k3": where x += alpha p runs
+    l2_keep: bool | None = None   # staged K1: x runs with an L2 evict_last hint
+    dag_spmv_slices: int = 0
+    dag_vec_rows: int = 0
 
     def to_c(self, variant: int) -> N.CgOptionsC:
         if self.backend != CgBackend.cuda:
@@ -530,6 +555,10 @@ class CgOptions:
         o.tol = float(self.tol)
         o.dispatch = (N.TW_DISPATCH_PERSISTENT if self.persistent else
                       N.TW_DISPATCH_AUTO if self.auto_dispatch else N.TW_DISPATCH_STREAMS)
+        o.x_update = {None: 0, "k2": 1, "k3": 2}[self.x_update]
+        o.l2_keep = 0 if self.l2_keep is None else (1 if self.l2_keep else 2)
+        o.dag_spmv_slices = int(self.dag_spmv_slices)
+        o.dag_vec_rows = int(self.dag_vec_rows)
         return o
 
 
@@ -663,6 +692,15 @@ class CgSolver:
         N.check(_lib().tw_cg_launches_per_iteration(self.h, C.byref(k), C.byref(c)))
         return k.value, c.value
 
+    def mode(self) -> dict:
+        """What this solver executes (tw_cg_mode): K1 form, x-run L2 policy,
+        x-update placement, dispatch, transport, launches per iteration."""
+        m = N.CgMode()
+        N.check(_lib().tw_cg_mode(self.h, C.byref(m)))
+        d = {k: getattr(m, k) for k, _ in N.CgMode._fields_}
+        d["k1_kernel"] = N.TW_K1_NAMES[m.k1_form]
+        return d
+
 
 class EmulatedRankGroup:
     """P z-slab ranks on ONE device, driven together (tw_cg_group_*): the
@@ -670,21 +708,24 @@ class EmulatedRankGroup:
     Test infrastructure for the multi-rank path on a single B200."""
 
     def __init__(self, nx: int, ny: int, nz: int, nranks: int, max_iterations: int,
-                 device: int = 0, transport: str = "loopback"):
+                 device: int = 0, transport: str = "loopback", x_staged: bool = True,
+                 options: CgOptions | None = None):
         if transport not in ("loopback", "peer"):
             raise ValueError(f"unknown transport {transport!r}")
         self.P = nranks
         self.transport = transport
         self.rts, self.mats, self.solvers = [], [], []
+        opt = options or CgOptions(iteration_marks=False)
         for r in range(nranks):
             rt = Runtime(device)
             rt.init_emulated_rank(r, nranks)
             zb, ze = slab_partition(nz, r, nranks)
             A = gen_stencil_matrix(nx, ny, nz, rt=rt, z_begin=zb, z_end=ze)
+            if not x_staged:
+                A.set_x_staged(False)
             self.rts.append(rt)
             self.mats.append(A)
-            self.solvers.append(CgSolver(rt, A, max_iterations,
-                                         CgOptions(iteration_marks=False),
+            self.solvers.append(CgSolver(rt, A, max_iterations, opt,
                                          variant=N.TW_CG_MONOLITHIC))
         self._arr = (C.c_void_p * nranks)(*[s.h.value for s in self.solvers])
         if transport == "peer":

@@ -65,3 +65,24 @@ def check_history(got, want, rel=1e-10, window=1e-15):
     assert np.all(g[inside] <= rel), (np.argmax(g * inside), g[inside].max())
     assert np.all(np.abs(got - want)[~inside] <= rel * res0)
     return float(g[inside].max()) if inside.any() else 0.0
+
+
+GOLDEN_256 = os.path.join(ROOT, "tests", "golden", "hpccg_golden_256.npz")
+
+
+@pytest.fixture(scope="session")
+def golden256():
+    """The reference's own 256^3 outputs (tests/golden/make_golden_256.py)."""
+    return np.load(GOLDEN_256)
+
+
+def csr_digests(row_ptr, col_idx, values):
+    """SHA-256 of (row_ptr relative to its first entry, col_idx, values) as
+    int64 / int64 / f64 bytes: make_golden_256.py's per-plane digest."""
+    import hashlib
+    rp = np.ascontiguousarray(np.asarray(row_ptr, np.int64) - int(row_ptr[0]))
+    out = np.zeros((3, 32), np.uint8)
+    for j, arr in enumerate((rp, np.ascontiguousarray(col_idx, np.int64),
+                             np.ascontiguousarray(values, np.float64))):
+        out[j] = np.frombuffer(hashlib.sha256(arr.tobytes()).digest(), np.uint8)
+    return out

@@ -23,14 +23,37 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_struct_layout():
     lib = N.load()
-    assert lib.tw_abi_version() == 2
+    assert lib.tw_abi_version() == 3
     assert C.sizeof(N.EllInfo) == 13 * 8 + 2 * 4
-    assert C.sizeof(N.CgOptionsC) == 4 * 5 + 4 + 8 + 8  # 5 ints + pad + double + int + pad
     o = N.CgOptionsC()
     lib.tw_cg_options_default(C.byref(o))
     # CgOptions defaults (cg.hpp:37-45): tiles 16, stream pool 4, marks on, tol 0
     assert (o.variant, o.tiles, o.stream_pool_capacity, o.iteration_marks, o.tol, o.dispatch) == \
         (N.TW_CG_TASKS, 16, 4, 1, 0.0, N.TW_DISPATCH_AUTO)
+    assert (o.x_update, o.l2_keep, o.dag_spmv_slices, o.dag_vec_rows) == (0, 0, 0, 0)
+
+
+def test_struct_layout_matches_the_c_header(tmp_path):
+    """The ctypes mirrors of the ABI structs against the C compiler's own
+    layout of include/tw_hpccg.h (sizeof and every field offset)."""
+    structs = {"tw_cg_options": N.CgOptionsC, "tw_ell_info_t": N.EllInfo, "tw_slab_t": N.SlabPlan,
+               "tw_cg_mode_t": N.CgMode}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "tw_hpccg.h"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(N.HEADER), "-o", str(exe), str(src)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                  check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == C.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, (cname, f)
 
 
 def test_exports_are_plain_c():

@@ -1,0 +1,162 @@
+"""GPU parity at the sizes the bench numbers are quoted on: BASELINE
+configs[2] (256^3 per GPU, b = xorshift64 seed 7 -- the headline) and
+configs[3] (512^3), through the exact kernel instantiations the headline runs
+(spmv_tma_staged_kernel<SPLIT=0, KEEP=0> with the x update in K3, one-iteration
+CUDA graph) and the other executors at that size.
+
+Checks:
+  * K0 structure at 256^3 bit-exact against the REFERENCE's own
+    gen_stencil_matrix (per-z-plane SHA-256 of row_ptr / col_idx / values,
+    tests/golden/hpccg_golden_256.npz), for both column forms the library
+    keeps (int32, and the 16-bit x-staged columns K1 reads, decoded);
+  * the 256^3 residual history (60 iterations) against the reference's own
+    cg_reference history under the window rule, the final x against the
+    committed sample of the reference's x and elementwise against the
+    threaded oracle (itself pinned to that sample and history bit for bit);
+  * 512^3 x 4 iterations against the threaded matrix-free oracle.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2602_21897_b200 as P
+from paper_2602_21897_b200 import _native as N
+
+from conftest import check_history, csr_digests, rel_gap
+
+pytestmark = pytest.mark.gpu
+
+D = 256
+ITERS = 60
+
+
+@pytest.fixture(scope="module")
+def A256(rt):
+    A = P.gen_stencil_matrix(D, D, D, rt=rt)
+    yield A
+    del A
+
+
+@pytest.fixture(scope="module")
+def oracle256(orc, golden256):
+    """The threaded oracle's 256^3 solve, pinned to the reference fixture."""
+    b = orc.rhs_xorshift(D ** 3, 7)
+    h, x = orc.cg_stencil_mt(D, D, D, b, ITERS)
+    assert np.array_equal(h, golden256["cg_256_xorshift7_history"])
+    idx = golden256["cg_256_xorshift7_x_idx"]
+    assert np.array_equal(x[idx], golden256["cg_256_xorshift7_x_val"])
+    assert math.fsum(x) == golden256["cg_256_xorshift7_x_fsum"][0]
+    return h, x
+
+
+def test_k0_structure_256_vs_reference(A256, golden256, orc):
+    plane = D * D
+    dg = golden256["csr_256_plane_digests"]
+    assert A256.nnz() == int(golden256["csr_256_nnz"][0])
+    assert A256.x_staged
+    chunk = 16
+    for staged in (False, True):
+        for z0 in range(0, D, chunk):
+            rp, ci, va = A256.to_csr_rows(z0 * plane, (z0 + chunk) * plane, staged=staged)
+            for j in range(chunk):
+                k0, k1 = rp[j * plane], rp[(j + 1) * plane]
+                got = csr_digests(rp[j * plane:(j + 1) * plane + 1], ci[k0:k1], va[k0:k1])
+                assert np.array_equal(got, dg[z0 + j]), (staged, z0 + j)
+            if z0 in (0, D - chunk):  # and element for element against the oracle
+                c = orc.stencil_rows(D, D, D, z0 * plane, (z0 + chunk) * plane)
+                assert np.array_equal(rp, c.row_ptr) and np.array_equal(ci, c.col_idx)
+                assert np.array_equal(va, c.values)
+
+
+EXECUTORS = {
+    # the bench headline: monolithic, one-iteration CUDA graph replayed
+    "mono_graph": (N.TW_CG_MONOLITHIC, dict(tiles=1, use_graph=True, iteration_marks=False)),
+    "mono_streams": (N.TW_CG_MONOLITHIC, dict(tiles=1, use_graph=False)),
+    # the same kernels with the x runs kept in L2 (KEEP=1): cache policy only
+    "mono_keep": (N.TW_CG_MONOLITHIC, dict(tiles=1, l2_keep=True)),
+    "mono_x_in_k2": (N.TW_CG_MONOLITHIC, dict(tiles=1, x_update="k2")),
+    # block-task DAG (configs[4] granularities at the per-GPU size)
+    "tasks_T4_graph": (N.TW_CG_TASKS, dict(tiles=4, use_graph=True)),
+    "tasks_T16_streams": (N.TW_CG_TASKS, dict(tiles=16)),
+    "persistent_T64": (N.TW_CG_TASKS, dict(tiles=64, persistent=True)),
+    "persistent_T512": (N.TW_CG_TASKS, dict(tiles=512, persistent=True)),
+}
+
+
+@pytest.mark.parametrize("name", list(EXECUTORS))
+def test_cg_256_vs_reference(rt, A256, golden256, oracle256, name):
+    variant, kw = EXECUTORS[name]
+    S = P.CgSolver(rt, A256, ITERS, P.CgOptions(**kw), variant=variant)
+    m = S.mode()
+    assert m["k1_form"] == N.TW_K1_STAGED  # spmv_tma_staged_kernel
+    if name in ("mono_graph", "mono_streams"):
+        # the headline instantiation: <SPLIT=0, KEEP=0>, x update in K3
+        assert (m["k1_l2_keep"], m["x_in_k3"], m["kernels_per_iteration"]) == (0, 1, 3)
+    if name == "mono_keep":
+        assert m["k1_l2_keep"] == 1
+    if name == "mono_x_in_k2":
+        assert m["x_in_k3"] == 0
+    b = P.rhs_xorshift(rt, A256.n, 7)  # the bench's device generator
+    S.set_rhs(b)
+    S.iterate(10)  # in two calls, as the bench's warm-up + timed passes
+    S.iterate(ITERS - 10)
+    h = S.history(ITERS)
+    x = S.solution()
+    S.close()
+    want_h = golden256["cg_256_xorshift7_history"]
+    worst = check_history(h, want_h)
+    idx = golden256["cg_256_xorshift7_x_idx"]
+    assert np.all(rel_gap(x[idx], golden256["cg_256_xorshift7_x_val"]) <= 1e-10)
+    assert abs(math.fsum(x) - golden256["cg_256_xorshift7_x_fsum"][0]) <= \
+        1e-10 * abs(golden256["cg_256_xorshift7_x_fsum"][0])
+    _, ox = oracle256
+    assert np.all(rel_gap(x, ox) <= 1e-10)
+    print(f"{name}: max history rel gap {worst:.2e}")
+
+
+def test_cg_256_placements_bit_identical(rt, A256):
+    """Cache policy (KEEP) and x-update placement change no bit at the
+    headline size."""
+    b = P.rhs_xorshift(rt, A256.n, 7)
+    out = []
+    for kw in (dict(), dict(l2_keep=True), dict(x_update="k2")):
+        S = P.CgSolver(rt, A256, 20, P.CgOptions(tiles=1, **kw), variant=N.TW_CG_MONOLITHIC)
+        S.set_rhs(b)
+        S.iterate(20)
+        out.append((S.history(20), S.solution()))
+        S.close()
+    for h, x in out[1:]:
+        assert np.array_equal(h, out[0][0]) and np.array_equal(x, out[0][1])
+
+
+def _host_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2 ** 30
+    except Exception:
+        return 0.0
+
+
+def test_cg_512_vs_oracle(rt, orc):
+    """configs[3]'s single-GPU case: 512^3 (3.6e9 nonzeros, 43 GB of sliced
+    ELL) x 4 iterations through the headline path against the threaded
+    matrix-free oracle (the reference's CSR would need 59 GB)."""
+    if _host_gb() < 12:
+        pytest.skip("the 512^3 oracle needs ~7 GB of host memory")
+    E = 512
+    A = P.gen_stencil_matrix(E, E, E, rt=rt)
+    assert A.nnz() == 3609741304 and A.x_staged
+    S = P.CgSolver(rt, A, 4, P.CgOptions(tiles=1, use_graph=True, iteration_marks=False),
+                   variant=N.TW_CG_MONOLITHIC)
+    m = S.mode()
+    assert (m["k1_form"], m["k1_l2_keep"], m["x_in_k3"]) == (N.TW_K1_STAGED, 0, 1)
+    b = orc.rhs_xorshift(E ** 3, 7)
+    S.set_rhs(b)
+    S.iterate(4)
+    h, x = S.history(4), S.solution()
+    S.close()
+    del A
+    want_h, want_x = orc.cg_stencil_mt(E, E, E, b, 4)
+    check_history(h, want_h)
+    assert np.all(rel_gap(x, want_x) <= 1e-10)

@@ -633,54 +633,6 @@ def _read_dev(rt, ptr, n):
     return out
 
 
-@pytest.mark.parametrize("dims", [(30, 20, 18), (64, 20, 18)])
-@pytest.mark.parametrize("graph", [False, True])
-def test_fused_p_update_matches_three_kernel_sequence(rt, orc, graph, dims, monkeypatch):
-    """Single-domain monolithic CG fuses K3 (p = r + beta p) into the next
-    iteration's K1 with p ping-ponging between two buffers (opt-in,
-    TW_FUSE_P=1).  Against the unfused K1/K2/K3 sequence every residual, x and the p
-    left behind by each tw_cg_iterate call must be bit-identical, whatever
-    the split of the iterations into calls (odd splits end in the other
-    buffer and are copied back by the final K3).  On an x-staged matrix
-    (64 x 20 x 18) the fused K1 stages the runs of r and p_old, forms p_new
-    in shared memory and also carries the x update."""
-    from paper_2602_21897_b200 import _native as N
-    A = P.gen_stencil_matrix(*dims, rt=rt)
-    assert A.x_staged == (dims[0] % 32 == 0)
-    b = orc.rhs_xorshift(A.n, 5)
-    splits = [1, 1, 3, 2, 7, 6]
-    total = sum(splits)
-    runs = []
-    for fuse in ("1", "0"):
-        monkeypatch.setenv("TW_FUSE_P", fuse)
-        s = P.CgSolver(rt, A, total, P.CgOptions(use_graph=graph, iteration_marks=False),
-                       variant=N.TW_CG_MONOLITHIC)
-        assert s.launches_per_iteration()[0] == (2 if fuse == "1" else 3)
-        s.set_rhs(b)
-        ps = []
-        for k in splits:
-            s.iterate(k)
-            ps.append(_read_dev(rt, s.vectors()[2], A.n))
-        runs.append((s.history(total), s.solution(), ps))
-        s.close()
-    (h1, x1, p1), (h0, x0, p0) = runs
-    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
-    check_history(h1, want_h)
-    if A.x_staged:
-        # the staged fused K1 runs 16-warp CTAs (both run sets fill shared
-        # memory), so its p.Ap tree differs from the 18-warp K1's: same
-        # per-element roundings, results within the rule
-        check_history(h0, want_h)
-        assert np.all(rel_gap(x1, want_x) <= 1e-10) and np.all(rel_gap(x0, want_x) <= 1e-10)
-        for a, c in zip(p1, p0):
-            assert np.max(np.abs(a - c)) <= 1e-9 * np.max(np.abs(c))
-        return
-    assert np.array_equal(h1, h0)
-    assert np.array_equal(x1, x0)
-    for a, c in zip(p1, p0):
-        assert np.array_equal(a, c)
-
-
 @pytest.mark.parametrize("maxw", [9, 33, 34, 70])
 def test_spmv_generic_widths_tma_and_register_paths(rt, orc, maxw):
     """Random general matrices whose slice widths are mostly outside the
@@ -780,6 +732,12 @@ def test_streams_events_and_task_aware_binding():
     assert x.item() == 1.0
     rt.release_stream(s1)
     rt.release_stream(s2)
+    with pytest.raises(P.ContractViolation):
+        rt.release_stream(s2)  # double release (QueuePool::release, task_aware.cpp:150-153)
+    s3 = rt.acquire_stream()
+    rt.release_stream(s3)
+    with pytest.raises(P.ContractViolation):
+        rt.release_stream(s3)
     ev.close()
     rt.close()
 
@@ -898,20 +856,22 @@ def test_abi_misuse_is_reported_not_crashed(rt):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("dims", [(32, 32, 32), (64, 32, 24), (96, 5, 7), (32, 1, 3)])
-def test_x_staged_k1_bit_identical(rt, orc, dims, monkeypatch):
-    """Single-domain stencil matrices with nx % 32 == 0 carry 16-bit columns
-    into per-slice staged runs of x, and the monolithic CG's K1 reads its
-    operands from shared memory.  Same per-row order and roundings, same
-    reductions: histories and x bit-identical to the gather path
-    (TW_STAGE_X=0), and within the rule of the oracle."""
-    from paper_2602_21897_b200 import _native as N
+@pytest.mark.parametrize("dims", [(32, 32, 32), (64, 32, 24), (96, 5, 7), (32, 1, 3), (30, 20, 18),
+                                  (5, 7, 9)])
+def test_x_staged_k1_bit_identical(rt, orc, dims):
+    """Every stencil matrix carries 16-bit columns into per-slice staged runs
+    of x (closed-form runs for nx % 32 == 0, a per-slice run table
+    otherwise), and the CG's K1 reads its operands from shared memory.  Same
+    per-row order and roundings, same reductions: histories and x
+    bit-identical to the gather path (the staged form dropped), and within
+    the rule of the oracle."""
     b = orc.rhs_xorshift(int(np.prod(dims)), 9)
     out = []
-    for stage in ("1", "0"):
-        monkeypatch.setenv("TW_STAGE_X", stage)
+    for stage in (True, False):
         A = P.gen_stencil_matrix(*dims, rt=rt)
-        assert A.x_staged == (stage == "1")
+        assert A.x_staged
+        if not stage:
+            assert not A.set_x_staged(False)
         for graph in (False, True):
             res = P.cg_monolithic(rt, A, b, 40, P.CgOptions(use_graph=graph))
             out.append((res.residual_history, res.x))
@@ -928,23 +888,86 @@ def test_x_staged_k1_bit_identical(rt, orc, dims, monkeypatch):
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
 
 
+@pytest.mark.parametrize("dims", [(32, 16, 8), (30, 20, 18), (7, 5, 3)])
+def test_csr_drop_in_gets_the_staged_k1(rt, orc, dims):
+    """A caller's CsrMatrix (the reference's gen_stencil_matrix output, here
+    the oracle's bit-identical one) through tw_ell_from_csr gets the x-staged
+    form as a per-slice run table; its CG is bit-identical to the device-
+    generated stencil's, and its staged columns decode to the CSR exactly."""
+    m = orc.stencil(*dims)
+    A = P.ell_from_csr(m.row_ptr, m.col_idx, m.values, rt=rt)
+    assert A.x_staged
+    rp, ci, va = A.to_csr_rows(0, m.n, staged=True)
+    assert np.array_equal(rp, m.row_ptr) and np.array_equal(ci, m.col_idx)
+    assert np.array_equal(va, m.values)
+    G = P.gen_stencil_matrix(*dims, rt=rt)
+    b = orc.rhs_xorshift(m.n, 3)
+    r1 = P.cg_monolithic(rt, A, b, 30, P.CgOptions())
+    r2 = P.cg_monolithic(rt, G, b, 30, P.CgOptions())
+    assert np.array_equal(r1.residual_history, r2.residual_history)
+    assert np.array_equal(r1.x, r2.x)
+    r3 = P.cg_tasks(rt, A, b, 30, P.CgOptions(tiles=8, persistent=True))
+    want_h, want_x, _ = orc.cg(m, b, 30)
+    for r in (r1, r3):
+        check_history(r.residual_history, want_h)
+        assert np.all(rel_gap(r.x, want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_csr_run_table_general_matrix(rt, orc, seed):
+    """A random banded matrix (columns within +-40 of the diagonal, SPD by
+    diagonal dominance): its slices fit 9 runs of 36, so it is staged through
+    the run table; SpMV-driven CG bit-identical to the gather form, and the
+    staged columns decode to the CSR.  A matrix with wide-spread columns
+    stays unstaged (the gather K1)."""
+    rng = np.random.default_rng(seed)
+    n = 3000
+    rows, cols = [], []
+    for i in range(n):
+        c = np.unique(np.clip(i + rng.integers(-40, 41, size=9), 0, n - 1))
+        c = np.union1d(c, [i])
+        rows.append(len(c))
+        cols.append(c)
+    rp = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    ci = np.concatenate(cols).astype(np.int64)
+    va = np.where(ci == np.repeat(np.arange(n), rows), 20.0, -1.0)
+    A = P.ell_from_csr(rp, ci, va, rt=rt)
+    assert A.x_staged
+    r0, c0, v0 = A.to_csr_rows(0, n, staged=True)
+    assert np.array_equal(r0, rp) and np.array_equal(c0, ci) and np.array_equal(v0, va)
+    b = orc.rhs_splitmix(n, seed)
+    s1 = P.cg_monolithic(rt, A, b, 25, P.CgOptions())
+    assert not A.set_x_staged(False)
+    s2 = P.cg_monolithic(rt, A, b, 25, P.CgOptions())
+    assert np.array_equal(s1.residual_history, s2.residual_history) and np.array_equal(s1.x, s2.x)
+    from oracle import Csr
+    want_h, _, _ = orc.cg(Csr(n, rp, ci, va), b, 25)
+    check_history(s1.residual_history, want_h)
+    # spread columns: row i also touches column (i * 7919) % n
+    ci2 = [np.union1d(c, [(i * 7919) % n]) for i, c in enumerate(cols)]
+    rp2 = np.concatenate([[0], np.cumsum([len(c) for c in ci2])]).astype(np.int64)
+    ci2 = np.concatenate(ci2).astype(np.int64)
+    va2 = np.where(ci2 == np.repeat(np.arange(n), np.diff(rp2)), 30.0, -1.0)
+    B = P.ell_from_csr(rp2, ci2, va2, rt=rt)
+    assert not B.x_staged
+
+
 @pytest.mark.parametrize("dims,P_", [((64, 24, 40), 4), ((32, 8, 32), 8), ((32, 4, 4), 4),
-                                     ((320, 288, 12), 2)])
-def test_x_staged_slabs_multi_rank(orc, dims, P_, monkeypatch):
+                                     ((320, 288, 12), 2), ((30, 20, 18), 3)])
+def test_x_staged_slabs_multi_rank(orc, dims, P_):
     """z-slab matrices with nx % 32 == 0 are x-staged too: their staged runs
     reach into the ghost planes (global line geometry, local columns).  The
     NCCL-path phases (loopback) and the peer transport -- whose boundary
     slices stage x only after the ghost-plane flags are acquired, in one
     launch on the 320x288 planes -- must agree to the bit, and both within
-    the rule of the oracle; the gather slabs (TW_STAGE_X=0) too."""
+    the rule of the oracle; the gather slabs (staged form dropped) too."""
     b = orc.rhs_xorshift(int(np.prod(dims)), 4)
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 30)
     out = {}
-    for stage in ("1", "0"):
-        monkeypatch.setenv("TW_STAGE_X", stage)
+    for stage in (True, False):
         for transport in ("loopback", "peer"):
-            G = P.EmulatedRankGroup(*dims, P_, 30, transport=transport)
-            assert all(A.x_staged == (stage == "1") for A in G.mats)
+            G = P.EmulatedRankGroup(*dims, P_, 30, transport=transport, x_staged=stage)
+            assert all(A.x_staged == stage for A in G.mats)
             G.set_rhs(b)
             G.iterate(11)
             G.iterate(19)
@@ -955,37 +978,38 @@ def test_x_staged_slabs_multi_rank(orc, dims, P_, monkeypatch):
             G.close()
             check_history(hs[0], want_h)
             assert np.all(rel_gap(out[stage, transport][1], want_x) <= 1e-10)
-    for stage in ("1", "0"):
+    for stage in (True, False):
         (h0, x0), (h1, x1) = out[stage, "loopback"], out[stage, "peer"]
         assert np.array_equal(h0, h1) and np.array_equal(x0, x1)
 
 
 @pytest.mark.parametrize("where", ["mono", "mono_graph", "loopback", "peer", "tasks",
                                    "tasks_graph", "persistent"])
-def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
+def test_x_update_in_k3_bit_identical(rt, orc, where):
     """From 4M rows per rank the x update (x += alpha p_old) runs in K3, which
     reads p_old anyway, instead of K2 (in the tasks variant: in the p-update
     tile kernels / dispatcher chunks instead of the x/r ones).  x feeds
     nothing inside the iteration and keeps its roundings, so histories and x
-    must be bit-identical to the K2 placement (TW_X_IN_K3 forces either at
-    solver creation), on every executor and both multi-rank transports."""
+    must be bit-identical to the K2 placement (CgOptions.x_update forces
+    either), on every executor and both multi-rank transports."""
     dims = (64, 40, 36)
     b = orc.rhs_xorshift(int(np.prod(dims)), 6)
     out = []
-    for xk3 in ("1", "0"):
-        monkeypatch.setenv("TW_X_IN_K3", xk3)
+    for xk3 in ("k3", "k2"):
         if where.startswith("mono"):
             A = P.gen_stencil_matrix(*dims, rt=rt)
-            res = P.cg_monolithic(rt, A, b, 35, P.CgOptions(use_graph=where == "mono_graph"))
+            res = P.cg_monolithic(rt, A, b, 35, P.CgOptions(use_graph=where == "mono_graph",
+                                                            x_update=xk3))
             out.append((res.residual_history, res.x))
         elif where.startswith("tasks") or where == "persistent":
             A = P.gen_stencil_matrix(*dims, rt=rt)
             opt = P.CgOptions(tiles=5, use_graph=where == "tasks_graph",
-                              persistent=where == "persistent")
+                              persistent=where == "persistent", x_update=xk3)
             res = P.cg_tasks(rt, A, b, 35, opt)
             out.append((res.residual_history, res.x))
         else:
-            G = P.EmulatedRankGroup(*dims, 3, 35, transport=where)
+            G = P.EmulatedRankGroup(*dims, 3, 35, transport=where,
+                                    options=P.CgOptions(iteration_marks=False, x_update=xk3))
             G.set_rhs(b)
             G.iterate(20)
             G.iterate(15)
@@ -997,27 +1021,3 @@ def test_x_update_in_k3_bit_identical(rt, orc, where, monkeypatch):
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
 
 
-@pytest.mark.parametrize("dims", [(64, 40, 36), (96, 48, 33)])
-@pytest.mark.parametrize("graph", [False, True])
-def test_fold_k2_into_k1(rt, orc, dims, graph, monkeypatch):
-    """Opt-in TW_FOLD_K2=1: K1 and K2 of the single-domain CG in one
-    cooperative launch (grid barrier on alpha, then r -= alpha Ap streamed
-    through the K1 warps' stages).  Two launches per iteration; its r.r tree
-    differs from the standalone K2's, so it is checked under the parity rule,
-    with the x update in the fold (TW_X_IN_K3=0) and in K3 (=1)."""
-    from paper_2602_21897_b200 import _native as N
-    b = orc.rhs_xorshift(int(np.prod(dims)), 8)
-    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, 40)
-    monkeypatch.setenv("TW_FOLD_K2", "1")
-    A = P.gen_stencil_matrix(*dims, rt=rt)
-    for xk3 in ("0", "1"):
-        monkeypatch.setenv("TW_X_IN_K3", xk3)
-        s = P.CgSolver(rt, A, 40, P.CgOptions(use_graph=graph, iteration_marks=False),
-                       variant=N.TW_CG_MONOLITHIC)
-        assert s.launches_per_iteration()[0] == 2
-        s.set_rhs(b)
-        s.iterate(13)
-        s.iterate(27)
-        check_history(s.history(40), want_h)
-        assert np.all(rel_gap(s.solution(), want_x) <= 1e-10)
-        s.close()

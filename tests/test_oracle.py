@@ -201,3 +201,56 @@ def test_reference_task_path_runs_on_threads(orc, ref):
     h, x, secs = ref.cg_tasks(M, b, 10, tiles=8, workers=4, real_threads=True)
     ho, xo, _ = orc.cg(orc.stencil(16, 16, 16), b, 10, tiles=8)
     assert np.array_equal(h, ho) and np.array_equal(x, xo) and secs > 0
+
+
+# ---- the headline size (256^3, BASELINE configs[2]) against the reference --
+
+def test_matrix_free_cg_threaded_bitwise(orc, golden):
+    """orc_cg_stencil_mt splits only row-independent work over threads: the
+    32^3 x 150 reference history and x to the bit for any thread / tile count."""
+    b = orc.rhs_xorshift(32 ** 3, 7)
+    for threads in (1, 3, 8):
+        h, x = orc.cg_stencil_mt(32, 32, 32, b, 150, threads=threads)
+        assert np.array_equal(h, golden["cg_32_xorshift7_history"])
+        assert np.array_equal(x, golden["cg_32_xorshift7_x"])
+    h4, x4 = orc.cg_stencil(32, 32, 32, b, 50, tiles=4)
+    h4t, x4t = orc.cg_stencil_mt(32, 32, 32, b, 50, tiles=4, threads=5)
+    assert np.array_equal(h4, h4t) and np.array_equal(x4, x4t)
+
+
+@pytest.mark.parametrize("dims,ranges", [((5, 4, 3), [(0, 60), (7, 33), (20, 20)]),
+                                         ((17, 9, 13), [(0, 153), (153, 1989), (1000, 1001)])])
+def test_stencil_rows_is_the_full_matrix_sliced(orc, dims, ranges):
+    m = orc.stencil(*dims)
+    for r0, r1 in ranges:
+        c = orc.stencil_rows(*dims, r0, r1)
+        k0, k1 = m.row_ptr[r0], m.row_ptr[r1]
+        assert np.array_equal(c.row_ptr, m.row_ptr[r0:r1 + 1] - k0)
+        assert np.array_equal(c.col_idx, m.col_idx[k0:k1])
+        assert np.array_equal(c.values, m.values[k0:k1])
+
+
+def test_oracle_256_structure_vs_reference_digests(orc, golden256):
+    """The oracle's gen_stencil_matrix restatement at 256^3 against the
+    reference's own matrix: per-plane SHA-256 of row_ptr / col_idx / values
+    for the boundary and a few interior planes (all 256 are compared with
+    the device matrix in tests/test_gpu_headline.py)."""
+    from conftest import csr_digests
+    D = 256
+    plane = D * D
+    assert orc.stencil_nnz(D, D, D) == int(golden256["csr_256_nnz"][0])
+    for z in (0, 1, 128, 254, 255):
+        c = orc.stencil_rows(D, D, D, z * plane, (z + 1) * plane)
+        assert np.array_equal(csr_digests(c.row_ptr, c.col_idx, c.values),
+                              golden256["csr_256_plane_digests"][z]), z
+
+
+def test_oracle_256_cg_vs_reference(orc, golden256):
+    """The threaded matrix-free oracle at the headline size reproduces the
+    reference's cg_reference (cg.cpp:372-395) history bit for bit (first 12
+    of the 60 committed iterations; the GPU test checks all 60)."""
+    D = 256
+    b = orc.rhs_xorshift(D ** 3, 7)
+    h, _ = orc.cg_stencil_mt(D, D, D, b, 12)
+    assert np.array_equal(h, golden256["cg_256_xorshift7_history"][:12])
+    assert h[0] == 9518.4498236045511  # SURVEY.md 8(c) probe value
