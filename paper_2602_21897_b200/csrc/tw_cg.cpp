@@ -803,7 +803,10 @@ int tw_cg_create(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* opt, int max
 }
 
 int tw_cg_destroy(tw_cg* cg) {
-    return guarded([&] { free_cg(cg); });
+    return guarded([&] {
+        free_cg(cg);
+        (void)cudaGetLastError(); // teardown is best effort: leave no stale error behind
+    });
 }
 
 int tw_cg_set_rhs(tw_cg* cg, const double* b, int b_is_device) {

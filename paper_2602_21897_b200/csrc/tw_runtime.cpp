@@ -725,6 +725,7 @@ int tw_ctx_destroy(tw_ctx* ctx) {
             cudaFree(kv.second.ticket);
         }
         delete ctx;
+        (void)cudaGetLastError();
     });
 }
 
@@ -979,6 +980,7 @@ int tw_ell_destroy(tw_ell* A) {
         if (!A) return;
         cudaSetDevice(A->ctx->device);
         free_ell(A);
+        (void)cudaGetLastError(); // teardown is best effort: leave no stale error behind
     });
 }
 
