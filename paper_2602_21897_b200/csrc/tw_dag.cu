@@ -123,8 +123,11 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
                         bulk_g2s(stage + P.val_bytes, P.A.cols16 + off, ents * 2u, bar, pol);
                     }
+                    int64_t starts[kStageRuns];
+                    run_starts(P.A, s, starts);
+#pragma unroll
                     for (int r = 0; r < kStageRuns; ++r) {
-                        const int64_t st = run_start(P.A, s, r);
+                        const int64_t st = starts[r];
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),

@@ -103,10 +103,23 @@ __host__ __device__ inline int64_t stage_run_start(int64_t s, int r, int64_t nx,
     return (in ? zz * ny + yy : z * ny + y) * nx + x0 - 2 - col_off;
 }
 
-// Start of staged run r of slice s, from the run table or the closed form.
-__host__ __device__ inline int64_t run_start(const EllView& A, int64_t s, int r) {
-    return A.sx_runs ? static_cast<int64_t>(A.sx_runs[s * kStageRuns + r])
-                     : stage_run_start(s, r, A.sx_nx, A.sx_ny, A.sx_nz, A.sx_row_off, A.sx_col_off);
+// Starts of the 9 staged runs of slice s, from the run table or the closed
+// form (its divisions done once per slice, not per run: lane 0 computes
+// them on K1's issue path, between one slice's copies and the next).
+__host__ __device__ inline void run_starts(const EllView& A, int64_t s, int64_t st[kStageRuns]) {
+    if (A.sx_runs) {
+        for (int r = 0; r < kStageRuns; ++r) st[r] = A.sx_runs[s * kStageRuns + r];
+        return;
+    }
+    const int64_t nx = A.sx_nx, ny = A.sx_ny, nz = A.sx_nz;
+    const int64_t row0 = s * 32 + A.sx_row_off, x0 = row0 % nx, t = row0 / nx, y = t % ny,
+                  z = t / ny;
+    const int64_t own = (z * ny + y) * nx + x0 - 2 - A.sx_col_off;
+    for (int r = 0; r < kStageRuns; ++r) {
+        const int64_t dz = r / 3 - 1, dy = r % 3 - 1;
+        const bool in = z + dz >= 0 && z + dz < nz && y + dy >= 0 && y + dy < ny;
+        st[r] = in ? own + (dz * ny + dy) * nx : own;
+    }
 }
 
 __host__ __device__ inline int64_t ell_val_pos(int k, int lane, int w) {

@@ -419,8 +419,11 @@ __device__ __forceinline__ void staged_spmv_body(
             thread_wait_flags(wait_flags, nwait, want);
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        int64_t starts[kStageRuns];
+        run_starts(A, s, starts);
+#pragma unroll
         for (int r = 0; r < kStageRuns; ++r) {
-            const int64_t st = run_start(A, s, r);
+            const int64_t st = starts[r];
             if (KEEP) // small x: keep its lines in L2 (evict_last) for the other runs
                 bulk_g2s(xs + r * kStageRunLen, x + st, kRunBytes, bar, xpol);
             else
@@ -498,13 +501,31 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
 constexpr int kPairsUnroll = TW_PAIRS_UNROLL;
 // Pair-vectorised loop over [i0, i1): pairs (2j, 2j+1) fully inside use
 // 128-bit accesses, the (at most two) ragged ends go scalar.
-template <typename F>
+// Sweep direction of the vector passes (L2 reuse across kernel boundaries,
+// 126 MB of L2 against 134 MB vectors at 256^3): K2 walks up and stores r
+// with the default L2 policy (TW_K2_KEEP_R), K3 walks DOWN (TW_K3_REV), so
+// it starts on the r lines K2 wrote last, still in L2, and ends on the low
+// p lines the next K1 reads first.  Measured at 256^3: K3 112.6 -> 108.3 us,
+// the iteration 865 -> 859.6 us; K2 walking down instead (reusing K1's Ap)
+// gave 862 (profiles/r02_ab_k2k3_sweep.md).  K3 has no reduction, so its
+// direction changes no bit; TW_K2_REV (a different fixed r.r tree) stays off.
+#ifndef TW_K2_REV
+#define TW_K2_REV 0
+#endif
+#ifndef TW_K2_KEEP_R
+#define TW_K2_KEEP_R 1
+#endif
+#ifndef TW_K3_REV
+#define TW_K3_REV 1
+#endif
+template <bool REV = false, typename F>
 __device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&& f) {
     const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
     const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
 #pragma unroll kPairsUnroll
-    for (int64_t j = j0 + static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x; j < j1;
-         j += stride) {
+    for (int64_t t = j0 + static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x; t < j1;
+         t += stride) {
+        const int64_t j = REV ? j0 + j1 - 1 - t : t;
         const int64_t e = 2 * j;
         f(e, e >= i0, e + 1 < i1);
     }
@@ -531,14 +552,15 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
     if (!WX && asrc.count > 0 && g.bid == 0 && threadIdx.x == 0) sc->alpha = alpha;
     double part = 0.0;
-    for_pairs(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
+    for_pairs<TW_K2_REV != 0>(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
         if (!WX) {
             if (lo && hi) {
                 double2 rv = __ldcs(reinterpret_cast<const double2*>(r + e));
                 const double2 av = __ldcs(reinterpret_cast<const double2*>(Ap + e));
                 rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
                 rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                __stcs(reinterpret_cast<double2*>(r + e), rv);
+                if (TW_K2_KEEP_R) *reinterpret_cast<double2*>(r + e) = rv;
+                else __stcs(reinterpret_cast<double2*>(r + e), rv);
                 part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
                 part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
             } else {
@@ -613,10 +635,12 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
         *reinterpret_cast<double2*>(p + e) = pv;
     };
+    const int64_t J0 = a >> 1, J1 = b >> 1;
 #pragma unroll U
-    for (int64_t j = (a >> 1) + tid; j < (b >> 1); j += 2 * stride) {
-        const int64_t e0 = 2 * j, e1 = 2 * (j + stride);
-        const bool two = e1 < b;
+    for (int64_t j = J0 + tid; j < J1; j += 2 * stride) {
+        const bool two = j + stride < J1;
+        const int64_t e0 = 2 * (TW_K3_REV ? J0 + J1 - 1 - j : j);
+        const int64_t e1 = 2 * (TW_K3_REV ? J0 + J1 - 1 - (j + stride) : j + stride);
         const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
         const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
         double2 r1 = make_double2(0.0, 0.0), p1 = r1, x0 = r1, x1 = r1;
