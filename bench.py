@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--cpu-sample-nz", type=int, default=0,
                     help="planes of the CPU sample (0 = the full per-GPU workload)")
     ap.add_argument("--cpu-sample-iters", type=int, default=40)
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extra single-GPU configurations (C2 128^3 monolithic vs "
+                         "block-task DAG, the C5 granularity share, C4 512^3, the CSR drop-in)")
     return ap.parse_args()
 
 
@@ -248,29 +251,55 @@ def load_traffic(kernel: str = "k1"):
 
 # ------------------------------------------------------------ CPU baseline
 
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(nx, ny, nz_sample, iters, threads):
-    """The reference's own task-based CPU path (oracle/_ref: cg_tasks on the
-    threaded substrate with real_seconds_per_unit = 0, tiles = 8 x threads)
-    on a bounded z-slab sample of the workload.  Returns GFLOP/s etc."""
+    """The reference's own CPU paths (oracle/_ref, compiled from its sources)
+    on a bounded z-slab sample of the workload, BASELINE.md section 4:
+      (i)   cg_reference (cg.cpp:372-395) on 1 core;
+      (ii)  cg_tasks on the threaded substrate, real_seconds_per_unit = 0,
+            tiles = nproc;
+      (iii) the same with tiles = 8 x nproc (the headline CPU figure).
+    The cg_tasks legs are timed by the reference's own cg_iter marks after
+    one warm-up iteration (scenario.cpp:116-124); cg_reference by the wall
+    clock around the call (its setup_state included)."""
     from oracle import Oracle, Reference
     R = Reference()
     o = Oracle()
     M = R.stencil(nx, ny, nz_sample)
     b = o.rhs_xorshift(M.n, 7)
-    tiles = min(8 * threads, M.n)
-    # one run of 1 + iters iterations; the timed span is the reference's own
-    # cg_iter marks after the warm-up iteration (scenario.cpp:116-124), so
-    # runtime start-up and the first touch of the solver state are excluded
-    _, _, _, marks = R.cg_tasks_marks(M, b, 1 + iters, tiles=tiles, workers=threads,
-                                      real_threads=True)
-    secs = float(marks[iters] - marks[0])
-    flops = (2 * M.nnz + 10 * M.n) * iters
-    return {"value": flops / secs / 1e9, "unit": "GFLOP/s", "cores": threads,
-            "kind": "reference", "iters_per_s": iters / secs,
-            "sample": f"reference cg_tasks (oracle/_ref, real threads, tiles={tiles}) on a "
-                      f"{nx}x{ny}x{nz_sample} grid (the per-GPU workload when nz matches), "
-                      f"{iters} CG iterations after 1 warm-up, "
-                      f"{secs:.2f} s wall"}
+    flops_it = 2 * M.nnz + 10 * M.n
+    legs = []
+    k_ref = max(2, iters // 8)
+    t0 = time.perf_counter()
+    R.cg_reference(M, b, k_ref)
+    secs = time.perf_counter() - t0
+    legs.append({"leg": "cg_reference, 1 core", "cores": 1, "tiles": 1, "iterations": k_ref,
+                 "value": flops_it * k_ref / secs / 1e9, "iters_per_s": k_ref / secs,
+                 "secs": secs})
+    for tiles in (min(threads, M.n), min(8 * threads, M.n)):
+        _, _, _, marks = R.cg_tasks_marks(M, b, 1 + iters, tiles=tiles, workers=threads,
+                                          real_threads=True)
+        secs = float(marks[iters] - marks[0])
+        legs.append({"leg": f"cg_tasks real threads, tiles={tiles}", "cores": threads,
+                     "tiles": tiles, "iterations": iters, "value": flops_it * iters / secs / 1e9,
+                     "iters_per_s": iters / secs, "secs": secs})
+    head = legs[-1]
+    return {"value": head["value"], "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+            "iters_per_s": head["iters_per_s"], "cpu_model": cpu_model(),
+            "sample": f"reference cg_tasks (oracle/_ref, real threads, tiles={head['tiles']}) on "
+                      f"a {nx}x{ny}x{nz_sample} grid (the per-GPU workload when nz matches), "
+                      f"{iters} CG iterations after 1 warm-up, {head['secs']:.2f} s wall",
+            "legs": legs}
 
 
 def run_reference_arm(args, dist, rank, world):
@@ -312,6 +341,128 @@ def run_reference_arm(args, dist, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+
+def time_iterations(torch, S, b, K, W, stream):
+    """W untimed iterations from x0 = 0, then K timed by CUDA events on the
+    solver's launch stream; returns (ms per iteration, history)."""
+    S.set_rhs(b)
+    if W:
+        S.iterate(W)
+    S.wait()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    S.iterate(K)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / K, S.history(W + K)
+
+
+def extra_configs(torch, P, N, rt, A, b, stream, peak):
+    """Single-GPU figures of BASELINE configs beside the headline (rank 0,
+    N = 1): the reference-API drop-in at the headline size, C2 (128^3
+    monolithic vs block-task DAG), C5's per-GPU share (256^3, 1-64 tiles per
+    GPU = 8-512 blocks over 8 GPUs) and C4's 1-GPU point (512^3)."""
+    out = {}
+    W = 5
+
+    def opts(**kw):
+        return P.CgOptions(iteration_marks=False, **kw)
+
+    def solve_rate(Am, bm, K, variant, opt):
+        S = P.CgSolver(rt, Am, W + K, opt, variant=variant)
+        ms, hist = time_iterations(torch, S, bm, K, W, stream)
+        m = S.mode()
+        S.close()
+        assert np.all(np.isfinite(hist)) and hist[-1] < hist[0]
+        return ms, m, hist
+
+    def gflops(Am, ms):
+        return (2 * Am.nnz() + 10 * Am.n) / (ms / 1e3) / 1e9
+
+    # ---- the reference-API drop-in: a host CsrMatrix (here the device
+    # matrix's own export, i.e. gen_stencil_matrix's CSR) -> tw_ell_from_csr
+    # (validated, uploaded, converted; x-staged through the run table) ->
+    # tw_cg_solve with host b in and host history + x out, every call
+    rp, ci, va = A.to_csr()
+    t0 = time.perf_counter()
+    Ac = P.ell_from_csr(rp, ci, va, rt=rt)
+    rt.synchronize()
+    setup_s = time.perf_counter() - t0
+    del rp, ci, va
+    bh = np.empty(A.n)
+    import ctypes
+    N.check(N.load().tw_memcpy(rt.h, bh.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(b.ptr),
+                               8 * A.n, None))
+    rt.synchronize()
+    K = 100
+    xh = np.empty(A.n)
+    best, res = float("inf"), None
+    for _ in range(3):
+        t0 = time.perf_counter()
+        res = P.cg_solve(rt, Ac, bh, K, opts(tiles=1), N.TW_CG_MONOLITHIC, x_out=xh)
+        best = min(best, time.perf_counter() - t0)
+    ref = P.cg_solve(rt, A, bh, K, opts(tiles=1), N.TW_CG_MONOLITHIC)
+    Sc = P.CgSolver(rt, Ac, 1, opts(tiles=1), variant=N.TW_CG_MONOLITHIC)
+    mc = Sc.mode()
+    Sc.close()
+    flops = (2 * A.nnz() + 10 * A.n) * K
+    out["e2e_csr_drop_in"] = {
+        "value": flops / best / 1e9, "unit": "GFLOP/s", "iterations_per_call": K,
+        "h2d_bytes_per_step": 8 * A.n / K, "d2h_bytes_per_step": (8 * A.n + 8 * K) / K,
+        "setup_s": setup_s, "k1": mc["k1_kernel"],
+        "bit_identical_to_device_generated": bool(
+            np.array_equal(res.residual_history, ref.residual_history)
+            and np.array_equal(res.x, ref.x)),
+        "api": "tw_ell_from_csr(host CsrMatrix arrays) once (setup_s: validation, upload, "
+               "sliced ELL + run table), then per call tw_cg_solve(host b) -> host history + x"}
+    del Ac
+
+    # ---- C2: 128^3 on one GPU, monolithic vs the block-task DAG
+    A2 = P.gen_stencil_matrix(128, 128, 128, rt=rt)
+    b2 = P.rhs_xorshift(rt, A2.n, 7)
+    K2 = 800
+    rows = {}
+    mono = None
+    for name, variant, opt in (
+            ("mono_graph", N.TW_CG_MONOLITHIC, opts(tiles=1, use_graph=True)),
+            ("mono_streams", N.TW_CG_MONOLITHIC, opts(tiles=1)),
+            ("tasks_T4_graph", N.TW_CG_TASKS, opts(tiles=4, use_graph=True)),
+            ("tasks_T4_auto", N.TW_CG_TASKS, opts(tiles=4, auto_dispatch=True)),
+            ("tasks_T16_auto", N.TW_CG_TASKS, opts(tiles=16, auto_dispatch=True)),
+            ("tasks_T64_persistent", N.TW_CG_TASKS, opts(tiles=64, persistent=True))):
+        ms, m, _ = solve_rate(A2, b2, K2, variant, opt)
+        mono = ms if mono is None else mono
+        rows[name] = {"ms_per_iter": ms, "gflops": gflops(A2, ms), "vs_mono_graph": ms / mono,
+                      "dispatch": "persistent" if m["dispatch"] == N.TW_DISPATCH_PERSISTENT
+                      else ("graph" if m["use_graph"] else "streams")}
+    out["c2_128_mono_vs_tasks"] = rows
+    del A2, b2
+
+    # ---- C5's per-GPU share: 256^3 per GPU, 8-512 blocks over 8 GPUs =
+    # 1-64 tiles per GPU (the library's automatic dispatch choice)
+    rows = {}
+    for T in (1, 2, 4, 8, 16, 32, 64):
+        variant = N.TW_CG_MONOLITHIC if T == 1 else N.TW_CG_TASKS
+        ms, m, _ = solve_rate(A, b, 100, variant,
+                              opts(tiles=T, use_graph=T == 1, auto_dispatch=T > 1))
+        rows[f"T{T}"] = {"blocks_over_8_gpus": 8 * T, "ms_per_iter": ms, "gflops": gflops(A, ms),
+                         "dispatch": "persistent" if m["dispatch"] == N.TW_DISPATCH_PERSISTENT
+                         else ("graph" if m["use_graph"] else "streams")}
+    out["c5_256_per_gpu_share"] = rows
+
+    # ---- C4's 1-GPU point: 512^3 (43 GB of sliced ELL), the headline path
+    A4 = P.gen_stencil_matrix(512, 512, 512, rt=rt)
+    b4 = P.rhs_xorshift(rt, A4.n, 7)
+    ms, m, _ = solve_rate(A4, b4, 20, N.TW_CG_MONOLITHIC, opts(tiles=1, use_graph=True))
+    by = 12 * A4.nnz() + 88 * A4.n
+    out["c4_512_1gpu"] = {"ms_per_iter": ms, "gflops": gflops(A4, ms),
+                          "iters_per_s": 1e3 / ms, "roofline_frac": by / (ms / 1e3) / 1e9 / peak,
+                          "k1": m["k1_kernel"]}
+    del A4, b4
+    return out
+
 
 def run_ours(args, dist, rank, world, local):
     import torch
@@ -461,8 +612,11 @@ def run_ours(args, dist, rank, world, local):
 
     ms, clocks, hist = timed_run()
     bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    rejected = []
     if set(clocks["reasons"]) & bad:
-        ms, clocks, hist = timed_run()  # rejected: re-measure once
+        # rejected (throttled): kept in the line, and re-measured once
+        rejected.append({"ms_per_step": ms / K, "clocks": clocks})
+        ms, clocks, hist = timed_run()
     # the kernel-timing pass: KR iterations with K1 / K2 / K3 events recorded
     # around every kernel on its launch stream (roofline.achieved)
     kt_pass_ms, kt = None, None
@@ -574,6 +728,10 @@ def run_ours(args, dist, rank, world, local):
            "iters_per_s": K / e2e_t,
            "api": "CgSolver.set_rhs(host b) + iterate(K) + history + solution (C ABI tw_cg_*)"}
 
+    extras = None
+    if rank == 0 and world == 1 and not args.no_extras and not args.strong:
+        extras = extra_configs(torch, P, N, rt, A, b, stream, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -602,6 +760,10 @@ def run_ours(args, dist, rank, world, local):
             "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,
             "residual_last": float(hist[-1]),
         }
+        if rejected:
+            line["rejected_runs"] = rejected
+        if extras:
+            line["configs_single_gpu"] = extras
         print(json.dumps(line), flush=True)
     # release the solver, the matrix and the NCCL communicator while the
     # process group is still up (not in interpreter-exit destructors)

@@ -6,16 +6,19 @@ is the Python face that mirrors the reference's operator API
 (``hpccg.py``).  There is no CPU fallback.
 """
 from . import _native
-from .hpccg import (CgBackend, CgOptions, CgResult, CgSolver, ConfigError, ContractViolation, Event,
-                    CudaError, EllMatrix, EmulatedRankGroup, NcclError, Runtime, Tile, cg_monolithic, cg_tasks,
-                    default_runtime, dot_range, dump_csr, halo_exchange, update_p, update_xr_rr, load_csr, parse_csr, ell_from_csr, gen_stencil_matrix,
-                    make_tile_plan, rhs_splitmix, rhs_xorshift, slab_partition, slab_plan, spmv_dot,
-                    spmv_range, task_dag_edges, waxpby_range)
+from .hpccg import (CgBackend, CgOptions, CgResult, CgSolver, ConfigError, ContractViolation,
+                    CudaError, EllMatrix, EmulatedRankGroup, Event, NcclError, Runtime, Tile,
+                    cg_monolithic, cg_solve, cg_tasks, default_runtime, dot_range, dump_csr,
+                    ell_from_csr, gen_stencil_matrix, halo_exchange, load_csr, make_tile_plan,
+                    parse_csr, rhs_splitmix, rhs_xorshift, slab_partition, slab_plan, spmv_dot,
+                    spmv_range, task_dag_edges, update_p, update_xr_rr, waxpby_range)
 
 __all__ = [
-    "CgBackend", "CgOptions", "CgResult", "CgSolver", "ConfigError", "ContractViolation", "Event",
-    "CudaError", "EllMatrix", "EmulatedRankGroup", "NcclError", "Runtime", "Tile", "cg_monolithic", "cg_tasks",
-    "default_runtime", "dot_range", "dump_csr", "halo_exchange", "update_p", "update_xr_rr", "load_csr", "parse_csr", "ell_from_csr", "gen_stencil_matrix", "make_tile_plan",
-    "rhs_splitmix", "rhs_xorshift", "slab_partition", "slab_plan", "spmv_dot", "spmv_range", "task_dag_edges", "waxpby_range",
+    "CgBackend", "CgOptions", "CgResult", "CgSolver", "ConfigError", "ContractViolation",
+    "CudaError", "EllMatrix", "EmulatedRankGroup", "Event", "NcclError", "Runtime", "Tile",
+    "cg_monolithic", "cg_solve", "cg_tasks", "default_runtime", "dot_range", "dump_csr",
+    "ell_from_csr", "gen_stencil_matrix", "halo_exchange", "load_csr", "make_tile_plan",
+    "parse_csr", "rhs_splitmix", "rhs_xorshift", "slab_partition", "slab_plan", "spmv_dot",
+    "spmv_range", "task_dag_edges", "update_p", "update_xr_rr", "waxpby_range",
     "_native",
 ]

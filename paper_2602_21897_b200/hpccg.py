@@ -786,6 +786,24 @@ def _solve(rt: Runtime, A: EllMatrix, b, iterations: int, opt: CgOptions | None,
     return CgResult(hist, x, iterations, conv, marks)
 
 
+def cg_solve(rt: Runtime, A: EllMatrix, b: np.ndarray, iterations: int,
+             opt: CgOptions | None = None, variant: int = N.TW_CG_MONOLITHIC,
+             x_out: np.ndarray | None = None) -> CgResult:
+    """One solve through the single C-ABI entry a reference binding calls
+    (tw_cg_solve): host b in, host history and x out."""
+    opt = opt or CgOptions(iteration_marks=False)
+    bh = np.ascontiguousarray(b, np.float64)
+    if bh.shape != (A.n,):
+        raise ContractViolation("rhs length differs from the matrix rows")
+    hist = np.empty(max(iterations, 1), np.float64)
+    x = x_out if x_out is not None else np.empty(A.n, np.float64)
+    conv = C.c_int(0)
+    o = opt.to_c(variant)
+    N.check(_lib().tw_cg_solve(rt.h, A.h, bh.ctypes.data_as(C.c_void_p), iterations, C.byref(o),
+                               hist.ctypes.data_as(N.dp), x.ctypes.data_as(N.dp), C.byref(conv)))
+    return CgResult(hist[:iterations], x, iterations, bool(conv.value))
+
+
 def cg_monolithic(rt: Runtime, A: EllMatrix, b, iterations: int,
                   opt: CgOptions | None = None) -> CgResult:
     """cg_monolithic (cg.cpp:397-436): one stream, tiles forced to 1."""

@@ -3,6 +3,9 @@
 // tests/test_binding_cpu.py compiles it against the reference's own headers
 // (/root/reference/proj/include) and links it against libtw_hpccg.so with
 // --no-undefined, so every ABI call below resolves.  Not part of the product.
+#include <cstdint>
+#include <cstring>
+#include <map>
 #include <vector>
 
 #include "taskweave/cg.hpp"
@@ -23,14 +26,88 @@ struct TwCtx { // one device context per process (Runtime + sim::Device replacem
     }
 };
 
+// Device matrices cached across calls: the first cg_cuda on a CsrMatrix
+// uploads and converts it (tw_ell_from_csr: validation as csr.cpp:13-27, 16 B
+// per nonzero over the host link, sliced ELL + x-staged run table); later
+// calls on the same matrix reuse it, so a solve costs b in and history + x
+// out only.  Key: the object's address, its arrays' addresses and sizes and
+// a sampled fingerprint of the arrays; a caller that rewrites a matrix in
+// place calls cg_cuda_forget(A) first.
+struct EllCache {
+    struct Entry {
+        const std::int64_t* rp;
+        const std::int64_t* ci;
+        const double* va;
+        std::int64_t n, nnz;
+        std::uint64_t fp;
+        tw_ell* ell;
+    };
+    std::map<const CsrMatrix*, Entry> m;
+    std::uint64_t hits = 0;
+    ~EllCache() {
+        for (auto& kv : m) tw_ell_destroy(kv.second.ell);
+    }
+    static std::uint64_t fingerprint(const CsrMatrix& A) {
+        std::uint64_t h = 1469598103934665603ull;
+        auto mix = [&h](std::uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+        const std::size_t nnz = A.col_idx.size();
+        for (std::size_t k = 0; k < 4096 && nnz; ++k) {
+            const std::size_t i = k * nnz / 4096;
+            std::uint64_t v;
+            std::memcpy(&v, &A.values[i], 8);
+            mix(static_cast<std::uint64_t>(A.col_idx[i]));
+            mix(v);
+        }
+        for (std::size_t k = 0; k < 4096 && A.n; ++k)
+            mix(static_cast<std::uint64_t>(A.row_ptr[k * static_cast<std::size_t>(A.n) / 4096]));
+        return h;
+    }
+    tw_ell* get(tw_ctx* ctx, const CsrMatrix& A) {
+        const std::uint64_t fp = fingerprint(A);
+        auto it = m.find(&A);
+        if (it != m.end()) {
+            const Entry& e = it->second;
+            if (e.rp == A.row_ptr.data() && e.ci == A.col_idx.data() && e.va == A.values.data() &&
+                e.n == A.n && e.nnz == static_cast<std::int64_t>(A.col_idx.size()) && e.fp == fp) {
+                ++hits;
+                return e.ell;
+            }
+            tw_ell_destroy(e.ell);
+            m.erase(it);
+        }
+        tw_ell* ell = nullptr;
+        TwCtx::check(tw_ell_from_csr(ctx, A.n, A.row_ptr.data(), A.col_idx.data(),
+                                     A.values.data(), &ell));
+        m[&A] = Entry{A.row_ptr.data(), A.col_idx.data(), A.values.data(), A.n,
+                      static_cast<std::int64_t>(A.col_idx.size()), fp, ell};
+        return ell;
+    }
+    void forget(const CsrMatrix& A) {
+        auto it = m.find(&A);
+        if (it == m.end()) return;
+        tw_ell_destroy(it->second.ell);
+        m.erase(it);
+    }
+};
+
+TwCtx& context(unsigned pool) {
+    static TwCtx ctx(pool);
+    return ctx;
+}
+EllCache& cache() {
+    static EllCache c;
+    return c;
+}
+
 } // namespace
+
+void cg_cuda_forget(const CsrMatrix& A) { cache().forget(A); }
+std::uint64_t cg_cuda_cache_hits() { return cache().hits; }
 
 CgResult cg_cuda(const CsrMatrix& A, const std::vector<double>& b, int iterations,
                  const CgOptions& opt, int variant) {
-    static TwCtx ctx(opt.stream_pool_capacity);
-    tw_ell* ell = nullptr; // CsrMatrix -> device sliced ELL (validated like csr.cpp:13-27)
-    TwCtx::check(tw_ell_from_csr(ctx.h, A.n, A.row_ptr.data(), A.col_idx.data(),
-                                 A.values.data(), &ell));
+    TwCtx& ctx = context(opt.stream_pool_capacity);
+    tw_ell* ell = cache().get(ctx.h, A); // CsrMatrix -> device sliced ELL, once per matrix
     tw_cg_options o;
     tw_cg_options_default(&o);
     o.variant = variant; // TW_CG_MONOLITHIC | TW_CG_TASKS
@@ -42,10 +119,8 @@ CgResult cg_cuda(const CsrMatrix& A, const std::vector<double>& b, int iteration
     res.residual_history.resize(static_cast<size_t>(iterations));
     res.x.resize(static_cast<size_t>(A.n));
     int conv = 0;
-    const int rc = tw_cg_solve(ctx.h, ell, b.data(), iterations, &o, res.residual_history.data(),
-                               res.x.data(), &conv);
-    tw_ell_destroy(ell);
-    TwCtx::check(rc);
+    TwCtx::check(tw_cg_solve(ctx.h, ell, b.data(), iterations, &o, res.residual_history.data(),
+                             res.x.data(), &conv));
     res.iterations = iterations;
     res.converged = conv != 0;
     return res;

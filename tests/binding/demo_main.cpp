@@ -15,6 +15,8 @@
 namespace tw::bench {
 CgResult cg_cuda(const CsrMatrix& A, const std::vector<double>& b, int iterations,
                  const CgOptions& opt, int variant);
+void cg_cuda_forget(const CsrMatrix& A);
+std::uint64_t cg_cuda_cache_hits();
 }
 
 int main() {
@@ -56,8 +58,26 @@ int main() {
                 break;
             }
     }
+    // the device matrix was built once: the tasks solve reused it
+    if (cg_cuda_cache_hits() != 1) {
+        std::printf("ELL cache: %llu hits, want 1\n", (unsigned long long)cg_cuda_cache_hits());
+        ++bad;
+    }
+    // a matrix changed in place is re-uploaded once forgotten
+    CsrMatrix B = gen_stencil_matrix(8, 8, 8);
+    std::vector<double> bb(static_cast<size_t>(B.n), 1.0);
+    CgOptions o1;
+    o1.tiles = 1;
+    const CgResult r1 = cg_cuda(B, bb, 5, o1, TW_CG_MONOLITHIC);
+    for (auto& v : B.values) v *= 2.0;
+    cg_cuda_forget(B);
+    const CgResult r2 = cg_cuda(B, bb, 5, o1, TW_CG_MONOLITHIC);
+    if (!(std::fabs(2.0 * r2.x[0] - r1.x[0]) <= 1e-12 * std::fabs(r1.x[0]))) { // 2A: x halves
+        std::printf("a forgotten matrix was not re-uploaded\n");
+        ++bad;
+    }
     if (bad) return 1;
     std::printf("binding ok: the reference's CsrMatrix through tw_cg_solve matches cg_reference "
-                "(32^3, 150 iterations, monolithic and 8-tile tasks)\n");
+                "(32^3, 150 iterations, monolithic and 8-tile tasks; device matrix cached)\n");
     return 0;
 }
