@@ -344,7 +344,14 @@ def run_reference_arm(args, dist, rank, world):
 
 def time_iterations(torch, S, b, K, W, stream):
     """W untimed iterations from x0 = 0, then K timed by CUDA events on the
-    solver's launch stream; returns (ms per iteration, history)."""
+    solver's launch stream; returns (ms per iteration, history).  One
+    untimed pass of the same shape first, so the graphs / dispatcher tables
+    of these call lengths are built (and cached) outside the timed region."""
+    S.set_rhs(b)
+    if W:
+        S.iterate(W)
+    S.iterate(K)
+    S.wait()
     S.set_rhs(b)
     if W:
         S.iterate(W)

@@ -181,13 +181,16 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
     case PK_HALO:
         halo_exchange(cg, st);
         break;
-    case PK_SPMV: // the x-staged K1 when the matrix has it (single domain)
+    case PK_SPMV: { // the x-staged K1 when the matrix has it
+        const Fin f = cg->tile_fin(cg->pa, t, FIN_ALPHA, cg->tile_tickets);
         if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]},
-                                cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, st))
+                                cg->slot(t), f, st))
             launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0},
-                        true, cg->slot(t), Fin{FIN_STORE, cg->pa + t, nullptr, nullptr}, bs, st);
+                        true, cg->slot(t), f, bs, st);
         break;
-    case PK_ALPHA:
+    }
+    case PK_ALPHA: // folded into the last SpMV tile (an empty join node) on one rank
+        if (cg->fold_scalars()) break;
         if (!cg->dist) {
             launch_combine(cg->pa, cg->T, Fin{FIN_ALPHA, nullptr, cg->sc, nullptr}, st);
         } else {
@@ -200,9 +203,10 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
         launch_update_xr(cg->t_r0[t], cg->t_r1[t], x_in_k3(cg) ? nullptr : cg->x, cg->p_owned,
                          cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, cg->slot(t),
-                         Fin{FIN_STORE, cg->rrp + t, nullptr, nullptr}, bv, st);
+                         cg->tile_fin(cg->rrp, t, FIN_BETA, cg->tile_tickets + 1), bv, st);
         break;
-    case PK_BETA:
+    case PK_BETA: // folded into the last x/r-update tile on one rank
+        if (cg->fold_scalars()) break;
         if (!cg->dist) {
             launch_combine(cg->rrp, cg->T, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
         } else {
@@ -285,6 +289,31 @@ void build_graph(tw_cg* cg) {
     TW_CUDA(e);
 }
 
+cudaGraphExec_t build_chunk_graph(tw_cg* cg, int c) {
+    cudaStream_t s = cg->ctx->compute;
+    cudaGraph_t g = nullptr;
+    TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+        if (cg->opt.variant == TW_CG_TASKS) {
+            fork_streams(cg);
+            for (int i = 0; i < c; ++i) enqueue_tasks(cg, i & 1, i == 0);
+            join_streams(cg);
+        } else {
+            for (int i = 0; i < c; ++i) enqueue_mono(cg);
+        }
+    } catch (...) {
+        cudaStreamEndCapture(s, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    TW_CUDA(cudaStreamEndCapture(s, &g));
+    cudaGraphExec_t ge = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    TW_CUDA(e);
+    return ge;
+}
+
 void free_cg(tw_cg* cg) {
     if (!cg) return;
     cudaSetDevice(cg->ctx->device);
@@ -292,6 +321,7 @@ void free_cg(tw_cg* cg) {
     cg->ta.reset();
     if (cg->graph) cudaGraphExecDestroy(cg->graph);
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : cg->chunk_graphs) cudaGraphExecDestroy(kv.second);
     for (auto& v : cg->ev)
         for (auto e : v) cudaEventDestroy(e);
     for (auto e : cg->tail_ev) cudaEventDestroy(e);
@@ -311,6 +341,7 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->parts);
     cudaFree(cg->block_parts);
     cudaFree(cg->tickets);
+    cudaFree(cg->tile_tickets);
     for (void* m : cg->ipc_mapped) cudaIpcCloseMemHandle(m);
     cudaFree(cg->win);
     cudaFree(cg->d_links);
@@ -442,6 +473,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaMalloc(&cg->block_parts, sizeof(double) * static_cast<size_t>(cg->maxg) * T));
         TW_CUDA(cudaMalloc(&cg->tickets, sizeof(unsigned) * 4 * T));
         TW_CUDA(cudaMemset(cg->tickets, 0, sizeof(unsigned) * 4 * T));
+        TW_CUDA(cudaMalloc(&cg->tile_tickets, sizeof(unsigned) * 2));
+        TW_CUDA(cudaMemset(cg->tile_tickets, 0, sizeof(unsigned) * 2));
         TW_CUDA(cudaEventCreateWithFlags(&cg->fork_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->halo_ev, cudaEventDisableTiming));
         TW_CUDA(cudaEventCreateWithFlags(&cg->pready_ev, cudaEventDisableTiming));
@@ -733,8 +766,23 @@ void iterate(tw_cg* cg, int k) {
         cg->enqueued += k;
         return;
     }
-    if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     const bool tasks = cg->opt.variant == TW_CG_TASKS;
+    if (cg->opt.use_graph && !cg->opt.iteration_marks) {
+        // no per-iteration host marks: chunks of up to kGraphChunk iterations
+        // per graph launch, so consecutive iterations overlap where the DAG
+        // allows (tasks) and no graph boundary sits between two iterations
+        // of a chunk; one graph per chunk length, cached
+        for (int left = k; left > 0;) {
+            const int c = std::min(left, kGraphChunk);
+            auto it = cg->chunk_graphs.find(c);
+            if (it == cg->chunk_graphs.end()) it = cg->chunk_graphs.emplace(c, build_chunk_graph(cg, c)).first;
+            TW_CUDA(cudaGraphLaunch(it->second, s));
+            left -= c;
+        }
+        cg->enqueued += k;
+        return;
+    }
+    if (cg->opt.use_graph && !cg->graph) build_graph(cg);
     if (!cg->opt.use_graph && tasks) fork_streams(cg);
     if (cg->opt.iteration_marks && cg->enqueued == 0) TW_CUDA(cudaEventRecord(iter_event(cg, 0), s));
     for (int i = 0; i < k; ++i) {
@@ -971,7 +1019,7 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;
         } else {
-            k = 3 * cg->T + (cg->dist ? 4 : 2);
+            k = 3 * cg->T + (cg->dist ? 4 : 0); // one rank: alpha / beta_res fold into the tiles
             c = cg->dist ? 3 : 0;
         }
         if (kernels) *kernels = k;

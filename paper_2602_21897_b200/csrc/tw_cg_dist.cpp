@@ -166,6 +166,8 @@ void finish_links(tw_cg* cg) {
     }
     for (auto& kv : cg->timed_graphs) cudaGraphExecDestroy(kv.second);
     cg->timed_graphs.clear();
+    for (auto& kv : cg->chunk_graphs) cudaGraphExecDestroy(kv.second);
+    cg->chunk_graphs.clear();
 }
 
 // ------------------------------------------------ emulated rank group

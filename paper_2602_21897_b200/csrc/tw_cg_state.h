@@ -46,6 +46,7 @@ struct tw_cg {
     double* parts = nullptr;
     double* block_parts = nullptr;
     unsigned* tickets = nullptr;
+    unsigned* tile_tickets = nullptr; // [2]: the folded alpha / beta_res (FIN_TILES)
     int maxg = 0;
 
     // partial slots (offsets into parts)
@@ -63,6 +64,7 @@ struct tw_cg {
 
     cudaGraphExec_t graph = nullptr;
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
+    std::map<int, cudaGraphExec_t> chunk_graphs; // up to kGraphChunk iterations, untimed
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
@@ -95,6 +97,22 @@ struct tw_cg {
         return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
     }
     // K1's view of A; l2_keep overrides the x-run L2 policy of the staged K1
+    // tasks variant, one rank: alpha / beta_res folded into the last tile
+    // kernel of their phase (no combine launch between the phases)
+    bool fold_scalars() const { return opt.variant == TW_CG_TASKS && !dist; }
+    Fin tile_fin(double* parts, int t, int then, unsigned* ticket) const {
+        Fin f{FIN_STORE, parts + t, nullptr, nullptr};
+        if (fold_scalars()) {
+            f.mode = FIN_TILES;
+            f.sc = sc;
+            f.history = history;
+            f.tparts = parts;
+            f.ntiles = T;
+            f.then = then;
+            f.tticket = ticket;
+        }
+        return f;
+    }
     EllView view() const {
         EllView v = A->view();
         if (v.cols16 && opt.l2_keep == TW_L2KEEP_ON) v.sx_keep = 1;
@@ -126,6 +144,8 @@ void join_streams(tw_cg* cg);
 void enqueue_tasks(tw_cg* cg, int parity, bool first);
 void enqueue_iteration_body(tw_cg* cg, int parity, bool first);
 void build_graph(tw_cg* cg);
+constexpr int kGraphChunk = 16;
+cudaGraphExec_t build_chunk_graph(tw_cg* cg, int c);
 void free_cg(tw_cg* cg);
 tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_iters);
 void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s);

@@ -172,6 +172,27 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         fin.sc->rtrans = total;
         fin.sc->iter = 0;
         break;
+    case FIN_TILES: {
+        *fin.out = total;
+        __threadfence(); // the partial before the ticket
+        const unsigned t = atomicInc(fin.tticket, static_cast<unsigned>(fin.ntiles - 1));
+        if (t != static_cast<unsigned>(fin.ntiles - 1)) break; // wraps to 0: reset for the next use
+        __threadfence();
+        double s = 0.0;
+        for (int i = 0; i < fin.ntiles; ++i) s = __dadd_rn(s, __ldcg(fin.tparts + i));
+        CgScalars* sc = fin.sc;
+        if (fin.then == FIN_ALPHA) {
+            sc->pAp = s;
+            sc->alpha = __ddiv_rn(sc->rtrans, s);
+        } else {
+            sc->rr = s;
+            sc->beta = __ddiv_rn(s, sc->rtrans);
+            sc->rtrans = s;
+            if (sc->iter < sc->history_cap) fin.history[sc->iter] = __dsqrt_rn(s);
+            sc->iter = sc->iter + 1;
+        }
+        break;
+    }
     case FIN_PUBLISH_A:
     case FIN_PUBLISH_B: {
         if (fin.out) *fin.out = total;

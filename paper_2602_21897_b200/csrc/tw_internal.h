@@ -193,7 +193,13 @@ enum FinMode : int {
     // total; v -> recv_a / recv_b [rank] of every rank's window over NVLink,
     // then the matching flags get this iteration's stamp (release, .sys)
     FIN_PUBLISH_A = 5,
-    FIN_PUBLISH_B = 6
+    FIN_PUBLISH_B = 6,
+    // tasks variant, one rank: the alpha / beta_res reduction tasks
+    // (cg.cpp:209-225, 290-311) folded into the tile kernels: *out = this
+    // tile's partial, then a ticket over the `ntiles` tile kernels; the last
+    // to finish sums tparts[0..ntiles) in tile order and finalizes with
+    // `then` (FIN_ALPHA / FIN_BETA) -- the sum combine_kernel would form
+    FIN_TILES = 7
 };
 
 struct PeerLinks;
@@ -205,6 +211,12 @@ struct Fin {
     double* history;
     const PeerLinks* links = nullptr; // FIN_PUBLISH_*: device copy of the links
     const double* pre = nullptr;      // FIN_PUBLISH_A: the interior rows' partial
+    // FIN_TILES: tile partials, their count, the cross-kernel ticket, the
+    // finalize of the last tile
+    const double* tparts = nullptr;
+    int ntiles = 0;
+    int then = FIN_NONE;
+    unsigned* tticket = nullptr;
 };
 
 // Where an update kernel takes its scalar from: sc->alpha / sc->beta when
