@@ -189,8 +189,10 @@ void group_check(tw_cg** g, int P) {
             contract_error("rank group entry " + std::to_string(r) +
                            " is not emulated rank r of P (tw_ctx_init_emulated_rank)");
         if (c->device != g[0]->ctx->device) contract_error("emulated ranks share one device");
-        if (g[r]->opt.variant != TW_CG_MONOLITHIC)
-            config_error("the emulated rank group runs the monolithic variant");
+        if (g[r]->opt.variant != g[0]->opt.variant || g[r]->T != g[0]->T)
+            config_error("the ranks of a group run the same variant and tile count");
+        if (g[r]->opt.variant == TW_CG_TASKS && g[r]->opt.dispatch == TW_DISPATCH_PERSISTENT)
+            config_error("the emulated rank group runs the tasks variant on streams");
     }
 }
 
@@ -225,6 +227,8 @@ void group_join(tw_cg** g, int P, cudaStream_t s) {
 // other ranks' buffers on the same device.
 void group_enable_peer(tw_cg** g, int P) {
     group_check(g, P);
+    if (g[0]->opt.variant != TW_CG_MONOLITHIC)
+        config_error("the peer transport runs the monolithic variant");
     for (int r = 0; r < P; ++r)
         if (g[r]->peer) contract_error("the peer transport is already connected");
     TW_CUDA(cudaSetDevice(g[0]->ctx->device));
@@ -262,6 +266,34 @@ void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
     for (int r = 0; r < P; ++r) reset_solve_state(g[r]);
 }
 
+// One block-task iteration of every rank (cg_tasks' DAG with the halo task,
+// spawn_iteration, cg.cpp:166-334): the ranks' physical nodes phase by phase
+// -- halo (loopback), the SpMV tiles, alpha (tile-order combine, the
+// allgather, the rank-order combine), the x/r tiles, beta_res likewise, the
+// p tiles -- with the very kernels and partial orders of the NCCL tasks path
+// (launch_node), so its numbers are the multi-GPU executor's.
+static void group_tasks_iteration(tw_cg** g, int P, cudaStream_t s) {
+    auto nodes_of = [&](int kind) {
+        for (int r = 0; r < P; ++r)
+            for (const PNode& nd : g[r]->nodes)
+                if (nd.kind == kind) launch_node(g[r], nd, s);
+    };
+    auto reduce = [&](double* tw_cg::*tile_parts, double* tw_cg::*send, double* tw_cg::*recv,
+                      int fin_mode) {
+        for (int r = 0; r < P; ++r)
+            launch_combine(g[r]->*tile_parts, g[r]->T, Fin{FIN_STORE, g[r]->*send, nullptr, nullptr}, s);
+        loopback_allgather(g, P, send, recv, s);
+        for (int r = 0; r < P; ++r)
+            launch_combine(g[r]->*recv, P, Fin{fin_mode, nullptr, g[r]->sc, g[r]->history}, s);
+    };
+    loopback_halo(g, P, s);
+    nodes_of(PK_SPMV);
+    reduce(&tw_cg::pa, &tw_cg::send_a, &tw_cg::recv_a, FIN_ALPHA);
+    nodes_of(PK_UPD);
+    reduce(&tw_cg::rrp, &tw_cg::send_b, &tw_cg::recv_b, FIN_BETA);
+    nodes_of(PK_UPDP);
+}
+
 void group_iterate(tw_cg** g, int P, int k) {
     group_check(g, P);
     if (k < 0) config_error("negative iteration count");
@@ -273,12 +305,15 @@ void group_iterate(tw_cg** g, int P, int k) {
         TW_CUDA(cudaEventRecord(g[r]->fork_ev, g[r]->ctx->compute));
         TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
     }
-    for (int it = 0; it < k && g[0]->peer; ++it) { // peer transport: stores + flags
+    const bool tasks = g[0]->opt.variant == TW_CG_TASKS;
+    if (tasks && g[0]->peer) contract_error("the peer transport runs the monolithic variant");
+    for (int it = 0; it < k && tasks; ++it) group_tasks_iteration(g, P, s);
+    for (int it = 0; it < k && !tasks && g[0]->peer; ++it) { // peer transport: stores + flags
         for (int r = 0; r < P; ++r) peer_spmv(g[r], s);
         for (int r = 0; r < P; ++r) peer_update_xr(g[r], s);
         for (int r = 0; r < P; ++r) peer_update_p(g[r], s);
     }
-    for (int it = 0; it < k && !g[0]->peer; ++it) {
+    for (int it = 0; it < k && !tasks && !g[0]->peer; ++it) {
         loopback_halo(g, P, s);
         for (int r = 0; r < P; ++r) {
             dist_spmv_interior(g[r], s);

@@ -119,10 +119,14 @@ struct tw_cg {
         if (v.cols16 && opt.l2_keep == TW_L2KEEP_OFF) v.sx_keep = 0;
         return v;
     }
+    // Across ranks every node that calls NCCL (the halo; alpha / beta_res:
+    // combine, allgather, combine) runs on the comm stream, so one rank's
+    // collectives are issued in program order on one stream -- the order
+    // every rank shares (halo(i) < alpha(i) < beta_res(i) < halo(i+1)).
     cudaStream_t node_stream(const PNode& nd) const {
         if (nd.kind == PK_HALO) return ctx->comm;
         const unsigned C = ctx->pool.capacity();
-        if (nd.kind == PK_ALPHA || nd.kind == PK_BETA) return ctx->pool.stream(0);
+        if (nd.kind == PK_ALPHA || nd.kind == PK_BETA) return dist ? ctx->comm : ctx->pool.stream(0);
         return ctx->pool.stream(static_cast<int>(static_cast<unsigned>(nd.tile) % C));
     }
 };

@@ -704,12 +704,15 @@ class CgSolver:
 
 class EmulatedRankGroup:
     """P z-slab ranks on ONE device, driven together (tw_cg_group_*): the
-    multi-GPU algorithm with loopback copies in place of the NCCL transport.
-    Test infrastructure for the multi-rank path on a single B200."""
+    multi-GPU algorithm with loopback copies in place of the NCCL transport,
+    for the monolithic variant (also over the peer transport) and the
+    block-task DAG (variant TW_CG_TASKS, options.tiles tiles per rank, the
+    halo task and rank-ordered alpha / beta_res).  Test infrastructure for
+    the multi-rank path on a single B200."""
 
     def __init__(self, nx: int, ny: int, nz: int, nranks: int, max_iterations: int,
                  device: int = 0, transport: str = "loopback", x_staged: bool = True,
-                 options: CgOptions | None = None):
+                 options: CgOptions | None = None, variant: int = N.TW_CG_MONOLITHIC):
         if transport not in ("loopback", "peer"):
             raise ValueError(f"unknown transport {transport!r}")
         self.P = nranks
@@ -725,8 +728,7 @@ class EmulatedRankGroup:
                 A.set_x_staged(False)
             self.rts.append(rt)
             self.mats.append(A)
-            self.solvers.append(CgSolver(rt, A, max_iterations, opt,
-                                         variant=N.TW_CG_MONOLITHIC))
+            self.solvers.append(CgSolver(rt, A, max_iterations, opt, variant=variant))
         self._arr = (C.c_void_p * nranks)(*[s.h.value for s in self.solvers])
         if transport == "peer":
             N.check(_lib().tw_cg_group_enable_peer(self._arr, nranks))

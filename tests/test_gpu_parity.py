@@ -1022,3 +1022,37 @@ def test_x_update_in_k3_bit_identical(rt, orc, where):
     assert np.all(rel_gap(out[0][1], want_x) <= 1e-10)
 
 
+
+
+@pytest.mark.parametrize("P_", [2, 3, 4, 8])
+@pytest.mark.parametrize("T", [1, 4, 16])
+def test_multi_rank_block_task_dag(orc, P_, T):
+    """The block-task DAG across z-slab ranks (cg_tasks with the halo task,
+    cg.cpp:166-334): every rank's tile kernels, the loopback halo, tile-order
+    then rank-order alpha / beta_res -- the kernels and partial orders of the
+    NCCL tasks executor -- against the oracle under the SURVEY 8(c) rule;
+    every rank holds the same history, and a re-solve repeats it bit for
+    bit.  x-staged slabs (nx % 32 == 0) and run-table slabs (nx = 30)."""
+    for dims in ((32, 16, 24), (30, 12, 16)):
+        m = orc.stencil(*dims)
+        b = orc.rhs_xorshift(m.n, 5)
+        want_h, want_x, _ = orc.cg(m, b, 40)
+        G = P.EmulatedRankGroup(*dims, P_, 40, variant=N_TASKS,
+                                options=P.CgOptions(tiles=T, iteration_marks=False))
+        assert all(s.mode()["variant"] == N_TASKS and s.mode()["tiles"] == T for s in G.solvers)
+        runs = []
+        for _ in range(2):
+            G.set_rhs(b)
+            G.iterate(17)
+            G.iterate(23)
+            hs = G.history(40)
+            for h in hs:
+                assert np.array_equal(h, hs[0])
+            runs.append((hs[0], G.solution()))
+        G.close()
+        assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+        check_history(runs[0][0], want_h)
+        assert np.all(rel_gap(runs[0][1], want_x) <= 1e-10)
+
+
+N_TASKS = 1  # TW_CG_TASKS
