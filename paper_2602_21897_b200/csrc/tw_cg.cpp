@@ -8,11 +8,12 @@
 //   K1 spmv_pAp   Ap = A p, p.Ap            (spmv:i:t + dot_pAp:i:t)
 //   K2 update_xr  x += a p, r -= a Ap, r.r  (x_up:i:t + r_up:i:t + dot_rr:i:t)
 //   K3 update_p   p = r + b p               (p_up:i:t)
-// with alpha:i / beta_res:i folded into the last block of K1 / K2 (one tile,
-// one rank) or run as one-warp combine kernels over the tile / rank partials.
+// with alpha:i / beta_res:i folded into the last block of K1 / K2 (one tile),
+// into the last tile kernel of the phase (tiles, one rank), or run as one-warp
+// combine kernels over the tile / rank partials (across ranks).
 //
-// The tasks variant keeps the reference's data-flow semantics: a region
-// ledger infers the per-iteration logical DAG from the same byte-interval
+// The tasks variant keeps the reference's data-flow semantics: the depsys
+// dependency rule infers the per-iteration logical DAG from the same byte-interval
 // accesses spawn_iteration declares (cg.cpp:173-333); fused physical nodes
 // inherit the union of their members' edges and become cudaStreamWaitEvent
 // edges between pooled streams (or edges of a captured CUDA graph).

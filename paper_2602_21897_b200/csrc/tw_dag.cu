@@ -481,7 +481,24 @@ __global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(DagPar
         if (c < 0) break;
         if (!slots[b].ready) { // wait for the task's predecessors (compute warps only)
             if (tid == 0) {
-                while (ld_acquire(P.remaining + slots[b].task) > 0) __nanosleep(32);
+                // bounded like every device wait of the library: a broken
+                // task table (a counter that never reaches zero) reports and
+                // traps instead of hanging the GPU
+                unsigned spins = 0;
+                unsigned long long t0 = 0;
+                while (ld_acquire(P.remaining + slots[b].task) > 0) {
+                    __nanosleep(32);
+                    if ((++spins & 4095u) == 0) {
+                        const unsigned long long t = global_ns();
+                        if (!t0) {
+                            t0 = t;
+                        } else if (t - t0 > TW_PEER_TIMEOUT_NS) {
+                            printf("tw_hpccg: dispatcher task %d still has %d predecessors\n",
+                                   slots[b].task, ld_acquire(P.remaining + slots[b].task));
+                            __trap();
+                        }
+                    }
+                }
                 __threadfence();
             }
             bar_sync(5, kComputeWarps * 32);

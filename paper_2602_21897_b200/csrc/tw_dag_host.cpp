@@ -11,7 +11,7 @@ namespace tw {
 
 namespace {
 
-// Synthetic byte addresses for the ledger: one 2^40-byte window per array,
+// Synthetic byte addresses for the dependency rule: one 2^40-byte window per array,
 // element i of array k at (k << 40) + 8 i.  Only overlap matters for edges.
 enum Arr : uint64_t { A_X = 1, A_R, A_P, A_AP, A_PA, A_RR, A_RTRANS, A_ALPHA, A_BETA };
 Acc reg(Arr a, int64_t i0, int64_t i1, int mode) {
@@ -97,11 +97,11 @@ void build_logical(const DagSpec& d, int iter, std::vector<LTask>& out,
                             off_updp + t});
 }
 
-// Runs the ledger over `iters` iterations; returns logical edges (global
+// Runs the dependency rule over `iters` iterations; returns logical edges (global
 // task ids = iter * tasks_per_iter + k) and, optionally, the label list.
 void logical_edges(const DagSpec& d, int iters, std::vector<std::pair<int, int>>& edges,
                    std::vector<std::string>* labels, std::vector<int>* phys_of) {
-    Ledger led;
+    AccessLog log;
     std::vector<LTask> it_tasks;
     int base = 0;
     for (int it = 0; it < iters; ++it) {
@@ -109,12 +109,12 @@ void logical_edges(const DagSpec& d, int iters, std::vector<std::pair<int, int>>
         for (size_t k = 0; k < it_tasks.size(); ++k) {
             const int id = base + static_cast<int>(k);
             std::vector<int> pr;
-            for (const Acc& a : it_tasks[k].acc) led.conflicts(a, pr);
+            for (const Acc& a : it_tasks[k].acc) log.depends(a, pr);
             std::sort(pr.begin(), pr.end());
             pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
             for (int p : pr)
                 if (p != id) edges.emplace_back(p, id);
-            for (const Acc& a : it_tasks[k].acc) led.record(a, id);
+            for (const Acc& a : it_tasks[k].acc) log.add(a, id);
             if (labels) labels->push_back(it_tasks[k].label);
             if (phys_of) phys_of->push_back(it_tasks[k].phys);
         }

@@ -1,6 +1,6 @@
 // Host-side inference of the cg_tasks block-task DAG: the reference's
 // spawn_iteration tasks and access regions (cg.cpp:166-334) and the
-// RAW/WAR/WAW rules of its depsys (region_ledger.cpp, dep_system.cpp:22-65),
+// RAW/WAR/WAW rule of its depsys (dep_system.cpp:22-65),
 // plus the fused physical nodes the CUDA executors launch.  No device code.
 #pragma once
 
@@ -13,11 +13,17 @@
 
 namespace tw {
 
-// --------------------------------------------------------------- ledger
+// ------------------------------------------------------ dependency rule
 //
-// Byte-interval dependency inference with the reference's rules
-// (region_ledger.hpp:11-27): a read conflicts with the last writer; a write
-// or readwrite conflicts with the last writer and every reader since.
+// The depsys semantics the reference's tests pin (region_ledger.hpp:11-27,
+// dep_system.cpp:22-65), stated per byte: a read depends on the byte's last
+// writer; a write or readwrite depends on the last writer and on every read
+// since that write.  AccessLog applies the rule directly: it keeps the
+// accesses in issue order and, for a new one, walks them newest first while
+// some of its bytes still lack their last writer.  A write found there is
+// the last writer of the bytes it covers (they close); a read found there
+// happened after those bytes' last write, so a new write depends on it
+// (the bytes stay open).  Empty intervals take no part.
 
 enum AccMode { ACC_R = 0, ACC_W = 1, ACC_RW = 2 };
 struct Acc {
@@ -25,61 +31,43 @@ struct Acc {
     int mode;
 };
 
-class Ledger {
+class AccessLog {
 public:
-    void conflicts(const Acc& a, std::vector<int>& out) const {
-        auto it = seg_.upper_bound(a.lo);
-        if (it != seg_.begin()) --it;
-        for (; it != seg_.end() && it->first < a.hi; ++it) {
-            const Seg& s = it->second;
-            if (s.hi <= a.lo) continue;
-            if (s.writer >= 0) out.push_back(s.writer);
-            if (a.mode != ACC_R) out.insert(out.end(), s.readers.begin(), s.readers.end());
+    // Tasks the access `a` depends on (appended to out, unsorted).
+    void depends(const Acc& a, std::vector<int>& out) const {
+        if (a.hi <= a.lo) return;
+        std::vector<std::pair<uint64_t, uint64_t>> open{{a.lo, a.hi}}, next;
+        for (auto it = log_.rbegin(); it != log_.rend() && !open.empty(); ++it) {
+            const Acc& e = it->a;
+            const bool writes = e.mode != ACC_R;
+            if (!writes && a.mode == ACC_R) continue; // read after read
+            bool hit = false;
+            next.clear();
+            for (const auto& [lo, hi] : open) {
+                const uint64_t l = std::max(lo, e.lo), h = std::min(hi, e.hi);
+                if (l >= h || !writes) {
+                    hit = hit || l < h;
+                    next.emplace_back(lo, hi);
+                    continue;
+                }
+                hit = true;
+                if (lo < l) next.emplace_back(lo, l);
+                if (h < hi) next.emplace_back(h, hi);
+            }
+            if (hit) out.push_back(it->task);
+            open.swap(next);
         }
     }
-    void record(const Acc& a, int task) {
-        split(a.lo);
-        split(a.hi);
-        if (a.mode != ACC_R) {
-            seg_.erase(seg_.lower_bound(a.lo), seg_.lower_bound(a.hi));
-            seg_[a.lo] = Seg{a.hi, task, {}};
-            return;
-        }
-        uint64_t pos = a.lo;
-        auto it = seg_.lower_bound(a.lo);
-        while (pos < a.hi) {
-            if (it == seg_.end() || it->first >= a.hi) {
-                seg_[pos] = Seg{a.hi, -1, {task}};
-                break;
-            }
-            if (it->first > pos) {
-                seg_[pos] = Seg{it->first, -1, {task}};
-                pos = it->first;
-                continue;
-            }
-            auto& rd = it->second.readers;
-            if (std::find(rd.begin(), rd.end(), task) == rd.end()) rd.push_back(task);
-            pos = it->second.hi;
-            ++it;
-        }
+    void add(const Acc& a, int task) {
+        if (a.hi > a.lo) log_.push_back(Rec{a, task});
     }
 
 private:
-    struct Seg {
-        uint64_t hi;
-        int writer;
-        std::vector<int> readers;
+    struct Rec {
+        Acc a;
+        int task;
     };
-    void split(uint64_t x) {
-        auto it = seg_.upper_bound(x);
-        if (it == seg_.begin()) return;
-        --it;
-        if (it->first == x || it->second.hi <= x) return;
-        Seg right = it->second;
-        it->second.hi = x;
-        seg_[x] = std::move(right);
-    }
-    std::map<uint64_t, Seg> seg_;
+    std::vector<Rec> log_;
 };
 
 enum PhysKind { PK_HALO, PK_SPMV, PK_ALPHA, PK_UPD, PK_BETA, PK_UPDP };
@@ -113,7 +101,7 @@ struct PNode {
 // physical nodes of one iteration).
 void build_logical(const DagSpec& d, int iter, std::vector<LTask>& out,
                    std::vector<PNode>* nodes);
-// Ledger over `iters` iterations: logical edges (ids = iter * tasks_per_iter
+// The dependency rule over `iters` iterations: logical edges (ids = iter * tasks_per_iter
 // + k), optional labels and physical node of every logical task.
 void logical_edges(const DagSpec& d, int iters, std::vector<std::pair<int, int>>& edges,
                    std::vector<std::string>* labels, std::vector<int>* phys_of);
