@@ -155,3 +155,152 @@ def test_partition_covers_grid():
         P.slab_partition(3, 0, 4)
     with pytest.raises(P.ContractViolation):
         P.slab_plan(4, 4, 4, 3, 3)
+
+
+def _rank_tasks_main(rank, world, port, dims, T, iters, seed, out_dir):
+    """cg_tasks across ranks on the host: this rank's logical block-task DAG
+    as the product infers it (tw_task_dag_edges, halo task included) run in
+    a RANDOM topological order (seeded per rank); the collective tasks --
+    halo:i, alpha:i, beta_res:i -- therefore run in whatever order the edges
+    force, so the ranks only agree on them (and do not deadlock) if the edges
+    order them.  Arithmetic: the oracle's, tile order then rank order."""
+    import random
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21897_b200 as P
+    from oracle import Csr, Oracle
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    nx, ny, nz = dims
+    o = Oracle()
+    zb, ze = P.slab_partition(nz, rank, world)
+    sp = P.slab_plan(nx, ny, nz, zb, ze)
+    m = o.stencil(nx, ny, nz)
+    r0, r1 = sp.row_offset, sp.row_offset + sp.n_rows
+    loc = Csr(sp.n_rows, m.row_ptr[r0:r1 + 1] - m.row_ptr[r0],
+              m.col_idx[m.row_ptr[r0]:m.row_ptr[r1]] - sp.col_offset,
+              m.values[m.row_ptr[r0]:m.row_ptr[r1]])
+    n, ds, pl = sp.n_rows, sp.diag_shift, sp.plane
+    tr0, tr1, tlo, thi = o.tile_plan(loc, T)
+    tiles = [P.Tile(int(a), int(b), int(c), int(d)) for a, b, c, d in zip(tr0, tr1, tlo, thi)]
+    edges = P.task_dag_edges(n, tiles, iters, diag_shift=ds, plane=pl,
+                             ghost_lo=bool(sp.ghost_lo), ghost_hi=bool(sp.ghost_hi))
+    fams = (["halo"] if (sp.ghost_lo or sp.ghost_hi) else []) + \
+        ["spmv", "dot_pAp", "alpha", "x_up", "r_up", "dot_rr", "beta_res", "p_up"]
+    tasks = [f"{f}:{i}:{t}" for i in range(iters) for f in fams
+             for t in (range(T) if f not in ("halo", "alpha", "beta_res") else [0])]
+    preds = {k: set() for k in tasks}
+    succ = {k: [] for k in tasks}
+    for a, b in edges:
+        preds[b].add(a)
+        succ[a].append(b)
+    rng = random.Random(seed * 101 + rank)
+    ready = [k for k in tasks if not preds[k]]
+    order = []
+    while ready:
+        k = ready.pop(rng.randrange(len(ready)))
+        order.append(k)
+        for s in succ[k]:
+            preds[s].discard(k)
+            if not preds[s]:
+                ready.append(s)
+    assert len(order) == len(tasks)
+
+    def allgather_sum(v):
+        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(parts, torch.tensor([v], dtype=torch.float64))
+        s = 0.0
+        for q in parts:
+            s += float(q.item())
+        return s
+
+    b_all = o.rhs_xorshift(nx * ny * nz, 7)
+    b = b_all[r0:r1].copy()
+    p = np.zeros(sp.x_len)
+    p[ds:ds + n] = b
+    r, x, Ap = b.copy(), np.zeros(n), np.zeros(n)
+    pa, rrp = np.zeros(T), np.zeros(T)
+    st = {"rtrans": allgather_sum(o.dot(r, r)), "alpha": 0.0, "beta": 0.0}
+    hist = [0.0] * iters
+    colls = []
+    for k in order:
+        f, i, t = k.split(":")
+        i, t = int(i), int(t)
+        a0, a1 = int(tr0[t]), int(tr1[t])
+        po = p[ds:ds + n]
+        if f == "halo":
+            colls.append(k)
+            reqs = []
+            if sp.ghost_lo:
+                reqs.append(dist.irecv(torch.from_numpy(p[sp.recv_lo:sp.recv_lo + pl]), src=rank - 1))
+                reqs.append(dist.isend(torch.from_numpy(p[sp.send_lo:sp.send_lo + pl].copy()),
+                                       dst=rank - 1))
+            if sp.ghost_hi:
+                reqs.append(dist.irecv(torch.from_numpy(p[sp.recv_hi:sp.recv_hi + pl]), src=rank + 1))
+                reqs.append(dist.isend(torch.from_numpy(p[sp.send_hi:sp.send_hi + pl].copy()),
+                                       dst=rank + 1))
+            for q in reqs:
+                q.wait()
+        elif f == "spmv":
+            o.spmv(loc, p, a0, a1, y=Ap)
+        elif f == "dot_pAp":
+            pa[t] = o.dot(po, Ap, a0, a1)
+        elif f == "alpha":
+            colls.append(k)
+            s = 0.0
+            for v in pa:  # tile order (cg.cpp:218-221), then rank order
+                s += v
+            st["alpha"] = st["rtrans"] / allgather_sum(s)
+        elif f == "x_up":
+            o.waxpby(1.0, x, st["alpha"], po, x, a0, a1)
+        elif f == "r_up":
+            o.waxpby(1.0, r, -st["alpha"], Ap, r, a0, a1)
+        elif f == "dot_rr":
+            rrp[t] = o.dot(r, r, a0, a1)
+        elif f == "beta_res":
+            colls.append(k)
+            s = 0.0
+            for v in rrp:
+                s += v
+            rr = allgather_sum(s)
+            st["beta"] = rr / st["rtrans"]
+            st["rtrans"] = rr
+            hist[i] = np.sqrt(rr)
+        elif f == "p_up":
+            p[ds + a0:ds + a1] = o.waxpby(1.0, r, st["beta"], po, None, a0, a1)[a0:a1]
+    np.save(os.path.join(out_dir, f"x{rank}.npy"), x)
+    np.save(os.path.join(out_dir, f"h{rank}.npy"), np.array(hist))
+    with open(os.path.join(out_dir, f"c{rank}.txt"), "w") as fh:
+        fh.write("\n".join(colls))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,T", [(2, (8, 6, 10), 3), (3, (6, 5, 12), 2), (2, (5, 4, 6), 1)])
+def test_tasks_dag_across_ranks_random_order(tmp_path, orc, world, dims, T):
+    """The multi-rank block-task DAG's edges are complete and order every
+    rank's collectives identically: two random topological orders per rank
+    give the same history and x bit for bit, within the rule of the
+    single-rank reference."""
+    iters = 12
+    outs = []
+    for seed in (1, 2):
+        d = tmp_path / f"s{seed}"
+        d.mkdir()
+        mp.spawn(_rank_tasks_main, args=(world, _free_port(), dims, T, iters, seed, str(d)),
+                 nprocs=world, join=True)
+        hs = [np.load(d / f"h{r}.npy") for r in range(world)]
+        for h in hs:
+            assert np.array_equal(h, hs[0])
+        colls = [(d / f"c{r}.txt").read_text() for r in range(world)]
+        assert all(c.replace("halo", "") == colls[0].replace("halo", "") for c in colls)
+        outs.append((hs[0], np.concatenate([np.load(d / f"x{r}.npy") for r in range(world)])))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    m = orc.stencil(*dims)
+    want_h, want_x, _ = orc.cg(m, orc.rhs_xorshift(m.n, 7), iters)
+    check_history(outs[0][0], want_h)
+    assert np.all(rel_gap(outs[0][1], want_x) <= 1e-10)
