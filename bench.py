@@ -426,6 +426,15 @@ def extra_configs(torch, P, N, rt, A, b, stream, peak):
                "sliced ELL + run table), then per call tw_cg_solve(host b) -> host history + x"}
     del Ac
 
+    # ---- K0: gen_stencil_matrix on the device at the headline size (one-time
+    # setup: widths, slice-offset scan, the 128-bit fill of values, int32 and
+    # x-staged columns), host wall clock around the whole call
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    Ak = P.gen_stencil_matrix(A.info.nx, A.info.ny, A.info.nz, rt=rt)
+    out["k0_gen_stencil_ms"] = (time.perf_counter() - t0) * 1e3
+    del Ak
+
     # ---- C2: 128^3 on one GPU, monolithic vs the block-task DAG
     A2 = P.gen_stencil_matrix(128, 128, 128, rt=rt)
     b2 = P.rhs_xorshift(rt, A2.n, 7)

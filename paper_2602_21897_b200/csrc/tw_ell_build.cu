@@ -47,12 +47,18 @@ __global__ void stencil_widths_kernel(int64_t nx, int64_t ny, int64_t nz, int64_
 }
 
 // One warp per slice, lane = row: walk the row's neighbours in the
-// reference's (dz, dy, dx) order (csr.cpp:46-54) and drop them into the
-// chunked slice layout; pad to the slice width with col = -1.
-__global__ void stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
-                                    int64_t col_offset, int64_t n_rows, int64_t n_slices,
-                                    const int64_t* __restrict__ slice_off, double* vals,
-                                    int32_t* cols) {
+// reference's (dz, dy, dx) order (csr.cpp:46-54) into registers, then write
+// the slice block in its chunked layout with 128-bit stores -- 2 values, 4
+// int32 columns or 8 x-staged 16-bit columns per lane and store, a warp
+// writing 512 contiguous bytes -- padding to the slice width (value 0,
+// column -1, staged 0xFFFF).  With c16 (nx % 32 == 0: each slice is one
+// x-line segment starting at x0) the staged index of neighbour (dz, dy, cx)
+// is run (dz + 1) * 3 + (dy + 1), offset cx - x0 + 2 (stage_run_start).
+constexpr int kMaxStencilWidth = 27;
+__global__ void __launch_bounds__(kThreads)
+stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset, int64_t col_offset,
+                    int64_t n_rows, int64_t n_slices, const int64_t* __restrict__ slice_off,
+                    double* vals, int32_t* cols, uint16_t* c16) {
     const int lane = threadIdx.x & 31;
     const int64_t warp_g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -60,32 +66,91 @@ __global__ void stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t 
     for (int64_t s = warp_g; s < n_slices; s += nwarps) {
         const int64_t off = slice_off[s];
         const int w = static_cast<int>((slice_off[s + 1] - off) >> 5);
-        double* vb = vals + off;
-        int32_t* cb = cols + off;
         const int64_t row = s * 32 + lane;
-        int k = 0;
+        const int64_t x0 = (s * 32 + row_offset) % nx;
+        // entry k of the row is neighbour (iz, iy, ix) of its per-axis spans,
+        // (dz, dy, dx) lexicographic = ascending column (csr.cpp:46-53)
+        int len = 0, sx = 0, sxy = 0;
+        int64_t x = 0, y = 0, z = 0, xlo = 0, ylo = 0, zlo = 0;
         if (row < n_rows) {
             const int64_t g = row + row_offset;
-            const int64_t z = g / plane, rem = g - z * plane, y = rem / nx, x = rem - y * nx;
-            for (int64_t cz = z - 1; cz <= z + 1; ++cz) {
-                if (cz < 0 || cz >= nz) continue;
-                for (int64_t cy = y - 1; cy <= y + 1; ++cy) {
-                    if (cy < 0 || cy >= ny) continue;
-                    const int64_t line = (cz * ny + cy) * nx;
-                    for (int64_t cx = x - 1; cx <= x + 1; ++cx) {
-                        if (cx < 0 || cx >= nx) continue;
-                        const bool diag = cx == x && cy == y && cz == z;
-                        vb[ell_val_pos(k, lane, w)] = diag ? 27.0 : -1.0;
-                        cb[ell_col_pos(k, lane, w)] = static_cast<int32_t>(line + cx - col_offset);
-                        ++k;
-                    }
-                }
-            }
+            z = g / plane;
+            const int64_t rem = g - z * plane;
+            y = rem / nx;
+            x = rem - y * nx;
+            xlo = x > 0 ? x - 1 : x;
+            ylo = y > 0 ? y - 1 : y;
+            zlo = z > 0 ? z - 1 : z;
+            sx = static_cast<int>(axis_span(x, nx));
+            sxy = sx * static_cast<int>(axis_span(y, ny));
+            len = sxy * static_cast<int>(axis_span(z, nz));
         }
-        for (; k < w; ++k) {
-            vb[ell_val_pos(k, lane, w)] = 0.0;
-            cb[ell_col_pos(k, lane, w)] = -1;
+        auto nb = [&](int k, int64_t& cx, int64_t& cy, int64_t& cz) {
+            const int iz = k / sxy, t = k - iz * sxy, iy = t / sx;
+            cz = zlo + iz;
+            cy = ylo + iy;
+            cx = xlo + (t - iy * sx);
+        };
+        auto val = [&](int k) {
+            if (k >= len) return 0.0;
+            int64_t cx, cy, cz;
+            nb(k, cx, cy, cz);
+            return cx == x && cy == y && cz == z ? 27.0 : -1.0;
+        };
+        auto cl = [&](int k) {
+            if (k >= len) return -1;
+            int64_t cx, cy, cz;
+            nb(k, cx, cy, cz);
+            return static_cast<int32_t>((cz * ny + cy) * nx + cx - col_offset);
+        };
+        auto s16 = [&](int k) {
+            if (k >= len) return uint32_t(kStagePad);
+            int64_t cx, cy, cz;
+            nb(k, cx, cy, cz);
+            return static_cast<uint32_t>(((cz - z + 1) * 3 + (cy - y + 1)) * kStageRunLen +
+                                         (cx - x0 + 2));
+        };
+        double* vb = vals + off;
+        int32_t* cb = cols + off;
+        // values: pairs [k/2][l][2] (one double2 per lane), odd tail [w-1][l]
+#pragma unroll
+        for (int j = 0; j < kMaxStencilWidth / 2; ++j)
+            if (2 * j + 1 < w)
+                __stcs(reinterpret_cast<double2*>(vb + 64 * j) + lane,
+                       make_double2(val(2 * j), val(2 * j + 1)));
+        if (w & 1) vb[32 * (w - 1) + lane] = val(w - 1);
+        // int32 columns: quads [k/4][l][4], then a pair, then a single
+        const int f4 = w & ~3;
+#pragma unroll
+        for (int q = 0; q < kMaxStencilWidth / 4; ++q)
+            if (4 * q < f4)
+                __stcs(reinterpret_cast<int4*>(cb + 128 * q) + lane,
+                       make_int4(cl(4 * q), cl(4 * q + 1), cl(4 * q + 2), cl(4 * q + 3)));
+        if (w - f4 >= 2)
+            reinterpret_cast<int2*>(cb + 32 * f4)[lane] = make_int2(cl(f4), cl(f4 + 1));
+        if ((w - f4) & 1) cb[32 * (w - 1) + lane] = cl(w - 1);
+        if (!c16) continue;
+        // staged columns: [k/8][l][8] (one uint4 per lane), then 4, 2, 1
+        uint16_t* hb = c16 + off;
+        const int f8 = w & ~7;
+        auto pk = [&](int k) { return s16(k) | (s16(k + 1) << 16); };
+#pragma unroll
+        for (int q = 0; q < kMaxStencilWidth / 8; ++q)
+            if (8 * q < f8)
+                __stcs(reinterpret_cast<uint4*>(hb + 256 * q) + lane,
+                       make_uint4(pk(8 * q), pk(8 * q + 2), pk(8 * q + 4), pk(8 * q + 6)));
+        int base = f8, rem = w - f8;
+        if (rem >= 4) {
+            reinterpret_cast<uint2*>(hb + 32 * base)[lane] = make_uint2(pk(base), pk(base + 2));
+            base += 4;
+            rem -= 4;
         }
+        if (rem >= 2) {
+            reinterpret_cast<uint32_t*>(hb + 32 * base)[lane] = pk(base);
+            base += 2;
+            rem -= 2;
+        }
+        if (rem) hb[32 * base + lane] = static_cast<uint16_t>(s16(base));
     }
 }
 
@@ -389,10 +454,10 @@ void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offse
 
 void launch_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
                          int64_t col_offset, int64_t n_rows, int64_t n_slices,
-                         const int64_t* slice_off, double* vals, int32_t* cols, int blocks,
-                         cudaStream_t s) {
+                         const int64_t* slice_off, double* vals, int32_t* cols, uint16_t* c16,
+                         int blocks, cudaStream_t s) {
     stencil_fill_kernel<<<clamp_blocks(n_slices * 32, blocks), kThreads, 0, s>>>(
-        nx, ny, nz, row_offset, col_offset, n_rows, n_slices, slice_off, vals, cols);
+        nx, ny, nz, row_offset, col_offset, n_rows, n_slices, slice_off, vals, cols, c16);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -351,8 +351,8 @@ void launch_stencil_widths(int64_t nx, int64_t ny, int64_t nz, int64_t row_offse
                            cudaStream_t s);
 void launch_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset,
                          int64_t col_offset, int64_t n_rows, int64_t n_slices,
-                         const int64_t* slice_off, double* vals, int32_t* cols, int blocks,
-                         cudaStream_t s);
+                         const int64_t* slice_off, double* vals, int32_t* cols, uint16_t* c16,
+                         int blocks, cudaStream_t s);
 void launch_csr_fill(const int64_t* row_ptr, const int64_t* col_idx, const double* values,
                      int64_t n_rows, int64_t n_slices, const int64_t* slice_off, double* vals,
                      int32_t* cols, int blocks, cudaStream_t s);

@@ -414,8 +414,13 @@ static tw_ell* gen_stencil(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int6
         launch_stencil_widths(nx, ny, nz, in.row_offset, in.n_rows, n_slices, widths,
                               ctx->cfg.stream_blocks, s);
         finish_ell(A, widths, n_slices, s);
+        // nx % 32 == 0: the fill writes the closed-form x-staged columns in
+        // the same pass (otherwise build_x_staged adds a run table)
+        if (nx % 32 == 0 &&
+            spmv_staged_smem_bytes(static_cast<int>(in.max_width)) + 2048 <= 227 * 1024)
+            TW_CUDA(cudaMalloc(&A->cols16, sizeof(uint16_t) * static_cast<size_t>(in.ell_entries + 64)));
         launch_stencil_fill(nx, ny, nz, in.row_offset, in.col_offset, in.n_rows, n_slices,
-                            A->slice_off, A->vals, A->cols, ctx->cfg.stream_blocks, s);
+                            A->slice_off, A->vals, A->cols, A->cols16, ctx->cfg.stream_blocks, s);
 #ifdef TW_CHECKS
         launch_ell_check(A->view(), s);
 #endif
