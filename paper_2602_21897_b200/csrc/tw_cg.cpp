@@ -397,9 +397,6 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             if (cg->opt.variant != TW_CG_TASKS)
                 config_error("the persistent dispatcher runs the tasks variant");
-            if (ctx->nccl_comm)
-                config_error("the persistent dispatcher runs without a communicator (halo and "
-                             "allgathers are NCCL launches)");
             int sb, vb, cb;
             if (dag_smem_bytes(A->info.max_width, A->cols16 != nullptr, &sb, &vb, &cb) > 225 * 1024)
                 config_error("matrix rows too wide for the dispatcher's shared-memory stages");
@@ -590,49 +587,99 @@ int64_t dag_vec_chunk_rows(const tw_cg* cg) {
     return fit >= 24576 ? 32768 : std::max<int64_t>(2048, fit & ~int64_t(255));
 }
 
-void build_dag_table(tw_cg* cg, int k) {
-    const int L = static_cast<int>(cg->nodes.size());
-    const int64_t spmv_cs = dag_spmv_chunk_slices(cg);
-    const int64_t vec_cr = dag_vec_chunk_rows(cg);
-    std::vector<DagTask> tasks(static_cast<size_t>(k) * L);
+// The task table of k iterations of the ranks g[0..P) (one rank on a GPU;
+// every rank of an emulated group in one launch), kept in g[0]->dag_tables[k].
+// Order: per iteration, phase by phase (halo, SpMV tiles, alpha, x/r tiles,
+// beta_res, p tiles), rank by rank inside a phase.  That order is
+// topological for the local edges and for the cross-rank ones (a ghost
+// plane's halo task precedes the SpMV tiles reading it; every rank's alpha
+// / beta_res publishes before it waits), so with every CTA resident a chunk
+// only ever waits on chunks already taken: no deadlock.
+void build_dag_table(tw_cg** g, int P, int k) {
+    const int64_t spmv_cs = dag_spmv_chunk_slices(g[0]);
+    const int64_t vec_cr = dag_vec_chunk_rows(g[0]);
+    // id of (rank, iteration, node), assigned in the launch order above (the
+    // end ranks have no halo node: node lists differ by at most one entry)
+    size_t L = 0;
+    for (int r = 0; r < P; ++r) L = std::max(L, g[r]->nodes.size());
+    std::vector<int> id_of(static_cast<size_t>(P) * k * L, -1);
+    auto key = [&](int r, int it, int j) {
+        return (static_cast<size_t>(r) * k + static_cast<size_t>(it)) * L + static_cast<size_t>(j);
+    };
+    std::vector<DagTask> tasks;
+    std::vector<std::pair<int, int>> who; // (rank, node) of every task, for the preds pass
+    std::vector<int> iter_of;
+    static const PhysKind kPhases[] = {PK_HALO, PK_SPMV, PK_ALPHA, PK_UPD, PK_BETA, PK_UPDP};
+    for (int it = 0; it < k; ++it)
+        for (PhysKind ph : kPhases)
+            for (int r = 0; r < P; ++r) {
+                const tw_cg* cg = g[r];
+                for (int j = 0; j < static_cast<int>(cg->nodes.size()); ++j) {
+                    const PNode& nd = cg->nodes[static_cast<size_t>(j)];
+                    if (nd.kind != ph) continue;
+                    id_of[key(r, it, j)] = static_cast<int>(tasks.size());
+                    DagTask t{};
+                    t.tile = nd.tile;
+                    t.rank = r;
+                    t.iter = it;
+                    t.r0 = cg->t_r0[static_cast<size_t>(nd.tile)];
+                    t.r1 = cg->t_r1[static_cast<size_t>(nd.tile)];
+                    t.nchunks = 1;
+                    switch (nd.kind) {
+                    case PK_SPMV: {
+                        t.kind = DK_SPMV;
+                        const int64_t ns = ((t.r1 + 31) >> 5) - (t.r0 >> 5);
+                        t.nchunks = static_cast<int>((ns + spmv_cs - 1) / spmv_cs);
+                        if (cg->peer) { // band (local x, inclusive) reaching a ghost plane
+                            if (cg->glo && cg->t_lo[static_cast<size_t>(nd.tile)] < cg->diag_shift)
+                                t.flags |= kDagGhostLo;
+                            if (cg->ghi && cg->t_hi[static_cast<size_t>(nd.tile)] >= cg->diag_shift + cg->n)
+                                t.flags |= kDagGhostHi;
+                        }
+                        break;
+                    }
+                    case PK_ALPHA: t.kind = DK_ALPHA; break;
+                    case PK_UPD:
+                        t.kind = DK_UPD;
+                        t.nchunks = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr);
+                        break;
+                    case PK_BETA: t.kind = DK_BETA; break;
+                    case PK_UPDP:
+                        t.kind = DK_UPDP;
+                        t.nchunks = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr);
+                        break;
+                    case PK_HALO:
+                        if (!cg->peer)
+                            contract_error("the dispatcher's halo task needs the peer transport");
+                        t.kind = DK_HALO;
+                        break;
+                    }
+                    tasks.push_back(t);
+                    who.emplace_back(r, j);
+                    iter_of.push_back(it);
+                }
+            }
     std::vector<std::vector<int>> succ(tasks.size());
     std::vector<int> npred(tasks.size(), 0), chunk_task;
-    for (int it = 0; it < k; ++it)
-        for (int j = 0; j < L; ++j) {
-            const PNode& nd = cg->nodes[static_cast<size_t>(j)];
-            const int id = it * L + j;
-            DagTask& t = tasks[static_cast<size_t>(id)];
-            t.tile = nd.tile;
-            t.r0 = cg->t_r0[static_cast<size_t>(nd.tile)];
-            t.r1 = cg->t_r1[static_cast<size_t>(nd.tile)];
-            int nch = 1;
-            switch (nd.kind) {
-            case PK_SPMV: {
-                t.kind = DK_SPMV;
-                const int64_t ns = ((t.r1 + 31) >> 5) - (t.r0 >> 5);
-                nch = static_cast<int>((ns + spmv_cs - 1) / spmv_cs);
-                break;
-            }
-            case PK_ALPHA: t.kind = DK_ALPHA; break;
-            case PK_UPD: t.kind = DK_UPD; nch = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr); break;
-            case PK_BETA: t.kind = DK_BETA; break;
-            case PK_UPDP: t.kind = DK_UPDP; nch = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr); break;
-            default: contract_error("halo task in the single-rank dispatcher");
-            }
-            t.chunk0 = static_cast<int>(chunk_task.size());
-            t.nchunks = nch;
-            chunk_task.insert(chunk_task.end(), static_cast<size_t>(nch), id);
-            auto add = [&](int pred) {
-                succ[static_cast<size_t>(pred)].push_back(id);
-                ++npred[static_cast<size_t>(id)];
-            };
-            if (it == 0) {
-                for (int p : nd.preds_first) add(p);
-            } else {
-                for (int p : nd.preds_intra) add(it * L + p);
-                for (int p : nd.preds_cross) add((it - 1) * L + p);
-            }
+    for (size_t id = 0; id < tasks.size(); ++id) {
+        const auto [r, j] = who[id];
+        const int it = iter_of[id];
+        const PNode& nd = g[r]->nodes[static_cast<size_t>(j)];
+        auto add = [&](int pit, int pj) {
+            const int pid = id_of[key(r, pit, pj)];
+            if (pid < 0 || pid >= static_cast<int>(id)) contract_error("task order is not topological");
+            succ[static_cast<size_t>(pid)].push_back(static_cast<int>(id));
+            ++npred[id];
+        };
+        if (it == 0) {
+            for (int p : nd.preds_first) add(0, p);
+        } else {
+            for (int p : nd.preds_intra) add(it, p);
+            for (int p : nd.preds_cross) add(it - 1, p);
         }
+        tasks[id].chunk0 = static_cast<int>(chunk_task.size());
+        chunk_task.insert(chunk_task.end(), static_cast<size_t>(tasks[id].nchunks), static_cast<int>(id));
+    }
     std::vector<int> flat;
     for (size_t i = 0; i < tasks.size(); ++i) {
         tasks[i].succ0 = static_cast<int>(flat.size());
@@ -645,7 +692,7 @@ void build_dag_table(tw_cg* cg, int k) {
         p = nullptr;
         TW_CUDA(cudaMalloc(&p, sizeof(*p) * std::max<size_t>(n, 1)));
     };
-    tw_cg::DagTable& tb = cg->dag_tables[k];
+    tw_cg::DagTable& tb = g[0]->dag_tables[k];
     realloc(tb.d_tasks, tasks.size());
     realloc(tb.d_chunk_task, chunk_task.size());
     realloc(tb.d_succ, flat.size());
@@ -662,62 +709,74 @@ void build_dag_table(tw_cg* cg, int k) {
     tb.nchunks = static_cast<int>(chunk_task.size());
 }
 
-// k iterations of cg_tasks as ONE persistent kernel (tw_dag.cu).
-void enqueue_persistent(tw_cg* cg, int k) {
+// k iterations of cg_tasks of the ranks g[0..P) as ONE persistent kernel
+// (tw_dag.cu) on g[0]'s compute stream.
+void enqueue_persistent(tw_cg** g, int P, int k) {
+    tw_cg* cg = g[0];
+    if (P > kDagMaxRanks) config_error("more ranks than one dispatcher launch holds");
     cudaStream_t s = cg->ctx->compute;
     if (!cg->dag_tables.count(k)) {
         TW_CUDA(cudaStreamSynchronize(s));
-        build_dag_table(cg, k);
+        build_dag_table(g, P, k);
     }
     const tw_cg::DagTable& tb = cg->dag_tables[k];
     TW_CUDA(cudaMemcpyAsync(tb.d_remaining, tb.d_npred, sizeof(int) * tb.ntasks,
                             cudaMemcpyDeviceToDevice, s));
     TW_CUDA(cudaMemsetAsync(tb.d_chunk_done, 0, sizeof(unsigned) * tb.ntasks, s));
-    TW_CUDA(cudaMemsetAsync(cg->d_ticket, 0, sizeof(unsigned), s));
-    DagParams P{};
-    P.tasks = tb.d_tasks;
-    P.chunk_task = tb.d_chunk_task;
-    P.succ = tb.d_succ;
-    P.remaining = tb.d_remaining;
-    P.chunk_done = tb.d_chunk_done;
-    P.chunk_part = tb.d_chunk_part;
-    P.ticket = cg->d_ticket;
-    P.nchunks = tb.nchunks;
-    P.ntasks = tb.ntasks;
-    P.T = cg->T;
-    P.A = cg->view();
-    P.p_local = cg->p_local;
-    P.p_owned = cg->p_owned;
-    P.x = cg->x;
-    P.r = cg->r;
-    P.Ap = cg->Ap;
-    P.sc = cg->sc;
-    P.history = cg->history;
-    P.stamps = cg->d_stamps;
-    P.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
-    P.pa = cg->pa;
-    P.rr = cg->rrp;
-    P.spmv_chunk_slices = dag_spmv_chunk_slices(cg);
-    P.vec_chunk_rows = dag_vec_chunk_rows(cg);
-    dag_smem_bytes(cg->A->info.max_width, P.A.cols16 != nullptr, &P.stage_bytes, &P.val_bytes,
-                   &P.c16_bytes);
+    for (int r = 0; r < P; ++r) // the chunk ticket and the tile-publication counters
+        TW_CUDA(cudaMemsetAsync(g[r]->d_ticket, 0, sizeof(unsigned) * 4, s));
+    DagParams D{};
+    D.tasks = tb.d_tasks;
+    D.chunk_task = tb.d_chunk_task;
+    D.succ = tb.d_succ;
+    D.remaining = tb.d_remaining;
+    D.chunk_done = tb.d_chunk_done;
+    D.chunk_part = tb.d_chunk_part;
+    D.ticket = cg->d_ticket;
+    D.nchunks = tb.nchunks;
+    D.ntasks = tb.ntasks;
+    D.T = cg->T;
+    D.nranks = P;
+    for (int r = 0; r < P; ++r) {
+        const tw_cg* c = g[r];
+        DagRank& R = D.rk[r];
+        R.A = c->view();
+        R.p_local = c->p_local;
+        R.p_owned = c->p_owned;
+        R.x = c->x;
+        R.r = c->r;
+        R.Ap = c->Ap;
+        R.sc = c->sc;
+        R.history = c->history;
+        R.stamps = c->d_stamps;
+        R.pa = c->pa;
+        R.rr = c->rrp;
+        R.links = c->peer ? c->d_links : nullptr;
+        R.win = c->peer ? c->win : nullptr;
+        R.tctr = c->d_ticket + 2;
+        R.iter0 = c->enqueued;
+    }
+    D.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
+    D.spmv_chunk_slices = dag_spmv_chunk_slices(cg);
+    D.vec_chunk_rows = dag_vec_chunk_rows(cg);
+    dag_smem_bytes(cg->A->info.max_width, D.rk[0].A.cols16 != nullptr, &D.stage_bytes,
+                   &D.val_bytes, &D.c16_bytes);
     // update chunks by TMA when the stage holds >= 128 rows of each operand
-    // (multiples of 64 rows: one 16-byte pair per lane and step)
-    // (the register path remains for stages too small for that)
-    const bool upd_tma = true;
-    // x update in the p-update chunks (x_in_k3): x/r chunks stream r, Ap and
-    // p chunks r, p, x; else x, p, r, Ap and r, p
-    const int rows2 = (P.stage_bytes / 16) & ~63, rows3 = (P.stage_bytes / 24) & ~63,
-              rows4 = (P.stage_bytes / 32) & ~63;
-    P.x_in_updp = upd_tma && x_in_k3(cg) && rows3 >= 128;
+    // (multiples of 64 rows: one 16-byte pair per lane and step); the
+    // register path remains for stages too small for that.  With the x
+    // update in the p-update chunks (x_in_k3) x/r chunks stream r, Ap and p
+    // chunks r, p, x; else x, p, r, Ap and r, p
+    const int rows2 = (D.stage_bytes / 16) & ~63, rows3 = (D.stage_bytes / 24) & ~63,
+              rows4 = (D.stage_bytes / 32) & ~63;
+    D.x_in_updp = x_in_k3(cg) && rows3 >= 128;
     // x/r chunks keep the 4-operand block size either way: a lane's rows (and
     // so its r.r partial) do not depend on where x is updated
-    const int ru = rows4, rp = P.x_in_updp ? rows3 : rows2;
-    P.upd_block_rows = upd_tma && ru >= 128 ? ru : 0;
-    P.updp_block_rows = upd_tma && rp >= 128 ? rp : 0;
+    const int ru = rows4, rp = D.x_in_updp ? rows3 : rows2;
+    D.upd_block_rows = ru >= 128 ? ru : 0;
+    D.updp_block_rows = rp >= 128 ? rp : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
-    launch_dag(P, cg->dag_grid, s);
+    launch_dag(D, cg->dag_grid, s);
 }
 
 void iterate(tw_cg* cg, int k) {
@@ -729,7 +788,10 @@ void iterate(tw_cg* cg, int k) {
     TW_CUDA(cudaSetDevice(cg->ctx->device));
     cudaStream_t s = cg->ctx->compute;
     if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
-        enqueue_persistent(cg, k);
+        // across ranks the dispatcher's cross edges are the peer protocol
+        if (cg->dist && cg->P > 1 && !cg->peer)
+            contract_error("the multi-rank dispatcher runs over the peer transport (tw_cg_peer_connect)");
+        enqueue_persistent(&cg, 1, k);
         if (cg->opt.iteration_marks) {
             cudaEvent_t e = cg->ta->take_event();
             TW_CUDA(cudaEventRecord(e, s));

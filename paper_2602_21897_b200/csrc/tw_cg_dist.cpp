@@ -144,8 +144,8 @@ void peer_update_p(tw_cg* cg, cudaStream_t s) {
 
 void alloc_window(tw_cg* cg) {
     if (!cg->dist) contract_error("the peer transport needs a multi-rank context");
-    if (cg->opt.variant != TW_CG_MONOLITHIC)
-        config_error("the peer transport runs the monolithic variant");
+    if (cg->opt.variant != TW_CG_MONOLITHIC && cg->opt.dispatch != TW_DISPATCH_PERSISTENT)
+        config_error("the peer transport runs the monolithic variant or the persistent dispatcher");
     if (cg->P > kMaxRanks) config_error("more ranks than the peer window holds");
     if (!cg->win) {
         TW_CUDA(cudaMalloc(&cg->win, sizeof(PeerWindow)));
@@ -191,8 +191,8 @@ void group_check(tw_cg** g, int P) {
         if (c->device != g[0]->ctx->device) contract_error("emulated ranks share one device");
         if (g[r]->opt.variant != g[0]->opt.variant || g[r]->T != g[0]->T)
             config_error("the ranks of a group run the same variant and tile count");
-        if (g[r]->opt.variant == TW_CG_TASKS && g[r]->opt.dispatch == TW_DISPATCH_PERSISTENT)
-            config_error("the emulated rank group runs the tasks variant on streams");
+        if (g[r]->opt.dispatch != g[0]->opt.dispatch)
+            config_error("the ranks of a group use the same dispatch");
     }
 }
 
@@ -227,8 +227,8 @@ void group_join(tw_cg** g, int P, cudaStream_t s) {
 // other ranks' buffers on the same device.
 void group_enable_peer(tw_cg** g, int P) {
     group_check(g, P);
-    if (g[0]->opt.variant != TW_CG_MONOLITHIC)
-        config_error("the peer transport runs the monolithic variant");
+    if (g[0]->opt.variant != TW_CG_MONOLITHIC && g[0]->opt.dispatch != TW_DISPATCH_PERSISTENT)
+        config_error("the peer transport runs the monolithic variant or the persistent dispatcher");
     for (int r = 0; r < P; ++r)
         if (g[r]->peer) contract_error("the peer transport is already connected");
     TW_CUDA(cudaSetDevice(g[0]->ctx->device));
@@ -306,8 +306,14 @@ void group_iterate(tw_cg** g, int P, int k) {
         TW_CUDA(cudaStreamWaitEvent(s, g[r]->fork_ev, 0));
     }
     const bool tasks = g[0]->opt.variant == TW_CG_TASKS;
-    if (tasks && g[0]->peer) contract_error("the peer transport runs the monolithic variant");
-    for (int it = 0; it < k && tasks; ++it) group_tasks_iteration(g, P, s);
+    const bool persistent = g[0]->opt.dispatch == TW_DISPATCH_PERSISTENT;
+    if (persistent && !g[0]->peer)
+        contract_error("the multi-rank dispatcher runs over the peer transport (tw_cg_group_enable_peer)");
+    // the block-task DAG of every rank in ONE persistent kernel: the ranks'
+    // cross edges are the peer protocol's flag waits, so all ranks run at
+    // once in one launch (never as separate launches waiting on each other)
+    if (persistent && k > 0) enqueue_persistent(g, P, k);
+    for (int it = 0; it < k && tasks && !persistent; ++it) group_tasks_iteration(g, P, s);
     for (int it = 0; it < k && !tasks && g[0]->peer; ++it) { // peer transport: stores + flags
         for (int r = 0; r < P; ++r) peer_spmv(g[r], s);
         for (int r = 0; r < P; ++r) peer_update_xr(g[r], s);

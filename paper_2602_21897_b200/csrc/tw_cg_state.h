@@ -158,8 +158,8 @@ void set_rhs(tw_cg* cg, const double* b, bool on_device);
 cudaEvent_t iter_event(tw_cg* cg, int i);
 int64_t dag_spmv_chunk_slices(const tw_cg* cg);
 int64_t dag_vec_chunk_rows(const tw_cg* cg);
-void build_dag_table(tw_cg* cg, int k);
-void enqueue_persistent(tw_cg* cg, int k);
+void build_dag_table(tw_cg** g, int P, int k);
+void enqueue_persistent(tw_cg** g, int P, int k);
 void iterate(tw_cg* cg, int k);
 void wait_cg(tw_cg* cg);
 

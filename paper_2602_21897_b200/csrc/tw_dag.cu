@@ -89,10 +89,50 @@ struct Slot {
     DagTask t;
 };
 
+// Stamp of the peer flags a task of iteration T.iter publishes / waits for.
+__device__ __forceinline__ unsigned long long task_stamp(const DagRank& R, const DagTask& T) {
+    return (static_cast<unsigned long long>(R.sc->epoch) << 32) |
+           static_cast<unsigned long long>(R.iter0 + T.iter + 1);
+}
+
+// alpha / beta_res across ranks, in two halves so that no publication ever
+// waits behind a wait (one thread each):
+//  * publish: by the scheduler completing the rank's LAST SpMV (x/r) tile of
+//    the iteration -- the tile partials summed in tile order into slot
+//    `rank` of every rank's window, its flag raised with the stamp
+//    (release, system scope); it waits on nothing;
+//  * gather: by the alpha (beta_res) task, once every rank's flag in the own
+//    window carries the stamp -- the partials summed in rank order, the sum
+//    the NCCL executor forms from its allgather (tw_cg_dist.cpp).
+// Every wait of the dispatcher is then on chunks with smaller tickets
+// (earlier in the table's order), which every CTA runs in ticket order: the
+// lowest-ticket waiting chunk always gets its producer.
+__device__ __noinline__ void publish_partial(const DagRank& R, const DagTask& T, int ntiles,
+                                             bool a) {
+    const double* tp = a ? R.pa : R.rr;
+    double v = 0.0;
+    for (int t = 0; t < ntiles; ++t) v = __dadd_rn(v, __ldcg(tp + t));
+    const PeerLinks* L = R.links;
+    const int me = L->rank, P = L->nranks;
+    const unsigned long long st = task_stamp(R, T);
+    for (int q = 0; q < P; ++q) (a ? L->win[q]->recv_a : L->win[q]->recv_b)[me] = v;
+    for (int q = 0; q < P; ++q) st_release_sys((a ? L->win[q]->flag_a : L->win[q]->flag_b) + me, st);
+}
+
+__device__ __noinline__ double gather_partials(const DagRank& R, const DagTask& T, bool a) {
+    const int P = R.links->nranks;
+    const unsigned long long st = task_stamp(R, T);
+    thread_wait_flags(a ? R.win->flag_a : R.win->flag_b, P, st);
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s = __dadd_rn(s, __ldcg((a ? R.win->recv_a : R.win->recv_b) + q));
+    return s;
+}
+
 // One chunk on the compute warps; returns this thread's dot partial.
 __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T, int j, int warp,
                                             int lane, unsigned char* stage, uint64_t* bar,
                                             int* stage_w, uint32_t& phase, uint64_t pol) {
+    const DagRank& R = P.rk[T.rank];
     const int ctid = warp * 32 + lane, cthreads = kComputeWarps * 32;
     double part = 0.0;
     switch (T.kind) {
@@ -104,7 +144,14 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
         int64_t s_hi = s_lo + P.spmv_chunk_slices;
         if (s_hi > s_end) s_hi = s_end;
-        if (P.A.cols16) { // x-staged matrix: the slice's x runs ride its TMA transaction
+        if (R.A.cols16) { // x-staged matrix: the slice's x runs ride its TMA transaction
+            // a tile reading a ghost plane: the neighbour's halo task of this
+            // iteration must have landed it (its flag carries the stamp)
+            if (lane == 0 && T.flags) {
+                const unsigned long long st = task_stamp(R, T);
+                if (T.flags & kDagGhostLo) thread_wait_flags(&R.win->flag_ghost_lo, 1, st);
+                if (T.flags & kDagGhostHi) thread_wait_flags(&R.win->flag_ghost_hi, 1, st);
+            }
             // p was written inside this kernel by other CTAs' generic stores
             // (made visible by the chunk's dependency acquire); order this
             // warp's async-proxy reads of it after that acquire
@@ -115,23 +162,23 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
             constexpr uint32_t kRunBytes = kStageRunLen * 8;
             for (int64_t s = s_lo + warp; s < s_hi; s += kComputeWarps) {
                 if (lane == 0) {
-                    const int64_t off = P.A.slice_off[s];
-                    const uint32_t ents = static_cast<uint32_t>(P.A.slice_off[s + 1] - off);
+                    const int64_t off = R.A.slice_off[s];
+                    const uint32_t ents = static_cast<uint32_t>(R.A.slice_off[s + 1] - off);
                     *stage_w = static_cast<int>(ents >> 5);
                     mbar_expect_tx(bar, ents * 10u + kStageRuns * kRunBytes);
                     if (ents) {
-                        bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
-                        bulk_g2s(stage + P.val_bytes, P.A.cols16 + off, ents * 2u, bar, pol);
+                        bulk_g2s(stage, R.A.vals + off, ents * 8u, bar, pol);
+                        bulk_g2s(stage + P.val_bytes, R.A.cols16 + off, ents * 2u, bar, pol);
                     }
                     int64_t starts[kStageRuns];
-                    run_starts(P.A, s, starts);
+                    run_starts(R.A, s, starts);
 #pragma unroll
                     for (int r = 0; r < kStageRuns; ++r) {
                         const int64_t st = starts[r];
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
-                            "l"(P.p_local + st), "r"(kRunBytes), "r"(smem_u32(bar))
+                            "l"(R.p_local + st), "r"(kRunBytes), "r"(smem_u32(bar))
                             : "memory");
                     }
                 }
@@ -149,7 +196,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 }
                 const int64_t row = (s << 5) + lane;
                 if (row >= T.r0 && row < T.r1) {
-                    P.Ap[row] = acc;
+                    R.Ap[row] = acc;
                     part = __dadd_rn(part, __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc));
                 }
                 __syncwarp();
@@ -159,13 +206,13 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         }
         for (int64_t s = s_lo + warp; s < s_hi; s += kComputeWarps) {
             if (lane == 0) {
-                const int64_t off = P.A.slice_off[s], end = P.A.slice_off[s + 1];
+                const int64_t off = R.A.slice_off[s], end = R.A.slice_off[s + 1];
                 const uint32_t ents = static_cast<uint32_t>(end - off);
                 *stage_w = static_cast<int>(ents >> 5);
                 mbar_expect_tx(bar, ents * 12u); // ents == 0 (all rows empty): completes at once
                 if (ents) {
-                    bulk_g2s(stage, P.A.vals + off, ents * 8u, bar, pol);
-                    bulk_g2s(stage + P.val_bytes, P.A.cols + off, ents * 4u, bar, pol);
+                    bulk_g2s(stage, R.A.vals + off, ents * 8u, bar, pol);
+                    bulk_g2s(stage + P.val_bytes, R.A.cols + off, ents * 4u, bar, pol);
                 }
             }
             __syncwarp();
@@ -176,19 +223,30 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
             const int32_t* cb = reinterpret_cast<const int32_t*>(stage + P.val_bytes);
             double acc;
             switch (w) {
-            case 27: acc = smem_row_fixed<27, kGatherCA>(vb, cb, P.p_local, lane); break;
-            case 18: acc = smem_row_fixed<18, kGatherCA>(vb, cb, P.p_local, lane); break;
-            case 12: acc = smem_row_fixed<12, kGatherCA>(vb, cb, P.p_local, lane); break;
-            case 8: acc = smem_row_fixed<8, kGatherCA>(vb, cb, P.p_local, lane); break;
-            default: acc = smem_row_generic<kGatherCA>(vb, cb, P.p_local, lane, w); break;
+            case 27: acc = smem_row_fixed<27, kGatherCA>(vb, cb, R.p_local, lane); break;
+            case 18: acc = smem_row_fixed<18, kGatherCA>(vb, cb, R.p_local, lane); break;
+            case 12: acc = smem_row_fixed<12, kGatherCA>(vb, cb, R.p_local, lane); break;
+            case 8: acc = smem_row_fixed<8, kGatherCA>(vb, cb, R.p_local, lane); break;
+            default: acc = smem_row_generic<kGatherCA>(vb, cb, R.p_local, lane, w); break;
             }
             const int64_t row = (s << 5) + lane;
             if (row >= T.r0 && row < T.r1) {
-                P.Ap[row] = acc;
-                part = __dadd_rn(part, __dmul_rn(P.p_owned[row], acc));
+                R.Ap[row] = acc;
+                part = __dadd_rn(part, __dmul_rn(R.p_owned[row], acc));
             }
             __syncwarp();
             if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        break;
+    }
+    case DK_HALO: {
+        // this rank's first / last owned plane of p into the neighbours'
+        // ghost planes (NVLink stores; the scheduler raises the flags)
+        const PeerLinks* L = R.links;
+        const int64_t pl = L->plane, n = R.A.n_rows;
+        for (int64_t i = ctid; i < pl; i += cthreads) {
+            if (L->ghost_lo_dst) L->ghost_lo_dst[i] = __ldcg(R.p_owned + i);
+            if (L->ghost_hi_dst) L->ghost_hi_dst[i] = __ldcg(R.p_owned + n - pl + i);
         }
         break;
     }
@@ -202,8 +260,8 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         // (alpha of this iteration is still in sc: the next alpha task waits
         // for every p update of this one)
         const bool xin = P.x_in_updp != 0;
-        const double alpha = upd || xin ? P.sc->alpha : 0.0, nalpha = -alpha;
-        const double beta = upd ? 0.0 : P.sc->beta;
+        const double alpha = upd || xin ? R.sc->alpha : 0.0, nalpha = -alpha;
+        const double beta = upd ? 0.0 : R.sc->beta;
         const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
         int64_t b = a + P.vec_chunk_rows;
         if (b > T.r1) b = T.r1;
@@ -227,17 +285,17 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 if (lane == 0) {
                     mbar_expect_tx(bar, (upd ? (xin ? 2u : 4u) : (xin ? 3u : 2u)) * bytes);
                     if (upd && xin) { // r, Ap
-                        bulk_g2s_plain(s0, P.r + q, bytes, bar);
-                        bulk_g2s_plain(s1, P.Ap + q, bytes, bar);
+                        bulk_g2s_plain(s0, R.r + q, bytes, bar);
+                        bulk_g2s_plain(s1, R.Ap + q, bytes, bar);
                     } else if (upd) {
-                        bulk_g2s_plain(s0, P.x + q, bytes, bar);
-                        bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
-                        bulk_g2s_plain(s2, P.r + q, bytes, bar);
-                        bulk_g2s_plain(s3, P.Ap + q, bytes, bar);
+                        bulk_g2s_plain(s0, R.x + q, bytes, bar);
+                        bulk_g2s_plain(s1, R.p_owned + q, bytes, bar);
+                        bulk_g2s_plain(s2, R.r + q, bytes, bar);
+                        bulk_g2s_plain(s3, R.Ap + q, bytes, bar);
                     } else { // r, p (and x)
-                        bulk_g2s_plain(s0, P.r + q, bytes, bar);
-                        bulk_g2s_plain(s1, P.p_owned + q, bytes, bar);
-                        if (xin) bulk_g2s_plain(s2, P.x + q, bytes, bar);
+                        bulk_g2s_plain(s0, R.r + q, bytes, bar);
+                        bulk_g2s_plain(s1, R.p_owned + q, bytes, bar);
+                        if (xin) bulk_g2s_plain(s2, R.x + q, bytes, bar);
                     }
                 }
                 __syncwarp();
@@ -249,7 +307,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         const double2 av = *reinterpret_cast<const double2*>(s1 + i);
                         rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
                         rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                        *reinterpret_cast<double2*>(P.r + q + i) = rv;
+                        *reinterpret_cast<double2*>(R.r + q + i) = rv;
                         part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
                         part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
                     } else if (upd) {
@@ -261,8 +319,8 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
                         rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
                         rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                        *reinterpret_cast<double2*>(P.x + q + i) = xv;
-                        *reinterpret_cast<double2*>(P.r + q + i) = rv;
+                        *reinterpret_cast<double2*>(R.x + q + i) = xv;
+                        *reinterpret_cast<double2*>(R.r + q + i) = rv;
                         part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
                         part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
                     } else {
@@ -272,11 +330,11 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                             double2 xv = *reinterpret_cast<const double2*>(s2 + i);
                             xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
                             xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
-                            *reinterpret_cast<double2*>(P.x + q + i) = xv;
+                            *reinterpret_cast<double2*>(R.x + q + i) = xv;
                         }
                         pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
                         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-                        *reinterpret_cast<double2*>(P.p_owned + q + i) = pv;
+                        *reinterpret_cast<double2*>(R.p_owned + q + i) = pv;
                     }
                 }
                 __syncwarp();
@@ -297,10 +355,10 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 for (int u = 0; u < U; ++u) {
                     const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
                     if (e < 2 * q1) {
-                        xv[u] = *reinterpret_cast<const double2*>(P.x + e);
-                        pv[u] = *reinterpret_cast<const double2*>(P.p_owned + e);
-                        rv[u] = *reinterpret_cast<const double2*>(P.r + e);
-                        av[u] = *reinterpret_cast<const double2*>(P.Ap + e);
+                        xv[u] = *reinterpret_cast<const double2*>(R.x + e);
+                        pv[u] = *reinterpret_cast<const double2*>(R.p_owned + e);
+                        rv[u] = *reinterpret_cast<const double2*>(R.r + e);
+                        av[u] = *reinterpret_cast<const double2*>(R.Ap + e);
                     }
                 }
 #pragma unroll
@@ -311,8 +369,8 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         xv[u].y = __dadd_rn(xv[u].y, __dmul_rn(alpha, pv[u].y));
                         rv[u].x = __dadd_rn(rv[u].x, __dmul_rn(nalpha, av[u].x));
                         rv[u].y = __dadd_rn(rv[u].y, __dmul_rn(nalpha, av[u].y));
-                        *reinterpret_cast<double2*>(P.x + e) = xv[u];
-                        *reinterpret_cast<double2*>(P.r + e) = rv[u];
+                        *reinterpret_cast<double2*>(R.x + e) = xv[u];
+                        *reinterpret_cast<double2*>(R.r + e) = rv[u];
                         part = __dadd_rn(part, __dmul_rn(rv[u].x, rv[u].x));
                         part = __dadd_rn(part, __dmul_rn(rv[u].y, rv[u].y));
                     }
@@ -323,8 +381,8 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 for (int u = 0; u < U; ++u) {
                     const int64_t e = 2 * (q + static_cast<int64_t>(u) * cthreads);
                     if (e < 2 * q1) {
-                        rv[u] = *reinterpret_cast<const double2*>(P.r + e);
-                        pv[u] = *reinterpret_cast<const double2*>(P.p_owned + e);
+                        rv[u] = *reinterpret_cast<const double2*>(R.r + e);
+                        pv[u] = *reinterpret_cast<const double2*>(R.p_owned + e);
                     }
                 }
 #pragma unroll
@@ -333,7 +391,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                     if (e < 2 * q1) {
                         pv[u].x = __dadd_rn(rv[u].x, __dmul_rn(beta, pv[u].x));
                         pv[u].y = __dadd_rn(rv[u].y, __dmul_rn(beta, pv[u].y));
-                        *reinterpret_cast<double2*>(P.p_owned + e) = pv[u];
+                        *reinterpret_cast<double2*>(R.p_owned + e) = pv[u];
                     }
                 }
             }
@@ -344,13 +402,13 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         const int64_t i = ctid == 0 ? lo : (ctid == 1 ? hi : -1);
         if (i >= 0) {
             if (upd) {
-                if (!xin) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
-                const double rv = __dadd_rn(P.r[i], __dmul_rn(nalpha, P.Ap[i]));
-                P.r[i] = rv;
+                if (!xin) R.x[i] = __dadd_rn(R.x[i], __dmul_rn(alpha, R.p_owned[i]));
+                const double rv = __dadd_rn(R.r[i], __dmul_rn(nalpha, R.Ap[i]));
+                R.r[i] = rv;
                 part = __dadd_rn(part, __dmul_rn(rv, rv));
             } else {
-                if (xin) P.x[i] = __dadd_rn(P.x[i], __dmul_rn(alpha, P.p_owned[i]));
-                P.p_owned[i] = __dadd_rn(P.r[i], __dmul_rn(beta, P.p_owned[i]));
+                if (xin) R.x[i] = __dadd_rn(R.x[i], __dmul_rn(alpha, R.p_owned[i]));
+                R.p_owned[i] = __dadd_rn(R.r[i], __dmul_rn(beta, R.p_owned[i]));
             }
         }
         break;
@@ -367,25 +425,42 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
 __device__ __forceinline__ void complete_chunk(const DagParams& P, const Slot& S,
                                                const double* wpart, int lane) {
     const DagTask& T = S.t;
+    const DagRank& R = P.rk[T.rank];
     if (lane == 0) {
         if (T.kind == DK_ALPHA) { // alpha task: tile partials in tile order (cg.cpp:217-222)
             double pAp = 0.0;
-            for (int t = 0; t < P.T; ++t) pAp = __dadd_rn(pAp, P.pa[t]);
-            P.sc->pAp = pAp;
-            P.sc->alpha = __ddiv_rn(P.sc->rtrans, pAp);
+            if (R.links) {
+                pAp = gather_partials(R, T, true);
+            } else {
+                for (int t = 0; t < P.T; ++t) pAp = __dadd_rn(pAp, R.pa[t]);
+            }
+            R.sc->pAp = pAp;
+            R.sc->alpha = __ddiv_rn(R.sc->rtrans, pAp);
         } else if (T.kind == DK_BETA) { // beta_res task (cg.cpp:299-309)
             double rr = 0.0;
-            for (int t = 0; t < P.T; ++t) rr = __dadd_rn(rr, P.rr[t]);
-            CgScalars* sc = P.sc;
+            if (R.links) {
+                rr = gather_partials(R, T, false);
+            } else {
+                for (int t = 0; t < P.T; ++t) rr = __dadd_rn(rr, R.rr[t]);
+            }
+            CgScalars* sc = R.sc;
             sc->rr = rr;
             sc->beta = __ddiv_rn(rr, sc->rtrans);
             sc->rtrans = rr;
             if (sc->iter < sc->history_cap) {
-                P.history[sc->iter] = __dsqrt_rn(rr);
-                P.stamps[sc->iter + 1] = globaltimer();
+                R.history[sc->iter] = __dsqrt_rn(rr);
+                R.stamps[sc->iter + 1] = globaltimer();
             }
             sc->iter = sc->iter + 1;
         }
+    }
+    if (T.kind == DK_HALO && lane == 0) {
+        // the compute warps' plane stores (ordered before the slot's EMPTY
+        // barrier) land in the neighbours' memory, then their ghost flags rise
+        __threadfence_system();
+        const unsigned long long st = task_stamp(R, T);
+        if (R.links->ghost_lo_flag) st_release_sys(R.links->ghost_lo_flag, st);
+        if (R.links->ghost_hi_flag) st_release_sys(R.links->ghost_hi_flag, st);
     }
     const bool has_part = T.kind == DK_SPMV || T.kind == DK_UPD;
     unsigned last = 0;
@@ -406,7 +481,18 @@ __device__ __forceinline__ void complete_chunk(const DagParams& P, const Slot& S
         double acc = 0.0;
         for (int i = lane; i < T.nchunks; i += 32) acc = __dadd_rn(acc, __ldcg(P.chunk_part + T.chunk0 + i));
         acc = warp_sum(acc);
-        if (lane == 0) (T.kind == DK_SPMV ? P.pa : P.rr)[T.tile] = acc;
+        if (lane == 0) {
+            (T.kind == DK_SPMV ? R.pa : R.rr)[T.tile] = acc;
+            if (R.links) { // across ranks: the last tile of the phase publishes
+                __threadfence();
+                const bool sp = T.kind == DK_SPMV;
+                const unsigned d = atomicInc(R.tctr + (sp ? 0 : 1), static_cast<unsigned>(P.T - 1));
+                if (d == static_cast<unsigned>(P.T - 1)) { // wraps to 0: reset for the next iteration
+                    __threadfence();
+                    publish_partial(R, T, P.T, sp);
+                }
+            }
+        }
     }
     __syncwarp();
     if (lane == 0) __threadfence();
@@ -443,7 +529,7 @@ __device__ __forceinline__ void fill_slot(const DagParams& P, Slot* S, int lane)
 // dependency acquire) while the compute warps run slot b, and completes slot
 // b (partials, counters, successor release) while they run slot b+1, so the
 // per-chunk bookkeeping is off the critical path and chunks can be small.
-__global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(DagParams P) {
+__global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(const __grid_constant__ DagParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kComputeWarps];
     __shared__ int stage_w[kComputeWarps];
@@ -543,7 +629,7 @@ int dag_blocks(int max_width, bool staged, int sm_count) {
 
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s) {
     int stage, vb, cb;
-    const int smem = dag_smem_bytes(P.A.max_width, P.A.cols16 != nullptr, &stage, &vb, &cb);
+    const int smem = dag_smem_bytes(P.rk[0].A.max_width, P.rk[0].A.cols16 != nullptr, &stage, &vb, &cb);
     dag_kernel<<<blocks, kDagWarps * 32, smem, s>>>(P);
     TW_CUDA(cudaGetLastError());
 }

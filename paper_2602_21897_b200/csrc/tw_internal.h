@@ -370,17 +370,50 @@ int spmv_tma_warps(); // consumer warps per CTA of the TMA SpMV
 
 // ------------------------------------------------- persistent DAG dispatcher
 
-enum DagKind : int { DK_SPMV = 0, DK_ALPHA = 1, DK_UPD = 2, DK_BETA = 3, DK_UPDP = 4 };
+enum DagKind : int { DK_SPMV = 0, DK_ALPHA = 1, DK_UPD = 2, DK_BETA = 3, DK_UPDP = 4, DK_HALO = 5 };
+
+// DagTask::flags: an SpMV tile whose band reads a ghost plane waits for that
+// plane's flag (the neighbour's halo task of the same iteration) first.
+constexpr int kDagGhostLo = 1, kDagGhostHi = 2;
 
 // One physical task of the flattened K-iteration DAG (tw_dag.cu).
 struct DagTask {
     int kind;
     int tile;
+    int rank;         // index into DagParams::rk (0 on one rank)
+    int iter;         // iteration within the launch (stamps of the peer flags)
+    int flags;        // kDagGhost*
     int64_t r0, r1;   // local rows of the tile
     int chunk0;       // first index in the global chunk list
     int nchunks;
     int succ0, nsucc; // successor task ids in DagParams::succ
 };
+
+// One rank's solver state as the dispatcher reads it.  Across ranks (the
+// NVLink peer transport) the cross-rank edges of the DAG are the peer
+// protocol of the monolithic path: the halo task stores the rank's first /
+// last owned plane into the neighbours' ghost planes and raises their ghost
+// flags; alpha / beta_res publish the rank's tile-order partial into every
+// rank's window and wait for all P (sums in rank order).  Flags carry the
+// stamp epoch << 32 | (iter0 + task.iter + 1).
+struct DagRank {
+    EllView A;
+    const double* p_local;   // gathered (owned + ghost planes)
+    double* p_owned;
+    double* x;
+    double* r;
+    double* Ap;
+    CgScalars* sc;
+    double* history;
+    unsigned long long* stamps; // globaltimer at each iteration end (index iter + 1)
+    double* pa;              // tile partials of p.Ap
+    double* rr;              // tile partials of r.r
+    const PeerLinks* links;  // device copy; null on one rank
+    PeerWindow* win;         // this rank's window (flags it waits on)
+    unsigned* tctr;          // [2] SpMV / x-r tiles done this iteration (publication)
+    int iter0;               // iterations done before this launch
+};
+constexpr int kDagMaxRanks = 16; // ranks of one launch (a real GPU: 1; an emulated group: P)
 
 struct DagParams {
     const DagTask* tasks;
@@ -392,19 +425,9 @@ struct DagParams {
     unsigned* ticket;        // next chunk to hand out
     int nchunks;
     int ntasks;              // entries of tasks (bounds of the checked build)
-    int T;                   // tiles per iteration
-    EllView A;
-    const double* p_local;   // gathered (owned + ghost planes)
-    double* p_owned;
-    double* x;
-    double* r;
-    double* Ap;
-    CgScalars* sc;
-    double* history;
-    unsigned long long* stamps; // globaltimer at each iteration end (index iter + 1)
+    int T;                   // tiles per iteration and rank
+    int nranks;              // entries of rk
     unsigned long long* start_stamp; // globaltimer when chunk 0 is taken
-    double* pa;              // tile partials of p.Ap
-    double* rr;              // tile partials of r.r
     int64_t spmv_chunk_slices;
     int64_t vec_chunk_rows;
     int stage_bytes, val_bytes, c16_bytes; // c16_bytes: the column block (16- or 32-bit)
@@ -412,6 +435,7 @@ struct DagParams {
     // warp's stage); 0 = register path
     int upd_block_rows, updp_block_rows;
     int x_in_updp; // x += alpha p_old in the p-update chunks (TMA path only)
+    DagRank rk[kDagMaxRanks];
 };
 
 int dag_smem_bytes(int max_width, bool staged, int* stage_bytes, int* val_bytes, int* c16_bytes);

@@ -470,8 +470,20 @@ def test_distributed_code_path_on_one_rank(orc, golden):
     xv = dev(b)
     P.halo_exchange(A, xv)
     assert np.array_equal(host(xv), b)
-    with pytest.raises(P.ConfigError):
-        P.CgSolver(rt2, A, 4, P.CgOptions(tiles=4, persistent=True))
+    # the persistent dispatcher on the 1-rank communicator (no halo task,
+    # alpha / beta_res local) and over its peer transport (publication and
+    # gather through the one rank's window, flags stamped per iteration)
+    for peer in (False, True):
+        s = P.CgSolver(rt2, A, 150, P.CgOptions(tiles=4, persistent=True, iteration_marks=False),
+                       variant=1)
+        if peer:
+            s.peer_connect([s.peer_export()])
+        s.set_rhs(b)
+        s.iterate(60)
+        s.iterate(90)
+        check_history(s.history(150), golden["cg_32_xorshift7_history"])
+        assert np.all(rel_gap(s.solution(), golden["cg_32_xorshift7_x"]) <= 1e-10)
+        s.close()
     # the NVLink peer transport on the same 1-rank communicator: export /
     # connect (own window, no IPC mapping), fused publish / wait kernels
     for graph in (False, True):
@@ -1056,3 +1068,36 @@ def test_multi_rank_block_task_dag(orc, P_, T):
 
 
 N_TASKS = 1  # TW_CG_TASKS
+
+
+@pytest.mark.parametrize("P_", [2, 3, 4, 8])
+@pytest.mark.parametrize("T", [1, 4, 16])
+def test_multi_rank_persistent_dispatcher(orc, P_, T):
+    """The persistent dispatcher across z-slab ranks: every rank's task table
+    in ONE launch (an emulated group on one GPU; on a real node each GPU runs
+    its own), the cross-rank edges being the peer protocol -- halo tasks
+    storing planes into the neighbours' ghost planes and raising their
+    flags, the ghost-reading SpMV tiles waiting for them, alpha / beta_res
+    publishing tile-order partials and summing every rank's in rank order.
+    Against the oracle under the rule; ranks agree; a re-solve (new epoch
+    stamps) repeats every bit; split calls (stamps continue) too."""
+    for dims in ((32, 16, 24), (30, 12, 16)):
+        m = orc.stencil(*dims)
+        b = orc.rhs_xorshift(m.n, 5)
+        want_h, want_x, _ = orc.cg(m, b, 40)
+        G = P.EmulatedRankGroup(*dims, P_, 40, variant=N_TASKS, transport="peer",
+                                options=P.CgOptions(tiles=T, persistent=True, iteration_marks=False))
+        assert all(s.mode()["dispatch"] == 1 for s in G.solvers)
+        runs = []
+        for split in ((40,), (13, 27)):
+            G.set_rhs(b)
+            for k in split:
+                G.iterate(k)
+            hs = G.history(40)
+            for h in hs:
+                assert np.array_equal(h, hs[0])
+            runs.append((hs[0], G.solution()))
+        G.close()
+        assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+        check_history(runs[0][0], want_h)
+        assert np.all(rel_gap(runs[0][1], want_x) <= 1e-10)
