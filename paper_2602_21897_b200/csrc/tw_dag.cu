@@ -243,6 +243,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         // this rank's first / last owned plane of p into the neighbours'
         // ghost planes (NVLink stores; the scheduler raises the flags)
         const PeerLinks* L = R.links;
+        if (!L) break; // no neighbours
         const int64_t pl = L->plane, n = R.A.n_rows;
         for (int64_t i = ctid; i < pl; i += cthreads) {
             if (L->ghost_lo_dst) L->ghost_lo_dst[i] = __ldcg(R.p_owned + i);
@@ -454,7 +455,7 @@ __device__ __forceinline__ void complete_chunk(const DagParams& P, const Slot& S
             sc->iter = sc->iter + 1;
         }
     }
-    if (T.kind == DK_HALO && lane == 0) {
+    if (T.kind == DK_HALO && R.links && lane == 0) {
         // the compute warps' plane stores (ordered before the slot's EMPTY
         // barrier) land in the neighbours' memory, then their ghost flags rise
         __threadfence_system();
