@@ -5,4 +5,3 @@ for f in paper_2602_21897_b200/_lib/variants/*.so; do
   TW_HPCCG_LIB=$f timeout 120 python scripts/kbench.py 256 30 >> gpurun_out/tune.log 2>&1
 done
 timeout 120 python scripts/kbench.py 256 30 >> gpurun_out/tune.log 2>&1
-TW_SPMV_PLAIN=1 timeout 120 python scripts/kbench.py 256 30 >> gpurun_out/tune.log 2>&1
