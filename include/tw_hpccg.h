@@ -119,9 +119,10 @@ int tw_gen_stencil_ell(tw_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t 
 int tw_ell_from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
                     const double* values, tw_ell** out);
 int tw_ell_info(const tw_ell* A, tw_ell_info_t* out);
-/* 1 when the matrix also carries the x-staged form the CG's K1 uses (a
- * stencil matrix or z-slab with nx % 32 == 0: 16-bit column indices into
- * per-slice windows of x; TW_STAGE_X=0 at build time disables it), else 0. */
+/* 1 when the matrix also carries the x-staged form the CG's K1 uses (16-bit
+ * column indices into 9 per-slice windows of x: closed-form windows for a
+ * stencil or z-slab with nx % 32 == 0, a per-slice run table otherwise),
+ * else 0. */
 int tw_ell_x_staged(const tw_ell* A, int* staged);
 /* Builds (enable != 0) or drops the x-staged form; *staged (optional) says
  * whether the matrix carries it afterwards.  tw_ell_from_csr matrices get it

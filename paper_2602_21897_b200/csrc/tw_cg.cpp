@@ -1082,7 +1082,7 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives) {
             k = cg->dist ? 5 : 3;
             c = cg->dist ? 3 : 0;
         } else {
-            k = 3 * cg->T + (cg->dist ? 4 : 0); // one rank: alpha / beta_res fold into the tiles
+            k = 3 * cg->T + (cg->dist ? 4 : cg->fold_scalars() ? 0 : 2); // one rank: alpha / beta_res fold into the tiles
             c = cg->dist ? 3 : 0;
         }
         if (kernels) *kernels = k;

@@ -97,9 +97,19 @@ struct tw_cg {
         return RedScratch{block_parts + static_cast<size_t>(i) * maxg, tickets + 4 * i};
     }
     // K1's view of A; l2_keep overrides the x-run L2 policy of the staged K1
-    // tasks variant, one rank: alpha / beta_res folded into the last tile
-    // kernel of their phase (no combine launch between the phases)
-    bool fold_scalars() const { return opt.variant == TW_CG_TASKS && !dist; }
+    // tasks variant, one rank, up to 4 tiles: alpha / beta_res folded into
+    // the last tile kernel of their phase (no combine launch between the
+    // phases; 128^3, 4 tiles: streams 132.7 -> 130.0 us).  With more tiles
+    // the empty join node turns into T x T edges between the phases (a
+    // captured graph has no node left to join on): 16 tiles 193 -> 212 us,
+    // 64 tiles 330 -> 523 us as one 16-iteration graph (profiles/
+    // r02_ab_tasks_executors.md), so there the combine kernels stay.
+#ifndef TW_FOLD_TILES
+#define TW_FOLD_TILES 4 // most tiles folded
+#endif
+    bool fold_scalars() const {
+        return opt.variant == TW_CG_TASKS && !dist && T <= TW_FOLD_TILES;
+    }
     Fin tile_fin(double* parts, int t, int then, unsigned* ticket) const {
         Fin f{FIN_STORE, parts + t, nullptr, nullptr};
         if (fold_scalars()) {

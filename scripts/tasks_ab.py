@@ -40,7 +40,11 @@ for nx, K, rows in ((128, 400, [("mono graph", 0, dict(tiles=1, use_graph=True, 
                                 ("T4 graph1", 1, dict(tiles=4, use_graph=True, iteration_marks=True)),
                                 ("T4 graphK", 1, dict(tiles=4, use_graph=True, iteration_marks=False)),
                                 ("T16 persistent", 1, dict(tiles=16, persistent=True, iteration_marks=False)),
-                                ("T16 graphK", 1, dict(tiles=16, use_graph=True, iteration_marks=False))]),
+                                ("T16 streams", 1, dict(tiles=16, iteration_marks=False)),
+                                ("T16 graph1", 1, dict(tiles=16, use_graph=True, iteration_marks=True)),
+                                ("T16 graphK", 1, dict(tiles=16, use_graph=True, iteration_marks=False)),
+                                ("T64 graph1", 1, dict(tiles=64, use_graph=True, iteration_marks=True)),
+                                ("T64 graphK", 1, dict(tiles=64, use_graph=True, iteration_marks=False))]),
                     (256, 60, [("mono graph", 0, dict(tiles=1, use_graph=True, iteration_marks=False)),
                                ("T4 streams", 1, dict(tiles=4, iteration_marks=False)),
                                ("T8 persistent", 1, dict(tiles=8, persistent=True, iteration_marks=False)),
