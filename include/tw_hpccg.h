@@ -130,7 +130,10 @@ int tw_ell_x_staged(const tw_ell* A, int* staged);
  * most 9 windows of 36 entries (the 27-point stencil does for nx % 32 == 0:
  * the reference's own gen_stencil_matrix output passed as a CsrMatrix runs
  * the same K1 as a device-generated grid); dropping it frees 2 B per entry
- * and makes the CG run the gather K1 (the results are bit-identical). */
+ * and makes the CG run the gather K1 (the results are bit-identical).  Call
+ * it before creating solvers on A (their graphs and dispatcher tables hold
+ * the form they were built with); tw_cg_solve's cached solvers of A are
+ * dropped here. */
 int tw_ell_set_x_staged(tw_ell* A, int enable, int* staged);
 /* Device ELL -> host CSR with GLOBAL column indices (row_ptr int64[n_rows+1],
  * col_idx int64[nnz], values double[nnz]); the structure parity check. */
@@ -375,7 +378,13 @@ int tw_cg_peer_ping_send(tw_cg* cg);
 int tw_cg_peer_ping_check(tw_cg* cg, int timeout_ms, int* ok);
 
 /* cg_monolithic / cg_tasks in one call (cg.cpp:397-447): host b in, host
- * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17). */
+ * history[iterations] and x[n_rows] out, *converged per CgResult (cg.hpp:12-17).
+ * The context keeps one solver per matrix between calls (rebuilt when the
+ * options change or more iterations are asked for; dropped with the matrix
+ * or the context); calls on one context are serialised.  Pageable host
+ * buffers move through pinned staging buffers filled / drained by host
+ * threads while the copy engine runs (tw_cg_set_rhs, tw_cg_solution and
+ * tw_ell_from_csr do the same). */
 int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iterations,
                 const tw_cg_options* opt, double* history_out, double* x_out, int* converged);
 

@@ -519,8 +519,10 @@ void set_rhs_prefix(tw_cg* cg, const double* b, bool on_device, cudaStream_t s) 
     TW_CUDA(cudaMemsetAsync(cg->x, 0, bytes, s));
     TW_CUDA(cudaMemsetAsync(cg->Ap, 0, bytes, s));
     TW_CUDA(cudaMemsetAsync(cg->p_local, 0, sizeof(double) * static_cast<size_t>(cg->x_len), s));
-    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, k, s));
+    if (on_device)
+        TW_CUDA(cudaMemcpyAsync(cg->r, b, bytes, cudaMemcpyDeviceToDevice, s));
+    else
+        copy_h2d(ctx, cg->r, b, bytes, s);
     TW_CUDA(cudaMemcpyAsync(cg->p_owned, cg->r, bytes, cudaMemcpyDeviceToDevice, s));
     const RedScratch rs = cg->slot(0);
     if (!cg->dist)
@@ -890,6 +892,20 @@ void wait_cg(tw_cg* cg) {
 
 using namespace tw::cgi;
 
+namespace tw {
+void drop_solve_cache(tw_ctx* ctx, const tw_ell* A) {
+    std::lock_guard lk(ctx->solve_mu);
+    for (auto it = ctx->solve_cache.begin(); it != ctx->solve_cache.end();) {
+        if (A && it->first != A) {
+            ++it;
+            continue;
+        }
+        free_cg(it->second);
+        it = ctx->solve_cache.erase(it);
+    }
+}
+} // namespace tw
+
 extern "C" {
 
 
@@ -964,8 +980,8 @@ int tw_cg_solution(tw_cg* cg, double* host_x) {
     return guarded([&] {
         if (!cg) contract_error("null solver");
         wait_cg(cg);
-        TW_CUDA(cudaMemcpy(host_x, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
-                           cudaMemcpyDeviceToHost));
+        copy_d2h(cg->ctx, host_x, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
+                 cg->ctx->compute);
     });
 }
 
@@ -1125,7 +1141,30 @@ int tw_cg_mode(tw_cg* cg, tw_cg_mode_t* out) {
 int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iterations,
                 const tw_cg_options* opt, double* history_out, double* x_out, int* converged) {
     return guarded([&] {
-        tw_cg* cg = create_cg(ctx, A, opt, iterations);
+        if (!ctx || !A) contract_error("null context or matrix");
+        // one solver per matrix kept between calls (no per-call allocation of
+        // x | r | p | Ap); reused when the options match and it holds enough
+        // history, rebuilt otherwise; set_rhs resets its whole state
+        std::lock_guard lk(ctx->solve_mu);
+        tw_cg_options o;
+        tw_cg_options_default(&o);
+        if (opt) o = *opt;
+        tw_cg*& cg = ctx->solve_cache[A];
+        const tw_cg_options& q = cg ? cg->req : o;
+        const bool same = q.variant == o.variant && q.tiles == o.tiles &&
+                          q.stream_pool_capacity == o.stream_pool_capacity &&
+                          q.use_graph == o.use_graph && q.iteration_marks == o.iteration_marks &&
+                          q.tol == o.tol && q.dispatch == o.dispatch && q.x_update == o.x_update &&
+                          q.l2_keep == o.l2_keep && q.dag_spmv_slices == o.dag_spmv_slices &&
+                          q.dag_vec_rows == o.dag_vec_rows;
+        if (cg && (!same || cg->max_iters < iterations)) {
+            free_cg(cg);
+            cg = nullptr;
+        }
+        if (!cg) {
+            cg = create_cg(ctx, A, &o, std::max(iterations, 1));
+            cg->req = o;
+        }
         try {
             set_rhs(cg, b_host, false);
             iterate(cg, iterations);
@@ -1136,15 +1175,15 @@ int tw_cg_solve(tw_ctx* ctx, const tw_ell* A, const double* b_host, int iteratio
                                    cudaMemcpyDeviceToHost));
             if (history_out) std::copy(h.begin(), h.begin() + iterations, history_out);
             if (x_out)
-                TW_CUDA(cudaMemcpy(x_out, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
-                                   cudaMemcpyDeviceToHost));
+                copy_d2h(ctx, x_out, cg->x, sizeof(double) * static_cast<size_t>(cg->n),
+                         ctx->compute);
             if (converged) // CgResult::converged (cg.cpp:392-393)
                 *converged = cg->opt.tol > 0 && iterations > 0 && h[iterations - 1] < cg->opt.tol;
         } catch (...) {
             free_cg(cg);
+            ctx->solve_cache.erase(A);
             throw;
         }
-        free_cg(cg);
     });
 }
 

@@ -17,6 +17,7 @@ struct tw_cg {
     tw_ctx* ctx = nullptr;
     const tw_ell* A = nullptr;
     tw_cg_options opt{};
+    tw_cg_options req{}; // the options as requested (tw_cg_solve's cache key)
     int max_iters = 0;
     int T = 1;
     int P = 1;

@@ -4,6 +4,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <deque>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <unordered_map>
@@ -128,6 +129,15 @@ struct tw_ctx {
     // task-aware completion for tw_event_bind_async (lazily started poller)
     std::unique_ptr<tw::TaskAware> ta;
     std::mutex ta_mu;
+    // two pinned staging buffers for pageable host <-> device copies
+    // (tw::copy_h2d / copy_d2h), allocated on first use
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+    std::mutex stage_mu;
+    // tw_cg_solve's solvers, kept per matrix between calls (the matrix's
+    // destroy and the context's release drop them)
+    std::map<const tw_ell*, tw_cg*> solve_cache;
+    std::mutex solve_mu;
 };
 
 struct tw_ell {
@@ -157,6 +167,15 @@ struct tw_ell {
 };
 
 namespace tw {
+// Host <-> device copies of caller buffers (tw_runtime.cpp).  Pinned memory
+// goes straight to the copy engine; pageable memory -- a reference caller's
+// std::vector -- through the context's two pinned staging buffers, host
+// threads filling (draining) one while the copy engine moves the other.
+// copy_h2d returns once the source may be reused; copy_d2h once dst holds
+// the data (both order on stream s).
+void copy_h2d(tw_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void copy_d2h(tw_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s);
+void drop_solve_cache(tw_ctx* ctx, const tw_ell* A); // A == nullptr: every entry
 // helpers shared across translation units
 RedScratch ctx_red_scratch(tw_ctx* ctx, cudaStream_t s);
 void tile_plan(const tw_ell* A, int tiles, std::vector<int64_t>& r0, std::vector<int64_t>& r1,

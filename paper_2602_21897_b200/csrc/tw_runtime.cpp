@@ -218,6 +218,90 @@ size_t TaskAware::pending() const {
     return binds_.size();
 }
 
+// ------------------------------------------------------- host <-> device
+
+constexpr size_t kStageBytes = size_t(32) << 20; // per staging buffer
+
+static bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy split over up to 8 host threads (>= 4 MB each)
+static void par_memcpy(void* dst, const void* src, size_t n) {
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t k = std::min<size_t>({8, hw, std::max<size_t>(1, n >> 22)});
+    std::vector<std::thread> th;
+    for (size_t i = 1; i < k; ++i) {
+        const size_t a = n * i / k, b = n * (i + 1) / k;
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+        });
+    }
+    std::memcpy(dst, src, n / k);
+    for (auto& t : th) t.join();
+}
+
+static void ensure_staging(tw_ctx* ctx) {
+    for (int i = 0; i < 2; ++i) {
+        if (!ctx->stage[i]) TW_CUDA(cudaMallocHost(&ctx->stage[i], kStageBytes));
+        if (!ctx->stage_ev[i]) {
+            TW_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+            TW_CUDA(cudaEventRecord(ctx->stage_ev[i], ctx->compute));
+        }
+    }
+}
+
+void copy_h2d(tw_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < (size_t(8) << 20) || host_pinned(src)) {
+        TW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    std::lock_guard lk(ctx->stage_mu);
+    ensure_staging(ctx);
+    for (size_t off = 0, i = 0; off < bytes; off += kStageBytes, ++i) {
+        const int b = static_cast<int>(i & 1);
+        const size_t n = std::min(kStageBytes, bytes - off);
+        TW_CUDA(cudaEventSynchronize(ctx->stage_ev[b])); // its previous copy has left
+        par_memcpy(ctx->stage[b], static_cast<const char*>(src) + off, n);
+        TW_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->stage[b], n,
+                                cudaMemcpyHostToDevice, s));
+        TW_CUDA(cudaEventRecord(ctx->stage_ev[b], s));
+    }
+}
+
+void copy_d2h(tw_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < (size_t(8) << 20) || host_pinned(dst)) {
+        TW_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        TW_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    std::lock_guard lk(ctx->stage_mu);
+    ensure_staging(ctx);
+    const size_t nch = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](size_t i) {
+        const int b = static_cast<int>(i & 1);
+        const size_t off = i * kStageBytes, n = std::min(kStageBytes, bytes - off);
+        TW_CUDA(cudaEventSynchronize(ctx->stage_ev[b]));
+        TW_CUDA(cudaMemcpyAsync(ctx->stage[b], static_cast<const char*>(src) + off, n,
+                                cudaMemcpyDeviceToHost, s));
+        TW_CUDA(cudaEventRecord(ctx->stage_ev[b], s));
+    };
+    issue(0);
+    if (nch > 1) issue(1);
+    for (size_t i = 0; i < nch; ++i) {
+        const int b = static_cast<int>(i & 1);
+        const size_t off = i * kStageBytes, n = std::min(kStageBytes, bytes - off);
+        TW_CUDA(cudaEventSynchronize(ctx->stage_ev[b]));
+        par_memcpy(static_cast<char*>(dst) + off, ctx->stage[b], n);
+        if (i + 2 < nch) issue(i + 2);
+    }
+}
+
 // ------------------------------------------------------------------ helpers
 
 RedScratch ctx_red_scratch(tw_ctx* ctx, cudaStream_t s) {
@@ -466,10 +550,10 @@ static tw_ell* from_csr(tw_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
         TW_CUDA(cudaMalloc(&d_ci, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
         TW_CUDA(cudaMalloc(&d_v, sizeof(double) * std::max<int64_t>(nnz, 1)));
         TW_CUDA(cudaMalloc(&widths, sizeof(int64_t) * std::max<int64_t>(n_slices, 1)));
-        TW_CUDA(cudaMemcpyAsync(d_rp, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+        copy_h2d(ctx, d_rp, row_ptr, sizeof(int64_t) * (n + 1), s);
         if (nnz) {
-            TW_CUDA(cudaMemcpyAsync(d_ci, col_idx, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
-            TW_CUDA(cudaMemcpyAsync(d_v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+            copy_h2d(ctx, d_ci, col_idx, sizeof(int64_t) * nnz, s);
+            copy_h2d(ctx, d_v, values, sizeof(double) * nnz, s);
         }
         launch_csr_widths(d_rp, n, n_slices, widths, ctx->cfg.stream_blocks, s);
         finish_ell(A, widths, n_slices, s);
@@ -719,6 +803,11 @@ int tw_ctx_destroy(tw_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaDeviceSynchronize();
+        drop_solve_cache(ctx, nullptr);
+        for (int i = 0; i < 2; ++i) {
+            if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
+            if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+        }
         if (ctx->ta) ctx->ta->poll_now(); // fire what completed, then stop the poller
         ctx->ta.reset();
         if (ctx->nccl_comm && nccl().CommDestroy) nccl().CommDestroy(ctx->nccl_comm);
@@ -957,6 +1046,7 @@ int tw_ell_set_x_staged(tw_ell* A, int enable, int* staged) {
         check_ell(A);
         TW_CUDA(cudaSetDevice(A->ctx->device));
         TW_CUDA(cudaStreamSynchronize(A->ctx->compute));
+        drop_solve_cache(A->ctx, A); // their graphs / tables may hold the old form
         if (enable) build_x_staged(A, A->ctx->compute);
         else drop_x_staged(A);
         if (staged) *staged = A->cols16 ? 1 : 0;
@@ -984,6 +1074,7 @@ int tw_ell_destroy(tw_ell* A) {
     return guarded([&] {
         if (!A) return;
         cudaSetDevice(A->ctx->device);
+        drop_solve_cache(A->ctx, A); // tw_cg_solve's solvers of this matrix
         free_ell(A);
         (void)cudaGetLastError(); // teardown is best effort: leave no stale error behind
     });

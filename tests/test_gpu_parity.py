@@ -1101,3 +1101,36 @@ def test_multi_rank_persistent_dispatcher(orc, P_, T):
         assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
         check_history(runs[0][0], want_h)
         assert np.all(rel_gap(runs[0][1], want_x) <= 1e-10)
+
+
+def test_cg_solve_cache_and_staged_copies(rt, orc):
+    """tw_cg_solve keeps its solver per matrix between calls (same results
+    call after call, a longer solve or other options rebuild it, dropping
+    the staged form drops it); pageable and pinned host buffers above the
+    staging threshold (8 MB) give the same bits."""
+    import torch
+    dims = (160, 128, 64)  # 1.3M rows: 10.5 MB vectors, above the staging threshold
+    m = orc.stencil(*dims)
+    A = P.ell_from_csr(m.row_ptr, m.col_idx, m.values, rt=rt)
+    b = orc.rhs_xorshift(m.n, 11)
+    assert b.nbytes > (8 << 20)
+    want_h, want_x, _ = orc.cg(m, b, 12)
+    opt = P.CgOptions(tiles=1, iteration_marks=False)
+    r1 = P.cg_solve(rt, A, b, 12, opt)
+    r2 = P.cg_solve(rt, A, b, 12, opt)                      # the cached solver
+    bp = torch.from_numpy(b.copy()).pin_memory().numpy()
+    xp = torch.empty(m.n, dtype=torch.float64).pin_memory().numpy()
+    r3 = P.cg_solve(rt, A, bp, 12, opt, x_out=xp)           # pinned: direct copies
+    r4 = P.cg_solve(rt, A, b, 20, opt)                      # more iterations: rebuilt
+    r5 = P.cg_solve(rt, A, b, 12, P.CgOptions(tiles=4, iteration_marks=False), variant=1)
+    for r in (r2, r3):
+        assert np.array_equal(r.residual_history, r1.residual_history)
+        assert np.array_equal(r.x, r1.x)
+    assert np.array_equal(r4.residual_history[:12], r1.residual_history)
+    check_history(r1.residual_history, want_h)
+    check_history(r5.residual_history, want_h)
+    assert np.all(rel_gap(r1.x, want_x) <= 1e-10)
+    assert not A.set_x_staged(False)                         # drops the cached solver
+    r6 = P.cg_solve(rt, A, b, 12, opt)
+    assert np.array_equal(r6.residual_history, r1.residual_history)
+    assert np.array_equal(r6.x, r1.x)
