@@ -62,12 +62,7 @@ int tw_ctx_device_info(tw_ctx* ctx, int* device, int* sm_count);
 int tw_comm_unique_id(unsigned char id_out[128]);
 int tw_ctx_init_comm(tw_ctx* ctx, int rank, int nranks, const unsigned char id[128]);
 int tw_ctx_comm_info(tw_ctx* ctx, int* rank, int* nranks);
-/* Emulated rank r of an nranks group on ONE device (no NCCL): for testing the
- * multi-rank algorithm on a single GPU.  Solvers on such contexts are driven
- * together by tw_cg_group_set_rhs / tw_cg_group_iterate, which run every
- * rank's phases on one stream with loopback device copies in place of the
- * NCCL halo and allgathers (no kernel waits on another). */
-int tw_ctx_init_emulated_rank(tw_ctx* ctx, int rank, int nranks);
+/* (Emulated ranks on one device for the multi-rank tests: tw_hpccg_emulation.h.) */
 
 /* Device buffers for callers without another allocator (tests, bench). */
 int tw_malloc(tw_ctx* ctx, void** ptr, int64_t bytes);
@@ -346,19 +341,6 @@ typedef struct tw_cg_mode_t {
 } tw_cg_mode_t;
 int tw_cg_mode(tw_cg* cg, tw_cg_mode_t* out);
 
-/* Emulated rank group (see tw_ctx_init_emulated_rank): cgs[r] is rank r's
- * monolithic solver, b[r] its rows of b. */
-int tw_cg_group_set_rhs(tw_cg** cgs, int nranks, const double* const* b, int b_is_device);
-int tw_cg_group_iterate(tw_cg** cgs, int nranks, int iterations);
-/* The emulated group over the NVLink peer transport (below) instead of the
- * loopback copies: the "peers" are the other ranks' buffers on the device. */
-int tw_cg_group_enable_peer(tw_cg** cgs, int nranks);
-/* The peer-transport group as ONE cooperative kernel: the ranks' blocks run
- * concurrently and wait on one another's flags (the multi-GPU protocol under
- * real concurrency on one device; the per-rank launches of a real multi-GPU
- * run must never share a GPU).  jitter != 0 delays rank-dependent blocks to
- * vary the interleavings.  Synchronous. */
-int tw_cg_group_iterate_concurrent(tw_cg** cgs, int nranks, int iterations, int jitter);
 
 /* NVLink peer transport for the monolithic multi-rank iteration: the halo is
  * stored by K3 straight into the neighbours' ghost planes and the rank

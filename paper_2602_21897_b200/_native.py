@@ -194,9 +194,14 @@ def check(rc: int) -> None:
         raise _ERRS.get(rc, TwError)(msg)
 
 
-def declared_symbols(header: str = HEADER) -> list[str]:
-    """Every function name include/tw_hpccg.h declares."""
+HEADERS = (HEADER, os.path.join(os.path.dirname(HEADER), "tw_hpccg_emulation.h"))
+
+
+def declared_symbols(headers=HEADERS) -> list[str]:
+    """Every function name include/tw_hpccg.h and tw_hpccg_emulation.h declare."""
     import re
-    text = open(header).read()
+    if isinstance(headers, str):
+        headers = (headers,)
+    text = "".join(open(h).read() for h in headers)
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(tw_[a-z0-9_]+)\s*\(", text)))

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "tw_hpccg.h"
+#include "tw_hpccg_emulation.h"
 
 namespace tw {
 
