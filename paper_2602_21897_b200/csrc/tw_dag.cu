@@ -132,6 +132,7 @@ __device__ __noinline__ double gather_partials(const DagRank& R, const DagTask& 
 __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T, int j, int warp,
                                             int lane, unsigned char* stage, uint64_t* bar,
                                             int* stage_w, uint32_t& phase, uint64_t pol) {
+    TW_DCHECK(T.rank >= 0 && T.rank < P.nranks);
     const DagRank& R = P.rk[T.rank];
     const int ctid = warp * 32 + lane, cthreads = kComputeWarps * 32;
     double part = 0.0;
@@ -175,6 +176,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
 #pragma unroll
                     for (int r = 0; r < kStageRuns; ++r) {
                         const int64_t st = starts[r];
+                        TW_DCHECK(st >= -2 && st <= R.A.x_len);
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),

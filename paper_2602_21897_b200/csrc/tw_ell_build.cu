@@ -107,6 +107,7 @@ stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset, int6
             if (k >= len) return uint32_t(kStagePad);
             int64_t cx, cy, cz;
             nb(k, cx, cy, cz);
+            TW_DCHECK(cx - x0 + 2 >= 0 && cx - x0 + 2 < kStageRunLen);
             return static_cast<uint32_t>(((cz - z + 1) * 3 + (cy - y + 1)) * kStageRunLen +
                                          (cx - x0 + 2));
         };
@@ -383,6 +384,7 @@ __global__ void csr_runs_kernel(EllView A, int32_t* runs, uint16_t* cols16, unsi
         }
         if (col(k) != kNone) atomicOr(bad, 1u);
         if (lane < kStageRuns) {
+            TW_DCHECK(start[lane < kStageRuns ? lane : 0] >= -2);
             int64_t v = start[0];
             for (int r = 1; r < kStageRuns; ++r)
                 if (lane == r) v = start[r];

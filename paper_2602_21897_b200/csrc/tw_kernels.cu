@@ -424,6 +424,8 @@ __device__ __forceinline__ void staged_spmv_body(
 #pragma unroll
         for (int r = 0; r < kStageRuns; ++r) {
             const int64_t st = starts[r];
+            // x carries 2 doubles of slack before index 0 and kStageRunLen after x_len
+            TW_DCHECK(st >= -2 && st <= A.x_len);
             if (KEEP) // small x: keep its lines in L2 (evict_last) for the other runs
                 bulk_g2s(xs + r * kStageRunLen, x + st, kRunBytes, bar, xpol);
             else
