@@ -1,8 +1,8 @@
 """GPU parity at the sizes the bench numbers are quoted on: BASELINE
 configs[2] (256^3 per GPU, b = xorshift64 seed 7 -- the headline) and
 configs[3] (512^3), through the exact kernel instantiations the headline runs
-(spmv_tma_staged_kernel<SPLIT=0, KEEP=0> with the x update in K3, one-iteration
-CUDA graph) and the other executors at that size.
+(spmv_tma_staged_kernel<SPLIT=0, KEEP=0> with the x update in K3, chunked
+CUDA graphs) and the other executors at that size.
 
 Checks:
   * K0 structure at 256^3 bit-exact against the REFERENCE's own
@@ -13,7 +13,10 @@ Checks:
     cg_reference history under the window rule, the final x against the
     committed sample of the reference's x and elementwise against the
     threaded oracle (itself pinned to that sample and history bit for bit);
-  * 512^3 x 4 iterations against the threaded matrix-free oracle.
+  * 512^3 x 4 iterations against the threaded matrix-free oracle;
+  * the multi-rank paths at the per-GPU sizes: 2 x 256^3 weak-scaling slabs
+    (loopback, concurrent peer protocol, multi-rank dispatcher) and 512^3 in
+    8 strong-scaling slabs, emulated on the one GPU, against the oracle.
 """
 import math
 
@@ -70,7 +73,7 @@ def test_k0_structure_256_vs_reference(A256, golden256, orc):
 
 
 EXECUTORS = {
-    # the bench headline: monolithic, one-iteration CUDA graph replayed
+    # the bench headline: monolithic, CUDA graphs of up to 16 iterations
     "mono_graph": (N.TW_CG_MONOLITHIC, dict(tiles=1, use_graph=True, iteration_marks=False)),
     "mono_streams": (N.TW_CG_MONOLITHIC, dict(tiles=1, use_graph=False)),
     # the same kernels with the x runs kept in L2 (KEEP=1): cache policy only
@@ -159,4 +162,65 @@ def test_cg_512_vs_oracle(rt, orc):
     del A
     want_h, want_x = orc.cg_stencil_mt(E, E, E, b, 4)
     check_history(h, want_h)
+    assert np.all(rel_gap(x, want_x) <= 1e-10)
+
+
+@pytest.fixture(scope="module")
+def oracle_weak2(orc):
+    """The threaded oracle on the 2-GPU weak-scaling grid (256 x 256 x 512)."""
+    dims = (256, 256, 512)
+    b = orc.rhs_xorshift(256 * 256 * 512, 7)
+    h, x = orc.cg_stencil_mt(*dims, b, 20)
+    return dims, b, h, x
+
+
+@pytest.mark.parametrize("how", ["loopback", "peer_concurrent", "tasks_dispatcher"])
+def test_weak_scaling_two_ranks_at_size(oracle_weak2, how):
+    """BASELINE configs[2] at N = 2, emulated on the one GPU: two z-slab ranks
+    of 256^3 each (256 x 256 x 512 global), at the per-GPU size the weak-
+    scaling numbers are quoted on -- the x-staged slab K1 with KEEP = 0, the x
+    update in K3, ghost planes of 512 KB -- over the loopback (NCCL-path
+    phases), the NVLink peer protocol under real concurrency (one
+    cooperative launch) and the multi-rank persistent dispatcher (16 tiles
+    per rank), against the threaded oracle."""
+    dims, b, want_h, want_x = oracle_weak2
+    if how == "tasks_dispatcher":
+        G = P.EmulatedRankGroup(*dims, 2, 20, variant=1, transport="peer",
+                                options=P.CgOptions(tiles=16, persistent=True,
+                                                    iteration_marks=False))
+    else:
+        G = P.EmulatedRankGroup(*dims, 2, 20, transport="loopback" if how == "loopback" else "peer")
+    m = G.solvers[0].mode()
+    assert m["k1_form"] == N.TW_K1_STAGED and m["k1_l2_keep"] == 0 and m["x_in_k3"] == 1
+    G.set_rhs(b)
+    if how == "peer_concurrent":
+        G.iterate_concurrent(20)
+    else:
+        G.iterate(20)
+    hs = G.history(20)
+    assert np.array_equal(hs[0], hs[1])
+    x = G.solution()
+    G.close()
+    check_history(hs[0], want_h)
+    assert np.all(rel_gap(x, want_x) <= 1e-10)
+
+
+def test_strong_scaling_512_eight_ranks(orc):
+    """BASELINE configs[3] at N = 8, emulated: 512^3 in eight 64-plane slabs
+    (over the loopback phases of the NCCL path), 3 iterations against the
+    threaded matrix-free oracle."""
+    if _host_gb() < 12:
+        pytest.skip("the 512^3 oracle needs ~7 GB of host memory")
+    E = 512
+    b = orc.rhs_xorshift(E ** 3, 7)
+    G = P.EmulatedRankGroup(E, E, E, 8, 3)
+    G.set_rhs(b)
+    G.iterate(3)
+    hs = G.history(3)
+    x = G.solution()
+    G.close()
+    for h in hs:
+        assert np.array_equal(h, hs[0])
+    want_h, want_x = orc.cg_stencil_mt(E, E, E, b, 3)
+    check_history(hs[0], want_h)
     assert np.all(rel_gap(x, want_x) <= 1e-10)
