@@ -329,6 +329,17 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
 }
 
 // ------------------------------------------------------ K1, x staged in smem
+#ifndef TW_K1_AP_KEEP
+#define TW_K1_AP_KEEP 1
+#endif
+__device__ __forceinline__ void st_evict_last(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st2_evict_last(double* p, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+                 "l"(pol)
+                 : "memory");
+}
 // (row bodies staged_row_fixed / staged_row_generic: tw_device.cuh)
 
 // Up to three row ranges walked as one index space of slices (range k's
@@ -397,6 +408,7 @@ __device__ __forceinline__ void staged_spmv_body(
     };
     const uint64_t pol = l2_evict_first_policy();
     const uint64_t xpol = KEEP ? l2_evict_last_policy() : 0;
+    const uint64_t appol = TW_K1_AP_KEEP ? l2_evict_last_policy() : 0;
     constexpr uint32_t kRunBytes = kStageRunLen * 8;
     const unsigned long long want = nwait ? stamp_of(fin.sc, 0) : 0ull;
     // lane 0: the slice block (values + 16-bit columns) and then its 9 x runs,
@@ -456,7 +468,8 @@ __device__ __forceinline__ void staged_spmv_body(
         }
         const int64_t row = (s << 5) + lane;
         if (row >= rr.r0 && row < rr.r1) {
-            y[row] = acc;
+            if (TW_K1_AP_KEEP) st_evict_last(y + row, acc, appol);
+            else y[row] = acc;
             const double d = __dmul_rn(xs[4 * kStageRunLen + 2 + lane], acc); // p[row] * (Ap)[row]
             if (SPLIT && k < mine_a) part_a = __dadd_rn(part_a, d);
             else part_b = __dadd_rn(part_b, d);
@@ -520,6 +533,14 @@ constexpr int kPairsUnroll = TW_PAIRS_UNROLL;
 #ifndef TW_K3_REV
 #define TW_K3_REV 1
 #endif
+// Cache hints of the produced vectors (same-box A/Bs in
+// profiles/r02_ab_k2k3_sweep.md): K1 stores Ap with L2 evict_last, so K2
+// finds more of it in L2 (256^3: K2 68 -> 62 us, iteration -4.3 us); K3
+// stores p with evict_last for the next K1 (128^3 -0.6 %, neutral at 256^3);
+// K2's r keeps the default policy (evict_last there: neutral).
+#ifndef TW_K3_P_KEEP
+#define TW_K3_P_KEEP 1
+#endif
 template <bool REV = false, typename F>
 __device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&& f) {
     const int64_t j0 = i0 >> 1, j1 = (i1 + 1) >> 1;
@@ -561,7 +582,8 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
                 const double2 av = __ldcs(reinterpret_cast<const double2*>(Ap + e));
                 rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
                 rv.y = __dadd_rn(rv.y, __dmul_rn(nalpha, av.y));
-                if (TW_K2_KEEP_R) *reinterpret_cast<double2*>(r + e) = rv;
+                if (TW_K2_KEEP_R == 2) st2_evict_last(r + e, rv, l2_evict_last_policy());
+                else if (TW_K2_KEEP_R) *reinterpret_cast<double2*>(r + e) = rv;
                 else __stcs(reinterpret_cast<double2*>(r + e), rv);
                 part = __dadd_rn(part, __dmul_rn(rv.x, rv.x));
                 part = __dadd_rn(part, __dmul_rn(rv.y, rv.y));
@@ -627,6 +649,7 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
                                          const double* __restrict__ psrc, double* __restrict__ p,
                                          double beta, double* __restrict__ x, double alpha) {
     const int64_t a = (a0 + 1) & ~int64_t(1), b = b0 & ~int64_t(1);
+    const uint64_t ppol = TW_K3_P_KEEP ? l2_evict_last_policy() : 0;
     auto pair = [&](int64_t e, double2 rv, double2 pv, double2 xv) {
         if (WX) {
             xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
@@ -635,7 +658,8 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
         }
         pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-        *reinterpret_cast<double2*>(p + e) = pv;
+        if (TW_K3_P_KEEP) st2_evict_last(p + e, pv, ppol);
+        else *reinterpret_cast<double2*>(p + e) = pv;
     };
     const int64_t J0 = a >> 1, J1 = b >> 1;
 #pragma unroll U
