@@ -329,17 +329,6 @@ spmv_tma_split_kernel(EllView A, const double* __restrict__ x, double* __restric
 }
 
 // ------------------------------------------------------ K1, x staged in smem
-#ifndef TW_K1_AP_KEEP
-#define TW_K1_AP_KEEP 1
-#endif
-__device__ __forceinline__ void st_evict_last(double* p, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st2_evict_last(double* p, double2 v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
-                 "l"(pol)
-                 : "memory");
-}
 // (row bodies staged_row_fixed / staged_row_generic: tw_device.cuh)
 
 // Up to three row ranges walked as one index space of slices (range k's
@@ -532,14 +521,6 @@ constexpr int kPairsUnroll = TW_PAIRS_UNROLL;
 #endif
 #ifndef TW_K3_REV
 #define TW_K3_REV 1
-#endif
-// Cache hints of the produced vectors (same-box A/Bs in
-// profiles/r02_ab_k2k3_sweep.md): K1 stores Ap with L2 evict_last, so K2
-// finds more of it in L2 (256^3: K2 68 -> 62 us, iteration -4.3 us); K3
-// stores p with evict_last for the next K1 (128^3 -0.6 %, neutral at 256^3);
-// K2's r keeps the default policy (evict_last there: neutral).
-#ifndef TW_K3_P_KEEP
-#define TW_K3_P_KEEP 1
 #endif
 template <bool REV = false, typename F>
 __device__ __forceinline__ void for_pairs(GridPos g, int64_t i0, int64_t i1, F&& f) {
