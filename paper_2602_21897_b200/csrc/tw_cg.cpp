@@ -761,8 +761,21 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
     D.start_stamp = cg->enqueued == 0 ? cg->d_stamps : cg->d_stamps + cg->max_iters + 1;
     D.spmv_chunk_slices = dag_spmv_chunk_slices(cg);
     D.vec_chunk_rows = dag_vec_chunk_rows(cg);
-    dag_smem_bytes(cg->A->info.max_width, D.rk[0].A.cols16 != nullptr, &D.stage_bytes,
-                   &D.val_bytes, &D.c16_bytes);
+    // the stages hold the widest slice of ANY rank of the launch (an end
+    // slab's rows reach one plane fewer than a middle slab's: 18 against 27
+    // entries), and the grid is what fits on the device at that size
+    int mw = 0;
+    bool staged = true;
+    for (int r = 0; r < P; ++r) {
+        mw = std::max(mw, static_cast<int>(g[r]->A->info.max_width));
+        staged = staged && D.rk[r].A.cols16 != nullptr;
+    }
+    if (!staged)
+        for (int r = 0; r < P; ++r)
+            if (D.rk[r].A.cols16) config_error("the ranks of one launch mix staged and gather matrices");
+    D.max_width = mw;
+    dag_smem_bytes(mw, staged, &D.stage_bytes, &D.val_bytes, &D.c16_bytes);
+    const int grid = P == 1 ? cg->dag_grid : dag_blocks(mw, staged, cg->ctx->sm_count);
     // update chunks by TMA when the stage holds >= 128 rows of each operand
     // (multiples of 64 rows: one 16-byte pair per lane and step); the
     // register path remains for stages too small for that.  With the x
@@ -778,7 +791,7 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
     D.updp_block_rows = rp >= 128 ? rp : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
-    launch_dag(D, cg->dag_grid, s);
+    launch_dag(D, grid, s);
 }
 
 void iterate(tw_cg* cg, int k) {

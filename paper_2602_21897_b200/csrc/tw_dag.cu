@@ -165,6 +165,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 if (lane == 0) {
                     const int64_t off = R.A.slice_off[s];
                     const uint32_t ents = static_cast<uint32_t>(R.A.slice_off[s + 1] - off);
+                    TW_DCHECK(ents <= 32u * static_cast<uint32_t>(P.max_width)); // fits the stage
                     *stage_w = static_cast<int>(ents >> 5);
                     mbar_expect_tx(bar, ents * 10u + kStageRuns * kRunBytes);
                     if (ents) {
@@ -210,6 +211,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
             if (lane == 0) {
                 const int64_t off = R.A.slice_off[s], end = R.A.slice_off[s + 1];
                 const uint32_t ents = static_cast<uint32_t>(end - off);
+                TW_DCHECK(ents <= 32u * static_cast<uint32_t>(P.max_width)); // fits the stage
                 *stage_w = static_cast<int>(ents >> 5);
                 mbar_expect_tx(bar, ents * 12u); // ents == 0 (all rows empty): completes at once
                 if (ents) {
@@ -632,7 +634,7 @@ int dag_blocks(int max_width, bool staged, int sm_count) {
 
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s) {
     int stage, vb, cb;
-    const int smem = dag_smem_bytes(P.rk[0].A.max_width, P.rk[0].A.cols16 != nullptr, &stage, &vb, &cb);
+    const int smem = dag_smem_bytes(P.max_width, P.rk[0].A.cols16 != nullptr, &stage, &vb, &cb);
     dag_kernel<<<blocks, kDagWarps * 32, smem, s>>>(P);
     TW_CUDA(cudaGetLastError());
 }

@@ -428,6 +428,7 @@ struct DagParams {
     int ntasks;              // entries of tasks (bounds of the checked build)
     int T;                   // tiles per iteration and rank
     int nranks;              // entries of rk
+    int max_width;           // widest slice over the ranks (sizes the stages)
     unsigned long long* start_stamp; // globaltimer when chunk 0 is taken
     int64_t spmv_chunk_slices;
     int64_t vec_chunk_rows;

@@ -1134,3 +1134,28 @@ def test_cg_solve_cache_and_staged_copies(rt, orc):
     r6 = P.cg_solve(rt, A, b, 12, opt)
     assert np.array_equal(r6.residual_history, r1.residual_history)
     assert np.array_equal(r6.x, r1.x)
+
+
+@pytest.mark.parametrize("dims,P_,T", [((32, 16, 4), 4, 1), ((48, 24, 3), 3, 1), ((48, 24, 3), 2, 2),
+                                       ((32, 16, 4), 4, 3)])
+def test_multi_rank_dispatcher_thin_slabs(orc, dims, P_, T):
+    """One-plane slabs next to wider ones: an end slab's rows reach one plane
+    fewer than a middle slab's (18 against 27 entries per row), so one launch
+    holds slices of different widths -- its stages and grid are sized by the
+    widest rank (found by scripts/stress_dispatcher.py: sizing them by rank
+    0 overran the stages)."""
+    m = orc.stencil(*dims)
+    b = orc.rhs_xorshift(m.n, 5)
+    want_h, want_x, _ = orc.cg(m, b, 15)
+    G = P.EmulatedRankGroup(*dims, P_, 15, variant=N_TASKS, transport="peer",
+                            options=P.CgOptions(tiles=T, persistent=True, iteration_marks=False))
+    G.set_rhs(b)
+    G.iterate(4)
+    G.iterate(11)
+    hs = G.history(15)
+    x = G.solution()
+    G.close()
+    for h in hs:
+        assert np.array_equal(h, hs[0])
+    check_history(hs[0], want_h)
+    assert np.all(rel_gap(x, want_x) <= 1e-10)
