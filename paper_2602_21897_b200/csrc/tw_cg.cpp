@@ -783,7 +783,11 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
     // chunks r, p, x; else x, p, r, Ap and r, p
     const int rows2 = (D.stage_bytes / 16) & ~63, rows3 = (D.stage_bytes / 24) & ~63,
               rows4 = (D.stage_bytes / 32) & ~63;
-    D.x_in_updp = x_in_k3(cg) && rows3 >= 128;
+    // (only when BOTH update kinds take the TMA path: the register path of
+    // the x/r chunks always updates x -- a stage too small for 4-operand
+    // blocks but not for 3 once updated x twice; found by
+    // scripts/stress_random.py on tiny grids)
+    D.x_in_updp = x_in_k3(cg) && rows3 >= 128 && rows4 >= 128;
     // x/r chunks keep the 4-operand block size either way: a lane's rows (and
     // so its r.r partial) do not depend on where x is updated
     const int ru = rows4, rp = D.x_in_updp ? rows3 : rows2;

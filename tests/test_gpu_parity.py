@@ -1159,3 +1159,19 @@ def test_multi_rank_dispatcher_thin_slabs(orc, dims, P_, T):
         assert np.array_equal(h, hs[0])
     check_history(hs[0], want_h)
     assert np.all(rel_gap(x, want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("dims,T", [((7, 1, 1), 1), ((3, 1, 12), 16), ((5, 3, 2), 2)])
+def test_dispatcher_x_update_on_tiny_stages(rt, orc, dims, T):
+    """Grids so small that the dispatcher's stages hold 3-operand but not
+    4-operand TMA blocks: with the x update placed in the p-update chunks,
+    the x/r chunks (register path) must not update x as well
+    (scripts/stress_random.py found x updated twice)."""
+    m = orc.stencil(*dims)
+    b = orc.rhs_xorshift(m.n, 2)
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    for xu in ("k2", "k3"):
+        res = P.cg_tasks(rt, A, b, 6, P.CgOptions(tiles=T, persistent=True, x_update=xu))
+        want_h, want_x, _ = orc.cg(m, b, 6)
+        check_history(res.residual_history, want_h)
+        assert np.all(rel_gap(res.x, want_x) <= 1e-10), xu
