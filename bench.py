@@ -793,7 +793,10 @@ def run_ours(args, dist, rank, world, local):
                        "k1": mode["k1_kernel"], "x_update_in": "K3" if mode["x_in_k3"] else "K2"},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": kernels_it * K, "nccl_calls": colls_it * K,
+            # the persistent dispatcher runs every iteration of a call in ONE launch
+            "gpu_launches": (len(reps) if mode["dispatch"] == N.TW_DISPATCH_PERSISTENT
+                             else kernels_it * K),
+            "nccl_calls": colls_it * K,
             "residual_last": float(hist[-1]),
         }
         if rejected:
