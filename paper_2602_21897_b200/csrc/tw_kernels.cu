@@ -738,32 +738,37 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // an edge plane without a neighbour streams with the bulk
     const int64_t lo_end = lo_dst ? (i0 + plane < i1 ? i0 + plane : i1) : i0;
     const int64_t hi_beg = hi_dst ? (i1 - plane > lo_end ? i1 - plane : lo_end) : i1;
-    stream(lo_end, hi_beg);
+    // the edge planes FIRST, so their system-scope fence waits only for the
+    // edge stores (after the bulk it waited for the block's share of the
+    // bulk too: 20 us of a 100 us K3 on a 1-rank communicator), and the
+    // neighbours' flags rise a whole K3 earlier
     const int ne = g.nblk < kEdgeBlocks ? g.nblk : kEdgeBlocks;
-    if (g.bid >= ne) return;
     const int64_t nlo = lo_end - i0, nedge = nlo + (i1 - hi_beg);
-    const int64_t etid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
-    const int64_t estride = static_cast<int64_t>(ne) * blockDim.x;
+    if (g.bid < ne && nedge > 0) {
+        const int64_t etid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
+        const int64_t estride = static_cast<int64_t>(ne) * blockDim.x;
 #pragma unroll 1
-    for (int64_t k = etid; k < nedge; k += estride) {
-        const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
-        TW_DCHECK(i >= i0 && i < i1);
-        if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
-        const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
-        p[i] = v;
-        if (lo_dst && i - i0 < plane) lo_dst[i - i0] = v;
-        if (hi_dst && i >= i1 - plane) hi_dst[i - (i1 - plane)] = v;
-    }
-    __syncthreads(); // the block's ghost stores are issued
-    if (threadIdx.x == 0) {
-        __threadfence_system(); // ... and have landed in the neighbours' memory
-        const unsigned t = atomicInc(rs.ticket + 1, static_cast<unsigned>(ne - 1));
-        if (t == static_cast<unsigned>(ne - 1)) {
-            __threadfence_system();
-            if (links->ghost_lo_flag) st_release_sys(links->ghost_lo_flag, next);
-            if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
+        for (int64_t k = etid; k < nedge; k += estride) {
+            const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
+            TW_DCHECK(i >= i0 && i < i1);
+            if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
+            const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
+            p[i] = v;
+            if (lo_dst && i - i0 < plane) lo_dst[i - i0] = v;
+            if (hi_dst && i >= i1 - plane) hi_dst[i - (i1 - plane)] = v;
+        }
+        __syncthreads(); // the block's ghost stores are issued
+        if (threadIdx.x == 0) {
+            __threadfence_system(); // ... and have landed in the neighbours' memory
+            const unsigned t = atomicInc(rs.ticket + 1, static_cast<unsigned>(ne - 1));
+            if (t == static_cast<unsigned>(ne - 1)) {
+                __threadfence_system();
+                if (links->ghost_lo_flag) st_release_sys(links->ghost_lo_flag, next);
+                if (links->ghost_hi_flag) st_release_sys(links->ghost_hi_flag, next);
+            }
         }
     }
+    stream(lo_end, hi_beg);
 }
 
 template <bool PEER, bool WX>
