@@ -572,21 +572,51 @@ cudaEvent_t iter_event(tw_cg* cg, int i) {
 // Flattens k iterations of the physical DAG into the dispatcher's task table
 // (topological order, chunk list, successor lists, predecessor counts).
 // Chunk sizes: up to 216 slices (12 per compute warp) per SpMV chunk and
-// 32768 rows per update chunk (the 256^3 optimum), but about 4 SpMV chunks
-// and 2 update chunks per CTA per pass on smaller problems (the 128^3
-// optimum; profiles/r01_dispatcher_summary.md).
+// 32768 rows per update chunk (the 256^3 optimum); on smaller problems SpMV
+// chunks in whole waves over the CTAs and update chunks of the next power
+// of two above half a CTA's rows (round-2 sweeps at 128^3, 16 tiles: 144.7
+// -> 132.7 us per iteration; profiles/r02_ab_tasks_executors.md).
 // tw_cg_options::dag_spmv_slices / dag_vec_rows override (tuning sweeps).
 int64_t dag_spmv_chunk_slices(const tw_cg* cg) {
     if (cg->opt.dag_spmv_slices > 0) return cg->opt.dag_spmv_slices;
-    const int64_t w = dag_compute_warps(), ns = (cg->n + 31) / 32;
-    const int64_t fit = ns / (4 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
-    return std::max(w, std::min(12 * w, fit));
+    const int64_t w = dag_compute_warps(), grid = std::max(cg->dag_grid, 1);
+    const int64_t ns_tile = ((cg->n + 31) / 32 + cg->T - 1) / cg->T;
+    // a whole number of slices per compute warp (the warps of a CTA share a
+    // chunk round-robin: one slice more than a multiple costs a round), and
+    // the phase's chunks in whole waves over the CTAs: among 1..12 slices
+    // per warp, the size whose chunk count fills its last wave best, with
+    // 4 to 8 waves per phase; a problem with more waves than that at 12
+    // slices per warp (256^3) takes 12
+    int64_t best = 12 * w;
+    double best_fill = -1.0;
+    for (int64_t k = 1; k <= 12; ++k) {
+        const int64_t sl = k * w;
+        const int64_t chunks = cg->T * ((ns_tile + sl - 1) / sl);
+        const double waves = static_cast<double>(chunks) / static_cast<double>(grid);
+        if (waves < 4.0 || waves > 8.0) continue;
+        const double fill = waves / std::ceil(waves);
+        if (fill > best_fill + 1e-9 || (std::abs(fill - best_fill) <= 1e-9 && sl > best)) {
+            best_fill = fill;
+            best = sl;
+        }
+    }
+    if (best_fill < 0.0) { // no size gives 4-8 waves: the largest that gives at least 4
+        best = w;
+        for (int64_t k = 12; k >= 1; --k)
+            if (cg->T * ((ns_tile + k * w - 1) / (k * w)) >= 4 * grid) {
+                best = k * w;
+                break;
+            }
+    }
+    return best;
 }
 int64_t dag_vec_chunk_rows(const tw_cg* cg) {
-    const int64_t fit = cg->n / (2 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
-    // multiples of 256 rows keep chunk boundaries on 2 KB (cache-line) edges
     if (cg->opt.dag_vec_rows > 0) return cg->opt.dag_vec_rows;
-    return fit >= 24576 ? 32768 : std::max<int64_t>(2048, fit & ~int64_t(255));
+    const int64_t fit = cg->n / (2 * static_cast<int64_t>(std::max(cg->dag_grid, 1)));
+    if (fit >= 24576) return 32768;
+    int64_t rows = 2048;
+    while (rows < fit) rows *= 2;
+    return rows;
 }
 
 // The task table of k iterations of the ranks g[0..P) (one rank on a GPU;
