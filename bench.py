@@ -33,6 +33,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+X_UPDATE_IN = {0: "K2", 1: "K3", 2: "K3 pairs"}  # tw_cg_mode_t.x_in_k3
 
 
 def parse():
@@ -696,9 +697,11 @@ def run_ours(args, dist, rank, world, local):
         traffic = traffic_of("k1")
         # the library moves the x update (x += alpha p_old) from K2 into K3
         # from 4M rows per rank (CgOptions.x_update): K2 then streams 24 n
-        # bytes and K3 40 n, 8 n less per iteration
-        xk3 = bool(mode["x_in_k3"])
-        k2_alg, k3_alg = (24 * n, 40 * n) if xk3 else (48 * n, 24 * n)
+        # bytes and K3 40 n, 8 n less per iteration; on one rank the K3s of
+        # each pair of iterations share one x pass (x_in_k3 == 2): 24 n and
+        # 48 n, 36 n per K3 on average, 12 n less than the x update in K2
+        xk3 = mode["x_in_k3"]
+        k2_alg, k3_alg = {0: (48 * n, 24 * n), 1: (24 * n, 40 * n), 2: (24 * n, 36 * n)}[xk3]
         roofline = {"bound": "hbm", "kernel": kname,
                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                     "traffic": traffic, "algorithmic_bytes": k1_bytes,
@@ -710,7 +713,7 @@ def run_ours(args, dist, rank, world, local):
                     "kernel_timing": (f"separate timed pass of {nt} iterations with events around "
                                       f"each kernel: {kt_pass_ms / nt:.4f} ms/iteration there, "
                                       f"{ms_max / K:.4f} in the event-free headline"),
-                    "x_update_in": "K3" if xk3 else "K2",
+                    "x_update_in": X_UPDATE_IN[xk3],
                     "k2_update_xr_gbs": k2_alg / (k2_ms / nt / 1e3) / 1e9,
                     "k3_update_p_gbs": k3_alg / (k3_ms / k3_launches / 1e3) / 1e9,
                     "k3_launches": k3_launches,
@@ -725,7 +728,7 @@ def run_ours(args, dist, rank, world, local):
                      "frac": iter_gbs / (peak * world), "algorithmic_bytes_per_iter": total_bytes}
     if roofline and roofline.get("format_bytes") != k1_bytes:
         fb = (bytes_it - k1_bytes + roofline["format_bytes"]
-              - (8 * n if roofline.get("x_update_in") == "K3" else 0)) * world
+              - {"K2": 0, "K3": 8 * n, "K3 pairs": 12 * n}[roofline.get("x_update_in")]) * world
         roofline_iter["format_bytes_per_iter"] = fb
         roofline_iter["achieved_format"] = fb / (ms_max / 1e3 / K) / 1e9
         roofline_iter["frac_format"] = roofline_iter["achieved_format"] / (peak * world)
@@ -790,7 +793,7 @@ def run_ours(args, dist, rank, world, local):
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
                        "nccl_comm": world > 1 or args.comm,
                        "transport": transport,
-                       "k1": mode["k1_kernel"], "x_update_in": "K3" if mode["x_in_k3"] else "K2"},
+                       "k1": mode["k1_kernel"], "x_update_in": X_UPDATE_IN[mode["x_in_k3"]]},
             "roofline": roofline, "roofline_iteration": roofline_iter,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             # the persistent dispatcher runs every iteration of a call in ONE launch

@@ -246,9 +246,12 @@ typedef struct tw_cg_options {
     int64_t dag_vec_rows;          /* persistent dispatcher: rows per update chunk         */
 } tw_cg_options;
 
-#define TW_XUPD_AUTO 0   /* K3 from 4M rows per rank (8n bytes less per iteration), else K2 */
+#define TW_XUPD_AUTO 0   /* K3 from 4M rows per rank (8n bytes less per iteration), else K2;
+                          * one-rank monolithic solves: K3 pairs from 512k rows             */
 #define TW_XUPD_K2 1     /* in K2 with r -= alpha Ap                                        */
 #define TW_XUPD_K3 2     /* in K3, reading p before it is overwritten                       */
+#define TW_XUPD_K3_PAIRS 3 /* in K3 once per pair of iterations, x = (x + a_k p_k) + a_k+1 p_k+1
+                            * (monolithic, one rank; 4n bytes less per iteration than _K3)       */
 #define TW_L2KEEP_AUTO 0 /* evict_last on the staged x runs while x has <= 8M entries       */
 #define TW_L2KEEP_ON 1
 #define TW_L2KEEP_OFF 2
@@ -311,9 +314,11 @@ int tw_task_dag_edges(int64_t n_rows, int tiles, const int64_t* r0, const int64_
                       const int64_t* band_lo, const int64_t* band_hi, int64_t diag_shift,
                       int64_t plane, int ghost_lo, int ghost_hi, int iterations, char* buf,
                       int64_t cap, int64_t* needed);
-/* Physical launches per iteration (kernels + NCCL calls), for reports.
- * Single-domain monolithic solves fuse K3 into the next iteration's K1:
- * 2 kernels per iteration plus one K3 per tw_cg_iterate call. */
+/* Physical launches per iteration (kernels + NCCL calls), for reports:
+ * monolithic 3 kernels (K1, K2, K3; across ranks 5 over NCCL, 3-4 over the
+ * peer transport); tasks 3 per tile plus the alpha / beta_res combines (none
+ * when folded into the tiles, 4 across ranks); the persistent dispatcher is
+ * one launch per tw_cg_iterate call (reported as 0). */
 int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
 
 /* What a solver actually executes (for reports and tests: the bench line
@@ -333,7 +338,7 @@ typedef struct tw_cg_mode_t {
     int32_t use_graph;
     int32_t k1_form;   /* TW_K1_*                                            */
     int32_t k1_l2_keep; /* staged K1 stages the x runs with L2 evict_last     */
-    int32_t x_in_k3;   /* x += alpha p runs in K3 (else in K2)               */
+    int32_t x_in_k3;   /* x += alpha p runs in K3 (else in K2); 2: in pairs  */
     int32_t transport; /* TW_TRANSPORT_*                                     */
     int32_t nranks;
     int32_t kernels_per_iteration;

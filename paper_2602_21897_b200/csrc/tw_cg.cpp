@@ -38,10 +38,39 @@ namespace cgi {
 // placement changes no bit (each element's update is the same rounding).
 bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
 
-static bool decide_x_in_k3(const tw_cg_options& o, int64_t n) { // at solver creation
-    if (o.x_update == TW_XUPD_K2) return false;
-    if (o.x_update == TW_XUPD_K3) return true;
-    return n >= (int64_t(1) << 22);
+// Paired x updates (one rank, monolithic): x = (x + a_k p_k) + a_k+1 p_k+1
+// in the second K3 of each pair of iterations, so x is read and written once
+// per pair; the first K3 writes p_k+1 to a second buffer and keeps p_k.
+// 4 n bytes less per iteration than the x update in every K3, no bit
+// changes.  Measured per iteration (profiles/r02_ab_k2k3_sweep.md), K3
+// every iteration / pairs / K2: 256^3 857-868 / 846-854 / 887-894 us,
+// 128^3 114.0-114.5 / 113.4-113.8 / 116.9-117.1, 96^3 57.6-57.9 /
+// 56.9-57.1 / 58.1-58.4, 64^3 29.0 / 28.7-28.8 / 28.4-28.6: pairs from
+// 512k rows on such a solver.
+static bool auto_pairs(const tw_cg* cg) {
+    return !cg->dist && cg->opt.variant == TW_CG_MONOLITHIC && cg->n >= (int64_t(1) << 19);
+}
+
+static bool decide_x_in_k3(const tw_cg* cg) { // at solver creation
+    const int xu = cg->opt.x_update;
+    if (xu == TW_XUPD_K2) return false;
+    if (xu == TW_XUPD_K3 || xu == TW_XUPD_K3_PAIRS) return true;
+    return cg->n >= (int64_t(1) << 22) || (TW_XPAIRS_AUTO && auto_pairs(cg));
+}
+
+static bool decide_x_pairs(const tw_cg* cg) {
+    if (cg->dist || cg->opt.variant != TW_CG_MONOLITHIC || !cg->x_k3) return false;
+    if (cg->opt.x_update == TW_XUPD_K3_PAIRS) return true;
+    return cg->opt.x_update == TW_XUPD_AUTO && TW_XPAIRS_AUTO && auto_pairs(cg);
+}
+
+// The x-update phase of iteration i of a run of k enqueued together: pairs
+// inside the run, a single update for an odd run's last iteration, so x and
+// p (in p_local) are current at the end of every run.
+int x_phase(const tw_cg* cg, int i, int k) {
+    if (!cg->x_pairs) return XPH_SINGLE;
+    if (i & 1) return XPH_PAIR;
+    return i + 1 < k ? XPH_DEFER : XPH_SINGLE;
 }
 
 // Physical predecessor lists from the logical DAG of iterations 0 and 1.
@@ -105,25 +134,35 @@ void record(cudaEvent_t e, cudaStream_t s) {
 // stream: K1 -> K2 -> K3 (x rides on K2 or on K3, x_in_k3); across ranks the
 // SpMV is split so the interior rows overlap the halo exchange on the comm
 // stream.
-void enqueue_mono(tw_cg* cg) {
+void enqueue_mono(tw_cg* cg, int xph) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
     if (!cg->dist) {
+        if (xph != XPH_SINGLE && !cg->x_pairs) contract_error("paired x update not enabled");
+        // p_k of this iteration: in the pair buffer for the second of a pair
+        double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
+        double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
         const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
-        if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{0, cg->n}, rs, fa, s))
-            launch_spmv(A, cg->p_owned, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs,
-                        s);
+        if (!launch_spmv_staged(A, pl, cg->Ap, RowRange{0, cg->n}, rs, fa, s))
+            launch_spmv(A, po, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s);
         record(tmark(cg, 1), s);
         const bool xk3 = x_in_k3(cg);
-        launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, cg->p_owned, cg->r, cg->Ap, cg->sc,
+        launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, po, cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv,
                          s);
         record(tmark(cg, 2), s);
-        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                        cg->history, bv, s, nullptr, nullptr, false, xk3 ? cg->x : nullptr);
+        if (xph == XPH_DEFER) // p_k+1 into the pair buffer, p_k and x left as they are
+            launch_update_p(0, cg->n, cg->r, cg->p2_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                            cg->history, bv, s, nullptr, cg->p_owned, false, nullptr);
+        else if (xph == XPH_PAIR) // x gets a_k-1 p_k-1 + a_k p_k; p_k+1 back into p_owned
+            launch_update_p_pair(0, cg->n, cg->r, cg->p_owned, cg->sc, cg->p2_owned, cg->p_owned,
+                                 cg->x, bv, s);
+        else
+            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                            cg->history, bv, s, nullptr, nullptr, false, xk3 ? cg->x : nullptr);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
@@ -300,7 +339,7 @@ cudaGraphExec_t build_chunk_graph(tw_cg* cg, int c) {
             for (int i = 0; i < c; ++i) enqueue_tasks(cg, i & 1, i == 0);
             join_streams(cg);
         } else {
-            for (int i = 0; i < c; ++i) enqueue_mono(cg);
+            for (int i = 0; i < c; ++i) enqueue_mono(cg, x_phase(cg, i, c));
         }
     } catch (...) {
         cudaStreamEndCapture(s, &g);
@@ -336,6 +375,7 @@ void free_cg(tw_cg* cg) {
     cudaFree(cg->x);
     cudaFree(cg->r_base);
     cudaFree(cg->p_base);
+    cudaFree(cg->p2_base);
     cudaFree(cg->Ap);
     cudaFree(cg->sc);
     cudaFree(cg->history);
@@ -406,6 +446,10 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         }
         if (cg->opt.variant != TW_CG_MONOLITHIC && cg->opt.variant != TW_CG_TASKS)
             config_error("unknown CG variant");
+        if (cg->opt.x_update < TW_XUPD_AUTO || cg->opt.x_update > TW_XUPD_K3_PAIRS)
+            config_error("unknown x_update placement");
+        if (cg->opt.l2_keep < TW_L2KEEP_AUTO || cg->opt.l2_keep > TW_L2KEEP_OFF)
+            config_error("unknown l2_keep policy");
         cg->T = cg->opt.variant == TW_CG_MONOLITHIC ? 1 : cg->opt.tiles; // cg.cpp:400
         cg->P = ctx->nranks;
         // rank-partial path: an NCCL communicator (also 1 rank) or an emulated rank
@@ -451,7 +495,16 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
         cg->p_local = cg->p_base + front;
         cg->p_owned = cg->p_local + cg->diag_shift;
-        cg->x_k3 = decide_x_in_k3(cg->opt, n);
+        cg->x_k3 = decide_x_in_k3(cg);
+        cg->x_pairs = decide_x_pairs(cg);
+        if (cg->x_pairs) { // the pair buffer: same line offset and slack as p_local
+            TW_CUDA(cudaMalloc(&cg->p2_base,
+                               sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
+            TW_CUDA(cudaMemset(cg->p2_base, 0,
+                               sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
+            cg->p2_local = cg->p2_base + front;
+            cg->p2_owned = cg->p2_local + cg->diag_shift;
+        }
         TW_CUDA(cudaMalloc(&cg->sc, sizeof(CgScalars)));
         TW_CUDA(cudaMalloc(&cg->history, sizeof(double) * std::max(max_iters, 1)));
         const int T = cg->T, P = cg->P;
@@ -860,7 +913,7 @@ void iterate(tw_cg* cg, int k) {
             cg->timed = 0;
             TW_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             try {
-                for (int i = 0; i < k; ++i) enqueue_mono(cg);
+                for (int i = 0; i < k; ++i) enqueue_mono(cg, x_phase(cg, i, k));
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
                 if (g) cudaGraphDestroy(g);
@@ -902,7 +955,7 @@ void iterate(tw_cg* cg, int k) {
         if (cg->opt.use_graph) {
             TW_CUDA(cudaGraphLaunch(cg->graph, s));
         } else if (!tasks) {
-            enqueue_mono(cg);
+            enqueue_mono(cg, x_phase(cg, i, k));
         } else {
             enqueue_iteration_body(cg, it & 1, i == 0);
         }
@@ -1171,7 +1224,7 @@ int tw_cg_mode(tw_cg* cg, tw_cg_mode_t* out) {
                             ? TW_K1_TMA_GATHER
                             : TW_K1_REGISTER;
         }
-        m.x_in_k3 = x_in_k3(cg);
+        m.x_in_k3 = cg->x_pairs ? 2 : x_in_k3(cg);
         m.transport = cg->ctx->emulated ? TW_TRANSPORT_LOOPBACK
                       : cg->peer        ? TW_TRANSPORT_PEER
                       : cg->dist        ? TW_TRANSPORT_NCCL

@@ -39,6 +39,9 @@ struct tw_cg {
     double* r = nullptr;      // r_base + 16: 2+ doubles of slack each side (staged runs of r)
     double* r_base = nullptr;
     double* p_base = nullptr;
+    double* p2_base = nullptr; // pair buffer (x_pairs): p_k+1 between the two K3s of a pair
+    double* p2_local = nullptr;
+    double* p2_owned = nullptr;
     double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
     double* p_owned = nullptr;
     double* Ap = nullptr;
@@ -67,6 +70,7 @@ struct tw_cg {
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
     std::map<int, cudaGraphExec_t> chunk_graphs; // up to kGraphChunk iterations, untimed
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
+    bool x_pairs = false; // ... once per pair of iterations (monolithic, one rank)
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;
@@ -151,7 +155,12 @@ void build_schedule(tw_cg* cg);
 int launch_blocks(const tw_cg* cg, bool spmv);
 cudaEvent_t tmark(tw_cg* cg, int k);
 void record(cudaEvent_t e, cudaStream_t s);
-void enqueue_mono(tw_cg* cg);
+#ifndef TW_XPAIRS_AUTO
+#define TW_XPAIRS_AUTO 1 // TW_XUPD_AUTO pairs the x updates wherever it puts them in K3
+#endif
+enum { XPH_SINGLE = 0, XPH_DEFER = 1, XPH_PAIR = 2 };
+int x_phase(const tw_cg* cg, int i, int k);
+void enqueue_mono(tw_cg* cg, int xph = XPH_SINGLE);
 int tile_share(const tw_cg* cg);
 void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st);
 void fork_streams(tw_cg* cg);

@@ -157,6 +157,7 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         break;
     case FIN_ALPHA:
         fin.sc->pAp = total;
+        fin.sc->alpha_prev = fin.sc->alpha;
         fin.sc->alpha = __ddiv_rn(fin.sc->rtrans, total);
         break;
     case FIN_BETA: {

@@ -148,6 +148,7 @@ struct CgScalars {
     int history_cap;
     unsigned epoch; // solve number (set_rhs count): high half of the peer flag stamps
     unsigned pad_;
+    double alpha_prev; // the previous iteration's alpha (FIN_ALPHA keeps it: paired x update)
 };
 
 // ------------------------------------------------- NVLink peer transport
@@ -266,6 +267,11 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
                      const double* psrc = nullptr, bool pdl = false, double* x = nullptr);
+// K3 of the second iteration of an x-update pair: p = r + beta p1,
+// x = (x + alpha_prev p0) + alpha p1 (p may alias p0)
+void launch_update_p_pair(int64_t i0, int64_t i1, const double* r, double* p,
+                          const CgScalars* sc, const double* p1, const double* p0, double* x,
+                          int blocks, cudaStream_t s);
 // K1 of the peer transport as one launch (interior, then the two boundary
 // ranges after a per-warp ghost-flag acquire), partials bit-identical to
 // the two launches; pm[0] = interior p.Ap into *fin.pre, fin (FIN_PUBLISH_A)

@@ -623,15 +623,37 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 #ifndef TW_K3X_UNROLL
 #define TW_K3X_UNROLL 4 // lean K3 with the x update (126 registers; 1.5 % faster than 2)
 #endif
-// WX: also x += alpha p_old (the x update moved out of K2).
-template <int U, bool WX>
+// The K3s of an x-update pair run best at the highest occupancy (no extra
+// unroll; 60 / 72 registers): 256^3, K3 averaged over the pair 118.0 us
+// with unroll 4 / 2, 98.3 with 1 / 1 (profiles/r02_ab_k2k3_sweep.md)
+#ifndef TW_K3_UNROLL
+#define TW_K3_UNROLL 1 // lean K3 without the x update
+#endif
+#ifndef TW_K3XX_UNROLL
+#define TW_K3XX_UNROLL 1 // K3 with the paired x update
+#endif
+// XU: the x update riding on K3's read of p_old --
+//   0: none;
+//   1: x += alpha p_old (the x update moved out of K2);
+//   2: the second iteration of a pair: x = (x + alpha0 p0) + alpha p_old,
+//      p0 / alpha0 = the previous iteration's p and alpha, whose update the
+//      first iteration of the pair deferred (the same two roundings in the
+//      same order as two single updates; x is read and written once per pair).
+template <int U, int XU>
 __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, int64_t stride,
                                          const double* __restrict__ r,
                                          const double* __restrict__ psrc, double* __restrict__ p,
-                                         double beta, double* __restrict__ x, double alpha) {
+                                         double beta, double* __restrict__ x, double alpha,
+                                         const double* __restrict__ p0 = nullptr,
+                                         double alpha0 = 0.0) {
+    constexpr bool WX = XU != 0;
     const int64_t a = (a0 + 1) & ~int64_t(1), b = b0 & ~int64_t(1);
     const uint64_t ppol = TW_K3_P_KEEP ? l2_evict_last_policy() : 0;
-    auto pair = [&](int64_t e, double2 rv, double2 pv, double2 xv) {
+    auto pair = [&](int64_t e, double2 rv, double2 pv, double2 xv, double2 ov) {
+        if (XU == 2) {
+            xv.x = __dadd_rn(xv.x, __dmul_rn(alpha0, ov.x));
+            xv.y = __dadd_rn(xv.y, __dmul_rn(alpha0, ov.y));
+        }
         if (WX) {
             xv.x = __dadd_rn(xv.x, __dmul_rn(alpha, pv.x));
             xv.y = __dadd_rn(xv.y, __dmul_rn(alpha, pv.y));
@@ -649,19 +671,22 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
         const int64_t e0 = 2 * (TW_K3_REV ? J0 + J1 - 1 - j : j);
         const int64_t e1 = 2 * (TW_K3_REV ? J0 + J1 - 1 - (j + stride) : j + stride);
         const double2 r0 = __ldcs(reinterpret_cast<const double2*>(r + e0));
-        const double2 p0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
-        double2 r1 = make_double2(0.0, 0.0), p1 = r1, x0 = r1, x1 = r1;
+        const double2 q0 = __ldcs(reinterpret_cast<const double2*>(psrc + e0));
+        double2 r1 = make_double2(0.0, 0.0), q1 = r1, x0 = r1, x1 = r1, o0 = r1, o1 = r1;
         if (WX) x0 = __ldcs(reinterpret_cast<const double2*>(x + e0));
+        if (XU == 2) o0 = __ldcs(reinterpret_cast<const double2*>(p0 + e0));
         if (two) {
             r1 = __ldcs(reinterpret_cast<const double2*>(r + e1));
-            p1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
+            q1 = __ldcs(reinterpret_cast<const double2*>(psrc + e1));
             if (WX) x1 = __ldcs(reinterpret_cast<const double2*>(x + e1));
+            if (XU == 2) o1 = __ldcs(reinterpret_cast<const double2*>(p0 + e1));
         }
-        pair(e0, r0, p0, x0);
-        if (two) pair(e1, r1, p1, x1);
+        pair(e0, r0, q0, x0, o0);
+        if (two) pair(e1, r1, q1, x1, o1);
     }
     if (tid == 0) {
         auto one = [&](int64_t i) {
+            if (XU == 2) x[i] = __dadd_rn(x[i], __dmul_rn(alpha0, p0[i]));
             if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
             p[i] = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
         };
@@ -718,7 +743,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // step (both pairs' loads issued before either store: twice the bytes in
     // flight of a one-pair loop); the at most two ragged ends go scalar.
     auto stream = [&](int64_t a0, int64_t b0) {
-        p_stream<PEER ? (WX ? TW_K3PX_UNROLL : 2) : (WX ? TW_K3X_UNROLL : 4), WX>(
+        p_stream<PEER ? (WX ? TW_K3PX_UNROLL : 2) : (WX ? TW_K3X_UNROLL : TW_K3_UNROLL), WX ? 1 : 0>(
             a0, b0, tid, stride, r, psrc, p, beta, x, alpha);
     };
     if (!links) {
@@ -777,6 +802,26 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
                 const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x) {
     update_p_rows<PEER, WX>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x);
+}
+
+// K3 of the second iteration of an x-update pair (one rank, monolithic):
+// p = r + beta p1 with p1 = this iteration's p_old, and x = (x + alpha_prev
+// p0) + alpha p1, p0 = the previous iteration's p_old, kept by the first
+// iteration of the pair (whose K3 wrote its new p to the other buffer and
+// left x alone).  p may alias p0 (each element read, then written, by the
+// same thread).  x moves 16 n bytes per PAIR instead of per iteration, for
+// 8 n bytes more reading p0: 4 n bytes less per iteration.
+__global__ void __launch_bounds__(kThreads)
+update_p_pair_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* p,
+                     const CgScalars* sc, const double* __restrict__ p1, const double* p0,
+                     double* __restrict__ x) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const double beta = sc->beta, alpha = sc->alpha, alpha0 = sc->alpha_prev;
+    const GridPos g = launch_grid();
+    const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
+    p_stream<TW_K3XX_UNROLL, 2>(i0, i1, tid, stride, r, p1, p, beta, x, alpha, p0, alpha0);
 }
 
 // ------------------------------------------- concurrent rank group (1 GPU)
@@ -1211,6 +1256,24 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
     if (x && !sc) throw Error(TW_ERR_CONTRACT, "the fused x update needs the solver's scalars");
     launch_k(kerns[which], dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history,
              links, psrc ? psrc : p, x);
+    TW_CUDA(cudaGetLastError());
+}
+
+void launch_update_p_pair(int64_t i0, int64_t i1, const double* r, double* p,
+                          const CgScalars* sc, const double* p1, const double* p0, double* x,
+                          int blocks, cudaStream_t s) {
+    static const int occ = [] {
+        int o = 0;
+        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &o, reinterpret_cast<const void*>(update_p_pair_kernel), kThreads, 0));
+        return o > 0 ? o : 1;
+    }();
+    int dev = 0, sms = 0;
+    TW_CUDA(cudaGetDevice(&dev));
+    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int wave = occ * sms;
+    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
+    update_p_pair_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, p1, p0, x);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -538,7 +538,7 @@ class CgOptions:
     auto_dispatch: bool = False  # TW_DISPATCH_AUTO: persistent for > 8 tiles on one rank
     # placement / tuning (no result bit changes, except the dispatcher's chunk
     # sizes, which set its chunk-order reduction tree): None = the library's choice
-    x_update: str | None = None   # "k2" | "k3": where x += alpha p runs
+    x_update: str | None = None   # "k2" | "k3" | "k3_pairs": where x += alpha p runs
     l2_keep: bool | None = None   # staged K1: x runs with an L2 evict_last hint
     dag_spmv_slices: int = 0
     dag_vec_rows: int = 0
@@ -555,7 +555,7 @@ class CgOptions:
         o.tol = float(self.tol)
         o.dispatch = (N.TW_DISPATCH_PERSISTENT if self.persistent else
                       N.TW_DISPATCH_AUTO if self.auto_dispatch else N.TW_DISPATCH_STREAMS)
-        o.x_update = {None: 0, "k2": 1, "k3": 2}[self.x_update]
+        o.x_update = {None: 0, "k2": 1, "k3": 2, "k3_pairs": 3}[self.x_update]
         o.l2_keep = 0 if self.l2_keep is None else (1 if self.l2_keep else 2)
         o.dag_spmv_slices = int(self.dag_spmv_slices)
         o.dag_vec_rows = int(self.dag_vec_rows)

@@ -66,7 +66,7 @@ for c in range(ncases):
         persistent = variant == 1 and rng.random() < 0.5
         opt = P.CgOptions(tiles=T, use_graph=not persistent and rng.random() < 0.5,
                           iteration_marks=rng.random() < 0.5, persistent=persistent,
-                          x_update=rng.choice([None, "k2", "k3"]),
+                          x_update=rng.choice([None, "k2", "k3", "k3_pairs"]),
                           l2_keep=rng.choice([None, True, False]))
         tag = (kind, dims, variant, T, persistent, opt.use_graph, opt.x_update, opt.l2_keep)
         try:

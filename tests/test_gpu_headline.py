@@ -1,8 +1,9 @@
 """GPU parity at the sizes the bench numbers are quoted on: BASELINE
 configs[2] (256^3 per GPU, b = xorshift64 seed 7 -- the headline) and
 configs[3] (512^3), through the exact kernel instantiations the headline runs
-(spmv_tma_staged_kernel<SPLIT=0, KEEP=0> with the x update in K3, chunked
-CUDA graphs) and the other executors at that size.
+(spmv_tma_staged_kernel<SPLIT=0, KEEP=0> with the x update in K3 once per
+pair of iterations, chunked CUDA graphs) and the other executors at that
+size.
 
 Checks:
   * K0 structure at 256^3 bit-exact against the REFERENCE's own
@@ -79,6 +80,7 @@ EXECUTORS = {
     # the same kernels with the x runs kept in L2 (KEEP=1): cache policy only
     "mono_keep": (N.TW_CG_MONOLITHIC, dict(tiles=1, l2_keep=True)),
     "mono_x_in_k2": (N.TW_CG_MONOLITHIC, dict(tiles=1, x_update="k2")),
+    "mono_x_every_k3": (N.TW_CG_MONOLITHIC, dict(tiles=1, x_update="k3")),
     # block-task DAG (configs[4] granularities at the per-GPU size)
     "tasks_T4_graph": (N.TW_CG_TASKS, dict(tiles=4, use_graph=True)),
     "tasks_T16_streams": (N.TW_CG_TASKS, dict(tiles=16)),
@@ -94,12 +96,14 @@ def test_cg_256_vs_reference(rt, A256, golden256, oracle256, name):
     m = S.mode()
     assert m["k1_form"] == N.TW_K1_STAGED  # spmv_tma_staged_kernel
     if name in ("mono_graph", "mono_streams"):
-        # the headline instantiation: <SPLIT=0, KEEP=0>, x update in K3
-        assert (m["k1_l2_keep"], m["x_in_k3"], m["kernels_per_iteration"]) == (0, 1, 3)
+        # the headline instantiation: <SPLIT=0, KEEP=0>, x update in K3 in pairs
+        assert (m["k1_l2_keep"], m["x_in_k3"], m["kernels_per_iteration"]) == (0, 2, 3)
     if name == "mono_keep":
         assert m["k1_l2_keep"] == 1
     if name == "mono_x_in_k2":
         assert m["x_in_k3"] == 0
+    if name == "mono_x_every_k3":
+        assert m["x_in_k3"] == 1
     b = P.rhs_xorshift(rt, A256.n, 7)  # the bench's device generator
     S.set_rhs(b)
     S.iterate(10)  # in two calls, as the bench's warm-up + timed passes
@@ -119,11 +123,11 @@ def test_cg_256_vs_reference(rt, A256, golden256, oracle256, name):
 
 
 def test_cg_256_placements_bit_identical(rt, A256):
-    """Cache policy (KEEP) and x-update placement change no bit at the
-    headline size."""
+    """Cache policy (KEEP) and x-update placement (K2, every K3, K3 pairs)
+    change no bit at the headline size."""
     b = P.rhs_xorshift(rt, A256.n, 7)
     out = []
-    for kw in (dict(), dict(l2_keep=True), dict(x_update="k2")):
+    for kw in (dict(), dict(l2_keep=True), dict(x_update="k2"), dict(x_update="k3")):
         S = P.CgSolver(rt, A256, 20, P.CgOptions(tiles=1, **kw), variant=N.TW_CG_MONOLITHIC)
         S.set_rhs(b)
         S.iterate(20)
@@ -153,7 +157,7 @@ def test_cg_512_vs_oracle(rt, orc):
     S = P.CgSolver(rt, A, 4, P.CgOptions(tiles=1, use_graph=True, iteration_marks=False),
                    variant=N.TW_CG_MONOLITHIC)
     m = S.mode()
-    assert (m["k1_form"], m["k1_l2_keep"], m["x_in_k3"]) == (N.TW_K1_STAGED, 0, 1)
+    assert (m["k1_form"], m["k1_l2_keep"], m["x_in_k3"]) == (N.TW_K1_STAGED, 0, 2)
     b = orc.rhs_xorshift(E ** 3, 7)
     S.set_rhs(b)
     S.iterate(4)

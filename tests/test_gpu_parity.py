@@ -1175,3 +1175,54 @@ def test_dispatcher_x_update_on_tiny_stages(rt, orc, dims, T):
         want_h, want_x, _ = orc.cg(m, b, 6)
         check_history(res.residual_history, want_h)
         assert np.all(rel_gap(res.x, want_x) <= 1e-10), xu
+
+
+@pytest.mark.parametrize("how", ["streams", "graph_chunks", "graph_marks", "timed_graph"])
+def test_x_update_pairs_bit_identical(rt, orc, how):
+    """Paired x updates (CgOptions.x_update="k3_pairs", the default of a
+    one-rank monolithic solve from 4M rows): the first K3 of each pair of
+    iterations writes p_k+1 to a second buffer and leaves x alone, the second
+    applies x = (x + a_k p_k) + a_k+1 p_k+1 -- the two roundings of two single
+    updates in the same order.  Histories, x, r and p (at every call
+    boundary: an odd call's last iteration is a single update) must be
+    bit-identical to the x update in every K3, for calls of odd and even
+    lengths on every monolithic executor."""
+    from paper_2602_21897_b200 import _native as N
+    dims = (64, 40, 36)
+    n = int(np.prod(dims))
+    b = orc.rhs_xorshift(n, 6)
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    calls = (1, 2, 3, 5, 16, 17, 4)
+    total = sum(calls)
+    kw = dict(streams=dict(use_graph=False),
+              graph_chunks=dict(use_graph=True, iteration_marks=False),
+              graph_marks=dict(use_graph=True, iteration_marks=True),
+              timed_graph=dict(use_graph=True, iteration_marks=False))[how]
+    out = {}
+    for xu in ("k3", "k3_pairs", None):
+        S = P.CgSolver(rt, A, total, P.CgOptions(x_update=xu, **kw), variant=N.TW_CG_MONOLITHIC)
+        want_mode = {"k3": 1, "k3_pairs": 2, None: 0}[xu]  # auto below 4M rows: K2
+        assert S.mode()["x_in_k3"] == want_mode
+        if how == "timed_graph":
+            S.enable_kernel_timing(True)
+        S.set_rhs(b)
+        snaps = []
+        for c in calls:
+            S.iterate(c)
+            S.wait()
+            xp, rp, pp, _ = S.vectors()
+            for ptr in (xp, rp, pp):
+                h = np.empty(n, np.float64)
+                N.check(N.load().tw_memcpy(rt.h, h.ctypes.data_as(N.C.c_void_p), N.C.c_void_p(ptr),
+                                           h.nbytes, None))
+                rt.synchronize()
+                snaps.append(h)
+        out[xu] = (S.history(total), snaps)
+        S.close()
+    for xu in ("k3_pairs", None):
+        assert np.array_equal(out[xu][0], out["k3"][0]), xu
+        for k, (a, c) in enumerate(zip(out[xu][1], out["k3"][1])):
+            assert np.array_equal(a, c), (xu, k // 3, "xrp"[k % 3])
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
+    check_history(out["k3"][0], want_h)
+    assert np.all(rel_gap(out["k3"][1][-3], want_x) <= 1e-10)
