@@ -24,13 +24,16 @@ for k, m in per.items():
     a[1] += m.get("gpu__time_duration.sum", 0)
     a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
 it = [k for k in agg if k.startswith(("spmv", "update"))]
-tot = sum(agg[k][1] / agg[k][0] for k in it)
+# x-update pairs: the two K3 kernels alternate, one of them per iteration
+half = {"update_p_kernel", "update_p_pair_kernel"} if "update_p_pair_kernel" in agg else set()
+wgt = {k: 0.5 if k in half else 1.0 for k in it}
+tot = sum(wgt[k] * agg[k][1] / agg[k][0] for k in it)
 out = [f"# ncu launch list ({tag}): bench.py --steps 6 --warmup 3 at 256^3, 1 B200, --clock-control none",
        "# kernel, launches, avg us, avg dram bytes/launch, share of the iteration's kernels"]
 for k, (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     ours = k.startswith(("spmv", "update", "stencil", "band", "rhs", "dot", "scan", "combine",
                          "fill", "csr", "ell", "rank_group", "dag", "peer", "waxpby"))
-    sh = (f"share_of_iteration={t / c / tot:.3f}" if k in it else
+    sh = (f"share_of_iteration={wgt[k] * t / c / tot:.3f}" if k in it else
           "setup (once per solve)" if ours else "not this library (torch: bench's read-stream reference)")
     out.append(f"{k:28s} {c:4d} {t / c / 1e3:10.1f} us {b / c / 1e9:8.3f} GB  {sh}")
 open(f"profiles/{tag}_ncu_launches_summary.txt", "w").write("\n".join(out) + "\n")
@@ -46,7 +49,7 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
 NNZ, N = 449455096, 16777216  # 256^3
 
 
-def summarize(rep_path, kernel, algorithmic, out_json, format_bytes=None):
+def summarize(rep_path, kernel, algorithmic, out_json=None, format_bytes=None):
     raw = subprocess.run(["ncu", "-i", rep_path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     r = list(csv.reader(raw.splitlines()))
@@ -59,8 +62,10 @@ def summarize(rep_path, kernel, algorithmic, out_json, format_bytes=None):
          "dram_bytes_per_launch": traffic, "algorithmic_bytes": algorithmic, "metrics": summ}
     if format_bytes:
         d["format_bytes"] = format_bytes  # 16-bit staged columns: 10 B per nonzero
-    json.dump(d, open(out_json, "w"), indent=1)
-    print(json.dumps(d, indent=1))
+    if out_json:
+        json.dump(d, open(out_json, "w"), indent=1)
+        print(json.dumps(d, indent=1))
+    return d
 
 
 # the K1 capture is whichever TMA SpMV the bench ran (-k regex:spmv_tma)
@@ -80,12 +85,28 @@ def _name_of(path):  # demangled kernel name of a one-kernel capture
 
 
 # from 4M rows the x update runs in K3 (update_xr_kernel<false> streams
-# r, Ap -> r: 24 n; update_p_kernel<false, true> r, p, x -> p, x: 40 n)
+# r, Ap -> r: 24 n; update_p_kernel<false, true> r, p, x -> p, x: 40 n); a
+# one-GPU monolithic solve pairs it (prof_k3p: update_p_pair_kernel, r, p,
+# p_prev, x -> p, x: 48 n; prof_k3 then holds the pair's first K3,
+# update_p_kernel<false, false>, r, p -> p: 24 n)
 _xk3 = "update_xr_kernel<0>" in _name_of(os.path.join(base, "prof_k2.ncu-rep"))
-for name, kern, alg in (("prof_k2.ncu-rep", "update_xr_kernel (K2%s)" % (", r only" if _xk3 else ""),
-                         (24 if _xk3 else 48) * N),
-                        ("prof_k3.ncu-rep", "update_p_kernel<false%s> (K3)" % (", true" if _xk3 else ""),
-                         (40 if _xk3 else 24) * N)):
-    if os.path.exists(os.path.join(base, name)):
-        summarize(os.path.join(base, name), kern, alg,
-                  f"profiles/{name.split('_')[1].split('.')[0]}_traffic.json")
+_k3p = os.path.join(base, "prof_k3p.ncu-rep")
+_pairs = os.path.exists(_k3p) and "update_p_pair" in _name_of(_k3p)
+if os.path.exists(os.path.join(base, "prof_k2.ncu-rep")):
+    summarize(os.path.join(base, "prof_k2.ncu-rep"),
+              "update_xr_kernel (K2%s)" % (", r only" if _xk3 else ""), (24 if _xk3 else 48) * N,
+              "profiles/k2_traffic.json")
+_k3 = os.path.join(base, "prof_k3.ncu-rep")
+if _pairs and os.path.exists(_k3):
+    a = summarize(_k3, "update_p_kernel<false, false> (K3, first of an x pair)", 24 * N)
+    b = summarize(_k3p, "update_p_pair_kernel (K3, second of an x pair)", 48 * N)
+    d = {"kernel": "K3 x-update pair: update_p_kernel<false, false> + update_p_pair_kernel, "
+                   "per launch averaged over the pair",
+         "workload": "256x256x256", "round": tag, "source": a["source"],
+         "dram_bytes_per_launch": (a["dram_bytes_per_launch"] + b["dram_bytes_per_launch"]) / 2,
+         "algorithmic_bytes": 36 * N, "launches": {"first": a, "second": b}}
+    json.dump(d, open("profiles/k3_traffic.json", "w"), indent=1)
+    print(json.dumps(d, indent=1))
+elif os.path.exists(_k3):
+    summarize(_k3, "update_p_kernel<false%s> (K3)" % (", true" if _xk3 else ""),
+              (40 if _xk3 else 24) * N, "profiles/k3_traffic.json")
