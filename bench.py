@@ -435,11 +435,18 @@ def extra_configs(torch, P, N, rt, A, b, stream, peak):
     # ---- K0: gen_stencil_matrix on the device at the headline size (one-time
     # setup: widths, slice-offset scan, the 128-bit fill of values, int32 and
     # x-staged columns), host wall clock around the whole call
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    Ak = P.gen_stencil_matrix(A.info.nx, A.info.ny, A.info.nz, rt=rt)
-    out["k0_gen_stencil_ms"] = (time.perf_counter() - t0) * 1e3
-    del Ak
+    # (best of two; the first call right after the drop-in's device frees
+    # once took 0.39 s against 8-36 ms in scripts/k0_probe.py's situations,
+    # so both are reported: k0_gen_stencil_first_ms)
+    k0 = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Ak = P.gen_stencil_matrix(A.info.nx, A.info.ny, A.info.nz, rt=rt)
+        k0.append((time.perf_counter() - t0) * 1e3)
+        del Ak
+    out["k0_gen_stencil_ms"] = min(k0)
+    out["k0_gen_stencil_first_ms"] = k0[0]
 
     # ---- C2: 128^3 on one GPU, monolithic vs the block-task DAG
     A2 = P.gen_stencil_matrix(128, 128, 128, rt=rt)
