@@ -46,9 +46,16 @@ bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
 // every iteration / pairs / K2: 256^3 857-868 / 846-854 / 887-894 us,
 // 128^3 114.0-114.5 / 113.4-113.8 / 116.9-117.1, 96^3 57.6-57.9 /
 // 56.9-57.1 / 58.1-58.4, 64^3 29.0 / 28.7-28.8 / 28.4-28.6: pairs from
-// 512k rows on such a solver.
+// 512k rows on such a solver.  The block-task DAG on streams / graphs (one
+// rank) pairs them in its p-update tiles the same way: 256^3, 2 / 4 / 16
+// tiles, 873-885 -> 859-872 us (streams), 868-874 -> 859-864 (4 tiles,
+// chunked graphs), 941 -> 922 (16 tiles); 128^3 125.6 -> 123.5 (4 tiles,
+// chunked graphs; 125.2 with x in the x/r tiles).  The persistent
+// dispatcher keeps a single update (its TMA update chunks stream r and p).
 static bool auto_pairs(const tw_cg* cg) {
-    return !cg->dist && cg->opt.variant == TW_CG_MONOLITHIC && cg->n >= (int64_t(1) << 19);
+    if (cg->dist || cg->n < (int64_t(1) << 19)) return false;
+    return cg->opt.variant == TW_CG_MONOLITHIC ||
+           (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch != TW_DISPATCH_PERSISTENT);
 }
 
 static bool decide_x_in_k3(const tw_cg* cg) { // at solver creation
@@ -59,7 +66,8 @@ static bool decide_x_in_k3(const tw_cg* cg) { // at solver creation
 }
 
 static bool decide_x_pairs(const tw_cg* cg) {
-    if (cg->dist || cg->opt.variant != TW_CG_MONOLITHIC || !cg->x_k3) return false;
+    if (cg->dist || !cg->x_k3) return false;
+    if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT) return false;
     if (cg->opt.x_update == TW_XUPD_K3_PAIRS) return true;
     return cg->opt.x_update == TW_XUPD_AUTO && TW_XPAIRS_AUTO && auto_pairs(cg);
 }
@@ -210,7 +218,11 @@ int tile_share(const tw_cg* cg) {
     return std::max(1, std::min(cg->T, cap));
 }
 
-void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
+    if (xph != XPH_SINGLE && (!cg->x_pairs || cg->dist)) contract_error("paired x update not enabled");
+    // the iteration's p_old: in the pair buffer for the second of a pair
+    double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
+    double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
     const int share = tile_share(cg);
     EllView A = cg->view();
     A.tma_blocks = (A.tma_blocks + share - 1) / share;
@@ -223,10 +235,10 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
         break;
     case PK_SPMV: { // the x-staged K1 when the matrix has it
         const Fin f = cg->tile_fin(cg->pa, t, FIN_ALPHA, cg->tile_tickets);
-        if (!launch_spmv_staged(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]},
-                                cg->slot(t), f, st))
-            launch_spmv(A, cg->p_local, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0},
-                        true, cg->slot(t), f, bs, st);
+        if (!launch_spmv_staged(A, pl, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, cg->slot(t), f,
+                                st))
+            launch_spmv(A, pl, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0}, true,
+                        cg->slot(t), f, bs, st);
         break;
     }
     case PK_ALPHA: // folded into the last SpMV tile (an empty join node) on one rank
@@ -240,7 +252,7 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
         }
         break;
     case PK_UPD: // x += alpha p moves into the p update from 4M rows (x_in_k3)
-        launch_update_xr(cg->t_r0[t], cg->t_r1[t], x_in_k3(cg) ? nullptr : cg->x, cg->p_owned,
+        launch_update_xr(cg->t_r0[t], cg->t_r1[t], x_in_k3(cg) ? nullptr : cg->x, po,
                          cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, cg->slot(t),
                          cg->tile_fin(cg->rrp, t, FIN_BETA, cg->tile_tickets + 1), bv, st);
@@ -255,10 +267,18 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st) {
             launch_combine(cg->recv_b, cg->P, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, st);
         }
         break;
-    case PK_UPDP:
-        launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0},
-                        cg->slot(t), cg->history, bv, st, nullptr, nullptr, false,
-                        x_in_k3(cg) ? cg->x : nullptr);
+    case PK_UPDP: // paired x updates: as in enqueue_mono, per tile
+        if (xph == XPH_DEFER)
+            launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p2_owned, cg->sc,
+                            ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
+                            cg->p_owned, false, nullptr);
+        else if (xph == XPH_PAIR)
+            launch_update_p_pair(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
+                                 cg->p2_owned, cg->p_owned, cg->x, bv, st);
+        else
+            launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
+                            ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
+                            nullptr, false, x_in_k3(cg) ? cg->x : nullptr);
         break;
     }
 }
@@ -283,7 +303,7 @@ void join_streams(tw_cg* cg) {
 
 // One block-task iteration: physical nodes in topological order, each on its
 // stream after waiting for predecessors on other streams.
-void enqueue_tasks(tw_cg* cg, int parity, bool first) {
+void enqueue_tasks(tw_cg* cg, int parity, bool first, int xph) {
     for (size_t j = 0; j < cg->nodes.size(); ++j) {
         const PNode& nd = cg->nodes[j];
         cudaStream_t st = cg->node_stream(nd);
@@ -294,16 +314,16 @@ void enqueue_tasks(tw_cg* cg, int parity, bool first) {
             for (int p : nd.preds_cross)
                 if (cg->node_stream(cg->nodes[static_cast<size_t>(p)]) != st)
                     TW_CUDA(cudaStreamWaitEvent(st, cg->ev[parity ^ 1][static_cast<size_t>(p)], 0));
-        launch_node(cg, nd, st);
+        launch_node(cg, nd, st, xph);
         TW_CUDA(cudaEventRecord(cg->ev[parity][j], st));
     }
 }
 
-void enqueue_iteration_body(tw_cg* cg, int parity, bool first) {
+void enqueue_iteration_body(tw_cg* cg, int parity, bool first, int xph) {
     if (cg->opt.variant == TW_CG_MONOLITHIC)
-        enqueue_mono(cg);
+        enqueue_mono(cg, xph);
     else
-        enqueue_tasks(cg, parity, first);
+        enqueue_tasks(cg, parity, first, xph);
 }
 
 void build_graph(tw_cg* cg) {
@@ -336,7 +356,7 @@ cudaGraphExec_t build_chunk_graph(tw_cg* cg, int c) {
     try {
         if (cg->opt.variant == TW_CG_TASKS) {
             fork_streams(cg);
-            for (int i = 0; i < c; ++i) enqueue_tasks(cg, i & 1, i == 0);
+            for (int i = 0; i < c; ++i) enqueue_tasks(cg, i & 1, i == 0, x_phase(cg, i, c));
             join_streams(cg);
         } else {
             for (int i = 0; i < c; ++i) enqueue_mono(cg, x_phase(cg, i, c));
@@ -957,7 +977,7 @@ void iterate(tw_cg* cg, int k) {
         } else if (!tasks) {
             enqueue_mono(cg, x_phase(cg, i, k));
         } else {
-            enqueue_iteration_body(cg, it & 1, i == 0);
+            enqueue_iteration_body(cg, it & 1, i == 0, x_phase(cg, i, k));
         }
         if (cg->opt.iteration_marks) {
             // cg_iter=i mark (cg.cpp:307-308): the poller stamps the host time

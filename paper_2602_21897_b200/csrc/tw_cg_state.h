@@ -70,7 +70,7 @@ struct tw_cg {
     std::map<int, cudaGraphExec_t> timed_graphs; // K iterations + per-kernel timing events
     std::map<int, cudaGraphExec_t> chunk_graphs; // up to kGraphChunk iterations, untimed
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
-    bool x_pairs = false; // ... once per pair of iterations (monolithic, one rank)
+    bool x_pairs = false; // ... once per pair of iterations (one rank; monolithic, tasks on streams)
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;
@@ -162,11 +162,11 @@ enum { XPH_SINGLE = 0, XPH_DEFER = 1, XPH_PAIR = 2 };
 int x_phase(const tw_cg* cg, int i, int k);
 void enqueue_mono(tw_cg* cg, int xph = XPH_SINGLE);
 int tile_share(const tw_cg* cg);
-void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st);
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph = XPH_SINGLE);
 void fork_streams(tw_cg* cg);
 void join_streams(tw_cg* cg);
-void enqueue_tasks(tw_cg* cg, int parity, bool first);
-void enqueue_iteration_body(tw_cg* cg, int parity, bool first);
+void enqueue_tasks(tw_cg* cg, int parity, bool first, int xph = XPH_SINGLE);
+void enqueue_iteration_body(tw_cg* cg, int parity, bool first, int xph = XPH_SINGLE);
 void build_graph(tw_cg* cg);
 constexpr int kGraphChunk = 16;
 cudaGraphExec_t build_chunk_graph(tw_cg* cg, int c);

@@ -184,6 +184,7 @@ __device__ __forceinline__ void finalize(const Fin& fin, double total) {
         CgScalars* sc = fin.sc;
         if (fin.then == FIN_ALPHA) {
             sc->pAp = s;
+            sc->alpha_prev = sc->alpha;
             sc->alpha = __ddiv_rn(sc->rtrans, s);
         } else {
             sc->rr = s;

@@ -1177,7 +1177,9 @@ def test_dispatcher_x_update_on_tiny_stages(rt, orc, dims, T):
         assert np.all(rel_gap(res.x, want_x) <= 1e-10), xu
 
 
-@pytest.mark.parametrize("how", ["streams", "graph_chunks", "graph_marks", "timed_graph"])
+@pytest.mark.parametrize("how", ["streams", "graph_chunks", "graph_marks", "timed_graph",
+                                 "tasks_streams", "tasks_graph_chunks", "tasks_graph_marks",
+                                 "tasks_fold_chunks"])
 def test_x_update_pairs_bit_identical(rt, orc, how):
     """Paired x updates (CgOptions.x_update="k3_pairs", the default of a
     one-rank monolithic solve from 4M rows): the first K3 of each pair of
@@ -1186,7 +1188,9 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
     updates in the same order.  Histories, x, r and p (at every call
     boundary: an odd call's last iteration is a single update) must be
     bit-identical to the x update in every K3, for calls of odd and even
-    lengths on every monolithic executor."""
+    lengths on every monolithic executor and on the block-task DAG's streams
+    and graphs (one rank: the p-update tiles alternate the buffers, the
+    iteration's global reductions order the buffer reuse)."""
     from paper_2602_21897_b200 import _native as N
     dims = (64, 40, 36)
     n = int(np.prod(dims))
@@ -1197,14 +1201,21 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
     kw = dict(streams=dict(use_graph=False),
               graph_chunks=dict(use_graph=True, iteration_marks=False),
               graph_marks=dict(use_graph=True, iteration_marks=True),
-              timed_graph=dict(use_graph=True, iteration_marks=False))[how]
+              timed_graph=dict(use_graph=True, iteration_marks=False),
+              tasks_streams=dict(tiles=5, use_graph=False),
+              tasks_graph_chunks=dict(tiles=7, use_graph=True, iteration_marks=False),
+              tasks_graph_marks=dict(tiles=6, use_graph=True, iteration_marks=True),
+              tasks_fold_chunks=dict(tiles=3, use_graph=True, iteration_marks=False))[how]
+    variant = N.TW_CG_TASKS if how.startswith("tasks") else N.TW_CG_MONOLITHIC
     out = {}
     for xu in ("k3", "k3_pairs", None):
-        S = P.CgSolver(rt, A, total, P.CgOptions(x_update=xu, **kw), variant=N.TW_CG_MONOLITHIC)
+        S = P.CgSolver(rt, A, total, P.CgOptions(x_update=xu, **kw), variant=variant)
         want_mode = {"k3": 1, "k3_pairs": 2, None: 0}[xu]  # auto below 4M rows: K2
         assert S.mode()["x_in_k3"] == want_mode
         if how == "timed_graph":
             S.enable_kernel_timing(True)
+        if variant == N.TW_CG_TASKS:
+            assert S.mode()["dispatch"] == N.TW_DISPATCH_STREAMS
         S.set_rhs(b)
         snaps = []
         for c in calls:
