@@ -247,13 +247,13 @@ typedef struct tw_cg_options {
 } tw_cg_options;
 
 #define TW_XUPD_AUTO 0   /* K3 from 4M rows per rank (8n bytes less per iteration), else K2;
-                          * one rank, monolithic or tasks on streams / graphs: K3 pairs from
-                          * 512k rows                                                        */
+                          * one rank: K3 pairs from 512k rows (monolithic, tasks on streams /
+                          * graphs) or 4M rows (the persistent dispatcher)                   */
 #define TW_XUPD_K2 1     /* in K2 with r -= alpha Ap                                        */
 #define TW_XUPD_K3 2     /* in K3, reading p before it is overwritten                       */
 #define TW_XUPD_K3_PAIRS 3 /* in K3 once per pair of iterations, x = (x + a_k p_k) + a_k+1 p_k+1
-                            * (one rank, monolithic or tasks on streams / graphs, else as _K3;
-                            * 4n bytes less per iteration than _K3)                           */
+                            * (one rank, any executor, else as _K3; 4n bytes less per
+                            * iteration than _K3)                                              */
 #define TW_L2KEEP_AUTO 0 /* evict_last on the staged x runs while x has <= 8M entries       */
 #define TW_L2KEEP_ON 1
 #define TW_L2KEEP_OFF 2

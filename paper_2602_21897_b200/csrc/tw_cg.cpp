@@ -51,11 +51,15 @@ bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
 // tiles, 873-885 -> 859-872 us (streams), 868-874 -> 859-864 (4 tiles,
 // chunked graphs), 941 -> 922 (16 tiles); 128^3 125.6 -> 123.5 (4 tiles,
 // chunked graphs; 125.2 with x in the x/r tiles).  The persistent
-// dispatcher keeps a single update (its TMA update chunks stream r and p).
+// dispatcher pairs them where it moves x into the p updates, from 4M rows
+// (256^3, 8 / 16 / 64 tiles: 888-892 -> 876-881 us; at 128^3 the x update in
+// the x/r chunks stays best: 133 against 136 us either way).
+static bool dag_pairs_fit(const tw_cg* cg);
 static bool auto_pairs(const tw_cg* cg) {
     if (cg->dist || cg->n < (int64_t(1) << 19)) return false;
-    return cg->opt.variant == TW_CG_MONOLITHIC ||
-           (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch != TW_DISPATCH_PERSISTENT);
+    if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT)
+        return cg->n >= (int64_t(1) << 22) && dag_pairs_fit(cg);
+    return true;
 }
 
 static bool decide_x_in_k3(const tw_cg* cg) { // at solver creation
@@ -65,9 +69,20 @@ static bool decide_x_in_k3(const tw_cg* cg) { // at solver creation
     return cg->n >= (int64_t(1) << 22) || (TW_XPAIRS_AUTO && auto_pairs(cg));
 }
 
+// The persistent dispatcher pairs them in its TMA update chunks, which need
+// stages of >= 128 rows for 3 and 4 operand streams (else its register path
+// runs, with single updates).
+static bool dag_pairs_fit(const tw_cg* cg) {
+    int sb, vb, cb;
+    dag_smem_bytes(static_cast<int>(cg->A->info.max_width), cg->A->cols16 != nullptr, &sb, &vb, &cb);
+    return ((sb / 24) & ~63) >= 128 && ((sb / 32) & ~63) >= 128;
+}
+
 static bool decide_x_pairs(const tw_cg* cg) {
     if (cg->dist || !cg->x_k3) return false;
-    if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT) return false;
+    if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT &&
+        !dag_pairs_fit(cg))
+        return false;
     if (cg->opt.x_update == TW_XUPD_K3_PAIRS) return true;
     return cg->opt.x_update == TW_XUPD_AUTO && TW_XPAIRS_AUTO && auto_pairs(cg);
 }
@@ -730,9 +745,11 @@ void build_dag_table(tw_cg** g, int P, int k) {
                     t.r0 = cg->t_r0[static_cast<size_t>(nd.tile)];
                     t.r1 = cg->t_r1[static_cast<size_t>(nd.tile)];
                     t.nchunks = 1;
+                    const int xph = x_phase(cg, it, k); // paired x updates (one rank)
                     switch (nd.kind) {
                     case PK_SPMV: {
                         t.kind = DK_SPMV;
+                        if (xph == XPH_PAIR) t.flags |= kDagReadP2;
                         const int64_t ns = ((t.r1 + 31) >> 5) - (t.r0 >> 5);
                         t.nchunks = static_cast<int>((ns + spmv_cs - 1) / spmv_cs);
                         if (cg->peer) { // band (local x, inclusive) reaching a ghost plane
@@ -752,6 +769,8 @@ void build_dag_table(tw_cg** g, int P, int k) {
                     case PK_UPDP:
                         t.kind = DK_UPDP;
                         t.nchunks = static_cast<int>((t.r1 - t.r0 + vec_cr - 1) / vec_cr);
+                        if (xph == XPH_DEFER) t.flags |= kDagXDefer;
+                        if (xph == XPH_PAIR) t.flags |= kDagXPair;
                         break;
                     case PK_HALO: // a no-op without neighbours (a 1-rank communicator)
                         if (!cg->peer && (cg->glo || cg->ghi))
@@ -848,6 +867,8 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
         R.A = c->view();
         R.p_local = c->p_local;
         R.p_owned = c->p_owned;
+        R.p2_local = c->p2_local;
+        R.p2_owned = c->p2_owned;
         R.x = c->x;
         R.r = c->r;
         R.Ap = c->Ap;
@@ -896,6 +917,9 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
     const int ru = rows4, rp = D.x_in_updp ? rows3 : rows2;
     D.upd_block_rows = ru >= 128 ? ru : 0;
     D.updp_block_rows = rp >= 128 ? rp : 0;
+    if (cg->x_pairs && (P != 1 || !D.x_in_updp || !D.upd_block_rows))
+        contract_error("paired x updates need the dispatcher's TMA update chunks on one rank");
+    D.x_pairs = cg->x_pairs ? 1 : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place
     launch_dag(D, grid, s);

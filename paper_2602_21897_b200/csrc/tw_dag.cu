@@ -129,6 +129,10 @@ __device__ __noinline__ double gather_partials(const DagRank& R, const DagTask& 
 }
 
 // One chunk on the compute warps; returns this thread's dot partial.
+// XP: the paired-x-update instantiation (buffer choice per task); the
+// other one compiles the single-update chunks without that generality
+// (which cost 3 us per iteration at 128^3 when it was a runtime choice)
+template <bool XP>
 __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T, int j, int warp,
                                             int lane, unsigned char* stage, uint64_t* bar,
                                             int* stage_w, uint32_t& phase, uint64_t pol) {
@@ -145,10 +149,15 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         const int64_t s_lo = s_first + static_cast<int64_t>(j) * P.spmv_chunk_slices;
         int64_t s_hi = s_lo + P.spmv_chunk_slices;
         if (s_hi > s_end) s_hi = s_end;
+        // p of this iteration: the pair buffer in the second of an x pair
+        const bool p2 = XP && (T.flags & kDagReadP2) != 0;
+        const double* pl = p2 ? R.p2_local : R.p_local;
+        const double* po = p2 ? R.p2_owned : R.p_owned;
+        TW_DCHECK(pl != nullptr);
         if (R.A.cols16) { // x-staged matrix: the slice's x runs ride its TMA transaction
             // a tile reading a ghost plane: the neighbour's halo task of this
             // iteration must have landed it (its flag carries the stamp)
-            if (lane == 0 && T.flags) {
+            if (lane == 0 && (T.flags & (kDagGhostLo | kDagGhostHi))) {
                 const unsigned long long st = task_stamp(R, T);
                 if (T.flags & kDagGhostLo) thread_wait_flags(&R.win->flag_ghost_lo, 1, st);
                 if (T.flags & kDagGhostHi) thread_wait_flags(&R.win->flag_ghost_hi, 1, st);
@@ -181,7 +190,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         asm volatile(
                             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
                             " [%0], [%1], %2, [%3];" ::"r"(smem_u32(xs + r * kStageRunLen)),
-                            "l"(R.p_local + st), "r"(kRunBytes), "r"(smem_u32(bar))
+                            "l"(pl + st), "r"(kRunBytes), "r"(smem_u32(bar))
                             : "memory");
                     }
                 }
@@ -227,16 +236,16 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
             const int32_t* cb = reinterpret_cast<const int32_t*>(stage + P.val_bytes);
             double acc;
             switch (w) {
-            case 27: acc = smem_row_fixed<27, kGatherCA>(vb, cb, R.p_local, lane); break;
-            case 18: acc = smem_row_fixed<18, kGatherCA>(vb, cb, R.p_local, lane); break;
-            case 12: acc = smem_row_fixed<12, kGatherCA>(vb, cb, R.p_local, lane); break;
-            case 8: acc = smem_row_fixed<8, kGatherCA>(vb, cb, R.p_local, lane); break;
-            default: acc = smem_row_generic<kGatherCA>(vb, cb, R.p_local, lane, w); break;
+            case 27: acc = smem_row_fixed<27, kGatherCA>(vb, cb, pl, lane); break;
+            case 18: acc = smem_row_fixed<18, kGatherCA>(vb, cb, pl, lane); break;
+            case 12: acc = smem_row_fixed<12, kGatherCA>(vb, cb, pl, lane); break;
+            case 8: acc = smem_row_fixed<8, kGatherCA>(vb, cb, pl, lane); break;
+            default: acc = smem_row_generic<kGatherCA>(vb, cb, pl, lane, w); break;
             }
             const int64_t row = (s << 5) + lane;
             if (row >= T.r0 && row < T.r1) {
                 R.Ap[row] = acc;
-                part = __dadd_rn(part, __dmul_rn(R.p_owned[row], acc));
+                part = __dadd_rn(part, __dmul_rn(po[row], acc));
             }
             __syncwarp();
             if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -261,16 +270,26 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
         break;
 #endif
         const bool upd = T.kind == DK_UPD;
+        // paired x updates (p updates only): defer = p into the pair buffer,
+        // x left alone; pair = x = (x + alpha_prev p0) + alpha p1 with p1 the
+        // pair buffer and p0 = p_owned, p back into p_owned
+        const bool xdef = XP && !upd && (T.flags & kDagXDefer) != 0;
+        const bool xpair = XP && !upd && (T.flags & kDagXPair) != 0;
         // x_in_updp: x += alpha p_old rides on the p update's read of p_old
         // (alpha of this iteration is still in sc: the next alpha task waits
         // for every p update of this one)
-        const bool xin = P.x_in_updp != 0;
+        const bool xin = P.x_in_updp != 0 && !xdef;
         const double alpha = upd || xin ? R.sc->alpha : 0.0, nalpha = -alpha;
+        const double alpha0 = xpair ? R.sc->alpha_prev : 0.0;
         const double beta = upd ? 0.0 : R.sc->beta;
+        const double* pin = xpair ? R.p2_owned : R.p_owned;  // this iteration's p_old
+        double* pout = xdef ? R.p2_owned : R.p_owned;       // the new p
         const int64_t a = T.r0 + static_cast<int64_t>(j) * P.vec_chunk_rows;
         int64_t b = a + P.vec_chunk_rows;
         if (b > T.r1) b = T.r1;
-        const int sb = upd ? P.upd_block_rows : P.updp_block_rows;
+        // the pair's four operand streams take the x/r chunks' block size
+        const int sb = upd || xpair ? P.upd_block_rows : P.updp_block_rows;
+        TW_DCHECK(!(xdef || xpair) || (sb > 0 && P.x_in_updp));
         if (sb > 0) {
             // TMA path: each warp streams blocks of sb rows of its operands
             // (x, p, r, Ap or r, p) into its stage with bulk copies -- a whole
@@ -288,8 +307,13 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 const int rows = static_cast<int>((q + sb < b2 ? q + sb : b2) - q);
                 const uint32_t bytes = static_cast<uint32_t>(rows) * 8u;
                 if (lane == 0) {
-                    mbar_expect_tx(bar, (upd ? (xin ? 2u : 4u) : (xin ? 3u : 2u)) * bytes);
-                    if (upd && xin) { // r, Ap
+                    mbar_expect_tx(bar, (upd ? (xin ? 2u : 4u) : xpair ? 4u : (xin ? 3u : 2u)) * bytes);
+                    if (xpair) { // r, p1, p0, x
+                        bulk_g2s_plain(s0, R.r + q, bytes, bar);
+                        bulk_g2s_plain(s1, pin + q, bytes, bar);
+                        bulk_g2s_plain(s2, R.p_owned + q, bytes, bar);
+                        bulk_g2s_plain(s3, R.x + q, bytes, bar);
+                    } else if (upd && xin) { // r, Ap
                         bulk_g2s_plain(s0, R.r + q, bytes, bar);
                         bulk_g2s_plain(s1, R.Ap + q, bytes, bar);
                     } else if (upd) {
@@ -299,7 +323,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         bulk_g2s_plain(s3, R.Ap + q, bytes, bar);
                     } else { // r, p (and x)
                         bulk_g2s_plain(s0, R.r + q, bytes, bar);
-                        bulk_g2s_plain(s1, R.p_owned + q, bytes, bar);
+                        bulk_g2s_plain(s1, pin + q, bytes, bar);
                         if (xin) bulk_g2s_plain(s2, R.x + q, bytes, bar);
                     }
                 }
@@ -307,7 +331,18 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 mbar_wait(bar, phase & 1u);
                 ++phase;
                 for (int i = 2 * lane; i < rows; i += 64) {
-                    if (upd && xin) {
+                    if (xpair) {
+                        const double2 rv = *reinterpret_cast<const double2*>(s0 + i);
+                        double2 pv = *reinterpret_cast<const double2*>(s1 + i);
+                        const double2 ov = *reinterpret_cast<const double2*>(s2 + i);
+                        double2 xv = *reinterpret_cast<const double2*>(s3 + i);
+                        xv.x = __dadd_rn(__dadd_rn(xv.x, __dmul_rn(alpha0, ov.x)), __dmul_rn(alpha, pv.x));
+                        xv.y = __dadd_rn(__dadd_rn(xv.y, __dmul_rn(alpha0, ov.y)), __dmul_rn(alpha, pv.y));
+                        *reinterpret_cast<double2*>(R.x + q + i) = xv;
+                        pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
+                        pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
+                        *reinterpret_cast<double2*>(pout + q + i) = pv;
+                    } else if (upd && xin) {
                         double2 rv = *reinterpret_cast<const double2*>(s0 + i);
                         const double2 av = *reinterpret_cast<const double2*>(s1 + i);
                         rv.x = __dadd_rn(rv.x, __dmul_rn(nalpha, av.x));
@@ -339,7 +374,7 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                         }
                         pv.x = __dadd_rn(rv.x, __dmul_rn(beta, pv.x));
                         pv.y = __dadd_rn(rv.y, __dmul_rn(beta, pv.y));
-                        *reinterpret_cast<double2*>(R.p_owned + q + i) = pv;
+                        *reinterpret_cast<double2*>(pout + q + i) = pv;
                     }
                 }
                 __syncwarp();
@@ -412,8 +447,10 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
                 R.r[i] = rv;
                 part = __dadd_rn(part, __dmul_rn(rv, rv));
             } else {
-                if (xin) R.x[i] = __dadd_rn(R.x[i], __dmul_rn(alpha, R.p_owned[i]));
-                R.p_owned[i] = __dadd_rn(R.r[i], __dmul_rn(beta, R.p_owned[i]));
+                const double pv = pin[i];
+                if (xpair) R.x[i] = __dadd_rn(R.x[i], __dmul_rn(alpha0, R.p_owned[i]));
+                if (xin) R.x[i] = __dadd_rn(R.x[i], __dmul_rn(alpha, pv));
+                pout[i] = __dadd_rn(R.r[i], __dmul_rn(beta, pv));
             }
         }
         break;
@@ -440,6 +477,7 @@ __device__ __forceinline__ void complete_chunk(const DagParams& P, const Slot& S
                 for (int t = 0; t < P.T; ++t) pAp = __dadd_rn(pAp, R.pa[t]);
             }
             R.sc->pAp = pAp;
+            R.sc->alpha_prev = R.sc->alpha; // paired x updates
             R.sc->alpha = __ddiv_rn(R.sc->rtrans, pAp);
         } else if (T.kind == DK_BETA) { // beta_res task (cg.cpp:299-309)
             double rr = 0.0;
@@ -534,6 +572,7 @@ __device__ __forceinline__ void fill_slot(const DagParams& P, Slot* S, int lane)
 // dependency acquire) while the compute warps run slot b, and completes slot
 // b (partials, counters, successor release) while they run slot b+1, so the
 // per-chunk bookkeeping is off the critical path and chunks can be small.
+template <bool XP>
 __global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(const __grid_constant__ DagParams P) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kComputeWarps];
@@ -595,7 +634,7 @@ __global__ void __launch_bounds__(kDagWarps * 32, TW_DAG_CTAS) dag_kernel(const 
             bar_sync(5, kComputeWarps * 32);
         }
         const DagTask T = slots[b].t;
-        const double part = run_chunk(P, T, c - T.chunk0, warp, lane, stage, &bars[warp],
+        const double part = run_chunk<XP>(P, T, c - T.chunk0, warp, lane, stage, &bars[warp],
                                       &stage_w[warp], phase, pol);
         const double ws = warp_sum(part);
         if (lane == 0) wpart[b][warp] = ws;
@@ -625,9 +664,13 @@ int dag_compute_warps() { return kComputeWarps; }
 int dag_blocks(int max_width, bool staged, int sm_count) {
     int stage, vb, cb;
     const int smem = dag_smem_bytes(max_width, staged, &stage, &vb, &cb);
-    TW_CUDA(cudaFuncSetAttribute(dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    TW_CUDA(cudaFuncSetAttribute(dag_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    TW_CUDA(cudaFuncSetAttribute(dag_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel, kDagWarps * 32, smem));
+    int per_sm_xp = 0; // both instantiations must fit the same grid
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dag_kernel<false>, kDagWarps * 32, smem));
+    TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_xp, dag_kernel<true>, kDagWarps * 32, smem));
+    per_sm = std::min(per_sm, per_sm_xp);
     if (per_sm < 1) config_error("dispatcher CTA does not fit on an SM");
     return per_sm * sm_count;
 }
@@ -635,7 +678,10 @@ int dag_blocks(int max_width, bool staged, int sm_count) {
 void launch_dag(const DagParams& P, int blocks, cudaStream_t s) {
     int stage, vb, cb;
     const int smem = dag_smem_bytes(P.max_width, P.rk[0].A.cols16 != nullptr, &stage, &vb, &cb);
-    dag_kernel<<<blocks, kDagWarps * 32, smem, s>>>(P);
+    if (P.x_pairs)
+        dag_kernel<true><<<blocks, kDagWarps * 32, smem, s>>>(P);
+    else
+        dag_kernel<false><<<blocks, kDagWarps * 32, smem, s>>>(P);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -382,6 +382,10 @@ enum DagKind : int { DK_SPMV = 0, DK_ALPHA = 1, DK_UPD = 2, DK_BETA = 3, DK_UPDP
 // DagTask::flags: an SpMV tile whose band reads a ghost plane waits for that
 // plane's flag (the neighbour's halo task of the same iteration) first.
 constexpr int kDagGhostLo = 1, kDagGhostHi = 2;
+// paired x updates (one rank): the SpMV of a pair's second iteration reads
+// p from the pair buffer; the pair's first p update writes it there and
+// leaves x, the second applies both x updates and writes p back
+constexpr int kDagReadP2 = 4, kDagXDefer = 8, kDagXPair = 16;
 
 // One physical task of the flattened K-iteration DAG (tw_dag.cu).
 struct DagTask {
@@ -389,7 +393,7 @@ struct DagTask {
     int tile;
     int rank;         // index into DagParams::rk (0 on one rank)
     int iter;         // iteration within the launch (stamps of the peer flags)
-    int flags;        // kDagGhost*
+    int flags;        // kDagGhost*, kDagReadP2, kDagXDefer, kDagXPair
     int64_t r0, r1;   // local rows of the tile
     int chunk0;       // first index in the global chunk list
     int nchunks;
@@ -407,6 +411,8 @@ struct DagRank {
     EllView A;
     const double* p_local;   // gathered (owned + ghost planes)
     double* p_owned;
+    const double* p2_local;  // the pair buffer (paired x updates), else null
+    double* p2_owned;
     double* x;
     double* r;
     double* Ap;
@@ -443,6 +449,7 @@ struct DagParams {
     // warp's stage); 0 = register path
     int upd_block_rows, updp_block_rows;
     int x_in_updp; // x += alpha p_old in the p-update chunks (TMA path only)
+    int x_pairs;   // paired x updates (the dag_kernel<true> instantiation)
     DagRank rk[kDagMaxRanks];
 };
 

@@ -25,15 +25,20 @@ for k, m in per.items():
     a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
 it = [k for k in agg if k.startswith(("spmv", "update"))]
 # x-update pairs: the two K3 kernels alternate, one of them per iteration
-half = {"update_p_kernel", "update_p_pair_kernel"} if "update_p_pair_kernel" in agg else set()
-wgt = {k: 0.5 if k in half else 1.0 for k in it}
+# x-update pairs: the pair's two K3 kernels alternate, one of them per
+# iteration; the single-update K3 then only ends a call of odd length
+pairs = "update_p_pair_kernel" in agg
+half = {"update_p_kernel<0, 0>", "update_p_pair_kernel"} if pairs else set()
+wgt = {k: 0.5 if k in half else 0.0 if pairs and k == "update_p_kernel<0, 1>" else 1.0
+       for k in it}
 tot = sum(wgt[k] * agg[k][1] / agg[k][0] for k in it)
 out = [f"# ncu launch list ({tag}): bench.py --steps 6 --warmup 3 at 256^3, 1 B200, --clock-control none",
        "# kernel, launches, avg us, avg dram bytes/launch, share of the iteration's kernels"]
 for k, (c, t, b) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     ours = k.startswith(("spmv", "update", "stencil", "band", "rhs", "dot", "scan", "combine",
                          "fill", "csr", "ell", "rank_group", "dag", "peer", "waxpby"))
-    sh = (f"share_of_iteration={wgt[k] * t / c / tot:.3f}" if k in it else
+    sh = ("odd-length call's last K3 (single x update)" if k in it and wgt[k] == 0 else
+          f"share_of_iteration={wgt[k] * t / c / tot:.3f}" if k in it else
           "setup (once per solve)" if ours else "not this library (torch: bench's read-stream reference)")
     out.append(f"{k:28s} {c:4d} {t / c / 1e3:10.1f} us {b / c / 1e9:8.3f} GB  {sh}")
 open(f"profiles/{tag}_ncu_launches_summary.txt", "w").write("\n".join(out) + "\n")

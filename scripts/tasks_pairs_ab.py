@@ -35,7 +35,11 @@ ROWS = (("mono graphK", 0, dict(tiles=1, use_graph=True, iteration_marks=False))
         ("T2 streams", 1, dict(tiles=2, iteration_marks=False)),
         ("T4 streams", 1, dict(tiles=4, iteration_marks=False)),
         ("T4 graphK", 1, dict(tiles=4, use_graph=True, iteration_marks=False)),
-        ("T16 graphK", 1, dict(tiles=16, use_graph=True, iteration_marks=False)))
+        ("T16 graphK", 1, dict(tiles=16, use_graph=True, iteration_marks=False)),
+        ("T8 persistent", 1, dict(tiles=8, persistent=True, iteration_marks=False)),
+        ("T16 persistent", 1, dict(tiles=16, persistent=True, iteration_marks=False)),
+        ("T64 persistent", 1, dict(tiles=64, persistent=True, iteration_marks=False)))
+ROWS = tuple(r for r in ROWS if os.environ.get("ONLY", "") in r[0])
 for nx, K in ((256, 60), (128, 400)):
     A = P.gen_stencil_matrix(nx, nx, nx, rt=rt)
     b = P.rhs_xorshift(rt, A.n, 7)

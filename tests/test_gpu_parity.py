@@ -1179,7 +1179,7 @@ def test_dispatcher_x_update_on_tiny_stages(rt, orc, dims, T):
 
 @pytest.mark.parametrize("how", ["streams", "graph_chunks", "graph_marks", "timed_graph",
                                  "tasks_streams", "tasks_graph_chunks", "tasks_graph_marks",
-                                 "tasks_fold_chunks"])
+                                 "tasks_fold_chunks", "tasks_persistent", "tasks_persistent_marks"])
 def test_x_update_pairs_bit_identical(rt, orc, how):
     """Paired x updates (CgOptions.x_update="k3_pairs", the default of a
     one-rank monolithic solve from 4M rows): the first K3 of each pair of
@@ -1189,8 +1189,9 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
     boundary: an odd call's last iteration is a single update) must be
     bit-identical to the x update in every K3, for calls of odd and even
     lengths on every monolithic executor and on the block-task DAG's streams
-    and graphs (one rank: the p-update tiles alternate the buffers, the
-    iteration's global reductions order the buffer reuse)."""
+    and graphs and in the persistent dispatcher (one rank: the p-update
+    tiles / chunks alternate the buffers, the iteration's global reductions
+    order the buffer reuse)."""
     from paper_2602_21897_b200 import _native as N
     dims = (64, 40, 36)
     n = int(np.prod(dims))
@@ -1205,7 +1206,9 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
               tasks_streams=dict(tiles=5, use_graph=False),
               tasks_graph_chunks=dict(tiles=7, use_graph=True, iteration_marks=False),
               tasks_graph_marks=dict(tiles=6, use_graph=True, iteration_marks=True),
-              tasks_fold_chunks=dict(tiles=3, use_graph=True, iteration_marks=False))[how]
+              tasks_fold_chunks=dict(tiles=3, use_graph=True, iteration_marks=False),
+              tasks_persistent=dict(tiles=16, persistent=True, iteration_marks=False),
+              tasks_persistent_marks=dict(tiles=5, persistent=True, iteration_marks=True))[how]
     variant = N.TW_CG_TASKS if how.startswith("tasks") else N.TW_CG_MONOLITHIC
     out = {}
     for xu in ("k3", "k3_pairs", None):
@@ -1215,7 +1218,8 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
         if how == "timed_graph":
             S.enable_kernel_timing(True)
         if variant == N.TW_CG_TASKS:
-            assert S.mode()["dispatch"] == N.TW_DISPATCH_STREAMS
+            assert S.mode()["dispatch"] == (N.TW_DISPATCH_PERSISTENT if "persistent" in how
+                                            else N.TW_DISPATCH_STREAMS)
         S.set_rhs(b)
         snaps = []
         for c in calls:
