@@ -644,7 +644,7 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
                                          const double* __restrict__ r,
                                          const double* __restrict__ psrc, double* __restrict__ p,
                                          double beta, double* __restrict__ x, double alpha,
-                                         const double* __restrict__ p0 = nullptr,
+                                         const double* p0 = nullptr, // may alias p (pair: p_k+2 over p_k)
                                          double alpha0 = 0.0) {
     constexpr bool WX = XU != 0;
     const int64_t a = (a0 + 1) & ~int64_t(1), b = b0 & ~int64_t(1);
