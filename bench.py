@@ -159,17 +159,20 @@ class ClockSampler:
             self.max_mhz = None
         self._stop = threading.Event()
 
-    def _run(self):
+    def _sample(self):
         nv = self.nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if mask & bit and bit != 0x1:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            self._sample()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -180,6 +183,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.ok:
+            self._sample()  # at least one sample at the end of the region, whatever the thread got
             self._stop.set()
             self.t.join()
 
@@ -631,6 +635,7 @@ def run_ours(args, dist, rank, world, local):
         e0.record(stream)
         S.iterate(kr)
         e1.record(stream)
+        rt.synchronize()  # the long wait in a ctypes call (GIL released: the clock sampler runs)
         torch.cuda.synchronize()
         barrier(dist)
         kt = S.kernel_times() if timing else None
