@@ -55,8 +55,15 @@ bool x_in_k3(const tw_cg* cg) { return cg->x_k3; }
 // (256^3, 8 / 16 / 64 tiles: 888-892 -> 876-881 us; at 128^3 the x update in
 // the x/r chunks stays best: 133 against 136 us either way).
 static bool dag_pairs_fit(const tw_cg* cg);
+// Across ranks (monolithic: the halo then alternates buffers too) every
+// rank must make the same choice, so it rests on the global rows per rank.
 static bool auto_pairs(const tw_cg* cg) {
-    if (cg->dist || cg->n < (int64_t(1) << 19)) return false;
+    if (cg->dist) {
+        const tw_ell_info_t& in = cg->A->info;
+        return cg->opt.variant == TW_CG_MONOLITHIC &&
+               in.n_global / std::max(cg->P, 1) >= (int64_t(1) << 19);
+    }
+    if (cg->n < (int64_t(1) << 19)) return false;
     if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT)
         return cg->n >= (int64_t(1) << 22) && dag_pairs_fit(cg);
     return true;
@@ -79,7 +86,8 @@ static bool dag_pairs_fit(const tw_cg* cg) {
 }
 
 static bool decide_x_pairs(const tw_cg* cg) {
-    if (cg->dist || !cg->x_k3) return false;
+    if (!cg->x_k3) return false;
+    if (cg->dist && cg->opt.variant != TW_CG_MONOLITHIC) return false; // tasks across ranks: single
     if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT &&
         !dag_pairs_fit(cg))
         return false;
@@ -162,8 +170,8 @@ void enqueue_mono(tw_cg* cg, int xph) {
     const EllView A = cg->view();
     const int bs = launch_blocks(cg, true), bv = launch_blocks(cg, false);
     const RedScratch rs = cg->slot(0);
+    if (xph != XPH_SINGLE && !cg->x_pairs) contract_error("paired x update not enabled");
     if (!cg->dist) {
-        if (xph != XPH_SINGLE && !cg->x_pairs) contract_error("paired x update not enabled");
         // p_k of this iteration: in the pair buffer for the second of a pair
         double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
         double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
@@ -181,8 +189,8 @@ void enqueue_mono(tw_cg* cg, int xph) {
             launch_update_p(0, cg->n, cg->r, cg->p2_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
                             cg->history, bv, s, nullptr, cg->p_owned, false, nullptr);
         else if (xph == XPH_PAIR) // x gets a_k-1 p_k-1 + a_k p_k; p_k+1 back into p_owned
-            launch_update_p_pair(0, cg->n, cg->r, cg->p_owned, cg->sc, cg->p2_owned, cg->p_owned,
-                                 cg->x, bv, s);
+            launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
+                            cg->history, bv, s, nullptr, cg->p2_owned, false, cg->x, cg->p_owned);
         else
             launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
                             cg->history, bv, s, nullptr, nullptr, false, xk3 ? cg->x : nullptr);
@@ -192,30 +200,33 @@ void enqueue_mono(tw_cg* cg, int xph) {
     }
     if (cg->peer) {
         record(tmark(cg, 0), s);
-        peer_spmv(cg, s);
+        peer_spmv(cg, s, xph);
         record(tmark(cg, 1), s);
         peer_update_xr(cg, s);
         record(tmark(cg, 2), s);
-        peer_update_p(cg, s);
+        peer_update_p(cg, s, xph);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
     }
+    // p of this iteration: the pair buffer in the second of an x pair (its
+    // halo is exchanged, its ghost planes read)
+    double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
     cudaStream_t c = cg->ctx->comm;
     TW_CUDA(cudaEventRecord(cg->pready_ev, s));
     TW_CUDA(cudaStreamWaitEvent(c, cg->pready_ev, 0));
-    halo_exchange(cg, c);
+    halo_exchange(cg, c, pl);
     TW_CUDA(cudaEventRecord(cg->halo_ev, c));
     record(tmark(cg, 0), s);
-    dist_spmv_interior(cg, s);
+    dist_spmv_interior(cg, s, pl);
     TW_CUDA(cudaStreamWaitEvent(s, cg->halo_ev, 0));
-    dist_spmv_boundary(cg, s);
+    dist_spmv_boundary(cg, s, pl);
     allgather1(cg, cg->send_a, cg->recv_a, s);
     record(tmark(cg, 1), s);
     dist_update_xr(cg, s);
     allgather1(cg, cg->send_b, cg->recv_b, s);
     record(tmark(cg, 2), s);
-    dist_update_p(cg, s);
+    dist_update_p(cg, s, xph);
     record(tmark(cg, 3), s);
     if (cg->timing) ++cg->timed;
 }
@@ -288,8 +299,9 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
                             ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
                             cg->p_owned, false, nullptr);
         else if (xph == XPH_PAIR)
-            launch_update_p_pair(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
-                                 cg->p2_owned, cg->p_owned, cg->x, bv, st);
+            launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
+                            ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
+                            cg->p2_owned, false, cg->x, cg->p_owned);
         else
             launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
                             ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
@@ -409,8 +421,7 @@ void free_cg(tw_cg* cg) {
     if (cg->ag_out_ev) cudaEventDestroy(cg->ag_out_ev);
     cudaFree(cg->x);
     cudaFree(cg->r_base);
-    cudaFree(cg->p_base);
-    cudaFree(cg->p2_base);
+    cudaFree(cg->p_base); // (the pair buffer included)
     cudaFree(cg->Ap);
     cudaFree(cg->sc);
     cudaFree(cg->history);
@@ -421,6 +432,7 @@ void free_cg(tw_cg* cg) {
     for (void* m : cg->ipc_mapped) cudaIpcCloseMemHandle(m);
     cudaFree(cg->win);
     cudaFree(cg->d_links);
+    cudaFree(cg->d_links2);
     for (auto& kv : cg->dag_tables) {
         auto& t = kv.second;
         cudaFree(t.d_tasks);
@@ -527,16 +539,20 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         if (front < 2) front += 16;
         // (and at least kStageRunLen after: a run-table run may start at the
         // last column)
-        TW_CUDA(cudaMalloc(&cg->p_base, sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
-        cg->p_local = cg->p_base + front;
-        cg->p_owned = cg->p_local + cg->diag_shift;
         cg->x_k3 = decide_x_in_k3(cg);
         cg->x_pairs = decide_x_pairs(cg);
-        if (cg->x_pairs) { // the pair buffer: same line offset and slack as p_local
-            TW_CUDA(cudaMalloc(&cg->p2_base,
-                               sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
-            TW_CUDA(cudaMemset(cg->p2_base, 0,
-                               sizeof(double) * (static_cast<size_t>(cg->x_len + front) + 48)));
+        // the pair buffer (paired x updates) sits in the same allocation, one
+        // stride of whole 128-byte lines further: same line offset and slack
+        // as p_local, and one IPC mapping of p_base reaches both (a peer
+        // rank stores its halo planes into either buffer's ghost planes)
+        const int64_t stride = (cg->x_len + front + 48 + 15) / 16 * 16;
+        const size_t pbytes = sizeof(double) * static_cast<size_t>(stride * (cg->x_pairs ? 2 : 1));
+        TW_CUDA(cudaMalloc(&cg->p_base, pbytes));
+        TW_CUDA(cudaMemset(cg->p_base, 0, pbytes));
+        cg->p_local = cg->p_base + front;
+        cg->p_owned = cg->p_local + cg->diag_shift;
+        if (cg->x_pairs) {
+            cg->p2_base = cg->p_base + stride;
             cg->p2_local = cg->p2_base + front;
             cg->p2_owned = cg->p2_local + cg->diag_shift;
         }

@@ -26,12 +26,14 @@ void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s) {
     TW_CUDA(cudaStreamWaitEvent(s, cg->ag_out_ev, 0));
 }
 
-void halo_exchange(tw_cg* cg, cudaStream_t s) {
+// p_local: the buffer the next K1 reads (the pair buffer in the second
+// iteration of an x-update pair), by default p_local
+void halo_exchange(tw_cg* cg, cudaStream_t s, double* p_local) {
     const auto& api = nccl();
     const size_t pl = static_cast<size_t>(cg->plane);
     const int rank = cg->ctx->rank;
     const tw_slab_t& sp = cg->slab;
-    double* p = cg->p_local;
+    double* p = p_local ? p_local : cg->p_local;
     TW_NCCL(api.GroupStart());
     if (sp.ghost_lo) {
         TW_NCCL(api.Recv(p + sp.recv_lo, pl, ncclDouble, rank - 1, cg->ctx->nccl_comm, s));
@@ -50,21 +52,23 @@ void halo_exchange(tw_cg* cg, cudaStream_t s) {
 // loopback copies in place of NCCL.
 // On an x-staged slab both launches are the staged K1 (the peer transport's
 // one-launch form walks the same two index spaces, so the sums agree to the bit).
-void dist_spmv_interior(tw_cg* cg, cudaStream_t s) { // rows that read no ghost plane
+void dist_spmv_interior(tw_cg* cg, cudaStream_t s, const double* p_local) { // rows that read no ghost plane
+    const double* p = p_local ? p_local : cg->p_local;
     const RowRange ri{cg->slab.interior_r0, cg->slab.interior_r1};
-    if (launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, ri, cg->slot(0),
+    if (launch_spmv_staged(cg->view(), p, cg->Ap, ri, cg->slot(0),
                            Fin{FIN_STORE, cg->pm, nullptr, nullptr}, s))
         return;
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
+    launch_spmv(cg->view(), p, cg->Ap, RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
                 RowRange{0, 0}, true, cg->slot(0), Fin{FIN_STORE, cg->pm, nullptr, nullptr},
                 launch_blocks(cg, true), s);
 }
 
-void dist_spmv_boundary(tw_cg* cg, cudaStream_t s) { // the ghost-reading planes, then p.Ap
-    if (!launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+void dist_spmv_boundary(tw_cg* cg, cudaStream_t s, const double* p_local) { // the ghost-reading planes, then p.Ap
+    const double* p = p_local ? p_local : cg->p_local;
+    if (!launch_spmv_staged(cg->view(), p, cg->Ap, RowRange{0, cg->slab.interior_r0},
                             RowRange{cg->slab.interior_r1, cg->n}, RowRange{0, 0}, false,
                             cg->slot(0), Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, s))
-        launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+        launch_spmv(cg->view(), p, cg->Ap, RowRange{0, cg->slab.interior_r0},
                 RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
                     Fin{FIN_STORE, cg->pm + 1, nullptr, nullptr}, launch_blocks(cg, true), s);
     launch_combine(cg->pm, 2, Fin{FIN_STORE, cg->send_a, nullptr, nullptr}, s);
@@ -76,10 +80,18 @@ void dist_update_xr(tw_cg* cg, cudaStream_t s) { // alpha from the rank partials
                      Fin{FIN_STORE, cg->send_b, nullptr, nullptr}, launch_blocks(cg, false), s);
 }
 
-void dist_update_p(tw_cg* cg, cudaStream_t s) { // beta from the rank partials; commit
-    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{cg->recv_b, cg->P}, cg->slot(0),
-                    cg->history, launch_blocks(cg, false), s, nullptr, nullptr, false,
-                    x_in_k3(cg) ? cg->x : nullptr);
+void dist_update_p(tw_cg* cg, cudaStream_t s, int xph) { // beta from the rank partials; commit
+    const ScalarSrc bs{cg->recv_b, cg->P};
+    const int bv = launch_blocks(cg, false);
+    if (xph == XPH_DEFER) // p_k+1 into the pair buffer, x left alone
+        launch_update_p(0, cg->n, cg->r, cg->p2_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, nullptr, cg->p_owned, false, nullptr);
+    else if (xph == XPH_PAIR) // both x updates; p_k+2 back into p_owned
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, nullptr, cg->p2_owned, false, cg->x, cg->p_owned);
+    else
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, nullptr, nullptr, false, x_in_k3(cg) ? cg->x : nullptr);
 }
 
 // Phases of the peer transport (NVLink stores + flags, fused into the
@@ -97,32 +109,35 @@ bool peer_k1_fused(const tw_cg* cg) {
            slices(0, cg->slab.interior_r0) + slices(cg->slab.interior_r1, cg->n) >= full;
 }
 
-void peer_spmv(tw_cg* cg, cudaStream_t s) {
+void peer_spmv(tw_cg* cg, cudaStream_t s, int xph) {
+    // p of this iteration (and its ghost planes): the pair buffer in the
+    // second iteration of an x-update pair
+    const double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
     const int ng = cg->slab.ghost_lo + cg->slab.ghost_hi;
     const unsigned long long* gf = cg->slab.ghost_lo ? &cg->win->flag_ghost_lo : &cg->win->flag_ghost_hi;
     const Fin fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm};
     const RowRange ri{cg->slab.interior_r0, cg->slab.interior_r1}, b0{0, cg->slab.interior_r0},
         b1{cg->slab.interior_r1, cg->n};
     if (cg->view().cols16) { // x-staged slab: the same two forms with staged x runs
-        if (launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, ri, b0, b1, true, cg->slot(0), fin,
+        if (launch_spmv_staged(cg->view(), pl, cg->Ap, ri, b0, b1, true, cg->slot(0), fin,
                                s, ng ? gf : nullptr, ng))
             return;
-        dist_spmv_interior(cg, s);
-        if (!launch_spmv_staged(cg->view(), cg->p_local, cg->Ap, b0, b1, RowRange{0, 0}, false,
+        dist_spmv_interior(cg, s, pl);
+        if (!launch_spmv_staged(cg->view(), pl, cg->Ap, b0, b1, RowRange{0, 0}, false,
                                 cg->slot(0), fin, s, ng ? gf : nullptr, ng))
             throw Error(TW_ERR_CUDA, "staged boundary SpMV did not launch after the interior did");
         return;
     }
     // one launch: interior rows first (they read no ghost plane, so they
     // overlap the neighbours' K3 tails), then the boundary rows
-    if (launch_spmv_split(cg->view(), cg->p_local, cg->Ap,
+    if (launch_spmv_split(cg->view(), pl, cg->Ap,
                           RowRange{cg->slab.interior_r0, cg->slab.interior_r1},
                           RowRange{0, cg->slab.interior_r0}, RowRange{cg->slab.interior_r1, cg->n},
                           cg->slot(0), Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
                           s, ng ? gf : nullptr, ng))
         return;
-    dist_spmv_interior(cg, s);
-    launch_spmv(cg->view(), cg->p_local, cg->Ap, RowRange{0, cg->slab.interior_r0},
+    dist_spmv_interior(cg, s, pl);
+    launch_spmv(cg->view(), pl, cg->Ap, RowRange{0, cg->slab.interior_r0},
                 RowRange{cg->slab.interior_r1, cg->n}, true, cg->slot(0),
                 Fin{FIN_PUBLISH_A, cg->pm + 1, cg->sc, nullptr, cg->d_links, cg->pm},
                 launch_blocks(cg, true), s, ng ? gf : nullptr, ng);
@@ -135,11 +150,18 @@ void peer_update_xr(tw_cg* cg, cudaStream_t s) {
                      launch_blocks(cg, false), s);
 }
 
-void peer_update_p(tw_cg* cg, cudaStream_t s) {
-    launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc,
-                    ScalarSrc{cg->win->recv_b, cg->P, cg->win->flag_b}, cg->slot(0), cg->history,
-                    launch_blocks(cg, false), s, cg->d_links, nullptr, false,
-                    x_in_k3(cg) ? cg->x : nullptr);
+void peer_update_p(tw_cg* cg, cudaStream_t s, int xph) {
+    const ScalarSrc bs{cg->win->recv_b, cg->P, cg->win->flag_b};
+    const int bv = launch_blocks(cg, false);
+    if (xph == XPH_DEFER) // p_k+1 into the pair buffer and the neighbours' pair-buffer ghosts
+        launch_update_p(0, cg->n, cg->r, cg->p2_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, cg->d_links2, cg->p_owned, false, nullptr);
+    else if (xph == XPH_PAIR) // both x updates; p_k+2 back into p_owned and its ghosts
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, cg->d_links, cg->p2_owned, false, cg->x, cg->p_owned);
+    else
+        launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, bs, cg->slot(0), cg->history, bv,
+                        s, cg->d_links, nullptr, false, x_in_k3(cg) ? cg->x : nullptr);
 }
 
 void alloc_window(tw_cg* cg) {
@@ -153,12 +175,25 @@ void alloc_window(tw_cg* cg) {
     }
 }
 
+// (the caller set links' windows, flags and ghost targets, and links2's
+// ghost targets when the x updates are paired)
 void finish_links(tw_cg* cg) {
     cg->links.rank = cg->ctx->rank;
     cg->links.nranks = cg->P;
     cg->links.plane = cg->plane;
     if (!cg->d_links) TW_CUDA(cudaMalloc(&cg->d_links, sizeof(PeerLinks)));
     TW_CUDA(cudaMemcpy(cg->d_links, &cg->links, sizeof(PeerLinks), cudaMemcpyHostToDevice));
+    if (cg->x_pairs) {
+        PeerLinks L2 = cg->links;
+        L2.ghost_lo_dst = cg->links2.ghost_lo_dst;
+        L2.ghost_hi_dst = cg->links2.ghost_hi_dst;
+        if ((L2.ghost_lo_dst == nullptr) != (cg->links.ghost_lo_dst == nullptr) ||
+            (L2.ghost_hi_dst == nullptr) != (cg->links.ghost_hi_dst == nullptr))
+            contract_error("a neighbour's pair buffer is missing (all ranks pair their x updates or none)");
+        cg->links2 = L2;
+        if (!cg->d_links2) TW_CUDA(cudaMalloc(&cg->d_links2, sizeof(PeerLinks)));
+        TW_CUDA(cudaMemcpy(cg->d_links2, &cg->links2, sizeof(PeerLinks), cudaMemcpyHostToDevice));
+    }
     cg->peer = true;
     if (cg->graph) { // graphs captured before the switch used the NCCL path
         cudaGraphExecDestroy(cg->graph);
@@ -193,6 +228,8 @@ void group_check(tw_cg** g, int P) {
             config_error("the ranks of a group run the same variant and tile count");
         if (g[r]->opt.dispatch != g[0]->opt.dispatch)
             config_error("the ranks of a group use the same dispatch");
+        if (g[r]->x_pairs != g[0]->x_pairs)
+            config_error("the ranks of a group pair their x updates alike");
     }
 }
 
@@ -204,15 +241,18 @@ void loopback_allgather(tw_cg** g, int P, double* tw_cg::*send, double* tw_cg::*
                                     cudaMemcpyDeviceToDevice, s));
 }
 
-void loopback_halo(tw_cg** g, int P, cudaStream_t s) {
+void loopback_halo(tw_cg** g, int P, cudaStream_t s, int xph) {
+    // the buffer this iteration's K1 reads: the pair buffer in the second
+    // iteration of an x-update pair
+    auto buf = [&](int r) { return xph == XPH_PAIR ? g[r]->p2_local : g[r]->p_local; };
     for (int r = 0; r < P; ++r) {
         const tw_slab_t& sp = g[r]->slab;
         const size_t bytes = sizeof(double) * static_cast<size_t>(sp.plane);
         if (sp.ghost_lo) // my lower ghost <- rank r-1's last owned plane
-            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_lo, g[r - 1]->p_local + g[r - 1]->slab.send_hi,
+            TW_CUDA(cudaMemcpyAsync(buf(r) + sp.recv_lo, buf(r - 1) + g[r - 1]->slab.send_hi,
                                     bytes, cudaMemcpyDeviceToDevice, s));
         if (sp.ghost_hi) // my upper ghost <- rank r+1's first owned plane
-            TW_CUDA(cudaMemcpyAsync(g[r]->p_local + sp.recv_hi, g[r + 1]->p_local + g[r + 1]->slab.send_lo,
+            TW_CUDA(cudaMemcpyAsync(buf(r) + sp.recv_hi, buf(r + 1) + g[r + 1]->slab.send_lo,
                                     bytes, cudaMemcpyDeviceToDevice, s));
     }
 }
@@ -237,13 +277,17 @@ void group_enable_peer(tw_cg** g, int P) {
         PeerLinks& L = g[r]->links;
         L = PeerLinks{};
         for (int q = 0; q < P; ++q) L.win[q] = g[q]->win;
+        PeerLinks& L2 = g[r]->links2; // (its ghost targets: the pair buffers)
+        L2 = PeerLinks{};
         if (r > 0) {
             L.ghost_lo_dst = g[r - 1]->p_local + g[r - 1]->slab.recv_hi;
             L.ghost_lo_flag = &g[r - 1]->win->flag_ghost_hi;
+            if (g[r - 1]->p2_local) L2.ghost_lo_dst = g[r - 1]->p2_local + g[r - 1]->slab.recv_hi;
         }
         if (r + 1 < P) {
             L.ghost_hi_dst = g[r + 1]->p_local + g[r + 1]->slab.recv_lo;
             L.ghost_hi_flag = &g[r + 1]->win->flag_ghost_lo;
+            if (g[r + 1]->p2_local) L2.ghost_hi_dst = g[r + 1]->p2_local + g[r + 1]->slab.recv_lo;
         }
         finish_links(g[r]);
     }
@@ -315,20 +359,23 @@ void group_iterate(tw_cg** g, int P, int k) {
     if (persistent && k > 0) enqueue_persistent(g, P, k);
     for (int it = 0; it < k && tasks && !persistent; ++it) group_tasks_iteration(g, P, s);
     for (int it = 0; it < k && !tasks && g[0]->peer; ++it) { // peer transport: stores + flags
-        for (int r = 0; r < P; ++r) peer_spmv(g[r], s);
+        const int xph = x_phase(g[0], it, k);
+        for (int r = 0; r < P; ++r) peer_spmv(g[r], s, xph);
         for (int r = 0; r < P; ++r) peer_update_xr(g[r], s);
-        for (int r = 0; r < P; ++r) peer_update_p(g[r], s);
+        for (int r = 0; r < P; ++r) peer_update_p(g[r], s, xph);
     }
     for (int it = 0; it < k && !tasks && !g[0]->peer; ++it) {
-        loopback_halo(g, P, s);
+        const int xph = x_phase(g[0], it, k);
+        loopback_halo(g, P, s, xph);
         for (int r = 0; r < P; ++r) {
-            dist_spmv_interior(g[r], s);
-            dist_spmv_boundary(g[r], s);
+            const double* pl = xph == XPH_PAIR ? g[r]->p2_local : g[r]->p_local;
+            dist_spmv_interior(g[r], s, pl);
+            dist_spmv_boundary(g[r], s, pl);
         }
         loopback_allgather(g, P, &tw_cg::send_a, &tw_cg::recv_a, s);
         for (int r = 0; r < P; ++r) dist_update_xr(g[r], s);
         loopback_allgather(g, P, &tw_cg::send_b, &tw_cg::recv_b, s);
-        for (int r = 0; r < P; ++r) dist_update_p(g[r], s);
+        for (int r = 0; r < P; ++r) dist_update_p(g[r], s, xph);
     }
     group_join(g, P, s);
     for (int r = 0; r < P; ++r) g[r]->enqueued += k;
@@ -460,7 +507,9 @@ int tw_cg_peer_ping_check(tw_cg* cg, int timeout_ms, int* ok) {
 // blob: [0,64) window IPC handle, [64,128) p_base IPC handle, [128,136)
 // byte offset of the lower ghost plane in p_base, [136,144) of the upper,
 // [144,148) rank, [148,152) rank count, [152,160) plane size (checked on
-// connect: a neighbour's ghost planes must match this rank's planes).
+// connect: a neighbour's ghost planes must match this rank's planes),
+// [160,168) byte offset of the pair buffer in p_base (0 without paired x
+// updates; all ranks must agree).
 int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
     return guarded([&] {
         if (!cg || !blob) contract_error("null solver or blob");
@@ -481,6 +530,9 @@ int tw_cg_peer_export(tw_cg* cg, unsigned char* blob) {
         std::memcpy(blob + 148, &nranks, 4);
         const int64_t plane = cg->plane;
         std::memcpy(blob + 152, &plane, 8); // a neighbour's ghost planes must be this size
+        // paired x updates: the pair buffer's byte offset from p_base (0: none)
+        const int64_t p2 = cg->p2_base ? (cg->p2_base - cg->p_base) * static_cast<int64_t>(sizeof(double)) : 0;
+        std::memcpy(blob + 160, &p2, 8);
     });
 }
 
@@ -493,6 +545,7 @@ int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
         const int P = cg->P, me = cg->ctx->rank;
         PeerLinks& L = cg->links;
         L = PeerLinks{};
+        cg->links2 = PeerLinks{};
         auto open = [&](const unsigned char* h) {
             cudaIpcMemHandle_t mh;
             std::memcpy(&mh, h, sizeof(mh));
@@ -511,6 +564,10 @@ int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
             if (rq != q) contract_error("peer blobs must be in rank order");
             if (pq != P) contract_error("peer blob of a different rank count");
             if (plane_q != cg->plane) contract_error("peer blob of a different plane size (nx * ny)");
+            int64_t p2_q = 0;
+            std::memcpy(&p2_q, b + 160, 8);
+            if ((p2_q != 0) != cg->x_pairs)
+                contract_error("peer blob of a rank that pairs its x updates differently");
         }
         for (int q = 0; q < P; ++q) {
             const unsigned char* b = blobs + static_cast<size_t>(q) * TW_PEER_BLOB_BYTES;
@@ -522,15 +579,18 @@ int tw_cg_peer_connect(tw_cg* cg, const unsigned char* blobs) {
             L.win[q] = w;
             if (q == me - 1 || q == me + 1) {
                 unsigned char* pb = open(b + 64);
-                int64_t lo = 0, hi = 0;
+                int64_t lo = 0, hi = 0, p2 = 0;
                 std::memcpy(&lo, b + 128, 8);
                 std::memcpy(&hi, b + 136, 8);
+                std::memcpy(&p2, b + 160, 8);
                 if (q == me - 1) { // my first plane -> its upper ghost
                     L.ghost_lo_dst = reinterpret_cast<double*>(pb + hi);
                     L.ghost_lo_flag = &w->flag_ghost_hi;
+                    if (p2) cg->links2.ghost_lo_dst = reinterpret_cast<double*>(pb + p2 + hi);
                 } else {           // my last plane -> its lower ghost
                     L.ghost_hi_dst = reinterpret_cast<double*>(pb + lo);
                     L.ghost_hi_flag = &w->flag_ghost_lo;
+                    if (p2) cg->links2.ghost_hi_dst = reinterpret_cast<double*>(pb + p2 + lo);
                 }
             }
         }

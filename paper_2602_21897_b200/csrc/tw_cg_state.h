@@ -31,6 +31,10 @@ struct tw_cg {
     PeerWindow* win = nullptr;
     PeerLinks links{};
     PeerLinks* d_links = nullptr;
+    // paired x updates: the same links with the neighbours' pair-buffer
+    // ghost planes as the halo targets (the K3 that writes the pair buffer)
+    PeerLinks links2{};
+    PeerLinks* d_links2 = nullptr;
     unsigned long long ping_seq = 0; // transport-check round (same on every rank)
     std::vector<void*> ipc_mapped;
     unsigned epoch = 0; // set_rhs count
@@ -39,7 +43,7 @@ struct tw_cg {
     double* r = nullptr;      // r_base + 16: 2+ doubles of slack each side (staged runs of r)
     double* r_base = nullptr;
     double* p_base = nullptr;
-    double* p2_base = nullptr; // pair buffer (x_pairs): p_k+1 between the two K3s of a pair
+    double* p2_base = nullptr; // pair buffer (x_pairs; inside the p_base allocation): p_k+1 between the two K3s of a pair
     double* p2_local = nullptr;
     double* p2_owned = nullptr;
     double* p_local = nullptr; // x_len entries: [ghost lo] owned [ghost hi]
@@ -185,21 +189,21 @@ void wait_cg(tw_cg* cg);
 
 // tw_cg_dist.cpp
 void allgather1(tw_cg* cg, const double* send, double* recv, cudaStream_t s);
-void halo_exchange(tw_cg* cg, cudaStream_t s);
-void dist_spmv_interior(tw_cg* cg, cudaStream_t s);
-void dist_spmv_boundary(tw_cg* cg, cudaStream_t s);
+void halo_exchange(tw_cg* cg, cudaStream_t s, double* p_local = nullptr);
+void dist_spmv_interior(tw_cg* cg, cudaStream_t s, const double* p_local = nullptr);
+void dist_spmv_boundary(tw_cg* cg, cudaStream_t s, const double* p_local = nullptr);
 void dist_update_xr(tw_cg* cg, cudaStream_t s);
-void dist_update_p(tw_cg* cg, cudaStream_t s);
+void dist_update_p(tw_cg* cg, cudaStream_t s, int xph = XPH_SINGLE);
 bool peer_k1_fused(const tw_cg* cg);
-void peer_spmv(tw_cg* cg, cudaStream_t s);
+void peer_spmv(tw_cg* cg, cudaStream_t s, int xph = XPH_SINGLE);
 void peer_update_xr(tw_cg* cg, cudaStream_t s);
-void peer_update_p(tw_cg* cg, cudaStream_t s);
+void peer_update_p(tw_cg* cg, cudaStream_t s, int xph = XPH_SINGLE);
 void alloc_window(tw_cg* cg);
 void finish_links(tw_cg* cg);
 void group_check(tw_cg** g, int P);
 void loopback_allgather(tw_cg** g, int P, double* tw_cg::*send, double* tw_cg::*recv,
                         cudaStream_t s);
-void loopback_halo(tw_cg** g, int P, cudaStream_t s);
+void loopback_halo(tw_cg** g, int P, cudaStream_t s, int xph = XPH_SINGLE);
 void group_join(tw_cg** g, int P, cudaStream_t s);
 void group_enable_peer(tw_cg** g, int P);
 void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device);

@@ -266,12 +266,10 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
-                     const double* psrc = nullptr, bool pdl = false, double* x = nullptr);
-// K3 of the second iteration of an x-update pair: p = r + beta p1,
-// x = (x + alpha_prev p0) + alpha p1 (p may alias p0)
-void launch_update_p_pair(int64_t i0, int64_t i1, const double* r, double* p,
-                          const CgScalars* sc, const double* p1, const double* p0, double* x,
-                          int blocks, cudaStream_t s);
+                     const double* psrc = nullptr, bool pdl = false, double* x = nullptr,
+                     const double* p0 = nullptr);
+// (with p0: the K3 of an x-update pair's second iteration, p = r + beta psrc,
+// x = (x + alpha_prev p0) + alpha psrc; p may alias p0)
 // K1 of the peer transport as one launch (interior, then the two boundary
 // ranges after a per-warp ghost-flag acquire), partials bit-identical to
 // the two launches; pm[0] = interior p.Ap into *fin.pre, fin (FIN_PUBLISH_A)

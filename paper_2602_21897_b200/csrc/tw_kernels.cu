@@ -554,7 +554,10 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
     else
         alpha = sc ? sc->alpha : __ldcg(asrc.parts); // standalone op: alpha from a device scalar
     const double nalpha = -alpha; // waxpby(1, r, -alpha, Ap, r) (cg.cpp:383)
-    if (!WX && asrc.count > 0 && g.bid == 0 && threadIdx.x == 0) sc->alpha = alpha;
+    if (!WX && asrc.count > 0 && g.bid == 0 && threadIdx.x == 0) {
+        sc->alpha_prev = sc->alpha; // the previous iteration's (paired x updates in K3)
+        sc->alpha = alpha;
+    }
     double part = 0.0;
     for_pairs<TW_K2_REV != 0>(g, i0, i1, [&](int64_t e, bool lo, bool hi) {
         if (!WX) {
@@ -632,6 +635,9 @@ update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* _
 #ifndef TW_K3XX_UNROLL
 #define TW_K3XX_UNROLL 1 // K3 with the paired x update
 #endif
+#ifndef TW_K3PXX_UNROLL
+#define TW_K3PXX_UNROLL 1 // the peer K3 with the paired x update
+#endif
 // XU: the x update riding on K3's read of p_old --
 //   0: none;
 //   1: x += alpha p_old (the x update moved out of K2);
@@ -697,20 +703,26 @@ __device__ __forceinline__ void p_stream(int64_t a0, int64_t b0, int64_t tid, in
 
 // PEER: the peer-transport instantiation (flag wait, fused halo stores);
 // the plain one stays lean so the grid keeps its full occupancy.
-template <bool PEER, bool WX>
+// XU: the x update riding on this K3 (p_stream): 0 none, 1 x += alpha p_old,
+// 2 the second K3 of an x-update pair (p0 = the previous iteration's p,
+// alpha0 = its alpha, kept in sc->alpha_prev by K1's alpha finalisation).
+template <bool PEER, int XU>
 __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
                                               const double* __restrict__ r, double* __restrict__ p,
                                               CgScalars* sc, ScalarSrc bsrc, RedScratch rs,
                                               double* history, const PeerLinks* links_,
                                               const double* __restrict__ psrc,
-                                              double* __restrict__ x) {
+                                              double* __restrict__ x, const double* p0) {
     // psrc: p_old, == p in place (each element is read, then written, by the
-    // same thread, so the restrict-qualified aliasing is never observable)
+    // same thread, so the restrict-qualified aliasing is never observable);
+    // p0 may alias p the same way (the pair writes p_k+2 over p_k)
+    constexpr bool WX = XU != 0;
     const PeerLinks* links = PEER ? links_ : nullptr;
     pdl_launch_dependents();
     pdl_wait(); // r and beta come from K2
     double beta, rr = 0.0;
     const double alpha = WX ? sc->alpha : 0.0; // this iteration's (K1 / K2 left it there)
+    const double alpha0 = XU == 2 ? sc->alpha_prev : 0.0;
     unsigned long long next = 0; // flag stamp of the next iteration (peer ghost flags)
     if (PEER && bsrc.flags) block_wait_flags(bsrc.flags, bsrc.count, stamp_of(sc, 0));
     if (bsrc.count > 0) {
@@ -742,9 +754,10 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     // Full pairs of [a0, b0) with 128-bit accesses, two pairs per thread and
     // step (both pairs' loads issued before either store: twice the bytes in
     // flight of a one-pair loop); the at most two ragged ends go scalar.
+    constexpr int U = XU == 2 ? (PEER ? TW_K3PXX_UNROLL : TW_K3XX_UNROLL)
+                              : PEER ? (WX ? TW_K3PX_UNROLL : 2) : (WX ? TW_K3X_UNROLL : TW_K3_UNROLL);
     auto stream = [&](int64_t a0, int64_t b0) {
-        p_stream<PEER ? (WX ? TW_K3PX_UNROLL : 2) : (WX ? TW_K3X_UNROLL : TW_K3_UNROLL), WX ? 1 : 0>(
-            a0, b0, tid, stride, r, psrc, p, beta, x, alpha);
+        p_stream<U, XU>(a0, b0, tid, stride, r, psrc, p, beta, x, alpha, p0, alpha0);
     };
     if (!links) {
         stream(i0, i1);
@@ -776,6 +789,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
         for (int64_t k = etid; k < nedge; k += estride) {
             const int64_t i = k < nlo ? i0 + k : hi_beg + (k - nlo);
             TW_DCHECK(i >= i0 && i < i1);
+            if (XU == 2) x[i] = __dadd_rn(x[i], __dmul_rn(alpha0, p0[i]));
             if (WX) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, psrc[i]));
             const double v = __dadd_rn(r[i], __dmul_rn(beta, psrc[i]));
             p[i] = v;
@@ -796,32 +810,13 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     stream(lo_end, hi_beg);
 }
 
-template <bool PEER, bool WX>
+template <bool PEER, int XU>
 __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
-                const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x) {
-    update_p_rows<PEER, WX>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x);
-}
-
-// K3 of the second iteration of an x-update pair (one rank, monolithic):
-// p = r + beta p1 with p1 = this iteration's p_old, and x = (x + alpha_prev
-// p0) + alpha p1, p0 = the previous iteration's p_old, kept by the first
-// iteration of the pair (whose K3 wrote its new p to the other buffer and
-// left x alone).  p may alias p0 (each element read, then written, by the
-// same thread).  x moves 16 n bytes per PAIR instead of per iteration, for
-// 8 n bytes more reading p0: 4 n bytes less per iteration.
-__global__ void __launch_bounds__(kThreads)
-update_p_pair_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* p,
-                     const CgScalars* sc, const double* __restrict__ p1, const double* p0,
-                     double* __restrict__ x) {
-    pdl_launch_dependents();
-    pdl_wait();
-    const double beta = sc->beta, alpha = sc->alpha, alpha0 = sc->alpha_prev;
-    const GridPos g = launch_grid();
-    const int64_t tid = static_cast<int64_t>(g.bid) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(g.nblk) * blockDim.x;
-    p_stream<TW_K3XX_UNROLL, 2>(i0, i1, tid, stride, r, p1, p, beta, x, alpha, p0, alpha0);
+                const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x,
+                const double* p0) {
+    update_p_rows<PEER, XU>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x, p0);
 }
 
 // ------------------------------------------- concurrent rank group (1 GPU)
@@ -916,9 +911,9 @@ rank_group_kernel(const GroupRank* ranks, int B, int iterations, int jitter) {
 #endif
                        Fin{FIN_PUBLISH_B, R.send_b, R.sc, nullptr, R.links, nullptr});
         group_barrier(R.bar, B);
-        update_p_rows<true, true>(g, 0, R.n, R.r, R.p_owned, R.sc,
+        update_p_rows<true, 1>(g, 0, R.n, R.r, R.p_owned, R.sc,
                                   ScalarSrc{R.win->recv_b, R.P, R.win->flag_b}, R.rs, R.history,
-                                  R.links, R.p_owned, R.x);
+                                  R.links, R.p_owned, R.x, nullptr);
         group_barrier(R.bar, B);
     }
 }
@@ -1230,14 +1225,17 @@ void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links, const double* psrc, bool pdl,
-                     double* x) {
+                     double* x, const double* p0) {
     // grid: at most one resident wave of this instantiation (a partial
     // second wave of a grid-stride loop would double the tail)
     const bool peer = links != nullptr || bsrc.flags != nullptr;
-    const int which = (peer ? 2 : 0) + (x ? 1 : 0);
-    using K = decltype(&update_p_kernel<false, false>);
-    static const K kerns[4] = {update_p_kernel<false, false>, update_p_kernel<false, true>,
-                               update_p_kernel<true, false>, update_p_kernel<true, true>};
+    const int xu = x ? (p0 ? 2 : 1) : 0;
+    if (p0 && !x) throw Error(TW_ERR_CONTRACT, "the pair's p0 comes with its x update");
+    const int which = (peer ? 3 : 0) + xu;
+    using K = decltype(&update_p_kernel<false, 0>);
+    static const K kerns[6] = {update_p_kernel<false, 0>, update_p_kernel<false, 1>,
+                               update_p_kernel<false, 2>, update_p_kernel<true, 0>,
+                               update_p_kernel<true, 1>, update_p_kernel<true, 2>};
     // resident blocks per SM of each instantiation (thread-safe one-time init;
     // the grid multiplies by this device's SM count)
     auto occupancy = [](K k) {
@@ -1246,8 +1244,8 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
                                                               kThreads, 0));
         return o > 0 ? o : 1;
     };
-    static const int occ[4] = {occupancy(kerns[0]), occupancy(kerns[1]), occupancy(kerns[2]),
-                               occupancy(kerns[3])};
+    static const int occ[6] = {occupancy(kerns[0]), occupancy(kerns[1]), occupancy(kerns[2]),
+                               occupancy(kerns[3]), occupancy(kerns[4]), occupancy(kerns[5])};
     int dev = 0, sms = 0;
     TW_CUDA(cudaGetDevice(&dev));
     TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1255,25 +1253,7 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
     if (x && !sc) throw Error(TW_ERR_CONTRACT, "the fused x update needs the solver's scalars");
     launch_k(kerns[which], dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history,
-             links, psrc ? psrc : p, x);
-    TW_CUDA(cudaGetLastError());
-}
-
-void launch_update_p_pair(int64_t i0, int64_t i1, const double* r, double* p,
-                          const CgScalars* sc, const double* p1, const double* p0, double* x,
-                          int blocks, cudaStream_t s) {
-    static const int occ = [] {
-        int o = 0;
-        TW_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &o, reinterpret_cast<const void*>(update_p_pair_kernel), kThreads, 0));
-        return o > 0 ? o : 1;
-    }();
-    int dev = 0, sms = 0;
-    TW_CUDA(cudaGetDevice(&dev));
-    TW_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int wave = occ * sms;
-    const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
-    update_p_pair_kernel<<<g, kThreads, 0, s>>>(i0, i1, r, p, sc, p1, p0, x);
+             links, psrc ? psrc : p, x, p0);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -1241,3 +1241,44 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
     check_history(out["k3"][0], want_h)
     assert np.all(rel_gap(out["k3"][1][-3], want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("transport", ["loopback", "peer"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_x_update_pairs_across_ranks(orc, transport, nranks):
+    """Paired x updates across z-slab ranks (monolithic): the halo alternates
+    buffers with the x updates -- the loopback / NCCL halo exchanges the pair
+    buffer's planes before the second iteration of a pair, the peer K3 of the
+    first stores its edge planes into the neighbours' pair-buffer ghost
+    planes (a second set of links).  Histories and x bit-identical to the x
+    update in every K3 for calls of odd and even lengths, also with the
+    concurrent group (single updates) interleaved, and within the rule of
+    the oracle."""
+    dims = (64, 40, 48)
+    b = orc.rhs_xorshift(int(np.prod(dims)), 9)
+    calls = (1, 4, 3, 2, 5)
+    total = sum(calls)
+    out = {}
+    for xu in ("k3", "k3_pairs"):
+        G = P.EmulatedRankGroup(*dims, nranks, total, transport=transport,
+                                 options=P.CgOptions(iteration_marks=False, x_update=xu))
+        assert G.solvers[0].mode()["x_in_k3"] == (2 if xu == "k3_pairs" else 1)
+        G.set_rhs(b)
+        xs = []
+        for j, c in enumerate(calls):
+            if transport == "peer" and j == 2:
+                G.iterate_concurrent(c)  # single updates in one cooperative kernel
+            else:
+                G.iterate(c)
+            xs.append(G.solution())
+        hs = G.history(total)
+        for h in hs:
+            assert np.array_equal(h, hs[0])
+        out[xu] = (hs[0], xs)
+        G.close()
+    assert np.array_equal(out["k3"][0], out["k3_pairs"][0])
+    for a, c in zip(out["k3"][1], out["k3_pairs"][1]):
+        assert np.array_equal(a, c)
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
+    check_history(out["k3_pairs"][0], want_h)
+    assert np.all(rel_gap(out["k3_pairs"][1][-1], want_x) <= 1e-10)
