@@ -27,8 +27,8 @@ it = [k for k in agg if k.startswith(("spmv", "update"))]
 # x-update pairs: the two K3 kernels alternate, one of them per iteration
 # x-update pairs: the pair's two K3 kernels alternate, one of them per
 # iteration; the single-update K3 then only ends a call of odd length
-pairs = "update_p_pair_kernel" in agg
-half = {"update_p_kernel<0, 0>", "update_p_pair_kernel"} if pairs else set()
+pairs = "update_p_kernel<0, 2>" in agg  # update_p_kernel<PEER, XU>: XU 2 = the pair's second K3
+half = {"update_p_kernel<0, 0>", "update_p_kernel<0, 2>"} if pairs else set()
 wgt = {k: 0.5 if k in half else 0.0 if pairs and k == "update_p_kernel<0, 1>" else 1.0
        for k in it}
 tot = sum(wgt[k] * agg[k][1] / agg[k][0] for k in it)
@@ -91,21 +91,21 @@ def _name_of(path):  # demangled kernel name of a one-kernel capture
 
 # from 4M rows the x update runs in K3 (update_xr_kernel<false> streams
 # r, Ap -> r: 24 n; update_p_kernel<false, true> r, p, x -> p, x: 40 n); a
-# one-GPU monolithic solve pairs it (prof_k3p: update_p_pair_kernel, r, p,
-# p_prev, x -> p, x: 48 n; prof_k3 then holds the pair's first K3,
-# update_p_kernel<false, false>, r, p -> p: 24 n)
+# one-GPU monolithic solve pairs it (prof_k3p: update_p_kernel<false, 2>,
+# r, p, p_prev, x -> p, x: 48 n; prof_k3 then holds the pair's first K3,
+# update_p_kernel<false, 0>, r, p -> p: 24 n)
 _xk3 = "update_xr_kernel<0>" in _name_of(os.path.join(base, "prof_k2.ncu-rep"))
 _k3p = os.path.join(base, "prof_k3p.ncu-rep")
-_pairs = os.path.exists(_k3p) and "update_p_pair" in _name_of(_k3p)
+_pairs = os.path.exists(_k3p)
 if os.path.exists(os.path.join(base, "prof_k2.ncu-rep")):
     summarize(os.path.join(base, "prof_k2.ncu-rep"),
               "update_xr_kernel (K2%s)" % (", r only" if _xk3 else ""), (24 if _xk3 else 48) * N,
               "profiles/k2_traffic.json")
 _k3 = os.path.join(base, "prof_k3.ncu-rep")
 if _pairs and os.path.exists(_k3):
-    a = summarize(_k3, "update_p_kernel<false, false> (K3, first of an x pair)", 24 * N)
-    b = summarize(_k3p, "update_p_pair_kernel (K3, second of an x pair)", 48 * N)
-    d = {"kernel": "K3 x-update pair: update_p_kernel<false, false> + update_p_pair_kernel, "
+    a = summarize(_k3, "update_p_kernel<false, 0> (K3, first of an x pair)", 24 * N)
+    b = summarize(_k3p, "update_p_kernel<false, 2> (K3, second of an x pair)", 48 * N)
+    d = {"kernel": "K3 x-update pair: update_p_kernel<false, 0> + update_p_kernel<false, 2>, "
                    "per launch averaged over the pair",
          "workload": "256x256x256", "round": tag, "source": a["source"],
          "dram_bytes_per_launch": (a["dram_bytes_per_launch"] + b["dram_bytes_per_launch"]) / 2,
