@@ -17,8 +17,8 @@ ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 4 -c
     -o gpurun_out/prof_k1 -f $CMD > gpurun_out/ncu_full.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:update_xr -s 4 -c 1 \
     -o gpurun_out/prof_k2 -f $CMD > gpurun_out/ncu_full_k2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:update_p_kernel<.*0, .*0>" -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:update_p_kernel<.*0, .*0>" -s 2 -c 1 \
     -o gpurun_out/prof_k3 -f $CMD > gpurun_out/ncu_full_k3.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k "regex:update_p_kernel<.*0, .*2>" -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:update_p_kernel<.*0, .*2>" -s 2 -c 1 \
     -o gpurun_out/prof_k3p -f $CMD > gpurun_out/ncu_full_k3p.log 2>&1
 echo "ncu exit $?"
