@@ -246,13 +246,14 @@ typedef struct tw_cg_options {
     int64_t dag_vec_rows;          /* persistent dispatcher: rows per update chunk         */
 } tw_cg_options;
 
-#define TW_XUPD_AUTO 0   /* K3 from 4M rows per rank (8n bytes less per iteration), else K2;
-                          * one rank: K3 pairs from 512k rows (monolithic, tasks on streams /
-                          * graphs) or 4M rows (the persistent dispatcher)                   */
+#define TW_XUPD_AUTO 0   /* K3 pairs from 512k rows per rank (monolithic, tasks on streams /
+                          * graphs) or 4M (the persistent dispatcher; across ranks the global
+                          * rows per rank decide, alike on every rank); else K3 from 4M rows
+                          * per rank (8n bytes less per iteration), else K2                  */
 #define TW_XUPD_K2 1     /* in K2 with r -= alpha Ap                                        */
 #define TW_XUPD_K3 2     /* in K3, reading p before it is overwritten                       */
 #define TW_XUPD_K3_PAIRS 3 /* in K3 once per pair of iterations, x = (x + a_k p_k) + a_k+1 p_k+1
-                            * (one rank, any executor, else as _K3; 4n bytes less per
+                            * (every executor, one rank or across ranks; 4n bytes less per
                             * iteration than _K3)                                              */
 #define TW_L2KEEP_AUTO 0 /* evict_last on the staged x runs while x has <= 8M entries       */
 #define TW_L2KEEP_ON 1

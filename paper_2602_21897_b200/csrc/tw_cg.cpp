@@ -58,14 +58,10 @@ static bool dag_pairs_fit(const tw_cg* cg);
 // Across ranks (monolithic: the halo then alternates buffers too) every
 // rank must make the same choice, so it rests on the global rows per rank.
 static bool auto_pairs(const tw_cg* cg) {
-    if (cg->dist) {
-        const tw_ell_info_t& in = cg->A->info;
-        return cg->opt.variant == TW_CG_MONOLITHIC &&
-               in.n_global / std::max(cg->P, 1) >= (int64_t(1) << 19);
-    }
-    if (cg->n < (int64_t(1) << 19)) return false;
+    const int64_t rows = cg->dist ? cg->A->info.n_global / std::max(cg->P, 1) : cg->n;
+    if (rows < (int64_t(1) << 19)) return false;
     if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT)
-        return cg->n >= (int64_t(1) << 22) && dag_pairs_fit(cg);
+        return rows >= (int64_t(1) << 22) && dag_pairs_fit(cg);
     return true;
 }
 
@@ -87,7 +83,6 @@ static bool dag_pairs_fit(const tw_cg* cg) {
 
 static bool decide_x_pairs(const tw_cg* cg) {
     if (!cg->x_k3) return false;
-    if (cg->dist && cg->opt.variant != TW_CG_MONOLITHIC) return false; // tasks across ranks: single
     if (cg->opt.variant == TW_CG_TASKS && cg->opt.dispatch == TW_DISPATCH_PERSISTENT &&
         !dag_pairs_fit(cg))
         return false;
@@ -245,7 +240,7 @@ int tile_share(const tw_cg* cg) {
 }
 
 void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
-    if (xph != XPH_SINGLE && (!cg->x_pairs || cg->dist)) contract_error("paired x update not enabled");
+    if (xph != XPH_SINGLE && !cg->x_pairs) contract_error("paired x update not enabled");
     // the iteration's p_old: in the pair buffer for the second of a pair
     double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
     double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
@@ -256,8 +251,8 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
     const int bs = (launch_blocks(cg, true) + share - 1) / share;
     const int bv = (launch_blocks(cg, false) + share - 1) / share;
     switch (nd.kind) {
-    case PK_HALO:
-        halo_exchange(cg, st);
+    case PK_HALO: // the buffer this iteration's SpMV tiles read
+        halo_exchange(cg, st, xph == XPH_PAIR ? cg->p2_local : nullptr);
         break;
     case PK_SPMV: { // the x-staged K1 when the matrix has it
         const Fin f = cg->tile_fin(cg->pa, t, FIN_ALPHA, cg->tile_tickets);
@@ -792,6 +787,7 @@ void build_dag_table(tw_cg** g, int P, int k) {
                         if (!cg->peer && (cg->glo || cg->ghi))
                             contract_error("the dispatcher's halo task needs the peer transport");
                         t.kind = DK_HALO;
+                        if (xph == XPH_PAIR) t.flags |= kDagReadP2; // the pair buffer's planes
                         break;
                     }
                     tasks.push_back(t);
@@ -894,6 +890,7 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
         R.pa = c->pa;
         R.rr = c->rrp;
         R.links = c->peer ? c->d_links : nullptr;
+        R.links2 = c->peer && c->x_pairs ? c->d_links2 : nullptr;
         R.win = c->peer ? c->win : nullptr;
         R.tctr = c->d_ticket + 2;
         R.iter0 = c->enqueued;
@@ -933,8 +930,10 @@ void enqueue_persistent(tw_cg** g, int P, int k) {
     const int ru = rows4, rp = D.x_in_updp ? rows3 : rows2;
     D.upd_block_rows = ru >= 128 ? ru : 0;
     D.updp_block_rows = rp >= 128 ? rp : 0;
-    if (cg->x_pairs && (P != 1 || !D.x_in_updp || !D.upd_block_rows))
-        contract_error("paired x updates need the dispatcher's TMA update chunks on one rank");
+    for (int r = 0; r < P; ++r)
+        if (g[r]->x_pairs != cg->x_pairs) contract_error("the ranks of a launch pair their x updates alike");
+    if (cg->x_pairs && (!D.x_in_updp || !D.upd_block_rows))
+        contract_error("paired x updates need the dispatcher's TMA update chunks");
     D.x_pairs = cg->x_pairs ? 1 : 0;
     // stamps[0] is the start of the first launch after set_rhs; later launches
     // write their start into a spare slot so iteration ends stay in place

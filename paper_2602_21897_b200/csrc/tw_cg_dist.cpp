@@ -316,11 +316,11 @@ void group_set_rhs(tw_cg** g, int P, const double* const* b, bool on_device) {
 // allgather, the rank-order combine), the x/r tiles, beta_res likewise, the
 // p tiles -- with the very kernels and partial orders of the NCCL tasks path
 // (launch_node), so its numbers are the multi-GPU executor's.
-static void group_tasks_iteration(tw_cg** g, int P, cudaStream_t s) {
+static void group_tasks_iteration(tw_cg** g, int P, cudaStream_t s, int xph) {
     auto nodes_of = [&](int kind) {
         for (int r = 0; r < P; ++r)
             for (const PNode& nd : g[r]->nodes)
-                if (nd.kind == kind) launch_node(g[r], nd, s);
+                if (nd.kind == kind) launch_node(g[r], nd, s, xph);
     };
     auto reduce = [&](double* tw_cg::*tile_parts, double* tw_cg::*send, double* tw_cg::*recv,
                       int fin_mode) {
@@ -330,7 +330,7 @@ static void group_tasks_iteration(tw_cg** g, int P, cudaStream_t s) {
         for (int r = 0; r < P; ++r)
             launch_combine(g[r]->*recv, P, Fin{fin_mode, nullptr, g[r]->sc, g[r]->history}, s);
     };
-    loopback_halo(g, P, s);
+    loopback_halo(g, P, s, xph);
     nodes_of(PK_SPMV);
     reduce(&tw_cg::pa, &tw_cg::send_a, &tw_cg::recv_a, FIN_ALPHA);
     nodes_of(PK_UPD);
@@ -357,7 +357,8 @@ void group_iterate(tw_cg** g, int P, int k) {
     // cross edges are the peer protocol's flag waits, so all ranks run at
     // once in one launch (never as separate launches waiting on each other)
     if (persistent && k > 0) enqueue_persistent(g, P, k);
-    for (int it = 0; it < k && tasks && !persistent; ++it) group_tasks_iteration(g, P, s);
+    for (int it = 0; it < k && tasks && !persistent; ++it)
+        group_tasks_iteration(g, P, s, x_phase(g[0], it, k));
     for (int it = 0; it < k && !tasks && g[0]->peer; ++it) { // peer transport: stores + flags
         const int xph = x_phase(g[0], it, k);
         for (int r = 0; r < P; ++r) peer_spmv(g[r], s, xph);

@@ -254,13 +254,16 @@ __device__ __forceinline__ double run_chunk(const DagParams& P, const DagTask& T
     }
     case DK_HALO: {
         // this rank's first / last owned plane of p into the neighbours'
-        // ghost planes (NVLink stores; the scheduler raises the flags)
-        const PeerLinks* L = R.links;
+        // ghost planes (NVLink stores; the scheduler raises the flags); in
+        // the second iteration of an x pair from and into the pair buffers
+        const bool p2 = XP && (T.flags & kDagReadP2) != 0;
+        const PeerLinks* L = p2 ? R.links2 : R.links;
         if (!L) break; // no neighbours
+        const double* src = p2 ? R.p2_owned : R.p_owned;
         const int64_t pl = L->plane, n = R.A.n_rows;
         for (int64_t i = ctid; i < pl; i += cthreads) {
-            if (L->ghost_lo_dst) L->ghost_lo_dst[i] = __ldcg(R.p_owned + i);
-            if (L->ghost_hi_dst) L->ghost_hi_dst[i] = __ldcg(R.p_owned + n - pl + i);
+            if (L->ghost_lo_dst) L->ghost_lo_dst[i] = __ldcg(src + i);
+            if (L->ghost_hi_dst) L->ghost_hi_dst[i] = __ldcg(src + n - pl + i);
         }
         break;
     }

@@ -420,6 +420,7 @@ struct DagRank {
     double* pa;              // tile partials of p.Ap
     double* rr;              // tile partials of r.r
     const PeerLinks* links;  // device copy; null on one rank
+    const PeerLinks* links2; // the same with the pair-buffer ghost targets (paired x updates)
     PeerWindow* win;         // this rank's window (flags it waits on)
     unsigned* tctr;          // [2] SpMV / x-r tiles done this iteration (publication)
     int iter0;               // iterations done before this launch

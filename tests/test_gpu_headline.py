@@ -195,9 +195,8 @@ def test_weak_scaling_two_ranks_at_size(oracle_weak2, how):
     else:
         G = P.EmulatedRankGroup(*dims, 2, 20, transport="loopback" if how == "loopback" else "peer")
     m = G.solvers[0].mode()
-    # x update in K3: paired on the monolithic ranks, single in the dispatcher across ranks
-    assert m["k1_form"] == N.TW_K1_STAGED and m["k1_l2_keep"] == 0
-    assert m["x_in_k3"] == (1 if how == "tasks_dispatcher" else 2)
+    # x updates paired in K3 (the dispatcher's p-update chunks) on every rank
+    assert m["k1_form"] == N.TW_K1_STAGED and m["k1_l2_keep"] == 0 and m["x_in_k3"] == 2
     G.set_rhs(b)
     if how == "peer_concurrent":
         G.iterate_concurrent(20)

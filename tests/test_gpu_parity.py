@@ -1282,3 +1282,42 @@ def test_x_update_pairs_across_ranks(orc, transport, nranks):
     want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
     check_history(out["k3_pairs"][0], want_h)
     assert np.all(rel_gap(out["k3_pairs"][1][-1], want_x) <= 1e-10)
+
+
+@pytest.mark.parametrize("how", ["streams", "persistent"])
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_x_update_pairs_tasks_across_ranks(orc, how, nranks):
+    """Paired x updates in the block-task DAG across z-slab ranks: the halo
+    task alternates buffers with the pairs (loopback copies of the NCCL
+    executor; the dispatcher's halo chunks store the pair buffer's planes
+    through the second set of peer links), the p-update tiles / chunks
+    alternate them as on one rank.  Bit-identical to the x update in every
+    p update for calls of odd and even lengths; ranks agree; the oracle's
+    rule holds."""
+    dims = (32, 16, 24)
+    b = orc.rhs_xorshift(int(np.prod(dims)), 11)
+    calls = (3, 6, 1, 4)
+    total = sum(calls)
+    out = {}
+    for xu in ("k3", "k3_pairs"):
+        opt = P.CgOptions(tiles=4, persistent=how == "persistent", iteration_marks=False,
+                          x_update=xu)
+        G = P.EmulatedRankGroup(*dims, nranks, total, variant=N_TASKS, options=opt,
+                                transport="peer" if how == "persistent" else "loopback")
+        assert G.solvers[0].mode()["x_in_k3"] == (2 if xu == "k3_pairs" else 1)
+        G.set_rhs(b)
+        xs = []
+        for c in calls:
+            G.iterate(c)
+            xs.append(G.solution())
+        hs = G.history(total)
+        for h in hs:
+            assert np.array_equal(h, hs[0])
+        out[xu] = (hs[0], xs)
+        G.close()
+    assert np.array_equal(out["k3"][0], out["k3_pairs"][0])
+    for a, c in zip(out["k3"][1], out["k3_pairs"][1]):
+        assert np.array_equal(a, c)
+    want_h, want_x, _ = orc.cg(orc.stencil(*dims), b, total)
+    check_history(out["k3_pairs"][0], want_h)
+    assert np.all(rel_gap(out["k3_pairs"][1][-1], want_x) <= 1e-10)
