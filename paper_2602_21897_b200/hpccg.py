@@ -555,8 +555,10 @@ class CgOptions:
         o.tol = float(self.tol)
         o.dispatch = (N.TW_DISPATCH_PERSISTENT if self.persistent else
                       N.TW_DISPATCH_AUTO if self.auto_dispatch else N.TW_DISPATCH_STREAMS)
-        o.x_update = {None: 0, "k2": 1, "k3": 2, "k3_pairs": 3}[self.x_update]
-        o.l2_keep = 0 if self.l2_keep is None else (1 if self.l2_keep else 2)
+        o.x_update = {None: N.TW_XUPD_AUTO, "k2": N.TW_XUPD_K2, "k3": N.TW_XUPD_K3,
+                      "k3_pairs": N.TW_XUPD_K3_PAIRS}[self.x_update]
+        o.l2_keep = (N.TW_L2KEEP_AUTO if self.l2_keep is None else
+                     N.TW_L2KEEP_ON if self.l2_keep else N.TW_L2KEEP_OFF)
         o.dag_spmv_slices = int(self.dag_spmv_slices)
         o.dag_vec_rows = int(self.dag_vec_rows)
         return o

@@ -33,6 +33,26 @@ def test_abi_version_and_struct_layout():
     assert (o.x_update, o.l2_keep, o.dag_spmv_slices, o.dag_vec_rows) == (0, 0, 0, 0)
 
 
+def test_constants_match_the_c_header():
+    """Every integer constant of the header that the Python mirror binds has
+    the header's value (placements, dispatch, K1 forms, transports, codes)."""
+    import re
+    defs = {}
+    for h in N.HEADERS:
+        for m in re.finditer(r"^#define\s+(TW_\w+)\s+(\d+)\b", open(h).read(), re.M):
+            defs[m.group(1)] = int(m.group(2))
+    for prefix in ("TW_XUPD_", "TW_L2KEEP_", "TW_DISPATCH_", "TW_K1_", "TW_TRANSPORT_", "TW_CG_",
+                   "TW_ERR_"):
+        names = [k for k in defs if k.startswith(prefix)]
+        assert names, prefix
+        for k in names:
+            assert getattr(N, k) == defs[k], k
+    o = P.CgOptions(x_update="k3_pairs", l2_keep=False).to_c(N.TW_CG_MONOLITHIC)
+    assert (o.x_update, o.l2_keep) == (N.TW_XUPD_K3_PAIRS, N.TW_L2KEEP_OFF)
+    with pytest.raises(KeyError):
+        P.CgOptions(x_update="k4").to_c(N.TW_CG_MONOLITHIC)
+
+
 def test_struct_layout_matches_the_c_header(tmp_path):
     """The ctypes mirrors of the ABI structs against the C compiler's own
     layout of include/tw_hpccg.h (sizeof and every field offset)."""
