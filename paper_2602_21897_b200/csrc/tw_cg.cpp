@@ -160,6 +160,16 @@ void record(cudaEvent_t e, cudaStream_t s) {
 // stream: K1 -> K2 -> K3 (x rides on K2 or on K3, x_in_k3); across ranks the
 // SpMV is split so the interior rows overlap the halo exchange on the comm
 // stream.
+// Programmatic dependent launch in the one-rank chain (bit 0 K1, 1 K2, 2 K3).
+// K1 only: its one 205 KB CTA per SM cannot co-reside with a full-occupancy
+// K3 wave, so its blocks take each SM as K3's blocks leave it, stream their
+// first matrix block and wait (griddepcontrol.wait) only before the x runs.
+// 128^3: 114.1 -> 111.6 us per iteration, 256^3 842.7 -> 841.4-842.7; K2
+// after K1 co-resides with K1 and loses (all three: 895 us at 256^3); the
+// SpMV tiles of the tasks variant gain nothing (profiles/r02_ab_pdl.md).
+#ifndef TW_MONO_PDL
+#define TW_MONO_PDL 1
+#endif
 void enqueue_mono(tw_cg* cg, int xph) {
     cudaStream_t s = cg->ctx->compute;
     const EllView A = cg->view();
@@ -172,23 +182,26 @@ void enqueue_mono(tw_cg* cg, int xph) {
         double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
         const Fin fa{FIN_ALPHA, nullptr, cg->sc, nullptr};
         record(tmark(cg, 0), s);
-        if (!launch_spmv_staged(A, pl, cg->Ap, RowRange{0, cg->n}, rs, fa, s))
+        const bool pdl1 = (TW_MONO_PDL & 1) && !cg->timing, pdl2 = (TW_MONO_PDL & 2) && !cg->timing,
+                   pdl3 = (TW_MONO_PDL & 4) && !cg->timing;
+        if (!launch_spmv_staged(A, pl, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, RowRange{0, 0},
+                                false, rs, fa, s, nullptr, 0, pdl1))
             launch_spmv(A, po, cg->Ap, RowRange{0, cg->n}, RowRange{0, 0}, true, rs, fa, bs, s);
         record(tmark(cg, 1), s);
         const bool xk3 = x_in_k3(cg);
         launch_update_xr(0, cg->n, xk3 ? nullptr : cg->x, po, cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, rs, Fin{FIN_BETA, nullptr, cg->sc, cg->history}, bv,
-                         s);
+                         s, pdl2);
         record(tmark(cg, 2), s);
         if (xph == XPH_DEFER) // p_k+1 into the pair buffer, p_k and x left as they are
             launch_update_p(0, cg->n, cg->r, cg->p2_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p_owned, false, nullptr);
+                            cg->history, bv, s, nullptr, cg->p_owned, pdl3, nullptr);
         else if (xph == XPH_PAIR) // x gets a_k-1 p_k-1 + a_k p_k; p_k+1 back into p_owned
             launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, cg->p2_owned, false, cg->x, cg->p_owned);
+                            cg->history, bv, s, nullptr, cg->p2_owned, pdl3, cg->x, cg->p_owned);
         else
             launch_update_p(0, cg->n, cg->r, cg->p_owned, cg->sc, ScalarSrc{nullptr, 0}, rs,
-                            cg->history, bv, s, nullptr, nullptr, false, xk3 ? cg->x : nullptr);
+                            cg->history, bv, s, nullptr, nullptr, pdl3, xk3 ? cg->x : nullptr);
         record(tmark(cg, 3), s);
         if (cg->timing) ++cg->timed;
         return;
