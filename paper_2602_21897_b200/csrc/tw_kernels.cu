@@ -31,6 +31,38 @@ namespace tw {
 
 namespace {
 
+#ifdef TW_TIMELINE
+// Probe builds only (scripts/timeline.py): one record per CTA of the
+// annotated kernels -- tag | SM | block, the first row of its range, and
+// thread 0's globaltimer at entry and exit.  Not in the product library.
+constexpr unsigned kTlCap = 1u << 20;
+__device__ unsigned long long tw_tl_buf[kTlCap][4];
+__device__ unsigned tw_tl_n;
+struct TlScope {
+    unsigned long long t0, i0;
+    int tag;
+    __device__ TlScope(int t, int64_t first) : t0(0), i0(static_cast<unsigned long long>(first)), tag(t) {
+        if (threadIdx.x == 0) t0 = dev::global_ns();
+    }
+    __device__ ~TlScope() {
+        if (threadIdx.x != 0) return;
+        const unsigned long long t1 = dev::global_ns();
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        const unsigned k = atomicAdd(&tw_tl_n, 1u);
+        if (k >= kTlCap) return;
+        tw_tl_buf[k][0] = static_cast<unsigned long long>(tag) | (static_cast<unsigned long long>(sm) << 8) |
+                          (static_cast<unsigned long long>(blockIdx.x) << 16);
+        tw_tl_buf[k][1] = i0;
+        tw_tl_buf[k][2] = t0;
+        tw_tl_buf[k][3] = t1;
+    }
+};
+#define TW_TL(tag, first) TlScope tw_tl_scope_((tag), (first))
+#else
+#define TW_TL(tag, first)
+#endif
+
 using namespace dev;
 
 
@@ -484,6 +516,7 @@ spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restri
                        RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
                        int c16_bytes, RedScratch rs, Fin fin, const unsigned long long* wait_flags,
                        int nwait) {
+    TW_TL(1, ra.r1 > ra.r0 ? ra.r0 : rb0.r0);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps];
     __shared__ int stage_w[kTmaWarps];
@@ -614,6 +647,7 @@ __global__ void __launch_bounds__(kThreads)
 update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
                  double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
                  ScalarSrc asrc, RedScratch rs, Fin fin) {
+    TW_TL(2, i0);
     update_xr_rows<WX>(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
 }
 
@@ -816,6 +850,7 @@ update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
                 const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x,
                 const double* p0) {
+    TW_TL(3, i0);
     update_p_rows<PEER, XU>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x, p0);
 }
 
@@ -941,6 +976,7 @@ waxpby_kernel(double alpha, const double* x, double beta, const double* y, doubl
 }
 
 __global__ void combine_kernel(const double* parts, int count, Fin fin) {
+    TW_TL(4, 0);
     if (threadIdx.x == 0) finalize(fin, sum_parts(parts, count));
 }
 
@@ -1300,3 +1336,19 @@ void launch_rhs_xorshift(const uint64_t* chunk_states, int64_t chunk, int64_t co
 }
 
 } // namespace tw
+
+#ifdef TW_TIMELINE
+extern "C" int tw_timeline_fetch(unsigned long long* host, int max_records) {
+    unsigned n = 0;
+    if (cudaMemcpyFromSymbol(&n, tw::tw_tl_n, sizeof(n)) != cudaSuccess) return -1;
+    if (n > tw::kTlCap) n = tw::kTlCap;
+    const unsigned m = static_cast<unsigned>(max_records) < n ? static_cast<unsigned>(max_records) : n;
+    if (m && cudaMemcpyFromSymbol(host, tw::tw_tl_buf, static_cast<size_t>(m) * 32) != cudaSuccess)
+        return -1;
+    return static_cast<int>(n);
+}
+extern "C" int tw_timeline_reset() {
+    const unsigned z = 0;
+    return cudaMemcpyToSymbol(tw::tw_tl_n, &z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif
