@@ -33,6 +33,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+HBM_SPEC_GBS = 8000.0  # B200 HBM3e data-sheet bandwidth (reported beside the measured peak)
 X_UPDATE_IN = {0: "K2", 1: "K3", 2: "K3 pairs"}  # tw_cg_mode_t.x_in_k3
 
 
@@ -744,6 +745,11 @@ def run_ours(args, dist, rank, world, local):
         roofline_iter["format_bytes_per_iter"] = fb
         roofline_iter["achieved_format"] = fb / (ms_max / 1e3 / K) / 1e9
         roofline_iter["frac_format"] = roofline_iter["achieved_format"] / (peak * world)
+    # next to the measured copy bandwidth, the HBM3e spec figure
+    roofline_iter["spec_gbs"] = HBM_SPEC_GBS * world
+    roofline_iter["frac_of_spec"] = iter_gbs / (HBM_SPEC_GBS * world)
+    if "achieved_format" in roofline_iter:
+        roofline_iter["frac_format_of_spec"] = roofline_iter["achieved_format"] / (HBM_SPEC_GBS * world)
 
     # ---- e2e: through the public API with host buffers (pinned b in, history + x out)
     b_host = torch.empty(n, dtype=torch.float64).pin_memory()
