@@ -1243,6 +1243,52 @@ def test_x_update_pairs_bit_identical(rt, orc, how):
     assert np.all(rel_gap(out["k3"][1][-3], want_x) <= 1e-10)
 
 
+@pytest.mark.parametrize("dims,xu", [((64, 40, 36), "k3_pairs"), ((64, 40, 36), None),
+                                     ((128, 64, 96), None)])
+@pytest.mark.parametrize("graph", [True, False])
+def test_k1_programmatic_launch_bit_identical(rt, orc, dims, xu, graph):
+    """The one-rank monolithic chain launches K1 programmatically after K3
+    (griddepcontrol.wait before the slice's x runs; tw_cg.cpp TW_MONO_PDL);
+    the per-kernel timing pass launches it plainly (events between the
+    kernels).  Histories and x, r, p after every call must be bit-identical
+    between the two, for chunked graphs and plain streams, paired and single
+    x updates and the 786k-row grid (x-staged K1, x update in K3), and
+    within the rule of the oracle."""
+    from paper_2602_21897_b200 import _native as N
+    n = int(np.prod(dims))
+    b = orc.rhs_xorshift(n, 11)
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    assert A.x_staged
+    calls = (1, 6, 3, 20)
+    total = sum(calls)
+    out = []
+    for timed in (False, True):
+        S = P.CgSolver(rt, A, total, P.CgOptions(use_graph=graph, iteration_marks=False,
+                                                 x_update=xu), variant=N.TW_CG_MONOLITHIC)
+        assert S.mode()["k1_form"] == N.TW_K1_STAGED
+        if timed:
+            S.enable_kernel_timing(True)
+        S.set_rhs(b)
+        snaps = []
+        for c in calls:
+            S.iterate(c)
+            S.wait()
+            for ptr in S.vectors()[:3]:
+                h = np.empty(n, np.float64)
+                N.check(N.load().tw_memcpy(rt.h, h.ctypes.data_as(N.C.c_void_p), N.C.c_void_p(ptr),
+                                           h.nbytes, None))
+                rt.synchronize()
+                snaps.append(h)
+        out.append((S.history(total), snaps))
+        S.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    for k, (a, c) in enumerate(zip(out[0][1], out[1][1])):
+        assert np.array_equal(a, c), (k // 3, "xrp"[k % 3])
+    want_h, want_x = orc.cg_stencil(*dims, b, total)
+    check_history(out[0][0], want_h)
+    assert np.all(rel_gap(out[0][1][-3], want_x) <= 1e-10)
+
+
 @pytest.mark.parametrize("transport", ["loopback", "peer"])
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_x_update_pairs_across_ranks(orc, transport, nranks):
