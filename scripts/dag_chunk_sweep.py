@@ -1,6 +1,7 @@
 """Persistent-dispatcher chunk sizes (CgOptions.dag_spmv_slices /
 dag_vec_rows) at 128^3 (4/16/64 tiles) and 256^3 (16/64 tiles): us per iteration, best of two
-passes.  0 = the library's choice."""
+passes.  0 = the library's choice.  `big256`: larger SpMV / update chunks at
+256^3 (8 / 16 / 64 tiles)."""
 import os
 import sys
 
@@ -14,6 +15,10 @@ rt = P.Runtime(0)
 s = torch.cuda.ExternalStream(rt.compute_stream)
 CASES = ((128, 300, (4, 16, 64), (0, 54, 72, 90, 108), (0, 8192)),
          (256, 60, (16, 64), (0, 180, 216), (0,)))
+if sys.argv[1:] == ["big256"]:  # SpMV chunks above 12 slices per warp at 256^3
+    CASES = ((256, 60, (8, 16, 64), (0, 288, 432, 648, 864), (0, 65536)),)
+if sys.argv[1:] == ["small256"]:  # ... and below
+    CASES = ((256, 60, (8, 16, 64), (0, 72, 108, 144, 180), (0, 16384)),)
 for nx, K, tiles, slices, vecs in CASES:
     A = P.gen_stencil_matrix(nx, nx, nx, rt=rt)
     b = P.rhs_xorshift(rt, A.n, 7)
