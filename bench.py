@@ -49,9 +49,10 @@ def parse():
     ap.add_argument("--strong", action="store_true", help="nz is the GLOBAL plane count")
     ap.add_argument("--variant", choices=["mono", "tasks"], default="mono")
     ap.add_argument("--tiles", type=int, default=4)
-    ap.add_argument("--dispatch", choices=["auto", "streams", "persistent"], default="auto",
-                    help="tasks variant: one launch per task (streams / graphs) or the persistent "
-                         "device-side dispatcher (across ranks over the NVLink peer transport); "
+    ap.add_argument("--dispatch", choices=["auto", "streams", "persistent", "chain"], default="auto",
+                    help="tasks variant: one launch per task (streams / graphs), the persistent "
+                         "device-side dispatcher (across ranks over the NVLink peer transport) or "
+                         "the programmatic chain (one rank); "
                          "auto = the library's choice on one rank, persistent from 8 tiles per "
                          "GPU across ranks")
     ap.add_argument("--no-graph", action="store_true",
@@ -377,6 +378,14 @@ def time_iterations(torch, S, b, K, W, stream):
     return e0.elapsed_time(e1) / K, S.history(W + K)
 
 
+def dispatch_name(N, m) -> str:
+    """The executor a solver runs (tw_cg_mode)."""
+    if m["dispatch"] == N.TW_DISPATCH_PERSISTENT:
+        return "persistent"
+    chain = m["dispatch"] == N.TW_DISPATCH_CHAIN
+    return ("chain " if chain else "") + ("graph" if m["use_graph"] else "streams")
+
+
 def extra_configs(torch, P, N, rt, A, b, stream, peak):
     """Single-GPU figures of BASELINE configs beside the headline (rank 0,
     N = 1): the reference-API drop-in at the headline size, C2 (128^3
@@ -469,8 +478,7 @@ def extra_configs(torch, P, N, rt, A, b, stream, peak):
         ms, m, _ = solve_rate(A2, b2, K2, variant, opt)
         mono = ms if mono is None else mono
         rows[name] = {"ms_per_iter": ms, "gflops": gflops(A2, ms), "vs_mono_graph": ms / mono,
-                      "dispatch": "persistent" if m["dispatch"] == N.TW_DISPATCH_PERSISTENT
-                      else ("graph" if m["use_graph"] else "streams")}
+                      "dispatch": dispatch_name(N, m)}
     out["c2_128_mono_vs_tasks"] = rows
     del A2, b2
 
@@ -482,8 +490,7 @@ def extra_configs(torch, P, N, rt, A, b, stream, peak):
         ms, m, _ = solve_rate(A, b, 100, variant,
                               opts(tiles=T, use_graph=T == 1, auto_dispatch=T > 1))
         rows[f"T{T}"] = {"blocks_over_8_gpus": 8 * T, "ms_per_iter": ms, "gflops": gflops(A, ms),
-                         "dispatch": "persistent" if m["dispatch"] == N.TW_DISPATCH_PERSISTENT
-                         else ("graph" if m["use_graph"] else "streams")}
+                         "dispatch": dispatch_name(N, m)}
     out["c5_256_per_gpu_share"] = rows
 
     # ---- C4's 1-GPU point: 512^3 (43 GB of sliced ELL), the headline path
@@ -538,8 +545,10 @@ def run_ours(args, dist, rank, world, local):
     persistent = variant == 1 and (args.dispatch == "persistent" or
                                    (args.dispatch == "auto" and multi and args.tiles >= 8))
     use_graph = not args.no_graph and not persistent
+    if args.dispatch == "chain" and (variant != 1 or multi):
+        raise SystemExit("--dispatch chain runs the tasks variant on one rank")
     opt = P.CgOptions(tiles=args.tiles, use_graph=use_graph, iteration_marks=False,
-                      persistent=persistent,
+                      persistent=persistent, chain=args.dispatch == "chain",
                       auto_dispatch=variant == 1 and args.dispatch == "auto" and not multi)
     S = P.CgSolver(rt, A, W + KR, opt, variant=variant)
     want_peer = multi and (args.transport == "peer" or
@@ -806,8 +815,8 @@ def run_ours(args, dist, rank, world, local):
             "iters_per_s": its,
             "config": {**workload_config(args, world), "variant": args.variant,
                        "tiles": 1 if variant == 0 else args.tiles, "cuda_graph": use_graph,
-                       "dispatch": ("persistent" if mode["dispatch"] == N.TW_DISPATCH_PERSISTENT
-                                    else "streams"),
+                       "dispatch": {N.TW_DISPATCH_PERSISTENT: "persistent",
+                                    N.TW_DISPATCH_CHAIN: "chain"}.get(mode["dispatch"], "streams"),
                        "rows_per_gpu": n, "nnz_per_gpu": nnz,
                        "nccl_comm": world > 1 or args.comm,
                        "transport": transport,

@@ -236,7 +236,7 @@ typedef struct tw_cg_options {
     int use_graph;                 /* capture one iteration as a CUDA graph            */
     int iteration_marks;           /* CgOptions::iteration_marks: host poller stamps cg_iter=i */
     double tol;                    /* CgOptions::tol: converged = last residual < tol  */
-    int dispatch;                  /* TW_DISPATCH_AUTO (default) | _STREAMS | _PERSISTENT */
+    int dispatch;                  /* TW_DISPATCH_AUTO (default) | _STREAMS | _PERSISTENT | _CHAIN */
     /* Placement and tuning choices that change no result bit (x_update,
      * l2_keep) or only the dispatcher's chunk-order reduction tree (chunk
      * sizes; within the SURVEY 8(c) rule).  0 = the library's choice. */
@@ -262,8 +262,16 @@ typedef struct tw_cg_options {
 #define TW_DISPATCH_STREAMS 0    /* one launch per task, cudaStreamWaitEvent edges (or graph) */
 #define TW_DISPATCH_PERSISTENT 1 /* one persistent kernel runs the whole DAG: chunked tasks,
                                     device-side dependency counters (tasks variant, 1 rank) */
-#define TW_DISPATCH_AUTO 2       /* persistent for the tasks variant with > 8 tiles on one
-                                    rank (where it is measured faster), else streams */
+#define TW_DISPATCH_AUTO 2       /* tasks variant on one rank, no graph requested: the
+                                    programmatic chain for 2-8 tiles of 50k-3M rows on an
+                                    x-staged matrix, the persistent dispatcher for more / smaller
+                                    tiles, streams otherwise (the measured winners) */
+#define TW_DISPATCH_CHAIN 3      /* the tasks variant's tile kernels in DAG order on ONE
+                                    stream, each launched programmatically: a phase's
+                                    first tile waits for the grids before it
+                                    (griddepcontrol.wait), its other tiles start behind it
+                                    and run side by side (tasks variant, 1 rank, x-staged
+                                    matrix; also under use_graph) */
 
 /* Fills the defaults of CgOptions (cg.hpp:37-45) with the cuda backend. */
 void tw_cg_options_default(tw_cg_options* opt);
@@ -337,7 +345,7 @@ int tw_cg_launches_per_iteration(tw_cg* cg, int* kernels, int* collectives);
 typedef struct tw_cg_mode_t {
     int32_t variant;   /* TW_CG_MONOLITHIC | TW_CG_TASKS                     */
     int32_t tiles;
-    int32_t dispatch;  /* TW_DISPATCH_STREAMS | _PERSISTENT (AUTO resolved)  */
+    int32_t dispatch;  /* TW_DISPATCH_STREAMS | _PERSISTENT | _CHAIN (AUTO resolved) */
     int32_t use_graph;
     int32_t k1_form;   /* TW_K1_*                                            */
     int32_t k1_l2_keep; /* staged K1 stages the x runs with L2 evict_last     */

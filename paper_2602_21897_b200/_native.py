@@ -15,7 +15,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "tw_hpccg.h")
 
 TW_OK, TW_ERR_CONFIG, TW_ERR_CONTRACT, TW_ERR_CUDA, TW_ERR_NCCL = 0, 1, 2, 3, 4
 TW_CG_MONOLITHIC, TW_CG_TASKS = 0, 1
-TW_DISPATCH_STREAMS, TW_DISPATCH_PERSISTENT, TW_DISPATCH_AUTO = 0, 1, 2
+TW_DISPATCH_STREAMS, TW_DISPATCH_PERSISTENT, TW_DISPATCH_AUTO, TW_DISPATCH_CHAIN = 0, 1, 2, 3
 TW_K1_REGISTER, TW_K1_TMA_GATHER, TW_K1_STAGED, TW_K1_STAGED_TABLE = 0, 1, 2, 3
 TW_TRANSPORT_NONE, TW_TRANSPORT_NCCL, TW_TRANSPORT_PEER, TW_TRANSPORT_LOOPBACK = 0, 1, 2, 3
 TW_XUPD_AUTO, TW_XUPD_K2, TW_XUPD_K3, TW_XUPD_K3_PAIRS = 0, 1, 2, 3

@@ -252,7 +252,7 @@ int tile_share(const tw_cg* cg) {
     return std::max(1, std::min(cg->T, cap));
 }
 
-void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph, int chain_role) {
     if (xph != XPH_SINGLE && !cg->x_pairs) contract_error("paired x update not enabled");
     // the iteration's p_old: in the pair buffer for the second of a pair
     double* pl = xph == XPH_PAIR ? cg->p2_local : cg->p_local;
@@ -263,6 +263,9 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
     const int t = nd.tile;
     const int bs = (launch_blocks(cg, true) + share - 1) / share;
     const int bv = (launch_blocks(cg, false) + share - 1) / share;
+    // the programmatic chain (chain_role >= 0): a programmatic launch with the role
+    const bool pdl = chain_role >= 0;
+    const int role = pdl ? chain_role : PDL_DEFAULT;
     switch (nd.kind) {
     case PK_HALO: // the buffer this iteration's SpMV tiles read
         halo_exchange(cg, st, xph == XPH_PAIR ? cg->p2_local : nullptr);
@@ -270,9 +273,11 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
     case PK_SPMV: { // the x-staged K1 when the matrix has it
         const Fin f = cg->tile_fin(cg->pa, t, FIN_ALPHA, cg->tile_tickets);
         if (!launch_spmv_staged(A, pl, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, cg->slot(t), f,
-                                st))
+                                st, pdl, role)) {
+            if (pdl) contract_error("the programmatic chain needs the staged K1");
             launch_spmv(A, pl, cg->Ap, RowRange{cg->t_r0[t], cg->t_r1[t]}, RowRange{0, 0}, true,
                         cg->slot(t), f, bs, st);
+        }
         break;
     }
     case PK_ALPHA: // folded into the last SpMV tile (an empty join node) on one rank
@@ -289,7 +294,8 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
         launch_update_xr(cg->t_r0[t], cg->t_r1[t], x_in_k3(cg) ? nullptr : cg->x, po,
                          cg->r, cg->Ap, cg->sc,
                          ScalarSrc{nullptr, 0}, cg->slot(t),
-                         cg->tile_fin(cg->rrp, t, FIN_BETA, cg->tile_tickets + 1), bv, st);
+                         cg->tile_fin(cg->rrp, t, FIN_BETA, cg->tile_tickets + 1), bv, st, pdl,
+                         role);
         break;
     case PK_BETA: // folded into the last x/r-update tile on one rank
         if (cg->fold_scalars()) break;
@@ -305,15 +311,15 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
         if (xph == XPH_DEFER)
             launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p2_owned, cg->sc,
                             ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
-                            cg->p_owned, false, nullptr);
+                            cg->p_owned, pdl, nullptr, nullptr, role);
         else if (xph == XPH_PAIR)
             launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
                             ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
-                            cg->p2_owned, false, cg->x, cg->p_owned);
+                            cg->p2_owned, pdl, cg->x, cg->p_owned, role);
         else
             launch_update_p(cg->t_r0[t], cg->t_r1[t], cg->r, cg->p_owned, cg->sc,
                             ScalarSrc{nullptr, 0}, cg->slot(t), cg->history, bv, st, nullptr,
-                            nullptr, false, x_in_k3(cg) ? cg->x : nullptr);
+                            nullptr, pdl, x_in_k3(cg) ? cg->x : nullptr, nullptr, role);
         break;
     }
 }
@@ -321,6 +327,7 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph) {
 // All pooled streams (and the comm stream) start after everything already
 // on the compute stream.
 void fork_streams(tw_cg* cg) {
+    if (cg->opt.dispatch == TW_DISPATCH_CHAIN) return; // one stream
     TW_CUDA(cudaEventRecord(cg->fork_ev, cg->ctx->compute));
     for (unsigned i = 0; i < cg->ctx->pool.capacity(); ++i)
         TW_CUDA(cudaStreamWaitEvent(cg->ctx->pool.stream(static_cast<int>(i)), cg->fork_ev, 0));
@@ -328,6 +335,7 @@ void fork_streams(tw_cg* cg) {
 }
 
 void join_streams(tw_cg* cg) {
+    if (cg->opt.dispatch == TW_DISPATCH_CHAIN) return;
     const unsigned C = cg->ctx->pool.capacity();
     for (unsigned i = 0; i <= C; ++i) {
         cudaStream_t st = i < C ? cg->ctx->pool.stream(static_cast<int>(i)) : cg->ctx->comm;
@@ -338,7 +346,35 @@ void join_streams(tw_cg* cg) {
 
 // One block-task iteration: physical nodes in topological order, each on its
 // stream after waiting for predecessors on other streams.
+// TW_DISPATCH_CHAIN: the iteration's physical nodes in DAG order on the
+// compute stream, every tile kernel launched programmatically with its role
+// in its phase (PdlRole): the first tile waits for every grid before it,
+// the later ones start behind it without a wait, the last lets the next
+// phase's first tile launch after its main loop.  alpha / beta_res combine
+// kernels (more tiles than the fold takes) launch plainly.  Stream order is
+// stronger than the DAG's edges (a p tile -> only its band's SpMV tiles)
+// and replaces them: no events, one graph branch.
+static void enqueue_tasks_chain(tw_cg* cg, int xph) {
+    cudaStream_t s = cg->ctx->compute;
+    const size_t m = cg->nodes.size();
+    for (size_t j = 0; j < m; ++j) {
+        const PNode& nd = cg->nodes[j];
+        const bool tile = nd.kind == PK_SPMV || nd.kind == PK_UPD || nd.kind == PK_UPDP;
+        int role = -1;
+        if (tile) {
+            const bool first = j == 0 || cg->nodes[j - 1].kind != nd.kind;
+            const bool last = j + 1 == m || cg->nodes[j + 1].kind != nd.kind;
+            role = first ? (last ? PDL_GATE_LAST : PDL_GATE) : (last ? PDL_LAST : PDL_INNER);
+        }
+        launch_node(cg, nd, s, xph, role);
+    }
+}
+
 void enqueue_tasks(tw_cg* cg, int parity, bool first, int xph) {
+    if (cg->opt.dispatch == TW_DISPATCH_CHAIN) {
+        enqueue_tasks_chain(cg, xph);
+        return;
+    }
     for (size_t j = 0; j < cg->nodes.size(); ++j) {
         const PNode& nd = cg->nodes[j];
         cudaStream_t st = cg->node_stream(nd);
@@ -484,10 +520,20 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
                 cg->opt.tiles > 1 &&
                 (A->cols16 ? rows_per_tile < 400000 || (cg->opt.tiles >= 8 && rows_per_tile < 3000000)
                            : cg->opt.tiles > 8);
-            cg->opt.dispatch = cg->opt.variant == TW_CG_TASKS && small && !ctx->nccl_comm &&
-                                       !ctx->emulated && fits && !cg->opt.use_graph
-                                   ? TW_DISPATCH_PERSISTENT
-                                   : TW_DISPATCH_STREAMS;
+            // the programmatic chain for 2 to 8 tiles of 50k to 3M rows on an
+            // x-staged matrix (128^3: 2 / 4 / 8 tiles 118.5 / 119.0 / 128.5 us
+            // against streams 124.2 / 126.3 and the dispatcher's 135.4 at 8;
+            // 96^3, 4 tiles: 61.5 against the dispatcher's 82.5; 256^3, 8
+            // tiles: 856 against 875; below ~50k rows per tile (64^3, 8
+            // tiles) the dispatcher's one launch wins, from ~4M (256^3, 2 / 4
+            // tiles) the branch-parallel streams; profiles/r02_ab_chain.md)
+            const bool chain = A->cols16 && cg->opt.tiles > 1 && cg->opt.tiles <= 8 &&
+                               rows_per_tile >= 50000 && rows_per_tile < 3000000;
+            const bool one_rank = cg->opt.variant == TW_CG_TASKS && !ctx->nccl_comm &&
+                                  !ctx->emulated && !cg->opt.use_graph;
+            cg->opt.dispatch = one_rank && chain            ? TW_DISPATCH_CHAIN
+                               : one_rank && small && fits ? TW_DISPATCH_PERSISTENT
+                                                           : TW_DISPATCH_STREAMS;
         }
         if (cg->opt.dispatch == TW_DISPATCH_PERSISTENT) {
             if (cg->opt.variant != TW_CG_TASKS)
@@ -496,6 +542,10 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
             if (dag_smem_bytes(A->info.max_width, A->cols16 != nullptr, &sb, &vb, &cb) > 225 * 1024)
                 config_error("matrix rows too wide for the dispatcher's shared-memory stages");
             if (cg->opt.use_graph) config_error("the persistent dispatcher is one launch; no graph");
+        } else if (cg->opt.dispatch == TW_DISPATCH_CHAIN) {
+            if (cg->opt.variant != TW_CG_TASKS) config_error("the programmatic chain runs the tasks variant");
+            if (ctx->nccl_comm || ctx->emulated) config_error("the programmatic chain runs on one rank");
+            if (!A->cols16) config_error("the programmatic chain needs the x-staged matrix form");
         } else if (cg->opt.dispatch != TW_DISPATCH_STREAMS) {
             config_error("unknown dispatch mode");
         }

@@ -166,7 +166,8 @@ enum { XPH_SINGLE = 0, XPH_DEFER = 1, XPH_PAIR = 2 };
 int x_phase(const tw_cg* cg, int i, int k);
 void enqueue_mono(tw_cg* cg, int xph = XPH_SINGLE);
 int tile_share(const tw_cg* cg);
-void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph = XPH_SINGLE);
+void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph = XPH_SINGLE,
+                 int chain_role = -1);
 void fork_streams(tw_cg* cg);
 void join_streams(tw_cg* cg);
 void enqueue_tasks(tw_cg* cg, int parity, bool first, int xph = XPH_SINGLE);

@@ -74,6 +74,23 @@ __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Roles of a tile kernel in the tasks variant's programmatic chain (one
+// stream, every tile kernel launched programmatically; tw_cg.cpp
+// enqueue_tasks_chain), PdlRole in tw_internal.h.  A griddepcontrol.wait
+// returns once every grid before it in the stream has completed (completion
+// is in stream order: scripts/pdl_transitive.cu), so only a phase's first
+// tile waits; it lets the next tile launch after its wait, so the later
+// tiles start after the previous phase has completed and need no wait; the
+// last tile lets the next phase's first tile launch only after its main loop
+// (that tile's blocks then wait beside the phase's tail, not beside its bulk).
+__device__ __forceinline__ void pdl_role_entry(int role) {
+    if (role == PDL_DEFAULT || role == PDL_INNER) pdl_launch_dependents();
+    if (role == PDL_DEFAULT || role == PDL_GATE || role == PDL_GATE_LAST) pdl_wait();
+    if (role == PDL_GATE) pdl_launch_dependents();
+}
+__device__ __forceinline__ void pdl_role_exit(int role) {
+    if (role == PDL_LAST || role == PDL_GATE_LAST) pdl_launch_dependents();
+}
 
 // ------------------------------------------------ peer transport primitives
 

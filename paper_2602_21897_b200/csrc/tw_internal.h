@@ -15,6 +15,18 @@
 
 namespace tw {
 
+// Where a tile kernel waits for the grids before it and where it lets the
+// next one launch (programmatic dependent launch; tw_device.cuh
+// pdl_role_entry / pdl_role_exit).  PDL_DEFAULT: trigger at entry, wait
+// before the inputs -- the monolithic chain's K1 and every plain launch.
+enum PdlRole : int {
+    PDL_DEFAULT = 0,
+    PDL_GATE = 1,      // a phase's first tile: wait, then trigger
+    PDL_INNER = 2,     // a later tile: trigger at entry, no wait (its gate waited)
+    PDL_LAST = 3,      // the phase's last tile: no wait, trigger after the main loop
+    PDL_GATE_LAST = 4, // the phase's only tile: wait, trigger after the main loop
+};
+
 // Exceptions mapped 1:1 onto the ABI status codes at the extern "C" boundary
 // (mirrors the reference's ConfigError / ContractViolation, types.hpp:23-33).
 struct Error : std::runtime_error {
@@ -257,7 +269,7 @@ void launch_spmv(const EllView& A, const double* x, double* y, RowRange a, RowRa
 // r only (K3 applies the x update, launch_update_p's x).
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc alpha_src, RedScratch rs,
-                      Fin fin, int blocks, cudaStream_t s, bool pdl = false);
+                      Fin fin, int blocks, cudaStream_t s, bool pdl = false, int role = PDL_DEFAULT);
 // K3: p = r + beta p (beta from sc or recomputed from partials; with x,
 // also x += alpha p_old, alpha = sc->alpha; with
 // partials, the last block also commits rtrans/history/iter).
@@ -267,7 +279,7 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
                      ScalarSrc beta_src, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links = nullptr,
                      const double* psrc = nullptr, bool pdl = false, double* x = nullptr,
-                     const double* p0 = nullptr);
+                     const double* p0 = nullptr, int role = PDL_DEFAULT);
 // (with p0: the K3 of an x-update pair's second iteration, p = r + beta psrc,
 // x = (x + alpha_prev p0) + alpha psrc; p may alias p0)
 // K1 of the peer transport as one launch (interior, then the two boundary
@@ -327,11 +339,12 @@ void launch_csr_runs(const EllView& A, int32_t* runs, uint16_t* cols16, unsigned
 bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange ra, RowRange rb0,
                         RowRange rb1, bool split, RedScratch rs, Fin fin, cudaStream_t s,
                         const unsigned long long* wait_flags = nullptr, int nwait = 0,
-                        bool pdl = false);
+                        bool pdl = false, int role = PDL_DEFAULT);
 inline bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange rows,
-                               RedScratch rs, Fin fin, cudaStream_t s, bool pdl = false) {
+                               RedScratch rs, Fin fin, cudaStream_t s, bool pdl = false,
+                               int role = PDL_DEFAULT) {
     return launch_spmv_staged(A, x, y, rows, RowRange{0, 0}, RowRange{0, 0}, false, rs, fin, s,
-                              nullptr, 0, pdl);
+                              nullptr, 0, pdl, role);
 }
 int spmv_staged_smem_bytes(int max_width);
 // Checked build only: every stored column in [-1, x_len), padding only

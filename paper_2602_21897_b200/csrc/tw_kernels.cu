@@ -397,7 +397,7 @@ __device__ __forceinline__ void staged_spmv_body(
     GridPos g, const EllView& A, const double* __restrict__ x, double* __restrict__ y, RowRange ra,
     RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes, int c16_bytes, RedScratch rs,
     const Fin& fin, const unsigned long long* wait_flags, int nwait, unsigned char* smem,
-    uint64_t* bars, int* stage_ws, uint32_t& phase) {
+    uint64_t* bars, int* stage_ws, uint32_t& phase, int role = PDL_DEFAULT) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* stage = smem + static_cast<size_t>(warp) * stage_bytes;
     uint64_t* bar = bars + warp;
@@ -471,7 +471,10 @@ __device__ __forceinline__ void staged_spmv_body(
     int64_t s = mine > 0 ? locate(0, rr) : 0;
     if (lane == 0 && mine > 0) issue_block(s);
     __syncwarp();
-    if (PDL) pdl_wait();
+    if (PDL) {
+        if (role == PDL_DEFAULT || role == PDL_GATE || role == PDL_GATE_LAST) pdl_wait();
+        if (role == PDL_GATE) pdl_launch_dependents();
+    }
     if (lane == 0 && mine > 0) issue_x(0, s);
     __syncwarp();
     double part_a = 0.0, part_b = 0.0;
@@ -506,6 +509,7 @@ __device__ __forceinline__ void staged_spmv_body(
         }
         __syncwarp();
     }
+    if (PDL) pdl_role_exit(role);
     if (SPLIT) grid_reduce2_finalize(part_a, part_b, rs, fin, g);
     else grid_reduce_finalize(part_b, rs, fin, g);
 }
@@ -515,19 +519,19 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 1)
 spmv_tma_staged_kernel(EllView A, const double* __restrict__ x, double* __restrict__ y,
                        RowRange ra, RowRange rb0, RowRange rb1, int stage_bytes, int val_bytes,
                        int c16_bytes, RedScratch rs, Fin fin, const unsigned long long* wait_flags,
-                       int nwait) {
+                       int nwait, int role) {
     TW_TL(1, ra.r1 > ra.r0 ? ra.r0 : rb0.r0);
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t bars[kTmaWarps];
     __shared__ int stage_w[kTmaWarps];
-    pdl_launch_dependents();
+    if (role == PDL_DEFAULT || role == PDL_INNER) pdl_launch_dependents();
     if ((threadIdx.x & 31) == 0) mbar_init(&bars[threadIdx.x >> 5], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
     uint32_t phase = 0;
     staged_spmv_body<SPLIT, kTmaWarps, true, KEEP>(launch_grid(), A, x, y, ra, rb0, rb1, stage_bytes,
                                              val_bytes, c16_bytes, rs, fin, wait_flags, nwait, smem,
-                                             bars, stage_w, phase);
+                                             bars, stage_w, phase, role);
 }
 
 // --------------------------------------------------------- K2 / K3 / K4 streams
@@ -577,9 +581,8 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
                                                double* __restrict__ x, const double* __restrict__ p,
                                                double* __restrict__ r, const double* __restrict__ Ap,
                                                CgScalars* sc, ScalarSrc asrc, RedScratch rs,
-                                               const Fin& fin) {
-    pdl_launch_dependents();
-    pdl_wait(); // Ap and alpha come from K1
+                                               const Fin& fin, int role = PDL_DEFAULT) {
+    pdl_role_entry(role); // Ap and alpha come from K1
     double alpha;
     if (asrc.flags) block_wait_flags(asrc.flags, asrc.count, stamp_of(sc, 0));
     if (asrc.count > 0)
@@ -639,6 +642,7 @@ __device__ __forceinline__ void update_xr_rows(GridPos g, int64_t i0, int64_t i1
             }
         }
     });
+    pdl_role_exit(role);
     grid_reduce_finalize(part, rs, fin, g);
 }
 
@@ -646,9 +650,9 @@ template <bool WX>
 __global__ void __launch_bounds__(kThreads)
 update_xr_kernel(int64_t i0, int64_t i1, double* __restrict__ x, const double* __restrict__ p,
                  double* __restrict__ r, const double* __restrict__ Ap, CgScalars* sc,
-                 ScalarSrc asrc, RedScratch rs, Fin fin) {
+                 ScalarSrc asrc, RedScratch rs, Fin fin, int role) {
     TW_TL(2, i0);
-    update_xr_rows<WX>(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin);
+    update_xr_rows<WX>(launch_grid(), i0, i1, x, p, r, Ap, sc, asrc, rs, fin, role);
 }
 
 // K3's streaming loop over [a0, b0): p = r + beta psrc, two pairs per
@@ -746,14 +750,14 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
                                               CgScalars* sc, ScalarSrc bsrc, RedScratch rs,
                                               double* history, const PeerLinks* links_,
                                               const double* __restrict__ psrc,
-                                              double* __restrict__ x, const double* p0) {
+                                              double* __restrict__ x, const double* p0,
+                                              int role = PDL_DEFAULT) {
     // psrc: p_old, == p in place (each element is read, then written, by the
     // same thread, so the restrict-qualified aliasing is never observable);
     // p0 may alias p the same way (the pair writes p_k+2 over p_k)
     constexpr bool WX = XU != 0;
     const PeerLinks* links = PEER ? links_ : nullptr;
-    pdl_launch_dependents();
-    pdl_wait(); // r and beta come from K2
+    pdl_role_entry(role); // r and beta come from K2
     double beta, rr = 0.0;
     const double alpha = WX ? sc->alpha : 0.0; // this iteration's (K1 / K2 left it there)
     const double alpha0 = XU == 2 ? sc->alpha_prev : 0.0;
@@ -795,6 +799,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
     };
     if (!links) {
         stream(i0, i1);
+        pdl_role_exit(role);
         return;
     }
     // Fused halo (peer transport): the first / last owned plane of p also
@@ -842,6 +847,7 @@ __device__ __forceinline__ void update_p_rows(GridPos g, int64_t i0, int64_t i1,
         }
     }
     stream(lo_end, hi_beg);
+    pdl_role_exit(role);
 }
 
 template <bool PEER, int XU>
@@ -849,9 +855,10 @@ __global__ void __launch_bounds__(kThreads)
 update_p_kernel(int64_t i0, int64_t i1, const double* __restrict__ r, double* __restrict__ p,
                 CgScalars* sc, ScalarSrc bsrc, RedScratch rs, double* history,
                 const PeerLinks* links, const double* __restrict__ psrc, double* __restrict__ x,
-                const double* p0) {
+                const double* p0, int role) {
     TW_TL(3, i0);
-    update_p_rows<PEER, XU>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x, p0);
+    update_p_rows<PEER, XU>(launch_grid(), i0, i1, r, p, sc, bsrc, rs, history, links, psrc, x, p0,
+                            role);
 }
 
 // ------------------------------------------- concurrent rank group (1 GPU)
@@ -1209,7 +1216,7 @@ static bool staged_attr(int smem) {
 
 bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange ra, RowRange rb0,
                         RowRange rb1, bool split, RedScratch rs, Fin fin, cudaStream_t s,
-                        const unsigned long long* wait_flags, int nwait, bool pdl) {
+                        const unsigned long long* wait_flags, int nwait, bool pdl, int role) {
     if (!A.cols16 || A.max_width <= 0 || A.tma_blocks <= 0) return false;
     int vb, cb;
     const int stage = staged_stage_bytes(A.max_width, &vb, &cb);
@@ -1236,7 +1243,7 @@ bool launch_spmv_staged(const EllView& A, const double* x, double* y, RowRange r
                          : (keep ? spmv_tma_staged_kernel<false, true>
                                  : spmv_tma_staged_kernel<false, false>);
     launch_k(kern, dim3(g), dim3(kTmaWarps * 32), smem, s, pdl, A, x, y, ra, rb0, rb1, stage, vb, cb,
-             rs, fin, wait_flags, nwait);
+             rs, fin, wait_flags, nwait, role);
     return true;
 }
 
@@ -1247,21 +1254,21 @@ int spmv_staged_smem_bytes(int max_width) {
 
 void launch_update_xr(int64_t i0, int64_t i1, double* x, const double* p, double* r,
                       const double* Ap, CgScalars* sc, ScalarSrc asrc, RedScratch rs, Fin fin,
-                      int blocks, cudaStream_t s, bool pdl) {
+                      int blocks, cudaStream_t s, bool pdl, int role) {
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks);
     if (x)
         launch_k(update_xr_kernel<true>, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap, sc,
-                 asrc, rs, fin);
+                 asrc, rs, fin, role);
     else
         launch_k(update_xr_kernel<false>, dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, x, p, r, Ap,
-                 sc, asrc, rs, fin);
+                 sc, asrc, rs, fin, role);
     TW_CUDA(cudaGetLastError());
 }
 
 void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScalars* sc,
                      ScalarSrc bsrc, RedScratch rs, double* history, int blocks,
                      cudaStream_t s, const PeerLinks* links, const double* psrc, bool pdl,
-                     double* x, const double* p0) {
+                     double* x, const double* p0, int role) {
     // grid: at most one resident wave of this instantiation (a partial
     // second wave of a grid-stride loop would double the tail)
     const bool peer = links != nullptr || bsrc.flags != nullptr;
@@ -1289,7 +1296,7 @@ void launch_update_p(int64_t i0, int64_t i1, const double* r, double* p, CgScala
     const int g = clamp_blocks((i1 - i0 + 1) / 2 + 1, blocks < wave ? blocks : wave);
     if (x && !sc) throw Error(TW_ERR_CONTRACT, "the fused x update needs the solver's scalars");
     launch_k(kerns[which], dim3(g), dim3(kThreads), 0, s, pdl, i0, i1, r, p, sc, bsrc, rs, history,
-             links, psrc ? psrc : p, x, p0);
+             links, psrc ? psrc : p, x, p0, role);
     TW_CUDA(cudaGetLastError());
 }
 

@@ -535,7 +535,8 @@ class CgOptions:
     tol: float = 0.0
     use_graph: bool = False
     persistent: bool = False  # tasks variant: one persistent kernel runs the whole DAG
-    auto_dispatch: bool = False  # TW_DISPATCH_AUTO: persistent for > 8 tiles on one rank
+    auto_dispatch: bool = False  # TW_DISPATCH_AUTO: chain / persistent / streams, the measured winner
+    chain: bool = False  # TW_DISPATCH_CHAIN: tile kernels on one stream, programmatic launches
     # placement / tuning (no result bit changes, except the dispatcher's chunk
     # sizes, which set its chunk-order reduction tree): None = the library's choice
     x_update: str | None = None   # "k2" | "k3" | "k3_pairs": where x += alpha p runs
@@ -553,8 +554,11 @@ class CgOptions:
         o.use_graph = 1 if self.use_graph else 0
         o.iteration_marks = 1 if self.iteration_marks else 0
         o.tol = float(self.tol)
+        if self.persistent + self.auto_dispatch + self.chain > 1:
+            raise ConfigError("persistent, auto_dispatch and chain are exclusive")
         o.dispatch = (N.TW_DISPATCH_PERSISTENT if self.persistent else
-                      N.TW_DISPATCH_AUTO if self.auto_dispatch else N.TW_DISPATCH_STREAMS)
+                      N.TW_DISPATCH_AUTO if self.auto_dispatch else
+                      N.TW_DISPATCH_CHAIN if self.chain else N.TW_DISPATCH_STREAMS)
         o.x_update = {None: N.TW_XUPD_AUTO, "k2": N.TW_XUPD_K2, "k3": N.TW_XUPD_K3,
                       "k3_pairs": N.TW_XUPD_K3_PAIRS}[self.x_update]
         o.l2_keep = (N.TW_L2KEEP_AUTO if self.l2_keep is None else

@@ -101,3 +101,4 @@ def probe(name, variant, **kw):
 probe("mono graph", 0, tiles=1, use_graph=True)
 probe("T4 graphK", 1, tiles=4, use_graph=True)
 probe("T4 streams", 1, tiles=4)
+probe("T4 chain graphK", 1, tiles=4, use_graph=True, chain=True)

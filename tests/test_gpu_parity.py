@@ -1289,6 +1289,52 @@ def test_k1_programmatic_launch_bit_identical(rt, orc, dims, xu, graph):
     assert np.all(rel_gap(out[0][1][-3], want_x) <= 1e-10)
 
 
+@pytest.mark.parametrize("dims,T", [((64, 40, 36), 1), ((64, 40, 36), 2), ((64, 40, 36), 3),
+                                    ((64, 40, 36), 4), ((64, 40, 36), 7), ((64, 40, 36), 16),
+                                    ((128, 64, 96), 4)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_tasks_programmatic_chain(rt, orc, dims, T, graph):
+    """TW_DISPATCH_CHAIN: the block-task DAG's tile kernels in DAG order on
+    one stream, each launched programmatically (a phase's first tile waits
+    for every grid before it, the others start behind it without a wait).
+    Histories and x bit-identical to the stream / event executor (same tile
+    kernels, same tile partials and alpha / beta_res orders) for calls of
+    odd and even lengths, with and without graphs, single and paired x
+    updates (the 786k-row grid), and within the rule of the oracle."""
+    from paper_2602_21897_b200 import _native as N
+    n = int(np.prod(dims))
+    b = orc.rhs_xorshift(n, 13)
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    calls = (1, 4, 3, 16)
+    total = sum(calls)
+    out = []
+    for chain in (False, True):
+        S = P.CgSolver(rt, A, total, P.CgOptions(tiles=T, use_graph=graph, iteration_marks=False,
+                                                 chain=chain), variant=N.TW_CG_TASKS)
+        assert S.mode()["dispatch"] == (N.TW_DISPATCH_CHAIN if chain else N.TW_DISPATCH_STREAMS)
+        S.set_rhs(b)
+        for c in calls:
+            S.iterate(c)
+        S.wait()
+        out.append((S.history(total), S.solution()))
+        S.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    want_h, want_x = orc.cg_stencil(*dims, b, total)
+    check_history(out[1][0], want_h)
+    assert np.all(rel_gap(out[1][1], want_x) <= 1e-10)
+
+
+def test_tasks_programmatic_chain_refusals(rt):
+    """The chain runs the tasks variant (on one rank, over an x-staged matrix)."""
+    from paper_2602_21897_b200 import _native as N
+    A = P.gen_stencil_matrix(64, 8, 8, rt=rt)
+    with pytest.raises(P.ConfigError):
+        P.CgSolver(rt, A, 4, P.CgOptions(tiles=1, chain=True), variant=N.TW_CG_MONOLITHIC)
+    with pytest.raises(P.ConfigError):
+        P.CgOptions(tiles=2, chain=True, persistent=True).to_c(N.TW_CG_TASKS)
+
+
 @pytest.mark.parametrize("transport", ["loopback", "peer"])
 @pytest.mark.parametrize("nranks", [2, 3])
 def test_x_update_pairs_across_ranks(orc, transport, nranks):
