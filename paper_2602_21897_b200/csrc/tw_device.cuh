@@ -88,8 +88,11 @@ __device__ __forceinline__ void pdl_role_entry(int role) {
     if (role == PDL_DEFAULT || role == PDL_GATE || role == PDL_GATE_LAST) pdl_wait();
     if (role == PDL_GATE) pdl_launch_dependents();
 }
+#ifndef TW_CHAIN_EARLY_NEXT
+#define TW_CHAIN_EARLY_NEXT 1 // 0: the last tile triggers only by completing (A/B)
+#endif
 __device__ __forceinline__ void pdl_role_exit(int role) {
-    if (role == PDL_LAST || role == PDL_GATE_LAST) pdl_launch_dependents();
+    if (TW_CHAIN_EARLY_NEXT && (role == PDL_LAST || role == PDL_GATE_LAST)) pdl_launch_dependents();
 }
 
 // ------------------------------------------------ peer transport primitives

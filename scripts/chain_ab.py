@@ -37,17 +37,21 @@ def rate(A, b, K, variant, **kw):
 CASES = ((128, 400, (2, 4, 8, 16)), (256, 60, (2, 4, 8, 16, 32, 64)))
 if sys.argv[1:] == ["small"]:  # the lower end of the chain's range
     CASES = ((64, 1500, (2, 4, 8)), (96, 800, (2, 4, 8)))
+tag = os.path.basename(os.environ.get("TW_HPCCG_LIB", "default"))
 for nx, K, tiles in CASES:
     A = P.gen_stencil_matrix(nx, nx, nx, rt=rt)
     b = P.rhs_xorshift(rt, A.n, 7)
     for rnd in range(2):
         out = [f"mono {rate(A, b, K, 0, tiles=1, use_graph=True):.1f}"]
         for T in tiles:
+            if os.environ.get("CHAIN_ONLY"):  # library A/Bs of the chain itself
+                out.append(f"T{T}: chain {rate(A, b, K, 1, tiles=T, chain=True):.1f}")
+                continue
             row = [f"chain {rate(A, b, K, 1, tiles=T, chain=True):.1f}",
                    f"chainK {rate(A, b, K, 1, tiles=T, chain=True, use_graph=True):.1f}",
                    f"graphK {rate(A, b, K, 1, tiles=T, use_graph=True):.1f}" if T <= 16 else "",
                    f"streams {rate(A, b, K, 1, tiles=T):.1f}" if T <= 8 else "",
                    f"persistent {rate(A, b, K, 1, tiles=T, persistent=True):.1f}" if T >= 4 else ""]
             out.append(f"T{T}: " + " ".join(x for x in row if x))
-        print(f"{nx}^3 round {rnd}: " + " | ".join(out), flush=True)
+        print(f"{tag} {nx}^3 round {rnd}: " + " | ".join(out), flush=True)
     del A
