@@ -263,7 +263,7 @@ typedef struct tw_cg_options {
 #define TW_DISPATCH_PERSISTENT 1 /* one persistent kernel runs the whole DAG: chunked tasks,
                                     device-side dependency counters (tasks variant, 1 rank) */
 #define TW_DISPATCH_AUTO 2       /* tasks variant on one rank, no graph requested: the
-                                    programmatic chain for 2-8 tiles of 50k-3M rows on an
+                                    programmatic chain for 2-8 tiles of >= 50k rows on an
                                     x-staged matrix, the persistent dispatcher for more / smaller
                                     tiles, streams otherwise (the measured winners) */
 #define TW_DISPATCH_CHAIN 3      /* the tasks variant's tile kernels in DAG order on ONE

@@ -264,8 +264,11 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph, int chain
     const int bs = (launch_blocks(cg, true) + share - 1) / share;
     const int bv = (launch_blocks(cg, false) + share - 1) / share;
     // the programmatic chain (chain_role >= 0): a programmatic launch with the role
-    const bool pdl = chain_role >= 0;
-    const int role = pdl ? chain_role : PDL_DEFAULT;
+    // (large tiles: the x/r phase's gate launched plainly, after the SpMV
+    // tiles have completed; its role still lets the later tiles launch)
+    const bool gate = chain_role == PDL_GATE || chain_role == PDL_GATE_LAST;
+    const bool pdl = chain_role >= 0 && !(gate && nd.kind == PK_UPD && cg->chain_plain_upd);
+    const int role = chain_role >= 0 ? chain_role : PDL_DEFAULT;
     switch (nd.kind) {
     case PK_HALO: // the buffer this iteration's SpMV tiles read
         halo_exchange(cg, st, xph == XPH_PAIR ? cg->p2_local : nullptr);
@@ -520,15 +523,15 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
                 cg->opt.tiles > 1 &&
                 (A->cols16 ? rows_per_tile < 400000 || (cg->opt.tiles >= 8 && rows_per_tile < 3000000)
                            : cg->opt.tiles > 8);
-            // the programmatic chain for 2 to 8 tiles of 50k to 3M rows on an
-            // x-staged matrix (128^3: 2 / 4 / 8 tiles 118.5 / 119.0 / 128.5 us
+            // the programmatic chain for 2 to 8 tiles of 50k rows and more on
+            // an x-staged matrix (128^3: 2 / 4 / 8 tiles 118.5 / 119.0 / 128.5 us
             // against streams 124.2 / 126.3 and the dispatcher's 135.4 at 8;
-            // 96^3, 4 tiles: 61.5 against the dispatcher's 82.5; 256^3, 8
-            // tiles: 856 against 875; below ~50k rows per tile (64^3, 8
-            // tiles) the dispatcher's one launch wins, from ~4M (256^3, 2 / 4
-            // tiles) the branch-parallel streams; profiles/r02_ab_chain.md)
+            // 96^3, 4 tiles: 61.5 against the dispatcher's 82.5; 256^3, 2 / 4
+            // / 8 tiles 853 / 853 / 861 against streams 858 / 858 and the
+            // dispatcher's 875 at 8; below ~50k rows per tile (64^3, 8 tiles)
+            // the dispatcher's one launch wins; profiles/r02_ab_chain.md)
             const bool chain = A->cols16 && cg->opt.tiles > 1 && cg->opt.tiles <= 8 &&
-                               rows_per_tile >= 50000 && rows_per_tile < 3000000;
+                               rows_per_tile >= 50000;
             const bool one_rank = cg->opt.variant == TW_CG_TASKS && !ctx->nccl_comm &&
                                   !ctx->emulated && !cg->opt.use_graph;
             cg->opt.dispatch = one_rank && chain            ? TW_DISPATCH_CHAIN
@@ -562,6 +565,8 @@ tw_cg* create_cg(tw_ctx* ctx, const tw_ell* A, const tw_cg_options* o, int max_i
         cg->max_iters = max_iters;
         const tw_ell_info_t& in = A->info;
         cg->n = in.n_rows;
+        cg->chain_plain_upd = cg->opt.dispatch == TW_DISPATCH_CHAIN &&
+                              cg->n / std::max(cg->T, 1) >= 3000000;
         cg->x_len = in.x_len;
         cg->diag_shift = A->diag_shift;
         if (cg->dist) {

@@ -75,6 +75,10 @@ struct tw_cg {
     std::map<int, cudaGraphExec_t> chunk_graphs; // up to kGraphChunk iterations, untimed
     bool x_k3 = false; // x += alpha p_old in K3, not K2 (decided at creation)
     bool x_pairs = false; // ... once per pair of iterations (one rank; monolithic, tasks on streams)
+    // programmatic chain: its x/r phase's first tile launched plainly (tiles of
+    // 3M rows and more, where a programmatic x/r gate behind the SpMV tiles
+    // costs 2 %; profiles/r02_ab_chain.md)
+    bool chain_plain_upd = false;
     int enqueued = 0;
     // per-kernel timing (monolithic, no graph): 4 events per timed iteration
     bool timing = false;

@@ -1291,7 +1291,7 @@ def test_k1_programmatic_launch_bit_identical(rt, orc, dims, xu, graph):
 
 @pytest.mark.parametrize("dims,T", [((64, 40, 36), 1), ((64, 40, 36), 2), ((64, 40, 36), 3),
                                     ((64, 40, 36), 4), ((64, 40, 36), 7), ((64, 40, 36), 16),
-                                    ((128, 64, 96), 4)])
+                                    ((128, 64, 96), 4), ((256, 256, 96), 2)])
 @pytest.mark.parametrize("graph", [False, True])
 def test_tasks_programmatic_chain(rt, orc, dims, T, graph):
     """TW_DISPATCH_CHAIN: the block-task DAG's tile kernels in DAG order on
@@ -1300,7 +1300,9 @@ def test_tasks_programmatic_chain(rt, orc, dims, T, graph):
     Histories and x bit-identical to the stream / event executor (same tile
     kernels, same tile partials and alpha / beta_res orders) for calls of
     odd and even lengths, with and without graphs, single and paired x
-    updates (the 786k-row grid), and within the rule of the oracle."""
+    updates (the 786k-row grid), the plainly launched x/r gate of tiles of
+    3M rows and more (256 x 256 x 96 in 2 tiles), and within the rule of
+    the oracle."""
     from paper_2602_21897_b200 import _native as N
     n = int(np.prod(dims))
     b = orc.rhs_xorshift(n, 13)
@@ -1320,7 +1322,7 @@ def test_tasks_programmatic_chain(rt, orc, dims, T, graph):
         S.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
-    want_h, want_x = orc.cg_stencil(*dims, b, total)
+    want_h, want_x = orc.cg_stencil_mt(*dims, b, total)
     check_history(out[1][0], want_h)
     assert np.all(rel_gap(out[1][1], want_x) <= 1e-10)
 
