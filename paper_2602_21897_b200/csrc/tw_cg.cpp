@@ -1090,7 +1090,7 @@ void iterate(tw_cg* cg, int k) {
             // cg_iter=i mark (cg.cpp:307-308): the poller stamps the host time
             // at which it first sees this iteration complete.
             cudaStream_t ms = s;
-            if (tasks && !cg->opt.use_graph) {
+            if (tasks && !cg->opt.use_graph && cg->opt.dispatch != TW_DISPATCH_CHAIN) {
                 for (const PNode& nd : cg->nodes)
                     if (nd.kind == PK_BETA) ms = cg->node_stream(nd);
             }

@@ -1327,6 +1327,32 @@ def test_tasks_programmatic_chain(rt, orc, dims, T, graph):
     assert np.all(rel_gap(out[1][1], want_x) <= 1e-10)
 
 
+def test_tasks_programmatic_chain_marks(rt, orc):
+    """Host cg_iter marks and device iteration times under the chain (all
+    its work on the compute stream, where the marks are recorded): positive,
+    non-decreasing marks, positive iteration times, and the automatic
+    dispatch picking the chain for 4 tiles of 50k+ rows."""
+    from paper_2602_21897_b200 import _native as N
+    dims = (64, 48, 72)  # 221k rows: 4 tiles of 55k
+    A = P.gen_stencil_matrix(*dims, rt=rt)
+    b = orc.rhs_xorshift(A.n, 5)
+    want_h, want_x = orc.cg_stencil(*dims, b, 30)
+    s = P.CgSolver(rt, A, 30, P.CgOptions(tiles=4, auto_dispatch=True, iteration_marks=True),
+                   variant=N.TW_CG_TASKS)
+    assert s.mode()["dispatch"] == N.TW_DISPATCH_CHAIN
+    s.set_rhs(b)
+    s.iterate(12)
+    s.iterate(18)
+    s.wait()
+    check_history(s.history(30), want_h)
+    assert np.all(rel_gap(s.solution(), want_x) <= 1e-10)
+    m = s.marks(30)
+    assert np.all(m > 0) and np.all(np.diff(m) >= 0)
+    t = s.iteration_times(30)
+    assert np.all(t > 0)
+    s.close()
+
+
 def test_tasks_programmatic_chain_refusals(rt):
     """The chain runs the tasks variant (on one rank, over an x-staged matrix)."""
     from paper_2602_21897_b200 import _native as N
