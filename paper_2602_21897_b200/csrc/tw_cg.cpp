@@ -259,7 +259,10 @@ void launch_node(tw_cg* cg, const PNode& nd, cudaStream_t st, int xph, int chain
     double* po = xph == XPH_PAIR ? cg->p2_owned : cg->p_owned;
     const int share = tile_share(cg);
     EllView A = cg->view();
-    A.tma_blocks = (A.tma_blocks + share - 1) / share;
+    // rounded down: the side-by-side tiles' one-CTA-per-SM SpMV grids must
+    // fit on the SMs together (3 tiles: 3 x 50 = 150 > 148 blocks would leave
+    // one tile's last blocks waiting for another tile to finish)
+    A.tma_blocks = std::max(1, A.tma_blocks / share);
     const int t = nd.tile;
     const int bs = (launch_blocks(cg, true) + share - 1) / share;
     const int bv = (launch_blocks(cg, false) + share - 1) / share;
