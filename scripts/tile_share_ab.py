@@ -12,7 +12,7 @@ for nx, K in ((128, 400), (256, 60)):
     A = P.gen_stencil_matrix(nx, nx, nx, rt=rt)
     b = P.rhs_xorshift(rt, A.n, 7)
     out = []
-    for T in (2, 3, 4, 6):
+    for T in ((2, 3, 4, 6) if not os.environ.get("TILES") else tuple(int(t) for t in os.environ["TILES"].split(","))):
         for name, kw in (("streams", {}), ("chain", dict(chain=True))):
             S = P.CgSolver(rt, A, K + 5, P.CgOptions(tiles=T, iteration_marks=False, **kw), variant=1)
             best = 1e9
