@@ -249,10 +249,6 @@ int tile_share(const tw_cg* cg) {
     // with many tiles each tile's grid is already bounded by its own size
     // (and measured: sharing then costs up to 15 %, profiles/r01_sweep_summary.md)
     if (cg->T > 2 * cap) return 1;
-    // the chain runs every tile of a phase side by side (one stream, no pool
-    // streams to share): a 1/T share each (5 / 6 / 7 tiles at 128^3: 154 /
-    // 139 / 131 -> 124 / 126 / 127 us per iteration; profiles/r02_ab_chain.md)
-    if (cg->opt.dispatch == TW_DISPATCH_CHAIN) return std::max(1, cg->T);
     return std::max(1, std::min(cg->T, cap));
 }
 

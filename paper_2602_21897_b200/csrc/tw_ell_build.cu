@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "tw_device.cuh"
 #include "tw_internal.h"
@@ -85,26 +86,39 @@ stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset, int6
             sxy = sx * static_cast<int>(axis_span(y, ny));
             len = sxy * static_cast<int>(axis_span(z, nz));
         }
+        // Interior slices (every row a full 27-point row, the bulk of any
+        // large grid) take a body whose spans are compile-time constants, so
+        // the neighbour decode of each unrolled entry folds to constants.
+        const bool full = w == kMaxStencilWidth && __all_sync(0xffffffffu, len == kMaxStencilWidth);
+        auto body = [&](auto full_tag) {
+        constexpr bool F = decltype(full_tag)::value;
+        const int SX = F ? 3 : sx, SXY = F ? 9 : sxy, LEN = F ? kMaxStencilWidth : len;
         auto nb = [&](int k, int64_t& cx, int64_t& cy, int64_t& cz) {
-            const int iz = k / sxy, t = k - iz * sxy, iy = t / sx;
+            const int iz = k / SXY, t = k - iz * SXY, iy = t / SX;
             cz = zlo + iz;
             cy = ylo + iy;
             cx = xlo + (t - iy * sx);
         };
         auto val = [&](int k) {
-            if (k >= len) return 0.0;
+            if (F) return k == 13 ? 27.0 : -1.0;
+            if (k >= LEN) return 0.0;
             int64_t cx, cy, cz;
             nb(k, cx, cy, cz);
             return cx == x && cy == y && cz == z ? 27.0 : -1.0;
         };
         auto cl = [&](int k) {
-            if (k >= len) return -1;
+            if (F) // (z + dz, y + dy, x + dx) = row + dz * plane + dy * nx + dx
+                return static_cast<int32_t>(row + row_offset - col_offset + (k / 9 - 1) * plane +
+                                            ((k % 9) / 3 - 1) * nx + (k % 3 - 1));
+            if (k >= LEN) return -1;
             int64_t cx, cy, cz;
             nb(k, cx, cy, cz);
             return static_cast<int32_t>((cz * ny + cy) * nx + cx - col_offset);
         };
         auto s16 = [&](int k) {
-            if (k >= len) return uint32_t(kStagePad);
+            if (F) // run (dz + 1) * 3 + (dy + 1), offset x + dx - x0 + 2
+                return static_cast<uint32_t>((k / 3) * kStageRunLen + (k % 3) + 1 + (x - x0));
+            if (k >= LEN) return uint32_t(kStagePad);
             int64_t cx, cy, cz;
             nb(k, cx, cy, cz);
             TW_DCHECK(cx - x0 + 2 >= 0 && cx - x0 + 2 < kStageRunLen);
@@ -130,7 +144,7 @@ stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset, int6
         if (w - f4 >= 2)
             reinterpret_cast<int2*>(cb + 32 * f4)[lane] = make_int2(cl(f4), cl(f4 + 1));
         if ((w - f4) & 1) cb[32 * (w - 1) + lane] = cl(w - 1);
-        if (!c16) continue;
+        if (!c16) return;
         // staged columns: [k/8][l][8] (one uint4 per lane), then 4, 2, 1
         uint16_t* hb = c16 + off;
         const int f8 = w & ~7;
@@ -152,6 +166,11 @@ stencil_fill_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_offset, int6
             rem -= 2;
         }
         if (rem) hb[32 * base + lane] = static_cast<uint16_t>(s16(base));
+        };
+        if (full)
+            body(std::true_type{});
+        else
+            body(std::false_type{});
     }
 }
 
